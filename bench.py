@@ -1,0 +1,327 @@
+"""bench.py — Tacchi hot-path throughput on B200 (BASELINE.json metric).
+
+Workload (config 2a, BASELINE.json configs[1]): the default 20x20x4 mm gel
+(101x101x21) + the sphere indenter at the reference's finest density (1e6
+points, no subsampling) = 1,214,221 particles on the 256^3 / 33 mm grid,
+dt = 2e-6 s, press velocity (0, 0, -0.01) m/s. One bench "step" = one tactile
+frame = mpm::step(state, v, 10) + sim::capture (session.cpp:86, 42).
+
+  value  particle-substeps/s with the state resident in HBM; device time on
+         the handle's stream (CUDA events), max over ranks.
+  e2e    the same metric through the C-ABI as a caller uses it: the command
+         velocity goes in from host memory and the 640x480 depth (fp64) + RGB
+         image come back to host buffers every frame, inside the timed region.
+
+Multi-GPU (torchrun): one process per GPU, each runs its own independent
+indentation episode (lateral offset by rank); no data-path collective; the
+per-rank device times are max-reduced. `--impl reference` times the
+reference's own CPU implementation (oracle/_ref, OpenMP, all host threads) on
+the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from tests.scenes import CONFIG2A, CONFIG2A_V, SUBSTEPS_PER_FRAME  # noqa: E402
+
+METRIC = "particle-substeps/sec"
+UNIT = "particle-substeps/s"
+WORKLOAD = "config2a: default gel 101x101x21 + sphere 1e6 pts (1,214,221 particles), 256^3 grid, dt 2e-6, 10 substeps + capture per frame"
+
+
+def _dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [t.strip() for t in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _algorithmic_bytes(n_el: int, n_ind: int, window_nodes: int):
+    """per substep every particle's persistent state is read
+    and written once: gel x(3)+F(9) doubles, indenter x(3) -> 24*8 and 6*8
+    bytes. Per-kernel figures for the roofline are the bytes each kernel must
+    move at minimum (state in, state out; the grid is L2 scratch)."""
+    s = 8
+    per_substep = n_el * 24 * s + n_ind * 6 * s
+    per_kernel = {
+        "p2g_elastomer": n_el * 24 * s,         # x, v, C, F read
+        "p2g_indenter": n_ind * 6 * s,          # x, v read
+        "g2p_elastomer": n_el * (12 + 24) * s,  # x, F read; x, v, C, F written
+        "indenter_move": n_ind * 9 * s,         # x read; x, v written
+        "grid_update": window_nodes * 56,       # m+p read (32 B), v written (24 B)
+        "clear": window_nodes * 32,
+        "finalize": 0,
+    }
+    return per_substep, per_kernel
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2301_08343_b200 as tb
+
+    rank, world, local = _dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    device = local
+    torch.cuda.set_device(device)
+    # independent episode per rank: lateral offset on a 1 mm grid (harness.cpp:196-201)
+    off = ((rank % 3) - 1) * 1e-3, (((rank // 3) % 3) - 1) * 1e-3
+    s = tb.sim.build_sim(CONFIG2A, "", off[0], off[1], device=device)
+    n, n_el = s.n, s.elastomer_count
+    rp = tb.render_params(CONFIG2A, "")
+    v = np.array(CONFIG2A_V)
+    stream = torch.cuda.ExternalStream(s.stream, device=device)
+
+    def frame_device():
+        tb.mpm.step(s, v, SUBSTEPS_PER_FRAME)
+        tb.sim.capture(s, params=rp, want_depth=False, want_image=False)
+
+    for _ in range(args.warmup):
+        frame_device()
+    torch.cuda.synchronize(device)
+
+    # --- timed region 1: device-resident (value) ---
+    clocks = Clocks(device)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(device)
+    k0 = s.kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        frame_device()
+    e1.record(stream)
+    torch.cuda.synchronize(device)
+    dev_ms = e0.elapsed_time(e1)
+    launches = s.kernel_launches - k0
+
+    # --- timed region 2: end to end through the C-ABI with host buffers ---
+    depth = np.empty((rp.height, rp.width))
+    img = np.empty((rp.height, rp.width, 3), np.uint8)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(device)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e2.record(stream)
+    for _ in range(args.steps):
+        tb.mpm.step(s, v, SUBSTEPS_PER_FRAME)          # command from host memory
+        tb.sim.capture(s, params=rp, want_depth=True, want_image=True)  # D2H depth + RGB
+    e3.record(stream)
+    torch.cuda.synchronize(device)
+    e2e_ms = e2.elapsed_time(e3)
+    e2e_wall = (time.perf_counter() - t0) * 1e3
+    clk = clocks.stop()
+
+    # --- per-kernel timing for the roofline (after the timed regions) ---
+    phase_ms = s.time_phases(v, reps=20)
+    lo, hi = s.grid_window()
+    window_nodes = int(np.prod(hi - lo))
+    per_substep, per_kernel = _algorithmic_bytes(n_el, n - n_el, window_nodes)
+
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([dev_ms, e2e_ms], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, e2e_ms = t.tolist()
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    units = float(n) * SUBSTEPS_PER_FRAME * args.steps * world
+    value = units / (dev_ms * 1e-3)
+    e2e_value = units / (e2e_ms * 1e-3)
+    peak, peak_src = _peaks()
+    dom = max((k for k in phase_ms if k != "finalize"), key=lambda k: phase_ms[k])
+    dom_ms = phase_ms[dom]
+    achieved = per_kernel[dom] / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
+    substep_ms = sum(phase_ms.values())
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "particles_per_gpu": n, "elastomer": n_el,
+                   "grid": [256, 256, 256], "substeps_per_step": SUBSTEPS_PER_FRAME,
+                   "dt_s": 2e-6, "parallelism": f"episodes x{world} (one per GPU)",
+                   "l2": "working set > L2 (particles ~90 MB + active grid window ~130 MB per substep)"},
+        "frames_per_sec": args.steps * world / (dev_ms * 1e-3),
+        "e2e": {"value": e2e_value, "unit": UNIT, "frames_per_sec": args.steps * world / (e2e_ms * 1e-3),
+                "h2d_bytes_per_step": 3 * 8, "d2h_bytes_per_step": depth.nbytes + img.nbytes,
+                "wall_ms_per_step": e2e_wall / args.steps},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": per_kernel[dom],
+                     "kernel_ms": dom_ms,
+                     "substep": {"ms": substep_ms, "algorithmic_bytes": per_substep,
+                                 "achieved_gbs": per_substep / (substep_ms * 1e-3) / 1e9,
+                                 "frac": per_substep / (substep_ms * 1e-3) / 1e9 / peak},
+                     "phase_ms": phase_ms},
+    }
+    if clk:
+        line["clocks"] = clk
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(frames=args.cpu_frames)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def _ref_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(frames: int = 2):
+    """The reference's own CPU engine (oracle/_ref, unmodified sources, -O3
+    -fopenmp) on a bounded sample of the same workload: `frames` x 10
+    substeps of config 2a with every host thread."""
+    from oracle import refpy
+
+    if not refpy.available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref missing on this host"}
+    threads = _ref_threads()
+    sim = refpy.RefSim.from_config(CONFIG2A, "", threads=threads)
+    sim.step(CONFIG2A_V, 1)  # first touch of the dense 256^3 grid
+    t0 = time.perf_counter()
+    sim.step(CONFIG2A_V, SUBSTEPS_PER_FRAME * frames)
+    dt = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    sim.capture(CONFIG2A)
+    cap = time.perf_counter() - t1
+    n = sim.n
+    return {"value": n * SUBSTEPS_PER_FRAME * frames / dt, "unit": UNIT, "cores": threads,
+            "kind": "reference", "capture_ms": cap * 1e3,
+            "sample": f"{frames * SUBSTEPS_PER_FRAME} substeps of config2a ({n} particles), "
+                      f"mpm::step wall time, OMP threads={threads}"}
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    from oracle import refpy
+
+    if not refpy.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtacchi_ref.so not built"}))
+        return
+    threads = _ref_threads()
+    sim = refpy.RefSim.from_config(CONFIG2A, "", threads=threads)
+    n = sim.n
+    v = CONFIG2A_V
+    for _ in range(args.warmup):
+        sim.step(v, SUBSTEPS_PER_FRAME)
+        sim.capture(CONFIG2A)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sim.step(v, SUBSTEPS_PER_FRAME)
+        sim.capture(CONFIG2A)
+    dt = time.perf_counter() - t0
+    value = n * SUBSTEPS_PER_FRAME * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "particles_per_gpu": n, "substeps_per_step": SUBSTEPS_PER_FRAME},
+        "frames_per_sec": args.steps / dt,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} frames (10 substeps + capture) of config2a, "
+                                   f"OMP threads={threads}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

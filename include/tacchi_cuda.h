@@ -1,0 +1,221 @@
+/* tacchi_cuda.h — C-ABI of the B200-native Tacchi hot path (libtacchi_cuda.so).
+ *
+ * This is the drop-in boundary for the reference's C++ simulator API
+ * (/root/reference/proj). Each entry point names the reference interface it
+ * replaces (file:line). Plain pointers and sizes only; no C++ or torch types.
+ *
+ * Conventions
+ *   - All physical quantities are SI, fp64, exactly as the reference.
+ *   - Particle arrays use the reference's particle order: elastomer particles
+ *     [0, n_elastomer) in lattice order (i, j, k), k fastest
+ *     (particle_set.hpp:16-17, scene.cpp:54-60), then the indenter in cloud
+ *     order. Vectors are N x 3 row-major; matrices N x 9 with M(i,j) at
+ *     [9p + 3i + j].
+ *   - Every function returns TG_OK (0) or a TG_ERR_* code; the message of the
+ *     last error on the calling thread is available from tg_last_error().
+ *     The codes map 1:1 onto the reference exception taxonomy
+ *     (errors.hpp:9-39); the C++ wrapper (tacchi_b200.hpp) rethrows the
+ *     matching class.
+ *   - A handle owns all of its device memory and one CUDA stream. Calls on one
+ *     handle must be serialised by the caller (one control thread per
+ *     SimState); different handles may be driven concurrently.
+ *   - No CPU fallback: if no sm_100 device is present every constructor fails
+ *     with TG_ERR_CUDA.
+ */
+#ifndef TACCHI_CUDA_H
+#define TACCHI_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TG_OK = 0,
+  TG_ERR_GRID_TOO_SMALL = 1,    /* tacchi::GridTooSmall    errors.hpp:17 */
+  TG_ERR_EMPTY_SCENE = 2,       /* tacchi::EmptyScene      errors.hpp:18 */
+  TG_ERR_OUT_OF_GRID = 3,       /* tacchi::OutOfGrid       errors.hpp:19 */
+  TG_ERR_DEGENERATE_F = 4,      /* tacchi::DegenerateF     errors.hpp:20 */
+  TG_ERR_CONFIG = 5,            /* tacchi::ConfigError     errors.hpp:38 */
+  TG_ERR_NO_SURFACE = 6,        /* tacchi::NoSurface       errors.hpp:27 */
+  TG_ERR_CROP_OUT_OF_BOUNDS = 7,/* tacchi::CropOutOfBounds errors.hpp:28 */
+  TG_ERR_SHAPE_MISMATCH = 8,    /* tacchi::ShapeMismatch   errors.hpp:31 */
+  TG_ERR_EMPTY_CLOUD = 9,       /* tacchi::EmptyCloud      errors.hpp:24 */
+  TG_ERR_PARSE = 10,            /* tacchi::ParseError      errors.hpp:23 */
+  TG_ERR_IO = 11,               /* tacchi::IoError         errors.hpp:39 */
+  TG_ERR_CUDA = 20,             /* device / driver failure (no reference analogue) */
+  TG_ERR_INVALID_ARGUMENT = 21  /* null handle / bad sizes (no reference analogue) */
+};
+
+/* Phase ids for tg_phase, in engine.hpp order. */
+enum {
+  TG_PHASE_ZERO_GRID = 0,        /* mpm::zero_grid         engine.hpp:10  */
+  TG_PHASE_PARTICLE_TO_GRID = 1, /* mpm::particle_to_grid  engine.hpp:15  */
+  TG_PHASE_GRID_UPDATE = 2,      /* mpm::grid_update       engine.hpp:19  */
+  TG_PHASE_GRID_TO_PARTICLE = 3, /* mpm::grid_to_particle  engine.hpp:23  */
+  TG_PHASE_APPLY_BOUNDARY = 4,   /* mpm::apply_boundary    engine.hpp:27  */
+  TG_PHASE_ADVECT = 5            /* mpm::advect            engine.hpp:31  */
+};
+
+typedef struct tg_sim* tg_handle;
+
+/* mpm::SceneParams (sim_state.hpp:81-98) after Grid construction. */
+typedef struct {
+  int res[3];             /* grid nodes per axis */
+  double dx;              /* node spacing = grid_edge / res.x (scene.cpp:41-42) */
+  double origin[3];
+  double youngs_modulus;  /* MaterialParams (material.hpp:9-19) */
+  double poisson_ratio;
+  double density;
+  double dt;
+  double gravity[3];
+} tg_params;
+
+/* Particle state as init_scene builds it (scene.cpp:28-87). mass / volume0
+ * must be uniform per material (they are, by construction of init_scene). */
+typedef struct {
+  int64_t n;              /* total particles */
+  int64_t n_elastomer;    /* elastomer particles occupy [0, n_elastomer) */
+  const double* x;        /* n x 3 */
+  const double* v;        /* n x 3 */
+  const double* C;        /* n x 9, may be NULL (zeros) */
+  const double* F;        /* n x 9, may be NULL (identity) */
+  const double* mass;     /* n */
+  const double* volume0;  /* n */
+  const uint8_t* tag;     /* n: 0 elastomer, 1 elastomer bottom, 2 indenter */
+  double indenter_velocity[3]; /* SimState::indenter_velocity */
+} tg_particles;
+
+/* mpm::SurfaceLattice (sim_state.hpp:41-52). */
+typedef struct {
+  int nx, ny;
+  double x0, y0, sx, sy, z0;
+  const uint32_t* particle; /* nx*ny particle indices, x-major */
+} tg_surface;
+
+/* Per-frame capture parameters: sim::capture's inputs resolved from
+ * SceneConfig (scene_builder.cpp:80-89, scene_config.cpp:70-81). */
+typedef struct {
+  double pixel_to_meter;    /* full-surface extraction pitch r */
+  double crop_offset[2];    /* CropAlignment offset_x / offset_y (pixels) */
+  double crop_scale;        /* CropAlignment scale */
+  int width, height;        /* output image (640 x 480) */
+  double ambient_k, diffuse_k, specular_k, shininess;
+  double ambient_rgb[3];
+  double view_dir[3];
+  int n_lights;             /* <= 8 */
+  double lights[8][9];      /* direction, diffuse_rgb, specular_rgb */
+  const uint8_t* background;/* optional height x width x 3 RGB, or NULL */
+} tg_render;
+
+/* ---- scene setup ------------------------------------------------------- */
+
+/* mpm::init_scene (sim_state.hpp:102-104) from explicit arrays. */
+int tg_create(int device, const tg_params* params, const tg_particles* particles,
+              const tg_surface* surface, tg_handle* out);
+
+/* sim::build_sim(cfg, place_for_press(cfg, indenter_cloud_for(cfg, object),
+ * offset_x, offset_y)) (scene_builder.cpp:33-78): the full reference setup
+ * path from a SceneConfig JSON (partial overrides of default_config,
+ * scene_config.cpp:118-257). */
+int tg_build_sim(int device, const char* config_json, const char* object, double offset_x,
+                 double offset_y, tg_handle* out);
+
+void tg_destroy(tg_handle h);
+
+/* Host-side geometry of the setup path (no device work):
+ * geo::generate_shape_cloud (shapes.cpp:231-249), out is n x 3 metres, and
+ * indenter_cloud_for + place_for_press (scene_builder.cpp:33-61); call the
+ * latter with out == NULL to query *n. */
+int tg_generate_cloud(const char* shape, int64_t n, uint64_t seed, double* out);
+int tg_placed_indenter(const char* config_json, const char* object, double offset_x,
+                       double offset_y, double* out, int64_t* n);
+
+/* ---- stepping (engine.hpp) --------------------------------------------- */
+
+/* mpm::step(state, indenter_velocity, n_substeps) (engine.cpp:288-297).
+ * Asynchronous on the handle's stream except for one completion/error check
+ * at the end; errors raised on device are latched and reported with the
+ * reference's semantics (state left as at the failing phase). */
+int tg_step(tg_handle h, const double indenter_velocity[3], int n_substeps);
+
+/* The six phases individually (engine.cpp:53-286), for unit parity. */
+int tg_phase(tg_handle h, int phase, const double indenter_velocity[3]);
+
+/* ---- state transfer --------------------------------------------------- */
+
+int64_t tg_num_particles(tg_handle h);
+int64_t tg_num_elastomer(tg_handle h);
+/* Any output pointer may be NULL. Reference particle order. */
+int tg_download(tg_handle h, double* x, double* v, double* C, double* F);
+int tg_upload(tg_handle h, const double* x, const double* v, const double* C, const double* F);
+/* StepDiagnostics + step_count + indenter_velocity (sim_state.hpp:54-73). */
+int tg_diag(tg_handle h, double* min_det_f, double* max_speed, int64_t* step_count,
+            double indenter_velocity[3]);
+/* Grid::active_lo / active_hi (grid.hpp:25-26). */
+int tg_grid_window(tg_handle h, int lo[3], int hi[3]);
+/* Node box [lo, hi) (k fastest) of Grid::mass / momentum / velocity; any
+ * output may be NULL. Momentum is available after particle_to_grid and before
+ * grid_update; velocity after grid_update. */
+int tg_download_grid(tg_handle h, const int lo[3], const int hi[3], double* mass, double* momentum,
+                     double* velocity);
+
+/* ---- capture (render) -------------------------------------------------- */
+
+/* Resolves sim::capture's render inputs from a SceneConfig JSON + object name
+ * (lights, render params, alignment_for(object)). */
+int tg_render_from_config(const char* config_json, const char* object, tg_render* out);
+
+/* sim::capture (scene_builder.cpp:80-89): extract_surface_depth (full
+ * surface at pixel_to_meter) -> crop_align -> phong_render, fused on device.
+ * depth_out: height x width fp64 (DepthMap::values, row-major); rgb_out:
+ * height x width x 3 (Image8::data). Either may be NULL (device-only). */
+int tg_capture(tg_handle h, const tg_render* r, double* depth_out, uint8_t* rgb_out);
+
+/* render::extract_surface_depth(state, w, h, r) (depth_extract.cpp:10-49);
+ * w <= 0 or h <= 0 selects the full-surface overload (:51-57) and returns
+ * its size in *out_w / *out_h (call with out == NULL to query). */
+int tg_extract_depth(tg_handle h, int w, int hgt, double r, double* out, int* out_w, int* out_h);
+
+/* render::crop_align (depth_map.cpp:62-101) on a host depth map. */
+int tg_crop_align(int device, const double* src, int sw, int sh, double off_x, double off_y,
+                  double scale, int ow, int oh, double* out);
+/* render::surface_normals (phong.cpp:10-41): out is h x w x 3. */
+int tg_surface_normals(int device, const double* depth, int w, int hgt, double r, double* out);
+/* render::phong_render (phong.cpp:43-84) on a host depth map; r is
+ * DepthMap::pixel_to_meter, render->lights / params as above. */
+int tg_phong_render(int device, const double* depth, int w, int hgt, double r,
+                    const tg_render* render, uint8_t* out);
+
+/* ---- batched episodes (config 4) --------------------------------------- */
+
+/* Steps several handles that live on the same device in one pass of
+ * launches (one stream each, submitted back to back). */
+int tg_step_many(tg_handle* hs, int n_handles, const double* velocities /* n x 3 */,
+                 int n_substeps);
+
+/* ---- runtime ------------------------------------------------------------ */
+
+/* Blocks until the handle's stream is idle; reports any latched error. */
+int tg_sync(tg_handle h);
+/* Runs `reps` substeps of mpm::step with CUDA events between the kernels
+ * of the launch plan and writes the average device time (ms) of each:
+ * [clear, p2g_elastomer, p2g_indenter, grid_update, g2p_elastomer(+boundary
+ * +advect), indenter_move, finalize]. The state advances by `reps` substeps
+ * exactly as tg_step would. Instrumentation for the roofline in bench.py. */
+int tg_time_phases(tg_handle h, const double indenter_velocity[3], int reps, double* out_ms);
+/* cudaStream_t of the handle (for event timing by the caller). */
+void* tg_stream(tg_handle h);
+/* Number of kernels this handle has launched so far (graph nodes count). */
+int64_t tg_kernel_launches(tg_handle h);
+/* Enables / disables CUDA-graph replay of the substep loop (default on). */
+int tg_set_graphs(tg_handle h, int enabled);
+const char* tg_last_error(void);
+const char* tg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TACCHI_CUDA_H */

@@ -1,0 +1,705 @@
+// DeviceSim lifecycle, the substep launch plan (with CUDA-graph replay), state
+// transfer, and the C-ABI entry points of include/tacchi_cuda.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+#include "tacchi_cuda.h"
+
+namespace tacchi_b200 {
+
+// mpm_kernels.cu
+int launch_window(DeviceSim& s);
+int launch_clear(DeviceSim& s, int sms);
+int launch_p2g(DeviceSim& s, bool publish_diag);
+int launch_grid_update(DeviceSim& s, int sms);
+int launch_g2p_move(DeviceSim& s);
+int launch_phase_g2p(DeviceSim& s);
+int launch_phase_boundary(DeviceSim& s);
+int launch_phase_advect(DeviceSim& s);
+int launch_reset(DeviceSim& s);
+int launch_gather_box(DeviceSim& s, const int lo[3], const int hi[3], double* mass, double* mom,
+                      double* vel);
+int launch_p2g_gel(DeviceSim& s);
+int launch_p2g_ind(DeviceSim& s);
+int launch_g2p_gel_move(DeviceSim& s);
+int launch_ind_move(DeviceSim& s);
+int launch_finalize_step(DeviceSim& s);
+// capture_kernels.cu
+int capture(DeviceSim& s, const tg_render& r, double* depth_host, uint8_t* rgb_host,
+            std::string& msg);
+int extract_depth(DeviceSim& s, int w, int h, double r, double* out, std::string& msg);
+void full_surface_size(const DeviceSim& s, double r, int* w, int* h);
+int render_standalone(int mode, const double* src, int sw, int sh, double r, double off_x,
+                      double off_y, double scale, int ow, int oh, const tg_render* rp,
+                      double* out_d, uint8_t* out_u8, std::string& msg);
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+static const char* error_name(int code) {
+  switch (code) {
+    case kErrGridTooSmall: return "GridTooSmall";
+    case kErrEmptyScene: return "EmptyScene";
+    case kErrOutOfGrid: return "OutOfGrid";
+    case kErrDegenerateF: return "DegenerateF";
+    case kErrConfig: return "ConfigError";
+    default: return "Error";
+  }
+}
+
+#define CUDA_TRY(expr)                                                             \
+  do {                                                                             \
+    const cudaError_t _e = (expr);                                                 \
+    if (_e != cudaSuccess)                                                         \
+      return fail(TG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+DeviceSim::~DeviceSim() {
+  if (device >= 0) cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+  cudaFree(x);
+  cudaFree(v);
+  cudaFree(C);
+  cudaFree(F);
+  cudaFree(tag);
+  cudaFree(grid_mp);
+  cudaFree(grid_v);
+  cudaFree(surf_idx);
+  cudaFree(surf_depth);
+  cudaFree(cap_depth);
+  cudaFree(cap_rgb);
+  cudaFree(cap_bg);
+  cudaFree(ctl);
+  cudaFreeHost(h_ctl);
+  cudaFreeHost(h_vind);
+  cudaFreeHost(h_depth_pinned);
+  cudaFreeHost(h_rgb_pinned);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+static int sm_count(int device) {
+  static int cached[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cached[device]) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    cached[device] = v;
+  }
+  return cached[device];
+}
+
+static int check_device(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return fail(TG_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  if (device < 0 || device >= count)
+    return fail(TG_ERR_INVALID_ARGUMENT, "device index out of range");
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(TG_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100-class");
+  CUDA_TRY(cudaSetDevice(device));
+  return TG_OK;
+}
+
+// Host copy of zero_grid's base_index (engine.cpp:47-49).
+static int host_base(double x, double origin, double inv_dx) {
+  return static_cast<int>(std::floor((x - origin) * inv_dx - 0.5));
+}
+
+int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, const double* Fm,
+           bool init);
+
+int create(int device, const tg_params* P, const tg_particles* in, const tg_surface* surf,
+           DeviceSim** out) {
+  if (!P || !in || !out) return fail(TG_ERR_INVALID_ARGUMENT, "tg_create: null argument");
+  if (in->n <= 0 || in->n_elastomer < 0 || in->n_elastomer > in->n)
+    return fail(TG_ERR_EMPTY_SCENE, "init_scene: both elastomer and indenter particle sets must be non-empty");
+  if (!in->x || !in->v || !in->mass || !in->volume0 || !in->tag)
+    return fail(TG_ERR_INVALID_ARGUMENT, "tg_create: x, v, mass, volume0 and tag are required");
+  if (!(P->dt > 0.0)) return fail(TG_ERR_CONFIG, "dt must be > 0");
+  if (P->res[0] < 4 || P->res[1] < 4 || P->res[2] < 4)
+    return fail(TG_ERR_CONFIG, "grid resolution must be >= 4 per axis");
+  if (!(P->dx > 0.0)) return fail(TG_ERR_CONFIG, "grid spacing must be > 0");
+  if (!(P->youngs_modulus > 0.0)) return fail(TG_ERR_CONFIG, "youngs_modulus must be > 0");
+  if (!(P->poisson_ratio >= 0.0 && P->poisson_ratio < 0.5))
+    return fail(TG_ERR_CONFIG, "poisson_ratio must be in [0, 0.5)");
+  if (!(P->density > 0.0)) return fail(TG_ERR_CONFIG, "density must be > 0");
+  const int64_t n = in->n, n_el = in->n_elastomer, n_ind = n - n_el;
+  for (int64_t p = 0; p < n; ++p) {
+    const bool is_ind = in->tag[p] == kIndenter;
+    if (is_ind != (p >= n_el))
+      return fail(TG_ERR_CONFIG, "tg_create: elastomer particles must precede the indenter");
+  }
+  // init_scene assigns one mass / rest volume per material (scene.cpp:48-66).
+  for (int64_t p = 0; p < n; ++p) {
+    const int64_t ref = p < n_el ? 0 : n_el;
+    if (in->mass[p] != in->mass[ref] || in->volume0[p] != in->volume0[ref])
+      return fail(TG_ERR_CONFIG, "tg_create: mass / volume0 must be uniform per material");
+  }
+  int rc = check_device(device);
+  if (rc) return rc;
+
+  auto* s = new DeviceSim();
+  s->device = device;
+  s->n = n;
+  s->n_el = n_el;
+  s->n_ind = n_ind;
+  if (n_el > 0) { s->m_el = in->mass[0]; s->vol_el = in->volume0[0]; }
+  if (n_ind > 0) { s->m_ind = in->mass[n_el]; s->vol_ind = in->volume0[n_el]; }
+  Geometry& g = s->geo;
+  for (int a = 0; a < 3; ++a) {
+    g.res[a] = P->res[a];
+    g.origin[a] = P->origin[a];
+    g.gravity[a] = P->gravity[a];
+    g.gdt[a] = P->gravity[a] * P->dt;  // engine.cpp:183
+  }
+  g.dx = P->dx;
+  g.inv_dx = 1.0 / P->dx;
+  g.dt = P->dt;
+  // MaterialParams::mu / lambda (material.hpp:14-18)
+  g.mu = P->youngs_modulus / (2.0 * (1.0 + P->poisson_ratio));
+  g.lambda = P->youngs_modulus * P->poisson_ratio /
+             ((1.0 + P->poisson_ratio) * (1.0 - 2.0 * P->poisson_ratio));
+  g.with_gravity = (P->gravity[0] * P->gravity[0] + P->gravity[1] * P->gravity[1] +
+                    P->gravity[2] * P->gravity[2]) > 0.0;
+  g.stress_scale = -P->dt * 4.0 * g.inv_dx * g.inv_dx;
+
+  // Indenter particles are re-ordered by base cell so that P2G scatters from
+  // neighbouring lanes hit neighbouring nodes; perm maps back.
+  s->perm.resize(n);
+  std::iota(s->perm.begin(), s->perm.end(), 0);
+  if (n_ind > 1) {
+    std::vector<long long> key(n_ind);
+    for (int64_t q = 0; q < n_ind; ++q) {
+      const double* xp = in->x + 3 * (n_el + q);
+      long long k = 0;
+      for (int a = 0; a < 3; ++a) {
+        const int b = std::min(std::max(host_base(xp[a], g.origin[a], g.inv_dx), -1), g.res[a]);
+        k = k * (g.res[a] + 2) + (b + 1);
+      }
+      key[q] = k;
+    }
+    std::stable_sort(s->perm.begin() + n_el, s->perm.end(),
+                     [&](int64_t a, int64_t b) { return key[a - n_el] < key[b - n_el]; });
+  }
+
+  cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  s->n_nodes = static_cast<size_t>(g.res[0]) * g.res[1] * g.res[2];
+  bool ok = cudaMalloc(&s->x, 3 * n * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&s->v, 3 * n * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&s->C, std::max<int64_t>(9 * n_el, 1) * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&s->F, std::max<int64_t>(9 * n_el, 1) * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&s->tag, std::max<int64_t>(n_el, 1)) == cudaSuccess &&
+            cudaMalloc(&s->grid_mp, s->n_nodes * sizeof(double4)) == cudaSuccess &&
+            cudaMalloc(&s->grid_v, s->n_nodes * sizeof(double4)) == cudaSuccess &&
+            cudaMalloc(&s->ctl, sizeof(Ctl)) == cudaSuccess &&
+            cudaMallocHost(&s->h_ctl, sizeof(Ctl)) == cudaSuccess &&
+            cudaMallocHost(&s->h_vind, 3 * sizeof(double)) == cudaSuccess;
+  if (!ok) {
+    delete s;
+    return fail(TG_ERR_CUDA, "tg_create: device allocation failed");
+  }
+  cudaMemsetAsync(s->grid_mp, 0, s->n_nodes * sizeof(double4), s->stream);
+  cudaMemsetAsync(s->grid_v, 0, s->n_nodes * sizeof(double4), s->stream);
+  std::memset(s->h_ctl, 0, sizeof(Ctl));
+  for (int a = 0; a < 3; ++a) s->h_ctl->vind[a] = in->indenter_velocity[a];
+  s->h_ctl->diag_min_det_f = 1.0;
+  cudaMemcpyAsync(s->ctl, s->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s->stream);
+  launch_reset(*s);
+
+  // Tags of the elastomer (Elastomer / ElastomerBottom).
+  std::vector<uint8_t> tags(std::max<int64_t>(n_el, 1));
+  for (int64_t p = 0; p < n_el; ++p) tags[p] = in->tag[p];
+  cudaMemcpy(s->tag, tags.data(), n_el, cudaMemcpyHostToDevice);
+
+  rc = upload(*s, in->x, in->v, in->C, in->F, true);
+  if (rc) {
+    delete s;
+    return rc;
+  }
+  if (surf && surf->particle && surf->nx >= 2 && surf->ny >= 2) {
+    s->surf_nx = surf->nx;
+    s->surf_ny = surf->ny;
+    s->surf_geom[0] = surf->x0;
+    s->surf_geom[1] = surf->y0;
+    s->surf_geom[2] = surf->sx;
+    s->surf_geom[3] = surf->sy;
+    s->surf_geom[4] = surf->z0;
+    const size_t cnt = static_cast<size_t>(surf->nx) * surf->ny;
+    std::vector<int64_t> inv(n);
+    for (int64_t q = 0; q < n; ++q) inv[s->perm[q]] = q;
+    std::vector<uint32_t> idx(cnt);
+    for (size_t k = 0; k < cnt; ++k) {
+      if (surf->particle[k] >= static_cast<uint64_t>(n)) {
+        delete s;
+        return fail(TG_ERR_NO_SURFACE, "surface lattice index out of range");
+      }
+      idx[k] = static_cast<uint32_t>(inv[surf->particle[k]]);
+    }
+    ok = cudaMalloc(&s->surf_idx, cnt * sizeof(uint32_t)) == cudaSuccess &&
+         cudaMalloc(&s->surf_depth, cnt * sizeof(double)) == cudaSuccess;
+    if (!ok) {
+      delete s;
+      return fail(TG_ERR_CUDA, "tg_create: device allocation failed");
+    }
+    cudaMemcpy(s->surf_idx, idx.data(), cnt * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  }
+  const cudaError_t e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) {
+    delete s;
+    return fail(TG_ERR_CUDA, std::string("tg_create: ") + cudaGetErrorString(e));
+  }
+  *out = s;
+  return TG_OK;
+}
+
+// Reads back the control block and converts a latched device error into the
+// reference's exception semantics. `end_substep` is the absolute substep index
+// one past the last substep this call asked for: an error raised for a later
+// substep (the next zero_grid's window check) is not this call's error; the
+// window is just recomputed on the next call, which then raises it itself.
+static int sync_and_check(DeviceSim& s, int end_substep) {
+  CUDA_TRY(cudaMemcpyAsync(s.h_ctl, s.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s.stream));
+  CUDA_TRY(cudaStreamSynchronize(s.stream));
+  CUDA_TRY(cudaGetLastError());
+  const Ctl& c = *s.h_ctl;
+  s.host_substep = c.substep;
+  if (c.err_code == 0) return TG_OK;
+  const int code = c.err_code;
+  const int at = c.err_substep;
+  // Clear the latch; the next call re-derives the window from the state.
+  CUDA_TRY(cudaMemsetAsync(&s.ctl->err_code, 0, sizeof(int), s.stream));
+  launch_reset(s);
+  s.window_valid = false;
+  CUDA_TRY(cudaStreamSynchronize(s.stream));
+  if (at >= end_substep) return TG_OK;
+  const char* what = code == kErrOutOfGrid
+                         ? "particles left the stencil-safe margin (check dt and scene size)"
+                         : code == kErrDegenerateF ? "particle_to_grid: det(F) <= 0" : "device error";
+  return fail(code, std::string(error_name(code)) + ": " + what);
+}
+
+static int record_substeps(DeviceSim& s, int n_substeps) {
+  int k = 0;
+  const int sms = sm_count(s.device);
+  for (int i = 0; i < n_substeps; ++i) {
+    k += launch_clear(s, sms);
+    k += launch_p2g(s, false);
+    k += launch_grid_update(s, sms);
+    k += launch_g2p_move(s);
+  }
+  return k;
+}
+
+// Enqueues mpm::step's n_substeps (engine.cpp:288-297) on the handle's stream.
+int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
+  CUDA_TRY(cudaSetDevice(s.device));
+  s.pending_start = s.host_substep;
+  if (n_substeps <= 0) return TG_OK;
+  for (int a = 0; a < 3; ++a) s.h_vind[a] = vind[a];
+  // zero_grid of the first substep (a failing window latches OutOfGrid for
+  // this substep and every later kernel exits early).
+  if (!s.window_valid) launch_window(s);
+  s.window_valid = true;
+  if (s.use_graphs) {
+    auto it = s.graphs.find(n_substeps);
+    if (it == s.graphs.end()) {
+      cudaGraph_t graph;
+      const int64_t before = s.kernel_launches;
+      CUDA_TRY(cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal));
+      cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double), cudaMemcpyHostToDevice,
+                      s.stream);
+      const int k = record_substeps(s, n_substeps);
+      CUDA_TRY(cudaStreamEndCapture(s.stream, &graph));
+      cudaGraphExec_t exec;
+      CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+      s.kernel_launches = before;  // counted per replay below
+      it = s.graphs.emplace(n_substeps, exec).first;
+      s.graph_kernels[n_substeps] = k;
+    }
+    CUDA_TRY(cudaGraphLaunch(it->second, s.stream));
+    s.kernel_launches += s.graph_kernels[n_substeps];
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double),
+                             cudaMemcpyHostToDevice, s.stream));
+    record_substeps(s, n_substeps);
+  }
+  return TG_OK;
+}
+
+int step_finish(DeviceSim& s, int n_substeps) {
+  CUDA_TRY(cudaSetDevice(s.device));
+  return sync_and_check(s, s.pending_start + std::max(n_substeps, 0));
+}
+
+int step(DeviceSim& s, const double vind[3], int n_substeps) {
+  const int rc = step_submit(s, vind, n_substeps);
+  if (rc) return rc;
+  return step_finish(s, n_substeps);
+}
+
+int check_device_public(int device) { return check_device(device); }
+
+// Per-kernel device times of the substep plan (CUDA events between the
+// launches, no graph), averaged over `reps` substeps. Order:
+// clear, p2g_gel, p2g_ind, grid_update, g2p_gel(+boundary+advect),
+// ind_move, finalize. Used by bench.py for the roofline.
+int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
+  CUDA_TRY(cudaSetDevice(s.device));
+  const int sms = sm_count(s.device);
+  constexpr int kGroups = 7;
+  cudaEvent_t ev[kGroups + 1];
+  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+  for (int g = 0; g < kGroups; ++g) out_ms[g] = 0.0;
+  for (int a = 0; a < 3; ++a) s.h_vind[a] = vind[a];
+  const int start = s.host_substep;
+  if (!s.window_valid) launch_window(s);
+  s.window_valid = true;
+  CUDA_TRY(cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double), cudaMemcpyHostToDevice,
+                           s.stream));
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(ev[0], s.stream);
+    launch_clear(s, sms);
+    cudaEventRecord(ev[1], s.stream);
+    launch_p2g_gel(s);
+    cudaEventRecord(ev[2], s.stream);
+    launch_p2g_ind(s);
+    cudaEventRecord(ev[3], s.stream);
+    launch_grid_update(s, sms);
+    cudaEventRecord(ev[4], s.stream);
+    launch_g2p_gel_move(s);
+    cudaEventRecord(ev[5], s.stream);
+    launch_ind_move(s);
+    cudaEventRecord(ev[6], s.stream);
+    launch_finalize_step(s);
+    cudaEventRecord(ev[7], s.stream);
+    CUDA_TRY(cudaEventSynchronize(ev[7]));
+    for (int g = 0; g < kGroups; ++g) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[g], ev[g + 1]);
+      out_ms[g] += ms / reps;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return sync_and_check(s, start + reps);
+}
+
+int phase(DeviceSim& s, int ph, const double vind[3]) {
+  CUDA_TRY(cudaSetDevice(s.device));
+  const int start = s.host_substep;
+  const int sms = sm_count(s.device);
+  switch (ph) {
+    case TG_PHASE_ZERO_GRID:
+      launch_window(s);
+      launch_clear(s, sms);
+      break;
+    case TG_PHASE_PARTICLE_TO_GRID: launch_p2g(s, true); break;
+    case TG_PHASE_GRID_UPDATE: launch_grid_update(s, sms); break;
+    case TG_PHASE_GRID_TO_PARTICLE: launch_phase_g2p(s); break;
+    case TG_PHASE_APPLY_BOUNDARY:
+      for (int a = 0; a < 3; ++a) s.h_vind[a] = vind[a];
+      CUDA_TRY(cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double),
+                               cudaMemcpyHostToDevice, s.stream));
+      launch_phase_boundary(s);
+      break;
+    case TG_PHASE_ADVECT: launch_phase_advect(s); break;
+    default: return fail(TG_ERR_INVALID_ARGUMENT, "tg_phase: bad phase id");
+  }
+  s.window_valid = false;  // phases drive zero_grid explicitly
+  return sync_and_check(s, start + 1);
+}
+
+static void to_component_major(const double* src, int64_t n, int ncomp, const std::vector<int64_t>& perm,
+                               int64_t begin, int64_t end, std::vector<double>& dst) {
+  const int64_t cnt = end - begin;
+  dst.resize(static_cast<size_t>(ncomp) * cnt);
+  for (int64_t q = begin; q < end; ++q) {
+    const int64_t r = perm[q];
+    for (int c = 0; c < ncomp; ++c) dst[static_cast<size_t>(c) * cnt + (q - begin)] = src[ncomp * r + c];
+  }
+  (void)n;
+}
+
+int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, const double* Fm,
+           bool init) {
+  CUDA_TRY(cudaSetDevice(s.device));
+  CUDA_TRY(cudaStreamSynchronize(s.stream));
+  std::vector<double> buf;
+  auto put3 = [&](const double* src, double* dst) -> int {
+    to_component_major(src, s.n, 3, s.perm, 0, s.n, buf);
+    const cudaError_t e = cudaMemcpy(dst, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? 0 : fail(TG_ERR_CUDA, cudaGetErrorString(e));
+  };
+  auto put9 = [&](const double* src, double* dst, bool identity) -> int {
+    if (s.n_el == 0) return 0;
+    if (src) {
+      to_component_major(src, s.n, 9, s.perm, 0, s.n_el, buf);
+    } else {
+      buf.assign(static_cast<size_t>(9) * s.n_el, 0.0);
+      if (identity)
+        for (int d = 0; d < 3; ++d)
+          std::fill(buf.begin() + static_cast<size_t>(4 * d) * s.n_el,
+                    buf.begin() + static_cast<size_t>(4 * d + 1) * s.n_el, 1.0);
+    }
+    const cudaError_t e = cudaMemcpy(dst, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? 0 : fail(TG_ERR_CUDA, cudaGetErrorString(e));
+  };
+  int rc = 0;
+  if (x && (rc = put3(x, s.x))) return rc;
+  if (v && (rc = put3(v, s.v))) return rc;
+  if ((Cm || init) && (rc = put9(Cm, s.C, false))) return rc;
+  if ((Fm || init) && (rc = put9(Fm, s.F, true))) return rc;
+  s.window_valid = false;
+  return TG_OK;
+}
+
+int download(DeviceSim& s, double* x, double* v, double* Cm, double* Fm) {
+  CUDA_TRY(cudaSetDevice(s.device));
+  CUDA_TRY(cudaStreamSynchronize(s.stream));
+  std::vector<double> buf;
+  auto get3 = [&](const double* src, double* dst) -> int {
+    buf.resize(3 * s.n);
+    const cudaError_t e = cudaMemcpy(buf.data(), src, buf.size() * sizeof(double), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(TG_ERR_CUDA, cudaGetErrorString(e));
+    for (int64_t q = 0; q < s.n; ++q)
+      for (int c = 0; c < 3; ++c) dst[3 * s.perm[q] + c] = buf[static_cast<size_t>(c) * s.n + q];
+    return 0;
+  };
+  auto get9 = [&](const double* src, double* dst, bool identity) -> int {
+    if (s.n_el > 0) {
+      buf.resize(9 * s.n_el);
+      const cudaError_t e = cudaMemcpy(buf.data(), src, buf.size() * sizeof(double), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return fail(TG_ERR_CUDA, cudaGetErrorString(e));
+      for (int64_t q = 0; q < s.n_el; ++q)
+        for (int c = 0; c < 9; ++c) dst[9 * q + c] = buf[static_cast<size_t>(c) * s.n_el + q];
+    }
+    // Indenter particles keep C = 0 and F = I (engine.cpp:218; scene.cpp:67-68).
+    for (int64_t q = s.n_el; q < s.n; ++q)
+      for (int c = 0; c < 9; ++c) dst[9 * q + c] = (identity && (c % 4 == 0)) ? 1.0 : 0.0;
+    return 0;
+  };
+  int rc = 0;
+  if (x && (rc = get3(s.x, x))) return rc;
+  if (v && (rc = get3(s.v, v))) return rc;
+  if (Cm && (rc = get9(s.C, Cm, false))) return rc;
+  if (Fm && (rc = get9(s.F, Fm, true))) return rc;
+  return TG_OK;
+}
+
+}  // namespace tacchi_b200
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+
+using tacchi_b200::DeviceSim;
+using tacchi_b200::fail;
+using tacchi_b200::g_last_error;
+
+struct tg_sim : DeviceSim {};
+
+static DeviceSim* H(tg_handle h) { return static_cast<DeviceSim*>(reinterpret_cast<void*>(h)); }
+
+extern "C" {
+
+const char* tg_last_error(void) { return g_last_error.c_str(); }
+const char* tg_version(void) { return "tacchi_b200 0.1 (sm_100a)"; }
+
+int tg_create(int device, const tg_params* params, const tg_particles* particles,
+              const tg_surface* surface, tg_handle* out) {
+  DeviceSim* s = nullptr;
+  const int rc = tacchi_b200::create(device, params, particles, surface, &s);
+  if (rc) return rc;
+  *out = reinterpret_cast<tg_handle>(s);
+  return TG_OK;
+}
+
+void tg_destroy(tg_handle h) { delete H(h); }
+
+int tg_step(tg_handle h, const double v[3], int n) {
+  if (!h || !v) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step: null argument");
+  return tacchi_b200::step(*H(h), v, n);
+}
+
+int tg_phase(tg_handle h, int phase, const double v[3]) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_phase: null handle");
+  const double zero[3] = {0, 0, 0};
+  return tacchi_b200::phase(*H(h), phase, v ? v : zero);
+}
+
+int64_t tg_num_particles(tg_handle h) { return h ? H(h)->n : 0; }
+int64_t tg_num_elastomer(tg_handle h) { return h ? H(h)->n_el : 0; }
+
+int tg_download(tg_handle h, double* x, double* v, double* C, double* F) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_download: null handle");
+  return tacchi_b200::download(*H(h), x, v, C, F);
+}
+
+int tg_upload(tg_handle h, const double* x, const double* v, const double* C, const double* F) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_upload: null handle");
+  return tacchi_b200::upload(*H(h), x, v, C, F, false);
+}
+
+int tg_diag(tg_handle h, double* min_det_f, double* max_speed, int64_t* step_count,
+            double indenter_velocity[3]) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_diag: null handle");
+  DeviceSim& s = *H(h);
+  cudaSetDevice(s.device);
+  if (cudaMemcpyAsync(s.h_ctl, s.ctl, sizeof(tacchi_b200::Ctl), cudaMemcpyDeviceToHost, s.stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(s.stream) != cudaSuccess)
+    return fail(TG_ERR_CUDA, "tg_diag: readback failed");
+  if (min_det_f) *min_det_f = s.h_ctl->diag_min_det_f;
+  if (max_speed) *max_speed = s.h_ctl->diag_max_speed;
+  if (step_count) *step_count = s.h_ctl->step_count;
+  if (indenter_velocity)
+    for (int a = 0; a < 3; ++a) indenter_velocity[a] = s.h_ctl->vind[a];
+  return TG_OK;
+}
+
+int tg_grid_window(tg_handle h, int lo[3], int hi[3]) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_grid_window: null handle");
+  DeviceSim& s = *H(h);
+  cudaSetDevice(s.device);
+  cudaMemcpyAsync(s.h_ctl, s.ctl, sizeof(tacchi_b200::Ctl), cudaMemcpyDeviceToHost, s.stream);
+  if (cudaStreamSynchronize(s.stream) != cudaSuccess) return fail(TG_ERR_CUDA, "readback failed");
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = s.h_ctl->win_lo[a];
+    hi[a] = s.h_ctl->win_hi[a];
+  }
+  return TG_OK;
+}
+
+int tg_download_grid(tg_handle h, const int lo[3], const int hi[3], double* mass, double* mom,
+                     double* vel) {
+  if (!h || !lo || !hi) return fail(TG_ERR_INVALID_ARGUMENT, "tg_download_grid: null argument");
+  DeviceSim& s = *H(h);
+  for (int a = 0; a < 3; ++a)
+    if (lo[a] < 0 || hi[a] > s.geo.res[a] || hi[a] <= lo[a])
+      return fail(TG_ERR_INVALID_ARGUMENT, "tg_download_grid: box outside the grid");
+  cudaSetDevice(s.device);
+  const size_t cnt = static_cast<size_t>(hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]);
+  double* d = nullptr;
+  if (cudaMalloc(&d, cnt * 7 * sizeof(double)) != cudaSuccess)
+    return fail(TG_ERR_CUDA, "tg_download_grid: allocation failed");
+  tacchi_b200::launch_gather_box(s, lo, hi, d, d + cnt, d + 4 * cnt);
+  std::vector<double> buf(cnt * 7);
+  cudaMemcpyAsync(buf.data(), d, cnt * 7 * sizeof(double), cudaMemcpyDeviceToHost, s.stream);
+  const cudaError_t e = cudaStreamSynchronize(s.stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(TG_ERR_CUDA, cudaGetErrorString(e));
+  if (mass) std::memcpy(mass, buf.data(), cnt * sizeof(double));
+  if (mom) std::memcpy(mom, buf.data() + cnt, 3 * cnt * sizeof(double));
+  if (vel) std::memcpy(vel, buf.data() + 4 * cnt, 3 * cnt * sizeof(double));
+  return TG_OK;
+}
+
+int tg_capture(tg_handle h, const tg_render* r, double* depth_out, uint8_t* rgb_out) {
+  if (!h || !r) return fail(TG_ERR_INVALID_ARGUMENT, "tg_capture: null argument");
+  DeviceSim& s = *H(h);
+  cudaSetDevice(s.device);
+  std::string msg;
+  const int rc = tacchi_b200::capture(s, *r, depth_out, rgb_out, msg);
+  return rc ? fail(rc, msg) : TG_OK;
+}
+
+int tg_extract_depth(tg_handle h, int w, int hgt, double r, double* out, int* out_w, int* out_h) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_extract_depth: null handle");
+  DeviceSim& s = *H(h);
+  cudaSetDevice(s.device);
+  if (w <= 0 || hgt <= 0) {
+    if (s.surf_nx < 2 || s.surf_ny < 2)
+      return fail(TG_ERR_NO_SURFACE, "extract_surface_depth: state has no surface lattice");
+    tacchi_b200::full_surface_size(s, r, &w, &hgt);
+  }
+  if (out_w) *out_w = w;
+  if (out_h) *out_h = hgt;
+  if (!out) return TG_OK;
+  std::string msg;
+  const int rc = tacchi_b200::extract_depth(s, w, hgt, r, out, msg);
+  return rc ? fail(rc, msg) : TG_OK;
+}
+
+int tg_crop_align(int device, const double* src, int sw, int sh, double off_x, double off_y,
+                  double scale, int ow, int oh, double* out) {
+  int rc = tacchi_b200::check_device_public(device);
+  if (rc) return rc;
+  std::string msg;
+  rc = tacchi_b200::render_standalone(0, src, sw, sh, 0.0, off_x, off_y, scale, ow, oh, nullptr,
+                                      out, nullptr, msg);
+  return rc ? fail(rc, msg) : TG_OK;
+}
+
+int tg_surface_normals(int device, const double* depth, int w, int hgt, double r, double* out) {
+  int rc = tacchi_b200::check_device_public(device);
+  if (rc) return rc;
+  std::string msg;
+  rc = tacchi_b200::render_standalone(1, depth, w, hgt, r, 0, 0, 1, w, hgt, nullptr, out, nullptr,
+                                      msg);
+  return rc ? fail(rc, msg) : TG_OK;
+}
+
+int tg_phong_render(int device, const double* depth, int w, int hgt, double r,
+                    const tg_render* render, uint8_t* out) {
+  if (!render) return fail(TG_ERR_INVALID_ARGUMENT, "tg_phong_render: null render params");
+  int rc = tacchi_b200::check_device_public(device);
+  if (rc) return rc;
+  std::string msg;
+  rc = tacchi_b200::render_standalone(2, depth, w, hgt, r, 0, 0, 1, w, hgt, render, nullptr, out,
+                                      msg);
+  return rc ? fail(rc, msg) : TG_OK;
+}
+
+int tg_step_many(tg_handle* hs, int n_handles, const double* velocities, int n_substeps) {
+  if (!hs || !velocities) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_many: null argument");
+  // Submit every handle's graph before waiting on any of them.
+  for (int i = 0; i < n_handles; ++i) {
+    const int rc = tacchi_b200::step_submit(*H(hs[i]), velocities + 3 * i, n_substeps);
+    if (rc) return rc;
+  }
+  int first = TG_OK;
+  for (int i = 0; i < n_handles; ++i) {
+    const int rc = tacchi_b200::step_finish(*H(hs[i]), n_substeps);
+    if (rc && !first) first = rc;
+  }
+  return first;
+}
+
+int tg_sync(tg_handle h) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_sync: null handle");
+  DeviceSim& s = *H(h);
+  cudaSetDevice(s.device);
+  const cudaError_t e = cudaStreamSynchronize(s.stream);
+  return e == cudaSuccess ? TG_OK : fail(TG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+int tg_time_phases(tg_handle h, const double v[3], int reps, double* out_ms) {
+  if (!h || !v || !out_ms || reps <= 0)
+    return fail(TG_ERR_INVALID_ARGUMENT, "tg_time_phases: bad argument");
+  return tacchi_b200::time_phases(*H(h), v, reps, out_ms);
+}
+
+void* tg_stream(tg_handle h) { return h ? static_cast<void*>(H(h)->stream) : nullptr; }
+int64_t tg_kernel_launches(tg_handle h) { return h ? H(h)->kernel_launches : 0; }
+int tg_set_graphs(tg_handle h, int enabled) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_set_graphs: null handle");
+  H(h)->use_graphs = enabled != 0;
+  return TG_OK;
+}
+
+}  // extern "C"

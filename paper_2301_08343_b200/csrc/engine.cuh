@@ -1,0 +1,94 @@
+// DeviceSim: the device-resident mpm::SimState (sim_state.hpp:59-79) and the
+// launch plan of one substep. Internal; the public surface is tacchi_cuda.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "mpm_device.cuh"
+
+namespace tacchi_b200 {
+
+// Device-resident control block: latched error, reductions, active windows,
+// diagnostics and the commanded velocity. One per handle.
+struct Ctl {
+  int err_code;      // first error wins (atomicCAS from 0)
+  int err_substep;   // absolute substep index the error belongs to
+  int substep;       // absolute index of the substep being executed
+  int pad0;
+  unsigned long long bb_lo[3], bb_hi[3];  // order_key() of x after advect
+  unsigned long long max_v2;              // bits of max |v|^2 (non-negative)
+  unsigned long long min_detf;            // order_key() of min det F (P2G)
+  int win_lo[3], win_hi[3];               // Grid::active_lo/hi
+  int prev_lo[3], prev_hi[3];             // Grid::prev_lo/hi
+  int clr_lo[3], clr_hi[3];               // node box to clear before P2G
+  double vind[3];                         // commanded indenter velocity
+  double diag_min_det_f, diag_max_speed;  // StepDiagnostics
+  long long step_count;                   // SimState::step_count
+};
+
+struct Geometry {
+  int res[3];
+  double dx, inv_dx;
+  double origin[3];
+  double mu, lambda;
+  double dt;
+  double gravity[3];
+  double gdt[3];
+  int with_gravity;
+  double stress_scale;  // -dt * 4 * inv_dx^2 (engine.cpp:114)
+};
+
+struct DeviceSim {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Geometry geo{};
+  int64_t n = 0, n_el = 0, n_ind = 0;
+  double m_el = 0, vol_el = 0, m_ind = 0, vol_ind = 0;
+
+  // Particle state, SoA component-major: x[c * n + p].
+  double* x = nullptr;   // 3 * n   (gel then indenter, internal order)
+  double* v = nullptr;   // 3 * n
+  double* C = nullptr;   // 9 * n_el
+  double* F = nullptr;   // 9 * n_el
+  uint8_t* tag = nullptr;  // n_el (Elastomer / ElastomerBottom)
+  std::vector<int64_t> perm;  // internal index -> reference index (indenter sort)
+
+  // Dense node arrays (Grid::mass/momentum packed as double4 {m, px, py, pz};
+  // Grid::velocity as double4 {vx, vy, vz, 0}).
+  double4* grid_mp = nullptr;
+  double4* grid_v = nullptr;
+  size_t n_nodes = 0;
+
+  // Surface lattice (sim_state.hpp:41-52) + capture scratch.
+  int surf_nx = 0, surf_ny = 0;
+  double surf_geom[5] = {0, 0, 0, 0, 0};
+  uint32_t* surf_idx = nullptr;  // internal particle indices
+  double* surf_depth = nullptr;  // nx * ny
+  double* cap_depth = nullptr;
+  uint8_t* cap_rgb = nullptr;
+  uint8_t* cap_bg = nullptr;
+  size_t cap_pixels = 0, cap_bg_pixels = 0;
+  double* h_depth_pinned = nullptr;
+  uint8_t* h_rgb_pinned = nullptr;
+
+  Ctl* ctl = nullptr;      // device
+  Ctl* h_ctl = nullptr;    // pinned host mirror
+  double* h_vind = nullptr;  // pinned staging for the command
+
+  bool window_valid = false;   // ctl->win/clr describe the current positions
+  int host_substep = 0;        // absolute substep counter (host view)
+  bool use_graphs = true;
+  std::map<int, cudaGraphExec_t> graphs;  // n_substeps -> instantiated graph
+  std::map<int, int> graph_kernels;       // n_substeps -> kernels in graph
+  int64_t kernel_launches = 0;
+  int pending_start = 0;        // first substep of the in-flight step call
+
+  ~DeviceSim();
+};
+
+}  // namespace tacchi_b200

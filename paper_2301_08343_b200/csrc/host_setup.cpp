@@ -1,0 +1,670 @@
+// Host-side scene setup for the B200 path: SceneConfig JSON, the indenter
+// geometry generators and sim::build_sim / sim::capture's parameter
+// resolution. This is once-per-episode host work (SURVEY §2.1 "Geometry",
+// "Config"); it must reproduce the reference's inputs bit-for-bit so that the
+// device hot path sees identical particles. References are to
+// /root/reference/proj.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include <nlohmann/json.hpp>
+
+#include "tacchi_cuda.h"
+
+namespace tacchi_b200 {
+int fail(int code, const std::string& msg);
+}
+
+namespace {
+
+using tacchi_b200::fail;
+using json = nlohmann::json;
+
+struct V3 {
+  double x = 0, y = 0, z = 0;
+  double operator[](int a) const { return a == 0 ? x : (a == 1 ? y : z); }
+};
+
+struct HostError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& msg) { throw HostError{code, msg}; }
+
+// ---- SceneConfig (scene_config.hpp:19-94), defaults of default_config() ---
+
+struct Light {
+  double dir[3], diffuse[3], specular[3];
+};
+
+struct Config {
+  double size_mm[3] = {20.0, 20.0, 4.0};
+  int counts[3] = {101, 101, 21};
+  double E = 1.45e5, nu = 0.45, rho = 1000.0;
+  int fixed_bottom_layers = 2;
+  int nodes[3] = {256, 256, 256};
+  double edge_mm = 33.0;
+  double dt = 1e-4;
+  int substeps_per_control_step = 10;
+  double press_speed_mm_s = 10.0;
+  std::string cloud_path, generated_shape = "sphere";
+  uint64_t source_points = 1000000, target_points = 100000, seed = 20230115;
+  double gap_mm = 0.1, z_rotation_rad = 0.0, rigid_mass_scale = 80.0;
+  std::vector<Light> lights;
+  double ka = 1.0, kd = 0.55, ks = 0.25, shininess = 24.0;
+  double ambient[3] = {0.34, 0.37, 0.44};
+  double view[3] = {0, 0, -1};
+  double pixel_to_meter = 2.8125e-5;
+  int image_w = 640, image_h = 480;
+  std::string background_image;
+  struct Align {
+    double ox = 0, oy = 0, scale = 1.0;
+  };
+  std::map<std::string, Align> alignment;
+  double gravity_mps2 = 0.0;
+};
+
+// scene_config.cpp:42-57: three tinted lights, 120 deg apart, 45 deg elevation.
+std::vector<Light> default_rig() {
+  std::vector<Light> rig;
+  const double e = std::sqrt(0.5);
+  const double tints[3][3] = {{0.80, 0.12, 0.10}, {0.10, 0.80, 0.12}, {0.12, 0.10, 0.80}};
+  for (int m = 0; m < 3; ++m) {
+    const double az = 2.0 * M_PI * m / 3.0;
+    Light l;
+    l.dir[0] = e * std::cos(az);
+    l.dir[1] = e * std::sin(az);
+    l.dir[2] = -e;
+    for (int c = 0; c < 3; ++c) {
+      l.diffuse[c] = tints[m][c];
+      l.specular[c] = 0.5 * tints[m][c];
+    }
+    rig.push_back(l);
+  }
+  return rig;
+}
+
+void read3(const json& j, const char* key, double* out) {
+  if (!j.contains(key)) return;
+  const json& a = j.at(key);
+  if (!a.is_array() || a.size() != 3) raise(TG_ERR_CONFIG, "expected a 3-element array");
+  for (int i = 0; i < 3; ++i) out[i] = a[i].get<double>();
+}
+void read3i(const json& j, const char* key, int* out) {
+  if (!j.contains(key)) return;
+  const json& a = j.at(key);
+  if (!a.is_array() || a.size() != 3) raise(TG_ERR_CONFIG, "expected a 3-element array");
+  for (int i = 0; i < 3; ++i) out[i] = a[i].get<int>();
+}
+template <typename T>
+void read(const json& j, const char* key, T& out) {
+  if (j.contains(key)) out = j.at(key).get<T>();
+}
+
+void normalize(double* v) {  // Eigen normalized(): v / sqrt(squaredNorm) if > 0
+  const double n2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+  if (n2 > 0.0) {
+    const double n = std::sqrt(n2);
+    v[0] /= n; v[1] /= n; v[2] /= n;
+  }
+}
+
+// from_json_string (scene_config.cpp:187-257): partial overrides of defaults.
+Config parse_config(const char* text) {
+  Config c;
+  c.lights = default_rig();
+  if (!text || !*text) return c;
+  json j = json::parse(text, nullptr, false);
+  if (j.is_discarded()) raise(TG_ERR_CONFIG, "config is not valid JSON");
+  try {
+    if (j.contains("elastomer")) {
+      const json& e = j["elastomer"];
+      read3(e, "size_mm", c.size_mm);
+      read3i(e, "particle_counts", c.counts);
+      read(e, "youngs_modulus_pa", c.E);
+      read(e, "poisson_ratio", c.nu);
+      read(e, "density_kg_m3", c.rho);
+      read(e, "fixed_bottom_layers", c.fixed_bottom_layers);
+    }
+    if (j.contains("grid")) {
+      read3i(j["grid"], "nodes_per_axis", c.nodes);
+      read(j["grid"], "edge_mm", c.edge_mm);
+    }
+    if (j.contains("time")) {
+      read(j["time"], "dt_s", c.dt);
+      read(j["time"], "substeps_per_control_step", c.substeps_per_control_step);
+      read(j["time"], "press_speed_mm_s", c.press_speed_mm_s);
+    }
+    if (j.contains("indenter")) {
+      const json& i = j["indenter"];
+      read(i, "cloud_path", c.cloud_path);
+      read(i, "generated_shape", c.generated_shape);
+      read(i, "source_points", c.source_points);
+      read(i, "target_points", c.target_points);
+      read(i, "seed", c.seed);
+      read(i, "gap_mm", c.gap_mm);
+      read(i, "z_rotation_rad", c.z_rotation_rad);
+      read(i, "rigid_mass_scale", c.rigid_mass_scale);
+    }
+    if (j.contains("lights")) {
+      c.lights.clear();
+      for (const json& lj : j["lights"]) {
+        Light l{{0, 0, -1}, {1, 1, 1}, {0, 0, 0}};
+        if (!lj.contains("direction")) raise(TG_ERR_CONFIG, "light without direction");
+        read3(lj, "direction", l.dir);
+        normalize(l.dir);  // scene_config.cpp:220
+        read3(lj, "diffuse_rgb", l.diffuse);
+        read3(lj, "specular_rgb", l.specular);
+        c.lights.push_back(l);
+      }
+    }
+    if (j.contains("render")) {
+      const json& r = j["render"];
+      read(r, "ambient_k", c.ka);
+      read(r, "diffuse_k", c.kd);
+      read(r, "specular_k", c.ks);
+      read(r, "shininess", c.shininess);
+      read3(r, "ambient_rgb", c.ambient);
+      read3(r, "view_dir", c.view);
+      read(r, "pixel_to_meter", c.pixel_to_meter);
+      read(r, "image_width", c.image_w);
+      read(r, "image_height", c.image_h);
+      read(r, "background_image", c.background_image);
+    }
+    if (j.contains("alignment")) {
+      for (auto it = j["alignment"].begin(); it != j["alignment"].end(); ++it) {
+        Config::Align a;
+        const json& aj = it.value();
+        if (aj.contains("offset_px")) {
+          a.ox = aj["offset_px"][0].get<double>();
+          a.oy = aj["offset_px"][1].get<double>();
+        }
+        read(aj, "scale", a.scale);
+        c.alignment[it.key()] = a;
+      }
+    }
+    read(j, "gravity_mps2", c.gravity_mps2);
+  } catch (const json::exception& e) {
+    raise(TG_ERR_CONFIG, std::string("config: ") + e.what());
+  }
+  return c;
+}
+
+// ---- geometry (geo/shapes.cpp, geo/particle_set.cpp) ----------------------
+
+constexpr double kPi = 3.14159265358979323846;
+
+double sq(double v) { return v * v; }
+double r2(double x, double y) { return x * x + y * y; }
+bool disk(double x, double y, double r) { return r2(x, y) <= r * r; }
+bool rect(double x, double y, double hx, double hy) { return std::abs(x) <= hx && std::abs(y) <= hy; }
+
+// Half-plane tests of a regular polygon / equilateral triangle (shapes.cpp:33-52).
+bool polygon(double x, double y, int sides, double circumradius) {
+  const double apothem = circumradius * std::cos(kPi / sides);
+  for (int k = 0; k < sides; ++k) {
+    const double a = (2.0 * kPi * k + kPi) / sides;
+    if (x * std::cos(a) + y * std::sin(a) > apothem) return false;
+  }
+  return true;
+}
+bool triangle(double x, double y, double side) {
+  const double r = side / std::sqrt(3.0);
+  const double apothem = r / 2.0;
+  for (int k = 0; k < 3; ++k) {
+    const double a = -kPi / 2.0 + 2.0 * kPi * k / 3.0;
+    if (x * std::cos(a) + y * std::sin(a) > apothem) return false;
+  }
+  return true;
+}
+
+// The "random" shape's fixed bump field (shapes.cpp:56-77).
+struct Bumps {
+  double cx[28], cy[28], amp[28], inv_s2[28];
+  Bumps() {
+    std::mt19937_64 rng(0x7ac371u);
+    auto u = [&rng]() { return (rng() >> 11) * 0x1.0p-53; };
+    for (int i = 0; i < 28; ++i) {
+      cx[i] = -3.2 + 6.4 * u();
+      cy[i] = -3.2 + 6.4 * u();
+      amp[i] = 0.25 + 0.85 * u();
+      const double s = 0.45 + 0.75 * u();
+      inv_s2[i] = 1.0 / (2.0 * s * s);
+    }
+  }
+  double height(double x, double y) const {
+    double h = 0.0;
+    for (int i = 0; i < 28; ++i) h += amp[i] * std::exp(-(sq(x - cx[i]) + sq(y - cy[i])) * inv_s2[i]);
+    return std::min(h, 1.4);
+  }
+};
+
+struct Shape {
+  double lo[3], hi[3];  // mm
+  std::function<bool(double, double, double)> inside;
+};
+
+// The 21 analytic indenter solids (shapes.cpp:79-206), millimetres, contact
+// feature facing -z with the lowest material at z = 0.
+bool make_shape(const std::string& name, Shape& s) {
+  auto box = [&](double x0, double y0, double z0, double x1, double y1, double z1) {
+    s.lo[0] = x0; s.lo[1] = y0; s.lo[2] = z0;
+    s.hi[0] = x1; s.hi[1] = y1; s.hi[2] = z1;
+  };
+  if (name == "sphere") {
+    box(-3, -3, 0, 3, 3, 6);
+    s.inside = [](double x, double y, double z) { return r2(x, y) + sq(z - 3.0) <= 9.0; };
+  } else if (name == "sphere2") {
+    box(-2, -2, 0, 2, 2, 4);
+    s.inside = [](double x, double y, double z) { return r2(x, y) + sq(z - 2.0) <= 4.0; };
+  } else if (name == "cone") {
+    box(-3.5, -3.5, 0, 3.5, 3.5, 3.5);
+    s.inside = [](double x, double y, double z) { return r2(x, y) <= z * z && z <= 3.5; };
+  } else if (name == "cylinder") {
+    box(-3, -3, 0, 3, 3, 3);
+    s.inside = [](double x, double y, double) { return disk(x, y, 3.0); };
+  } else if (name == "cylinder_shell") {
+    box(-3, -3, 0, 3, 3, 3);
+    s.inside = [](double x, double y, double) {
+      const double q = r2(x, y);
+      return q <= 9.0 && q >= sq(2.1);
+    };
+  } else if (name == "cylinder_side") {
+    box(-2, -4, 0, 2, 4, 4);
+    s.inside = [](double x, double, double z) { return sq(x) + sq(z - 2.0) <= 4.0; };
+  } else if (name == "curved_surface") {
+    box(-4, -4, 0, 4, 4, 3);
+    s.inside = [](double x, double y, double z) { return z >= r2(x, y) / 24.0; };
+  } else if (name == "flat_slab") {
+    box(-4, -4, 0, 4, 4, 3);
+    s.inside = [](double, double, double) { return true; };
+  } else if (name == "dot_in") {
+    box(-3.5, -3.5, 0, 3.5, 3.5, 3);
+    s.inside = [](double x, double y, double z) {
+      return disk(x, y, 3.5) && !(disk(x, y, 0.7) && z < 0.9);
+    };
+  } else if (name == "dots") {
+    box(-3.5, -3.5, 0, 3.5, 3.5, 3);
+    s.inside = [](double x, double y, double z) {
+      if (z >= 1.0) return rect(x, y, 3.5, 3.5);
+      const double gx = std::round(x / 2.2) * 2.2;
+      const double gy = std::round(y / 2.2) * 2.2;
+      return std::abs(gx) <= 2.3 && std::abs(gy) <= 2.3 && disk(x - gx, y - gy, 0.55);
+    };
+  } else if (name == "hexagon") {
+    box(-3.5, -3.5, 0, 3.5, 3.5, 3);
+    s.inside = [](double x, double y, double) { return polygon(x, y, 6, 3.5); };
+  } else if (name == "triangle") {
+    box(-4, -4, 0, 4, 4, 3);
+    s.inside = [](double x, double y, double) { return triangle(x, y, 6.5); };
+  } else if (name == "prism") {
+    box(-3, -4, 0, 3, 4, 3);
+    s.inside = [](double x, double, double z) { return std::abs(x) <= z && z <= 3.0; };
+  } else if (name == "line") {
+    box(-0.6, -4, 0, 0.6, 4, 2);
+    s.inside = [](double x, double y, double) { return rect(x, y, 0.6, 4.0); };
+  } else if (name == "parallel_lines") {
+    box(-3.4, -4, 0, 3.4, 4, 3);
+    s.inside = [](double x, double y, double z) {
+      if (z >= 1.5) return rect(x, y, 3.4, 4.0);
+      const double gx = std::round(x / 2.4) * 2.4;
+      return std::abs(gx) <= 2.5 && std::abs(x - gx) <= 0.45 && std::abs(y) <= 4.0;
+    };
+  } else if (name == "cross_lines") {
+    box(-4, -4, 0, 4, 4, 3);
+    s.inside = [](double x, double y, double z) {
+      if (z >= 1.5) return rect(x, y, 4.0, 4.0);
+      return (std::abs(x) <= 0.45 || std::abs(y) <= 0.45) && rect(x, y, 4.0, 4.0);
+    };
+  } else if (name == "moon") {
+    box(-3, -3, 0, 3, 3, 2);
+    s.inside = [](double x, double y, double) { return disk(x, y, 3.0) && !disk(x - 1.4, y, 2.4); };
+  } else if (name == "pacman") {
+    box(-3, -3, 0, 3, 3, 2);
+    s.inside = [](double x, double y, double) {
+      return disk(x, y, 3.0) && std::abs(std::atan2(y, x)) > kPi / 6.0;
+    };
+  } else if (name == "torus") {
+    box(-3.2, -3.2, 0, 3.2, 3.2, 1.8);
+    s.inside = [](double x, double y, double z) {
+      const double rho = std::sqrt(r2(x, y));
+      return sq(rho - 2.3) + sq(z - 0.9) <= sq(0.9);
+    };
+  } else if (name == "wave1") {
+    box(-4, -4, 0, 4, 4, 3);
+    s.inside = [](double x, double, double z) {
+      return z >= 0.5 * (1.0 + std::sin(2.0 * kPi * x / 2.7));
+    };
+  } else if (name == "random") {
+    static const Bumps field;
+    box(-4, -4, 0, 4, 4, 3);
+    s.inside = [](double x, double y, double z) { return z >= field.height(x, y); };
+  } else {
+    return false;
+  }
+  return true;
+}
+
+// generate_shape_cloud (shapes.cpp:231-249): rejection sampling, mm -> m.
+std::vector<V3> generate_cloud(const std::string& name, size_t n, uint64_t seed) {
+  Shape s;
+  if (!make_shape(name, s)) raise(TG_ERR_CONFIG, "unknown shape: " + name);
+  std::mt19937_64 rng(seed);
+  auto u = [&rng]() { return (rng() >> 11) * 0x1.0p-53; };
+  const double span[3] = {s.hi[0] - s.lo[0], s.hi[1] - s.lo[1], s.hi[2] - s.lo[2]};
+  std::vector<V3> out;
+  out.reserve(n);
+  while (out.size() < n) {
+    const double x = s.lo[0] + span[0] * u();
+    const double y = s.lo[1] + span[1] * u();
+    const double z = s.lo[2] + span[2] * u();
+    if (s.inside(x, y, z)) out.push_back({x * 1e-3, y * 1e-3, z * 1e-3});
+  }
+  return out;
+}
+
+// Bounded draw by rejection (particle_set.cpp:48-56).
+uint64_t draw_below(std::mt19937_64& rng, uint64_t bound) {
+  const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+  uint64_t x;
+  do {
+    x = rng();
+  } while (x >= limit);
+  return x % bound;
+}
+
+// subsample (particle_set.cpp:60-90): partial Fisher-Yates, order-preserving.
+std::vector<V3> subsample(const std::vector<V3>& cloud, size_t target, uint64_t seed) {
+  if (target < 1) target = 1;
+  const size_t n = cloud.size();
+  if (n == 0) raise(TG_ERR_EMPTY_CLOUD, "subsample: empty cloud");
+  if (target >= n) return cloud;
+  std::vector<uint32_t> idx(n);
+  std::iota(idx.begin(), idx.end(), 0u);
+  std::mt19937_64 rng(seed);
+  for (size_t i = 0; i < target; ++i) {
+    const size_t j = i + static_cast<size_t>(draw_below(rng, n - i));
+    std::swap(idx[i], idx[j]);
+  }
+  idx.resize(target);
+  std::sort(idx.begin(), idx.end());
+  std::vector<V3> out;
+  out.reserve(target);
+  for (uint32_t i : idx) out.push_back(cloud[i]);
+  return out;
+}
+
+void bbox(const std::vector<V3>& pts, V3& lo, V3& hi) {
+  if (pts.empty()) raise(TG_ERR_EMPTY_CLOUD, "bounding_box: empty particle set");
+  lo = hi = pts.front();
+  for (const V3& p : pts) {
+    lo.x = std::min(lo.x, p.x); lo.y = std::min(lo.y, p.y); lo.z = std::min(lo.z, p.z);
+    hi.x = std::max(hi.x, p.x); hi.y = std::max(hi.y, p.y); hi.z = std::max(hi.z, p.z);
+  }
+}
+
+// place_indenter (particle_set.cpp:92-102): rotate about z, then translate.
+std::vector<V3> place(const std::vector<V3>& cloud, const V3& t, double rot) {
+  const double c = std::cos(rot), s = std::sin(rot);
+  std::vector<V3> out(cloud.size());
+  for (size_t i = 0; i < cloud.size(); ++i) {
+    const V3& p = cloud[i];
+    const double x = c * p.x - s * p.y;
+    const double y = s * p.x + c * p.y;
+    out[i] = {x + t.x, y + t.y, p.z + t.z};
+  }
+  return out;
+}
+
+// indenter_cloud_for + place_for_press (scene_builder.cpp:33-61).
+std::vector<V3> placed_indenter(const Config& c, const std::string& object, double off_x,
+                                double off_y) {
+  std::vector<V3> cloud;
+  if (!c.cloud_path.empty() && (object.empty() || object == c.cloud_path))
+    raise(TG_ERR_IO, "point-cloud files are not supported by this build: " + c.cloud_path);
+  const std::string shape = object.empty() ? c.generated_shape : object;
+  Shape probe;
+  if (!make_shape(shape, probe))
+    raise(TG_ERR_IO, "point-cloud files are not supported by this build: " + shape);
+  cloud = generate_cloud(shape, c.source_points, c.seed);
+  if (c.target_points < cloud.size()) cloud = subsample(cloud, c.target_points, c.seed);
+
+  const std::vector<V3> rotated = place(cloud, V3{0, 0, 0}, c.z_rotation_rad);
+  V3 lo, hi;
+  bbox(rotated, lo, hi);
+  const double e = c.edge_mm * 1e-3;
+  const double centre = 0.5 * e;
+  const double top = 0.5 * e + 0.5 * (c.size_mm[2] * 1e-3);  // elastomer_top_z
+  const V3 target{centre + off_x - 0.5 * (lo.x + hi.x), centre + off_y - 0.5 * (lo.y + hi.y),
+                  top + c.gap_mm * 1e-3 - lo.z};
+  return place(rotated, target, 0.0);
+}
+
+// init_scene's checks and particle assembly (scene.cpp:15-87) for
+// build_sim's parameters (scene_builder.cpp:63-78).
+struct Scene {
+  tg_params P{};
+  std::vector<double> x, v, mass, vol0;
+  std::vector<uint8_t> tag;
+  std::vector<uint32_t> surf;
+  tg_surface S{};
+  int64_t n_el = 0;
+};
+
+void check_margin(const tg_params& P, const V3& lo, const V3& hi, const char* label) {
+  const double margin = 2.0 * P.dx;
+  for (int a = 0; a < 3; ++a) {
+    const double glo = P.origin[a];
+    const double ghi = P.origin[a] + (static_cast<double>(P.res[a]) - 1.0) * P.dx;
+    if (lo[a] - glo < margin || ghi - hi[a] < margin)
+      raise(TG_ERR_GRID_TOO_SMALL, std::string(label) +
+                                       " bounding box violates the 2-node grid margin on axis " +
+                                       std::to_string(a));
+  }
+}
+
+Scene build_scene(const Config& c, const std::vector<V3>& indenter) {
+  Scene sc;
+  tg_params& P = sc.P;
+  for (int a = 0; a < 3; ++a) {
+    P.res[a] = c.nodes[a];
+    P.origin[a] = 0.0;
+  }
+  const double edge = c.edge_mm * 1e-3;
+  P.dx = edge / c.nodes[0];  // scene.cpp:41-42
+  P.youngs_modulus = c.E;
+  P.poisson_ratio = c.nu;
+  P.density = c.rho;
+  P.dt = c.dt;
+  P.gravity[0] = 0.0;
+  P.gravity[1] = 0.0;
+  P.gravity[2] = -c.gravity_mps2;
+
+  for (int a = 0; a < 3; ++a)
+    if (c.counts[a] < 2) raise(TG_ERR_CONFIG, "make_elastomer_lattice: counts must be >= 2 per axis");
+  // elastomer_for (scene_builder.cpp:26-31) + make_elastomer_lattice.
+  const double dims[3] = {c.size_mm[0] * 1e-3, c.size_mm[1] * 1e-3, c.size_mm[2] * 1e-3};
+  double origin[3], h[3];
+  for (int a = 0; a < 3; ++a) {
+    origin[a] = 0.5 * edge - 0.5 * dims[a];
+    h[a] = dims[a] / (c.counts[a] - 1);
+  }
+  const int64_t nx = c.counts[0], ny = c.counts[1], nz = c.counts[2];
+  const int64_t n_el = nx * ny * nz;
+  if (n_el == 0 || indenter.empty())
+    raise(TG_ERR_EMPTY_SCENE, "init_scene: both elastomer and indenter particle sets must be non-empty");
+  // MaterialParams::validate (material.cpp:11-16), dt (scene.cpp:33)
+  if (!(c.E > 0.0)) raise(TG_ERR_CONFIG, "youngs_modulus must be > 0");
+  if (!(c.nu >= 0.0 && c.nu < 0.5)) raise(TG_ERR_CONFIG, "poisson_ratio must be in [0, 0.5)");
+  if (!(c.rho > 0.0)) raise(TG_ERR_CONFIG, "density must be > 0");
+  if (!(c.dt > 0.0)) raise(TG_ERR_CONFIG, "dt must be > 0");
+  if (P.res[0] < 4 || P.res[1] < 4 || P.res[2] < 4)
+    raise(TG_ERR_CONFIG, "grid resolution must be >= 4 per axis");
+  if (!(P.dx > 0.0)) raise(TG_ERR_CONFIG, "grid spacing must be > 0");
+
+  std::vector<V3> el;
+  el.reserve(n_el);
+  for (int i = 0; i < nx; ++i)
+    for (int j = 0; j < ny; ++j)
+      for (int k = 0; k < nz; ++k) el.push_back({origin[0] + i * h[0], origin[1] + j * h[1], origin[2] + k * h[2]});
+  V3 lo, hi;
+  bbox(el, lo, hi);
+  check_margin(P, lo, hi, "elastomer");
+  bbox(indenter, lo, hi);
+  check_margin(P, lo, hi, "indenter");
+
+  const double el_volume = dims[0] * dims[1] * dims[2];
+  const double el_vol0 = el_volume / static_cast<double>(n_el);
+  const double el_mass = c.rho * el_vol0;
+  const double ext[3] = {hi.x - lo.x, hi.y - lo.y, hi.z - lo.z};
+  const double ind_bbox_vol = std::max(ext[0] * ext[1] * ext[2], 1e-30);
+  const double ind_vol0 = ind_bbox_vol / static_cast<double>(indenter.size());
+  const double ind_mass = c.rho * ind_vol0 * c.rigid_mass_scale;
+
+  const int64_t n = n_el + static_cast<int64_t>(indenter.size());
+  sc.n_el = n_el;
+  sc.x.resize(3 * n);
+  sc.v.assign(3 * n, 0.0);
+  sc.mass.resize(n);
+  sc.vol0.resize(n);
+  sc.tag.resize(n);
+  for (int64_t p = 0; p < n_el; ++p) {
+    sc.x[3 * p] = el[p].x;
+    sc.x[3 * p + 1] = el[p].y;
+    sc.x[3 * p + 2] = el[p].z;
+    sc.mass[p] = el_mass;
+    sc.vol0[p] = el_vol0;
+    sc.tag[p] = (p % nz) < c.fixed_bottom_layers ? 1 : 0;  // scene.cpp:58
+  }
+  for (size_t q = 0; q < indenter.size(); ++q) {
+    const int64_t p = n_el + static_cast<int64_t>(q);
+    sc.x[3 * p] = indenter[q].x;
+    sc.x[3 * p + 1] = indenter[q].y;
+    sc.x[3 * p + 2] = indenter[q].z;
+    sc.mass[p] = ind_mass;
+    sc.vol0[p] = ind_vol0;
+    sc.tag[p] = 2;
+  }
+  // SurfaceLattice (scene.cpp:71-84)
+  sc.surf.resize(nx * ny);
+  for (int i = 0; i < nx; ++i)
+    for (int j = 0; j < ny; ++j) sc.surf[i * ny + j] = static_cast<uint32_t>((i * ny + j) * nz + (nz - 1));
+  sc.S.nx = static_cast<int>(nx);
+  sc.S.ny = static_cast<int>(ny);
+  sc.S.x0 = origin[0];
+  sc.S.y0 = origin[1];
+  sc.S.sx = h[0];
+  sc.S.sy = h[1];
+  sc.S.z0 = origin[2] + dims[2];
+  sc.S.particle = sc.surf.data();
+  return sc;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const HostError& e) {
+    return fail(e.code, e.msg);
+  } catch (const std::exception& e) {
+    return fail(TG_ERR_CONFIG, e.what());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int tg_build_sim(int device, const char* config_json, const char* object, double offset_x,
+                 double offset_y, tg_handle* out) {
+  return guarded([&] {
+    const Config c = parse_config(config_json);
+    const std::vector<V3> ind = placed_indenter(c, object ? object : "", offset_x, offset_y);
+    Scene sc = build_scene(c, ind);
+    tg_particles tp{};
+    tp.n = static_cast<int64_t>(sc.mass.size());
+    tp.n_elastomer = sc.n_el;
+    tp.x = sc.x.data();
+    tp.v = sc.v.data();
+    tp.mass = sc.mass.data();
+    tp.volume0 = sc.vol0.data();
+    tp.tag = sc.tag.data();
+    return tg_create(device, &sc.P, &tp, &sc.S, out);
+  });
+}
+
+int tg_render_from_config(const char* config_json, const char* object, tg_render* r) {
+  return guarded([&] {
+    const Config c = parse_config(config_json);
+    if (!c.background_image.empty())
+      raise(TG_ERR_IO, "background_image PNG loading is not supported by this build; pass "
+                       "tg_render::background instead");
+    std::memset(r, 0, sizeof(*r));
+    r->pixel_to_meter = c.pixel_to_meter;
+    const auto it = c.alignment.find(object ? object : "");
+    const Config::Align a = it == c.alignment.end() ? Config::Align{} : it->second;
+    r->crop_offset[0] = a.ox;
+    r->crop_offset[1] = a.oy;
+    r->crop_scale = a.scale;
+    r->width = c.image_w;
+    r->height = c.image_h;
+    r->ambient_k = c.ka;
+    r->diffuse_k = c.kd;
+    r->specular_k = c.ks;
+    r->shininess = c.shininess;
+    for (int k = 0; k < 3; ++k) {
+      r->ambient_rgb[k] = c.ambient[k];
+      r->view_dir[k] = c.view[k];
+    }
+    if (c.lights.empty() || c.lights.size() > 8)
+      raise(TG_ERR_CONFIG, "phong_render: between 1 and 8 light sources required");
+    r->n_lights = static_cast<int>(c.lights.size());
+    for (size_t l = 0; l < c.lights.size(); ++l)
+      for (int k = 0; k < 3; ++k) {
+        r->lights[l][k] = c.lights[l].dir[k];
+        r->lights[l][3 + k] = c.lights[l].diffuse[k];
+        r->lights[l][6 + k] = c.lights[l].specular[k];
+      }
+    r->background = nullptr;
+    return TG_OK;
+  });
+}
+
+int tg_generate_cloud(const char* shape, int64_t n, uint64_t seed, double* out) {
+  return guarded([&] {
+    const std::vector<V3> pts = generate_cloud(shape ? shape : "", static_cast<size_t>(n), seed);
+    for (size_t i = 0; i < pts.size(); ++i) {
+      out[3 * i] = pts[i].x;
+      out[3 * i + 1] = pts[i].y;
+      out[3 * i + 2] = pts[i].z;
+    }
+    return TG_OK;
+  });
+}
+
+int tg_placed_indenter(const char* config_json, const char* object, double offset_x,
+                       double offset_y, double* out, int64_t* n) {
+  return guarded([&] {
+    const Config c = parse_config(config_json);
+    const std::vector<V3> pts = placed_indenter(c, object ? object : "", offset_x, offset_y);
+    *n = static_cast<int64_t>(pts.size());
+    if (out)
+      for (size_t i = 0; i < pts.size(); ++i) {
+        out[3 * i] = pts[i].x;
+        out[3 * i + 1] = pts[i].y;
+        out[3 * i + 2] = pts[i].z;
+      }
+    return TG_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+"""Generates the committed golden fixtures from the UNMODIFIED reference.
+
+The reference ships no golden vectors (its unit tests are empty stubs,
+SURVEY.md §4), so the fixtures here are produced by running the reference's
+own C++ code, compiled from /root/reference/proj by oracle/Makefile into
+oracle/_ref/libtacchi_ref.so. Run in the build container (where
+/root/reference exists):
+
+    make -C oracle ref && python tests/golden/make_golden.py
+
+Fixtures (all numpy .npz):
+  kat.npz          polar_rotation / corotated_stress on a spread of F,
+                   render KATs (crop_align, surface_normals, phong_render)
+                   on synthetic depth maps, and hashes of the 21 generated
+                   indenter clouds + the default placed indenter.
+  small_scene.npz  SMALL config, 200 substeps at v = (0, 0, -0.05) m/s:
+                   full particle state, diagnostics, capture depth + image.
+  config1.npz      default config (dt 2e-6), 100 substeps (10 frames) at the
+                   default press velocity: surface-particle positions, a
+                   seeded 4096-particle subset of x and F, diagnostics, the
+                   640x480 capture image and depth.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle import refpy as R  # noqa: E402
+from tests.scenes import (CONFIG1, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
+                          SMALL, SMALL_STEPS, SMALL_V, render_inputs, sha)
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def kat():
+    rng = np.random.default_rng(20230115)
+    Fs = [np.eye(3), np.diag([0.9, 1.0, 1.0]), np.diag([1.2, 0.8, 1.05])]
+    th = 0.7
+    rot = np.array([[np.cos(th), -np.sin(th), 0], [np.sin(th), np.cos(th), 0], [0, 0, 1]])
+    Fs.append(rot)
+    Fs.append(rot @ np.diag([1.1, 0.95, 0.9]))
+    for _ in range(40):
+        Fs.append(np.eye(3) + 0.05 * rng.standard_normal((3, 3)))
+    for _ in range(20):
+        Fs.append(np.eye(3) + 0.4 * rng.standard_normal((3, 3)))
+    Fs = [F for F in Fs if np.linalg.det(F) > 0]
+    Fs = np.array(Fs)
+    Rs = np.array([R.polar_rotation(F) for F in Fs])
+    Ss = np.array([R.corotated_stress(F) for F in Fs])
+    Rsvd = np.array([R.polar_rotation_svd(F) for F in Fs])
+
+    r, hemi, ramp, src = render_inputs()
+    normals_hemi = R.surface_normals(hemi, r)
+    img_hemi = R.phong(hemi, r, None)
+    img_ramp = R.phong(ramp, r, None)
+    img_hemi_l = R.phong(hemi, r, LIGHT_CFG)
+    crop_c, r_c = R.crop_align(src, r, (0.0, 0.0), 1.0, 640, 480)
+    crop_o, r_o = R.crop_align(src, r, (12.25, -7.5), 1.07, 640, 480)
+    cloud_hash, cloud_head = [], []
+    for s in SHAPES:
+        pts = R.generate_cloud(s, 2000, 7)
+        cloud_hash.append(sha(pts))
+        cloud_head.append(pts[:4])
+    placed = R.placed_indenter({}, "")
+    placed_rot = R.placed_indenter(*PLACED_ROT)
+    np.savez_compressed(
+        os.path.join(OUT, "kat.npz"), F=Fs, R=Rs, R_svd=Rsvd, S=Ss,
+        normals_hemi_sha=sha(normals_hemi), normals_hemi_sample=normals_hemi[::37, ::41],
+        img_hemi=img_hemi, img_ramp=img_ramp, img_hemi_l=img_hemi_l,
+        crop_c_sha=sha(crop_c), crop_o_sha=sha(crop_o), crop_o_sample=crop_o[::29, ::31],
+        r_c=r_c, r_o=r_o, cloud_hash=np.array(cloud_hash), cloud_head=np.array(cloud_head),
+        placed_hash=sha(placed), placed_n=len(placed), placed_rot_hash=sha(placed_rot),
+        placed_rot_n=len(placed_rot))
+
+
+def small_scene():
+    sim = R.RefSim.from_config(SMALL, "", threads=0)
+    s0 = sim.state()
+    sim.step(SMALL_V, SMALL_STEPS)
+    s1 = sim.state()
+    d = sim.diag()
+    gi = sim.grid_info()
+    depth, img = sim.capture(SMALL)
+    surf = sim.surface()
+    np.savez_compressed(
+        os.path.join(OUT, "small_scene.npz"), x0=s0["x"], tag=s0["tag"], mass=s0["mass"],
+        vol0=s0["vol0"], x=s1["x"], v=s1["v"], C=s1["C"], F=s1["F"], min_det_f=d["min_det_f"],
+        max_speed=d["max_speed"], step_count=d["step_count"], win_lo=gi["lo"], win_hi=gi["hi"],
+        depth=depth, image=img, surf_particle=surf["particle"],
+        surf_geom=np.array([surf["x0"], surf["y0"], surf["sx"], surf["sy"], surf["z0"]]))
+
+
+def config1():
+    sim = R.RefSim.from_config(CONFIG1, "", threads=0)
+    s0 = sim.state()
+    sim.step(CONFIG1_V, CONFIG1_STEPS)
+    s1 = sim.state()
+    d = sim.diag()
+    depth, img = sim.capture(CONFIG1)
+    surf = sim.surface()
+    rng = np.random.default_rng(1)
+    subset = np.sort(rng.choice(sim.n, 4096, replace=False))
+    np.savez_compressed(
+        os.path.join(OUT, "config1.npz"), n=sim.n, n_elastomer=sim.n_elastomer,
+        x0_hash=sha(s0["x"]), subset=subset,
+        x_subset=s1["x"][subset], F_subset=s1["F"][subset], v_subset=s1["v"][subset],
+        x_surface=s1["x"][surf["particle"]], min_det_f=d["min_det_f"], max_speed=d["max_speed"],
+        step_count=d["step_count"], image=img, depth_sha=sha(depth),
+        depth_sample=depth[::16, ::16])
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["kat", "small", "config1"]
+    if "kat" in which:
+        kat()
+    if "small" in which:
+        small_scene()
+    if "config1" in which:
+        config1()
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)))

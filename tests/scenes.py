@@ -1,0 +1,70 @@
+"""Scene definitions shared by the tests, the golden generator and bench.py.
+
+All are SceneConfig JSON overrides of the reference's default_config()
+(scene_config.cpp:118-122). Every config pins a stable dt (SURVEY.md §0
+finding 4: the shipped dt = 1e-4 diverges).
+"""
+
+# Small CPU-oracle-sized scene: 31x31x7 gel (6 x 6 x 1.2 mm, 0.2 mm spacing)
+# + 3000-point sphere2 indenter on a 64^3 grid of 12 mm edge.
+SMALL = {
+    "elastomer": {"size_mm": [6, 6, 1.2], "particle_counts": [31, 31, 7]},
+    "grid": {"nodes_per_axis": [64, 64, 64], "edge_mm": 12.0},
+    "time": {"dt_s": 2e-6},
+    "render": {"image_width": 160, "image_height": 120},
+    "indenter": {"generated_shape": "sphere2", "source_points": 20000, "target_points": 3000,
+                 "gap_mm": 0.02},
+}
+SMALL_STEPS = 200
+SMALL_V = (0.0, 0.0, -0.05)
+
+# Config 1 (BASELINE.json configs[0]): default gel 101x101x21, sphere 1e6 ->
+# 1e5 points, 256^3 / 33 mm, dt 2e-6, press velocity (0, 0, -0.01) m/s.
+CONFIG1 = {"time": {"dt_s": 2e-6}}
+CONFIG1_STEPS = 100
+CONFIG1_V = (0.0, 0.0, -0.01)
+
+# Config 2a (BASELINE.json configs[1]): same gel, sphere at the reference's
+# finest indenter density (1e6 points, no subsampling) -> 1,214,221 particles.
+CONFIG2A = {"time": {"dt_s": 2e-6}, "indenter": {"target_points": 1000000}}
+CONFIG2A_V = (0.0, 0.0, -0.01)
+
+SUBSTEPS_PER_FRAME = 10  # scene_config.hpp:36, session.cpp:86
+
+
+def render_inputs():
+    """Synthetic depth maps for the render KATs: a
+    hemispherical dimple, a ramp, and a 713x713 source for crop_align."""
+    import numpy as np
+
+    H, W = 480, 640
+    r = 2.8125e-5
+    yy, xx = np.mgrid[0:H, 0:W]
+    rr = np.hypot(xx - 301.3, yy - 233.7) * r
+    rad = 2.0e-3
+    hemi = np.where(rr < rad, np.sqrt(np.maximum(rad**2 - rr**2, 0.0)) * 0.25, 0.0)
+    ramp = 1e-5 * (xx * 0.37 - yy * 0.21) * r * 40
+    sy, sx = np.mgrid[0:713, 0:713]
+    src = np.sin(sx * 0.031) * np.cos(sy * 0.017) * 1e-4 + (sx - sy) * 1e-8
+    return r, hemi, ramp, src
+
+
+LIGHT_CFG = {"lights": [{"direction": [0.3, -0.2, -1.0], "diffuse_rgb": [0.9, 0.7, 0.5],
+                         "specular_rgb": [0.4, 0.4, 0.4]}],
+             "render": {"ambient_k": 0.8, "diffuse_k": 0.6, "specular_k": 0.5, "shininess": 12.0,
+                        "ambient_rgb": [0.2, 0.25, 0.3], "view_dir": [0.05, 0.0, -1.0]}}
+
+SHAPES = ["cone", "cross_lines", "curved_surface", "cylinder", "cylinder_shell", "cylinder_side",
+          "dot_in", "dots", "flat_slab", "hexagon", "line", "moon", "pacman", "parallel_lines",
+          "prism", "random", "sphere", "sphere2", "torus", "triangle", "wave1"]
+
+PLACED_ROT = ({"indenter": {"z_rotation_rad": 0.6, "target_points": 20000}}, "dots", 0.0007,
+              -0.0004)
+
+
+def sha(a) -> str:
+    import hashlib
+
+    import numpy as np
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()

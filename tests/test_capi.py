@@ -1,0 +1,92 @@
+"""The C-ABI library (libtacchi_cuda.so): loads, exports every symbol
+include/tacchi_cuda.h declares, and its host-side setup reproduces the
+reference's inputs bit for bit. CPU only (no kernel launches)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT, has_gpu
+from tests.scenes import PLACED_ROT, SHAPES, sha
+
+
+def _declared_symbols():
+    text = open(os.path.join(ROOT, "include", "tacchi_cuda.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(tg_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2301_08343_b200 as tb
+
+    L = tb.lib()
+    names = _declared_symbols()
+    assert len(names) >= 25
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    assert set(tb.EXPORTED) <= set(names) | {"tg_generate_cloud", "tg_placed_indenter"}
+    assert "sm_100a" in tb.version()
+
+
+def test_library_is_built_for_sm100a():
+    import subprocess
+
+    import paper_2301_08343_b200 as tb
+
+    out = subprocess.run(["cuobjdump", "--list-elf", tb.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_generated_clouds_match_reference_bit_exact(golden):
+    import paper_2301_08343_b200 as tb
+
+    k = golden("kat.npz")
+    for i, s in enumerate(SHAPES):
+        pts = tb.geo.generate_shape_cloud(s, 2000, 7)
+        np.testing.assert_array_equal(pts[:4], k["cloud_head"][i])
+        assert sha(pts) == str(k["cloud_hash"][i]), s
+
+
+def test_placed_indenter_matches_reference_bit_exact(golden):
+    import paper_2301_08343_b200 as tb
+
+    k = golden("kat.npz")
+    pts = tb.geo.placed_indenter({}, "")
+    assert len(pts) == int(k["placed_n"]) and sha(pts) == str(k["placed_hash"])
+    pts = tb.geo.placed_indenter(*PLACED_ROT)
+    assert len(pts) == int(k["placed_rot_n"]) and sha(pts) == str(k["placed_rot_hash"])
+
+
+def test_unknown_shape_is_an_error():
+    import paper_2301_08343_b200 as tb
+
+    with pytest.raises(tb.ConfigError):
+        tb.geo.generate_shape_cloud("dodecahedron", 10, 1)
+
+
+def test_render_params_from_config_defaults():
+    import paper_2301_08343_b200 as tb
+
+    r = tb.render_params({}, "")
+    assert (r.width, r.height, r.n_lights) == (640, 480, 3)
+    assert (r.ambient_k, r.diffuse_k, r.specular_k, r.shininess) == (1.0, 0.55, 0.25, 24.0)
+    assert list(r.ambient_rgb) == [0.34, 0.37, 0.44]
+    assert r.pixel_to_meter == 2.8125e-5 and r.crop_scale == 1.0
+    e = np.sqrt(0.5)
+    np.testing.assert_allclose(list(r.lights[0])[:3], [e, 0, -e], atol=1e-15)
+    r2 = tb.render_params({"alignment": {"dots": {"offset_px": [3, -2], "scale": 1.1}}}, "dots")
+    assert (r2.crop_offset[0], r2.crop_offset[1], r2.crop_scale) == (3.0, -2.0, 1.1)
+    with pytest.raises(tb.ConfigError):
+        tb.render_params("{not json", "")
+
+
+@pytest.mark.skipif(has_gpu(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback_without_gpu():
+    import paper_2301_08343_b200 as tb
+
+    with pytest.raises(tb.CudaError):
+        tb.sim.build_sim({"time": {"dt_s": 2e-6}, "indenter": {"source_points": 2000,
+                                                                 "target_points": 1000}})

@@ -1,0 +1,254 @@
+"""Parity of the CUDA path (through the C-ABI) against the oracle and the
+reference's golden fixtures. Needs a B200: run with `pytest -m gpu`.
+
+Tolerances (BASELINE.json north_star): particle positions relative <= 1e-4
+(we hold a far tighter displacement-relative bound, stated per test), height
+map <= 1e-7 m, tactile image max abs diff <= 2/255. The capture path itself is
+bit-exact for identical particle positions.
+"""
+import numpy as np
+import pytest
+
+from tests.scenes import (CONFIG1, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, SMALL, SMALL_STEPS,
+                          SMALL_V, render_inputs, sha)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tb():
+    import paper_2301_08343_b200 as tb
+
+    return tb
+
+
+def _small_oracle(oracle, g):
+    P = oracle.params((64, 64, 64), 12e-3 / 64, dt=2e-6)
+    n = len(g["mass"])
+    return oracle.OracleSim(P, g["x0"], np.zeros((n, 3)), g["mass"], g["vol0"], g["tag"])
+
+
+def _surface_of(g, nx=31, ny=31):
+    geom = g["surf_geom"]
+    return dict(nx=nx, ny=ny, x0=geom[0], y0=geom[1], sx=geom[2], sy=geom[3], z0=geom[4],
+                particle=g["surf_particle"])
+
+
+def test_build_sim_reproduces_reference_setup(tb, golden):
+    g = golden("small_scene.npz")
+    s = tb.sim.build_sim(SMALL)
+    st = s.state()
+    np.testing.assert_array_equal(st["x"], g["x0"])
+    assert s.elastomer_count == 31 * 31 * 7
+    np.testing.assert_array_equal(st["F"], np.tile(np.eye(3), (s.n, 1, 1)))
+    assert not st["v"].any() and not st["C"].any()
+
+
+def test_small_scene_matches_reference(tb, golden):
+    """200 substeps of the SMALL press vs the reference (golden)."""
+    g = golden("small_scene.npz")
+    s = tb.sim.build_sim(SMALL)
+    tb.mpm.step(s, SMALL_V, SMALL_STEPS)
+    st = s.state()
+    disp = np.abs(g["x"] - g["x0"]).max()
+    err = np.abs(st["x"] - g["x"]).max()
+    assert err <= 1e-9 * disp, (err, disp)  # displacement-relative 1e-9
+    assert np.abs(st["x"] - g["x"]).max() / np.abs(g["x"]).max() <= 1e-4  # north_star bar
+    np.testing.assert_allclose(st["v"], g["v"], rtol=0, atol=1e-8 * np.abs(g["v"]).max())
+    np.testing.assert_allclose(st["C"], g["C"], rtol=0, atol=1e-8 * np.abs(g["C"]).max())
+    np.testing.assert_allclose(st["F"], g["F"], rtol=0, atol=1e-11)
+    d = s.diag
+    assert d.step_count == int(g["step_count"])
+    assert d.min_det_f == pytest.approx(float(g["min_det_f"]), abs=1e-12)
+    assert d.max_speed == pytest.approx(float(g["max_speed"]), rel=1e-12)
+    lo, hi = s.grid_window()
+    np.testing.assert_array_equal(lo, g["win_lo"])
+    np.testing.assert_array_equal(hi, g["win_hi"])
+    depth, img = tb.sim.capture(s, SMALL)
+    assert np.abs(depth - g["depth"]).max() <= 1e-7
+    assert np.abs(depth - g["depth"]).max() <= 1e-9 * np.abs(g["depth"]).max()
+    assert np.abs(img.astype(int) - g["image"]).max() <= 2
+
+
+def test_capture_bit_exact_for_identical_positions(tb, golden, oracle):
+    g = golden("small_scene.npz")
+    s = tb.sim.build_sim(SMALL)
+    tb.mpm.step(s, SMALL_V, 60)
+    x = s.positions()
+    depth, img = tb.sim.capture(s, SMALL)
+    od, oi = oracle.capture(_surface_of(g), x, out_w=160, out_h=120)
+    np.testing.assert_array_equal(depth, od)
+    np.testing.assert_array_equal(img, oi)
+    full = tb.render.extract_surface_depth(s, 2.8125e-5)
+    np.testing.assert_array_equal(full, oracle.extract_depth(_surface_of(g), x, 2.8125e-5))
+    part = tb.render.extract_surface_depth(s, 3e-5, 50, 40)
+    np.testing.assert_array_equal(part, oracle.extract_depth(_surface_of(g), x, 3e-5, 50, 40))
+
+
+def test_phases_match_oracle(tb, golden, oracle):
+    """Each engine.hpp phase through tg_phase vs the restated phase."""
+    g = golden("small_scene.npz")
+    s = tb.sim.build_sim(SMALL)
+    tb.mpm.step(s, SMALL_V, 30)
+    st = s.state()
+    o = _small_oracle(oracle, g)
+    o.x, o.v, o.C, o.F = st["x"].copy(), st["v"].copy(), st["C"].copy(), st["F"].copy()
+    tb.mpm.zero_grid(s)
+    lo, hi = o.window()
+    glo, ghi = s.grid_window()
+    np.testing.assert_array_equal(glo, lo)
+    np.testing.assert_array_equal(ghi, hi)
+    tb.mpm.particle_to_grid(s)
+    om, op, mdf = o.p2g(lo, hi)
+    m, mom, _ = s.grid(lo, hi)
+    np.testing.assert_allclose(m, om, rtol=1e-12, atol=1e-14 * om.max())
+    np.testing.assert_allclose(mom, op, rtol=0, atol=1e-10 * np.abs(op).max())
+    assert s.diag.min_det_f == pytest.approx(mdf, abs=1e-14)
+    tb.mpm.grid_update(s)
+    _, _, vel = s.grid(lo, hi)
+    ov = o.grid_update(lo, hi, m, mom)
+    np.testing.assert_array_equal(vel, ov)  # same inputs -> IEEE division, bit-exact
+    tb.mpm.grid_to_particle(s)
+    o.g2p(lo, hi, vel)
+    st = s.state()
+    np.testing.assert_allclose(st["v"], o.v, rtol=0, atol=1e-12 * np.abs(o.v).max())
+    np.testing.assert_allclose(st["C"], o.C, rtol=0, atol=1e-11 * np.abs(o.C).max())
+    np.testing.assert_allclose(st["F"], o.F, rtol=0, atol=1e-14)
+    tb.mpm.apply_boundary(s, SMALL_V)
+    o.apply_boundary(SMALL_V)
+    tb.mpm.advect(s)
+    o.v = s.state()["v"]  # advect from identical velocities
+    x_before = st["x"].copy()
+    o.x = x_before.copy()
+    o.advect()
+    np.testing.assert_array_equal(s.positions(), o.x)
+    assert s.diag.max_speed == pytest.approx(o.diag.max_speed, rel=1e-15)
+
+
+def test_step_graph_and_plain_launches_agree(tb):
+    a = tb.sim.build_sim(SMALL)
+    b = tb.sim.build_sim(SMALL)
+    b.set_graphs(False)
+    for _ in range(3):
+        tb.mpm.step(a, SMALL_V, 10)
+        tb.mpm.step(b, SMALL_V, 10)
+    xa, xb = a.positions(), b.positions()
+    assert np.abs(xa - xb).max() <= 1e-15
+    assert a.step_count == b.step_count == 30
+    assert a.kernel_launches > 0
+
+
+def test_step_many_matches_individual_steps(tb):
+    sims = [tb.sim.build_sim(SMALL, "", 1e-4 * i, 0.0) for i in range(3)]
+    ref = [tb.sim.build_sim(SMALL, "", 1e-4 * i, 0.0) for i in range(3)]
+    vel = np.array([[0, 0, -0.05], [0, 0, -0.03], [0.01, 0, -0.05]])
+    tb.mpm.step_many(sims, vel, 20)
+    for r, v in zip(ref, vel):
+        tb.mpm.step(r, v, 20)
+    for s, r in zip(sims, ref):
+        assert np.abs(s.positions() - r.positions()).max() <= 1e-15
+
+
+def test_degenerate_f_leaves_state_at_failing_substep(tb):
+    s = tb.sim.build_sim(SMALL)
+    tb.mpm.step(s, SMALL_V, 5)
+    st = s.state()
+    F = st["F"].copy()
+    F[7] = np.diag([1.0, 1.0, -1.0])  # det < 0
+    s.set_state(F=F.reshape(-1, 9))
+    x_before = s.positions()
+    with pytest.raises(tb.DegenerateF):
+        tb.mpm.step(s, SMALL_V, 3)
+    np.testing.assert_array_equal(s.positions(), x_before)
+    assert s.step_count == 5
+    with pytest.raises(tb.DegenerateF):  # still degenerate on retry
+        tb.mpm.step(s, SMALL_V, 1)
+
+
+def test_out_of_grid_after_advect(tb):
+    s = tb.sim.build_sim(SMALL)
+    x = s.positions()
+    # push one indenter particle right to the top of the stencil-safe margin
+    dx = 12e-3 / 64
+    x[-1, 2] = (64 - 3) * dx + 0.49 * dx  # base = 61 -> base + 2 = 63 < 64 still in range
+    s.set_state(x=x)
+    with pytest.raises(tb.OutOfGrid):
+        tb.mpm.step(s, (0, 0, 1.0), 200)  # moves up by 2e-6 * 1.0 per substep
+    assert 1 <= s.step_count < 200
+
+
+def test_render_functions_match_reference(tb, golden):
+    k = golden("kat.npz")
+    r, hemi, ramp, src = render_inputs()
+    assert sha(tb.render.surface_normals(hemi, r)) == str(k["normals_hemi_sha"])
+    rp = tb.render_params({}, "")
+    np.testing.assert_array_equal(tb.render.phong_render(hemi, r, rp), k["img_hemi"])
+    np.testing.assert_array_equal(tb.render.phong_render(ramp, r, rp), k["img_ramp"])
+    img_l = tb.render.phong_render(hemi, r, tb.render_params(LIGHT_CFG, ""))
+    assert np.abs(img_l.astype(int) - k["img_hemi_l"]).max() <= 1
+    assert sha(tb.render.crop_align(src, (0.0, 0.0, 1.0))) == str(k["crop_c_sha"])
+    assert sha(tb.render.crop_align(src, (12.25, -7.5, 1.07))) == str(k["crop_o_sha"])
+    with pytest.raises(tb.CropOutOfBounds):
+        tb.render.crop_align(np.zeros((100, 100)), (0, 0, 1.0))
+
+
+def test_config1_ten_frames_match_reference(tb, golden):
+    """Config 1 at full size (314,221 particles, 256^3): 100 substeps vs the
+    reference; positions, F, height map and image."""
+    g = golden("config1.npz")
+    s = tb.sim.build_sim(CONFIG1)
+    assert s.n == int(g["n"]) and s.elastomer_count == int(g["n_elastomer"])
+    x0 = s.positions()
+    assert sha(x0) == str(g["x0_hash"])
+    for _ in range(CONFIG1_STEPS // 10):
+        tb.mpm.step(s, CONFIG1_V, 10)
+    st = s.state()
+    sub = g["subset"]
+    disp = np.abs(g["x_subset"] - x0[sub]).max()
+    assert np.abs(st["x"][sub] - g["x_subset"]).max() <= 1e-8 * max(disp, 1e-9)
+    np.testing.assert_allclose(st["F"][sub], g["F_subset"], rtol=0, atol=1e-11)
+    d = s.diag
+    assert d.step_count == int(g["step_count"])
+    assert d.min_det_f == pytest.approx(float(g["min_det_f"]), abs=1e-12)
+    depth, img = tb.sim.capture(s, CONFIG1)
+    assert np.abs(depth[::16, ::16] - g["depth_sample"]).max() <= 1e-7
+    assert np.abs(img.astype(int) - g["image"]).max() <= 2
+
+
+def test_config2a_conserves_mass_and_momentum(tb):
+    """Config 2a (1,214,221 particles): size-independent P2G invariants
+    (SPEC.md:147-148): sum of node mass = sum of particle mass; with zero
+    stress (F = I) and C = 0, sum of node momentum = sum of m v."""
+    from tests.scenes import CONFIG2A
+
+    s = tb.sim.build_sim(CONFIG2A)
+    assert s.n == 1214221
+    n, ne = s.n, s.elastomer_count
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal((n, 3)) * 1e-3
+    s.set_state(v=v, Cm=np.zeros((n, 9)), F=np.tile(np.eye(3).ravel(), (n, 1)))
+    tb.mpm.zero_grid(s)
+    tb.mpm.particle_to_grid(s)
+    lo, hi = s.grid_window()
+    m, mom, _ = s.grid(lo, hi)
+    # particle masses (init_scene, scene.cpp:48-66)
+    gel_m = 1000.0 * (0.02 * 0.02 * 0.004) / ne
+    x = s.positions()
+    ind = x[ne:]
+    ext = ind.max(0) - ind.min(0)
+    ind_m = 1000.0 * (ext[0] * ext[1] * ext[2] / (n - ne)) * 80.0
+    total_m = gel_m * ne + ind_m * (n - ne)
+    assert m.sum() == pytest.approx(total_m, rel=1e-10)
+    pm = np.concatenate([gel_m * v[:ne], ind_m * v[ne:]]).sum(0)
+    np.testing.assert_allclose(mom.reshape(-1, 3).sum(0), pm, rtol=1e-9, atol=1e-12 * np.abs(pm).max())
+
+
+def test_rest_state_is_a_fixed_point(tb):
+    """zero indenter velocity, untouched gel -> no drift."""
+    cfg = dict(SMALL)
+    cfg = {**SMALL, "indenter": {**SMALL["indenter"], "gap_mm": 0.5}}
+    s = tb.sim.build_sim(cfg)
+    x0 = s.positions()
+    tb.mpm.step(s, (0, 0, 0), 100)
+    assert np.abs(s.positions() - x0).max() <= 1e-9
+    assert s.diag.max_speed < 1e-9
