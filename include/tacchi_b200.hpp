@@ -1,0 +1,175 @@
+// tacchi_b200.hpp — header-only C++ mirror of the reference simulator API
+// (/root/reference/proj/include/tacchi) over the C-ABI in tacchi_cuda.h.
+//
+// A caller of the reference swaps
+//     #include "tacchi/mpm/engine.hpp"        -> #include "tacchi_b200.hpp"
+//     tacchi::mpm::step(state, v, 10)         -> tacchi_b200::mpm::step(state, v, 10)
+//     tacchi::sim::capture(state, cfg, obj)   -> tacchi_b200::sim::capture(state, cfg_json, obj)
+// and keeps its control flow: the same functions, argument meaning and
+// exception classes (errors.hpp:9-39). SimState owns a device handle; its
+// particle arrays live in HBM and are copied to host only on request.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tacchi_cuda.h"
+
+namespace tacchi_b200 {
+
+// ---- errors (errors.hpp:9-39) ----------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class GridTooSmall : public Error { public: using Error::Error; };
+class EmptyScene : public Error { public: using Error::Error; };
+class OutOfGrid : public Error { public: using Error::Error; };
+class DegenerateF : public Error { public: using Error::Error; };
+class ParseError : public Error { public: using Error::Error; };
+class EmptyCloud : public Error { public: using Error::Error; };
+class NoSurface : public Error { public: using Error::Error; };
+class CropOutOfBounds : public Error { public: using Error::Error; };
+class ShapeMismatch : public Error { public: using Error::Error; };
+class ConfigError : public Error { public: using Error::Error; };
+class IoError : public Error { public: using Error::Error; };
+class CudaError : public Error { public: using Error::Error; };
+
+inline void check(int rc) {
+  if (rc == TG_OK) return;
+  const std::string m = tg_last_error();
+  switch (rc) {
+    case TG_ERR_GRID_TOO_SMALL: throw GridTooSmall(m);
+    case TG_ERR_EMPTY_SCENE: throw EmptyScene(m);
+    case TG_ERR_OUT_OF_GRID: throw OutOfGrid(m);
+    case TG_ERR_DEGENERATE_F: throw DegenerateF(m);
+    case TG_ERR_CONFIG: throw ConfigError(m);
+    case TG_ERR_NO_SURFACE: throw NoSurface(m);
+    case TG_ERR_CROP_OUT_OF_BOUNDS: throw CropOutOfBounds(m);
+    case TG_ERR_SHAPE_MISMATCH: throw ShapeMismatch(m);
+    case TG_ERR_EMPTY_CLOUD: throw EmptyCloud(m);
+    case TG_ERR_PARSE: throw ParseError(m);
+    case TG_ERR_IO: throw IoError(m);
+    case TG_ERR_CUDA: throw CudaError(m);
+    default: throw Error(m);
+  }
+}
+
+using Vec3 = std::array<double, 3>;
+
+// ---- render types (depth_map.hpp:11-22, image.hpp:10-23) ----------------
+namespace render {
+struct DepthMap {
+  int width = 0, height = 0;
+  double pixel_to_meter = 0.0;
+  std::vector<double> values;  // row-major, row = image y
+  double at(int row, int col) const { return values[static_cast<size_t>(row) * width + col]; }
+};
+struct Image8 {
+  int width = 0, height = 0;
+  std::vector<uint8_t> data;  // interleaved RGB
+  uint8_t at(int row, int col, int ch) const {
+    return data[(static_cast<size_t>(row) * width + col) * 3 + ch];
+  }
+};
+}  // namespace render
+
+namespace mpm {
+
+struct StepDiagnostics {
+  double min_det_f = 1.0;
+  double max_speed = 0.0;
+};
+
+// mpm::SimState (sim_state.hpp:59-79), device resident.
+class SimState {
+ public:
+  explicit SimState(tg_handle h) : h_(h, &tg_destroy) {}
+  tg_handle handle() const { return h_.get(); }
+  int64_t size() const { return tg_num_particles(h_.get()); }
+  int64_t elastomer_count() const { return tg_num_elastomer(h_.get()); }
+  StepDiagnostics diag() const {
+    StepDiagnostics d;
+    int64_t sc;
+    check(tg_diag(h_.get(), &d.min_det_f, &d.max_speed, &sc, nullptr));
+    return d;
+  }
+  int64_t step_count() const {
+    int64_t sc;
+    check(tg_diag(h_.get(), nullptr, nullptr, &sc, nullptr));
+    return sc;
+  }
+  // Host snapshots in the reference's particle order (row layout).
+  void download(std::vector<double>* x, std::vector<double>* v, std::vector<double>* C,
+                std::vector<double>* F) const {
+    const size_t n = static_cast<size_t>(size());
+    if (x) x->resize(3 * n);
+    if (v) v->resize(3 * n);
+    if (C) C->resize(9 * n);
+    if (F) F->resize(9 * n);
+    check(tg_download(h_.get(), x ? x->data() : nullptr, v ? v->data() : nullptr,
+                      C ? C->data() : nullptr, F ? F->data() : nullptr));
+  }
+  void upload(const double* x, const double* v, const double* C, const double* F) {
+    check(tg_upload(h_.get(), x, v, C, F));
+  }
+
+ private:
+  std::unique_ptr<tg_sim, void (*)(tg_handle)> h_;
+};
+
+// engine.hpp:10-35
+inline void zero_grid(SimState& s) { check(tg_phase(s.handle(), TG_PHASE_ZERO_GRID, nullptr)); }
+inline void particle_to_grid(SimState& s) {
+  check(tg_phase(s.handle(), TG_PHASE_PARTICLE_TO_GRID, nullptr));
+}
+inline void grid_update(SimState& s) { check(tg_phase(s.handle(), TG_PHASE_GRID_UPDATE, nullptr)); }
+inline void grid_to_particle(SimState& s) {
+  check(tg_phase(s.handle(), TG_PHASE_GRID_TO_PARTICLE, nullptr));
+}
+inline void apply_boundary(SimState& s, const Vec3& v) {
+  check(tg_phase(s.handle(), TG_PHASE_APPLY_BOUNDARY, v.data()));
+}
+inline void advect(SimState& s) { check(tg_phase(s.handle(), TG_PHASE_ADVECT, nullptr)); }
+inline void step(SimState& s, const Vec3& indenter_velocity, int n_substeps = 1) {
+  check(tg_step(s.handle(), indenter_velocity.data(), n_substeps));
+}
+
+}  // namespace mpm
+
+namespace sim {
+
+// sim::build_sim(cfg, place_for_press(cfg, indenter_cloud_for(cfg, object), ox, oy))
+inline mpm::SimState build_sim(const std::string& config_json, const std::string& object = "",
+                               double offset_x = 0.0, double offset_y = 0.0, int device = 0) {
+  tg_handle h = nullptr;
+  check(tg_build_sim(device, config_json.c_str(), object.c_str(), offset_x, offset_y, &h));
+  return mpm::SimState(h);
+}
+
+struct Capture {
+  render::DepthMap depth;
+  render::Image8 image;
+};
+
+// sim::capture (scene_builder.cpp:80-89)
+inline Capture capture(const mpm::SimState& s, const std::string& config_json,
+                       const std::string& object) {
+  tg_render r;
+  check(tg_render_from_config(config_json.c_str(), object.c_str(), &r));
+  Capture c;
+  c.depth.width = c.image.width = r.width;
+  c.depth.height = c.image.height = r.height;
+  c.depth.pixel_to_meter = r.pixel_to_meter * r.crop_scale;
+  c.depth.values.resize(static_cast<size_t>(r.width) * r.height);
+  c.image.data.resize(static_cast<size_t>(r.width) * r.height * 3);
+  check(tg_capture(s.handle(), &r, c.depth.values.data(), c.image.data.data()));
+  return c;
+}
+
+}  // namespace sim
+}  // namespace tacchi_b200

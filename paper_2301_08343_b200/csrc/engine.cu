@@ -182,21 +182,27 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   // neighbouring lanes hit neighbouring nodes; perm maps back.
   s->perm.resize(n);
   std::iota(s->perm.begin(), s->perm.end(), 0);
+  // Order: base cell (bx, by) of the initial position, then z. Under the press
+  // (motion along z) the order stays sorted by (bx, by, bz) for the whole
+  // episode, which keeps runs of equal base cell contiguous for the chunked
+  // indenter scatter (k_p2g_ind_chunk).
   if (n_ind > 1) {
     std::vector<long long> key(n_ind);
     for (int64_t q = 0; q < n_ind; ++q) {
       const double* xp = in->x + 3 * (n_el + q);
       long long k = 0;
-      for (int a = 0; a < 3; ++a) {
+      for (int a = 0; a < 2; ++a) {
         const int b = std::min(std::max(host_base(xp[a], g.origin[a], g.inv_dx), -1), g.res[a]);
         k = k * (g.res[a] + 2) + (b + 1);
       }
       key[q] = k;
     }
-    std::stable_sort(s->perm.begin() + n_el, s->perm.end(),
-                     [&](int64_t a, int64_t b) { return key[a - n_el] < key[b - n_el]; });
+    std::stable_sort(s->perm.begin() + n_el, s->perm.end(), [&](int64_t a, int64_t b) {
+      const long long ka = key[a - n_el], kb = key[b - n_el];
+      if (ka != kb) return ka < kb;
+      return in->x[3 * a + 2] < in->x[3 * b + 2];
+    });
   }
-
   cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
   s->n_nodes = static_cast<size_t>(g.res[0]) * g.res[1] * g.res[2];
   bool ok = cudaMalloc(&s->x, 3 * n * sizeof(double)) == cudaSuccess &&
@@ -217,6 +223,12 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   cudaMemsetAsync(s->grid_v, 0, s->n_nodes * sizeof(double4), s->stream);
   std::memset(s->h_ctl, 0, sizeof(Ctl));
   for (int a = 0; a < 3; ++a) s->h_ctl->vind[a] = in->indenter_velocity[a];
+  // Is the indenter velocity uniform (it is for init_scene's output)?
+  s->ind_v_uniform = true;
+  for (int64_t p = n_el + 1; p < n && s->ind_v_uniform; ++p)
+    for (int a = 0; a < 3; ++a)
+      if (in->v[3 * p + a] != in->v[3 * n_el + a]) s->ind_v_uniform = false;
+  for (int a = 0; a < 3; ++a) s->h_ctl->ind_v[a] = n_ind > 0 ? in->v[3 * n_el + a] : 0.0;
   s->h_ctl->diag_min_det_f = 1.0;
   cudaMemcpyAsync(s->ctl, s->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s->stream);
   launch_reset(*s);
@@ -462,6 +474,15 @@ int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, con
   int rc = 0;
   if (x && (rc = put3(x, s.x))) return rc;
   if (v && (rc = put3(v, s.v))) return rc;
+  if (v && s.n_ind > 0 && !init) {
+    bool uniform = true;
+    for (int64_t p = s.n_el + 1; p < s.n && uniform; ++p)
+      for (int a = 0; a < 3; ++a)
+        if (v[3 * p + a] != v[3 * s.n_el + a]) uniform = false;
+    s.ind_v_uniform = uniform;
+    if (uniform) CUDA_TRY(cudaMemcpy(&s.ctl->ind_v[0], v + 3 * s.n_el, 3 * sizeof(double),
+                                     cudaMemcpyHostToDevice));
+  }
   if ((Cm || init) && (rc = put9(Cm, s.C, false))) return rc;
   if ((Fm || init) && (rc = put9(Fm, s.F, true))) return rc;
   s.window_valid = false;
@@ -496,6 +517,12 @@ int download(DeviceSim& s, double* x, double* v, double* Cm, double* Fm) {
   int rc = 0;
   if (x && (rc = get3(s.x, x))) return rc;
   if (v && (rc = get3(s.v, v))) return rc;
+  if (v && s.ind_v_uniform && s.n_ind > 0) {
+    double u[3];
+    CUDA_TRY(cudaMemcpy(u, &s.ctl->ind_v[0], sizeof u, cudaMemcpyDeviceToHost));
+    for (int64_t q = s.n_el; q < s.n; ++q)
+      for (int a = 0; a < 3; ++a) v[3 * s.perm[q] + a] = u[a];
+  }
   if (Cm && (rc = get9(s.C, Cm, false))) return rc;
   if (Fm && (rc = get9(s.F, Fm, true))) return rc;
   return TG_OK;

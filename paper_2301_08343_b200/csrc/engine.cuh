@@ -27,6 +27,7 @@ struct Ctl {
   int prev_lo[3], prev_hi[3];             // Grid::prev_lo/hi
   int clr_lo[3], clr_hi[3];               // node box to clear before P2G
   double vind[3];                         // commanded indenter velocity
+  double ind_v[3];                        // uniform indenter velocity (P2G input)
   double diag_min_det_f, diag_max_speed;  // StepDiagnostics
   long long step_count;                   // SimState::step_count
 };
@@ -80,6 +81,7 @@ struct DeviceSim {
   Ctl* h_ctl = nullptr;    // pinned host mirror
   double* h_vind = nullptr;  // pinned staging for the command
 
+  bool ind_v_uniform = true;   // indenter v == Ctl::ind_v for every indenter particle
   bool window_valid = false;   // ctl->win/clr describe the current positions
   int host_substep = 0;        // absolute substep counter (host view)
   bool use_graphs = true;

@@ -39,22 +39,51 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 // advect's reductions: max |v|^2 and the bbox of x (engine.cpp:273-282).
+// Warp shuffles, then one shared-memory pass per block, then 7 atomics per
+// block (a per-warp atomic on 7 hot words serialises badly at 1e6 particles).
+// Every thread of the block must call this (no early exits before it).
 __device__ __forceinline__ void reduce_motion(Ctl* ctl, bool active, double v2, double x0,
                                               double x1, double x2) {
-  double m = active ? v2 : 0.0;
-  double l0 = active ? x0 : INFINITY, l1 = active ? x1 : INFINITY, l2 = active ? x2 : INFINITY;
-  double h0 = active ? x0 : -INFINITY, h1 = active ? x1 : -INFINITY, h2 = active ? x2 : -INFINITY;
-  m = warp_max(m);
-  l0 = warp_min(l0); l1 = warp_min(l1); l2 = warp_min(l2);
-  h0 = warp_max(h0); h1 = warp_max(h1); h2 = warp_max(h2);
-  if ((threadIdx.x & 31) == 0 && l0 <= h0) {
-    atomicMax(&ctl->max_v2, static_cast<unsigned long long>(__double_as_longlong(m)));
-    atomicMin(&ctl->bb_lo[0], order_key(l0));
-    atomicMin(&ctl->bb_lo[1], order_key(l1));
-    atomicMin(&ctl->bb_lo[2], order_key(l2));
-    atomicMax(&ctl->bb_hi[0], order_key(h0));
-    atomicMax(&ctl->bb_hi[1], order_key(h1));
-    atomicMax(&ctl->bb_hi[2], order_key(h2));
+  __shared__ double red[7][32];
+  double r[7];
+  r[0] = active ? v2 : 0.0;
+  r[1] = active ? x0 : INFINITY;
+  r[2] = active ? x1 : INFINITY;
+  r[3] = active ? x2 : INFINITY;
+  r[4] = active ? x0 : -INFINITY;
+  r[5] = active ? x1 : -INFINITY;
+  r[6] = active ? x2 : -INFINITY;
+  r[0] = warp_max(r[0]);
+#pragma unroll
+  for (int a = 1; a < 4; ++a) r[a] = warp_min(r[a]);
+#pragma unroll
+  for (int a = 4; a < 7; ++a) r[a] = warp_max(r[a]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int a = 0; a < 7; ++a) red[a][warp] = r[a];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int a = 0; a < 7; ++a) {
+      const double ident = a == 0 ? 0.0 : (a < 4 ? INFINITY : -INFINITY);
+      r[a] = lane < nwarps ? red[a][lane] : ident;
+    }
+    r[0] = warp_max(r[0]);
+#pragma unroll
+    for (int a = 1; a < 4; ++a) r[a] = warp_min(r[a]);
+#pragma unroll
+    for (int a = 4; a < 7; ++a) r[a] = warp_max(r[a]);
+    if (lane == 0 && r[1] <= r[4]) {
+      atomicMax(&ctl->max_v2, static_cast<unsigned long long>(__double_as_longlong(r[0])));
+      atomicMin(&ctl->bb_lo[0], order_key(r[1]));
+      atomicMin(&ctl->bb_lo[1], order_key(r[2]));
+      atomicMin(&ctl->bb_lo[2], order_key(r[3]));
+      atomicMax(&ctl->bb_hi[0], order_key(r[4]));
+      atomicMax(&ctl->bb_hi[1], order_key(r[5]));
+      atomicMax(&ctl->bb_hi[2], order_key(r[6]));
+    }
   }
 }
 
@@ -83,7 +112,7 @@ __global__ void k_reset(Ctl* ctl) {
   ctl->min_detf = order_key(1.0);
 }
 
-enum : int { kFinAdvect = 1, kFinWindow = 2 };
+enum : int { kFinAdvect = 1, kFinWindow = 2, kFinDiag = 4 };
 
 // grid.cpp:29-36: in_range divides by dx.
 __device__ bool in_range(const Geometry& g, const double* x) {
@@ -101,6 +130,10 @@ __global__ void k_finalize(Ctl* ctl, Geometry g, int mode) {
   for (int a = 0; a < 3; ++a) {
     lo[a] = order_val(ctl->bb_lo[a]);
     hi[a] = order_val(ctl->bb_hi[a]);
+  }
+  if (mode & kFinDiag) {  // particle_to_grid's min_det_f (engine.cpp:177)
+    ctl->diag_min_det_f = order_val(ctl->min_detf);
+    ctl->min_detf = order_key(1.0);
   }
   if (mode & kFinAdvect) {
     // engine.cpp:279-285
@@ -269,6 +302,69 @@ __global__ void __launch_bounds__(256) k_p2g_ind(const double* __restrict__ x,
   }
 }
 
+// particle_to_grid for the rigid indenter when every indenter particle carries
+// the same velocity (always true after the first apply_boundary,
+// engine.cpp:260-261). Each node then receives (sum_p w_p m) (1, v): the
+// scatter reduces to one weight sum per node. Particles are ordered by base
+// cell (bx, by) then z at creation, so a thread walking kChunk consecutive
+// particles sees long runs of one base cell; it accumulates the 27 weight
+// sums in registers and issues the 27 x 4 REDs only when the base changes.
+// This cuts the RED.F64 count by ~the particles-per-cell density (~19 for the
+// 1e6-point sphere).
+template <int kChunk>
+__global__ void __launch_bounds__(256) k_p2g_ind_chunk(const double* __restrict__ x, int64_t n,
+                                                       int64_t n_el, Ctl* ctl, Geometry g,
+                                                       double4* __restrict__ grid, double m) {
+  if (ctl->err_code) return;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t p0 = n_el + t * kChunk;
+  if (p0 >= n) return;
+  const int64_t p1 = p0 + kChunk < n ? p0 + kChunk : n;
+  const double mv0 = m * ctl->ind_v[0], mv1 = m * ctl->ind_v[1], mv2 = m * ctl->ind_v[2];
+  double acc[27];
+#pragma unroll
+  for (int i = 0; i < 27; ++i) acc[i] = 0.0;
+  int cb0 = 0, cb1 = 0, cb2 = 0;
+  bool have = false;
+  auto flush = [&]() {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        double* row = reinterpret_cast<double*>(grid + node_index(g, cb0 + a, cb1 + b, cb2));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double w = acc[9 * a + 3 * b + c];
+          if (w != 0.0) {
+            red_add(row + 4 * c + 0, w * m);
+            red_add(row + 4 * c + 1, w * mv0);
+            red_add(row + 4 * c + 2, w * mv1);
+            red_add(row + 4 * c + 3, w * mv2);
+          }
+          acc[9 * a + 3 * b + c] = 0.0;
+        }
+      }
+  };
+  for (int64_t p = p0; p < p1; ++p) {
+    Stencil st;
+    make_stencil(x[p], x[n + p], x[2 * n + p], g.origin, g.inv_dx, st);
+    if (have && (st.base[0] != cb0 || st.base[1] != cb1 || st.base[2] != cb2)) flush();
+    cb0 = st.base[0];
+    cb1 = st.base[1];
+    cb2 = st.base[2];
+    have = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const double wab = st.w[0][a] * st.w[1][b];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[9 * a + 3 * b + c] += wab * st.w[2][c];
+      }
+  }
+  flush();
+}
+
 // grid_update over the active window (engine.cpp:180-205).
 __global__ void k_grid_update(const double4* __restrict__ mp, double4* __restrict__ vel, Ctl* ctl,
                               Geometry g) {
@@ -382,39 +478,44 @@ __global__ void __launch_bounds__(256) k_g2p_gel(double* __restrict__ x, double*
 }
 
 // apply_boundary + advect for the indenter (engine.cpp:260-261, 275-279).
-template <bool kBoundary, bool kAdvect>
-__global__ void k_ind_move(double* __restrict__ x, double* __restrict__ v, int64_t n, int64_t n_el,
-                           Ctl* ctl, Geometry g) {
+// kUniform: all indenter velocities equal Ctl::ind_v (the per-particle v array
+// is not read or written; tg_download fills it in). apply_boundary makes the
+// velocity uniform, so after it the indenter is always in this mode.
+template <bool kBoundary, bool kAdvect, bool kUniform>
+__global__ void __launch_bounds__(256) k_ind_move(double* __restrict__ x, double* __restrict__ v,
+                                                  int64_t n, int64_t n_el, Ctl* ctl, Geometry g) {
   if (ctl->err_code) return;
   const int64_t p = n_el + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool active = p < n;
+  double v0, v1, vz;
+  if (kBoundary) {
+    v0 = ctl->vind[0];
+    v1 = ctl->vind[1];
+    vz = ctl->vind[2];
+  } else if (kUniform) {
+    v0 = ctl->ind_v[0];
+    v1 = ctl->ind_v[1];
+    vz = ctl->ind_v[2];
+  } else {
+    v0 = active ? v[p] : 0.0;
+    v1 = active ? v[n + p] : 0.0;
+    vz = active ? v[2 * n + p] : 0.0;
+  }
+  if (kBoundary && blockIdx.x == 0 && threadIdx.x == 0) {
+    // every thread read vind above; Ctl::ind_v is only read by later kernels
+    ctl->ind_v[0] = v0;
+    ctl->ind_v[1] = v1;
+    ctl->ind_v[2] = vz;
+  }
   double px0 = 0, px1 = 0, px2 = 0, v2 = 0;
-  if (active) {
-    double v0, v1, vz;
-    if (kBoundary) {
-      v0 = ctl->vind[0];
-      v1 = ctl->vind[1];
-      vz = ctl->vind[2];
-      v[p] = v0;
-      v[n + p] = v1;
-      v[2 * n + p] = vz;
-    } else {
-      v0 = v[p];
-      v1 = v[n + p];
-      vz = v[2 * n + p];
-    }
-    px0 = x[p];
-    px1 = x[n + p];
-    px2 = x[2 * n + p];
-    if (kAdvect) {
-      px0 = px0 + g.dt * v0;
-      px1 = px1 + g.dt * v1;
-      px2 = px2 + g.dt * vz;
-      x[p] = px0;
-      x[n + p] = px1;
-      x[2 * n + p] = px2;
-      v2 = v0 * v0 + v1 * v1 + vz * vz;
-    }
+  if (active && kAdvect) {
+    px0 = x[p] + g.dt * v0;
+    px1 = x[n + p] + g.dt * v1;
+    px2 = x[2 * n + p] + g.dt * vz;
+    x[p] = px0;
+    x[n + p] = px1;
+    x[2 * n + p] = px2;
+    v2 = v0 * v0 + v1 * v1 + vz * vz;
   }
   if (kAdvect) reduce_motion(ctl, active, v2, px0, px1, px2);
 }
@@ -514,10 +615,16 @@ int launch_p2g_gel(DeviceSim& s) {
   return 1;
 }
 
+constexpr int kIndChunk = 16;
+
 int launch_p2g_ind(DeviceSim& s) {
   if (s.n_ind <= 0) return 0;
-  k_p2g_ind<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el, s.ctl, s.geo,
-                                                            s.grid_mp, s.m_ind);
+  if (s.ind_v_uniform)
+    k_p2g_ind_chunk<kIndChunk><<<blocks_for((s.n_ind + kIndChunk - 1) / kIndChunk), kThreads, 0,
+                                 s.stream>>>(s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mp, s.m_ind);
+  else
+    k_p2g_ind<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el, s.ctl, s.geo,
+                                                              s.grid_mp, s.m_ind);
   s.kernel_launches += 1;
   return 1;
 }
@@ -548,14 +655,15 @@ int launch_g2p_gel_move(DeviceSim& s) {
 
 int launch_ind_move(DeviceSim& s) {
   if (s.n_ind <= 0) return 0;
-  k_ind_move<true, true><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el,
-                                                                        s.ctl, s.geo);
+  k_ind_move<true, true, true><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(
+      s.x, s.v, s.n, s.n_el, s.ctl, s.geo);
+  s.ind_v_uniform = true;
   s.kernel_launches += 1;
   return 1;
 }
 
 int launch_finalize_step(DeviceSim& s) {
-  k_finalize<<<1, 1, 0, s.stream>>>(s.ctl, s.geo, kFinAdvect | kFinWindow);
+  k_finalize<<<1, 1, 0, s.stream>>>(s.ctl, s.geo, kFinDiag | kFinAdvect | kFinWindow);
   s.kernel_launches += 1;
   return 1;
 }
@@ -577,8 +685,9 @@ int launch_phase_boundary(DeviceSim& s) {
   if (s.n_el > 0)
     k_gel_boundary<<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(s.v, s.tag, s.n, s.n_el, s.ctl);
   if (s.n_ind > 0)
-    k_ind_move<true, false><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el,
-                                                                           s.ctl, s.geo);
+    k_ind_move<true, false, true><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(
+        s.x, s.v, s.n, s.n_el, s.ctl, s.geo);
+  if (s.n_ind > 0) s.ind_v_uniform = true;
   s.kernel_launches += 2;
   return 2;
 }
@@ -588,8 +697,14 @@ int launch_phase_advect(DeviceSim& s) {
     k_gel_advect<<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el, s.ctl,
                                                                 s.geo);
   if (s.n_ind > 0)
-    k_ind_move<false, true><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el,
-                                                                           s.ctl, s.geo);
+  {
+    if (s.ind_v_uniform)
+      k_ind_move<false, true, true><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(
+          s.x, s.v, s.n, s.n_el, s.ctl, s.geo);
+    else
+      k_ind_move<false, true, false><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(
+          s.x, s.v, s.n, s.n_el, s.ctl, s.geo);
+  }
   k_finalize<<<1, 1, 0, s.stream>>>(s.ctl, s.geo, kFinAdvect);
   s.kernel_launches += 3;
   return 3;
