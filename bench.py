@@ -108,12 +108,11 @@ def _algorithmic_bytes(n_el: int, n_ind: int, window_nodes: int):
     s = 8
     per_substep = n_el * 24 * s + n_ind * 6 * s
     per_kernel = {
-        "p2g_elastomer": n_el * 24 * s,         # x, v, C, F read
-        "p2g_indenter": n_ind * 6 * s,          # x, v read
-        "g2p_elastomer": n_el * (12 + 24) * s,  # x, F read; x, v, C, F written
-        "indenter_move": n_ind * 9 * s,         # x read; x, v written
-        "grid_update": window_nodes * 56,       # m+p read (32 B), v written (24 B)
-        "clear": window_nodes * 32,
+        "p2g_elastomer_first": n_el * 24 * s,   # x, v, C, F read (first substep of a call)
+        "p2g_indenter_first": n_ind * 3 * s,    # x read
+        "grid_update": window_nodes * 64,       # A (32 B) + M_I (8 B) read, V (24 B) written
+        "g2p2g_elastomer": n_el * 36 * s,       # x, F read; x, v, C, F written
+        "indenter_move_p2g": n_ind * 6 * s,     # x read + written
         "finalize": 0,
     }
     return per_substep, per_kernel
@@ -201,10 +200,14 @@ def run_ours(args):
     value = units / (dev_ms * 1e-3)
     e2e_value = units / (e2e_ms * 1e-3)
     peak, peak_src = _peaks()
-    dom = max((k for k in phase_ms if k != "finalize"), key=lambda k: phase_ms[k])
+    dom = max((k for k in phase_ms if k != "finalize" and not k.endswith("_first")),
+              key=lambda k: phase_ms[k])
     dom_ms = phase_ms[dom]
     achieved = per_kernel[dom] / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
-    substep_ms = sum(phase_ms.values())
+    # per-substep kernels (the first-substep scatter is amortised over a frame)
+    substep_ms = (sum(v for k, v in phase_ms.items() if not k.endswith("_first")) +
+                  (phase_ms.get("p2g_elastomer_first", 0) + phase_ms.get("p2g_indenter_first", 0)) /
+                  SUBSTEPS_PER_FRAME)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
@@ -223,7 +226,9 @@ def run_ours(args):
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": per_kernel[dom],
                      "kernel_ms": dom_ms,
-                     "substep": {"ms": substep_ms, "algorithmic_bytes": per_substep,
+                     "substep": {"ms": substep_ms,
+                                 "ms_measured_in_frames": dev_ms / (args.steps * SUBSTEPS_PER_FRAME),
+                                 "algorithmic_bytes": per_substep,
                                  "achieved_gbs": per_substep / (substep_ms * 1e-3) / 1e9,
                                  "frac": per_substep / (substep_ms * 1e-3) / 1e9 / peak},
                      "phase_ms": phase_ms},

@@ -200,11 +200,12 @@ int tg_step_many(tg_handle* hs, int n_handles, const double* velocities /* n x 3
 
 /* Blocks until the handle's stream is idle; reports any latched error. */
 int tg_sync(tg_handle h);
-/* Runs `reps` substeps of mpm::step with CUDA events between the kernels
- * of the launch plan and writes the average device time (ms) of each:
- * [clear, p2g_elastomer, p2g_indenter, grid_update, g2p_elastomer(+boundary
- * +advect), indenter_move, finalize]. The state advances by `reps` substeps
- * exactly as tg_step would. Instrumentation for the roofline in bench.py. */
+/* Runs one mpm::step of `reps` substeps kernel by kernel with CUDA events
+ * between the launches and writes device times (ms): [p2g_elastomer and
+ * p2g_indenter of the first substep, then per-substep averages of
+ * grid_update, g2p2g_elastomer (G2P + boundary + advect + look-ahead P2G),
+ * indenter_move_p2g, finalize]. The state advances exactly as tg_step
+ * would. Instrumentation for the roofline in bench.py. */
 int tg_time_phases(tg_handle h, const double indenter_velocity[3], int reps, double* out_ms);
 /* cudaStream_t of the handle (for event timing by the caller). */
 void* tg_stream(tg_handle h);

@@ -99,8 +99,8 @@ EXPORTED = [
     "tg_generate_cloud", "tg_placed_indenter", "tg_time_phases",
 ]
 
-PHASE_TIMING_NAMES = ["clear", "p2g_elastomer", "p2g_indenter", "grid_update",
-                      "g2p_elastomer", "indenter_move", "finalize"]
+PHASE_TIMING_NAMES = ["p2g_elastomer_first", "p2g_indenter_first", "grid_update",
+                      "g2p2g_elastomer", "indenter_move_p2g", "finalize"]
 
 _lib = None
 

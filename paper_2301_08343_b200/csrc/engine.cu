@@ -16,22 +16,23 @@
 namespace tacchi_b200 {
 
 // mpm_kernels.cu
+int launch_reset(DeviceSim& s, int mask);
 int launch_window(DeviceSim& s);
 int launch_clear(DeviceSim& s, int sms);
 int launch_p2g(DeviceSim& s, bool publish_diag);
-int launch_grid_update(DeviceSim& s, int sms);
-int launch_g2p_move(DeviceSim& s);
+int launch_p2g_gel(DeviceSim& s);
+int launch_p2g_ind(DeviceSim& s);
+int launch_grid_update(DeviceSim& s, int sms, bool zero);
+int launch_g2p2g_gel(DeviceSim& s, bool lookahead);
+int launch_ind_move(DeviceSim& s, bool lookahead);
+int launch_finalize_step(DeviceSim& s);
 int launch_phase_g2p(DeviceSim& s);
 int launch_phase_boundary(DeviceSim& s);
 int launch_phase_advect(DeviceSim& s);
-int launch_reset(DeviceSim& s);
 int launch_gather_box(DeviceSim& s, const int lo[3], const int hi[3], double* mass, double* mom,
                       double* vel);
-int launch_p2g_gel(DeviceSim& s);
-int launch_p2g_ind(DeviceSim& s);
-int launch_g2p_gel_move(DeviceSim& s);
-int launch_ind_move(DeviceSim& s);
-int launch_finalize_step(DeviceSim& s);
+void configure_gel_tiling(DeviceSim& s, int nx, int ny, int nz);
+constexpr int kResetAll = 7;
 // capture_kernels.cu
 int capture(DeviceSim& s, const tg_render& r, double* depth_host, uint8_t* rgb_host,
             std::string& msg);
@@ -77,6 +78,7 @@ DeviceSim::~DeviceSim() {
   cudaFree(tag);
   cudaFree(grid_mp);
   cudaFree(grid_v);
+  cudaFree(grid_mi);
   cudaFree(surf_idx);
   cudaFree(surf_depth);
   cudaFree(cap_depth);
@@ -212,6 +214,7 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
             cudaMalloc(&s->tag, std::max<int64_t>(n_el, 1)) == cudaSuccess &&
             cudaMalloc(&s->grid_mp, s->n_nodes * sizeof(double4)) == cudaSuccess &&
             cudaMalloc(&s->grid_v, s->n_nodes * sizeof(double4)) == cudaSuccess &&
+            cudaMalloc(&s->grid_mi, s->n_nodes * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->ctl, sizeof(Ctl)) == cudaSuccess &&
             cudaMallocHost(&s->h_ctl, sizeof(Ctl)) == cudaSuccess &&
             cudaMallocHost(&s->h_vind, 3 * sizeof(double)) == cudaSuccess;
@@ -221,6 +224,7 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   }
   cudaMemsetAsync(s->grid_mp, 0, s->n_nodes * sizeof(double4), s->stream);
   cudaMemsetAsync(s->grid_v, 0, s->n_nodes * sizeof(double4), s->stream);
+  cudaMemsetAsync(s->grid_mi, 0, s->n_nodes * sizeof(double), s->stream);
   std::memset(s->h_ctl, 0, sizeof(Ctl));
   for (int a = 0; a < 3; ++a) s->h_ctl->vind[a] = in->indenter_velocity[a];
   // Is the indenter velocity uniform (it is for init_scene's output)?
@@ -231,7 +235,7 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   for (int a = 0; a < 3; ++a) s->h_ctl->ind_v[a] = n_ind > 0 ? in->v[3 * n_el + a] : 0.0;
   s->h_ctl->diag_min_det_f = 1.0;
   cudaMemcpyAsync(s->ctl, s->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s->stream);
-  launch_reset(*s);
+  launch_reset(*s, kResetAll);
 
   // Tags of the elastomer (Elastomer / ElastomerBottom).
   std::vector<uint8_t> tags(std::max<int64_t>(n_el, 1));
@@ -269,6 +273,10 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
       return fail(TG_ERR_CUDA, "tg_create: device allocation failed");
     }
     cudaMemcpy(s->surf_idx, idx.data(), cnt * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    // Lattice metadata (particle_set.hpp:16-17): the surface is the top layer
+    // of an nx x ny x nz elastomer lattice.
+    const int64_t cols = static_cast<int64_t>(surf->nx) * surf->ny;
+    if (n_el % cols == 0) configure_gel_tiling(*s, surf->nx, surf->ny, static_cast<int>(n_el / cols));
   }
   const cudaError_t e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) {
@@ -295,8 +303,9 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
   const int at = c.err_substep;
   // Clear the latch; the next call re-derives the window from the state.
   CUDA_TRY(cudaMemsetAsync(&s.ctl->err_code, 0, sizeof(int), s.stream));
-  launch_reset(s);
+  launch_reset(s, kResetAll);
   s.window_valid = false;
+  s.grid_dirty = true;  // a look-ahead scatter may have started
   CUDA_TRY(cudaStreamSynchronize(s.stream));
   if (at >= end_substep) return TG_OK;
   const char* what = code == kErrOutOfGrid
@@ -305,14 +314,21 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
   return fail(code, std::string(error_name(code)) + ": " + what);
 }
 
+// The substep plan of one mpm::step call (see mpm_kernels.cu): a standalone
+// scatter for the first substep, then per substep grid_update (re-zeroing the
+// accumulators) and the fused G2P(+boundary+advect)+look-ahead-P2G kernels;
+// the last substep does no look-ahead.
 static int record_substeps(DeviceSim& s, int n_substeps) {
   int k = 0;
   const int sms = sm_count(s.device);
+  if (s.grid_dirty) k += launch_clear(s, sms);
+  k += launch_p2g_gel(s) + launch_p2g_ind(s);
   for (int i = 0; i < n_substeps; ++i) {
-    k += launch_clear(s, sms);
-    k += launch_p2g(s, false);
-    k += launch_grid_update(s, sms);
-    k += launch_g2p_move(s);
+    const bool lookahead = i + 1 < n_substeps;
+    k += launch_grid_update(s, sms, true);
+    k += launch_g2p2g_gel(s, lookahead);
+    k += launch_ind_move(s, lookahead);
+    k += launch_finalize_step(s);
   }
   return k;
 }
@@ -328,7 +344,8 @@ int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
   if (!s.window_valid) launch_window(s);
   s.window_valid = true;
   if (s.use_graphs) {
-    auto it = s.graphs.find(n_substeps);
+    const int key = n_substeps * 4 + (s.grid_dirty ? 1 : 0) + (s.ind_v_uniform ? 2 : 0);
+    auto it = s.graphs.find(key);
     if (it == s.graphs.end()) {
       cudaGraph_t graph;
       const int64_t before = s.kernel_launches;
@@ -341,11 +358,13 @@ int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
       CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
       cudaGraphDestroy(graph);
       s.kernel_launches = before;  // counted per replay below
-      it = s.graphs.emplace(n_substeps, exec).first;
-      s.graph_kernels[n_substeps] = k;
+      it = s.graphs.emplace(key, exec).first;
+      s.graph_kernels[key] = k;
     }
     CUDA_TRY(cudaGraphLaunch(it->second, s.stream));
-    s.kernel_launches += s.graph_kernels[n_substeps];
+    s.kernel_launches += s.graph_kernels[key];
+    s.grid_dirty = false;
+    s.ind_v_uniform = true;
   } else {
     CUDA_TRY(cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double),
                              cudaMemcpyHostToDevice, s.stream));
@@ -368,13 +387,15 @@ int step(DeviceSim& s, const double vind[3], int n_substeps) {
 int check_device_public(int device) { return check_device(device); }
 
 // Per-kernel device times of the substep plan (CUDA events between the
-// launches, no graph), averaged over `reps` substeps. Order:
-// clear, p2g_gel, p2g_ind, grid_update, g2p_gel(+boundary+advect),
-// ind_move, finalize. Used by bench.py for the roofline.
+// launches, no graph), averaged over `reps` substeps: one mpm::step call of
+// `reps` substeps launched kernel by kernel. Order of out_ms:
+// [p2g_elastomer (standalone, first substep only), p2g_indenter (standalone),
+//  grid_update, g2p2g_elastomer (G2P+boundary+advect+look-ahead P2G),
+//  indenter_move_p2g, finalize]. Used by bench.py for the roofline.
 int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
   CUDA_TRY(cudaSetDevice(s.device));
   const int sms = sm_count(s.device);
-  constexpr int kGroups = 7;
+  constexpr int kGroups = 6;
   cudaEvent_t ev[kGroups + 1];
   for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
   for (int g = 0; g < kGroups; ++g) out_ms[g] = 0.0;
@@ -384,28 +405,37 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
   s.window_valid = true;
   CUDA_TRY(cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double), cudaMemcpyHostToDevice,
                            s.stream));
+  if (s.grid_dirty) launch_clear(s, sms);
+  float ms = 0.f;
+  cudaEventRecord(ev[0], s.stream);
+  launch_p2g_gel(s);
+  cudaEventRecord(ev[1], s.stream);
+  launch_p2g_ind(s);
+  cudaEventRecord(ev[2], s.stream);
+  CUDA_TRY(cudaEventSynchronize(ev[2]));
+  cudaEventElapsedTime(&ms, ev[0], ev[1]);
+  out_ms[0] = ms;
+  cudaEventElapsedTime(&ms, ev[1], ev[2]);
+  out_ms[1] = ms;
   for (int r = 0; r < reps; ++r) {
-    cudaEventRecord(ev[0], s.stream);
-    launch_clear(s, sms);
-    cudaEventRecord(ev[1], s.stream);
-    launch_p2g_gel(s);
+    const bool lookahead = r + 1 < reps;
     cudaEventRecord(ev[2], s.stream);
-    launch_p2g_ind(s);
+    launch_grid_update(s, sms, true);
     cudaEventRecord(ev[3], s.stream);
-    launch_grid_update(s, sms);
+    launch_g2p2g_gel(s, lookahead);
     cudaEventRecord(ev[4], s.stream);
-    launch_g2p_gel_move(s);
+    launch_ind_move(s, lookahead);
     cudaEventRecord(ev[5], s.stream);
-    launch_ind_move(s);
-    cudaEventRecord(ev[6], s.stream);
     launch_finalize_step(s);
-    cudaEventRecord(ev[7], s.stream);
-    CUDA_TRY(cudaEventSynchronize(ev[7]));
-    for (int g = 0; g < kGroups; ++g) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[g], ev[g + 1]);
-      out_ms[g] += ms / reps;
-    }
+    cudaEventRecord(ev[6], s.stream);
+    CUDA_TRY(cudaEventSynchronize(ev[6]));
+    // average over the look-ahead substeps (all but the last) when reps > 1
+    const int denom = reps > 1 ? reps - 1 : 1;
+    if (lookahead || reps == 1)
+      for (int g = 2; g < kGroups; ++g) {
+        cudaEventElapsedTime(&ms, ev[g], ev[g + 1]);
+        out_ms[g] += ms / denom;
+      }
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return sync_and_check(s, start + reps);
@@ -421,7 +451,7 @@ int phase(DeviceSim& s, int ph, const double vind[3]) {
       launch_clear(s, sms);
       break;
     case TG_PHASE_PARTICLE_TO_GRID: launch_p2g(s, true); break;
-    case TG_PHASE_GRID_UPDATE: launch_grid_update(s, sms); break;
+    case TG_PHASE_GRID_UPDATE: launch_grid_update(s, sms, false); break;
     case TG_PHASE_GRID_TO_PARTICLE: launch_phase_g2p(s); break;
     case TG_PHASE_APPLY_BOUNDARY:
       for (int a = 0; a < 3; ++a) s.h_vind[a] = vind[a];

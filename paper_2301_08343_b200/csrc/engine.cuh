@@ -20,9 +20,10 @@ struct Ctl {
   int err_substep;   // absolute substep index the error belongs to
   int substep;       // absolute index of the substep being executed
   int pad0;
-  unsigned long long bb_lo[3], bb_hi[3];  // order_key() of x after advect
+  unsigned long long bb_lo[3], bb_hi[3];  // order_key() of elastomer x after advect
+  unsigned long long ind_lo[3], ind_hi[3];  // order_key() of the indenter bbox
   unsigned long long max_v2;              // bits of max |v|^2 (non-negative)
-  unsigned long long min_detf;            // order_key() of min det F (P2G)
+  unsigned long long min_detf[2];         // order_key() of min det F, per substep parity
   int win_lo[3], win_hi[3];               // Grid::active_lo/hi
   int prev_lo[3], prev_hi[3];             // Grid::prev_lo/hi
   int clr_lo[3], clr_hi[3];               // node box to clear before P2G
@@ -63,7 +64,14 @@ struct DeviceSim {
   // Grid::velocity as double4 {vx, vy, vz, 0}).
   double4* grid_mp = nullptr;
   double4* grid_v = nullptr;
+  double* grid_mi = nullptr;  // indenter mass (uniform-velocity indenter scatter)
   size_t n_nodes = 0;
+  // Elastomer lattice (counts) when the elastomer is lattice-built; enables
+  // the lattice-block CTA tiling of the elastomer scatter.
+  int lat[3] = {0, 0, 0};
+  int tile[3] = {0, 0, 0};   // lattice block per CTA (ti, tj, tk)
+  int tiles[3] = {0, 0, 0};  // blocks per axis
+  bool grid_dirty = false;   // A / M_I may hold a phase-mode P2G (needs k_clear)
 
   // Surface lattice (sim_state.hpp:41-52) + capture scratch.
   int surf_nx = 0, surf_ny = 0;

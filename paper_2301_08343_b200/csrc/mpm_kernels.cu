@@ -1,22 +1,33 @@
 // MLS-MPM substep kernels for sm_100a.
 //
-// One substep (mpm::step body, engine.cpp:289-296) is launched as
-//   k_clear      zero_grid's clear of prev ∪ new window (engine.cpp:70-85)
-//   k_p2g_gel    particle_to_grid for elastomer particles: det F, Newton polar,
-//                corotated stress, APIC affine, 27-node RED.F64 scatter
-//                (engine.cpp:107-178, material.cpp:27-89)
-//   k_p2g_ind    particle_to_grid for the rigid indenter cloud (C = 0, no
-//                stress, engine.cpp:131)
-//   k_grid_update  v = p / m (+ g dt), zero normal velocity on the domain
-//                faces, 0 where m = 0 (engine.cpp:180-205)
-//   k_g2p_gel    grid_to_particle + apply_boundary + advect for elastomer
-//                particles (engine.cpp:207-252, 254-266, 268-279), fused, with
-//                the bbox / max-speed reductions of advect
-//   k_ind_move   apply_boundary + advect for the indenter (engine.cpp:260-261)
-//   k_finalize   advect's in_range check and step_count, then the next
-//                substep's zero_grid window (engine.cpp:53-68, 280-285)
-// Errors are latched in Ctl::err_code and every later kernel of the substep
-// exits early, which reproduces the reference's "state at the throwing phase".
+// Step path (mpm::step, engine.cpp:288-297), per substep s:
+//   k_grid_update<true>  grid_update (engine.cpp:180-205) over the active
+//                        window; reads Grid::mass/momentum (A, M_I), writes
+//                        Grid::velocity (V) and re-zeroes A / M_I, so the next
+//                        scatter needs no separate zero_grid clear.
+//   k_g2p2g_gel          grid_to_particle + apply_boundary + advect for the
+//                        elastomer (engine.cpp:207-279) and, fused in the same
+//                        CTA, particle_to_grid of substep s+1 (engine.cpp:
+//                        107-178: det F, Newton polar, corotated stress, APIC)
+//                        through a shared-memory node tile: 27 barrier-
+//                        separated conflict-free accumulation phases, then one
+//                        RED.F64 per touched node and component.
+//   k_ind_move_p2g       apply_boundary + advect of the rigid indenter
+//                        (engine.cpp:260-261, 275-279) fused with its s+1
+//                        scatter: run-length accumulation of B-spline weights
+//                        in registers along z-sorted particle runs, one
+//                        RED.F64 per touched node (mass only: the indenter's
+//                        momentum is M_I * v, v uniform).
+//   k_finalize           advect's in_range check / step_count / max_speed and
+//                        the next zero_grid window (engine.cpp:53-68, 279-285).
+// The first substep of a call starts with a standalone scatter (k_p2g_gel_tile,
+// k_ind_move_p2g<false, true>); the last substep does no look-ahead scatter so
+// the state is complete when mpm::step returns. Errors are latched in
+// Ctl::err_code with the substep they belong to; every kernel of a later or
+// equal substep exits early, reproducing the reference's "state at the
+// throwing phase".
+#include <climits>
+
 #include "engine.cuh"
 
 namespace tacchi_b200 {
@@ -25,6 +36,22 @@ namespace {
 
 __device__ __forceinline__ void raise(Ctl* ctl, int code, int substep) {
   if (atomicCAS(&ctl->err_code, 0, code) == 0) ctl->err_substep = substep;
+}
+
+// True when an error latched for substep <= s (the work of substep s must not run).
+__device__ __forceinline__ bool stale(const Ctl* ctl, int s) {
+  return ctl->err_code != 0 && ctl->err_substep <= s;
+}
+
+// Block-uniform version (one read, broadcast through shared memory) for
+// kernels that use __syncthreads after the check.
+__device__ __forceinline__ bool stale_block(const Ctl* ctl, int s) {
+  __shared__ int flag;
+  if (threadIdx.x == 0) flag = stale(ctl, s) ? 1 : 0;
+  __syncthreads();
+  const bool r = flag != 0;
+  __syncthreads();
+  return r;
 }
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -38,12 +65,12 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-// advect's reductions: max |v|^2 and the bbox of x (engine.cpp:273-282).
-// Warp shuffles, then one shared-memory pass per block, then 7 atomics per
-// block (a per-warp atomic on 7 hot words serialises badly at 1e6 particles).
-// Every thread of the block must call this (no early exits before it).
-__device__ __forceinline__ void reduce_motion(Ctl* ctl, bool active, double v2, double x0,
-                                              double x1, double x2) {
+// Block reduction of advect's quantities (engine.cpp:273-282): max |v|^2 and
+// the bbox of x. Warp shuffles, one shared-memory pass, then 7 atomics per
+// block. Every thread of the block must call it.
+__device__ void reduce_motion(unsigned long long* max_v2, unsigned long long* lo_keys,
+                              unsigned long long* hi_keys, bool active, double v2, double x0,
+                              double x1, double x2) {
   __shared__ double red[7][32];
   double r[7];
   r[0] = active ? v2 : 0.0;
@@ -60,6 +87,7 @@ __device__ __forceinline__ void reduce_motion(Ctl* ctl, bool active, double v2, 
   for (int a = 4; a < 7; ++a) r[a] = warp_max(r[a]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = (blockDim.x + 31) >> 5;
+  __syncthreads();
   if (lane == 0)
 #pragma unroll
     for (int a = 0; a < 7; ++a) red[a][warp] = r[a];
@@ -76,13 +104,13 @@ __device__ __forceinline__ void reduce_motion(Ctl* ctl, bool active, double v2, 
 #pragma unroll
     for (int a = 4; a < 7; ++a) r[a] = warp_max(r[a]);
     if (lane == 0 && r[1] <= r[4]) {
-      atomicMax(&ctl->max_v2, static_cast<unsigned long long>(__double_as_longlong(r[0])));
-      atomicMin(&ctl->bb_lo[0], order_key(r[1]));
-      atomicMin(&ctl->bb_lo[1], order_key(r[2]));
-      atomicMin(&ctl->bb_lo[2], order_key(r[3]));
-      atomicMax(&ctl->bb_hi[0], order_key(r[4]));
-      atomicMax(&ctl->bb_hi[1], order_key(r[5]));
-      atomicMax(&ctl->bb_hi[2], order_key(r[6]));
+      if (max_v2) atomicMax(max_v2, static_cast<unsigned long long>(__double_as_longlong(r[0])));
+      atomicMin(&lo_keys[0], order_key(r[1]));
+      atomicMin(&lo_keys[1], order_key(r[2]));
+      atomicMin(&lo_keys[2], order_key(r[3]));
+      atomicMax(&hi_keys[0], order_key(r[4]));
+      atomicMax(&hi_keys[1], order_key(r[5]));
+      atomicMax(&hi_keys[2], order_key(r[6]));
     }
   }
 }
@@ -93,26 +121,273 @@ __device__ __forceinline__ size_t node_index(const Geometry& g, int i, int j, in
 
 __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); }
 
+__device__ __forceinline__ bool stencil_in_grid(const Geometry& g, const Stencil& st) {
+  return st.base[0] >= 0 && st.base[1] >= 0 && st.base[2] >= 0 && st.base[0] + 2 < g.res[0] &&
+         st.base[1] + 2 < g.res[1] && st.base[2] + 2 < g.res[2];
+}
+
+// advect: x += dt * v with the reference's rounding (no FMA, engine.cpp:276).
+__device__ __forceinline__ double advance(double x, double dt, double v) {
+  return add_rn(x, mul_rn(dt, v));
+}
+
 }  // namespace
 
-// bbox of all positions (particle_bbox, engine.cpp:31-45), for a fresh window.
-__global__ void k_bbox(const double* __restrict__ x, int64_t n, Ctl* ctl) {
+// ---------------------------------------------------------------------------
+// Elastomer particle -> CTA mapping. With lattice metadata, a CTA owns a
+// (ti x tj x nz) block of lattice columns (particle (i,j,k) at
+// (i*ny + j)*nz + k, particle_set.hpp:16-17), which keeps its scatter
+// footprint compact; otherwise 256 consecutive particles.
+// ---------------------------------------------------------------------------
+struct GelMap {
+  int lat[3];
+  int tile[3];
+  int tiles[3];
+};
+
+namespace {
+
+__device__ __forceinline__ int64_t gel_particle(const GelMap& M, int64_t n_el) {
+  if (M.lat[0] > 0) {
+    const int t = threadIdx.x;
+    const int per_col = M.tile[2];
+    const int kk = t % per_col;
+    const int jj = (t / per_col) % M.tile[1];
+    const int ii = t / (per_col * M.tile[1]);
+    if (ii >= M.tile[0]) return -1;
+    const int bj = blockIdx.x % M.tiles[1];
+    const int bi = blockIdx.x / M.tiles[1];
+    const int i = bi * M.tile[0] + ii, j = bj * M.tile[1] + jj;
+    if (i >= M.lat[0] || j >= M.lat[1] || kk >= M.lat[2]) return -1;
+    return (static_cast<int64_t>(i) * M.lat[1] + j) * M.lat[2] + kk;
+  }
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool active = p < n;
-  reduce_motion(ctl, active, 0.0, active ? x[p] : 0.0, active ? x[n + p] : 0.0,
+  return p < n_el ? p : -1;
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory node tile for the elastomer scatter.
+// ---------------------------------------------------------------------------
+constexpr int kTileCap = 2816;  // nodes; 4 x 8 B x 2816 + 4 B x 2816 = 101 KB
+
+struct P2GTile {
+  double m[kTileCap], px[kTileCap], py[kTileCap], pz[kTileCap];
+  int owner[kTileCap];
+  int lo[3], hi[3], dim[3];
+  int ok;
+};
+
+// One particle's P2G payload (engine.cpp:128-145): stencil, m v and the
+// APIC + stress affine matrix.
+struct P2GPayload {
+  Stencil st;
+  double mv[3];
+  double aff[9];
+};
+
+__device__ __forceinline__ void scatter_direct(const Geometry& g, double4* grid, double m,
+                                               const P2GPayload& q) {
+  const double dx = g.dx;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double wa = q.st.w[0][a];
+    const double dxa = (a - q.st.fx[0]) * dx;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const double wab = wa * q.st.w[1][b];
+      const double dxb = (b - q.st.fx[1]) * dx;
+      const double m0 = q.mv[0] + q.aff[0] * dxa + q.aff[1] * dxb;
+      const double m1 = q.mv[1] + q.aff[3] * dxa + q.aff[4] * dxb;
+      const double m2 = q.mv[2] + q.aff[6] * dxa + q.aff[7] * dxb;
+      double* row = reinterpret_cast<double*>(
+          grid + node_index(g, q.st.base[0] + a, q.st.base[1] + b, q.st.base[2]));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double w = wab * q.st.w[2][c];
+        const double dxc = (c - q.st.fx[2]) * dx;
+        red_add(row + 4 * c + 0, w * m);
+        red_add(row + 4 * c + 1, w * (m0 + q.aff[2] * dxc));
+        red_add(row + 4 * c + 2, w * (m1 + q.aff[5] * dxc));
+        red_add(row + 4 * c + 3, w * (m2 + q.aff[8] * dxc));
+      }
+    }
+  }
+}
+
+// CTA-cooperative scatter. All threads of the block must call it.
+// Phase (a,b,c) adds each particle's contribution to node base + (a,b,c);
+// two particles of the CTA collide in a phase only if they share a base cell,
+// which an elastomer lattice coarser than the grid (0.2 mm vs 0.129 mm) never
+// does; the rare duplicates (detected through the owner table) and CTAs whose
+// footprint exceeds the tile fall back to direct REDs.
+__device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
+                                 const Geometry& g, double4* grid) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    T.lo[0] = T.lo[1] = T.lo[2] = INT_MAX;
+    T.hi[0] = T.hi[1] = T.hi[2] = INT_MIN;
+  }
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&T.lo[a], q.st.base[a]);
+      atomicMax(&T.hi[a], q.st.base[a]);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int vol = 1;
+    const bool any = T.lo[0] != INT_MAX;
+    for (int a = 0; a < 3; ++a) {
+      T.dim[a] = any ? T.hi[a] - T.lo[a] + 3 : 0;
+      vol *= T.dim[a];
+    }
+    T.ok = any && vol <= kTileCap;
+  }
+  __syncthreads();
+  const int d1 = T.dim[1], d2 = T.dim[2];
+  const int vol = T.dim[0] * d1 * d2;
+  const bool use_tile = T.ok != 0;
+  if (use_tile) {
+    for (int e = tid; e < vol; e += blockDim.x) {
+      T.m[e] = 0.0;
+      T.px[e] = 0.0;
+      T.py[e] = 0.0;
+      T.pz[e] = 0.0;
+      T.owner[e] = -1;
+    }
+  }
+  __syncthreads();
+  int base_idx = 0;
+  bool tiled = false;
+  if (active) {
+    if (use_tile) {
+      base_idx = ((q.st.base[0] - T.lo[0]) * d1 + (q.st.base[1] - T.lo[1])) * d2 +
+                 (q.st.base[2] - T.lo[2]);
+      tiled = atomicCAS(&T.owner[base_idx], -1, tid) == -1;
+    }
+    if (!tiled) scatter_direct(g, grid, m, q);
+  }
+  if (!use_tile) return;  // block-uniform
+  const double dx = g.dx;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double dxa = (a - q.st.fx[0]) * dx;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const double dxb = (b - q.st.fx[1]) * dx;
+      const double wab = q.st.w[0][a] * q.st.w[1][b];
+      const double m0 = q.mv[0] + q.aff[0] * dxa + q.aff[1] * dxb;
+      const double m1 = q.mv[1] + q.aff[3] * dxa + q.aff[4] * dxb;
+      const double m2 = q.mv[2] + q.aff[6] * dxa + q.aff[7] * dxb;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        __syncthreads();
+        if (tiled) {
+          const double dxc = (c - q.st.fx[2]) * dx;
+          const double w = wab * q.st.w[2][c];
+          const int e = base_idx + (a * d1 + b) * d2 + c;
+          T.m[e] += w * m;
+          T.px[e] += w * (m0 + q.aff[2] * dxc);
+          T.py[e] += w * (m1 + q.aff[5] * dxc);
+          T.pz[e] += w * (m2 + q.aff[8] * dxc);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < vol; e += blockDim.x) {
+    const double mm = T.m[e];
+    if (mm == 0.0) continue;
+    const int k = e % d2, r = e / d2;
+    const int j = r % d1, i = r / d1;
+    double* nd =
+        reinterpret_cast<double*>(grid + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2] + k));
+    red_add(nd + 0, mm);
+    red_add(nd + 1, T.px[e]);
+    red_add(nd + 2, T.py[e]);
+    red_add(nd + 3, T.pz[e]);
+  }
+}
+
+// det F check + polar + stress + affine (engine.cpp:130-139). Returns false
+// (and latches DegenerateF for substep s) when det F <= 0.
+__device__ __forceinline__ bool make_payload(const Geometry& g, Ctl* ctl, int s, double m,
+                                             double vol0, const double* F, const double* Cm,
+                                             const double* v, double x0, double x1, double x2,
+                                             P2GPayload& q, double& J) {
+  J = det3(F);
+  if (!(J > 0.0)) {
+    raise(ctl, kErrDegenerateF, s);
+    return false;
+  }
+  make_stencil(x0, x1, x2, g.origin, g.inv_dx, q.st);
+  double R[9];
+  polar_rotation(F, R);
+  double A[9], S[9];
+  const double s2mu = 2.0 * g.mu;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) A[i] = s2mu * (F[i] - R[i]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      S[3 * i + j] = A[3 * i] * F[3 * j] + A[3 * i + 1] * F[3 * j + 1] + A[3 * i + 2] * F[3 * j + 2];
+  const double sl = g.lambda * (J - 1.0) * J;
+  S[0] += sl;
+  S[4] += sl;
+  S[8] += sl;
+  const double ks = g.stress_scale * vol0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) q.aff[i] = m * Cm[i] + ks * S[i];
+  q.mv[0] = m * v[0];
+  q.mv[1] = m * v[1];
+  q.mv[2] = m * v[2];
+  return true;
+}
+
+// StepDiagnostics::min_det_f of substep s, seeded with 1.0 (engine.cpp:119,135).
+__device__ __forceinline__ void reduce_min_detf(Ctl* ctl, int s, bool active, double J) {
+  const double w = warp_min(active ? J : 1.0);
+  if ((threadIdx.x & 31) == 0 && w < 1.0) atomicMin(&ctl->min_detf[s & 1], order_key(w));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Window / bbox / finalize
+// ---------------------------------------------------------------------------
+
+enum : int { kResetMotion = 1, kResetIndBox = 2, kResetDetF = 4 };
+
+__global__ void k_reset(Ctl* ctl, int mask) {
+  for (int a = 0; a < 3; ++a) {
+    if (mask & kResetMotion) {
+      ctl->bb_lo[a] = order_key(INFINITY);
+      ctl->bb_hi[a] = order_key(-INFINITY);
+    }
+    if (mask & kResetIndBox) {
+      ctl->ind_lo[a] = order_key(INFINITY);
+      ctl->ind_hi[a] = order_key(-INFINITY);
+    }
+  }
+  if (mask & kResetMotion) ctl->max_v2 = 0ull;
+  if (mask & kResetDetF) ctl->min_detf[0] = ctl->min_detf[1] = order_key(1.0);
+}
+
+// particle_bbox (engine.cpp:31-45) over [begin, end): elastomer part into
+// bb_*, indenter part into ind_* (then advanced analytically by finalize).
+__global__ void k_bbox(const double* __restrict__ x, int64_t n, int64_t begin, int64_t end,
+                       Ctl* ctl, int indenter) {
+  const int64_t p = begin + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool active = p < end;
+  reduce_motion(nullptr, indenter ? ctl->ind_lo : ctl->bb_lo, indenter ? ctl->ind_hi : ctl->bb_hi,
+                active, 0.0, active ? x[p] : 0.0, active ? x[n + p] : 0.0,
                 active ? x[2 * n + p] : 0.0);
 }
 
-__global__ void k_reset(Ctl* ctl) {
-  for (int a = 0; a < 3; ++a) {
-    ctl->bb_lo[a] = order_key(INFINITY);
-    ctl->bb_hi[a] = order_key(-INFINITY);
-  }
-  ctl->max_v2 = 0ull;
-  ctl->min_detf = order_key(1.0);
-}
-
-enum : int { kFinAdvect = 1, kFinWindow = 2, kFinDiag = 4 };
+enum : int { kFinAdvect = 1, kFinWindow = 2, kFinDiag = 4, kFinIndShift = 8 };
 
 // grid.cpp:29-36: in_range divides by dx.
 __device__ bool in_range(const Geometry& g, const double* x) {
@@ -125,21 +400,33 @@ __device__ bool in_range(const Geometry& g, const double* x) {
 }
 
 __global__ void k_finalize(Ctl* ctl, Geometry g, int mode) {
-  if (ctl->err_code) return;
+  const int s = ctl->substep;
+  if (stale(ctl, s)) return;
+  if (mode & kFinDiag) {  // particle_to_grid's min_det_f (engine.cpp:119,177)
+    ctl->diag_min_det_f = order_val(ctl->min_detf[s & 1]);
+    ctl->min_detf[s & 1] = order_key(1.0);
+  }
+  double v2 = __longlong_as_double(static_cast<long long>(ctl->max_v2));
+  if ((mode & kFinIndShift) && ctl->ind_lo[0] <= ctl->ind_hi[0]) {
+    // The indenter moved rigidly with vind: fl(x + fl(dt v)) is monotone in
+    // x, so its bbox moves by exactly the same rounded step as its particles.
+    for (int a = 0; a < 3; ++a) {
+      const double d = mul_rn(g.dt, ctl->vind[a]);
+      ctl->ind_lo[a] = order_key(add_rn(order_val(ctl->ind_lo[a]), d));
+      ctl->ind_hi[a] = order_key(add_rn(order_val(ctl->ind_hi[a]), d));
+    }
+    const double* u = ctl->vind;
+    v2 = fmax(v2, u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+  }
   double lo[3], hi[3];
   for (int a = 0; a < 3; ++a) {
-    lo[a] = order_val(ctl->bb_lo[a]);
-    hi[a] = order_val(ctl->bb_hi[a]);
-  }
-  if (mode & kFinDiag) {  // particle_to_grid's min_det_f (engine.cpp:177)
-    ctl->diag_min_det_f = order_val(ctl->min_detf);
-    ctl->min_detf = order_key(1.0);
+    lo[a] = fmin(order_val(ctl->bb_lo[a]), order_val(ctl->ind_lo[a]));
+    hi[a] = fmax(order_val(ctl->bb_hi[a]), order_val(ctl->ind_hi[a]));
   }
   if (mode & kFinAdvect) {
     // engine.cpp:279-285
-    ctl->diag_max_speed = sqrt(__longlong_as_double(static_cast<long long>(ctl->max_v2)));
+    ctl->diag_max_speed = sqrt(v2);
     ctl->step_count += 1;
-    const int s = ctl->substep;
     ctl->substep = s + 1;
     if (!in_range(g, lo) || !in_range(g, hi)) {
       raise(ctl, kErrOutOfGrid, s);
@@ -175,9 +462,9 @@ __global__ void k_finalize(Ctl* ctl, Geometry g, int mode) {
   ctl->max_v2 = 0ull;
 }
 
-// Clear of Grid::mass / momentum over Ctl::clr box (engine.cpp:72-83).
-__global__ void k_clear(double4* __restrict__ grid, Ctl* ctl, Geometry g) {
-  if (ctl->err_code) return;
+// zero_grid's clear of Grid::mass / momentum over Ctl::clr (engine.cpp:72-83).
+__global__ void k_clear(double4* __restrict__ grid, double* __restrict__ mi, Ctl* ctl, Geometry g) {
+  if (stale(ctl, ctl->substep)) return;
   const int lx = ctl->clr_lo[0], ly = ctl->clr_lo[1], lz = ctl->clr_lo[2];
   const int ny = ctl->clr_hi[1] - ly, nz = ctl->clr_hi[2] - lz;
   const int64_t total = static_cast<int64_t>(ctl->clr_hi[0] - lx) * ny * nz;
@@ -188,190 +475,173 @@ __global__ void k_clear(double4* __restrict__ grid, Ctl* ctl, Geometry g) {
     const int64_t r = t / nz;
     const int j = static_cast<int>(r % ny);
     const int i = static_cast<int>(r / ny);
-    grid[node_index(g, lx + i, ly + j, lz + k)] = z;
+    const size_t nd = node_index(g, lx + i, ly + j, lz + k);
+    grid[nd] = z;
+    mi[nd] = 0.0;
   }
 }
 
-// particle_to_grid for elastomer particles (engine.cpp:126-168).
-__global__ void __launch_bounds__(256) k_p2g_gel(const double* __restrict__ x,
-                                                 const double* __restrict__ v,
-                                                 const double* __restrict__ Cm,
-                                                 const double* __restrict__ Fm, int64_t n,
-                                                 int64_t n_el, Ctl* ctl, Geometry g,
-                                                 double4* __restrict__ grid, double m,
-                                                 double vol0) {
-  if (ctl->err_code) return;
-  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool active = p < n_el;
-  double F[9];
+// ---------------------------------------------------------------------------
+// particle_to_grid
+// ---------------------------------------------------------------------------
+
+// Standalone elastomer scatter (first substep of a call / phase API).
+__global__ void __launch_bounds__(256, 2) k_p2g_gel_tile(
+    const double* __restrict__ x, const double* __restrict__ v, const double* __restrict__ Cm,
+    const double* __restrict__ Fm, int64_t n, int64_t n_el, GelMap M, Ctl* ctl, Geometry g,
+    double4* __restrict__ grid, double m, double vol0) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  P2GTile& T = *reinterpret_cast<P2GTile*>(smem_raw);
+  const int s = ctl->substep;
+  if (stale_block(ctl, s)) return;
+  const int64_t p = gel_particle(M, n_el);
+  bool active = p >= 0;
+  P2GPayload q;
   double J = 1.0;
   if (active) {
+    double F[9], C9[9], vv[3];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) F[i] = Fm[i * n_el + p];
-    J = det3(F);
-  }
-  // StepDiagnostics::min_det_f, seeded with 1.0 (engine.cpp:119,135).
-  const bool bad = active && !(J > 0.0);
-  if (__any_sync(0xffffffffu, bad)) {
-    if (bad) raise(ctl, kErrDegenerateF, ctl->substep);
-    return;
-  }
-  const double wmin = warp_min(active ? J : 1.0);
-  if ((threadIdx.x & 31) == 0) atomicMin(&ctl->min_detf, order_key(wmin));
-  if (!active) return;
-
-  Stencil st;
-  make_stencil(x[p], x[n + p], x[2 * n + p], g.origin, g.inv_dx, st);
-  double R[9];
-  polar_rotation(F, R);
-  // S = 2 mu (F - R) F^T + lambda (J - 1) J I   (engine.cpp:137-138)
-  double A[9], S[9];
-  const double s2mu = 2.0 * g.mu;
-#pragma unroll
-  for (int i = 0; i < 9; ++i) A[i] = s2mu * (F[i] - R[i]);
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-      S[3 * i + j] = A[3 * i] * F[3 * j] + A[3 * i + 1] * F[3 * j + 1] + A[3 * i + 2] * F[3 * j + 2];
-  const double sl = g.lambda * (J - 1.0) * J;
-  S[0] += sl; S[4] += sl; S[8] += sl;
-  // affine = m C + (-dt 4/dx^2 V0) S   (engine.cpp:130,139)
-  const double ks = g.stress_scale * vol0;
-  double aff[9];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) aff[i] = m * Cm[i * n_el + p] + ks * S[i];
-  const double mv0 = m * v[p], mv1 = m * v[n + p], mv2 = m * v[2 * n + p];
-  const double dx = g.dx;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double wa = st.w[0][a];
-    const double dxa = (a - st.fx[0]) * dx;
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      const double wab = wa * st.w[1][b];
-      const double dxb = (b - st.fx[1]) * dx;
-      const double m0 = mv0 + aff[0] * dxa + aff[1] * dxb;
-      const double m1 = mv1 + aff[3] * dxa + aff[4] * dxb;
-      const double m2 = mv2 + aff[6] * dxa + aff[7] * dxb;
-      double* row = reinterpret_cast<double*>(
-          grid + node_index(g, st.base[0] + a, st.base[1] + b, st.base[2]));
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double w = wab * st.w[2][c];
-        const double dxc = (c - st.fx[2]) * dx;
-        red_add(row + 4 * c + 0, w * m);
-        red_add(row + 4 * c + 1, w * (m0 + aff[2] * dxc));
-        red_add(row + 4 * c + 2, w * (m1 + aff[5] * dxc));
-        red_add(row + 4 * c + 3, w * (m2 + aff[8] * dxc));
-      }
+    for (int i = 0; i < 9; ++i) {
+      F[i] = Fm[i * n_el + p];
+      C9[i] = Cm[i * n_el + p];
     }
+    vv[0] = v[p];
+    vv[1] = v[n + p];
+    vv[2] = v[2 * n + p];
+    active = make_payload(g, ctl, s, m, vol0, F, C9, vv, x[p], x[n + p], x[2 * n + p], q, J);
+    if (active && !stencil_in_grid(g, q.st)) active = false;  // zero_grid already raised
   }
+  reduce_min_detf(ctl, s, active, J);
+  p2g_tile_scatter(T, active, q, m, g, grid);
 }
 
-// particle_to_grid for the rigid indenter (engine.cpp:126-168 with C = 0 and
-// no stress, engine.cpp:131): affine = m C = 0, so each node receives
-// w m and w m v. Direct RED.F64 scatter (baseline variant).
-__global__ void __launch_bounds__(256) k_p2g_ind(const double* __restrict__ x,
-                                                 const double* __restrict__ v, int64_t n,
-                                                 int64_t n_el, Ctl* ctl, Geometry g,
-                                                 double4* __restrict__ grid, double m) {
-  if (ctl->err_code) return;
+// Indenter scatter with a non-uniform velocity (only possible before the
+// first apply_boundary after tg_create / tg_upload): direct REDs of w m and
+// w m v into A.
+__global__ void __launch_bounds__(256) k_p2g_ind_direct(const double* __restrict__ x,
+                                                        const double* __restrict__ v, int64_t n,
+                                                        int64_t n_el, Ctl* ctl, Geometry g,
+                                                        double4* __restrict__ grid, double m) {
+  if (stale(ctl, ctl->substep)) return;
   const int64_t p = n_el + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  Stencil st;
-  make_stencil(x[p], x[n + p], x[2 * n + p], g.origin, g.inv_dx, st);
-  const double mv0 = m * v[p], mv1 = m * v[n + p], mv2 = m * v[2 * n + p];
+  P2GPayload q;
+  make_stencil(x[p], x[n + p], x[2 * n + p], g.origin, g.inv_dx, q.st);
+  if (!stencil_in_grid(g, q.st)) return;
+  q.mv[0] = m * v[p];
+  q.mv[1] = m * v[n + p];
+  q.mv[2] = m * v[2 * n + p];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double wa = st.w[0][a];
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      const double wab = wa * st.w[1][b];
-      double* row = reinterpret_cast<double*>(
-          grid + node_index(g, st.base[0] + a, st.base[1] + b, st.base[2]));
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double w = wab * st.w[2][c];
-        red_add(row + 4 * c + 0, w * m);
-        red_add(row + 4 * c + 1, w * mv0);
-        red_add(row + 4 * c + 2, w * mv1);
-        red_add(row + 4 * c + 3, w * mv2);
-      }
-    }
-  }
+  for (int i = 0; i < 9; ++i) q.aff[i] = 0.0;
+  scatter_direct(g, grid, m, q);
 }
 
-// particle_to_grid for the rigid indenter when every indenter particle carries
-// the same velocity (always true after the first apply_boundary,
-// engine.cpp:260-261). Each node then receives (sum_p w_p m) (1, v): the
-// scatter reduces to one weight sum per node. Particles are ordered by base
-// cell (bx, by) then z at creation, so a thread walking kChunk consecutive
-// particles sees long runs of one base cell; it accumulates the 27 weight
-// sums in registers and issues the 27 x 4 REDs only when the base changes.
-// This cuts the RED.F64 count by ~the particles-per-cell density (~19 for the
-// 1e6-point sphere).
-template <int kChunk>
-__global__ void __launch_bounds__(256) k_p2g_ind_chunk(const double* __restrict__ x, int64_t n,
-                                                       int64_t n_el, Ctl* ctl, Geometry g,
-                                                       double4* __restrict__ grid, double m) {
-  if (ctl->err_code) return;
+// Rigid indenter: optional apply_boundary + advect (kMove) and the scatter of
+// the (next) substep (kScatter). A thread walks kChunk consecutive particles
+// of the (bx, by, z)-sorted cloud; the B-spline weight sums of the last four
+// z-planes of a 3x3 column are kept in registers and a plane is flushed (one
+// RED.F64 per node, into M_I) only when the run leaves it.
+template <int kChunk, bool kMove, bool kScatter>
+__global__ void __launch_bounds__(256) k_ind_move_p2g(double* __restrict__ x, int64_t n,
+                                                      int64_t n_el, Ctl* ctl, Geometry g,
+                                                      double* __restrict__ mi) {
+  const int s = ctl->substep;
+  if (stale(ctl, s)) return;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t p0 = n_el + t * kChunk;
+  if (kMove && t == 0) {
+    // apply_boundary: every indenter velocity becomes the command
+    // (engine.cpp:260-261); the next grid_update uses it as M_I's velocity.
+    ctl->ind_v[0] = ctl->vind[0];
+    ctl->ind_v[1] = ctl->vind[1];
+    ctl->ind_v[2] = ctl->vind[2];
+  }
   if (p0 >= n) return;
   const int64_t p1 = p0 + kChunk < n ? p0 + kChunk : n;
-  const double mv0 = m * ctl->ind_v[0], mv1 = m * ctl->ind_v[1], mv2 = m * ctl->ind_v[2];
-  double acc[27];
+  double d[3] = {0, 0, 0};
+  if (kMove)
+    for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
+  double acc[4][9];
 #pragma unroll
-  for (int i = 0; i < 27; ++i) acc[i] = 0.0;
-  int cb0 = 0, cb1 = 0, cb2 = 0;
-  bool have = false;
-  auto flush = [&]() {
+  for (int z = 0; z < 4; ++z)
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        double* row = reinterpret_cast<double*>(grid + node_index(g, cb0 + a, cb1 + b, cb2));
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double w = acc[9 * a + 3 * b + c];
-          if (w != 0.0) {
-            red_add(row + 4 * c + 0, w * m);
-            red_add(row + 4 * c + 1, w * mv0);
-            red_add(row + 4 * c + 2, w * mv1);
-            red_add(row + 4 * c + 3, w * mv2);
-          }
-          acc[9 * a + 3 * b + c] = 0.0;
-        }
-      }
-  };
+    for (int i = 0; i < 9; ++i) acc[z][i] = 0.0;
+  int cb0 = INT_MIN, cb1 = INT_MIN, z0 = INT_MIN;
   for (int64_t p = p0; p < p1; ++p) {
+    double px = x[p], py = x[n + p], pz = x[2 * n + p];
+    if (kMove) {
+      px = add_rn(px, d[0]);
+      py = add_rn(py, d[1]);
+      pz = add_rn(pz, d[2]);
+      x[p] = px;
+      x[n + p] = py;
+      x[2 * n + p] = pz;
+    }
+    if (!kScatter) continue;
     Stencil st;
-    make_stencil(x[p], x[n + p], x[2 * n + p], g.origin, g.inv_dx, st);
-    if (have && (st.base[0] != cb0 || st.base[1] != cb1 || st.base[2] != cb2)) flush();
-    cb0 = st.base[0];
-    cb1 = st.base[1];
-    cb2 = st.base[2];
-    have = true;
+    make_stencil(px, py, pz, g.origin, g.inv_dx, st);
+    if (!stencil_in_grid(g, st)) continue;  // finalize raises OutOfGrid
+    const int b2 = st.base[2];
+    if (st.base[0] != cb0 || st.base[1] != cb1 || b2 < z0 || b2 > z0 + 3) {
+      if (cb0 != INT_MIN) {
+#pragma unroll
+        for (int z = 0; z < 4; ++z)
+#pragma unroll
+          for (int i = 0; i < 9; ++i) {
+            if (acc[z][i] != 0.0) red_add(mi + node_index(g, cb0 + i / 3, cb1 + i % 3, z0 + z), acc[z][i]);
+            acc[z][i] = 0.0;
+          }
+      }
+      cb0 = st.base[0];
+      cb1 = st.base[1];
+      z0 = b2;
+    }
+    while (b2 > z0 + 1) {  // slide the 4-plane window up one plane
+#pragma unroll
+      for (int i = 0; i < 9; ++i)
+        if (acc[0][i] != 0.0) red_add(mi + node_index(g, cb0 + i / 3, cb1 + i % 3, z0), acc[0][i]);
+#pragma unroll
+      for (int z = 0; z < 3; ++z)
+#pragma unroll
+        for (int i = 0; i < 9; ++i) acc[z][i] = acc[z + 1][i];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) acc[3][i] = 0.0;
+      ++z0;
+    }
+    const bool up = b2 != z0;  // planes 1..3 instead of 0..2
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int b = 0; b < 3; ++b) {
         const double wab = st.w[0][a] * st.w[1][b];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[9 * a + 3 * b + c] += wab * st.w[2][c];
+        for (int c = 0; c < 3; ++c) {
+          const double w = wab * st.w[2][c];
+          if (up) acc[c + 1][3 * a + b] += w;
+          else acc[c][3 * a + b] += w;
+        }
       }
   }
-  flush();
+  if (kScatter && cb0 != INT_MIN) {
+#pragma unroll
+    for (int z = 0; z < 4; ++z)
+#pragma unroll
+      for (int i = 0; i < 9; ++i)
+        if (acc[z][i] != 0.0) red_add(mi + node_index(g, cb0 + i / 3, cb1 + i % 3, z0 + z), acc[z][i]);
+  }
 }
 
-// grid_update over the active window (engine.cpp:180-205).
-__global__ void k_grid_update(const double4* __restrict__ mp, double4* __restrict__ vel, Ctl* ctl,
-                              Geometry g) {
-  if (ctl->err_code) return;
+// ---------------------------------------------------------------------------
+// grid_update (engine.cpp:180-205)
+// ---------------------------------------------------------------------------
+template <bool kZero>
+__global__ void k_grid_update(double4* __restrict__ mp, double* __restrict__ mi,
+                              double4* __restrict__ vel, Ctl* ctl, Geometry g, double m_ind) {
+  if (stale(ctl, ctl->substep)) return;
   const int lx = ctl->win_lo[0], ly = ctl->win_lo[1], lz = ctl->win_lo[2];
   const int ny = ctl->win_hi[1] - ly, nz = ctl->win_hi[2] - lz;
   const int64_t total = static_cast<int64_t>(ctl->win_hi[0] - lx) * ny * nz;
+  const double u0 = ctl->ind_v[0], u1 = ctl->ind_v[1], u2 = ctl->ind_v[2];
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int k = lz + static_cast<int>(t % nz);
@@ -380,11 +650,20 @@ __global__ void k_grid_update(const double4* __restrict__ mp, double4* __restric
     const int i = lx + static_cast<int>(r / ny);
     const size_t nd = node_index(g, i, j, k);
     const double4 q = mp[nd];
+    const double wi = mi[nd];  // indenter weight sum: mass m_ind wi, momentum (m_ind wi) u
     double4 o = make_double4(0, 0, 0, 0);
-    if (q.x > 0.0) {
-      o.x = q.y / q.x;
-      o.y = q.z / q.x;
-      o.z = q.w / q.x;
+    double mass = q.x, p0 = q.y, p1 = q.z, p2 = q.w;
+    if (wi != 0.0) {
+      const double M = wi * m_ind;
+      mass += M;
+      p0 += M * u0;
+      p1 += M * u1;
+      p2 += M * u2;
+    }
+    if (mass > 0.0) {
+      o.x = p0 / mass;
+      o.y = p1 / mass;
+      o.z = p2 / mass;
       if (g.with_gravity) {
         o.x = o.x + g.gdt[0];
         o.y = o.y + g.gdt[1];
@@ -394,137 +673,129 @@ __global__ void k_grid_update(const double4* __restrict__ mp, double4* __restric
       if (j == 0 || j == g.res[1] - 1) o.y = 0.0;
       if (k == 0 || k == g.res[2] - 1) o.z = 0.0;
     }
-    vel[nd] = o;
+    // Nodes without mass keep their (finite) stale velocity: every G2P read of
+    // such a node carries B-spline weight exactly 0 (the particle's own
+    // scatter would have given it mass otherwise).
+    if (!kZero || mass > 0.0) vel[nd] = o;
+    if (kZero) {
+      if (q.x != 0.0 || q.y != 0.0 || q.z != 0.0 || q.w != 0.0) mp[nd] = make_double4(0, 0, 0, 0);
+      if (wi != 0.0) mi[nd] = 0.0;
+    }
   }
 }
 
-// grid_to_particle (engine.cpp:217-251), optionally fused with
-// apply_boundary's bottom pin (engine.cpp:262-263) and advect
-// (engine.cpp:275-279).
-template <bool kBoundary, bool kAdvect>
-__global__ void __launch_bounds__(256) k_g2p_gel(double* __restrict__ x, double* __restrict__ v,
-                                                 double* __restrict__ Cm, double* __restrict__ Fm,
-                                                 const uint8_t* __restrict__ tag, int64_t n,
-                                                 int64_t n_el, Ctl* ctl, Geometry g,
-                                                 const double4* __restrict__ vel) {
-  if (ctl->err_code) return;
-  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool active = p < n_el;
+// ---------------------------------------------------------------------------
+// grid_to_particle (+ apply_boundary + advect) [+ next particle_to_grid]
+// ---------------------------------------------------------------------------
+
+namespace {
+// engine.cpp:217-249 for one particle: v and C from the node velocities.
+__device__ __forceinline__ void g2p_gather(const Geometry& g, const double4* __restrict__ vel,
+                                           double px0, double px1, double px2, double* vv,
+                                           double* Cn) {
+  Stencil st;
+  make_stencil(px0, px1, px2, g.origin, g.inv_dx, st);
+  double v0 = 0, v1 = 0, vz = 0;
+  double b00 = 0, b01 = 0, b02 = 0, b10 = 0, b11 = 0, b12 = 0, b20 = 0, b21 = 0, b22 = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double wa = st.w[0][a];
+    const double da = a - st.fx[0];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const double wab = wa * st.w[1][b];
+      const double db = b - st.fx[1];
+      const double4* row = vel + node_index(g, st.base[0] + a, st.base[1] + b, st.base[2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double w = wab * st.w[2][c];
+        const double dc = c - st.fx[2];
+        const double2* q2 = reinterpret_cast<const double2*>(row + c);
+        const double2 qa = __ldg(q2), qb = __ldg(q2 + 1);
+        const double wv0 = w * qa.x, wv1 = w * qa.y, wv2 = w * qb.x;
+        v0 += wv0; v1 += wv1; vz += wv2;
+        b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
+        b10 += wv1 * da; b11 += wv1 * db; b12 += wv1 * dc;
+        b20 += wv2 * da; b21 += wv2 * db; b22 += wv2 * dc;
+      }
+    }
+  }
+  vv[0] = v0;
+  vv[1] = v1;
+  vv[2] = vz;
+  const double k = 4.0 * g.inv_dx;
+  Cn[0] = k * b00; Cn[1] = k * b01; Cn[2] = k * b02;
+  Cn[3] = k * b10; Cn[4] = k * b11; Cn[5] = k * b12;
+  Cn[6] = k * b20; Cn[7] = k * b21; Cn[8] = k * b22;
+}
+}  // namespace
+
+template <bool kBoundary, bool kAdvect, bool kLookahead>
+__global__ void __launch_bounds__(256, 2) k_g2p2g_gel(
+    double* __restrict__ x, double* __restrict__ v, double* __restrict__ Cm,
+    double* __restrict__ Fm, const uint8_t* __restrict__ tag, int64_t n, int64_t n_el, GelMap M,
+    Ctl* ctl, Geometry g, const double4* __restrict__ vel, double4* __restrict__ grid, double m,
+    double vol0) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  P2GTile& T = *reinterpret_cast<P2GTile*>(smem_raw);
+  const int s = ctl->substep;
+  if (stale_block(ctl, s)) return;
+  const int64_t p = gel_particle(M, n_el);
+  const bool active = p >= 0;
   double px0 = 0, px1 = 0, px2 = 0, v2 = 0;
+  double F[9], vv[3] = {0, 0, 0}, Cn[9];
   if (active) {
     px0 = x[p];
     px1 = x[n + p];
     px2 = x[2 * n + p];
-    Stencil st;
-    make_stencil(px0, px1, px2, g.origin, g.inv_dx, st);
-    double v0 = 0, v1 = 0, vz = 0;
-    double b00 = 0, b01 = 0, b02 = 0, b10 = 0, b11 = 0, b12 = 0, b20 = 0, b21 = 0, b22 = 0;
+    g2p_gather(g, vel, px0, px1, px2, vv, Cn);
+    double F0[9];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double wa = st.w[0][a];
-      const double da = a - st.fx[0];
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        const double wab = wa * st.w[1][b];
-        const double db = b - st.fx[1];
-        const double4* row = vel + node_index(g, st.base[0] + a, st.base[1] + b, st.base[2]);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double w = wab * st.w[2][c];
-          const double dc = c - st.fx[2];
-          const double2* q2 = reinterpret_cast<const double2*>(row + c);
-          const double2 qa = __ldg(q2), qb = __ldg(q2 + 1);
-          const double wv0 = w * qa.x, wv1 = w * qa.y, wv2 = w * qb.x;
-          v0 += wv0; v1 += wv1; vz += wv2;
-          b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
-          b10 += wv1 * da; b11 += wv1 * db; b12 += wv1 * dc;
-          b20 += wv2 * da; b21 += wv2 * db; b22 += wv2 * dc;
-        }
-      }
-    }
-    const double k = 4.0 * g.inv_dx;
-    const double Cn[9] = {k * b00, k * b01, k * b02, k * b10, k * b11, k * b12,
-                          k * b20, k * b21, k * b22};
-    double F[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) F[i] = Fm[i * n_el + p];
+    for (int i = 0; i < 9; ++i) F0[i] = Fm[i * n_el + p];
     double G[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
       for (int j = 0; j < 3; ++j) G[3 * i + j] = (i == j ? 1.0 : 0.0) + g.dt * Cn[3 * i + j];
-    double Fn[9];
-    matmul3(G, F, Fn);
+    matmul3(G, F0, F);  // F <- (I + dt C) F  (engine.cpp:250)
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
       Cm[i * n_el + p] = Cn[i];
-      Fm[i * n_el + p] = Fn[i];
+      Fm[i * n_el + p] = F[i];
     }
-    if (kBoundary && tag[p] == kElastomerBottom) { v0 = 0.0; v1 = 0.0; vz = 0.0; }
-    v[p] = v0;
-    v[n + p] = v1;
-    v[2 * n + p] = vz;
+    if (kBoundary && tag[p] == kElastomerBottom) vv[0] = vv[1] = vv[2] = 0.0;
+    v[p] = vv[0];
+    v[n + p] = vv[1];
+    v[2 * n + p] = vv[2];
     if (kAdvect) {
-      px0 = px0 + g.dt * v0;
-      px1 = px1 + g.dt * v1;
-      px2 = px2 + g.dt * vz;
+      px0 = advance(px0, g.dt, vv[0]);
+      px1 = advance(px1, g.dt, vv[1]);
+      px2 = advance(px2, g.dt, vv[2]);
       x[p] = px0;
       x[n + p] = px1;
       x[2 * n + p] = px2;
-      v2 = v0 * v0 + v1 * v1 + vz * vz;
+      v2 = vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2];
     }
   }
-  if (kAdvect) reduce_motion(ctl, active, v2, px0, px1, px2);
+  if (kAdvect) reduce_motion(&ctl->max_v2, ctl->bb_lo, ctl->bb_hi, active, v2, px0, px1, px2);
+  if (kLookahead) {
+    // particle_to_grid of substep s + 1 with the state just written.
+    P2GPayload q;
+    double J = 1.0;
+    bool go = active;
+    if (go) {
+      go = make_payload(g, ctl, s + 1, m, vol0, F, Cn, vv, px0, px1, px2, q, J);
+      if (go && !stencil_in_grid(g, q.st)) go = false;  // finalize raises OutOfGrid
+    }
+    reduce_min_detf(ctl, s + 1, go, J);
+    p2g_tile_scatter(T, go, q, m, g, grid);
+  }
 }
 
-// apply_boundary + advect for the indenter (engine.cpp:260-261, 275-279).
-// kUniform: all indenter velocities equal Ctl::ind_v (the per-particle v array
-// is not read or written; tg_download fills it in). apply_boundary makes the
-// velocity uniform, so after it the indenter is always in this mode.
-template <bool kBoundary, bool kAdvect, bool kUniform>
-__global__ void __launch_bounds__(256) k_ind_move(double* __restrict__ x, double* __restrict__ v,
-                                                  int64_t n, int64_t n_el, Ctl* ctl, Geometry g) {
-  if (ctl->err_code) return;
-  const int64_t p = n_el + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool active = p < n;
-  double v0, v1, vz;
-  if (kBoundary) {
-    v0 = ctl->vind[0];
-    v1 = ctl->vind[1];
-    vz = ctl->vind[2];
-  } else if (kUniform) {
-    v0 = ctl->ind_v[0];
-    v1 = ctl->ind_v[1];
-    vz = ctl->ind_v[2];
-  } else {
-    v0 = active ? v[p] : 0.0;
-    v1 = active ? v[n + p] : 0.0;
-    vz = active ? v[2 * n + p] : 0.0;
-  }
-  if (kBoundary && blockIdx.x == 0 && threadIdx.x == 0) {
-    // every thread read vind above; Ctl::ind_v is only read by later kernels
-    ctl->ind_v[0] = v0;
-    ctl->ind_v[1] = v1;
-    ctl->ind_v[2] = vz;
-  }
-  double px0 = 0, px1 = 0, px2 = 0, v2 = 0;
-  if (active && kAdvect) {
-    px0 = x[p] + g.dt * v0;
-    px1 = x[n + p] + g.dt * v1;
-    px2 = x[2 * n + p] + g.dt * vz;
-    x[p] = px0;
-    x[n + p] = px1;
-    x[2 * n + p] = px2;
-    v2 = v0 * v0 + v1 * v1 + vz * vz;
-  }
-  if (kAdvect) reduce_motion(ctl, active, v2, px0, px1, px2);
-}
-
-// Phase-API pieces (engine.cpp:254-286) that the fused step path folds into
-// k_g2p_gel / k_ind_move.
+// Phase-API pieces (engine.cpp:254-286).
 __global__ void k_gel_boundary(double* __restrict__ v, const uint8_t* __restrict__ tag, int64_t n,
                                int64_t n_el, Ctl* ctl) {
-  if (ctl->err_code) return;
+  if (stale(ctl, ctl->substep)) return;
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p < n_el && tag[p] == kElastomerBottom) {
     v[p] = 0.0;
@@ -535,33 +806,64 @@ __global__ void k_gel_boundary(double* __restrict__ v, const uint8_t* __restrict
 
 __global__ void k_gel_advect(double* __restrict__ x, const double* __restrict__ v, int64_t n,
                              int64_t n_el, Ctl* ctl, Geometry g) {
-  if (ctl->err_code) return;
+  if (stale_block(ctl, ctl->substep)) return;
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool active = p < n_el;
   double px0 = 0, px1 = 0, px2 = 0, v2 = 0;
   if (active) {
     const double v0 = v[p], v1 = v[n + p], vz = v[2 * n + p];
-    px0 = x[p] + g.dt * v0;
-    px1 = x[n + p] + g.dt * v1;
-    px2 = x[2 * n + p] + g.dt * vz;
+    px0 = advance(x[p], g.dt, v0);
+    px1 = advance(x[n + p], g.dt, v1);
+    px2 = advance(x[2 * n + p], g.dt, vz);
     x[p] = px0;
     x[n + p] = px1;
     x[2 * n + p] = px2;
     v2 = v0 * v0 + v1 * v1 + vz * vz;
   }
-  reduce_motion(ctl, active, v2, px0, px1, px2);
+  reduce_motion(&ctl->max_v2, ctl->bb_lo, ctl->bb_hi, active, v2, px0, px1, px2);
 }
 
-// End of particle_to_grid: publish StepDiagnostics::min_det_f (engine.cpp:177).
+// Indenter advect in phase mode with its current (possibly non-uniform)
+// velocity; the indenter bbox is recomputed afterwards by k_bbox.
+template <bool kUniform>
+__global__ void k_ind_advect(double* __restrict__ x, const double* __restrict__ v, int64_t n,
+                             int64_t n_el, Ctl* ctl, Geometry g) {
+  if (stale(ctl, ctl->substep)) return;
+  const int64_t p = n_el + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool active = p < n;
+  double v2 = 0;
+  if (active) {
+    const double v0 = kUniform ? ctl->ind_v[0] : v[p];
+    const double v1 = kUniform ? ctl->ind_v[1] : v[n + p];
+    const double vz = kUniform ? ctl->ind_v[2] : v[2 * n + p];
+    x[p] = advance(x[p], g.dt, v0);
+    x[n + p] = advance(x[n + p], g.dt, v1);
+    x[2 * n + p] = advance(x[2 * n + p], g.dt, vz);
+    v2 = v0 * v0 + v1 * v1 + vz * vz;
+  }
+  const double m = warp_max(active ? v2 : 0.0);
+  if ((threadIdx.x & 31) == 0 && m > 0.0)
+    atomicMax(&ctl->max_v2, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+__global__ void k_ind_boundary(Ctl* ctl) {
+  if (stale(ctl, ctl->substep)) return;
+  for (int a = 0; a < 3; ++a) ctl->ind_v[a] = ctl->vind[a];
+}
+
+// End of particle_to_grid in phase mode: publish min_det_f (engine.cpp:177).
 __global__ void k_p2g_done(Ctl* ctl) {
-  if (ctl->err_code) return;
-  ctl->diag_min_det_f = order_val(ctl->min_detf);
-  ctl->min_detf = order_key(1.0);
+  const int s = ctl->substep;
+  if (stale(ctl, s)) return;
+  ctl->diag_min_det_f = order_val(ctl->min_detf[s & 1]);
+  ctl->min_detf[s & 1] = order_key(1.0);
 }
 
-// Copies a node box [lo, hi) into dense staging buffers (tg_download_grid).
-__global__ void k_gather_box(const double4* __restrict__ mp, const double4* __restrict__ vel,
-                             Geometry g, int3 lo, int3 hi, double* __restrict__ mass,
+// Copies a node box [lo, hi) into dense staging buffers (tg_download_grid):
+// Grid::mass / momentum as the reference holds them (elastomer + indenter).
+__global__ void k_gather_box(const double4* __restrict__ mp, const double* __restrict__ mi,
+                             const double4* __restrict__ vel, const Ctl* ctl, Geometry g,
+                             double m_ind, int3 lo, int3 hi, double* __restrict__ mass,
                              double* __restrict__ mom, double* __restrict__ velo) {
   const int ny = hi.y - lo.y, nz = hi.z - lo.z;
   const int64_t total = static_cast<int64_t>(hi.x - lo.x) * ny * nz;
@@ -573,10 +875,15 @@ __global__ void k_gather_box(const double4* __restrict__ mp, const double4* __re
     const int i = lo.x + static_cast<int>(r / ny);
     const size_t nd = node_index(g, i, j, k);
     const double4 q = mp[nd];
+    const double M = mi[nd] * m_ind;
     const double4 u = vel[nd];
-    mass[t] = q.x;
-    mom[3 * t] = q.y; mom[3 * t + 1] = q.z; mom[3 * t + 2] = q.w;
-    velo[3 * t] = u.x; velo[3 * t + 1] = u.y; velo[3 * t + 2] = u.z;
+    mass[t] = q.x + M;
+    mom[3 * t] = q.y + M * ctl->ind_v[0];
+    mom[3 * t + 1] = q.z + M * ctl->ind_v[1];
+    mom[3 * t + 2] = q.w + M * ctl->ind_v[2];
+    velo[3 * t] = u.x;
+    velo[3 * t + 1] = u.y;
+    velo[3 * t + 2] = u.z;
   }
 }
 
@@ -586,45 +893,112 @@ __global__ void k_gather_box(const double4* __restrict__ mp, const double4* __re
 
 namespace {
 constexpr int kThreads = 256;
+constexpr int kIndChunk = 16;
+constexpr size_t kTileSmem = sizeof(P2GTile);
+
 inline unsigned blocks_for(int64_t n) {
-  return static_cast<unsigned>((n + kThreads - 1) / kThreads > 0 ? (n + kThreads - 1) / kThreads : 1);
+  const int64_t b = (n + kThreads - 1) / kThreads;
+  return static_cast<unsigned>(b > 0 ? b : 1);
+}
+inline unsigned window_blocks(int sms) { return static_cast<unsigned>(sms * 8); }
+
+GelMap gel_map(const DeviceSim& s) {
+  GelMap M;
+  for (int a = 0; a < 3; ++a) {
+    M.lat[a] = s.lat[a];
+    M.tile[a] = s.tile[a];
+    M.tiles[a] = s.tiles[a];
+  }
+  return M;
+}
+
+unsigned gel_blocks(const DeviceSim& s) {
+  if (s.lat[0] > 0) return static_cast<unsigned>(s.tiles[0] * s.tiles[1]);
+  return blocks_for(s.n_el);
+}
+
+void configure_once() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(k_p2g_gel_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kTileSmem));
+  cudaFuncSetAttribute(k_g2p2g_gel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kTileSmem));
+  done = true;
 }
 }  // namespace
 
-int launch_window(DeviceSim& s) {
-  k_reset<<<1, 1, 0, s.stream>>>(s.ctl);
-  k_bbox<<<blocks_for(s.n), kThreads, 0, s.stream>>>(s.x, s.n, s.ctl);
-  k_finalize<<<1, 1, 0, s.stream>>>(s.ctl, s.geo, kFinWindow);
-  s.kernel_launches += 3;
-  return 3;
+// Chooses the lattice-block CTA tiling of the elastomer (engine.cuh).
+void configure_gel_tiling(DeviceSim& s, int nx, int ny, int nz) {
+  configure_once();
+  if (nx <= 0 || ny <= 0 || nz <= 0 || static_cast<int64_t>(nx) * ny * nz != s.n_el ||
+      nz > kThreads) {
+    s.lat[0] = s.lat[1] = s.lat[2] = 0;
+    return;
+  }
+  s.lat[0] = nx;
+  s.lat[1] = ny;
+  s.lat[2] = nz;
+  const int cols = kThreads / nz > 0 ? kThreads / nz : 1;
+  int ti = 1;
+  while ((ti + 1) * (ti + 1) <= cols) ++ti;
+  const int tj = cols / ti > 0 ? cols / ti : 1;
+  s.tile[0] = ti;
+  s.tile[1] = tj;
+  s.tile[2] = nz;
+  s.tiles[0] = (nx + ti - 1) / ti;
+  s.tiles[1] = (ny + tj - 1) / tj;
+  s.tiles[2] = 1;
 }
 
-static unsigned window_blocks(int sm_count) { return static_cast<unsigned>(sm_count * 8); }
+int launch_reset(DeviceSim& s, int mask) {
+  k_reset<<<1, 1, 0, s.stream>>>(s.ctl, mask);
+  s.kernel_launches += 1;
+  return 1;
+}
+
+// zero_grid's window from the current positions (both bboxes recomputed).
+int launch_window(DeviceSim& s) {
+  configure_once();
+  int k = launch_reset(s, kResetMotion | kResetIndBox | kResetDetF);
+  if (s.n_el > 0) {
+    k_bbox<<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(s.x, s.n, 0, s.n_el, s.ctl, 0);
+    ++k;
+  }
+  if (s.n_ind > 0) {
+    k_bbox<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.n, s.ctl, 1);
+    ++k;
+  }
+  k_finalize<<<1, 1, 0, s.stream>>>(s.ctl, s.geo, kFinWindow);
+  s.kernel_launches += k;  // reset counted in launch_reset
+  return k + 1;
+}
 
 int launch_clear(DeviceSim& s, int sms) {
-  k_clear<<<window_blocks(sms), kThreads, 0, s.stream>>>(s.grid_mp, s.ctl, s.geo);
+  k_clear<<<window_blocks(sms), kThreads, 0, s.stream>>>(s.grid_mp, s.grid_mi, s.ctl, s.geo);
   s.kernel_launches += 1;
+  s.grid_dirty = false;
   return 1;
 }
 
 int launch_p2g_gel(DeviceSim& s) {
   if (s.n_el <= 0) return 0;
-  k_p2g_gel<<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(s.x, s.v, s.C, s.F, s.n, s.n_el, s.ctl,
-                                                           s.geo, s.grid_mp, s.m_el, s.vol_el);
+  configure_once();
+  k_p2g_gel_tile<<<gel_blocks(s), kThreads, kTileSmem, s.stream>>>(
+      s.x, s.v, s.C, s.F, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_mp, s.m_el, s.vol_el);
   s.kernel_launches += 1;
   return 1;
 }
 
-constexpr int kIndChunk = 16;
-
 int launch_p2g_ind(DeviceSim& s) {
   if (s.n_ind <= 0) return 0;
   if (s.ind_v_uniform)
-    k_p2g_ind_chunk<kIndChunk><<<blocks_for((s.n_ind + kIndChunk - 1) / kIndChunk), kThreads, 0,
-                                 s.stream>>>(s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mp, s.m_ind);
+    k_ind_move_p2g<kIndChunk, false, true>
+        <<<blocks_for((s.n_ind + kIndChunk - 1) / kIndChunk), kThreads, 0, s.stream>>>(
+            s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   else
-    k_p2g_ind<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el, s.ctl, s.geo,
-                                                              s.grid_mp, s.m_ind);
+    k_p2g_ind_direct<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el, s.ctl,
+                                                                     s.geo, s.grid_mp, s.m_ind);
   s.kernel_launches += 1;
   return 1;
 }
@@ -636,90 +1010,112 @@ int launch_p2g(DeviceSim& s, bool publish_diag) {
     s.kernel_launches += 1;
     ++k;
   }
+  s.grid_dirty = true;
   return k;
 }
 
-int launch_grid_update(DeviceSim& s, int sms) {
-  k_grid_update<<<window_blocks(sms), kThreads, 0, s.stream>>>(s.grid_mp, s.grid_v, s.ctl, s.geo);
+int launch_grid_update(DeviceSim& s, int sms, bool zero) {
+  if (zero)
+    k_grid_update<true><<<window_blocks(sms), kThreads, 0, s.stream>>>(
+        s.grid_mp, s.grid_mi, s.grid_v, s.ctl, s.geo, s.m_ind);
+  else
+    k_grid_update<false><<<window_blocks(sms), kThreads, 0, s.stream>>>(
+        s.grid_mp, s.grid_mi, s.grid_v, s.ctl, s.geo, s.m_ind);
   s.kernel_launches += 1;
   return 1;
 }
 
-int launch_g2p_gel_move(DeviceSim& s) {
+// G2P + boundary + advect for the elastomer, with the look-ahead scatter.
+int launch_g2p2g_gel(DeviceSim& s, bool lookahead) {
   if (s.n_el <= 0) return 0;
-  k_g2p_gel<true, true><<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(
-      s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, s.ctl, s.geo, s.grid_v);
+  configure_once();
+  if (lookahead)
+    k_g2p2g_gel<true, true, true><<<gel_blocks(s), kThreads, kTileSmem, s.stream>>>(
+        s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
+        s.m_el, s.vol_el);
+  else
+    k_g2p2g_gel<true, true, false><<<gel_blocks(s), kThreads, 0, s.stream>>>(
+        s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
+        s.m_el, s.vol_el);
   s.kernel_launches += 1;
   return 1;
 }
 
-int launch_ind_move(DeviceSim& s) {
+int launch_ind_move(DeviceSim& s, bool lookahead) {
   if (s.n_ind <= 0) return 0;
-  k_ind_move<true, true, true><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(
-      s.x, s.v, s.n, s.n_el, s.ctl, s.geo);
+  const unsigned blocks = blocks_for((s.n_ind + kIndChunk - 1) / kIndChunk);
+  if (lookahead)
+    k_ind_move_p2g<kIndChunk, true, true><<<blocks, kThreads, 0, s.stream>>>(
+        s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
+  else
+    k_ind_move_p2g<kIndChunk, true, false><<<blocks, kThreads, 0, s.stream>>>(
+        s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   s.ind_v_uniform = true;
   s.kernel_launches += 1;
   return 1;
 }
 
 int launch_finalize_step(DeviceSim& s) {
-  k_finalize<<<1, 1, 0, s.stream>>>(s.ctl, s.geo, kFinDiag | kFinAdvect | kFinWindow);
+  k_finalize<<<1, 1, 0, s.stream>>>(
+      s.ctl, s.geo, kFinDiag | kFinAdvect | kFinWindow | (s.n_ind > 0 ? kFinIndShift : 0));
   s.kernel_launches += 1;
   return 1;
 }
 
-// Fused G2P + boundary + advect + finalize (the step path).
-int launch_g2p_move(DeviceSim& s) {
-  return launch_g2p_gel_move(s) + launch_ind_move(s) + launch_finalize_step(s);
-}
-
 int launch_phase_g2p(DeviceSim& s) {
-  if (s.n_el > 0)
-    k_g2p_gel<false, false><<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(
-        s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, s.ctl, s.geo, s.grid_v);
+  if (s.n_el <= 0) return 0;
+  k_g2p2g_gel<false, false, false><<<gel_blocks(s), kThreads, 0, s.stream>>>(
+      s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
+      s.m_el, s.vol_el);
   s.kernel_launches += 1;
   return 1;
 }
 
 int launch_phase_boundary(DeviceSim& s) {
-  if (s.n_el > 0)
+  int k = 0;
+  if (s.n_el > 0) {
     k_gel_boundary<<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(s.v, s.tag, s.n, s.n_el, s.ctl);
-  if (s.n_ind > 0)
-    k_ind_move<true, false, true><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(
-        s.x, s.v, s.n, s.n_el, s.ctl, s.geo);
-  if (s.n_ind > 0) s.ind_v_uniform = true;
-  s.kernel_launches += 2;
-  return 2;
+    ++k;
+  }
+  if (s.n_ind > 0) {
+    k_ind_boundary<<<1, 1, 0, s.stream>>>(s.ctl);
+    s.ind_v_uniform = true;
+    ++k;
+  }
+  s.kernel_launches += k;
+  return k;
 }
 
+// advect (engine.cpp:268-286) in phase mode: move, recompute the indenter box,
+// then finalize's in_range check.
 int launch_phase_advect(DeviceSim& s) {
-  if (s.n_el > 0)
+  int k = 0;
+  if (s.n_el > 0) {
     k_gel_advect<<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el, s.ctl,
                                                                 s.geo);
-  if (s.n_ind > 0)
-  {
+    ++k;
+  }
+  if (s.n_ind > 0) {
     if (s.ind_v_uniform)
-      k_ind_move<false, true, true><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(
-          s.x, s.v, s.n, s.n_el, s.ctl, s.geo);
+      k_ind_advect<true><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el,
+                                                                        s.ctl, s.geo);
     else
-      k_ind_move<false, true, false><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(
-          s.x, s.v, s.n, s.n_el, s.ctl, s.geo);
+      k_ind_advect<false><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el,
+                                                                         s.ctl, s.geo);
+    k_reset<<<1, 1, 0, s.stream>>>(s.ctl, kResetIndBox);
+    k_bbox<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.n, s.ctl, 1);
+    k += 3;
   }
   k_finalize<<<1, 1, 0, s.stream>>>(s.ctl, s.geo, kFinAdvect);
-  s.kernel_launches += 3;
-  return 3;
-}
-
-int launch_reset(DeviceSim& s) {
-  k_reset<<<1, 1, 0, s.stream>>>(s.ctl);
-  s.kernel_launches += 1;
-  return 1;
+  ++k;
+  s.kernel_launches += k;
+  return k;
 }
 
 int launch_gather_box(DeviceSim& s, const int lo[3], const int hi[3], double* mass, double* mom,
                       double* vel) {
-  k_gather_box<<<1024, kThreads, 0, s.stream>>>(s.grid_mp, s.grid_v, s.geo,
-                                                make_int3(lo[0], lo[1], lo[2]),
+  k_gather_box<<<1024, kThreads, 0, s.stream>>>(s.grid_mp, s.grid_mi, s.grid_v, s.ctl, s.geo,
+                                                s.m_ind, make_int3(lo[0], lo[1], lo[2]),
                                                 make_int3(hi[0], hi[1], hi[2]), mass, mom, vel);
   s.kernel_launches += 1;
   return 1;
