@@ -305,7 +305,12 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
   CUDA_TRY(cudaMemsetAsync(&s.ctl->err_code, 0, sizeof(int), s.stream));
   launch_reset(s, kResetAll);
   s.window_valid = false;
-  s.grid_dirty = true;  // a look-ahead scatter may have started
+  // A look-ahead scatter may have started anywhere in the grid: reset the
+  // accumulators wholesale (errors are rare; this keeps the invariant simple).
+  CUDA_TRY(cudaMemsetAsync(s.grid_mp, 0, s.n_nodes * sizeof(double4), s.stream));
+  CUDA_TRY(cudaMemsetAsync(s.grid_mi, 0, s.n_nodes * sizeof(double), s.stream));
+  s.grid_dirty = false;
+  s.grid_ready = false;
   CUDA_TRY(cudaStreamSynchronize(s.stream));
   if (at >= end_substep) return TG_OK;
   const char* what = code == kErrOutOfGrid
@@ -318,13 +323,19 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
 // scatter for the first substep, then per substep grid_update (re-zeroing the
 // accumulators) and the fused G2P(+boundary+advect)+look-ahead-P2G kernels;
 // the last substep does no look-ahead.
+// When the previous call already scattered this call's first substep
+// (grid_ready), the standalone scatter is skipped; every substep, the last one
+// included, scatters the next substep's particles, so consecutive step() calls
+// chain without a standalone scatter.
 static int record_substeps(DeviceSim& s, int n_substeps) {
   int k = 0;
   const int sms = sm_count(s.device);
-  if (s.grid_dirty) k += launch_clear(s, sms);
-  k += launch_p2g_gel(s) + launch_p2g_ind(s);
+  if (!s.grid_ready) {
+    if (s.grid_dirty) k += launch_clear(s, sms);
+    k += launch_p2g_gel(s) + launch_p2g_ind(s);
+  }
   for (int i = 0; i < n_substeps; ++i) {
-    const bool lookahead = i + 1 < n_substeps;
+    const bool lookahead = true;
     k += launch_grid_update(s, sms, true);
     k += launch_g2p2g_gel(s, lookahead);
     k += launch_ind_move(s, lookahead);
@@ -344,7 +355,8 @@ int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
   if (!s.window_valid) launch_window(s);
   s.window_valid = true;
   if (s.use_graphs) {
-    const int key = n_substeps * 4 + (s.grid_dirty ? 1 : 0) + (s.ind_v_uniform ? 2 : 0);
+    const int key = n_substeps * 8 + (s.grid_dirty ? 1 : 0) + (s.ind_v_uniform ? 2 : 0) +
+                    (s.grid_ready ? 4 : 0);
     auto it = s.graphs.find(key);
     if (it == s.graphs.end()) {
       cudaGraph_t graph;
@@ -363,13 +375,14 @@ int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
     }
     CUDA_TRY(cudaGraphLaunch(it->second, s.stream));
     s.kernel_launches += s.graph_kernels[key];
-    s.grid_dirty = false;
-    s.ind_v_uniform = true;
   } else {
     CUDA_TRY(cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double),
                              cudaMemcpyHostToDevice, s.stream));
     record_substeps(s, n_substeps);
   }
+  s.grid_dirty = false;
+  s.ind_v_uniform = true;
+  s.grid_ready = true;
   return TG_OK;
 }
 
@@ -405,6 +418,10 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
   s.window_valid = true;
   CUDA_TRY(cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double), cudaMemcpyHostToDevice,
                            s.stream));
+  if (s.grid_ready) {  // discard the previous call's look-ahead scatter
+    s.grid_ready = false;
+    s.grid_dirty = true;
+  }
   if (s.grid_dirty) launch_clear(s, sms);
   float ms = 0.f;
   cudaEventRecord(ev[0], s.stream);
@@ -443,6 +460,10 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
 
 int phase(DeviceSim& s, int ph, const double vind[3]) {
   CUDA_TRY(cudaSetDevice(s.device));
+  if (s.grid_ready) {  // phases drive zero_grid / P2G themselves
+    s.grid_ready = false;
+    s.grid_dirty = true;
+  }
   const int start = s.host_substep;
   const int sms = sm_count(s.device);
   switch (ph) {
@@ -516,6 +537,10 @@ int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, con
   if ((Cm || init) && (rc = put9(Cm, s.C, false))) return rc;
   if ((Fm || init) && (rc = put9(Fm, s.F, true))) return rc;
   s.window_valid = false;
+  if (s.grid_ready) {  // the look-ahead scatter used the old state
+    s.grid_ready = false;
+    s.grid_dirty = true;
+  }
   return TG_OK;
 }
 

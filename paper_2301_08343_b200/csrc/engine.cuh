@@ -27,6 +27,7 @@ struct Ctl {
   int win_lo[3], win_hi[3];               // Grid::active_lo/hi
   int prev_lo[3], prev_hi[3];             // Grid::prev_lo/hi
   int clr_lo[3], clr_hi[3];               // node box to clear before P2G
+  int box_lo[2][3], box_hi[2][3];         // per-material node boxes (elastomer, indenter)
   double vind[3];                         // commanded indenter velocity
   double ind_v[3];                        // uniform indenter velocity (P2G input)
   double diag_min_det_f, diag_max_speed;  // StepDiagnostics
@@ -72,6 +73,8 @@ struct DeviceSim {
   int tile[3] = {0, 0, 0};   // lattice block per CTA (ti, tj, tk)
   int tiles[3] = {0, 0, 0};  // blocks per axis
   bool grid_dirty = false;   // A / M_I may hold a phase-mode P2G (needs k_clear)
+  bool grid_ready = false;   // A / M_I hold the scatter of the next substep (look-ahead
+                             // of the previous mpm::step call); skip the standalone P2G
 
   // Surface lattice (sim_state.hpp:41-52) + capture scratch.
   int surf_nx = 0, surf_ny = 0;

@@ -446,6 +446,22 @@ __global__ void k_finalize(Ctl* ctl, Geometry g, int mode) {
       wlo[a] = b0;
       whi[a] = b1 + 3;
     }
+    // The two materials' own node boxes: grid_update only needs their union
+    // (the stretch of the combined window between the gel and the indenter
+    // holds no mass). An empty set gives an empty box.
+    for (int a = 0; a < 3; ++a) {
+      const double l[2] = {order_val(ctl->bb_lo[a]), order_val(ctl->ind_lo[a])};
+      const double h[2] = {order_val(ctl->bb_hi[a]), order_val(ctl->ind_hi[a])};
+      for (int m = 0; m < 2; ++m) {
+        if (l[m] <= h[m]) {
+          ctl->box_lo[m][a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(l[m], g.origin[a]), g.inv_dx), 0.5)));
+          ctl->box_hi[m][a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(h[m], g.origin[a]), g.inv_dx), 0.5))) + 3;
+        } else {
+          ctl->box_lo[m][a] = 0;
+          ctl->box_hi[m][a] = 0;
+        }
+      }
+    }
     int pmin = 1 << 30;
     for (int a = 0; a < 3; ++a) pmin = min(pmin, ctl->prev_hi[a] - ctl->prev_lo[a]);
     for (int a = 0; a < 3; ++a) {
@@ -537,37 +553,43 @@ __global__ void __launch_bounds__(256) k_p2g_ind_direct(const double* __restrict
 }
 
 // Rigid indenter: optional apply_boundary + advect (kMove) and the scatter of
-// the (next) substep (kScatter). A thread walks kChunk consecutive particles
-// of the (bx, by, z)-sorted cloud; the B-spline weight sums of the last four
-// z-planes of a 3x3 column are kept in registers and a plane is flushed (one
+// the (next) substep (kScatter). A CTA owns kIndThreads * kChunk consecutive
+// particles of the (bx, by, z)-sorted cloud: it moves them with coalesced
+// loads/stores and stages the new positions in shared memory; then each thread
+// walks kChunk consecutive particles, keeping the B-spline weight sums of the
+// last four z-planes of its 3x3 column in registers, and flushes a plane (one
 // RED.F64 per node, into M_I) only when the run leaves it.
+constexpr int kIndThreads = 128;
+
+__device__ __forceinline__ int ind_pad(int e) { return e + (e >> 4); }  // 2-way max bank conflict
+
 template <int kChunk, bool kMove, bool kScatter>
-__global__ void __launch_bounds__(256) k_ind_move_p2g(double* __restrict__ x, int64_t n,
-                                                      int64_t n_el, Ctl* ctl, Geometry g,
-                                                      double* __restrict__ mi) {
+__global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict__ x, int64_t n,
+                                                              int64_t n_el, Ctl* ctl, Geometry g,
+                                                              double* __restrict__ mi) {
+  constexpr int kSeg = kIndThreads * kChunk;
+  constexpr int kPadded = kSeg + kSeg / 16;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* xs = reinterpret_cast<double*>(smem_raw);  // [3][kPadded]
   const int s = ctl->substep;
-  if (stale(ctl, s)) return;
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t p0 = n_el + t * kChunk;
-  if (kMove && t == 0) {
+  if (stale(ctl, s)) return;  // stable: nothing raises for substep s while this runs
+  const int tid = threadIdx.x;
+  const int64_t seg0 = n_el + static_cast<int64_t>(blockIdx.x) * kSeg;
+  if (kMove && blockIdx.x == 0 && tid == 0) {
     // apply_boundary: every indenter velocity becomes the command
     // (engine.cpp:260-261); the next grid_update uses it as M_I's velocity.
     ctl->ind_v[0] = ctl->vind[0];
     ctl->ind_v[1] = ctl->vind[1];
     ctl->ind_v[2] = ctl->vind[2];
   }
-  if (p0 >= n) return;
-  const int64_t p1 = p0 + kChunk < n ? p0 + kChunk : n;
   double d[3] = {0, 0, 0};
   if (kMove)
     for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
-  double acc[4][9];
-#pragma unroll
-  for (int z = 0; z < 4; ++z)
-#pragma unroll
-    for (int i = 0; i < 9; ++i) acc[z][i] = 0.0;
-  int cb0 = INT_MIN, cb1 = INT_MIN, z0 = INT_MIN;
-  for (int64_t p = p0; p < p1; ++p) {
+#pragma unroll 4
+  for (int i = 0; i < kChunk; ++i) {
+    const int e = i * kIndThreads + tid;
+    const int64_t p = seg0 + e;
+    if (p >= n) break;
     double px = x[p], py = x[n + p], pz = x[2 * n + p];
     if (kMove) {
       px = add_rn(px, d[0]);
@@ -577,9 +599,27 @@ __global__ void __launch_bounds__(256) k_ind_move_p2g(double* __restrict__ x, in
       x[n + p] = py;
       x[2 * n + p] = pz;
     }
-    if (!kScatter) continue;
+    if (kScatter) {
+      xs[ind_pad(e)] = px;
+      xs[kPadded + ind_pad(e)] = py;
+      xs[2 * kPadded + ind_pad(e)] = pz;
+    }
+  }
+  if (!kScatter) return;
+  __syncthreads();
+  const int64_t seg_len = n - seg0 < kSeg ? n - seg0 : kSeg;
+  const int e0 = tid * kChunk;
+  const int e1 = e0 + kChunk < seg_len ? e0 + kChunk : static_cast<int>(seg_len);
+  double acc[4][9];
+#pragma unroll
+  for (int z = 0; z < 4; ++z)
+#pragma unroll
+    for (int i = 0; i < 9; ++i) acc[z][i] = 0.0;
+  int cb0 = INT_MIN, cb1 = INT_MIN, z0 = INT_MIN;
+  for (int e = e0; e < e1; ++e) {
     Stencil st;
-    make_stencil(px, py, pz, g.origin, g.inv_dx, st);
+    make_stencil(xs[ind_pad(e)], xs[kPadded + ind_pad(e)], xs[2 * kPadded + ind_pad(e)], g.origin,
+                 g.inv_dx, st);
     if (!stencil_in_grid(g, st)) continue;  // finalize raises OutOfGrid
     const int b2 = st.base[2];
     if (st.base[0] != cb0 || st.base[1] != cb1 || b2 < z0 || b2 > z0 + 3) {
@@ -622,7 +662,7 @@ __global__ void __launch_bounds__(256) k_ind_move_p2g(double* __restrict__ x, in
         }
       }
   }
-  if (kScatter && cb0 != INT_MIN) {
+  if (cb0 != INT_MIN) {
 #pragma unroll
     for (int z = 0; z < 4; ++z)
 #pragma unroll
@@ -634,9 +674,52 @@ __global__ void __launch_bounds__(256) k_ind_move_p2g(double* __restrict__ x, in
 // ---------------------------------------------------------------------------
 // grid_update (engine.cpp:180-205)
 // ---------------------------------------------------------------------------
+// Node update shared by both traversals; kZero also re-zeroes A / M_I.
 template <bool kZero>
-__global__ void k_grid_update(double4* __restrict__ mp, double* __restrict__ mi,
-                              double4* __restrict__ vel, Ctl* ctl, Geometry g, double m_ind) {
+__device__ __forceinline__ void update_node(double4* __restrict__ mp, double* __restrict__ mi,
+                                            double4* __restrict__ vel, const Geometry& g,
+                                            double m_ind, double u0, double u1, double u2, int i,
+                                            int j, int k) {
+  const size_t nd = node_index(g, i, j, k);
+  const double4 q = mp[nd];
+  const double wi = mi[nd];  // indenter weight sum: mass m_ind wi, momentum (m_ind wi) u
+  double4 o = make_double4(0, 0, 0, 0);
+  double mass = q.x, p0 = q.y, p1 = q.z, p2 = q.w;
+  if (wi != 0.0) {
+    const double M = wi * m_ind;
+    mass += M;
+    p0 += M * u0;
+    p1 += M * u1;
+    p2 += M * u2;
+  }
+  if (mass > 0.0) {
+    o.x = p0 / mass;
+    o.y = p1 / mass;
+    o.z = p2 / mass;
+    if (g.with_gravity) {
+      o.x = o.x + g.gdt[0];
+      o.y = o.y + g.gdt[1];
+      o.z = o.z + g.gdt[2];
+    }
+    if (i == 0 || i == g.res[0] - 1) o.x = 0.0;
+    if (j == 0 || j == g.res[1] - 1) o.y = 0.0;
+    if (k == 0 || k == g.res[2] - 1) o.z = 0.0;
+  }
+  // Step path: nodes without mass keep their (finite) stale velocity; every
+  // G2P read of such a node carries B-spline weight exactly 0 (the particle's
+  // own scatter would have given it mass otherwise).
+  if (!kZero || mass > 0.0) vel[nd] = o;
+  if (kZero) {
+    if (q.x != 0.0 || q.y != 0.0 || q.z != 0.0 || q.w != 0.0) mp[nd] = make_double4(0, 0, 0, 0);
+    if (wi != 0.0) mi[nd] = 0.0;
+  }
+}
+
+// Phase API: the full active window, as the reference (Grid::velocity is 0
+// on every massless window node).
+__global__ void k_grid_update_window(double4* __restrict__ mp, double* __restrict__ mi,
+                                     double4* __restrict__ vel, Ctl* ctl, Geometry g,
+                                     double m_ind) {
   if (stale(ctl, ctl->substep)) return;
   const int lx = ctl->win_lo[0], ly = ctl->win_lo[1], lz = ctl->win_lo[2];
   const int ny = ctl->win_hi[1] - ly, nz = ctl->win_hi[2] - lz;
@@ -646,41 +729,41 @@ __global__ void k_grid_update(double4* __restrict__ mp, double* __restrict__ mi,
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int k = lz + static_cast<int>(t % nz);
     const int64_t r = t / nz;
-    const int j = ly + static_cast<int>(r % ny);
-    const int i = lx + static_cast<int>(r / ny);
-    const size_t nd = node_index(g, i, j, k);
-    const double4 q = mp[nd];
-    const double wi = mi[nd];  // indenter weight sum: mass m_ind wi, momentum (m_ind wi) u
-    double4 o = make_double4(0, 0, 0, 0);
-    double mass = q.x, p0 = q.y, p1 = q.z, p2 = q.w;
-    if (wi != 0.0) {
-      const double M = wi * m_ind;
-      mass += M;
-      p0 += M * u0;
-      p1 += M * u1;
-      p2 += M * u2;
+    update_node<false>(mp, mi, vel, g, m_ind, u0, u1, u2, lx + static_cast<int>(r / ny),
+                       ly + static_cast<int>(r % ny), k);
+  }
+}
+
+// Step path: only the union of the elastomer and indenter node boxes (every
+// node a scatter can have touched), re-zeroing the accumulators.
+__global__ void k_grid_update_boxes(double4* __restrict__ mp, double* __restrict__ mi,
+                                    double4* __restrict__ vel, Ctl* ctl, Geometry g,
+                                    double m_ind) {
+  if (stale(ctl, ctl->substep)) return;
+  int lo[2][3], dm[2][3];
+  int64_t vol[2];
+  for (int m = 0; m < 2; ++m) {
+    vol[m] = 1;
+    for (int a = 0; a < 3; ++a) {
+      lo[m][a] = ctl->box_lo[m][a];
+      dm[m][a] = max(ctl->box_hi[m][a] - lo[m][a], 0);
+      vol[m] *= dm[m][a];
     }
-    if (mass > 0.0) {
-      o.x = p0 / mass;
-      o.y = p1 / mass;
-      o.z = p2 / mass;
-      if (g.with_gravity) {
-        o.x = o.x + g.gdt[0];
-        o.y = o.y + g.gdt[1];
-        o.z = o.z + g.gdt[2];
-      }
-      if (i == 0 || i == g.res[0] - 1) o.x = 0.0;
-      if (j == 0 || j == g.res[1] - 1) o.y = 0.0;
-      if (k == 0 || k == g.res[2] - 1) o.z = 0.0;
-    }
-    // Nodes without mass keep their (finite) stale velocity: every G2P read of
-    // such a node carries B-spline weight exactly 0 (the particle's own
-    // scatter would have given it mass otherwise).
-    if (!kZero || mass > 0.0) vel[nd] = o;
-    if (kZero) {
-      if (q.x != 0.0 || q.y != 0.0 || q.z != 0.0 || q.w != 0.0) mp[nd] = make_double4(0, 0, 0, 0);
-      if (wi != 0.0) mi[nd] = 0.0;
-    }
+  }
+  const double u0 = ctl->ind_v[0], u1 = ctl->ind_v[1], u2 = ctl->ind_v[2];
+  const int64_t total = vol[0] + vol[1];
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int m = t < vol[0] ? 0 : 1;
+    const int64_t u = m == 0 ? t : t - vol[0];
+    const int k = lo[m][2] + static_cast<int>(u % dm[m][2]);
+    const int64_t r = u / dm[m][2];
+    const int j = lo[m][1] + static_cast<int>(r % dm[m][1]);
+    const int i = lo[m][0] + static_cast<int>(r / dm[m][1]);
+    if (m == 1 && vol[0] > 0 && i >= lo[0][0] && i < lo[0][0] + dm[0][0] && j >= lo[0][1] &&
+        j < lo[0][1] + dm[0][1] && k >= lo[0][2] && k < lo[0][2] + dm[0][2])
+      continue;  // already handled in the elastomer box
+    update_node<true>(mp, mi, vel, g, m_ind, u0, u1, u2, i, j, k);
   }
 }
 
@@ -895,6 +978,8 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kIndChunk = 16;
 constexpr size_t kTileSmem = sizeof(P2GTile);
+constexpr size_t kIndSmem =
+    3 * sizeof(double) * (kIndThreads * kIndChunk + kIndThreads * kIndChunk / 16);
 
 inline unsigned blocks_for(int64_t n) {
   const int64_t b = (n + kThreads - 1) / kThreads;
@@ -924,6 +1009,10 @@ void configure_once() {
                        static_cast<int>(kTileSmem));
   cudaFuncSetAttribute(k_g2p2g_gel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(kTileSmem));
+  cudaFuncSetAttribute(k_ind_move_p2g<kIndChunk, false, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIndSmem));
+  cudaFuncSetAttribute(k_ind_move_p2g<kIndChunk, true, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIndSmem));
   done = true;
 }
 }  // namespace
@@ -990,12 +1079,17 @@ int launch_p2g_gel(DeviceSim& s) {
   return 1;
 }
 
+inline unsigned ind_blocks(const DeviceSim& s) {
+  const int64_t seg = static_cast<int64_t>(kIndThreads) * kIndChunk;
+  return static_cast<unsigned>((s.n_ind + seg - 1) / seg);
+}
+
 int launch_p2g_ind(DeviceSim& s) {
   if (s.n_ind <= 0) return 0;
+  configure_once();
   if (s.ind_v_uniform)
-    k_ind_move_p2g<kIndChunk, false, true>
-        <<<blocks_for((s.n_ind + kIndChunk - 1) / kIndChunk), kThreads, 0, s.stream>>>(
-            s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
+    k_ind_move_p2g<kIndChunk, false, true><<<ind_blocks(s), kIndThreads, kIndSmem, s.stream>>>(
+        s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   else
     k_p2g_ind_direct<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el, s.ctl,
                                                                      s.geo, s.grid_mp, s.m_ind);
@@ -1016,10 +1110,10 @@ int launch_p2g(DeviceSim& s, bool publish_diag) {
 
 int launch_grid_update(DeviceSim& s, int sms, bool zero) {
   if (zero)
-    k_grid_update<true><<<window_blocks(sms), kThreads, 0, s.stream>>>(
+    k_grid_update_boxes<<<window_blocks(sms), kThreads, 0, s.stream>>>(
         s.grid_mp, s.grid_mi, s.grid_v, s.ctl, s.geo, s.m_ind);
   else
-    k_grid_update<false><<<window_blocks(sms), kThreads, 0, s.stream>>>(
+    k_grid_update_window<<<window_blocks(sms), kThreads, 0, s.stream>>>(
         s.grid_mp, s.grid_mi, s.grid_v, s.ctl, s.geo, s.m_ind);
   s.kernel_launches += 1;
   return 1;
@@ -1043,12 +1137,12 @@ int launch_g2p2g_gel(DeviceSim& s, bool lookahead) {
 
 int launch_ind_move(DeviceSim& s, bool lookahead) {
   if (s.n_ind <= 0) return 0;
-  const unsigned blocks = blocks_for((s.n_ind + kIndChunk - 1) / kIndChunk);
+  configure_once();
   if (lookahead)
-    k_ind_move_p2g<kIndChunk, true, true><<<blocks, kThreads, 0, s.stream>>>(
+    k_ind_move_p2g<kIndChunk, true, true><<<ind_blocks(s), kIndThreads, kIndSmem, s.stream>>>(
         s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   else
-    k_ind_move_p2g<kIndChunk, true, false><<<blocks, kThreads, 0, s.stream>>>(
+    k_ind_move_p2g<kIndChunk, true, false><<<ind_blocks(s), kIndThreads, 0, s.stream>>>(
         s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   s.ind_v_uniform = true;
   s.kernel_launches += 1;
