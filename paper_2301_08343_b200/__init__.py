@@ -19,7 +19,7 @@ from types import SimpleNamespace
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libtacchi_cuda.so")
+LIB_PATH = os.environ.get("TACCHI_LIB") or os.path.join(_HERE, "_lib", "libtacchi_cuda.so")
 
 # ---------------------------------------------------------------------------
 # Errors (errors.hpp:9-39)

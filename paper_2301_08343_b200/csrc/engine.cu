@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -179,6 +180,7 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   g.with_gravity = (P->gravity[0] * P->gravity[0] + P->gravity[1] * P->gravity[1] +
                     P->gravity[2] * P->gravity[2]) > 0.0;
   g.stress_scale = -P->dt * 4.0 * g.inv_dx * g.inv_dx;
+  if (const char* m = std::getenv("TACCHI_SCATTER")) g.scatter_mode = std::atoi(m);
 
   // Indenter particles are re-ordered by base cell so that P2G scatters from
   // neighbouring lanes hit neighbouring nodes; perm maps back.

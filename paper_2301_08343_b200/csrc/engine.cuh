@@ -44,6 +44,7 @@ struct Geometry {
   double gdt[3];
   int with_gravity;
   double stress_scale;  // -dt * 4 * inv_dx^2 (engine.cpp:114)
+  int scatter_mode;     // 0: shared-memory tile (default), 1: direct RED (A/B switch)
 };
 
 struct DeviceSim {

@@ -168,7 +168,15 @@ __device__ __forceinline__ int64_t gel_particle(const GelMap& M, int64_t n_el) {
 // ---------------------------------------------------------------------------
 // Shared-memory node tile for the elastomer scatter.
 // ---------------------------------------------------------------------------
-constexpr int kTileCap = 2816;  // nodes; 4 x 8 B x 2816 + 4 B x 2816 = 101 KB
+#ifndef TACCHI_TILE_CAP
+#define TACCHI_TILE_CAP 2816
+#endif
+#ifndef TACCHI_GEL_THREADS
+#define TACCHI_GEL_THREADS 256
+#endif
+constexpr int kTileCap = TACCHI_TILE_CAP;  // nodes; 2816 -> 4 x 8 B x 2816 + 4 B x 2816 = 101 KB
+constexpr int kGelThreads = TACCHI_GEL_THREADS;
+constexpr int kGelMinBlocks = (2 * 256) / TACCHI_GEL_THREADS;
 
 struct P2GTile {
   double m[kTileCap], px[kTileCap], py[kTileCap], pz[kTileCap];
@@ -214,15 +222,45 @@ __device__ __forceinline__ void scatter_direct(const Geometry& g, double4* grid,
   }
 }
 
-// CTA-cooperative scatter. All threads of the block must call it.
-// Phase (a,b,c) adds each particle's contribution to node base + (a,b,c);
-// two particles of the CTA collide in a phase only if they share a base cell,
-// which an elastomer lattice coarser than the grid (0.2 mm vs 0.129 mm) never
-// does; the rare duplicates (detected through the owner table) and CTAs whose
-// footprint exceeds the tile fall back to direct REDs.
-__device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
-                                 const Geometry& g, double4* grid) {
+// Walks the flat indices e = first, first + stride, ... of a (d0, d1, d2) box
+// (k fastest) keeping (i, j, k) up to date with carries instead of a div/mod
+// per step.
+struct BoxIter {
+  int e, i, j, k;
+  int di, dj, dk, stride;
+  __device__ __forceinline__ BoxIter(int first, int step, int d1, int d2) {
+    e = first;
+    stride = step;
+    k = first % d2;
+    const int r = first / d2;
+    j = r % d1;
+    i = r / d1;
+    dk = step % d2;
+    const int rs = step / d2;
+    dj = rs % d1;
+    di = rs / d1;
+  }
+  __device__ __forceinline__ void next(int d1, int d2) {
+    e += stride;
+    k += dk;
+    j += dj;
+    i += di;
+    if (k >= d2) {
+      k -= d2;
+      ++j;
+    }
+    if (j >= d1) {
+      j -= d1;
+      ++i;
+    }
+  }
+};
+
+// The CTA's node box [min base, max base + 3) per axis; T.ok when it fits
+// the tile. All threads of the block must call it (3 barriers).
+__device__ void tile_box(P2GTile& T, bool active, const int* base) {
   const int tid = threadIdx.x;
+  __syncthreads();  // previous users of T.lo / T.hi are done
   if (tid == 0) {
     T.lo[0] = T.lo[1] = T.lo[2] = INT_MAX;
     T.hi[0] = T.hi[1] = T.hi[2] = INT_MIN;
@@ -231,8 +269,8 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
   if (active) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      atomicMin(&T.lo[a], q.st.base[a]);
-      atomicMax(&T.hi[a], q.st.base[a]);
+      atomicMin(&T.lo[a], base[a]);
+      atomicMax(&T.hi[a], base[a]);
     }
   }
   __syncthreads();
@@ -246,6 +284,23 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
     T.ok = any && vol <= kTileCap;
   }
   __syncthreads();
+}
+
+// CTA-cooperative scatter. All threads of the block must call it.
+// Phase (a,b,c) adds each particle's contribution to node base + (a,b,c);
+// two particles of the CTA collide in a phase only if they share a base cell,
+// which an elastomer lattice coarser than the grid (0.2 mm vs 0.129 mm) never
+// does; the rare duplicates (detected through the owner table) and CTAs whose
+// footprint exceeds the tile fall back to direct REDs.
+__device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
+                                 const Geometry& g, double4* grid) {
+  const int tid = threadIdx.x;
+  if (g.scatter_mode == 1) {  // A/B: per-particle REDs, no tile
+    if (active) scatter_direct(g, grid, m, q);
+    return;
+  }
+  if (g.scatter_mode == 3) return;  // A/B timing: no scatter at all
+  tile_box(T, active, q.st.base);
   const int d1 = T.dim[1], d2 = T.dim[2];
   const int vol = T.dim[0] * d1 * d2;
   const bool use_tile = T.ok != 0;
@@ -284,7 +339,7 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         __syncthreads();
-        if (tiled) {
+        if (tiled && g.scatter_mode != 2) {
           const double dxc = (c - q.st.fx[2]) * dx;
           const double w = wab * q.st.w[2][c];
           const int e = base_idx + (a * d1 + b) * d2 + c;
@@ -297,13 +352,12 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
     }
   }
   __syncthreads();
-  for (int e = tid; e < vol; e += blockDim.x) {
+  for (BoxIter it(tid, blockDim.x, d1, d2); it.e < vol; it.next(d1, d2)) {
+    const int e = it.e;
     const double mm = T.m[e];
     if (mm == 0.0) continue;
-    const int k = e % d2, r = e / d2;
-    const int j = r % d1, i = r / d1;
-    double* nd =
-        reinterpret_cast<double*>(grid + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2] + k));
+    double* nd = reinterpret_cast<double*>(
+        grid + node_index(g, T.lo[0] + it.i, T.lo[1] + it.j, T.lo[2] + it.k));
     red_add(nd + 0, mm);
     red_add(nd + 1, T.px[e]);
     red_add(nd + 2, T.py[e]);
@@ -502,7 +556,7 @@ __global__ void k_clear(double4* __restrict__ grid, double* __restrict__ mi, Ctl
 // ---------------------------------------------------------------------------
 
 // Standalone elastomer scatter (first substep of a call / phase API).
-__global__ void __launch_bounds__(256, 2) k_p2g_gel_tile(
+__global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_p2g_gel_tile(
     const double* __restrict__ x, const double* __restrict__ v, const double* __restrict__ Cm,
     const double* __restrict__ Fm, int64_t n, int64_t n_el, GelMap M, Ctl* ctl, Geometry g,
     double4* __restrict__ grid, double m, double vol0) {
@@ -553,121 +607,168 @@ __global__ void __launch_bounds__(256) k_p2g_ind_direct(const double* __restrict
 }
 
 // Rigid indenter: optional apply_boundary + advect (kMove) and the scatter of
-// the (next) substep (kScatter). A CTA owns kIndThreads * kChunk consecutive
-// particles of the (bx, by, z)-sorted cloud: it moves them with coalesced
-// loads/stores and stages the new positions in shared memory; then each thread
-// walks kChunk consecutive particles, keeping the B-spline weight sums of the
-// last four z-planes of its 3x3 column in registers, and flushes a plane (one
-// RED.F64 per node, into M_I) only when the run leaves it.
-constexpr int kIndThreads = 128;
+// the (next) substep (kScatter). Every node receives (sum_p w_p) m (1, v)
+// (C = 0, uniform v, engine.cpp:130,144), so only the weight sums M_I are
+// scattered. Particles are sorted by (bx, by, z) at creation (engine.cu), so
+// consecutive particles share a base cell in runs of ~particles-per-cell.
+//   1. each thread moves kIndK consecutive particles (32-byte vector
+//      loads/stores) and sums their 27 stencil weights in registers (an
+//      in-chunk base change, rare, is flushed with direct REDs);
+//   2. the per-thread partial sums go to shared memory with the base key;
+//      threads with equal keys form contiguous runs;
+//   3. (run, component) tasks sum a run's partials and issue one RED.F64 per
+//      node (~1.5 per particle instead of 108).
+constexpr int kIndThreads = 256;
+constexpr int kIndK = 4;
 
-__device__ __forceinline__ int ind_pad(int e) { return e + (e >> 4); }  // 2-way max bank conflict
+struct IndSmem {
+  double w[27][kIndThreads + 1];  // +1: (run, component) tasks read down columns
+  long long key[kIndThreads];
+  int run_start[kIndThreads + 1];
+  int nruns;
+  int warp_heads[kIndThreads / 32];
+};
 
-template <int kChunk, bool kMove, bool kScatter>
+__device__ __forceinline__ long long base_key(const Geometry& g, const int* b) {
+  return static_cast<long long>(node_index(g, b[0], b[1], b[2]));
+}
+
+template <bool kMove, bool kScatter>
 __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict__ x, int64_t n,
                                                               int64_t n_el, Ctl* ctl, Geometry g,
                                                               double* __restrict__ mi) {
-  constexpr int kSeg = kIndThreads * kChunk;
-  constexpr int kPadded = kSeg + kSeg / 16;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* xs = reinterpret_cast<double*>(smem_raw);  // [3][kPadded]
+  IndSmem& S = *reinterpret_cast<IndSmem*>(smem_raw);
   const int s = ctl->substep;
   if (stale(ctl, s)) return;  // stable: nothing raises for substep s while this runs
   const int tid = threadIdx.x;
-  const int64_t seg0 = n_el + static_cast<int64_t>(blockIdx.x) * kSeg;
-  if (kMove && blockIdx.x == 0 && tid == 0) {
+  const int64_t gt = static_cast<int64_t>(blockIdx.x) * kIndThreads + tid;
+  if (kMove && gt == 0) {
     // apply_boundary: every indenter velocity becomes the command
     // (engine.cpp:260-261); the next grid_update uses it as M_I's velocity.
     ctl->ind_v[0] = ctl->vind[0];
     ctl->ind_v[1] = ctl->vind[1];
     ctl->ind_v[2] = ctl->vind[2];
   }
-  double d[3] = {0, 0, 0};
-  if (kMove)
+  // Coalesced move: the warp's 32 * kIndK consecutive particles, lane l
+  // touching elements l + 32 i; then a register transpose (shuffles) gives
+  // lane l the kIndK consecutive elements kIndK*l .. kIndK*l + kIndK - 1.
+  const int lane = tid & 31;
+  const int64_t wbase = n_el + (static_cast<int64_t>(blockIdx.x) * kIndThreads + (tid & ~31)) * kIndK;
+  double cx[kIndK], cy[kIndK], cz[kIndK];
+#pragma unroll
+  for (int i = 0; i < kIndK; ++i) {
+    const int64_t p = wbase + lane + 32 * i;
+    const bool ok = p < n;
+    cx[i] = ok ? x[p] : 0.0;
+    cy[i] = ok ? x[n + p] : 0.0;
+    cz[i] = ok ? x[2 * n + p] : 0.0;
+  }
+  if (kMove) {
+    double d[3];
     for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
-#pragma unroll 4
-  for (int i = 0; i < kChunk; ++i) {
-    const int e = i * kIndThreads + tid;
-    const int64_t p = seg0 + e;
-    if (p >= n) break;
-    double px = x[p], py = x[n + p], pz = x[2 * n + p];
-    if (kMove) {
-      px = add_rn(px, d[0]);
-      py = add_rn(py, d[1]);
-      pz = add_rn(pz, d[2]);
-      x[p] = px;
-      x[n + p] = py;
-      x[2 * n + p] = pz;
-    }
-    if (kScatter) {
-      xs[ind_pad(e)] = px;
-      xs[kPadded + ind_pad(e)] = py;
-      xs[2 * kPadded + ind_pad(e)] = pz;
+#pragma unroll
+    for (int i = 0; i < kIndK; ++i) {
+      const int64_t p = wbase + lane + 32 * i;
+      if (p < n) {
+        cx[i] = add_rn(cx[i], d[0]);
+        cy[i] = add_rn(cy[i], d[1]);
+        cz[i] = add_rn(cz[i], d[2]);
+        x[p] = cx[i];
+        x[n + p] = cy[i];
+        x[2 * n + p] = cz[i];
+      }
     }
   }
   if (!kScatter) return;
-  __syncthreads();
-  const int64_t seg_len = n - seg0 < kSeg ? n - seg0 : kSeg;
-  const int e0 = tid * kChunk;
-  const int e1 = e0 + kChunk < seg_len ? e0 + kChunk : static_cast<int>(seg_len);
-  double acc[4][9];
+  double px[kIndK], py[kIndK], pz[kIndK];
+  const int reg = (kIndK * lane) >> 5;  // register slot holding this lane's elements
 #pragma unroll
-  for (int z = 0; z < 4; ++z)
+  for (int j = 0; j < kIndK; ++j) {
+    const int src = (kIndK * lane + j) & 31;
+    px[j] = py[j] = pz[j] = 0.0;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) acc[z][i] = 0.0;
-  int cb0 = INT_MIN, cb1 = INT_MIN, z0 = INT_MIN;
-  for (int e = e0; e < e1; ++e) {
-    Stencil st;
-    make_stencil(xs[ind_pad(e)], xs[kPadded + ind_pad(e)], xs[2 * kPadded + ind_pad(e)], g.origin,
-                 g.inv_dx, st);
-    if (!stencil_in_grid(g, st)) continue;  // finalize raises OutOfGrid
-    const int b2 = st.base[2];
-    if (st.base[0] != cb0 || st.base[1] != cb1 || b2 < z0 || b2 > z0 + 3) {
-      if (cb0 != INT_MIN) {
-#pragma unroll
-        for (int z = 0; z < 4; ++z)
-#pragma unroll
-          for (int i = 0; i < 9; ++i) {
-            if (acc[z][i] != 0.0) red_add(mi + node_index(g, cb0 + i / 3, cb1 + i % 3, z0 + z), acc[z][i]);
-            acc[z][i] = 0.0;
-          }
+    for (int r = 0; r < kIndK; ++r) {
+      const double vx = __shfl_sync(0xffffffffu, cx[r], src);
+      const double vy = __shfl_sync(0xffffffffu, cy[r], src);
+      const double vz = __shfl_sync(0xffffffffu, cz[r], src);
+      if (r == reg) {
+        px[j] = vx;
+        py[j] = vy;
+        pz[j] = vz;
       }
-      cb0 = st.base[0];
-      cb1 = st.base[1];
-      z0 = b2;
     }
-    while (b2 > z0 + 1) {  // slide the 4-plane window up one plane
+  }
+  const int64_t p0 = wbase + kIndK * lane;
+  const int cnt = p0 >= n ? 0 : (n - p0 < kIndK ? static_cast<int>(n - p0) : kIndK);
+  double acc[27];
 #pragma unroll
-      for (int i = 0; i < 9; ++i)
-        if (acc[0][i] != 0.0) red_add(mi + node_index(g, cb0 + i / 3, cb1 + i % 3, z0), acc[0][i]);
+  for (int i = 0; i < 27; ++i) acc[i] = 0.0;
+  int cb[3] = {0, 0, 0};
+  bool have = false;
 #pragma unroll
-      for (int z = 0; z < 3; ++z)
+  for (int j = 0; j < kIndK; ++j) {
+    if (j >= cnt) break;
+    Stencil st;
+    make_stencil(px[j], py[j], pz[j], g.origin, g.inv_dx, st);
+    if (!stencil_in_grid(g, st)) continue;  // finalize raises OutOfGrid
+    if (have && (st.base[0] != cb[0] || st.base[1] != cb[1] || st.base[2] != cb[2])) {
+      // rare: the chunk crosses a base cell; flush the first part directly
 #pragma unroll
-        for (int i = 0; i < 9; ++i) acc[z][i] = acc[z + 1][i];
-#pragma unroll
-      for (int i = 0; i < 9; ++i) acc[3][i] = 0.0;
-      ++z0;
+      for (int i = 0; i < 27; ++i) {
+        if (acc[i] != 0.0)
+          red_add(mi + node_index(g, cb[0] + i / 9, cb[1] + (i / 3) % 3, cb[2] + i % 3), acc[i]);
+        acc[i] = 0.0;
+      }
     }
-    const bool up = b2 != z0;  // planes 1..3 instead of 0..2
+    cb[0] = st.base[0];
+    cb[1] = st.base[1];
+    cb[2] = st.base[2];
+    have = true;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int b = 0; b < 3; ++b) {
         const double wab = st.w[0][a] * st.w[1][b];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double w = wab * st.w[2][c];
-          if (up) acc[c + 1][3 * a + b] += w;
-          else acc[c][3 * a + b] += w;
-        }
+        for (int c = 0; c < 3; ++c) acc[9 * a + 3 * b + c] += wab * st.w[2][c];
       }
   }
-  if (cb0 != INT_MIN) {
+  // 2. partials + keys to shared memory; runs of equal keys.
+  const long long key = have ? base_key(g, cb) : -1 - static_cast<long long>(tid);
+  S.key[tid] = key;
 #pragma unroll
-    for (int z = 0; z < 4; ++z)
-#pragma unroll
-      for (int i = 0; i < 9; ++i)
-        if (acc[z][i] != 0.0) red_add(mi + node_index(g, cb0 + i / 3, cb1 + i % 3, z0 + z), acc[z][i]);
+  for (int i = 0; i < 27; ++i) S.w[i][tid] = acc[i];
+  __syncthreads();
+  const bool head = have && (tid == 0 || S.key[tid - 1] != key);
+  const unsigned bal = __ballot_sync(0xffffffffu, head);
+  const int warp = tid >> 5;
+  if (lane == 0) S.warp_heads[warp] = __popc(bal);
+  __syncthreads();
+  int before = 0;
+  for (int w = 0; w < warp; ++w) before += S.warp_heads[w];
+  const int rank = before + __popc(bal & ((1u << lane) - 1));
+  if (head) S.run_start[rank] = tid;
+  if (tid == kIndThreads - 1) {
+    int total = 0;
+    for (int w = 0; w < kIndThreads / 32; ++w) total += S.warp_heads[w];
+    S.nruns = total;
+  }
+  __syncthreads();
+  // 3. (run, component) tasks. A run ends at the next head or at the first
+  // thread whose key differs (empty chunks carry unique negative keys).
+  const int nruns = S.nruns;
+  for (int task = tid; task < nruns * 27; task += kIndThreads) {
+    const int r = task / 27, c = task % 27;
+    const int t0 = S.run_start[r];
+    const long long k0 = S.key[t0];
+    double sum = 0.0;
+    for (int t = t0; t < kIndThreads && S.key[t] == k0; ++t) sum += S.w[c][t];
+    if (sum != 0.0) {
+      const int64_t node = k0;  // node index of the base cell
+      const int a = c / 9, b = (c / 3) % 3, cc = c % 3;
+      red_add(mi + node + (static_cast<int64_t>(a) * g.res[1] + b) * g.res[2] + cc, sum);
+    }
   }
 }
 
@@ -813,8 +914,46 @@ __device__ __forceinline__ void g2p_gather(const Geometry& g, const double4* __r
 }
 }  // namespace
 
+// G2P gather from the CTA's node box staged in shared memory (vx, vy, vz in
+// T.m, T.px, T.py), same arithmetic as g2p_gather.
+__device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile& T,
+                                                const Stencil& st, double* vv, double* Cn) {
+  const int d1 = T.dim[1], d2 = T.dim[2];
+  const int e0 = ((st.base[0] - T.lo[0]) * d1 + (st.base[1] - T.lo[1])) * d2 + (st.base[2] - T.lo[2]);
+  double v0 = 0, v1 = 0, vz = 0;
+  double b00 = 0, b01 = 0, b02 = 0, b10 = 0, b11 = 0, b12 = 0, b20 = 0, b21 = 0, b22 = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double wa = st.w[0][a];
+    const double da = a - st.fx[0];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const double wab = wa * st.w[1][b];
+      const double db = b - st.fx[1];
+      const int row = e0 + (a * d1 + b) * d2;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double w = wab * st.w[2][c];
+        const double dc = c - st.fx[2];
+        const double wv0 = w * T.m[row + c], wv1 = w * T.px[row + c], wv2 = w * T.py[row + c];
+        v0 += wv0; v1 += wv1; vz += wv2;
+        b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
+        b10 += wv1 * da; b11 += wv1 * db; b12 += wv1 * dc;
+        b20 += wv2 * da; b21 += wv2 * db; b22 += wv2 * dc;
+      }
+    }
+  }
+  vv[0] = v0;
+  vv[1] = v1;
+  vv[2] = vz;
+  const double k = 4.0 * g.inv_dx;
+  Cn[0] = k * b00; Cn[1] = k * b01; Cn[2] = k * b02;
+  Cn[3] = k * b10; Cn[4] = k * b11; Cn[5] = k * b12;
+  Cn[6] = k * b20; Cn[7] = k * b21; Cn[8] = k * b22;
+}
+
 template <bool kBoundary, bool kAdvect, bool kLookahead>
-__global__ void __launch_bounds__(256, 2) k_g2p2g_gel(
+__global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     double* __restrict__ x, double* __restrict__ v, double* __restrict__ Cm,
     double* __restrict__ Fm, const uint8_t* __restrict__ tag, int64_t n, int64_t n_el, GelMap M,
     Ctl* ctl, Geometry g, const double4* __restrict__ vel, double4* __restrict__ grid, double m,
@@ -827,11 +966,52 @@ __global__ void __launch_bounds__(256, 2) k_g2p2g_gel(
   const bool active = p >= 0;
   double px0 = 0, px1 = 0, px2 = 0, v2 = 0;
   double F[9], vv[3] = {0, 0, 0}, Cn[9];
+  bool staged = false;
+  Stencil st_old;
   if (active) {
     px0 = x[p];
     px1 = x[n + p];
     px2 = x[2 * n + p];
-    g2p_gather(g, vel, px0, px1, px2, vv, Cn);
+    make_stencil(px0, px1, px2, g.origin, g.inv_dx, st_old);
+  }
+  if (kLookahead) {
+    // Stage the grid velocities of the CTA's G2P footprint (coalesced rows
+    // along z) in the shared tile before the gathers.
+    tile_box(T, active, st_old.base);
+    staged = T.ok != 0;
+    if (staged) {
+      const int d1 = T.dim[1], d2 = T.dim[2];
+      const int vol = T.dim[0] * d1 * d2;
+      // two nodes per iteration so two loads are in flight per thread
+      const int step = 2 * blockDim.x;
+      BoxIter ia(threadIdx.x, step, d1, d2), ib(threadIdx.x + blockDim.x, step, d1, d2);
+      for (; ia.e < vol; ia.next(d1, d2), ib.next(d1, d2)) {
+        const bool hb = ib.e < vol;
+        const double2* qa2 = reinterpret_cast<const double2*>(
+            vel + node_index(g, T.lo[0] + ia.i, T.lo[1] + ia.j, T.lo[2] + ia.k));
+        const double2* qb2 = reinterpret_cast<const double2*>(
+            vel + node_index(g, T.lo[0] + ib.i, T.lo[1] + ib.j, T.lo[2] + ib.k));
+        const double2 a0 = __ldg(qa2), a1 = __ldg(qa2 + 1);
+        double2 b0 = make_double2(0, 0), b1 = make_double2(0, 0);
+        if (hb) {
+          b0 = __ldg(qb2);
+          b1 = __ldg(qb2 + 1);
+        }
+        T.m[ia.e] = a0.x;
+        T.px[ia.e] = a0.y;
+        T.py[ia.e] = a1.x;
+        if (hb) {
+          T.m[ib.e] = b0.x;
+          T.px[ib.e] = b0.y;
+          T.py[ib.e] = b1.x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (active) {
+    if (staged) g2p_gather_smem(g, T, st_old, vv, Cn);
+    else g2p_gather(g, vel, px0, px1, px2, vv, Cn);
     double F0[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) F0[i] = Fm[i * n_el + p];
@@ -866,7 +1046,11 @@ __global__ void __launch_bounds__(256, 2) k_g2p2g_gel(
     P2GPayload q;
     double J = 1.0;
     bool go = active;
-    if (go) {
+    if (go && g.scatter_mode == 4) {
+      make_stencil(px0, px1, px2, g.origin, g.inv_dx, q.st);
+      q.mv[0] = q.mv[1] = q.mv[2] = 0.0;
+      for (int i = 0; i < 9; ++i) q.aff[i] = 0.0;
+    } else if (go) {
       go = make_payload(g, ctl, s + 1, m, vol0, F, Cn, vv, px0, px1, px2, q, J);
       if (go && !stencil_in_grid(g, q.st)) go = false;  // finalize raises OutOfGrid
     }
@@ -976,10 +1160,8 @@ __global__ void k_gather_box(const double4* __restrict__ mp, const double* __res
 
 namespace {
 constexpr int kThreads = 256;
-constexpr int kIndChunk = 16;
 constexpr size_t kTileSmem = sizeof(P2GTile);
-constexpr size_t kIndSmem =
-    3 * sizeof(double) * (kIndThreads * kIndChunk + kIndThreads * kIndChunk / 16);
+constexpr size_t kIndSmem = sizeof(IndSmem);
 
 inline unsigned blocks_for(int64_t n) {
   const int64_t b = (n + kThreads - 1) / kThreads;
@@ -999,7 +1181,7 @@ GelMap gel_map(const DeviceSim& s) {
 
 unsigned gel_blocks(const DeviceSim& s) {
   if (s.lat[0] > 0) return static_cast<unsigned>(s.tiles[0] * s.tiles[1]);
-  return blocks_for(s.n_el);
+  return static_cast<unsigned>((s.n_el + kGelThreads - 1) / kGelThreads);
 }
 
 void configure_once() {
@@ -1009,9 +1191,9 @@ void configure_once() {
                        static_cast<int>(kTileSmem));
   cudaFuncSetAttribute(k_g2p2g_gel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(kTileSmem));
-  cudaFuncSetAttribute(k_ind_move_p2g<kIndChunk, false, true>,
+  cudaFuncSetAttribute(k_ind_move_p2g<false, true>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIndSmem));
-  cudaFuncSetAttribute(k_ind_move_p2g<kIndChunk, true, true>,
+  cudaFuncSetAttribute(k_ind_move_p2g<true, true>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIndSmem));
   done = true;
 }
@@ -1021,14 +1203,14 @@ void configure_once() {
 void configure_gel_tiling(DeviceSim& s, int nx, int ny, int nz) {
   configure_once();
   if (nx <= 0 || ny <= 0 || nz <= 0 || static_cast<int64_t>(nx) * ny * nz != s.n_el ||
-      nz > kThreads) {
+      nz > kGelThreads) {
     s.lat[0] = s.lat[1] = s.lat[2] = 0;
     return;
   }
   s.lat[0] = nx;
   s.lat[1] = ny;
   s.lat[2] = nz;
-  const int cols = kThreads / nz > 0 ? kThreads / nz : 1;
+  const int cols = kGelThreads / nz > 0 ? kGelThreads / nz : 1;
   int ti = 1;
   while ((ti + 1) * (ti + 1) <= cols) ++ti;
   const int tj = cols / ti > 0 ? cols / ti : 1;
@@ -1073,14 +1255,14 @@ int launch_clear(DeviceSim& s, int sms) {
 int launch_p2g_gel(DeviceSim& s) {
   if (s.n_el <= 0) return 0;
   configure_once();
-  k_p2g_gel_tile<<<gel_blocks(s), kThreads, kTileSmem, s.stream>>>(
+  k_p2g_gel_tile<<<gel_blocks(s), kGelThreads, kTileSmem, s.stream>>>(
       s.x, s.v, s.C, s.F, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_mp, s.m_el, s.vol_el);
   s.kernel_launches += 1;
   return 1;
 }
 
 inline unsigned ind_blocks(const DeviceSim& s) {
-  const int64_t seg = static_cast<int64_t>(kIndThreads) * kIndChunk;
+  const int64_t seg = static_cast<int64_t>(kIndThreads) * kIndK;
   return static_cast<unsigned>((s.n_ind + seg - 1) / seg);
 }
 
@@ -1088,7 +1270,7 @@ int launch_p2g_ind(DeviceSim& s) {
   if (s.n_ind <= 0) return 0;
   configure_once();
   if (s.ind_v_uniform)
-    k_ind_move_p2g<kIndChunk, false, true><<<ind_blocks(s), kIndThreads, kIndSmem, s.stream>>>(
+    k_ind_move_p2g<false, true><<<ind_blocks(s), kIndThreads, kIndSmem, s.stream>>>(
         s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   else
     k_p2g_ind_direct<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el, s.ctl,
@@ -1124,11 +1306,11 @@ int launch_g2p2g_gel(DeviceSim& s, bool lookahead) {
   if (s.n_el <= 0) return 0;
   configure_once();
   if (lookahead)
-    k_g2p2g_gel<true, true, true><<<gel_blocks(s), kThreads, kTileSmem, s.stream>>>(
+    k_g2p2g_gel<true, true, true><<<gel_blocks(s), kGelThreads, kTileSmem, s.stream>>>(
         s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
         s.m_el, s.vol_el);
   else
-    k_g2p2g_gel<true, true, false><<<gel_blocks(s), kThreads, 0, s.stream>>>(
+    k_g2p2g_gel<true, true, false><<<gel_blocks(s), kGelThreads, 0, s.stream>>>(
         s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
         s.m_el, s.vol_el);
   s.kernel_launches += 1;
@@ -1139,10 +1321,10 @@ int launch_ind_move(DeviceSim& s, bool lookahead) {
   if (s.n_ind <= 0) return 0;
   configure_once();
   if (lookahead)
-    k_ind_move_p2g<kIndChunk, true, true><<<ind_blocks(s), kIndThreads, kIndSmem, s.stream>>>(
+    k_ind_move_p2g<true, true><<<ind_blocks(s), kIndThreads, kIndSmem, s.stream>>>(
         s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   else
-    k_ind_move_p2g<kIndChunk, true, false><<<ind_blocks(s), kIndThreads, 0, s.stream>>>(
+    k_ind_move_p2g<true, false><<<ind_blocks(s), kIndThreads, 0, s.stream>>>(
         s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   s.ind_v_uniform = true;
   s.kernel_launches += 1;
@@ -1158,7 +1340,7 @@ int launch_finalize_step(DeviceSim& s) {
 
 int launch_phase_g2p(DeviceSim& s) {
   if (s.n_el <= 0) return 0;
-  k_g2p2g_gel<false, false, false><<<gel_blocks(s), kThreads, 0, s.stream>>>(
+  k_g2p2g_gel<false, false, false><<<gel_blocks(s), kGelThreads, 0, s.stream>>>(
       s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
       s.m_el, s.vol_el);
   s.kernel_launches += 1;
