@@ -27,6 +27,9 @@ int launch_grid_update(DeviceSim& s, int sms, bool zero);
 int launch_g2p2g_gel(DeviceSim& s, bool lookahead);
 int launch_ind_move(DeviceSim& s, bool lookahead);
 int launch_finalize_step(DeviceSim& s);
+int launch_call_begin(DeviceSim& s);
+int launch_ind_cols(DeviceSim& s, bool move);
+int launch_ind_catchup(DeviceSim& s);
 int launch_phase_g2p(DeviceSim& s);
 int launch_phase_boundary(DeviceSim& s);
 int launch_phase_advect(DeviceSim& s);
@@ -80,6 +83,8 @@ DeviceSim::~DeviceSim() {
   cudaFree(grid_mp);
   cudaFree(grid_v);
   cudaFree(grid_mi);
+  cudaFree(col_start);
+  cudaFree(ind_moves);
   cudaFree(surf_idx);
   cudaFree(surf_depth);
   cudaFree(cap_depth);
@@ -181,11 +186,13 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
                     P->gravity[2] * P->gravity[2]) > 0.0;
   g.stress_scale = -P->dt * 4.0 * g.inv_dx * g.inv_dx;
   if (const char* m = std::getenv("TACCHI_SCATTER")) g.scatter_mode = std::atoi(m);
+  if (const char* f = std::getenv("TACCHI_FULL_INDENTER")) s->full_indenter = std::atoi(f) != 0;
 
   // Indenter particles are re-ordered by base cell so that P2G scatters from
   // neighbouring lanes hit neighbouring nodes; perm maps back.
   s->perm.resize(n);
   std::iota(s->perm.begin(), s->perm.end(), 0);
+  std::vector<int64_t> col_starts;
   // Order: base cell (bx, by) of the initial position, then z. Under the press
   // (motion along z) the order stays sorted by (bx, by, bz) for the whole
   // episode, which keeps runs of equal base cell contiguous for the chunked
@@ -206,6 +213,12 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
       if (ka != kb) return ka < kb;
       return in->x[3 * a + 2] < in->x[3 * b + 2];
     });
+    col_starts.push_back(n_el);
+    for (int64_t q = n_el + 1; q < n; ++q)
+      if (key[s->perm[q] - n_el] != key[s->perm[q - 1] - n_el]) col_starts.push_back(q);
+    col_starts.push_back(n);
+  } else if (n_ind == 1) {
+    col_starts = {n_el, n};
   }
   cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
   s->n_nodes = static_cast<size_t>(g.res[0]) * g.res[1] * g.res[2];
@@ -217,6 +230,9 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
             cudaMalloc(&s->grid_mp, s->n_nodes * sizeof(double4)) == cudaSuccess &&
             cudaMalloc(&s->grid_v, s->n_nodes * sizeof(double4)) == cudaSuccess &&
             cudaMalloc(&s->grid_mi, s->n_nodes * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&s->col_start, std::max<size_t>(col_starts.size(), 1) * sizeof(int64_t)) ==
+                cudaSuccess &&
+            cudaMalloc(&s->ind_moves, std::max<int64_t>(n_ind, 1)) == cudaSuccess &&
             cudaMalloc(&s->ctl, sizeof(Ctl)) == cudaSuccess &&
             cudaMallocHost(&s->h_ctl, sizeof(Ctl)) == cudaSuccess &&
             cudaMallocHost(&s->h_vind, 3 * sizeof(double)) == cudaSuccess;
@@ -227,6 +243,11 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   cudaMemsetAsync(s->grid_mp, 0, s->n_nodes * sizeof(double4), s->stream);
   cudaMemsetAsync(s->grid_v, 0, s->n_nodes * sizeof(double4), s->stream);
   cudaMemsetAsync(s->grid_mi, 0, s->n_nodes * sizeof(double), s->stream);
+  cudaMemsetAsync(s->ind_moves, 0, std::max<int64_t>(n_ind, 1), s->stream);
+  s->n_cols = col_starts.empty() ? 0 : static_cast<int>(col_starts.size()) - 1;
+  if (s->n_cols > 0)
+    cudaMemcpy(s->col_start, col_starts.data(), col_starts.size() * sizeof(int64_t),
+               cudaMemcpyHostToDevice);
   std::memset(s->h_ctl, 0, sizeof(Ctl));
   for (int a = 0; a < 3; ++a) s->h_ctl->vind[a] = in->indenter_velocity[a];
   // Is the indenter velocity uniform (it is for init_scene's output)?
@@ -330,19 +351,21 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
 // included, scatters the next substep's particles, so consecutive step() calls
 // chain without a standalone scatter.
 static int record_substeps(DeviceSim& s, int n_substeps) {
-  int k = 0;
+  int k = launch_call_begin(s);
   const int sms = sm_count(s.device);
+  const bool cols = s.n_cols > 0 && !s.full_indenter;
   if (!s.grid_ready) {
     if (s.grid_dirty) k += launch_clear(s, sms);
-    k += launch_p2g_gel(s) + launch_p2g_ind(s);
+    k += launch_p2g_gel(s);
+    k += (cols && s.ind_v_uniform) ? launch_ind_cols(s, false) : launch_p2g_ind(s);
   }
   for (int i = 0; i < n_substeps; ++i) {
-    const bool lookahead = true;
     k += launch_grid_update(s, sms, true);
-    k += launch_g2p2g_gel(s, lookahead);
-    k += launch_ind_move(s, lookahead);
+    k += launch_g2p2g_gel(s, true);
+    k += cols ? launch_ind_cols(s, true) : launch_ind_move(s, true);
     k += launch_finalize_step(s);
   }
+  if (cols) k += launch_ind_catchup(s);
   return k;
 }
 
@@ -425,11 +448,14 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
     s.grid_dirty = true;
   }
   if (s.grid_dirty) launch_clear(s, sms);
+  const bool cols = s.n_cols > 0 && !s.full_indenter;
+  launch_call_begin(s);
   float ms = 0.f;
   cudaEventRecord(ev[0], s.stream);
   launch_p2g_gel(s);
   cudaEventRecord(ev[1], s.stream);
-  launch_p2g_ind(s);
+  if (cols && s.ind_v_uniform) launch_ind_cols(s, false);
+  else launch_p2g_ind(s);
   cudaEventRecord(ev[2], s.stream);
   CUDA_TRY(cudaEventSynchronize(ev[2]));
   cudaEventElapsedTime(&ms, ev[0], ev[1]);
@@ -437,26 +463,25 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
   cudaEventElapsedTime(&ms, ev[1], ev[2]);
   out_ms[1] = ms;
   for (int r = 0; r < reps; ++r) {
-    const bool lookahead = r + 1 < reps;
     cudaEventRecord(ev[2], s.stream);
     launch_grid_update(s, sms, true);
     cudaEventRecord(ev[3], s.stream);
-    launch_g2p2g_gel(s, lookahead);
+    launch_g2p2g_gel(s, true);
     cudaEventRecord(ev[4], s.stream);
-    launch_ind_move(s, lookahead);
+    if (cols) launch_ind_cols(s, true);
+    else launch_ind_move(s, true);
     cudaEventRecord(ev[5], s.stream);
     launch_finalize_step(s);
     cudaEventRecord(ev[6], s.stream);
     CUDA_TRY(cudaEventSynchronize(ev[6]));
-    // average over the look-ahead substeps (all but the last) when reps > 1
-    const int denom = reps > 1 ? reps - 1 : 1;
-    if (lookahead || reps == 1)
-      for (int g = 2; g < kGroups; ++g) {
-        cudaEventElapsedTime(&ms, ev[g], ev[g + 1]);
-        out_ms[g] += ms / denom;
-      }
+    for (int g = 2; g < kGroups; ++g) {
+      cudaEventElapsedTime(&ms, ev[g], ev[g + 1]);
+      out_ms[g] += ms / reps;
+    }
   }
+  if (cols) launch_ind_catchup(s);
   for (auto& e : ev) cudaEventDestroy(e);
+  s.grid_ready = true;  // the last substep scattered the next one, as in step()
   return sync_and_check(s, start + reps);
 }
 
@@ -617,7 +642,15 @@ void tg_destroy(tg_handle h) { delete H(h); }
 
 int tg_step(tg_handle h, const double v[3], int n) {
   if (!h || !v) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step: null argument");
-  return tacchi_b200::step(*H(h), v, n);
+  // The per-call indenter move counters are 8-bit: long calls run in chunks
+  // (identical results; one extra host sync per 200 substeps).
+  while (n > 0) {
+    const int chunk = n > 200 ? 200 : n;
+    const int rc = tacchi_b200::step(*H(h), v, chunk);
+    if (rc) return rc;
+    n -= chunk;
+  }
+  return TG_OK;
 }
 
 int tg_phase(tg_handle h, int phase, const double v[3]) {
@@ -752,6 +785,7 @@ int tg_phong_render(int device, const double* depth, int w, int hgt, double r,
 int tg_step_many(tg_handle* hs, int n_handles, const double* velocities, int n_substeps) {
   if (!hs || !velocities) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_many: null argument");
   // Submit every handle's graph before waiting on any of them.
+  if (n_substeps > 200) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_many: n_substeps > 200");
   for (int i = 0; i < n_handles; ++i) {
     const int rc = tacchi_b200::step_submit(*H(hs[i]), velocities + 3 * i, n_substeps);
     if (rc) return rc;

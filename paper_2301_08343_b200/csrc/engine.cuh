@@ -30,6 +30,7 @@ struct Ctl {
   int box_lo[2][3], box_hi[2][3];         // per-material node boxes (elastomer, indenter)
   double vind[3];                         // commanded indenter velocity
   double ind_v[3];                        // uniform indenter velocity (P2G input)
+  int call_start;                         // substep index at the start of the step() call
   double diag_min_det_f, diag_max_speed;  // StepDiagnostics
   long long step_count;                   // SimState::step_count
 };
@@ -67,6 +68,11 @@ struct DeviceSim {
   double4* grid_mp = nullptr;
   double4* grid_v = nullptr;
   double* grid_mi = nullptr;  // indenter mass (uniform-velocity indenter scatter)
+  // Indenter columns: maximal runs of equal initial (bx, by) in the sorted
+  // cloud (internal indices [col_start[c], col_start[c+1])), z ascending.
+  int n_cols = 0;
+  int64_t* col_start = nullptr;
+  uint8_t* ind_moves = nullptr;  // advects applied to each indenter particle this call
   size_t n_nodes = 0;
   // Elastomer lattice (counts) when the elastomer is lattice-built; enables
   // the lattice-block CTA tiling of the elastomer scatter.
@@ -74,6 +80,7 @@ struct DeviceSim {
   int tile[3] = {0, 0, 0};   // lattice block per CTA (ti, tj, tk)
   int tiles[3] = {0, 0, 0};  // blocks per axis
   bool grid_dirty = false;   // A / M_I may hold a phase-mode P2G (needs k_clear)
+  bool full_indenter = false; // scatter every indenter particle (TACCHI_FULL_INDENTER=1)
   bool grid_ready = false;   // A / M_I hold the scatter of the next substep (look-ahead
                              // of the previous mpm::step call); skip the standalone P2G
 

@@ -773,6 +773,153 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
 }
 
 // ---------------------------------------------------------------------------
+// Rigid-indenter scatter restricted to where it matters (step path).
+//
+// Grid velocities are only ever read by elastomer particles (the indenter
+// skips G2P, engine.cpp:218), at nodes of their own stencils, i.e. inside the
+// elastomer's node box. An indenter particle whose stencil misses that box
+// changes nothing the simulation reads, so the step path scatters only the
+// particles whose stencil meets it; M_I is then exact on every node that has
+// elastomer mass. Within each column of the (bx, by, z)-sorted cloud z is
+// ascending and stays so under the rigid translation (fl(z + d) is monotone),
+// so base_z is non-decreasing: a warp walks its column upward and stops at the
+// first particle above the box. Particles are still advected every substep in
+// exact arithmetic: the ones visited here are moved in place, the others
+// accumulate pending moves that k_ind_catchup applies (the same sequence of
+// rounded adds) before mpm::step returns.
+// ---------------------------------------------------------------------------
+__global__ void k_call_begin(Ctl* ctl) { ctl->call_start = ctl->substep; }
+
+constexpr int kColWarps = 8;
+
+struct ColSmem {
+  double w[kColWarps][27][33];
+  long long key[kColWarps][32];
+  int run_start[kColWarps][33];
+};
+
+template <bool kMove>
+__global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
+    double* __restrict__ x, int64_t n, int64_t n_el, const int64_t* __restrict__ col_start,
+    int n_cols, uint8_t* __restrict__ moves, Ctl* ctl, Geometry g, double* __restrict__ mi,
+    int box_from_bb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ColSmem& S = *reinterpret_cast<ColSmem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = ctl->substep;
+  if (stale(ctl, s)) return;
+  if (kMove && blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->ind_v[0] = ctl->vind[0];  // apply_boundary (engine.cpp:260-261)
+    ctl->ind_v[1] = ctl->vind[1];
+    ctl->ind_v[2] = ctl->vind[2];
+  }
+  const int c = blockIdx.x * kColWarps + warp;
+  if (c >= n_cols) return;  // warp-uniform; only __syncwarp below
+  // Elastomer node box of the substep being scattered.
+  int glo[3], ghi[3];
+  for (int a = 0; a < 3; ++a) {
+    if (box_from_bb) {
+      const double l = order_val(ctl->bb_lo[a]), h = order_val(ctl->bb_hi[a]);
+      if (!(l <= h)) return;  // no elastomer: nothing reads the grid
+      glo[a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(l, g.origin[a]), g.inv_dx), 0.5)));
+      ghi[a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(h, g.origin[a]), g.inv_dx), 0.5))) + 3;
+    } else {
+      glo[a] = ctl->box_lo[0][a];
+      ghi[a] = ctl->box_hi[0][a];
+      if (ghi[a] <= glo[a]) return;
+    }
+  }
+  const int target = s - ctl->call_start + (kMove ? 1 : 0);  // advects this call after this kernel
+  double d[3] = {0, 0, 0};
+  for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
+  const int64_t a0 = col_start[c], a1 = col_start[c + 1];
+  for (int64_t b0 = a0; b0 < a1; b0 += 32) {
+    const int64_t p = b0 + lane;
+    const bool valid = p < a1;
+    Stencil st;
+    bool beyond = false, contrib = false;
+    if (valid) {
+      double px = x[p], py = x[n + p], pz = x[2 * n + p];
+      const int done = moves[p - n_el];
+      if (done < target) {
+        for (int k = done; k < target; ++k) {
+          px = add_rn(px, d[0]);
+          py = add_rn(py, d[1]);
+          pz = add_rn(pz, d[2]);
+        }
+        x[p] = px;
+        x[n + p] = py;
+        x[2 * n + p] = pz;
+        moves[p - n_el] = static_cast<uint8_t>(target);
+      }
+      make_stencil(px, py, pz, g.origin, g.inv_dx, st);
+      beyond = st.base[2] > ghi[2] - 1;  // this and every later particle of the column miss
+      contrib = !beyond && stencil_in_grid(g, st);
+      for (int a = 0; a < 3; ++a)
+        contrib = contrib && st.base[a] + 2 >= glo[a] && st.base[a] <= ghi[a] - 1;
+    }
+    const unsigned bey = __ballot_sync(0xffffffffu, beyond);
+    const int first_beyond = bey ? __ffs(bey) - 1 : 32;
+    if (lane > first_beyond) contrib = false;
+    const long long key = contrib ? static_cast<long long>(node_index(g, st.base[0], st.base[1], st.base[2]))
+                                  : -1 - static_cast<long long>(lane);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const double wab = contrib ? st.w[0][a] * st.w[1][b] : 0.0;
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) S.w[warp][9 * a + 3 * b + cc][lane] = wab * (contrib ? st.w[2][cc] : 0.0);
+      }
+    S.key[warp][lane] = key;
+    __syncwarp();
+    const bool head = contrib && (lane == 0 || S.key[warp][lane - 1] != key);
+    const unsigned hb = __ballot_sync(0xffffffffu, head);
+    if (head) S.run_start[warp][__popc(hb & ((1u << lane) - 1))] = lane;
+    __syncwarp();
+    const int nruns = __popc(hb);
+    for (int task = lane; task < nruns * 27; task += 32) {
+      const int r = task / 27, comp = task % 27;
+      const int t0 = S.run_start[warp][r];
+      const long long k0 = S.key[warp][t0];
+      double sum = 0.0;
+      for (int t = t0; t < 32 && S.key[warp][t] == k0; ++t) sum += S.w[warp][comp][t];
+      if (sum != 0.0)
+        red_add(mi + k0 + (static_cast<int64_t>(comp / 9) * g.res[1] + (comp / 3) % 3) * g.res[2] +
+                    comp % 3,
+                sum);
+    }
+    __syncwarp();
+    if (bey) break;  // the rest of the column is above the elastomer box
+  }
+}
+
+// Applies the pending advects of the indenter particles the column walks did
+// not visit, so every particle has moved exactly (completed substeps of this
+// call) times, then resets the per-call move counters.
+__global__ void k_ind_catchup(double* __restrict__ x, int64_t n, int64_t n_el,
+                              uint8_t* __restrict__ moves, Ctl* ctl, Geometry g) {
+  const int64_t p = n_el + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int total = ctl->substep - ctl->call_start;  // advects that completed in this call
+  const int done = moves[p - n_el];
+  if (done < total) {
+    double d[3];
+    for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
+    double px = x[p], py = x[n + p], pz = x[2 * n + p];
+    for (int k = done; k < total; ++k) {
+      px = add_rn(px, d[0]);
+      py = add_rn(py, d[1]);
+      pz = add_rn(pz, d[2]);
+    }
+    x[p] = px;
+    x[n + p] = py;
+    x[2 * n + p] = pz;
+  }
+  if (done) moves[p - n_el] = 0;
+}
+
+// ---------------------------------------------------------------------------
 // grid_update (engine.cpp:180-205)
 // ---------------------------------------------------------------------------
 // Node update shared by both traversals; kZero also re-zeroes A / M_I.
@@ -1327,6 +1474,46 @@ int launch_ind_move(DeviceSim& s, bool lookahead) {
     k_ind_move_p2g<true, false><<<ind_blocks(s), kIndThreads, 0, s.stream>>>(
         s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   s.ind_v_uniform = true;
+  s.kernel_launches += 1;
+  return 1;
+}
+
+constexpr size_t kColSmem = sizeof(ColSmem);
+
+int launch_call_begin(DeviceSim& s) {
+  k_call_begin<<<1, 1, 0, s.stream>>>(s.ctl);
+  s.kernel_launches += 1;
+  return 1;
+}
+
+// Indenter scatter of the step path: standalone (first substep of a call,
+// positions as they are) or fused with this substep's advect (look-ahead).
+int launch_ind_cols(DeviceSim& s, bool move) {
+  if (s.n_ind <= 0 || s.n_cols <= 0) return 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ind_cols<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kColSmem));
+    cudaFuncSetAttribute(k_ind_cols<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kColSmem));
+    attr = true;
+  }
+  const unsigned blocks = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
+  if (move)
+    k_ind_cols<true><<<blocks, kColWarps * 32, kColSmem, s.stream>>>(
+        s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 1);
+  else
+    k_ind_cols<false><<<blocks, kColWarps * 32, kColSmem, s.stream>>>(
+        s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 0);
+  s.ind_v_uniform = true;
+  s.kernel_launches += 1;
+  return 1;
+}
+
+int launch_ind_catchup(DeviceSim& s) {
+  if (s.n_ind <= 0) return 0;
+  k_ind_catchup<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.ind_moves,
+                                                                s.ctl, s.geo);
   s.kernel_launches += 1;
   return 1;
 }
