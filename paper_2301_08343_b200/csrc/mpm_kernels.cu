@@ -923,14 +923,15 @@ __global__ void k_ind_catchup(double* __restrict__ x, int64_t n, int64_t n_el,
 // grid_update (engine.cpp:180-205)
 // ---------------------------------------------------------------------------
 // Node update shared by both traversals; kZero also re-zeroes A / M_I.
+// with_mi: the node may hold indenter weight (inside the indenter box).
 template <bool kZero>
 __device__ __forceinline__ void update_node(double4* __restrict__ mp, double* __restrict__ mi,
                                             double4* __restrict__ vel, const Geometry& g,
                                             double m_ind, double u0, double u1, double u2, int i,
-                                            int j, int k) {
+                                            int j, int k, bool with_mi) {
   const size_t nd = node_index(g, i, j, k);
   const double4 q = mp[nd];
-  const double wi = mi[nd];  // indenter weight sum: mass m_ind wi, momentum (m_ind wi) u
+  const double wi = with_mi ? mi[nd] : 0.0;  // indenter weight sum: mass m_ind wi, momentum (m_ind wi) u
   double4 o = make_double4(0, 0, 0, 0);
   double mass = q.x, p0 = q.y, p1 = q.z, p2 = q.w;
   if (wi != 0.0) {
@@ -971,25 +972,21 @@ __global__ void k_grid_update_window(double4* __restrict__ mp, double* __restric
   if (stale(ctl, ctl->substep)) return;
   const int lx = ctl->win_lo[0], ly = ctl->win_lo[1], lz = ctl->win_lo[2];
   const int ny = ctl->win_hi[1] - ly, nz = ctl->win_hi[2] - lz;
-  const int64_t total = static_cast<int64_t>(ctl->win_hi[0] - lx) * ny * nz;
+  const int vol = (ctl->win_hi[0] - lx) * ny * nz;
   const double u0 = ctl->ind_v[0], u1 = ctl->ind_v[1], u2 = ctl->ind_v[2];
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int k = lz + static_cast<int>(t % nz);
-    const int64_t r = t / nz;
-    update_node<false>(mp, mi, vel, g, m_ind, u0, u1, u2, lx + static_cast<int>(r / ny),
-                       ly + static_cast<int>(r % ny), k);
-  }
+  for (BoxIter it(blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, ny, nz); it.e < vol;
+       it.next(ny, nz))
+    update_node<false>(mp, mi, vel, g, m_ind, u0, u1, u2, lx + it.i, ly + it.j, lz + it.k, true);
 }
 
 // Step path: only the union of the elastomer and indenter node boxes (every
-// node a scatter can have touched), re-zeroing the accumulators.
+// node a scatter can have touched), re-zeroing the accumulators. M_I is read
+// only inside the indenter box.
 __global__ void k_grid_update_boxes(double4* __restrict__ mp, double* __restrict__ mi,
                                     double4* __restrict__ vel, Ctl* ctl, Geometry g,
                                     double m_ind) {
   if (stale(ctl, ctl->substep)) return;
-  int lo[2][3], dm[2][3];
-  int64_t vol[2];
+  int lo[2][3], dm[2][3], vol[2];
   for (int m = 0; m < 2; ++m) {
     vol[m] = 1;
     for (int a = 0; a < 3; ++a) {
@@ -999,20 +996,22 @@ __global__ void k_grid_update_boxes(double4* __restrict__ mp, double* __restrict
     }
   }
   const double u0 = ctl->ind_v[0], u1 = ctl->ind_v[1], u2 = ctl->ind_v[2];
-  const int64_t total = vol[0] + vol[1];
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int m = t < vol[0] ? 0 : 1;
-    const int64_t u = m == 0 ? t : t - vol[0];
-    const int k = lo[m][2] + static_cast<int>(u % dm[m][2]);
-    const int64_t r = u / dm[m][2];
-    const int j = lo[m][1] + static_cast<int>(r % dm[m][1]);
-    const int i = lo[m][0] + static_cast<int>(r / dm[m][1]);
-    if (m == 1 && vol[0] > 0 && i >= lo[0][0] && i < lo[0][0] + dm[0][0] && j >= lo[0][1] &&
-        j < lo[0][1] + dm[0][1] && k >= lo[0][2] && k < lo[0][2] + dm[0][2])
-      continue;  // already handled in the elastomer box
-    update_node<true>(mp, mi, vel, g, m_ind, u0, u1, u2, i, j, k);
-  }
+  const int first = blockIdx.x * blockDim.x + threadIdx.x, step = gridDim.x * blockDim.x;
+  auto in_box = [&](int m, int i, int j, int k) {
+    return vol[m] > 0 && i >= lo[m][0] && i < lo[m][0] + dm[m][0] && j >= lo[m][1] &&
+           j < lo[m][1] + dm[m][1] && k >= lo[m][2] && k < lo[m][2] + dm[m][2];
+  };
+  if (vol[0] > 0)
+    for (BoxIter it(first, step, dm[0][1], dm[0][2]); it.e < vol[0]; it.next(dm[0][1], dm[0][2])) {
+      const int i = lo[0][0] + it.i, j = lo[0][1] + it.j, k = lo[0][2] + it.k;
+      update_node<true>(mp, mi, vel, g, m_ind, u0, u1, u2, i, j, k, in_box(1, i, j, k));
+    }
+  if (vol[1] > 0)
+    for (BoxIter it(first, step, dm[1][1], dm[1][2]); it.e < vol[1]; it.next(dm[1][1], dm[1][2])) {
+      const int i = lo[1][0] + it.i, j = lo[1][1] + it.j, k = lo[1][2] + it.k;
+      if (in_box(0, i, j, k)) continue;  // already handled in the elastomer box
+      update_node<true>(mp, mi, vel, g, m_ind, u0, u1, u2, i, j, k, true);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1115,10 +1114,15 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
   double F[9], vv[3] = {0, 0, 0}, Cn[9];
   bool staged = false;
   Stencil st_old;
+  double F0[9];
   if (active) {
     px0 = x[p];
     px1 = x[n + p];
     px2 = x[2 * n + p];
+    // issue the deformation-gradient loads now; they complete while the
+    // footprint is reduced and the velocity tile is staged
+#pragma unroll
+    for (int i = 0; i < 9; ++i) F0[i] = Fm[i * n_el + p];
     make_stencil(px0, px1, px2, g.origin, g.inv_dx, st_old);
   }
   if (kLookahead) {
@@ -1159,9 +1163,6 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
   if (active) {
     if (staged) g2p_gather_smem(g, T, st_old, vv, Cn);
     else g2p_gather(g, vel, px0, px1, px2, vv, Cn);
-    double F0[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) F0[i] = Fm[i * n_el + p];
     double G[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
