@@ -15,7 +15,9 @@ Fixtures (all numpy .npz):
                    indenter clouds + the default placed indenter.
   small_scene.npz  SMALL config, 200 substeps at v = (0, 0, -0.05) m/s:
                    full particle state, diagnostics, capture depth + image.
-  config1.npz      default config (dt 2e-6), 100 substeps (10 frames) at the
+  config3.npz      SMALL3 scene per config-3 shape (cylinder, ring, wave,
+                   dots): press then slide; full positions, F, image.
+  config1.npz      default config (dt 2e-6), 1000 substeps (100 frames) at the
                    default press velocity: surface-particle positions, a
                    seeded 4096-particle subset of x and F, diagnostics, the
                    640x480 capture image and depth.
@@ -32,7 +34,8 @@ sys.path.insert(0, ROOT)
 
 from oracle import refpy as R  # noqa: E402
 from tests.scenes import (CONFIG1, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
-                          SMALL, SMALL_STEPS, SMALL_V, render_inputs, sha)
+                          SMALL, SMALL3, SMALL3_PRESS, SMALL3_SHAPES, SMALL3_SLIDE, SMALL_STEPS,
+                          SMALL_V, render_inputs, sha)
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
@@ -95,6 +98,32 @@ def small_scene():
         surf_geom=np.array([surf["x0"], surf["y0"], surf["sx"], surf["sy"], surf["z0"]]))
 
 
+def config3():
+    """Config 3 shapes (press then slide), scaled (tests/scenes.py SMALL3)."""
+    out = {}
+    for shape in SMALL3_SHAPES:
+        sim = R.RefSim.from_config(SMALL3, shape, threads=0)
+        x0 = sim.state()["x"]
+        sim.step(SMALL3_PRESS[1], SMALL3_PRESS[0])
+        sim.step(SMALL3_SLIDE[1], SMALL3_SLIDE[0])
+        st = sim.state()
+        d = sim.diag()
+        depth, img = sim.capture(SMALL3, shape)
+        rng = np.random.default_rng(3)
+        sub = np.sort(rng.choice(sim.n, 2000, replace=False))
+        surf = sim.surface()["particle"]
+        out[f"{shape}_x0_sha"] = sha(x0)
+        out[f"{shape}_subset"] = sub
+        out[f"{shape}_x_subset"] = st["x"][sub]
+        out[f"{shape}_F_subset"] = st["F"][sub]
+        out[f"{shape}_x_surface"] = st["x"][surf]
+        out[f"{shape}_min_det_f"] = d["min_det_f"]
+        out[f"{shape}_step_count"] = d["step_count"]
+        out[f"{shape}_image"] = img
+        out[f"{shape}_depth_sample"] = depth[::8, ::8]
+    np.savez_compressed(os.path.join(OUT, "config3.npz"), **out)
+
+
 def config1():
     sim = R.RefSim.from_config(CONFIG1, "", threads=0)
     s0 = sim.state()
@@ -115,13 +144,15 @@ def config1():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "small", "config1"]
+    which = sys.argv[1:] or ["kat", "small", "config1", "config3"]
     if "kat" in which:
         kat()
     if "small" in which:
         small_scene()
     if "config1" in which:
         config1()
+    if "config3" in which:
+        config3()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

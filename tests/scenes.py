@@ -21,7 +21,7 @@ SMALL_V = (0.0, 0.0, -0.05)
 # Config 1 (BASELINE.json configs[0]): default gel 101x101x21, sphere 1e6 ->
 # 1e5 points, 256^3 / 33 mm, dt 2e-6, press velocity (0, 0, -0.01) m/s.
 CONFIG1 = {"time": {"dt_s": 2e-6}}
-CONFIG1_STEPS = 100
+CONFIG1_STEPS = 1000  # 100 frames (SURVEY §8(d) CI parity)
 CONFIG1_V = (0.0, 0.0, -0.01)
 
 # Config 2a (BASELINE.json configs[1]): same gel, sphere at the reference's
@@ -30,6 +30,20 @@ CONFIG2A = {"time": {"dt_s": 2e-6}, "indenter": {"target_points": 1000000}}
 CONFIG2A_V = (0.0, 0.0, -0.01)
 
 SUBSTEPS_PER_FRAME = 10  # scene_config.hpp:36, session.cpp:86
+
+# Config 3 (textured / defect indenters, press then slide), scaled so the
+# reference finishes in seconds: 10 x 10 x 1.2 mm gel on a 96^3 / 16 mm grid,
+# 4000-point indenters; press 150 substeps at 0.05 m/s, then slide +x.
+SMALL3 = {
+    "elastomer": {"size_mm": [10, 10, 1.2], "particle_counts": [51, 51, 7]},
+    "grid": {"nodes_per_axis": [96, 96, 96], "edge_mm": 16.0},
+    "time": {"dt_s": 2e-6},
+    "render": {"image_width": 320, "image_height": 240},
+    "indenter": {"source_points": 40000, "target_points": 4000, "gap_mm": 0.005},
+}
+SMALL3_SHAPES = ["cylinder", "cylinder_shell", "wave1", "dots"]
+SMALL3_PRESS = (150, (0.0, 0.0, -0.05))
+SMALL3_SLIDE = (150, (0.05, 0.0, 0.0))
 
 
 def render_inputs():
