@@ -131,9 +131,12 @@ def run_ours(args):
         dist.init_process_group("nccl")
     device = local
     torch.cuda.set_device(device)
-    # independent episode per rank: lateral offset on a 1 mm grid (harness.cpp:196-201)
-    off = ((rank % 3) - 1) * 1e-3, (((rank // 3) % 3) - 1) * 1e-3
-    s = tb.sim.build_sim(CONFIG2A, "", off[0], off[1], device=device)
+    # independent episode per rank (config-4 style pose draw; no collective)
+    from paper_2301_08343_b200 import episodes
+
+    ep = episodes.make_episode(rank) if world > 1 else episodes.Episode(0, 0.0, 0.0, 0.0, 0.0)
+    s = tb.sim.build_sim(episodes.episode_config(CONFIG2A, ep), "", ep.offset_x_m, ep.offset_y_m,
+                         device=device)
     n, n_el = s.n, s.elastomer_count
     rp = tb.render_params(CONFIG2A, "")
     v = np.array(CONFIG2A_V)
@@ -143,12 +146,12 @@ def run_ours(args):
         tb.mpm.step(s, v, SUBSTEPS_PER_FRAME)
         tb.sim.capture(s, params=rp, want_depth=False, want_image=False)
 
+    clocks = Clocks(device)  # sampler runs from before warm-up until after the timed regions
     for _ in range(args.warmup):
         frame_device()
     torch.cuda.synchronize(device)
 
     # --- timed region 1: device-resident (value) ---
-    clocks = Clocks(device)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(device)
@@ -187,11 +190,8 @@ def run_ours(args):
     per_substep, per_kernel = _algorithmic_bytes(n_el, n - n_el, window_nodes)
 
     if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([dev_ms, e2e_ms], device=f"cuda:{device}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms, e2e_ms = t.tolist()
+        dev_ms = episodes.max_over_ranks(dev_ms, device=f"cuda:{device}")
+        e2e_ms = episodes.max_over_ranks(e2e_ms, device=f"cuda:{device}")
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -208,6 +208,16 @@ def run_ours(args):
     substep_ms = (sum(v for k, v in phase_ms.items() if not k.endswith("_first")) +
                   (phase_ms.get("p2g_elastomer_first", 0) + phase_ms.get("p2g_indenter_first", 0)) /
                   SUBSTEPS_PER_FRAME)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f)
+        kname = {"g2p2g_elastomer": "k_g2p2g_gel", "grid_update": "k_grid_update_boxes",
+                 "indenter_move_p2g": "k_ind_cols"}.get(dom)
+        if kname in tr:
+            traffic = tr[kname]["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
@@ -222,7 +232,8 @@ def run_ours(args):
                 "wall_ms_per_step": e2e_wall / args.steps},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write per launch)",
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": per_kernel[dom],
                      "kernel_ms": dom_ms,
@@ -314,7 +325,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-frames", type=int, default=2)

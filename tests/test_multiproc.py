@@ -1,0 +1,63 @@
+"""Multi-process (world_size 2, gloo, CPU) coverage of the episode sharding
+and the max-over-ranks reporting collective used by bench.py --gpus N."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2301_08343_b200 import episodes as E
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n_episodes, out):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = E.shard(n_episodes, rank, world)
+    # each rank reports a different "device time"; the job time is the max
+    t = E.max_over_ranks(10.0 + rank)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine)
+    out[rank] = (mine, t, gathered)
+    dist.destroy_process_group()
+
+
+def test_sharding_over_two_ranks_with_gloo():
+    world, n = 2, 1024
+    port = _free_port()
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_worker, args=(world, port, n, out), nprocs=world, join=True)
+    shards = [out[r][0] for r in range(world)]
+    assert sorted(sum(shards, [])) == list(range(n))  # disjoint, complete
+    assert all(out[r][1] == 11.0 for r in range(world))  # max over ranks
+    assert out[0][2] == out[1][2] == shards
+
+
+def test_episode_draws_are_deterministic_and_in_range():
+    a, b = E.make_episode(7), E.make_episode(7)
+    assert a == b
+    for i in range(200):
+        ep = E.make_episode(i)
+        assert -1e-3 <= ep.offset_x_m <= 1e-3 and -1e-3 <= ep.offset_y_m <= 1e-3
+        assert 0 <= ep.z_rotation_rad < 6.2832
+        assert 0.1e-3 <= ep.depth_m <= 1.0e-3
+    cfg = E.episode_config({"time": {"dt_s": 2e-6}}, a)
+    assert cfg["indenter"]["z_rotation_rad"] == a.z_rotation_rad
+    # harness schedule: (gap + depth) / (v dt) substeps
+    assert E.press_substeps({"time": {"dt_s": 2e-6}}, E.Episode(0, 0, 0, 0, 0.5e-3)) == 30000
+
+
+def test_shard_rejects_bad_rank():
+    with pytest.raises(ValueError):
+        E.shard(8, 2, 2)
