@@ -34,6 +34,12 @@ namespace tacchi_b200 {
 
 namespace {
 
+// Programmatic dependent launch: the step-path kernels are launched with
+// programmatic stream serialization so each is dispatched while its
+// predecessor drains; this waits until the predecessor's writes are visible
+// (a no-op for ordinary launches).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void raise(Ctl* ctl, int code, int substep) {
   if (atomicCAS(&ctl->err_code, 0, code) == 0) ctl->err_substep = substep;
 }
@@ -454,6 +460,7 @@ __device__ bool in_range(const Geometry& g, const double* x) {
 }
 
 __global__ void k_finalize(Ctl* ctl, Geometry g, int mode) {
+  pdl_wait();
   const int s = ctl->substep;
   if (stale(ctl, s)) return;
   if (mode & kFinDiag) {  // particle_to_grid's min_det_f (engine.cpp:119,177)
@@ -805,6 +812,7 @@ __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
     int box_from_bb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ColSmem& S = *reinterpret_cast<ColSmem*>(smem_raw);
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = ctl->substep;
   if (stale(ctl, s)) return;
@@ -899,6 +907,7 @@ __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
 // call) times, then resets the per-call move counters.
 __global__ void k_ind_catchup(double* __restrict__ x, int64_t n, int64_t n_el,
                               uint8_t* __restrict__ moves, Ctl* ctl, Geometry g) {
+  pdl_wait();
   const int64_t p = n_el + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int total = ctl->substep - ctl->call_start;  // advects that completed in this call
@@ -985,6 +994,7 @@ __global__ void k_grid_update_window(double4* __restrict__ mp, double* __restric
 __global__ void k_grid_update_boxes(double4* __restrict__ mp, double* __restrict__ mi,
                                     double4* __restrict__ vel, Ctl* ctl, Geometry g,
                                     double m_ind) {
+  pdl_wait();
   if (stale(ctl, ctl->substep)) return;
   int lo[2][3], dm[2][3], vol[2];
   for (int m = 0; m < 2; ++m) {
@@ -1106,6 +1116,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     double vol0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   P2GTile& T = *reinterpret_cast<P2GTile*>(smem_raw);
+  pdl_wait();
   const int s = ctl->substep;
   if (stale_block(ctl, s)) return;
   const int64_t p = gel_particle(M, n_el);
@@ -1307,6 +1318,23 @@ __global__ void k_gather_box(const double4* __restrict__ mp, const double* __res
 // ---------------------------------------------------------------------------
 
 namespace {
+// cudaLaunchKernelEx with programmatic stream serialization (see pdl_wait).
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 constexpr int kThreads = 256;
 constexpr size_t kTileSmem = sizeof(P2GTile);
 constexpr size_t kIndSmem = sizeof(IndSmem);
@@ -1440,8 +1468,8 @@ int launch_p2g(DeviceSim& s, bool publish_diag) {
 
 int launch_grid_update(DeviceSim& s, int sms, bool zero) {
   if (zero)
-    k_grid_update_boxes<<<window_blocks(sms), kThreads, 0, s.stream>>>(
-        s.grid_mp, s.grid_mi, s.grid_v, s.ctl, s.geo, s.m_ind);
+    launch_pdl(k_grid_update_boxes, dim3(window_blocks(sms)), dim3(kThreads), 0, s.stream,
+               s.grid_mp, s.grid_mi, s.grid_v, s.ctl, s.geo, s.m_ind);
   else
     k_grid_update_window<<<window_blocks(sms), kThreads, 0, s.stream>>>(
         s.grid_mp, s.grid_mi, s.grid_v, s.ctl, s.geo, s.m_ind);
@@ -1454,9 +1482,9 @@ int launch_g2p2g_gel(DeviceSim& s, bool lookahead) {
   if (s.n_el <= 0) return 0;
   configure_once();
   if (lookahead)
-    k_g2p2g_gel<true, true, true><<<gel_blocks(s), kGelThreads, kTileSmem, s.stream>>>(
-        s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
-        s.m_el, s.vol_el);
+    launch_pdl(k_g2p2g_gel<true, true, true>, dim3(gel_blocks(s)), dim3(kGelThreads), kTileSmem,
+               s.stream, s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo,
+               s.grid_v, s.grid_mp, s.m_el, s.vol_el);
   else
     k_g2p2g_gel<true, true, false><<<gel_blocks(s), kGelThreads, 0, s.stream>>>(
         s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
@@ -1501,8 +1529,8 @@ int launch_ind_cols(DeviceSim& s, bool move) {
   }
   const unsigned blocks = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
   if (move)
-    k_ind_cols<true><<<blocks, kColWarps * 32, kColSmem, s.stream>>>(
-        s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 1);
+    launch_pdl(k_ind_cols<true>, dim3(blocks), dim3(kColWarps * 32), kColSmem, s.stream, s.x,
+               s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 1);
   else
     k_ind_cols<false><<<blocks, kColWarps * 32, kColSmem, s.stream>>>(
         s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 0);
@@ -1513,15 +1541,15 @@ int launch_ind_cols(DeviceSim& s, bool move) {
 
 int launch_ind_catchup(DeviceSim& s) {
   if (s.n_ind <= 0) return 0;
-  k_ind_catchup<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.ind_moves,
-                                                                s.ctl, s.geo);
+  launch_pdl(k_ind_catchup, dim3(blocks_for(s.n_ind)), dim3(kThreads), 0, s.stream, s.x, s.n,
+             s.n_el, s.ind_moves, s.ctl, s.geo);
   s.kernel_launches += 1;
   return 1;
 }
 
 int launch_finalize_step(DeviceSim& s) {
-  k_finalize<<<1, 1, 0, s.stream>>>(
-      s.ctl, s.geo, kFinDiag | kFinAdvect | kFinWindow | (s.n_ind > 0 ? kFinIndShift : 0));
+  launch_pdl(k_finalize, dim3(1), dim3(1), 0, s.stream, s.ctl, s.geo,
+             static_cast<int>(kFinDiag | kFinAdvect | kFinWindow | (s.n_ind > 0 ? kFinIndShift : 0)));
   s.kernel_launches += 1;
   return 1;
 }
