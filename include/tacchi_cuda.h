@@ -45,6 +45,9 @@ enum {
   TG_ERR_EMPTY_CLOUD = 9,       /* tacchi::EmptyCloud      errors.hpp:24 */
   TG_ERR_PARSE = 10,            /* tacchi::ParseError      errors.hpp:23 */
   TG_ERR_IO = 11,               /* tacchi::IoError         errors.hpp:39 */
+  TG_ERR_SESSION_NOT_INITIALIZED = 12, /* tacchi::SessionNotInitialized errors.hpp:34 */
+  TG_ERR_NON_MONOTONIC_TIME = 13,      /* tacchi::NonMonotonicTime      errors.hpp:35 */
+  TG_ERR_PROTOCOL = 14,                /* tacchi::ProtocolError         errors.hpp:36 */
   TG_ERR_CUDA = 20,             /* device / driver failure (no reference analogue) */
   TG_ERR_INVALID_ARGUMENT = 21  /* null handle / bad sizes (no reference analogue) */
 };
@@ -215,6 +218,23 @@ int64_t tg_kernel_launches(tg_handle h);
 int tg_set_graphs(tg_handle h, int enabled);
 const char* tg_last_error(void);
 const char* tg_version(void);
+
+/* ---- co-simulation bridge, protocol "tacchi/1" (§8 row f1) ---------------
+ * bridge::run_protocol (server.cpp:49-113) over in-memory lines: `input` is
+ * newline-separated JSON messages (init / step / end); the reply lines are
+ * returned in *output (malloc'd, release with tg_free). Each session runs
+ * on `device` through the B200 step + capture path and writes
+ * step_NNNNNN.png / .depth and steps.jsonl like bridge::Session
+ * (session.cpp:36-98). `base_config_json` is the SceneConfig used by an
+ * init without "config"/"config_path"; sessions without "session_dir" go to
+ * `session_root`/session_<k>. */
+int tg_bridge_run(int device, const char* base_config_json, const char* session_root,
+                  const char* input, char** output);
+/* bridge::serve_stdio (port < 0) or bridge::serve_tcp on 127.0.0.1:port
+ * (server.cpp:115-182); max_connections = 0 serves forever. */
+int tg_bridge_serve(int device, const char* base_config_json, const char* session_root,
+                    int port, int max_connections);
+void tg_free(void* p);
 
 #ifdef __cplusplus
 }

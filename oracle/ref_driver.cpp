@@ -21,7 +21,12 @@
 #include <string>
 #include <vector>
 
+#include <cstdio>
+#include <cstdlib>
+#include <sstream>
+
 #include "oracle/reference_mpm.hpp"
+#include "tacchi/bridge/server.hpp"
 #include "tacchi/config/scene_config.hpp"
 #include "tacchi/errors.hpp"
 #include "tacchi/geo/particle_set.hpp"
@@ -37,11 +42,19 @@
 
 using namespace tacchi;
 
-// PNG I/O (render/image.cpp) needs libpng, which is absent here; the hot path
-// never calls it. Stubs keep the link closed.
+// PNG I/O (render/image.cpp) needs libpng, which is absent here. The hot path
+// never calls it; the bridge (session.cpp:47) does, so save_png is replaced by
+// a writer of the same pixels in binary PPM ("P6 w h 255" + RGB rows) under
+// the requested name — the bridge parity test decodes both formats and
+// compares pixels.
 namespace tacchi::render {
-void save_png(const Image8&, const std::filesystem::path& path) {
-  throw IoError("save_png unavailable in the oracle build: " + path.string());
+void save_png(const Image8& image, const std::filesystem::path& path) {
+  if (image.width <= 0 || image.height <= 0) throw IoError("save_png: empty image");
+  std::FILE* f = std::fopen(path.string().c_str(), "wb");
+  if (!f) throw IoError("cannot write " + path.string());
+  std::fprintf(f, "P6\n%d %d\n255\n", image.width, image.height);
+  std::fwrite(image.data.data(), 1, image.data.size(), f);
+  std::fclose(f);
 }
 Image8 load_png(const std::filesystem::path& path) {
   throw IoError("load_png unavailable in the oracle build: " + path.string());
@@ -413,3 +426,25 @@ int ref_oracle_step(long n, double* x, double* v, double* C, double* F, const do
 }
 
 }  // extern "C"
+
+// bridge::run_protocol (server.cpp:49-113) over in-memory lines, with the
+// SceneConfig base parsed from `base_json`; replies returned malloc'd in *out.
+extern "C" int ref_bridge_run(const char* base_json, const char* session_root, const char* input,
+                              char** out) {
+  return guard([&] {
+    const config::SceneConfig base = config::from_json_string(base_json ? base_json : "{}");
+    std::istringstream in(input ? input : "");
+    std::string replies;
+    bridge::run_protocol(
+        [&in](std::string& l) { return static_cast<bool>(std::getline(in, l)); },
+        [&replies](const std::string& l) {
+          replies += l;
+          replies += '\n';
+        },
+        base, session_root ? session_root : ".");
+    *out = static_cast<char*>(std::malloc(replies.size() + 1));
+    std::memcpy(*out, replies.c_str(), replies.size() + 1);
+  });
+}
+
+extern "C" void ref_free(void* p) { std::free(p); }

@@ -240,6 +240,31 @@ def generate_cloud(shape, n, seed):
     return out
 
 
+def bridge_run(messages, base_cfg=None, session_root="."):
+    """The reference's bridge::run_protocol over in-memory lines; parsed replies.
+    Images are written as binary PPM under the .png name (ref_driver.cpp)."""
+    L = lib()
+    L.ref_bridge_run.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]
+    L.ref_free.argtypes = [C.c_void_p]
+    lines = [m if isinstance(m, str) else json.dumps(m) for m in messages]
+    out = C.c_void_p()
+    _check(L.ref_bridge_run(cfg_json(base_cfg), session_root.encode(),
+                            ("\n".join(lines) + "\n").encode(), C.byref(out)))
+    try:
+        text = C.string_at(out.value).decode()
+    finally:
+        L.ref_free(out)
+    return [json.loads(x) for x in text.splitlines() if x]
+
+
+def load_ppm(path):
+    with open(path, "rb") as f:
+        data = f.read()
+    parts = data.split(b"\n", 3)
+    w, h = map(int, parts[1].split())
+    return np.frombuffer(parts[3], dtype=np.uint8)[: w * h * 3].reshape(h, w, 3)
+
+
 def placed_indenter(cfg=None, obj="", off_x=0.0, off_y=0.0):
     n = C.c_long()
     _check(lib().ref_placed_indenter(cfg_json(cfg), obj.encode(), off_x, off_y, None, C.byref(n)))

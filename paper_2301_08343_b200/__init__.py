@@ -43,11 +43,15 @@ class ConfigError(Error): ...
 class IoError(Error): ...
 class CudaError(Error): ...
 class InvalidArgument(Error): ...
+class SessionNotInitialized(Error): ...
+class NonMonotonicTime(Error): ...
+class ProtocolError(Error): ...
 
 
 ERRORS = {1: GridTooSmall, 2: EmptyScene, 3: OutOfGrid, 4: DegenerateF, 5: ConfigError,
           6: NoSurface, 7: CropOutOfBounds, 8: ShapeMismatch, 9: EmptyCloud, 10: ParseError,
-          11: IoError, 20: CudaError, 21: InvalidArgument}
+          11: IoError, 12: SessionNotInitialized, 13: NonMonotonicTime, 14: ProtocolError,
+          20: CudaError, 21: InvalidArgument}
 
 PHASES = dict(zero_grid=0, particle_to_grid=1, grid_update=2, grid_to_particle=3,
               apply_boundary=4, advect=5)
@@ -150,6 +154,10 @@ def lib():
         L.tg_generate_cloud.argtypes = [C.c_char_p, C.c_int64, C.c_uint64, _dp]
         L.tg_placed_indenter.argtypes = [C.c_char_p, C.c_char_p, C.c_double, C.c_double, _dp,
                                          _i64p]
+        L.tg_bridge_run.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_char_p,
+                                    C.POINTER(C.c_void_p)]
+        L.tg_bridge_serve.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_int, C.c_int]
+        L.tg_free.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -446,6 +454,91 @@ class geo:  # noqa: N801 — mirrors tacchi::geo (host setup)
         _check(lib().tg_placed_indenter(_cfg(cfg), obj.encode(), offset_x, offset_y, _p(out),
                                         C.byref(n)))
         return out
+
+
+class bridge:  # noqa: N801 — mirrors tacchi::bridge (server.hpp, session.hpp)
+    """Co-simulation protocol "tacchi/1" over the B200 path (§8 row f1)."""
+
+    @staticmethod
+    def run_protocol(messages, base_cfg=None, session_root: str = ".", device: int = 0) -> list:
+        """bridge::run_protocol (server.cpp:49-113) over in-memory lines.
+
+        `messages` are dicts (serialised with json.dumps) or raw strings; the
+        reply lines come back parsed."""
+        lines = [m if isinstance(m, str) else json.dumps(m) for m in messages]
+        out = C.c_void_p()
+        _check(lib().tg_bridge_run(device, _cfg(base_cfg), session_root.encode(),
+                                   ("\n".join(lines) + "\n").encode(), C.byref(out)))
+        try:
+            text = C.string_at(out.value).decode()
+        finally:
+            lib().tg_free(out)
+        return [json.loads(l) for l in text.splitlines() if l]
+
+    @staticmethod
+    def serve(base_cfg=None, session_root: str = ".", port: int = -1, max_connections: int = 0,
+              device: int = 0):
+        """serve_stdio (port < 0) or serve_tcp on 127.0.0.1:port (server.cpp:115-182)."""
+        _check(lib().tg_bridge_serve(device, _cfg(base_cfg), session_root.encode(), port,
+                                     max_connections))
+
+
+def load_depth_map(path: str):
+    """render::load_depth_map (depth_map.cpp:40-60): (values HxW float64, pixel_to_meter)."""
+    with open(path, "rb") as f:
+        header = json.loads(f.readline())
+        w, h = header["width"], header["height"]
+        buf = np.frombuffer(f.read(), dtype=np.float32)
+    if w <= 0 or h <= 0 or buf.size < w * h:
+        raise ParseError(f"{path}: bad depth map")
+    return buf[: w * h].astype(np.float64).reshape(h, w), header["pixel_to_meter"]
+
+
+def load_png(path: str) -> np.ndarray:
+    """Decodes an 8-bit RGB, non-interlaced PNG (what the bridge writes) to HxWx3."""
+    import struct
+    import zlib
+
+    with open(path, "rb") as f:
+        data = f.read()
+    if data[:8] != b"\x89PNG\r\n\x1a\n":
+        raise ParseError(f"not a PNG: {path}")
+    pos, idat, w, h = 8, b"", 0, 0
+    while pos < len(data):
+        (n,) = struct.unpack(">I", data[pos:pos + 4])
+        kind, body = data[pos + 4:pos + 8], data[pos + 8:pos + 8 + n]
+        if kind == b"IHDR":
+            w, h, depth, ctype = struct.unpack(">IIBB", body[:10])
+            if depth != 8 or ctype != 2:
+                raise ParseError(f"unsupported PNG layout: {path}")
+        elif kind == b"IDAT":
+            idat += body
+        pos += 12 + n
+    raw = np.frombuffer(zlib.decompress(idat), dtype=np.uint8).reshape(h, 1 + 3 * w)
+    img = np.zeros((h, 3 * w), dtype=np.int32)
+    prev = np.zeros(3 * w, dtype=np.int32)
+    for r in range(h):  # PNG filters (RFC 2083 §6)
+        ft, line = raw[r, 0], raw[r, 1:].astype(np.int32)
+        cur = line.copy() if ft == 0 else (line + prev) & 255 if ft == 2 else np.zeros_like(line)
+        for i in range(3 * w) if ft not in (0, 2) else ():
+            a = cur[i - 3] if i >= 3 else 0
+            b = prev[i]
+            c = prev[i - 3] if i >= 3 else 0
+            if ft == 0:
+                p = 0
+            elif ft == 1:
+                p = a
+            elif ft == 2:
+                p = b
+            elif ft == 3:
+                p = (a + b) // 2
+            else:
+                pa, pb, pc = abs(b - c), abs(a - c), abs(a + b - 2 * c)
+                p = a if pa <= pb and pa <= pc else (b if pb <= pc else c)
+            cur[i] = (line[i] + p) & 255
+        img[r] = cur
+        prev = cur
+    return img.astype(np.uint8).reshape(h, w, 3)
 
 
 def version() -> str:

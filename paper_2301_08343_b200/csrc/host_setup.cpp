@@ -19,11 +19,13 @@
 
 #include "tacchi_cuda.h"
 
+#include "host_config.hpp"
+
 namespace tacchi_b200 {
 int fail(int code, const std::string& msg);
 }
 
-namespace {
+namespace tacchi_b200::host {
 
 using tacchi_b200::fail;
 using json = nlohmann::json;
@@ -31,46 +33,6 @@ using json = nlohmann::json;
 struct V3 {
   double x = 0, y = 0, z = 0;
   double operator[](int a) const { return a == 0 ? x : (a == 1 ? y : z); }
-};
-
-struct HostError {
-  int code;
-  std::string msg;
-};
-
-[[noreturn]] void raise(int code, const std::string& msg) { throw HostError{code, msg}; }
-
-// ---- SceneConfig (scene_config.hpp:19-94), defaults of default_config() ---
-
-struct Light {
-  double dir[3], diffuse[3], specular[3];
-};
-
-struct Config {
-  double size_mm[3] = {20.0, 20.0, 4.0};
-  int counts[3] = {101, 101, 21};
-  double E = 1.45e5, nu = 0.45, rho = 1000.0;
-  int fixed_bottom_layers = 2;
-  int nodes[3] = {256, 256, 256};
-  double edge_mm = 33.0;
-  double dt = 1e-4;
-  int substeps_per_control_step = 10;
-  double press_speed_mm_s = 10.0;
-  std::string cloud_path, generated_shape = "sphere";
-  uint64_t source_points = 1000000, target_points = 100000, seed = 20230115;
-  double gap_mm = 0.1, z_rotation_rad = 0.0, rigid_mass_scale = 80.0;
-  std::vector<Light> lights;
-  double ka = 1.0, kd = 0.55, ks = 0.25, shininess = 24.0;
-  double ambient[3] = {0.34, 0.37, 0.44};
-  double view[3] = {0, 0, -1};
-  double pixel_to_meter = 2.8125e-5;
-  int image_w = 640, image_h = 480;
-  std::string background_image;
-  struct Align {
-    double ox = 0, oy = 0, scale = 1.0;
-  };
-  std::map<std::string, Align> alignment;
-  double gravity_mps2 = 0.0;
 };
 
 // scene_config.cpp:42-57: three tinted lights, 120 deg apart, 45 deg elevation.
@@ -117,6 +79,8 @@ void normalize(double* v) {  // Eigen normalized(): v / sqrt(squaredNorm) if > 0
     v[0] /= n; v[1] /= n; v[2] /= n;
   }
 }
+
+[[noreturn]] void raise(int code, const std::string& msg) { throw HostError{code, msg}; }
 
 // from_json_string (scene_config.cpp:187-257): partial overrides of defaults.
 Config parse_config(const char* text) {
@@ -192,6 +156,17 @@ Config parse_config(const char* text) {
         c.alignment[it.key()] = a;
       }
     }
+    if (j.contains("press_grid")) {
+      const json& p = j["press_grid"];
+      read(p, "positions_x", c.positions_x);
+      read(p, "positions_y", c.positions_y);
+      read(p, "step_mm", c.step_mm);
+      if (p.contains("depths_mm")) c.depths_mm = p["depths_mm"].get<std::vector<double>>();
+    }
+    if (j.contains("objects")) c.objects = j["objects"].get<std::vector<std::string>>();
+    read(j, "output_dir", c.output_dir);
+    read(j, "deterministic", c.deterministic);
+    read(j, "workers", c.workers);
     read(j, "gravity_mps2", c.gravity_mps2);
   } catch (const json::exception& e) {
     raise(TG_ERR_CONFIG, std::string("config: ") + e.what());
@@ -352,6 +327,11 @@ bool make_shape(const std::string& name, Shape& s) {
     return false;
   }
   return true;
+}
+
+bool is_known_shape(const std::string& name) {
+  Shape s;
+  return make_shape(name, s);
 }
 
 // generate_shape_cloud (shapes.cpp:231-249): rejection sampling, mm -> m.
@@ -580,7 +560,9 @@ int guarded(F&& f) {
   }
 }
 
-}  // namespace
+}  // namespace tacchi_b200::host
+
+using namespace tacchi_b200::host;
 
 extern "C" {
 

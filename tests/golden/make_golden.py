@@ -17,6 +17,10 @@ Fixtures (all numpy .npz):
                    full particle state, diagnostics, capture depth + image.
   config3.npz      SMALL3 scene per config-3 shape (cylinder, ring, wave,
                    dots): press then slide; full positions, F, image.
+  bridge.npz       the reference's bridge (server.cpp / session.cpp) driven
+                   by tests/scenes.bridge_script on the SMALL scene, plus the
+                   init errors of BAD_CONFIGS: replies, steps.jsonl, the
+                   .depth files (bytes) and the images (pixels).
   config1.npz      default config (dt 2e-6), 1000 substeps (100 frames) at the
                    default press velocity: surface-particle positions, a
                    seeded 4096-particle subset of x and F, diagnostics, the
@@ -33,7 +37,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import refpy as R  # noqa: E402
-from tests.scenes import (CONFIG1, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
+from tests.scenes import (BAD_CONFIGS, CONFIG1, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
                           SMALL, SMALL3, SMALL3_PRESS, SMALL3_SHAPES, SMALL3_SLIDE, SMALL_STEPS,
                           SMALL_V, render_inputs, sha)
 
@@ -143,8 +147,38 @@ def config1():
         depth_sample=depth[::16, ::16])
 
 
+def bridge():
+    import json
+    import shutil
+    import tempfile
+
+    root = tempfile.mkdtemp(prefix="tacchi_bridge_")
+    try:
+        sdir = os.path.join(root, "s0")
+        replies = R.bridge_run(bridge_script(sdir), session_root=root)
+        bad = R.bridge_run([{"type": "init", "config": c} for c in BAD_CONFIGS] + [{"type": "end"}],
+                           session_root=root)
+        with open(os.path.join(sdir, "steps.jsonl")) as f:
+            steps_jsonl = f.read().replace(sdir, "<dir>")
+        arrays = {}
+        for r in replies:
+            if r.get("type") == "reply" and r["image"]:
+                k = r["step"]
+                with open(r["depth_map"], "rb") as f:
+                    arrays[f"depth_{k}"] = np.frombuffer(f.read(), dtype=np.uint8)
+                arrays[f"image_{k}"] = R.load_ppm(r["image"])
+        np.savez_compressed(
+            os.path.join(OUT, "bridge.npz"),
+            replies=json.dumps(replies).replace(sdir, "<dir>"), bad_configs=json.dumps(bad),
+            steps_jsonl=steps_jsonl, **arrays)
+    finally:
+        shutil.rmtree(root)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "small", "config1", "config3"]
+    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "bridge"]
+    if "bridge" in which:
+        bridge()
     if "kat" in which:
         kat()
     if "small" in which:

@@ -82,3 +82,49 @@ def sha(a) -> str:
     import numpy as np
 
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# Bridge session script (§8 row f1, protocol "tacchi/1", server.cpp:49-113):
+# velocity and position commands, a non-monotonic sim_time, an image request
+# before and at the terminal depth, a frozen step after it, protocol errors.
+# SMALL scene, 10 substeps per control step (2e-5 s), gap 0.02 mm.
+BRIDGE_MAX_DEPTH = 2.0e-5
+
+
+def bridge_script(session_dir: str):
+    return [
+        {"type": "step", "vector": [0, 0, 0]},
+        "not json",
+        {"type": "init", "config": SMALL, "max_depth_m": BRIDGE_MAX_DEPTH,
+         "session_dir": session_dir},
+        {"type": "step", "mode": "velocity", "vector": [0.0, 0.0, -0.5], "sim_time": 0.0,
+         "request_image": True},
+        {"type": "step", "mode": "position", "vector": [0.0, 0.0, -2.5e-5], "sim_time": 2e-5},
+        {"type": "step", "mode": "velocity", "vector": [0.0, 0.0, -0.5], "sim_time": 1e-5},
+        {"type": "step", "mode": "sideways", "vector": [0.0, 0.0, -0.5]},
+        {"type": "step", "mode": "velocity", "vector": [0.0, 0.0]},
+        {"type": "step", "mode": "velocity", "vector": [0.0, 0.0, -0.5], "sim_time": 4e-5,
+         "request_image": True},
+        {"type": "step", "mode": "position", "vector": [0.0, 0.0, -9e-5], "request_image": True},
+        {"type": "step", "mode": "velocity", "vector": [0.0, 0.0, -0.5], "sim_time": 6e-5},
+        {"type": "step", "mode": "velocity", "vector": [0.0, 0.0, float("nan")]},
+        {"type": "end"},
+    ]
+
+
+# SceneConfig::validate failures (scene_config.cpp:83-116) reported by init.
+BAD_CONFIGS = [
+    {"elastomer": {"poisson_ratio": 0.5}},
+    {"elastomer": {"youngs_modulus_pa": 0.0}},
+    {"elastomer": {"density_kg_m3": -1.0}},
+    {"elastomer": {"particle_counts": [1, 5, 5]}},
+    {"grid": {"nodes_per_axis": [7, 64, 64]}},
+    {"time": {"substeps_per_control_step": 0}},
+    {"indenter": {"generated_shape": "no_such_shape"}},
+    {"press_grid": {"depths_mm": []}},
+    {"press_grid": {"positions_x": 0}},
+    {"time": {"dt_s": 0.0}},
+    {"lights": []},
+    {"render": {"image_width": 1}},
+    {"elastomer": {"fixed_bottom_layers": 21}},
+]
