@@ -17,6 +17,9 @@ Fixtures (all numpy .npz):
                    full particle state, diagnostics, capture depth + image.
   config3.npz      SMALL3 scene per config-3 shape (cylinder, ring, wave,
                    dots): press then slide; full positions, F, image.
+  config5.npz      large-area gel (848,421 + 1e5 particles, 512^3 grid):
+                   50 substeps pressing + 30 moving laterally; seeded
+                   4096-particle subset, every 7th surface particle, image.
   bridge.npz       the reference's bridge (server.cpp / session.cpp) driven
                    by tests/scenes.bridge_script on the SMALL scene, plus the
                    init errors of BAD_CONFIGS: replies, steps.jsonl, the
@@ -37,7 +40,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import refpy as R  # noqa: E402
-from tests.scenes import (BAD_CONFIGS, CONFIG1, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
+from tests.scenes import (BAD_CONFIGS, CONFIG1, CONFIG5, CONFIG5_MOVE, CONFIG5_PRESS, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
                           SMALL, SMALL3, SMALL3_PRESS, SMALL3_SHAPES, SMALL3_SLIDE, SMALL_STEPS,
                           SMALL_V, render_inputs, sha)
 
@@ -147,6 +150,26 @@ def config1():
         depth_sample=depth[::16, ::16])
 
 
+def config5():
+    sim = R.RefSim.from_config(CONFIG5, "", threads=0)
+    s0 = sim.state()
+    sim.step(CONFIG5_PRESS[1], CONFIG5_PRESS[0])
+    sim.step(CONFIG5_MOVE[1], CONFIG5_MOVE[0])
+    s1 = sim.state()
+    d = sim.diag()
+    depth, img = sim.capture(CONFIG5)
+    surf = sim.surface()
+    rng = np.random.default_rng(5)
+    subset = np.sort(rng.choice(sim.n, 4096, replace=False))
+    np.savez_compressed(
+        os.path.join(OUT, "config5.npz"), n=sim.n, n_elastomer=sim.n_elastomer,
+        x0_hash=sha(s0["x"]), subset=subset, x0_subset=s0["x"][subset],
+        x_subset=s1["x"][subset], F_subset=s1["F"][subset],
+        x_surface=s1["x"][surf["particle"]][::7], min_det_f=d["min_det_f"],
+        max_speed=d["max_speed"], step_count=d["step_count"], image=img,
+        depth_sample=depth[::16, ::16])
+
+
 def bridge():
     import json
     import shutil
@@ -176,7 +199,9 @@ def bridge():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "bridge"]
+    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge"]
+    if "config5" in which:
+        config5()
     if "bridge" in which:
         bridge()
     if "kat" in which:

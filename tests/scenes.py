@@ -31,6 +31,17 @@ CONFIG2A_V = (0.0, 0.0, -0.01)
 
 SUBSTEPS_PER_FRAME = 10  # scene_config.hpp:36, session.cpp:86
 
+# Config 5 (BASELINE.json configs[4]): large-area gel 40 x 40 x 4 mm at the
+# same 0.2 mm spacing (201 x 201 x 21 = 848,421 gel particles) + sphere 1e5,
+# 512^3 grid of 66 mm edge (same dx as config 1). The parity slice is short
+# enough for the CPU reference (80 substeps, ~30 s): gap 2 um, press at
+# 0.3 m/s, then move the indenter laterally while pressed.
+CONFIG5 = {"elastomer": {"size_mm": [40, 40, 4], "particle_counts": [201, 201, 21]},
+           "grid": {"nodes_per_axis": [512, 512, 512], "edge_mm": 66.0},
+           "time": {"dt_s": 2e-6}, "indenter": {"gap_mm": 0.002}}
+CONFIG5_PRESS = (50, (0.0, 0.0, -0.3))
+CONFIG5_MOVE = (30, (0.3, 0.1, 0.0))
+
 # Config 3 (textured / defect indenters, press then slide), scaled so the
 # reference finishes in seconds: 10 x 10 x 1.2 mm gel on a 96^3 / 16 mm grid,
 # 4000-point indenters; press 150 substeps at 0.05 m/s, then slide +x.

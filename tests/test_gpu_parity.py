@@ -252,6 +252,35 @@ def test_config3_press_and_slide_match_reference(tb, golden, shape):
     assert np.abs(img.astype(int) - g[f"{shape}_image"]).max() <= 2
 
 
+def test_config5_large_gel_matches_reference(tb, golden):
+    """Config 5 (large-area gel, 948,421 particles, 512^3 grid): press then
+    move laterally vs the reference (tests/scenes.py CONFIG5)."""
+    from tests.scenes import CONFIG5, CONFIG5_MOVE, CONFIG5_PRESS
+
+    g = golden("config5.npz")
+    s = tb.sim.build_sim(CONFIG5)
+    assert s.n == int(g["n"]) and s.elastomer_count == int(g["n_elastomer"])
+    x0 = s.positions()
+    assert sha(x0) == str(g["x0_hash"])
+    tb.mpm.step(s, CONFIG5_PRESS[1], CONFIG5_PRESS[0])
+    tb.mpm.step(s, CONFIG5_MOVE[1], CONFIG5_MOVE[0])
+    st = s.state()
+    sub = g["subset"]
+    disp = np.abs(g["x_subset"] - x0[sub]).max()
+    assert disp > 1e-5
+    assert np.abs(st["x"][sub] - g["x_subset"]).max() <= 1e-8 * disp
+    surf = _default_surface(201, 201, 21)[::7]
+    assert np.abs(st["x"][surf] - g["x_surface"]).max() <= 1e-8 * disp
+    np.testing.assert_allclose(st["F"][sub], g["F_subset"], rtol=0, atol=1e-11)
+    d = s.diag
+    assert d.step_count == int(g["step_count"])
+    assert d.min_det_f == pytest.approx(float(g["min_det_f"]), abs=1e-12)
+    assert d.max_speed == pytest.approx(float(g["max_speed"]), rel=1e-9)
+    depth, img = tb.sim.capture(s, CONFIG5)
+    assert np.abs(depth[::16, ::16] - g["depth_sample"]).max() <= 1e-7
+    assert np.abs(img.astype(int) - g["image"]).max() <= 2
+
+
 def test_config2a_conserves_mass_and_momentum(tb):
     """Config 2a (1,214,221 particles): size-independent P2G invariants
     (SPEC.md:147-148): sum of node mass = sum of particle mass; with zero
