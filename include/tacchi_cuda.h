@@ -45,9 +45,10 @@ enum {
   TG_ERR_EMPTY_CLOUD = 9,       /* tacchi::EmptyCloud      errors.hpp:24 */
   TG_ERR_PARSE = 10,            /* tacchi::ParseError      errors.hpp:23 */
   TG_ERR_IO = 11,               /* tacchi::IoError         errors.hpp:39 */
-  TG_ERR_SESSION_NOT_INITIALIZED = 12, /* tacchi::SessionNotInitialized errors.hpp:34 */
-  TG_ERR_NON_MONOTONIC_TIME = 13,      /* tacchi::NonMonotonicTime      errors.hpp:35 */
-  TG_ERR_PROTOCOL = 14,                /* tacchi::ProtocolError         errors.hpp:36 */
+  TG_ERR_SESSION_NOT_INITIALIZED = 12, /* tacchi::SessionNotInitialized errors.hpp:32 */
+  TG_ERR_NON_MONOTONIC_TIME = 13,      /* tacchi::NonMonotonicTime      errors.hpp:33 */
+  TG_ERR_PROTOCOL = 14,                /* tacchi::ProtocolError         errors.hpp:34 */
+  TG_ERR_MANIFEST_MISMATCH = 15,       /* tacchi::ManifestMismatch      errors.hpp:37 */
   TG_ERR_CUDA = 20,             /* device / driver failure (no reference analogue) */
   TG_ERR_INVALID_ARGUMENT = 21  /* null handle / bad sizes (no reference analogue) */
 };
@@ -235,6 +236,28 @@ int tg_bridge_run(int device, const char* base_config_json, const char* session_
 int tg_bridge_serve(int device, const char* base_config_json, const char* session_root,
                     int port, int max_connections);
 void tg_free(void* p);
+
+/* ---- dataset harness and metrics (§8 rows f2, f4) ------------------------
+ * dataset::run_press_dataset (harness.cpp:159-245): every object of the
+ * SceneConfig at every press-grid position, pressed at press_speed_mm_s with
+ * one capture per depth level -> out_dir/{config.json, manifest.csv,
+ * images/*.png, depth/*.depth}; complete (object, position) groups of an
+ * existing manifest are kept (resume). `batch` simulations are stepped
+ * together on `device` (0: config "workers", else 16). */
+int tg_run_press_dataset(int device, const char* config_json, const char* out_dir, int batch,
+                         int64_t* rows, int64_t* skipped_positions);
+/* dataset::compare_datasets (harness.cpp:247-321); out[7] = pairs, ssim
+ * mean/std, psnr mean/std, mae mean/std; per-pair CSV when csv_out != "". */
+int tg_compare_datasets(int device, const char* dir_a, const char* dir_b, const char* csv_out,
+                        double* out);
+/* metrics::ssim / psnr / mae (image_metrics.cpp:57-112) for `count` pairs of
+ * h x w x 3 uint8 images (pair-major) in one device launch; out: count x 3. */
+int tg_image_metrics(int device, const uint8_t* a, const uint8_t* b, int w, int h, int count,
+                     double* out);
+/* render::load_png / save_png (image.cpp:23-90); load with rgb == NULL
+ * queries the size. */
+int tg_load_png(const char* path, uint8_t* rgb, int* w, int* h);
+int tg_save_png(const char* path, const uint8_t* rgb, int w, int h);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,8 @@
 
 #include "oracle/reference_mpm.hpp"
 #include "tacchi/bridge/server.hpp"
+#include "tacchi/dataset/harness.hpp"
+#include "tacchi/metrics/image_metrics.hpp"
 #include "tacchi/config/scene_config.hpp"
 #include "tacchi/errors.hpp"
 #include "tacchi/geo/particle_set.hpp"
@@ -78,6 +80,10 @@ int code_of(const std::exception& e) {
   if (dynamic_cast<const EmptyCloud*>(&e)) return 9;
   if (dynamic_cast<const ParseError*>(&e)) return 10;
   if (dynamic_cast<const IoError*>(&e)) return 11;
+  if (dynamic_cast<const SessionNotInitialized*>(&e)) return 12;
+  if (dynamic_cast<const NonMonotonicTime*>(&e)) return 13;
+  if (dynamic_cast<const ProtocolError*>(&e)) return 14;
+  if (dynamic_cast<const ManifestMismatch*>(&e)) return 15;
   return 99;
 }
 
@@ -448,3 +454,28 @@ extern "C" int ref_bridge_run(const char* base_json, const char* session_root, c
 }
 
 extern "C" void ref_free(void* p) { std::free(p); }
+
+// dataset::run_press_dataset (harness.cpp:159-245); images land as PPM under
+// their .png names (save_png above).
+extern "C" int ref_run_press_dataset(const char* cfg_json, const char* out_dir, long* rows,
+                                     long* skipped) {
+  return guard([&] {
+    const config::SceneConfig cfg = config::from_json_string(cfg_json ? cfg_json : "{}");
+    const dataset::DatasetResult r = dataset::run_press_dataset(cfg, out_dir);
+    *rows = static_cast<long>(r.rows);
+    *skipped = static_cast<long>(r.skipped_positions);
+  });
+}
+
+// metrics::compare (image_metrics.cpp:110-112) on two h x w x 3 images.
+extern "C" int ref_image_metrics(const uint8_t* a, const uint8_t* b, int w, int h, double* out) {
+  return guard([&] {
+    render::Image8 ia(w, h), ib(w, h);
+    std::memcpy(ia.data.data(), a, static_cast<size_t>(w) * h * 3);
+    std::memcpy(ib.data.data(), b, static_cast<size_t>(w) * h * 3);
+    const metrics::MetricReport m = metrics::compare(ia, ib);
+    out[0] = m.ssim;
+    out[1] = m.psnr_db;
+    out[2] = m.mae_pct;
+  });
+}

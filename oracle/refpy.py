@@ -257,6 +257,27 @@ def bridge_run(messages, base_cfg=None, session_root="."):
     return [json.loads(x) for x in text.splitlines() if x]
 
 
+def run_press_dataset(cfg, out_dir):
+    """The reference's dataset::run_press_dataset; returns (rows, skipped)."""
+    L = lib()
+    L.ref_run_press_dataset.argtypes = [C.c_char_p, C.c_char_p, _lp, _lp]
+    rows, skipped = C.c_long(), C.c_long()
+    _check(L.ref_run_press_dataset(cfg_json(cfg), str(out_dir).encode(), C.byref(rows),
+                                   C.byref(skipped)))
+    return rows.value, skipped.value
+
+
+def image_metrics(a, b):
+    """metrics::compare -> (ssim, psnr_db, mae_pct)."""
+    L = lib()
+    L.ref_image_metrics.argtypes = [_u8p, _u8p, C.c_int, C.c_int, _dp]
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    b = np.ascontiguousarray(b, dtype=np.uint8)
+    out = np.zeros(3)
+    _check(L.ref_image_metrics(_p(a, _u8p), _p(b, _u8p), a.shape[1], a.shape[0], _p(out)))
+    return tuple(out)
+
+
 def load_ppm(path):
     with open(path, "rb") as f:
         data = f.read()

@@ -46,12 +46,13 @@ class InvalidArgument(Error): ...
 class SessionNotInitialized(Error): ...
 class NonMonotonicTime(Error): ...
 class ProtocolError(Error): ...
+class ManifestMismatch(Error): ...
 
 
 ERRORS = {1: GridTooSmall, 2: EmptyScene, 3: OutOfGrid, 4: DegenerateF, 5: ConfigError,
           6: NoSurface, 7: CropOutOfBounds, 8: ShapeMismatch, 9: EmptyCloud, 10: ParseError,
           11: IoError, 12: SessionNotInitialized, 13: NonMonotonicTime, 14: ProtocolError,
-          20: CudaError, 21: InvalidArgument}
+          15: ManifestMismatch, 20: CudaError, 21: InvalidArgument}
 
 PHASES = dict(zero_grid=0, particle_to_grid=1, grid_update=2, grid_to_particle=3,
               apply_boundary=4, advect=5)
@@ -158,6 +159,12 @@ def lib():
                                     C.POINTER(C.c_void_p)]
         L.tg_bridge_serve.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_int, C.c_int]
         L.tg_free.argtypes = [C.c_void_p]
+        L.tg_run_press_dataset.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_int, _i64p,
+                                           _i64p]
+        L.tg_compare_datasets.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_char_p, _dp]
+        L.tg_image_metrics.argtypes = [C.c_int, _u8p, _u8p, C.c_int, C.c_int, C.c_int, _dp]
+        L.tg_load_png.argtypes = [C.c_char_p, _u8p, _ip, _ip]
+        L.tg_save_png.argtypes = [C.c_char_p, _u8p, C.c_int, C.c_int]
         _lib = L
     return _lib
 
@@ -495,50 +502,62 @@ def load_depth_map(path: str):
 
 
 def load_png(path: str) -> np.ndarray:
-    """Decodes an 8-bit RGB, non-interlaced PNG (what the bridge writes) to HxWx3."""
-    import struct
-    import zlib
+    """render::load_png (image.cpp:51-90) -> H x W x 3 uint8."""
+    w, h = C.c_int(), C.c_int()
+    _check(lib().tg_load_png(path.encode(), None, C.byref(w), C.byref(h)))
+    out = np.empty((h.value, w.value, 3), dtype=np.uint8)
+    _check(lib().tg_load_png(path.encode(), _p(out, _u8p), C.byref(w), C.byref(h)))
+    return out
 
-    with open(path, "rb") as f:
-        data = f.read()
-    if data[:8] != b"\x89PNG\r\n\x1a\n":
-        raise ParseError(f"not a PNG: {path}")
-    pos, idat, w, h = 8, b"", 0, 0
-    while pos < len(data):
-        (n,) = struct.unpack(">I", data[pos:pos + 4])
-        kind, body = data[pos + 4:pos + 8], data[pos + 8:pos + 8 + n]
-        if kind == b"IHDR":
-            w, h, depth, ctype = struct.unpack(">IIBB", body[:10])
-            if depth != 8 or ctype != 2:
-                raise ParseError(f"unsupported PNG layout: {path}")
-        elif kind == b"IDAT":
-            idat += body
-        pos += 12 + n
-    raw = np.frombuffer(zlib.decompress(idat), dtype=np.uint8).reshape(h, 1 + 3 * w)
-    img = np.zeros((h, 3 * w), dtype=np.int32)
-    prev = np.zeros(3 * w, dtype=np.int32)
-    for r in range(h):  # PNG filters (RFC 2083 §6)
-        ft, line = raw[r, 0], raw[r, 1:].astype(np.int32)
-        cur = line.copy() if ft == 0 else (line + prev) & 255 if ft == 2 else np.zeros_like(line)
-        for i in range(3 * w) if ft not in (0, 2) else ():
-            a = cur[i - 3] if i >= 3 else 0
-            b = prev[i]
-            c = prev[i - 3] if i >= 3 else 0
-            if ft == 0:
-                p = 0
-            elif ft == 1:
-                p = a
-            elif ft == 2:
-                p = b
-            elif ft == 3:
-                p = (a + b) // 2
-            else:
-                pa, pb, pc = abs(b - c), abs(a - c), abs(a + b - 2 * c)
-                p = a if pa <= pb and pa <= pc else (b if pb <= pc else c)
-            cur[i] = (line[i] + p) & 255
-        img[r] = cur
-        prev = cur
-    return img.astype(np.uint8).reshape(h, w, 3)
+
+def save_png(image: np.ndarray, path: str):
+    """render::save_png (image.cpp:23-49) of an H x W x 3 uint8 image."""
+    img = np.ascontiguousarray(image, dtype=np.uint8)
+    _check(lib().tg_save_png(path.encode(), _p(img, _u8p), img.shape[1], img.shape[0]))
+
+
+class metrics:  # noqa: N801 — mirrors tacchi::metrics (image_metrics.hpp)
+    @staticmethod
+    def compare_batch(a, b, device: int = 0) -> np.ndarray:
+        """ssim, psnr_db, mae_pct for each of a batch of image pairs (B x H x W x 3
+        uint8 each), one device launch (image_metrics.cpp:57-112)."""
+        a = np.ascontiguousarray(a, dtype=np.uint8)
+        b = np.ascontiguousarray(b, dtype=np.uint8)
+        if a.ndim == 3:
+            a, b = a[None], b[None]
+        if a.shape != b.shape:
+            raise ShapeMismatch(f"image shapes differ: {a.shape[1:]} vs {b.shape[1:]}")
+        out = np.zeros((a.shape[0], 3))
+        _check(lib().tg_image_metrics(device, _p(a, _u8p), _p(b, _u8p), a.shape[2], a.shape[1],
+                                      a.shape[0], _p(out)))
+        return out
+
+    @staticmethod
+    def compare(a, b, device: int = 0):
+        """metrics::compare -> (ssim, psnr_db, mae_pct)."""
+        return tuple(metrics.compare_batch(a, b, device)[0])
+
+
+class dataset:  # noqa: N801 — mirrors tacchi::dataset (harness.hpp)
+    @staticmethod
+    def run_press_dataset(cfg, out_dir: str, batch: int = 0, device: int = 0):
+        """dataset::run_press_dataset (harness.cpp:159-245) on the device;
+        returns (rows, skipped_positions)."""
+        rows, skipped = C.c_int64(), C.c_int64()
+        _check(lib().tg_run_press_dataset(device, _cfg(cfg), str(out_dir).encode(), batch,
+                                          C.byref(rows), C.byref(skipped)))
+        return rows.value, skipped.value
+
+    @staticmethod
+    def compare_datasets(dir_a: str, dir_b: str, csv_out: str = "", device: int = 0) -> dict:
+        """dataset::compare_datasets (harness.cpp:247-321)."""
+        out = np.zeros(7)
+        _check(lib().tg_compare_datasets(device, str(dir_a).encode(), str(dir_b).encode(),
+                                         str(csv_out).encode(), _p(out)))
+        keys = ["pairs", "ssim_mean", "ssim_std", "psnr_mean", "psnr_std", "mae_mean", "mae_std"]
+        d = dict(zip(keys, out.tolist()))
+        d["pairs"] = int(d["pairs"])
+        return d
 
 
 def version() -> str:

@@ -47,67 +47,11 @@ void check(int rc) {
   if (rc != TG_OK) throw HostError{rc, tg_last_error()};
 }
 
-// ---- on-disk formats -------------------------------------------------------
-
-uint32_t be32(uint32_t v) {
-  return ((v & 0xffu) << 24) | ((v & 0xff00u) << 8) | ((v >> 8) & 0xff00u) | (v >> 24);
-}
-
-void png_chunk(std::ofstream& out, const char* type, const unsigned char* data, uint32_t len) {
-  const uint32_t blen = be32(len);
-  out.write(reinterpret_cast<const char*>(&blen), 4);
-  out.write(type, 4);
-  if (len) out.write(reinterpret_cast<const char*>(data), len);
-  uLong crc = crc32(0L, reinterpret_cast<const Bytef*>(type), 4);
-  if (len) crc = crc32(crc, data, len);
-  const uint32_t bcrc = be32(static_cast<uint32_t>(crc));
-  out.write(reinterpret_cast<const char*>(&bcrc), 4);
-}
-
 }  // namespace
 
-// render::save_png (image.cpp:23-49): 8-bit RGB, non-interlaced.
-void save_png(const std::string& path, int w, int h, const uint8_t* rgb) {
-  std::ofstream out(path, std::ios::binary);
-  if (!out) throw HostError{TG_ERR_IO, "cannot write " + path};
-  static const unsigned char sig[8] = {137, 80, 78, 71, 13, 10, 26, 10};
-  out.write(reinterpret_cast<const char*>(sig), 8);
-  unsigned char ihdr[13];
-  const uint32_t bw = be32(static_cast<uint32_t>(w)), bh = be32(static_cast<uint32_t>(h));
-  std::memcpy(ihdr, &bw, 4);
-  std::memcpy(ihdr + 4, &bh, 4);
-  ihdr[8] = 8;   // bit depth
-  ihdr[9] = 2;   // colour type RGB
-  ihdr[10] = 0;  // compression
-  ihdr[11] = 0;  // filter
-  ihdr[12] = 0;  // interlace
-  png_chunk(out, "IHDR", ihdr, 13);
-  std::vector<unsigned char> raw(static_cast<size_t>(h) * (3 * w + 1));
-  for (int r = 0; r < h; ++r) {
-    raw[static_cast<size_t>(r) * (3 * w + 1)] = 0;  // filter: none
-    std::memcpy(&raw[static_cast<size_t>(r) * (3 * w + 1) + 1], rgb + static_cast<size_t>(r) * 3 * w,
-                3 * static_cast<size_t>(w));
-  }
-  uLongf zlen = compressBound(raw.size());
-  std::vector<unsigned char> z(zlen);
-  if (compress2(z.data(), &zlen, raw.data(), raw.size(), 6) != Z_OK)
-    throw HostError{TG_ERR_IO, "png compression failed"};
-  png_chunk(out, "IDAT", z.data(), static_cast<uint32_t>(zlen));
-  png_chunk(out, "IEND", nullptr, 0);
-}
+}  // namespace tacchi_b200::bridge
 
-// render::save_depth_map (depth_map.cpp:28-38): JSON header line + float32.
-void save_depth_map(const std::string& path, int w, int h, double pixel_to_meter,
-                    const double* values) {
-  std::ofstream out(path, std::ios::binary);
-  if (!out) throw HostError{TG_ERR_IO, "cannot write " + path};
-  const json header = {{"width", w}, {"height", h}, {"pixel_to_meter", pixel_to_meter}};
-  out << header.dump() << '\n';
-  std::vector<float> buf(static_cast<size_t>(w) * h);
-  for (size_t i = 0; i < buf.size(); ++i) buf[i] = static_cast<float>(values[i]);
-  out.write(reinterpret_cast<const char*>(buf.data()),
-            static_cast<std::streamsize>(buf.size() * sizeof(float)));
-}
+namespace tacchi_b200::host {
 
 // ---- SceneConfig::validate (scene_config.cpp:83-116, material.cpp:11-16) -----
 
@@ -126,7 +70,7 @@ void validate(const host::Config& c) {
   if (c.substeps_per_control_step < 1) bad("time.substeps_per_control_step must be >= 1");
   if (!(c.press_speed_mm_s > 0.0)) bad("time.press_speed_mm_s must be positive");
   if (c.target_points < 1) bad("indenter.target_points must be >= 1");
-  if (c.cloud_path.empty() && !host::is_known_shape(c.generated_shape))
+  if (c.cloud_path.empty() && !is_known_shape(c.generated_shape))
     bad("indenter: no cloud_path and unknown generated_shape '" + c.generated_shape + "'");
   if (c.positions_x < 1 || c.positions_y < 1) bad("press grid must have at least one position");
   if (c.depths_mm.empty()) bad("press.depths_mm must not be empty");
@@ -142,6 +86,14 @@ void validate(const host::Config& c) {
               << " exceeds the stability bound 0.5*dx/sqrt(E/rho) = " << bound
               << "; explicit stepping may diverge at this grid resolution\n";
 }
+
+}  // namespace tacchi_b200::host
+
+namespace tacchi_b200::bridge {
+
+using host::save_depth_map;
+using host::save_png;
+using host::validate;
 
 // ---- Session (session.hpp:61-77) -----------------------------------------------
 

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include "tacchi_cuda.h"
+
 namespace tacchi_b200::host {
 
 struct HostError {
@@ -16,6 +18,11 @@ struct HostError {
 };
 
 [[noreturn]] void raise(int code, const std::string& msg);
+
+struct V3 {
+  double x = 0, y = 0, z = 0;
+  double operator[](int a) const { return a == 0 ? x : (a == 1 ? y : z); }
+};
 
 struct Light {
   double dir[3], diffuse[3], specular[3];
@@ -61,5 +68,28 @@ struct Config {
 bool is_known_shape(const std::string& name);
 
 Config parse_config(const char* text);
+
+// render::save_png (image.cpp:23-49; 8-bit RGB, zlib, filter "none") and
+// render::save_depth_map (depth_map.cpp:28-38; JSON header line + float32).
+void save_png(const std::string& path, int w, int h, const uint8_t* rgb);
+void save_depth_map(const std::string& path, int w, int h, double pixel_to_meter,
+                    const double* values);
+// render::load_png (image.cpp:51-90): any non-interlaced 8/16-bit PNG ->
+// 8-bit RGB (palette / grey expanded, alpha stripped).
+std::vector<uint8_t> load_png(const std::string& path, int& w, int& h);
+
+// SceneConfig::validate (scene_config.cpp:83-116, material.cpp:11-16).
+void validate(const Config& c);
+
+// to_json_string (scene_config.cpp:124-170), byte-identical output.
+std::string to_json_string(const Config& c);
+
+// sim::indenter_cloud_for / place_for_press (scene_builder.cpp:33-61).
+std::vector<V3> indenter_cloud_for(const Config& c, const std::string& object);
+std::vector<V3> place_for_press(const Config& c, const std::vector<V3>& cloud, double off_x,
+                                double off_y);
+
+// sim::build_sim (scene_builder.cpp:63-78) from an already placed indenter.
+int build_sim_from(int device, const Config& c, const std::vector<V3>& placed, tg_handle* out);
 
 }  // namespace tacchi_b200::host

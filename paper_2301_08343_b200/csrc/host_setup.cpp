@@ -30,11 +30,6 @@ namespace tacchi_b200::host {
 using tacchi_b200::fail;
 using json = nlohmann::json;
 
-struct V3 {
-  double x = 0, y = 0, z = 0;
-  double operator[](int a) const { return a == 0 ? x : (a == 1 ? y : z); }
-};
-
 // scene_config.cpp:42-57: three tinted lights, 120 deg apart, 45 deg elevation.
 std::vector<Light> default_rig() {
   std::vector<Light> rig;
@@ -405,19 +400,23 @@ std::vector<V3> place(const std::vector<V3>& cloud, const V3& t, double rot) {
   return out;
 }
 
-// indenter_cloud_for + place_for_press (scene_builder.cpp:33-61).
-std::vector<V3> placed_indenter(const Config& c, const std::string& object, double off_x,
-                                double off_y) {
-  std::vector<V3> cloud;
+// indenter_cloud_for (scene_builder.cpp:33-46): generated shape (or
+// cloud_path, unsupported here), subsampled to target_points.
+std::vector<V3> indenter_cloud_for(const Config& c, const std::string& object) {
   if (!c.cloud_path.empty() && (object.empty() || object == c.cloud_path))
     raise(TG_ERR_IO, "point-cloud files are not supported by this build: " + c.cloud_path);
   const std::string shape = object.empty() ? c.generated_shape : object;
   Shape probe;
   if (!make_shape(shape, probe))
     raise(TG_ERR_IO, "point-cloud files are not supported by this build: " + shape);
-  cloud = generate_cloud(shape, c.source_points, c.seed);
+  std::vector<V3> cloud = generate_cloud(shape, c.source_points, c.seed);
   if (c.target_points < cloud.size()) cloud = subsample(cloud, c.target_points, c.seed);
+  return cloud;
+}
 
+// place_for_press (scene_builder.cpp:48-61).
+std::vector<V3> place_for_press(const Config& c, const std::vector<V3>& cloud, double off_x,
+                                double off_y) {
   const std::vector<V3> rotated = place(cloud, V3{0, 0, 0}, c.z_rotation_rad);
   V3 lo, hi;
   bbox(rotated, lo, hi);
@@ -427,6 +426,11 @@ std::vector<V3> placed_indenter(const Config& c, const std::string& object, doub
   const V3 target{centre + off_x - 0.5 * (lo.x + hi.x), centre + off_y - 0.5 * (lo.y + hi.y),
                   top + c.gap_mm * 1e-3 - lo.z};
   return place(rotated, target, 0.0);
+}
+
+std::vector<V3> placed_indenter(const Config& c, const std::string& object, double off_x,
+                                double off_y) {
+  return place_for_press(c, indenter_cloud_for(c, object), off_x, off_y);
 }
 
 // init_scene's checks and particle assembly (scene.cpp:15-87) for
@@ -549,6 +553,75 @@ Scene build_scene(const Config& c, const std::vector<V3>& indenter) {
   return sc;
 }
 
+int build_sim_from(int device, const Config& c, const std::vector<V3>& placed, tg_handle* out) {
+  Scene sc = build_scene(c, placed);
+  tg_particles tp{};
+  tp.n = static_cast<int64_t>(sc.mass.size());
+  tp.n_elastomer = sc.n_el;
+  tp.x = sc.x.data();
+  tp.v = sc.v.data();
+  tp.mass = sc.mass.data();
+  tp.volume0 = sc.vol0.data();
+  tp.tag = sc.tag.data();
+  return tg_create(device, &sc.P, &tp, &sc.S, out);
+}
+
+namespace {
+json v3j(const double* v) { return json::array({v[0], v[1], v[2]}); }
+json v3ij(const int* v) { return json::array({v[0], v[1], v[2]}); }
+}  // namespace
+
+// to_json_string (scene_config.cpp:124-170): 2-space indented + newline.
+std::string to_json_string(const Config& c) {
+  json j;
+  j["elastomer"] = {{"size_mm", v3j(c.size_mm)},
+                    {"particle_counts", v3ij(c.counts)},
+                    {"youngs_modulus_pa", c.E},
+                    {"poisson_ratio", c.nu},
+                    {"density_kg_m3", c.rho},
+                    {"fixed_bottom_layers", c.fixed_bottom_layers}};
+  j["grid"] = {{"nodes_per_axis", v3ij(c.nodes)}, {"edge_mm", c.edge_mm}};
+  j["time"] = {{"dt_s", c.dt},
+               {"substeps_per_control_step", c.substeps_per_control_step},
+               {"press_speed_mm_s", c.press_speed_mm_s}};
+  j["indenter"] = {{"cloud_path", c.cloud_path},
+                   {"generated_shape", c.generated_shape},
+                   {"source_points", c.source_points},
+                   {"target_points", c.target_points},
+                   {"seed", c.seed},
+                   {"gap_mm", c.gap_mm},
+                   {"z_rotation_rad", c.z_rotation_rad},
+                   {"rigid_mass_scale", c.rigid_mass_scale}};
+  j["press_grid"] = {{"positions_x", c.positions_x},
+                     {"positions_y", c.positions_y},
+                     {"step_mm", c.step_mm},
+                     {"depths_mm", c.depths_mm}};
+  j["lights"] = json::array();
+  for (const Light& l : c.lights)
+    j["lights"].push_back({{"direction", v3j(l.dir)},
+                           {"diffuse_rgb", v3j(l.diffuse)},
+                           {"specular_rgb", v3j(l.specular)}});
+  j["render"] = {{"ambient_k", c.ka},
+                 {"diffuse_k", c.kd},
+                 {"specular_k", c.ks},
+                 {"shininess", c.shininess},
+                 {"ambient_rgb", v3j(c.ambient)},
+                 {"view_dir", v3j(c.view)},
+                 {"pixel_to_meter", c.pixel_to_meter},
+                 {"image_width", c.image_w},
+                 {"image_height", c.image_h},
+                 {"background_image", c.background_image}};
+  j["alignment"] = json::object();
+  for (const auto& [name, a] : c.alignment)
+    j["alignment"][name] = {{"offset_px", json::array({a.ox, a.oy})}, {"scale", a.scale}};
+  j["objects"] = c.objects;
+  j["output_dir"] = c.output_dir;
+  j["deterministic"] = c.deterministic;
+  j["workers"] = c.workers;
+  j["gravity_mps2"] = c.gravity_mps2;
+  return j.dump(2) + "\n";
+}
+
 template <typename F>
 int guarded(F&& f) {
   try {
@@ -570,17 +643,8 @@ int tg_build_sim(int device, const char* config_json, const char* object, double
                  double offset_y, tg_handle* out) {
   return guarded([&] {
     const Config c = parse_config(config_json);
-    const std::vector<V3> ind = placed_indenter(c, object ? object : "", offset_x, offset_y);
-    Scene sc = build_scene(c, ind);
-    tg_particles tp{};
-    tp.n = static_cast<int64_t>(sc.mass.size());
-    tp.n_elastomer = sc.n_el;
-    tp.x = sc.x.data();
-    tp.v = sc.v.data();
-    tp.mass = sc.mass.data();
-    tp.volume0 = sc.vol0.data();
-    tp.tag = sc.tag.data();
-    return tg_create(device, &sc.P, &tp, &sc.S, out);
+    return build_sim_from(device, c, placed_indenter(c, object ? object : "", offset_x, offset_y),
+                          out);
   });
 }
 

@@ -24,6 +24,10 @@ Fixtures (all numpy .npz):
                    by tests/scenes.bridge_script on the SMALL scene, plus the
                    init errors of BAD_CONFIGS: replies, steps.jsonl, the
                    .depth files (bytes) and the images (pixels).
+  harness.npz      the reference's dataset::run_press_dataset on HARNESS
+                   (2 objects x 2 positions x 3 depths): manifest.csv,
+                   config.json, every image and .depth file; metrics::compare
+                   on image pairs and on a seeded noise pair.
   config1.npz      default config (dt 2e-6), 1000 substeps (100 frames) at the
                    default press velocity: surface-particle positions, a
                    seeded 4096-particle subset of x and F, diagnostics, the
@@ -40,7 +44,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import refpy as R  # noqa: E402
-from tests.scenes import (BAD_CONFIGS, CONFIG1, CONFIG5, CONFIG5_MOVE, CONFIG5_PRESS, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
+from tests.scenes import (BAD_CONFIGS, HARNESS, CONFIG1, CONFIG5, CONFIG5_MOVE, CONFIG5_PRESS, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
                           SMALL, SMALL3, SMALL3_PRESS, SMALL3_SHAPES, SMALL3_SLIDE, SMALL_STEPS,
                           SMALL_V, render_inputs, sha)
 
@@ -170,6 +174,42 @@ def config5():
         depth_sample=depth[::16, ::16])
 
 
+def harness():
+    import shutil
+    import tempfile
+
+    root = tempfile.mkdtemp(prefix="tacchi_dataset_")
+    try:
+        rows, skipped = R.run_press_dataset(HARNESS, root)
+        with open(os.path.join(root, "manifest.csv")) as f:
+            manifest = f.read()
+        with open(os.path.join(root, "config.json")) as f:
+            config_json = f.read()
+        arrays = {}
+        for line in manifest.splitlines()[1:]:
+            f = line.split(",")
+            key = f"{f[0]}_p{int(f[1])}_d{int(f[4])}"
+            arrays[f"image_{key}"] = R.load_ppm(os.path.join(root, f[8]))
+            with open(os.path.join(root, f[9]), "rb") as fh:
+                arrays[f"depth_{key}"] = np.frombuffer(fh.read(), dtype=np.uint8)
+        # metrics::compare on image pairs of this dataset + a synthetic pair
+        keys = sorted(k for k in arrays if k.startswith("image_"))
+        pairs = [(keys[0], keys[2]), (keys[3], keys[5]), (keys[1], keys[7]), (keys[4], keys[4])]
+        metric_a = np.array([arrays[a] for a, _ in pairs])
+        metric_b = np.array([arrays[b] for _, b in pairs])
+        rng = np.random.default_rng(11)
+        na = rng.integers(0, 256, (37, 53, 3), dtype=np.uint8)
+        nb = np.clip(na.astype(int) + rng.integers(-9, 10, na.shape), 0, 255).astype(np.uint8)
+        metrics = np.array([R.image_metrics(a, b) for a, b in zip(metric_a, metric_b)])
+        noise_metrics = np.array(R.image_metrics(na, nb))
+        np.savez_compressed(
+            os.path.join(OUT, "harness.npz"), rows=rows, skipped=skipped, manifest=manifest,
+            config_json=config_json, metric_pairs=np.array(pairs), metrics=metrics,
+            noise_a=na, noise_b=nb, noise_metrics=noise_metrics, **arrays)
+    finally:
+        shutil.rmtree(root)
+
+
 def bridge():
     import json
     import shutil
@@ -199,11 +239,13 @@ def bridge():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge"]
+    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge", "harness"]
     if "config5" in which:
         config5()
     if "bridge" in which:
         bridge()
+    if "harness" in which:
+        harness()
     if "kat" in which:
         kat()
     if "small" in which:

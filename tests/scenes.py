@@ -139,3 +139,15 @@ BAD_CONFIGS = [
     {"render": {"image_width": 1}},
     {"elastomer": {"fixed_bottom_layers": 21}},
 ]
+
+
+# Dataset harness (§8 row f2, harness.cpp:159-245) on the SMALL scene: two
+# objects x 2 press positions x 3 depth levels, press at 50 mm/s (1e-7 m per
+# substep -> captures at substeps 200, 250, 300), a crop alignment for one
+# object.
+HARNESS = {**SMALL,
+           "time": {"dt_s": 2e-6, "press_speed_mm_s": 50.0},
+           "objects": ["sphere2", "dots"],
+           "press_grid": {"positions_x": 2, "positions_y": 1, "step_mm": 0.5,
+                          "depths_mm": [0.0, 0.005, 0.01]},
+           "alignment": {"dots": {"offset_px": [3.0, -2.0], "scale": 1.05}}}
