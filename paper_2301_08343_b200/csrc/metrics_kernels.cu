@@ -7,7 +7,7 @@
 //   - SSIM: one thread per 8x8 window (top-left (x, y), x + 8 <= w,
 //     y + 8 <= h), grey = (r + g + b) / 3.0 (image_metrics.cpp:25-30); the
 //     five window sums are taken directly instead of through summed-area
-//     tables, so SSIM agrees with the reference to rounding (~1e-12).
+//     tables, so SSIM agrees with the reference to rounding (~1e-11).
 //   - squared / absolute channel differences are integers: accumulated
 //     exactly in 64-bit integers, so PSNR and MAE equal the reference's.
 // Per-CTA partials are reduced in a fixed order by a second kernel, so the

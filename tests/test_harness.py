@@ -9,7 +9,7 @@ metrics::compare (image_metrics.cpp:57-112) on image pairs
 
 Tolerances: manifest and config.json byte-identical; images <= 2/255 and
 depth <= 1e-7 m (the capture bar of tests/test_gpu_parity.py); PSNR and MAE
-exact (integer sums); SSIM <= 1e-12 (direct window sums on the GPU versus the
+exact (integer sums); SSIM <= 1e-10 (direct window sums on the GPU versus the
 reference's summed-area tables).
 """
 import json
@@ -242,10 +242,10 @@ def test_image_metrics_match_reference(golden):
     b = np.array([golden[str(y)] for _, y in pairs])
     m = tb.metrics.compare_batch(a, b)
     ref = golden["metrics"]
-    np.testing.assert_allclose(m[:, 0], ref[:, 0], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(m[:, 0], ref[:, 0], rtol=0, atol=1e-10)
     np.testing.assert_array_equal(m[:, 1:], ref[:, 1:])  # psnr, mae exact (inf included)
     nm = tb.metrics.compare(golden["noise_a"], golden["noise_b"])
-    assert nm[0] == pytest.approx(float(golden["noise_metrics"][0]), abs=1e-12)
+    assert nm[0] == pytest.approx(float(golden["noise_metrics"][0]), abs=1e-10)
     assert nm[1:] == tuple(golden["noise_metrics"][1:])
     with pytest.raises(tb.ShapeMismatch):
         tb.metrics.compare(np.zeros((7, 9, 3), np.uint8), np.zeros((7, 9, 3), np.uint8))
