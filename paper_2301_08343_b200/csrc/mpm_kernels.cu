@@ -180,16 +180,91 @@ __device__ __forceinline__ int64_t gel_particle(const GelMap& M, int64_t n_el) {
 #ifndef TACCHI_GEL_THREADS
 #define TACCHI_GEL_THREADS 256
 #endif
-constexpr int kTileCap = TACCHI_TILE_CAP;  // nodes; 2816 -> 4 x 8 B x 2816 + 4 B x 2816 = 101 KB
+constexpr int kTileCap = TACCHI_TILE_CAP;  // nodes; 2816 -> 32 B x 2816 + 4 B x 2816 = 101 KB
 constexpr int kGelThreads = TACCHI_GEL_THREADS;
 constexpr int kGelMinBlocks = (2 * 256) / TACCHI_GEL_THREADS;
 
+// Node tile, array of structures so that a z-row of the CTA's node box is one
+// contiguous run in both shared and global memory (node (i,j,k) at
+// (i*res1 + j)*res2 + k, k fastest): rows move with single bulk-async (TMA)
+// copies / reductions. {m, px, py, pz} while scattering, {vx, vy, vz, -}
+// while staging the grid velocity for G2P.
 struct P2GTile {
-  double m[kTileCap], px[kTileCap], py[kTileCap], pz[kTileCap];
+  double4 node[kTileCap];
   int owner[kTileCap];
   int lo[3], hi[3], dim[3];
   int ok;
+  unsigned long long bar;  // mbarrier of the staging copies
 };
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// Generic-proxy shared-memory writes -> visible to the async (bulk) proxy.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Adds the CTA's node box into the global grid: one bulk-async reduction
+// (UBLKRED.ADD.F64, element-wise atomic in L2) per z-row, issued by the
+// first dim0*dim1 threads. Call after a __syncthreads that follows the last
+// tile write (and a fence_proxy_async by every writer).
+__device__ __forceinline__ void tile_bulk_reduce(const P2GTile& T, const Geometry& g,
+                                                 double4* grid) {
+  const int rows = T.dim[0] * T.dim[1];
+  const int d2 = T.dim[2];
+  bool issued = false;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+    const int i = r / T.dim[1], j = r - i * T.dim[1];
+    double4* dst = grid + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
+    asm volatile(
+        "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+        "r"(smem_addr(&T.node[r * d2])), "r"(static_cast<unsigned>(d2 * sizeof(double4)))
+        : "memory");
+    issued = true;
+  }
+  if (issued) {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // the tile must stay intact until the bulk engine has read it
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+// Stages grid rows [lo, lo + dim) of `src` into T.node with bulk-async copies
+// completing on T.bar; every thread returns after the bytes landed. All
+// threads of the block must call it; T.dim / T.lo / T.ok set by tile_box.
+__device__ __forceinline__ void tile_bulk_stage(P2GTile& T, const Geometry& g,
+                                                const double4* src) {
+  const int rows = T.dim[0] * T.dim[1];
+  const int d2 = T.dim[2];
+  const unsigned bar = smem_addr(&T.bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(static_cast<unsigned>(rows * d2 * sizeof(double4)))
+                 : "memory");
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+    const int i = r / T.dim[1], j = r - i * T.dim[1];
+    const double4* s = src + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_addr(&T.node[r * d2])),
+        "l"(s), "r"(static_cast<unsigned>(d2 * sizeof(double4))), "r"(bar)
+        : "memory");
+  }
+  asm volatile(
+      "{\n"
+      ".reg .pred done;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n"
+      "@!done bra WAIT_%=;\n"
+      "}\n" ::"r"(bar)
+      : "memory");
+}
 
 // One particle's P2G payload (engine.cpp:128-145): stencil, m v and the
 // APIC + stress affine matrix.
@@ -311,11 +386,11 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
   const int vol = T.dim[0] * d1 * d2;
   const bool use_tile = T.ok != 0;
   if (use_tile) {
+    const double2 z2 = make_double2(0.0, 0.0);
     for (int e = tid; e < vol; e += blockDim.x) {
-      T.m[e] = 0.0;
-      T.px[e] = 0.0;
-      T.py[e] = 0.0;
-      T.pz[e] = 0.0;
+      double2* n2 = reinterpret_cast<double2*>(&T.node[e]);
+      n2[0] = z2;
+      n2[1] = z2;
       T.owner[e] = -1;
     }
   }
@@ -349,26 +424,21 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
           const double dxc = (c - q.st.fx[2]) * dx;
           const double w = wab * q.st.w[2][c];
           const int e = base_idx + (a * d1 + b) * d2 + c;
-          T.m[e] += w * m;
-          T.px[e] += w * (m0 + q.aff[2] * dxc);
-          T.py[e] += w * (m1 + q.aff[5] * dxc);
-          T.pz[e] += w * (m2 + q.aff[8] * dxc);
+          double2* n2 = reinterpret_cast<double2*>(&T.node[e]);
+          double2 lo2 = n2[0], hi2 = n2[1];
+          lo2.x += w * m;
+          lo2.y += w * (m0 + q.aff[2] * dxc);
+          hi2.x += w * (m1 + q.aff[5] * dxc);
+          hi2.y += w * (m2 + q.aff[8] * dxc);
+          n2[0] = lo2;
+          n2[1] = hi2;
         }
       }
     }
   }
+  fence_proxy_async();
   __syncthreads();
-  for (BoxIter it(tid, blockDim.x, d1, d2); it.e < vol; it.next(d1, d2)) {
-    const int e = it.e;
-    const double mm = T.m[e];
-    if (mm == 0.0) continue;
-    double* nd = reinterpret_cast<double*>(
-        grid + node_index(g, T.lo[0] + it.i, T.lo[1] + it.j, T.lo[2] + it.k));
-    red_add(nd + 0, mm);
-    red_add(nd + 1, T.px[e]);
-    red_add(nd + 2, T.py[e]);
-    red_add(nd + 3, T.pz[e]);
-  }
+  tile_bulk_reduce(T, g, grid);
 }
 
 // det F check + polar + stress + affine (engine.cpp:130-139). Returns false
@@ -1071,7 +1141,7 @@ __device__ __forceinline__ void g2p_gather(const Geometry& g, const double4* __r
 }  // namespace
 
 // G2P gather from the CTA's node box staged in shared memory (vx, vy, vz in
-// T.m, T.px, T.py), same arithmetic as g2p_gather.
+// T.node[.].x/y/z), same arithmetic as g2p_gather.
 __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile& T,
                                                 const Stencil& st, double* vv, double* Cn) {
   const int d1 = T.dim[1], d2 = T.dim[2];
@@ -1091,7 +1161,9 @@ __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile
       for (int c = 0; c < 3; ++c) {
         const double w = wab * st.w[2][c];
         const double dc = c - st.fx[2];
-        const double wv0 = w * T.m[row + c], wv1 = w * T.px[row + c], wv2 = w * T.py[row + c];
+        const double2 vxy = *reinterpret_cast<const double2*>(&T.node[row + c]);
+        const double vzz = T.node[row + c].z;
+        const double wv0 = w * vxy.x, wv1 = w * vxy.y, wv2 = w * vzz;
         v0 += wv0; v1 += wv1; vz += wv2;
         b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
         b10 += wv1 * da; b11 += wv1 * db; b12 += wv1 * dc;
@@ -1141,35 +1213,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     // along z) in the shared tile before the gathers.
     tile_box(T, active, st_old.base);
     staged = T.ok != 0;
-    if (staged) {
-      const int d1 = T.dim[1], d2 = T.dim[2];
-      const int vol = T.dim[0] * d1 * d2;
-      // two nodes per iteration so two loads are in flight per thread
-      const int step = 2 * blockDim.x;
-      BoxIter ia(threadIdx.x, step, d1, d2), ib(threadIdx.x + blockDim.x, step, d1, d2);
-      for (; ia.e < vol; ia.next(d1, d2), ib.next(d1, d2)) {
-        const bool hb = ib.e < vol;
-        const double2* qa2 = reinterpret_cast<const double2*>(
-            vel + node_index(g, T.lo[0] + ia.i, T.lo[1] + ia.j, T.lo[2] + ia.k));
-        const double2* qb2 = reinterpret_cast<const double2*>(
-            vel + node_index(g, T.lo[0] + ib.i, T.lo[1] + ib.j, T.lo[2] + ib.k));
-        const double2 a0 = __ldg(qa2), a1 = __ldg(qa2 + 1);
-        double2 b0 = make_double2(0, 0), b1 = make_double2(0, 0);
-        if (hb) {
-          b0 = __ldg(qb2);
-          b1 = __ldg(qb2 + 1);
-        }
-        T.m[ia.e] = a0.x;
-        T.px[ia.e] = a0.y;
-        T.py[ia.e] = a1.x;
-        if (hb) {
-          T.m[ib.e] = b0.x;
-          T.px[ib.e] = b0.y;
-          T.py[ib.e] = b1.x;
-        }
-      }
-      __syncthreads();
-    }
+    if (staged) tile_bulk_stage(T, g, vel);
   }
   if (active) {
     if (staged) g2p_gather_smem(g, T, st_old, vv, Cn);
