@@ -30,6 +30,7 @@ int launch_finalize_step(DeviceSim& s);
 int launch_call_begin(DeviceSim& s);
 int launch_ind_cols(DeviceSim& s, bool move);
 int launch_ind_catchup(DeviceSim& s);
+int launch_zero_consumed(DeviceSim& s, int sms);
 int launch_phase_g2p(DeviceSim& s);
 int launch_phase_boundary(DeviceSim& s);
 int launch_phase_advect(DeviceSim& s);
@@ -83,6 +84,8 @@ DeviceSim::~DeviceSim() {
   cudaFree(grid_mp);
   cudaFree(grid_v);
   cudaFree(grid_mi);
+  cudaFree(grid_mp_alt);
+  cudaFree(grid_mi_alt);
   cudaFree(col_start);
   cudaFree(ind_moves);
   cudaFree(surf_idx);
@@ -187,6 +190,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   g.stress_scale = -P->dt * 4.0 * g.inv_dx * g.inv_dx;
   if (const char* m = std::getenv("TACCHI_SCATTER")) g.scatter_mode = std::atoi(m);
   if (const char* f = std::getenv("TACCHI_FULL_INDENTER")) s->full_indenter = std::atoi(f) != 0;
+  if (const char* f = std::getenv("TACCHI_FUSED_GU")) s->fused_gu = std::atoi(f) != 0;
+  s->sms = sm_count(device);
 
   // Indenter particles are re-ordered by base cell so that P2G scatters from
   // neighbouring lanes hit neighbouring nodes; perm maps back.
@@ -230,6 +235,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
             cudaMalloc(&s->grid_mp, s->n_nodes * sizeof(double4)) == cudaSuccess &&
             cudaMalloc(&s->grid_v, s->n_nodes * sizeof(double4)) == cudaSuccess &&
             cudaMalloc(&s->grid_mi, s->n_nodes * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&s->grid_mp_alt, s->n_nodes * sizeof(double4)) == cudaSuccess &&
+            cudaMalloc(&s->grid_mi_alt, s->n_nodes * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->col_start, std::max<size_t>(col_starts.size(), 1) * sizeof(int64_t)) ==
                 cudaSuccess &&
             cudaMalloc(&s->ind_moves, std::max<int64_t>(n_ind, 1)) == cudaSuccess &&
@@ -243,6 +250,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   cudaMemsetAsync(s->grid_mp, 0, s->n_nodes * sizeof(double4), s->stream);
   cudaMemsetAsync(s->grid_v, 0, s->n_nodes * sizeof(double4), s->stream);
   cudaMemsetAsync(s->grid_mi, 0, s->n_nodes * sizeof(double), s->stream);
+  cudaMemsetAsync(s->grid_mp_alt, 0, s->n_nodes * sizeof(double4), s->stream);
+  cudaMemsetAsync(s->grid_mi_alt, 0, s->n_nodes * sizeof(double), s->stream);
   cudaMemsetAsync(s->ind_moves, 0, std::max<int64_t>(n_ind, 1), s->stream);
   s->n_cols = col_starts.empty() ? 0 : static_cast<int>(col_starts.size()) - 1;
   if (s->n_cols > 0)
@@ -332,6 +341,8 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
   // accumulators wholesale (errors are rare; this keeps the invariant simple).
   CUDA_TRY(cudaMemsetAsync(s.grid_mp, 0, s.n_nodes * sizeof(double4), s.stream));
   CUDA_TRY(cudaMemsetAsync(s.grid_mi, 0, s.n_nodes * sizeof(double), s.stream));
+  CUDA_TRY(cudaMemsetAsync(s.grid_mp_alt, 0, s.n_nodes * sizeof(double4), s.stream));
+  CUDA_TRY(cudaMemsetAsync(s.grid_mi_alt, 0, s.n_nodes * sizeof(double), s.stream));
   s.grid_dirty = false;
   s.grid_ready = false;
   CUDA_TRY(cudaStreamSynchronize(s.stream));
@@ -350,6 +361,24 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
 // (grid_ready), the standalone scatter is skipped; every substep, the last one
 // included, scatters the next substep's particles, so consecutive step() calls
 // chain without a standalone scatter.
+// One substep of the step path. Fused (default): the G2P kernel computes
+// grid_update on its staged node box from A_s / M_I_s and scatters s+1 into
+// the other buffers; the indenter kernel re-zeroes A_s / M_I_s.
+static int record_substep(DeviceSim& s, int sms, bool cols) {
+  int k = 0;
+  if (!s.fused_gu) k += launch_grid_update(s, sms, true);
+  k += launch_g2p2g_gel(s, true);
+  if (cols) {
+    k += launch_ind_cols(s, true);
+  } else {
+    k += launch_ind_move(s, true);
+    if (s.fused_gu) k += launch_zero_consumed(s, sms);
+  }
+  k += launch_finalize_step(s);
+  if (s.fused_gu) s.swap_buffers();
+  return k;
+}
+
 static int record_substeps(DeviceSim& s, int n_substeps) {
   int k = launch_call_begin(s);
   const int sms = sm_count(s.device);
@@ -359,12 +388,7 @@ static int record_substeps(DeviceSim& s, int n_substeps) {
     k += launch_p2g_gel(s);
     k += (cols && s.ind_v_uniform) ? launch_ind_cols(s, false) : launch_p2g_ind(s);
   }
-  for (int i = 0; i < n_substeps; ++i) {
-    k += launch_grid_update(s, sms, true);
-    k += launch_g2p2g_gel(s, true);
-    k += cols ? launch_ind_cols(s, true) : launch_ind_move(s, true);
-    k += launch_finalize_step(s);
-  }
+  for (int i = 0; i < n_substeps; ++i) k += record_substep(s, sms, cols);
   if (cols) k += launch_ind_catchup(s);
   return k;
 }
@@ -380,10 +404,11 @@ int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
   if (!s.window_valid) launch_window(s);
   s.window_valid = true;
   if (s.use_graphs) {
-    const int key = n_substeps * 8 + (s.grid_dirty ? 1 : 0) + (s.ind_v_uniform ? 2 : 0) +
-                    (s.grid_ready ? 4 : 0);
+    const int key = n_substeps * 32 + (s.grid_dirty ? 1 : 0) + (s.ind_v_uniform ? 2 : 0) +
+                    (s.grid_ready ? 4 : 0) + (s.fused_gu ? 8 : 0) + (s.cur_buf ? 16 : 0);
     auto it = s.graphs.find(key);
-    if (it == s.graphs.end()) {
+    const bool replay = it != s.graphs.end();
+    if (!replay) {
       cudaGraph_t graph;
       const int64_t before = s.kernel_launches;
       CUDA_TRY(cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal));
@@ -400,6 +425,8 @@ int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
     }
     CUDA_TRY(cudaGraphLaunch(it->second, s.stream));
     s.kernel_launches += s.graph_kernels[key];
+    // recording advanced the buffer pair substep by substep; a replay does not
+    if (replay && s.fused_gu && (n_substeps & 1)) s.swap_buffers();
   } else {
     CUDA_TRY(cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double),
                              cudaMemcpyHostToDevice, s.stream));
@@ -464,15 +491,20 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
   out_ms[1] = ms;
   for (int r = 0; r < reps; ++r) {
     cudaEventRecord(ev[2], s.stream);
-    launch_grid_update(s, sms, true);
+    if (!s.fused_gu) launch_grid_update(s, sms, true);
     cudaEventRecord(ev[3], s.stream);
     launch_g2p2g_gel(s, true);
     cudaEventRecord(ev[4], s.stream);
-    if (cols) launch_ind_cols(s, true);
-    else launch_ind_move(s, true);
+    if (cols) {
+      launch_ind_cols(s, true);
+    } else {
+      launch_ind_move(s, true);
+      if (s.fused_gu) launch_zero_consumed(s, sms);
+    }
     cudaEventRecord(ev[5], s.stream);
     launch_finalize_step(s);
     cudaEventRecord(ev[6], s.stream);
+    if (s.fused_gu) s.swap_buffers();
     CUDA_TRY(cudaEventSynchronize(ev[6]));
     for (int g = 2; g < kGroups; ++g) {
       cudaEventElapsedTime(&ms, ev[g], ev[g + 1]);

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <map>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "mpm_device.cuh"
@@ -68,6 +69,14 @@ struct DeviceSim {
   double4* grid_mp = nullptr;
   double4* grid_v = nullptr;
   double* grid_mi = nullptr;  // indenter mass (uniform-velocity indenter scatter)
+  // Fused step path (grid_update inside the G2P staging): the accumulators
+  // are double-buffered; grid_mp / grid_mi always name the current substep's
+  // buffers, *_alt the next substep's (swap_buffers after every substep).
+  double4* grid_mp_alt = nullptr;
+  double* grid_mi_alt = nullptr;
+  int cur_buf = 0;
+  int sms = 148;              // multiprocessor count of `device`
+  bool fused_gu = false;      // TACCHI_FUSED_GU=1: grid_update inside the G2P staging (A/B)
   // Indenter columns: maximal runs of equal initial (bx, by) in the sorted
   // cloud (internal indices [col_start[c], col_start[c+1])), z ascending.
   int n_cols = 0;
@@ -109,6 +118,11 @@ struct DeviceSim {
   int64_t kernel_launches = 0;
   int pending_start = 0;        // first substep of the in-flight step call
 
+  void swap_buffers() {
+    std::swap(grid_mp, grid_mp_alt);
+    std::swap(grid_mi, grid_mi_alt);
+    cur_buf ^= 1;
+  }
   ~DeviceSim();
 };
 

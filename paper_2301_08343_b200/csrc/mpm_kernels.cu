@@ -865,6 +865,34 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
 // accumulate pending moves that k_ind_catchup applies (the same sequence of
 // rounded adds) before mpm::step returns.
 // ---------------------------------------------------------------------------
+// Re-zeroes the accumulators of the substep just consumed (A_s over the
+// elastomer and indenter node boxes, M_I_s over the indenter box; the boxes
+// are P2G(s)'s footprints, Ctl::box_* until k_finalize(s) replaces them), so
+// the buffer is clean when the scatter of substep s + 2 lands in it. Work is
+// split over `nblocks` blocks starting at block `b0`.
+__device__ __forceinline__ void zero_consumed(double4* __restrict__ mp, double* __restrict__ mi,
+                                              const Ctl* ctl, const Geometry& g, int b0,
+                                              int nblocks) {
+  const int first = (blockIdx.x - b0) * blockDim.x + threadIdx.x, step = nblocks * blockDim.x;
+  const double2 z2 = make_double2(0.0, 0.0);
+  for (int m = 0; m < 2; ++m) {
+    int lo[3], dm[3], vol = 1;
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = ctl->box_lo[m][a];
+      dm[a] = max(ctl->box_hi[m][a] - lo[a], 0);
+      vol *= dm[a];
+    }
+    if (vol <= 0) continue;
+    for (BoxIter it(first, step, dm[1], dm[2]); it.e < vol; it.next(dm[1], dm[2])) {
+      const size_t nd = node_index(g, lo[0] + it.i, lo[1] + it.j, lo[2] + it.k);
+      double2* q = reinterpret_cast<double2*>(mp + nd);
+      q[0] = z2;
+      q[1] = z2;
+      if (m == 1) mi[nd] = 0.0;
+    }
+  }
+}
+
 __global__ void k_call_begin(Ctl* ctl) { ctl->call_start = ctl->substep; }
 
 constexpr int kColWarps = 8;
@@ -875,11 +903,13 @@ struct ColSmem {
   int run_start[kColWarps][33];
 };
 
+// Blocks >= col_blocks (step path) re-zero the consumed accumulators
+// (zero_consumed) alongside the column walks.
 template <bool kMove>
 __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
     double* __restrict__ x, int64_t n, int64_t n_el, const int64_t* __restrict__ col_start,
     int n_cols, uint8_t* __restrict__ moves, Ctl* ctl, Geometry g, double* __restrict__ mi,
-    int box_from_bb) {
+    int box_from_bb, double4* __restrict__ zero_mp, double* __restrict__ zero_mi, int col_blocks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ColSmem& S = *reinterpret_cast<ColSmem*>(smem_raw);
   pdl_wait();
@@ -890,6 +920,10 @@ __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
     ctl->ind_v[0] = ctl->vind[0];  // apply_boundary (engine.cpp:260-261)
     ctl->ind_v[1] = ctl->vind[1];
     ctl->ind_v[2] = ctl->vind[2];
+  }
+  if (zero_mp != nullptr && static_cast<int>(blockIdx.x) >= col_blocks) {
+    zero_consumed(zero_mp, zero_mi, ctl, g, col_blocks, gridDim.x - col_blocks);
+    return;
   }
   const int c = blockIdx.x * kColWarps + warp;
   if (c >= n_cols) return;  // warp-uniform; only __syncwarp below
@@ -1001,16 +1035,12 @@ __global__ void k_ind_catchup(double* __restrict__ x, int64_t n, int64_t n_el,
 // ---------------------------------------------------------------------------
 // grid_update (engine.cpp:180-205)
 // ---------------------------------------------------------------------------
-// Node update shared by both traversals; kZero also re-zeroes A / M_I.
-// with_mi: the node may hold indenter weight (inside the indenter box).
-template <bool kZero>
-__device__ __forceinline__ void update_node(double4* __restrict__ mp, double* __restrict__ mi,
-                                            double4* __restrict__ vel, const Geometry& g,
-                                            double m_ind, double u0, double u1, double u2, int i,
-                                            int j, int k, bool with_mi) {
-  const size_t nd = node_index(g, i, j, k);
-  const double4 q = mp[nd];
-  const double wi = with_mi ? mi[nd] : 0.0;  // indenter weight sum: mass m_ind wi, momentum (m_ind wi) u
+// grid_update of one node (engine.cpp:186-203) from its accumulators: the
+// elastomer's A = {m, p} plus the indenter's weight sum wi (mass m_ind wi,
+// momentum m_ind wi u). Massless nodes get v = 0.
+__device__ __forceinline__ double4 node_velocity(const Geometry& g, double4 q, double wi,
+                                                 double m_ind, double u0, double u1, double u2,
+                                                 int i, int j, int k) {
   double4 o = make_double4(0, 0, 0, 0);
   double mass = q.x, p0 = q.y, p1 = q.z, p2 = q.w;
   if (wi != 0.0) {
@@ -1021,9 +1051,17 @@ __device__ __forceinline__ void update_node(double4* __restrict__ mp, double* __
     p2 += M * u2;
   }
   if (mass > 0.0) {
-    o.x = p0 / mass;
-    o.y = p1 / mass;
-    o.z = p2 / mass;
+    // p / mass, correctly rounded (Markstein: y = RN(1/mass), q = RN(p y),
+    // q + (p - mass q) y rounded once is RN(p / mass) for normal operands):
+    // one reciprocal shared by the three components.
+    const double y = __drcp_rn(mass);
+    double q0 = p0 * y, q1 = p1 * y, q2 = p2 * y;
+    q0 = fma(fma(-q0, mass, p0), y, q0);
+    q1 = fma(fma(-q1, mass, p1), y, q1);
+    q2 = fma(fma(-q2, mass, p2), y, q2);
+    o.x = q0;
+    o.y = q1;
+    o.z = q2;
     if (g.with_gravity) {
       o.x = o.x + g.gdt[0];
       o.y = o.y + g.gdt[1];
@@ -1032,15 +1070,39 @@ __device__ __forceinline__ void update_node(double4* __restrict__ mp, double* __
     if (i == 0 || i == g.res[0] - 1) o.x = 0.0;
     if (j == 0 || j == g.res[1] - 1) o.y = 0.0;
     if (k == 0 || k == g.res[2] - 1) o.z = 0.0;
+    o.w = 1.0;  // has mass (not part of Grid::velocity)
   }
+  return o;
+}
+
+// Node update of the grid_update kernels; kZero also re-zeroes A / M_I.
+// with_mi: the node may hold indenter weight (inside the indenter box).
+template <bool kZero>
+__device__ __forceinline__ void update_node(double4* __restrict__ mp, double* __restrict__ mi,
+                                            double4* __restrict__ vel, const Geometry& g,
+                                            double m_ind, double u0, double u1, double u2, int i,
+                                            int j, int k, bool with_mi) {
+  const size_t nd = node_index(g, i, j, k);
+  const double4 q = mp[nd];
+  const double wi = with_mi ? mi[nd] : 0.0;
+  double4 o = node_velocity(g, q, wi, m_ind, u0, u1, u2, i, j, k);
+  const bool massive = o.w != 0.0;
+  o.w = 0.0;
   // Step path: nodes without mass keep their (finite) stale velocity; every
   // G2P read of such a node carries B-spline weight exactly 0 (the particle's
   // own scatter would have given it mass otherwise).
-  if (!kZero || mass > 0.0) vel[nd] = o;
+  if (!kZero || massive) vel[nd] = o;
   if (kZero) {
     if (q.x != 0.0 || q.y != 0.0 || q.z != 0.0 || q.w != 0.0) mp[nd] = make_double4(0, 0, 0, 0);
     if (wi != 0.0) mi[nd] = 0.0;
   }
+}
+
+__global__ void k_zero_consumed(double4* __restrict__ mp, double* __restrict__ mi, Ctl* ctl,
+                                Geometry g) {
+  pdl_wait();
+  if (stale(ctl, ctl->substep)) return;
+  zero_consumed(mp, mi, ctl, g, 0, gridDim.x);
 }
 
 // Phase API: the full active window, as the reference (Grid::velocity is 0
@@ -1140,6 +1202,64 @@ __device__ __forceinline__ void g2p_gather(const Geometry& g, const double4* __r
 }
 }  // namespace
 
+// Grid-update inputs of the fused step path: G2P computes node velocities
+// from the accumulators of substep s (A_s, and M_I_s inside the indenter's
+// P2G footprint) instead of a materialised Grid::velocity.
+struct AccSrc {
+  const double4* acc;
+  const double* mi;
+  int lo[3], hi[3];  // indenter node box of P2G(s)
+  double u[3];       // uniform indenter velocity of P2G(s)
+  double m_ind;
+};
+
+__device__ __forceinline__ bool in_ind_box(const AccSrc& A, int i, int j, int k) {
+  return i >= A.lo[0] && i < A.hi[0] && j >= A.lo[1] && j < A.hi[1] && k >= A.lo[2] &&
+         k < A.hi[2];
+}
+
+__device__ __forceinline__ double4 acc_velocity(const Geometry& g, const AccSrc& A, int i, int j,
+                                                int k) {
+  const size_t nd = node_index(g, i, j, k);
+  const double wi = in_ind_box(A, i, j, k) ? A.mi[nd] : 0.0;
+  return node_velocity(g, A.acc[nd], wi, A.m_ind, A.u[0], A.u[1], A.u[2], i, j, k);
+}
+
+// g2p_gather with node velocities computed from the accumulators (fallback
+// when the CTA footprint exceeds the shared tile).
+__device__ __forceinline__ void g2p_gather_acc(const Geometry& g, const AccSrc& A, double px0,
+                                               double px1, double px2, double* vv, double* Cn) {
+  Stencil st;
+  make_stencil(px0, px1, px2, g.origin, g.inv_dx, st);
+  double v0 = 0, v1 = 0, vz = 0;
+  double b00 = 0, b01 = 0, b02 = 0, b10 = 0, b11 = 0, b12 = 0, b20 = 0, b21 = 0, b22 = 0;
+  for (int a = 0; a < 3; ++a) {
+    const double wa = st.w[0][a];
+    const double da = a - st.fx[0];
+    for (int b = 0; b < 3; ++b) {
+      const double wab = wa * st.w[1][b];
+      const double db = b - st.fx[1];
+      for (int c = 0; c < 3; ++c) {
+        const double w = wab * st.w[2][c];
+        const double dc = c - st.fx[2];
+        const double4 q = acc_velocity(g, A, st.base[0] + a, st.base[1] + b, st.base[2] + c);
+        const double wv0 = w * q.x, wv1 = w * q.y, wv2 = w * q.z;
+        v0 += wv0; v1 += wv1; vz += wv2;
+        b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
+        b10 += wv1 * da; b11 += wv1 * db; b12 += wv1 * dc;
+        b20 += wv2 * da; b21 += wv2 * db; b22 += wv2 * dc;
+      }
+    }
+  }
+  vv[0] = v0;
+  vv[1] = v1;
+  vv[2] = vz;
+  const double k = 4.0 * g.inv_dx;
+  Cn[0] = k * b00; Cn[1] = k * b01; Cn[2] = k * b02;
+  Cn[3] = k * b10; Cn[4] = k * b11; Cn[5] = k * b12;
+  Cn[6] = k * b20; Cn[7] = k * b21; Cn[8] = k * b22;
+}
+
 // G2P gather from the CTA's node box staged in shared memory (vx, vy, vz in
 // T.node[.].x/y/z), same arithmetic as g2p_gather.
 __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile& T,
@@ -1180,12 +1300,14 @@ __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile
   Cn[6] = k * b20; Cn[7] = k * b21; Cn[8] = k * b22;
 }
 
-template <bool kBoundary, bool kAdvect, bool kLookahead>
+// kFused (step path): `vel` is A_s and `mi_cur` M_I_s; grid_update runs on
+// the staged node box (node_velocity) instead of in a separate pass.
+template <bool kBoundary, bool kAdvect, bool kLookahead, bool kFused = false>
 __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     double* __restrict__ x, double* __restrict__ v, double* __restrict__ Cm,
     double* __restrict__ Fm, const uint8_t* __restrict__ tag, int64_t n, int64_t n_el, GelMap M,
     Ctl* ctl, Geometry g, const double4* __restrict__ vel, double4* __restrict__ grid, double m,
-    double vol0) {
+    double vol0, const double* __restrict__ mi_cur, double m_ind) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   P2GTile& T = *reinterpret_cast<P2GTile*>(smem_raw);
   pdl_wait();
@@ -1215,8 +1337,30 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     staged = T.ok != 0;
     if (staged) tile_bulk_stage(T, g, vel);
   }
+  AccSrc src;
+  if (kFused) {
+    src.acc = vel;
+    src.mi = mi_cur;
+    for (int a = 0; a < 3; ++a) {
+      src.lo[a] = ctl->box_lo[1][a];
+      src.hi[a] = ctl->box_hi[1][a];
+      src.u[a] = ctl->ind_v[a];
+    }
+    src.m_ind = m_ind;
+    if (staged) {  // grid_update (engine.cpp:180-205) of the staged box, in place
+      const int d1 = T.dim[1], d2 = T.dim[2];
+      const int vol = T.dim[0] * d1 * d2;
+      for (BoxIter it(threadIdx.x, blockDim.x, d1, d2); it.e < vol; it.next(d1, d2)) {
+        const int i = T.lo[0] + it.i, j = T.lo[1] + it.j, k = T.lo[2] + it.k;
+        const double wi = in_ind_box(src, i, j, k) ? mi_cur[node_index(g, i, j, k)] : 0.0;
+        T.node[it.e] = node_velocity(g, T.node[it.e], wi, m_ind, src.u[0], src.u[1], src.u[2], i, j, k);
+      }
+      __syncthreads();
+    }
+  }
   if (active) {
     if (staged) g2p_gather_smem(g, T, st_old, vv, Cn);
+    else if (kFused) g2p_gather_acc(g, src, px0, px1, px2, vv, Cn);
     else g2p_gather(g, vel, px0, px1, px2, vv, Cn);
     double G[9];
 #pragma unroll
@@ -1411,6 +1555,8 @@ void configure_once() {
                        static_cast<int>(kTileSmem));
   cudaFuncSetAttribute(k_g2p2g_gel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(kTileSmem));
+  cudaFuncSetAttribute(k_g2p2g_gel<true, true, true, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTileSmem));
   cudaFuncSetAttribute(k_ind_move_p2g<false, true>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIndSmem));
   cudaFuncSetAttribute(k_ind_move_p2g<true, true>,
@@ -1525,14 +1671,20 @@ int launch_grid_update(DeviceSim& s, int sms, bool zero) {
 int launch_g2p2g_gel(DeviceSim& s, bool lookahead) {
   if (s.n_el <= 0) return 0;
   configure_once();
-  if (lookahead)
+  if (lookahead && s.fused_gu)
+    launch_pdl(k_g2p2g_gel<true, true, true, true>, dim3(gel_blocks(s)), dim3(kGelThreads),
+               kTileSmem, s.stream, s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl,
+               s.geo, static_cast<const double4*>(s.grid_mp), s.grid_mp_alt, s.m_el, s.vol_el,
+               static_cast<const double*>(s.grid_mi), s.m_ind);
+  else if (lookahead)
     launch_pdl(k_g2p2g_gel<true, true, true>, dim3(gel_blocks(s)), dim3(kGelThreads), kTileSmem,
                s.stream, s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo,
-               s.grid_v, s.grid_mp, s.m_el, s.vol_el);
+               static_cast<const double4*>(s.grid_v), s.grid_mp, s.m_el, s.vol_el,
+               static_cast<const double*>(nullptr), 0.0);
   else
     k_g2p2g_gel<true, true, false><<<gel_blocks(s), kGelThreads, 0, s.stream>>>(
         s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
-        s.m_el, s.vol_el);
+        s.m_el, s.vol_el, nullptr, 0.0);
   s.kernel_launches += 1;
   return 1;
 }
@@ -1542,11 +1694,19 @@ int launch_ind_move(DeviceSim& s, bool lookahead) {
   configure_once();
   if (lookahead)
     k_ind_move_p2g<true, true><<<ind_blocks(s), kIndThreads, kIndSmem, s.stream>>>(
-        s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
+        s.x, s.n, s.n_el, s.ctl, s.geo, s.fused_gu ? s.grid_mi_alt : s.grid_mi);
   else
     k_ind_move_p2g<true, false><<<ind_blocks(s), kIndThreads, 0, s.stream>>>(
         s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   s.ind_v_uniform = true;
+  s.kernel_launches += 1;
+  return 1;
+}
+
+// Fused step path without the column walk: re-zero the consumed buffers.
+int launch_zero_consumed(DeviceSim& s, int sms) {
+  launch_pdl(k_zero_consumed, dim3(2 * sms), dim3(kThreads), 0, s.stream, s.grid_mp, s.grid_mi,
+             s.ctl, s.geo);
   s.kernel_launches += 1;
   return 1;
 }
@@ -1572,12 +1732,21 @@ int launch_ind_cols(DeviceSim& s, bool move) {
     attr = true;
   }
   const unsigned blocks = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
-  if (move)
+  if (move && s.fused_gu) {  // scatter into the next buffer, zero the consumed one
+    const unsigned zblocks = static_cast<unsigned>(2 * s.sms);
+    launch_pdl(k_ind_cols<true>, dim3(blocks + zblocks), dim3(kColWarps * 32), kColSmem, s.stream,
+               s.x, s.n, s.n_el, static_cast<const int64_t*>(s.col_start), s.n_cols, s.ind_moves,
+               s.ctl, s.geo, s.grid_mi_alt, 1, s.grid_mp, s.grid_mi, static_cast<int>(blocks));
+  } else if (move) {
     launch_pdl(k_ind_cols<true>, dim3(blocks), dim3(kColWarps * 32), kColSmem, s.stream, s.x,
-               s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 1);
-  else
+               s.n, s.n_el, static_cast<const int64_t*>(s.col_start), s.n_cols, s.ind_moves,
+               s.ctl, s.geo, s.grid_mi, 1, static_cast<double4*>(nullptr),
+               static_cast<double*>(nullptr), static_cast<int>(blocks));
+  } else {
     k_ind_cols<false><<<blocks, kColWarps * 32, kColSmem, s.stream>>>(
-        s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 0);
+        s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 0,
+        nullptr, nullptr, static_cast<int>(blocks));
+  }
   s.ind_v_uniform = true;
   s.kernel_launches += 1;
   return 1;
@@ -1602,7 +1771,7 @@ int launch_phase_g2p(DeviceSim& s) {
   if (s.n_el <= 0) return 0;
   k_g2p2g_gel<false, false, false><<<gel_blocks(s), kGelThreads, 0, s.stream>>>(
       s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
-      s.m_el, s.vol_el);
+      s.m_el, s.vol_el, nullptr, 0.0);
   s.kernel_launches += 1;
   return 1;
 }
