@@ -178,6 +178,17 @@ int tg_render_from_config(const char* config_json, const char* object, tg_render
  * height x width x 3 (Image8::data). Either may be NULL (device-only). */
 int tg_capture(tg_handle h, const tg_render* r, double* depth_out, uint8_t* rgb_out);
 
+/* The handle's pinned host buffers for r's capture (height x width fp64 and
+ * height x width x 3 u8). Passing them as tg_capture / tg_step_capture
+ * outputs skips the host copy; their content is replaced by the next capture. */
+int tg_capture_buffers(tg_handle h, const tg_render* r, double** depth, uint8_t** rgb);
+
+/* One control step of Session::handle_command (session.cpp:86, 42):
+ * mpm::step(state, v, n) then sim::capture, submitted together with a single
+ * host synchronisation. Errors are mpm::step's; outputs as tg_capture. */
+int tg_step_capture(tg_handle h, const double indenter_velocity[3], int n_substeps,
+                    const tg_render* r, double* depth_out, uint8_t* rgb_out);
+
 /* render::extract_surface_depth(state, w, h, r) (depth_extract.cpp:10-49);
  * w <= 0 or h <= 0 selects the full-surface overload (:51-57) and returns
  * its size in *out_w / *out_h (call with out == NULL to query). */

@@ -138,6 +138,10 @@ def lib():
         L.tg_download_grid.argtypes = [C.c_void_p, _ip, _ip, _dp, _dp, _dp]
         L.tg_render_from_config.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(TgRender)]
         L.tg_capture.argtypes = [C.c_void_p, C.POINTER(TgRender), _dp, _u8p]
+        L.tg_capture_buffers.argtypes = [C.c_void_p, C.POINTER(TgRender),
+                                         C.POINTER(C.POINTER(C.c_double)),
+                                         C.POINTER(C.POINTER(C.c_uint8))]
+        L.tg_step_capture.argtypes = [C.c_void_p, _dp, C.c_int, C.POINTER(TgRender), _dp, _u8p]
         L.tg_extract_depth.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, _dp, _ip, _ip]
         L.tg_crop_align.argtypes = [C.c_int, _dp, C.c_int, C.c_int, C.c_double, C.c_double,
                                     C.c_double, C.c_int, C.c_int, _dp]
@@ -442,6 +446,36 @@ class sim:  # noqa: N801 — mirrors tacchi::sim
         depth = np.empty((rp.height, rp.width)) if want_depth else None
         img = np.empty((rp.height, rp.width, 3), np.uint8) if want_image else None
         _check(lib().tg_capture(state.handle, C.byref(rp), _p(depth), _p(img, _u8p)))
+        return depth, img
+
+    @staticmethod
+    def _pinned_views(state: SimState, rp: TgRender):
+        """numpy views of the handle's pinned capture buffers (tg_capture_buffers);
+        valid until the next capture on this state."""
+        dptr, rptr = C.POINTER(C.c_double)(), C.POINTER(C.c_uint8)()
+        _check(lib().tg_capture_buffers(state.handle, C.byref(rp), C.byref(dptr), C.byref(rptr)))
+        depth = np.ctypeslib.as_array(dptr, shape=(rp.height, rp.width))
+        img = np.ctypeslib.as_array(rptr, shape=(rp.height, rp.width, 3))
+        return depth, img
+
+    @staticmethod
+    def step_capture(state: SimState, indenter_velocity, n_substeps: int, cfg=None, obj: str = "",
+                     params: TgRender | None = None, zero_copy: bool = False,
+                     want_depth: bool = True, want_image: bool = True):
+        """One Session control step (session.cpp:86, 42): mpm::step then
+        sim::capture with a single host sync -> (depth, image). zero_copy
+        returns views of pinned buffers that the next capture overwrites;
+        want_* False keeps that output on the device."""
+        rp = params if params is not None else render_params(cfg, obj)
+        if zero_copy:
+            depth, img = sim._pinned_views(state, rp)
+        else:
+            depth = np.empty((rp.height, rp.width))
+            img = np.empty((rp.height, rp.width, 3), np.uint8)
+        depth = depth if want_depth else None
+        img = img if want_image else None
+        _check(lib().tg_step_capture(state.handle, _p(_vec(indenter_velocity)), int(n_substeps),
+                                     C.byref(rp), _p(depth), _p(img, _u8p)))
         return depth, img
 
 

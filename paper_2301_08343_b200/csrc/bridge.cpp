@@ -136,6 +136,7 @@ class Session {
     gap_m_ = cfg_.gap_mm * 1e-3;
     check(tg_build_sim(device, config_json.c_str(), object_.c_str(), 0.0, 0.0, &h_));
     check(tg_render_from_config(config_json.c_str(), object_.c_str(), &render_));
+    check(tg_capture_buffers(h_, &render_, &cap_depth_, &cap_rgb_));
     std::filesystem::create_directories(dir_);
   }
   ~Session() {
@@ -172,7 +173,11 @@ class Session {
     double v[3];
     for (int a = 0; a < 3; ++a)
       v[a] = cmd.mode == CommandMode::Velocity ? cmd.vector[a] : (cmd.vector[a] - offset_[a]) / dtc;
-    check(tg_step(h_, v, cfg_.substeps_per_control_step));
+    // mpm::step, and sim::capture when an image is requested, with one sync
+    if (cmd.request_image)
+      check(tg_step_capture(h_, v, cfg_.substeps_per_control_step, &render_, cap_depth_, cap_rgb_));
+    else
+      check(tg_step(h_, v, cfg_.substeps_per_control_step));
     for (int a = 0; a < 3; ++a)
       offset_[a] = cmd.mode == CommandMode::Position ? cmd.vector[a] : offset_[a] + v[a] * dtc;
     ++control_steps_;
@@ -189,18 +194,15 @@ class Session {
     reply.step_index = control_steps_;
     reply.depth_m = depth();
     reply.terminal = terminal_;
-    if (request_image) {
+    if (request_image) {  // captured by handle_command into the pinned buffers
       const int w = render_.width, h = render_.height;
-      std::vector<double> depth(static_cast<size_t>(w) * h);
-      std::vector<uint8_t> rgb(static_cast<size_t>(w) * h * 3);
-      check(tg_capture(h_, &render_, depth.data(), rgb.data()));
       char name[64];
       std::snprintf(name, sizeof(name), "step_%06lld", static_cast<long long>(control_steps_));
       reply.image_path = (dir_ / (std::string(name) + ".png")).string();
       reply.depth_map_path = (dir_ / (std::string(name) + ".depth")).string();
-      save_png(reply.image_path, w, h, rgb.data());
+      save_png(reply.image_path, w, h, cap_rgb_);
       save_depth_map(reply.depth_map_path, w, h, render_.pixel_to_meter * render_.crop_scale,
-                     depth.data());
+                     cap_depth_);
     }
     std::ofstream log(dir_ / "steps.jsonl", std::ios::app);
     const json j = {{"step", reply.step_index},
@@ -218,6 +220,8 @@ class Session {
   TerminalCondition term_;
   tg_handle h_ = nullptr;
   tg_render render_{};
+  double* cap_depth_ = nullptr;  // the handle's pinned capture buffers
+  uint8_t* cap_rgb_ = nullptr;
   double offset_[3] = {0, 0, 0};
   double gap_m_ = 0.0;
   double last_sim_time_ = -std::numeric_limits<double>::infinity();

@@ -367,8 +367,10 @@ static void launch_surface_depth(DeviceSim& s) {
 }
 
 // sim::capture. depth_host / rgb_host may be null (device-resident result).
-int capture(DeviceSim& s, const tg_render& r, double* depth_host, uint8_t* rgb_host,
-            std::string& msg) {
+// Enqueues sim::capture on the handle's stream: the fused kernel and, when
+// requested, the D2H copies of depth / RGB into the handle's pinned buffers.
+int capture_enqueue(DeviceSim& s, const tg_render& r, bool want_depth, bool want_rgb,
+                    std::string& msg) {
   if (s.surf_nx < 2 || s.surf_ny < 2 || !s.surf_idx) {
     msg = "extract_surface_depth: state has no surface lattice";
     return kErrNoSurface;
@@ -407,24 +409,57 @@ int capture(DeviceSim& s, const tg_render& r, double* depth_host, uint8_t* rgb_h
       s.surf_depth, s.surf_ny, mx, my, r.pixel_to_meter, cx, cy, ow, oh, r_out, make_shade(r),
       r.background ? s.cap_bg : nullptr, s.cap_depth, s.cap_rgb);
   s.kernel_launches += 1;
-  if (depth_host)
+  if (want_depth)
     cudaMemcpyAsync(s.h_depth_pinned, s.cap_depth, pixels * sizeof(double),
                     cudaMemcpyDeviceToHost, s.stream);
-  if (rgb_host)
+  if (want_rgb)
     cudaMemcpyAsync(s.h_rgb_pinned, s.cap_rgb, pixels * 3, cudaMemcpyDeviceToHost, s.stream);
-  if (depth_host || rgb_host) {
-    if (cudaStreamSynchronize(s.stream) != cudaSuccess) {
-      msg = cudaGetErrorString(cudaGetLastError());
-      return TG_ERR_CUDA;
-    }
-    if (depth_host) std::memcpy(depth_host, s.h_depth_pinned, pixels * sizeof(double));
-    if (rgb_host) std::memcpy(rgb_host, s.h_rgb_pinned, pixels * 3);
-  }
+  s.cap_last_pixels = pixels;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     msg = cudaGetErrorString(e);
     return TG_ERR_CUDA;
   }
+  return TG_OK;
+}
+
+// After the stream is synchronised: copies the pinned results to caller
+// buffers (skipped when the caller passes the pinned buffers themselves,
+// see tg_capture_buffers).
+void capture_collect(DeviceSim& s, double* depth_host, uint8_t* rgb_host) {
+  const size_t pixels = s.cap_last_pixels;
+  if (depth_host && depth_host != s.h_depth_pinned)
+    std::memcpy(depth_host, s.h_depth_pinned, pixels * sizeof(double));
+  if (rgb_host && rgb_host != s.h_rgb_pinned) std::memcpy(rgb_host, s.h_rgb_pinned, pixels * 3);
+}
+
+int capture(DeviceSim& s, const tg_render& r, double* depth_host, uint8_t* rgb_host,
+            std::string& msg) {
+  const int rc = capture_enqueue(s, r, depth_host != nullptr, rgb_host != nullptr, msg);
+  if (rc) return rc;
+  if (depth_host || rgb_host) {
+    if (cudaStreamSynchronize(s.stream) != cudaSuccess) {
+      msg = cudaGetErrorString(cudaGetLastError());
+      return TG_ERR_CUDA;
+    }
+    capture_collect(s, depth_host, rgb_host);
+  }
+  return TG_OK;
+}
+
+// The handle's pinned capture buffers for r's output size (allocated here).
+int capture_buffers(DeviceSim& s, const tg_render& r, double** depth, uint8_t** rgb,
+                    std::string& msg) {
+  if (r.width < 2 || r.height < 2) {
+    msg = "capture: render image size too small";
+    return kErrConfig;
+  }
+  if (ensure_capture_buffers(s, static_cast<size_t>(r.width) * r.height, false)) {
+    msg = "capture: allocation failed";
+    return TG_ERR_CUDA;
+  }
+  if (depth) *depth = s.h_depth_pinned;
+  if (rgb) *rgb = s.h_rgb_pinned;
   return TG_OK;
 }
 

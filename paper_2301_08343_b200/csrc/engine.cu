@@ -41,6 +41,13 @@ constexpr int kResetAll = 7;
 // capture_kernels.cu
 int capture(DeviceSim& s, const tg_render& r, double* depth_host, uint8_t* rgb_host,
             std::string& msg);
+int capture_enqueue(DeviceSim& s, const tg_render& r, bool want_depth, bool want_rgb,
+                    std::string& msg);
+void capture_collect(DeviceSim& s, double* depth_host, uint8_t* rgb_host);
+int capture_buffers(DeviceSim& s, const tg_render& r, double** depth, uint8_t** rgb,
+                    std::string& msg);
+int step_submit(DeviceSim& s, const double vind[3], int n_substeps);
+int step_finish(DeviceSim& s, int n_substeps);
 int extract_depth(DeviceSim& s, int w, int h, double r, double* out, std::string& msg);
 void full_surface_size(const DeviceSim& s, double r, int* w, int* h);
 int render_standalone(int mode, const double* src, int sw, int sh, double r, double off_x,
@@ -765,6 +772,37 @@ int tg_capture(tg_handle h, const tg_render* r, double* depth_out, uint8_t* rgb_
   std::string msg;
   const int rc = tacchi_b200::capture(s, *r, depth_out, rgb_out, msg);
   return rc ? fail(rc, msg) : TG_OK;
+}
+
+int tg_capture_buffers(tg_handle h, const tg_render* r, double** depth, uint8_t** rgb) {
+  if (!h || !r) return fail(TG_ERR_INVALID_ARGUMENT, "tg_capture_buffers: null argument");
+  DeviceSim& s = *H(h);
+  cudaSetDevice(s.device);
+  std::string msg;
+  const int rc = tacchi_b200::capture_buffers(s, *r, depth, rgb, msg);
+  return rc ? fail(rc, msg) : TG_OK;
+}
+
+// One control step of the co-simulation loop (session.cpp:86 + 42): the
+// substeps and the capture are submitted together, with one host sync.
+int tg_step_capture(tg_handle h, const double v[3], int n, const tg_render* r, double* depth_out,
+                    uint8_t* rgb_out) {
+  if (!h || !v || !r) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture: null argument");
+  DeviceSim& s = *H(h);
+  while (n > 200) {  // long calls: chunks as tg_step
+    const int rc = tacchi_b200::step(s, v, 200);
+    if (rc) return rc;
+    n -= 200;
+  }
+  int rc = tacchi_b200::step_submit(s, v, n);
+  if (rc) return rc;
+  std::string msg;
+  const int crc = tacchi_b200::capture_enqueue(s, *r, depth_out != nullptr, rgb_out != nullptr, msg);
+  rc = tacchi_b200::step_finish(s, n);  // syncs the stream; the step's error wins
+  if (rc) return rc;
+  if (crc) return fail(crc, msg);
+  tacchi_b200::capture_collect(s, depth_out, rgb_out);
+  return TG_OK;
 }
 
 int tg_extract_depth(tg_handle h, int w, int hgt, double r, double* out, int* out_w, int* out_h) {

@@ -101,7 +101,7 @@ struct DeviceSim {
   double* cap_depth = nullptr;
   uint8_t* cap_rgb = nullptr;
   uint8_t* cap_bg = nullptr;
-  size_t cap_pixels = 0, cap_bg_pixels = 0;
+  size_t cap_pixels = 0, cap_bg_pixels = 0, cap_last_pixels = 0;
   double* h_depth_pinned = nullptr;
   uint8_t* h_rgb_pinned = nullptr;
 

@@ -138,6 +138,31 @@ def test_step_graph_and_plain_launches_agree(tb):
     assert a.kernel_launches > 0
 
 
+def test_step_capture_matches_step_then_capture(tb):
+    """tg_step_capture (one sync per control step) == mpm::step + sim::capture
+    (to the atomic-order rounding of two independent runs); zero-copy outputs
+    are views of the handle's pinned buffers."""
+    a, b = tb.sim.build_sim(SMALL), tb.sim.build_sim(SMALL)
+    rp = tb.render_params(SMALL, "")
+
+    def same(da, ia, db, ib):
+        np.testing.assert_allclose(da, db, rtol=0, atol=1e-12)
+        assert np.abs(ia.astype(int) - ib).max() <= 1
+
+    for _ in range(3):
+        tb.mpm.step(a, SMALL_V, 10)
+        da, ia = tb.sim.capture(a, params=rp)
+        db, ib = tb.sim.step_capture(b, SMALL_V, 10, params=rp)
+        same(da, ia, db, ib)
+    dz, iz = tb.sim.step_capture(b, SMALL_V, 10, params=rp, zero_copy=True)
+    tb.mpm.step(a, SMALL_V, 10)
+    da, ia = tb.sim.capture(a, params=rp)
+    same(da, ia, dz, iz)
+    np.testing.assert_allclose(a.state()["x"], b.state()["x"], rtol=0, atol=1e-15)
+    _, none = tb.sim.step_capture(b, SMALL_V, 250, params=rp, want_image=False)  # > 200: chunked
+    assert none is None and b.step_count == a.step_count + 250
+
+
 def test_step_many_matches_individual_steps(tb):
     sims = [tb.sim.build_sim(SMALL, "", 1e-4 * i, 0.0) for i in range(3)]
     ref = [tb.sim.build_sim(SMALL, "", 1e-4 * i, 0.0) for i in range(3)]
