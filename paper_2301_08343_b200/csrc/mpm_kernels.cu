@@ -529,8 +529,14 @@ __device__ bool in_range(const Geometry& g, const double* x) {
   return true;
 }
 
-__global__ void k_finalize(Ctl* ctl, Geometry g, int mode) {
+// Single thread. The control block is copied into registers with one batch
+// of independent loads, updated there and written back once: through the
+// pointer every read after a store would wait a full L2 round trip (possible
+// aliasing), which made this kernel a ~8 us latency chain.
+__global__ void k_finalize(Ctl* ctl_mem, Geometry g, int mode) {
   pdl_wait();
+  Ctl c = *ctl_mem;
+  Ctl* ctl = &c;
   const int s = ctl->substep;
   if (stale(ctl, s)) return;
   if (mode & kFinDiag) {  // particle_to_grid's min_det_f (engine.cpp:119,177)
@@ -560,7 +566,11 @@ __global__ void k_finalize(Ctl* ctl, Geometry g, int mode) {
     ctl->step_count += 1;
     ctl->substep = s + 1;
     if (!in_range(g, lo) || !in_range(g, hi)) {
-      raise(ctl, kErrOutOfGrid, s);
+      if (c.err_code == 0) {
+        c.err_code = kErrOutOfGrid;
+        c.err_substep = s;
+      }
+      *ctl_mem = c;
       return;
     }
   }
@@ -571,7 +581,11 @@ __global__ void k_finalize(Ctl* ctl, Geometry g, int mode) {
       const int b0 = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(lo[a], g.origin[a]), g.inv_dx), 0.5)));
       const int b1 = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(hi[a], g.origin[a]), g.inv_dx), 0.5)));
       if (b0 < 0 || b1 + 2 >= g.res[a]) {
-        raise(ctl, kErrOutOfGrid, ctl->substep);
+        if (c.err_code == 0) {
+          c.err_code = kErrOutOfGrid;
+          c.err_substep = c.substep;
+        }
+        *ctl_mem = c;
         return;
       }
       wlo[a] = b0;
@@ -607,6 +621,7 @@ __global__ void k_finalize(Ctl* ctl, Geometry g, int mode) {
     ctl->bb_hi[a] = order_key(-INFINITY);
   }
   ctl->max_v2 = 0ull;
+  *ctl_mem = c;
 }
 
 // zero_grid's clear of Grid::mass / momentum over Ctl::clr (engine.cpp:72-83).
