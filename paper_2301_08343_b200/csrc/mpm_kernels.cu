@@ -529,99 +529,106 @@ __device__ bool in_range(const Geometry& g, const double* x) {
   return true;
 }
 
-// Single thread. The control block is copied into registers with one batch
-// of independent loads, updated there and written back once: through the
-// pointer every read after a store would wait a full L2 round trip (possible
-// aliasing), which made this kernel a ~8 us latency chain.
-__global__ void k_finalize(Ctl* ctl_mem, Geometry g, int mode) {
+// One warp; lanes 0-2 own one axis each (the per-axis work is independent:
+// bbox shift, in_range, window, material boxes, clear box), lane 0 the
+// scalar diagnostics. Each lane reads only its fields, once, and writes its
+// results once, so no read waits on an aliasing store; cross-axis decisions
+// (in_range of all axes, the previous window's emptiness) are warp votes.
+__device__ __forceinline__ int base_of(const Geometry& g, int a, double x) {
+  return static_cast<int>(floor(sub_rn(mul_rn(sub_rn(x, g.origin[a]), g.inv_dx), 0.5)));
+}
+
+__global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode) {
   pdl_wait();
-  Ctl c = *ctl_mem;
-  Ctl* ctl = &c;
+  const int lane = threadIdx.x;
+  const bool ax = lane < 3;
+  const int a = ax ? lane : 0;
   const int s = ctl->substep;
   if (stale(ctl, s)) return;
-  if (mode & kFinDiag) {  // particle_to_grid's min_det_f (engine.cpp:119,177)
-    ctl->diag_min_det_f = order_val(ctl->min_detf[s & 1]);
-    ctl->min_detf[s & 1] = order_key(1.0);
-  }
-  double v2 = __longlong_as_double(static_cast<long long>(ctl->max_v2));
-  if ((mode & kFinIndShift) && ctl->ind_lo[0] <= ctl->ind_hi[0]) {
+  // per-axis inputs
+  const bool ind_any = order_val(ctl->ind_lo[0]) <= order_val(ctl->ind_hi[0]);
+  double bl = order_val(ctl->bb_lo[a]), bh = order_val(ctl->bb_hi[a]);
+  double il = order_val(ctl->ind_lo[a]), ih = order_val(ctl->ind_hi[a]);
+  const double va = ctl->vind[a];
+  const int pl = ctl->prev_lo[a], ph = ctl->prev_hi[a];
+  const bool shift = (mode & kFinIndShift) && ind_any;
+  if (shift) {
     // The indenter moved rigidly with vind: fl(x + fl(dt v)) is monotone in
     // x, so its bbox moves by exactly the same rounded step as its particles.
-    for (int a = 0; a < 3; ++a) {
-      const double d = mul_rn(g.dt, ctl->vind[a]);
-      ctl->ind_lo[a] = order_key(add_rn(order_val(ctl->ind_lo[a]), d));
-      ctl->ind_hi[a] = order_key(add_rn(order_val(ctl->ind_hi[a]), d));
-    }
-    const double* u = ctl->vind;
-    v2 = fmax(v2, u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    const double d = mul_rn(g.dt, va);
+    il = add_rn(il, d);
+    ih = add_rn(ih, d);
   }
-  double lo[3], hi[3];
-  for (int a = 0; a < 3; ++a) {
-    lo[a] = fmin(order_val(ctl->bb_lo[a]), order_val(ctl->ind_lo[a]));
-    hi[a] = fmax(order_val(ctl->bb_hi[a]), order_val(ctl->ind_hi[a]));
-  }
+  const double lo = fmin(bl, il), hi = fmax(bh, ih);
+  int err = 0;  // warp-uniform
   if (mode & kFinAdvect) {
-    // engine.cpp:279-285
-    ctl->diag_max_speed = sqrt(v2);
-    ctl->step_count += 1;
-    ctl->substep = s + 1;
-    if (!in_range(g, lo) || !in_range(g, hi)) {
-      if (c.err_code == 0) {
-        c.err_code = kErrOutOfGrid;
-        c.err_substep = s;
+    // engine.cpp:279-285 (grid.cpp:29-36 per axis: xn = (x - o) / dx)
+    bool ok = true;
+    if (ax) {
+      const int b0 = static_cast<int>(floor(sub_rn(div_rn(sub_rn(lo, g.origin[a]), g.dx), 0.5)));
+      const int b1 = static_cast<int>(floor(sub_rn(div_rn(sub_rn(hi, g.origin[a]), g.dx), 0.5)));
+      ok = b0 >= 0 && b0 + 2 < g.res[a] && b1 >= 0 && b1 + 2 < g.res[a];
+    }
+    if (__any_sync(0xffffffffu, !ok)) err = 1;
+  }
+  int wlo = 0, whi = 0;
+  if (!err && (mode & kFinWindow)) {
+    // engine.cpp:60-85 — window [base(lo), base(hi) + 3); clear prev ∪ new.
+    bool ok = true;
+    if (ax) {
+      const int b0 = base_of(g, a, lo), b1 = base_of(g, a, hi);
+      ok = !(b0 < 0 || b1 + 2 >= g.res[a]);
+      wlo = b0;
+      whi = b1 + 3;
+    }
+    if (__any_sync(0xffffffffu, !ok)) err = 2;
+  }
+  const bool prev_empty = __any_sync(0xffffffffu, ax && ph - pl <= 0);
+  if (lane == 0) {
+    if (mode & kFinDiag) {  // particle_to_grid's min_det_f (engine.cpp:119,177)
+      ctl->diag_min_det_f = order_val(ctl->min_detf[s & 1]);
+      ctl->min_detf[s & 1] = order_key(1.0);
+    }
+    if (mode & kFinAdvect) {
+      double v2 = __longlong_as_double(static_cast<long long>(ctl->max_v2));
+      if (shift) {
+        const double u0 = ctl->vind[0], u1 = ctl->vind[1], u2 = ctl->vind[2];
+        v2 = fmax(v2, u0 * u0 + u1 * u1 + u2 * u2);
       }
-      *ctl_mem = c;
-      return;
+      ctl->diag_max_speed = sqrt(v2);
+      ctl->step_count += 1;
+      ctl->substep = s + 1;
+    }
+    if (err && ctl->err_code == 0) {
+      ctl->err_code = kErrOutOfGrid;
+      ctl->err_substep = err == 1 ? s : ((mode & kFinAdvect) ? s + 1 : s);
     }
   }
-  if (mode & kFinWindow) {
-    // engine.cpp:60-85 — window [base(lo), base(hi) + 3); clear prev ∪ new.
-    int wlo[3], whi[3];
-    for (int a = 0; a < 3; ++a) {
-      const int b0 = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(lo[a], g.origin[a]), g.inv_dx), 0.5)));
-      const int b1 = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(hi[a], g.origin[a]), g.inv_dx), 0.5)));
-      if (b0 < 0 || b1 + 2 >= g.res[a]) {
-        if (c.err_code == 0) {
-          c.err_code = kErrOutOfGrid;
-          c.err_substep = c.substep;
-        }
-        *ctl_mem = c;
-        return;
-      }
-      wlo[a] = b0;
-      whi[a] = b1 + 3;
-    }
+  if (ax && shift) {
+    ctl->ind_lo[a] = order_key(il);
+    ctl->ind_hi[a] = order_key(ih);
+  }
+  if (err) return;
+  if (ax && (mode & kFinWindow)) {
     // The two materials' own node boxes: grid_update only needs their union
     // (the stretch of the combined window between the gel and the indenter
     // holds no mass). An empty set gives an empty box.
-    for (int a = 0; a < 3; ++a) {
-      const double l[2] = {order_val(ctl->bb_lo[a]), order_val(ctl->ind_lo[a])};
-      const double h[2] = {order_val(ctl->bb_hi[a]), order_val(ctl->ind_hi[a])};
-      for (int m = 0; m < 2; ++m) {
-        if (l[m] <= h[m]) {
-          ctl->box_lo[m][a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(l[m], g.origin[a]), g.inv_dx), 0.5)));
-          ctl->box_hi[m][a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(h[m], g.origin[a]), g.inv_dx), 0.5))) + 3;
-        } else {
-          ctl->box_lo[m][a] = 0;
-          ctl->box_hi[m][a] = 0;
-        }
-      }
+    const double l[2] = {bl, il}, h[2] = {bh, ih};
+    for (int m = 0; m < 2; ++m) {
+      const bool any = l[m] <= h[m];
+      ctl->box_lo[m][a] = any ? base_of(g, a, l[m]) : 0;
+      ctl->box_hi[m][a] = any ? base_of(g, a, h[m]) + 3 : 0;
     }
-    int pmin = 1 << 30;
-    for (int a = 0; a < 3; ++a) pmin = min(pmin, ctl->prev_hi[a] - ctl->prev_lo[a]);
-    for (int a = 0; a < 3; ++a) {
-      ctl->clr_lo[a] = pmin <= 0 ? wlo[a] : min(wlo[a], ctl->prev_lo[a]);
-      ctl->clr_hi[a] = pmin <= 0 ? whi[a] : max(whi[a], ctl->prev_hi[a]);
-      ctl->win_lo[a] = ctl->prev_lo[a] = wlo[a];
-      ctl->win_hi[a] = ctl->prev_hi[a] = whi[a];
-    }
+    ctl->clr_lo[a] = prev_empty ? wlo : min(wlo, pl);
+    ctl->clr_hi[a] = prev_empty ? whi : max(whi, ph);
+    ctl->win_lo[a] = ctl->prev_lo[a] = wlo;
+    ctl->win_hi[a] = ctl->prev_hi[a] = whi;
   }
-  for (int a = 0; a < 3; ++a) {
+  if (ax) {
     ctl->bb_lo[a] = order_key(INFINITY);
     ctl->bb_hi[a] = order_key(-INFINITY);
   }
-  ctl->max_v2 = 0ull;
-  *ctl_mem = c;
+  if (lane == 0) ctl->max_v2 = 0ull;
 }
 
 // zero_grid's clear of Grid::mass / momentum over Ctl::clr (engine.cpp:72-83).
@@ -1621,7 +1628,7 @@ int launch_window(DeviceSim& s) {
     k_bbox<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.n, s.ctl, 1);
     ++k;
   }
-  k_finalize<<<1, 1, 0, s.stream>>>(s.ctl, s.geo, kFinWindow);
+  k_finalize<<<1, 32, 0, s.stream>>>(s.ctl, s.geo, kFinWindow);
   s.kernel_launches += k;  // reset counted in launch_reset
   return k + 1;
 }
@@ -1776,7 +1783,7 @@ int launch_ind_catchup(DeviceSim& s) {
 }
 
 int launch_finalize_step(DeviceSim& s) {
-  launch_pdl(k_finalize, dim3(1), dim3(1), 0, s.stream, s.ctl, s.geo,
+  launch_pdl(k_finalize, dim3(1), dim3(32), 0, s.stream, s.ctl, s.geo,
              static_cast<int>(kFinDiag | kFinAdvect | kFinWindow | (s.n_ind > 0 ? kFinIndShift : 0)));
   s.kernel_launches += 1;
   return 1;
@@ -1826,7 +1833,7 @@ int launch_phase_advect(DeviceSim& s) {
     k_bbox<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.n, s.ctl, 1);
     k += 3;
   }
-  k_finalize<<<1, 1, 0, s.stream>>>(s.ctl, s.geo, kFinAdvect);
+  k_finalize<<<1, 32, 0, s.stream>>>(s.ctl, s.geo, kFinAdvect);
   ++k;
   s.kernel_launches += k;
   return k;
