@@ -24,6 +24,9 @@ Fixtures (all numpy .npz):
                    by tests/scenes.bridge_script on the SMALL scene, plus the
                    init errors of BAD_CONFIGS: replies, steps.jsonl, the
                    .depth files (bytes) and the images (pixels).
+  parts.npz        mpm::init_scene from explicit parts (PARTS: gravity, moving
+                   indenter at creation, then a non-uniform indenter velocity):
+                   initial arrays and the state after PARTS_STEPS substeps.
   harness.npz      the reference's dataset::run_press_dataset on HARNESS
                    (2 objects x 2 positions x 3 depths): manifest.csv,
                    config.json, every image and .depth file; metrics::compare
@@ -44,7 +47,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import refpy as R  # noqa: E402
-from tests.scenes import (BAD_CONFIGS, HARNESS, CONFIG1, CONFIG5, CONFIG5_MOVE, CONFIG5_PRESS, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
+from tests.scenes import (BAD_CONFIGS, HARNESS, PARTS, PARTS_STEPS, PARTS_V, CONFIG1, CONFIG5, CONFIG5_MOVE, CONFIG5_PRESS, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
                           SMALL, SMALL3, SMALL3_PRESS, SMALL3_SHAPES, SMALL3_SLIDE, SMALL_STEPS,
                           SMALL_V, render_inputs, sha)
 
@@ -210,6 +213,41 @@ def harness():
         shutil.rmtree(root)
 
 
+def parts_indenter():
+    P = PARTS
+    pts = R.generate_cloud(P["ind_shape"], P["ind_points"], 11) * P["ind_scale"]
+    top = P["lat_origin"][2] + P["lat_dims"][2]
+    centre = np.array(P["lat_origin"][:2]) + 0.5 * np.array(P["lat_dims"][:2])
+    pts[:, :2] += centre - 0.5 * (pts[:, :2].min(0) + pts[:, :2].max(0))
+    pts[:, 2] += top + P["gap"] - pts[:, 2].min()
+    return pts
+
+
+def parts():
+    P = PARTS
+    ind = parts_indenter()
+    sim = R.RefSim.from_parts(P["res"], P["grid_edge"], P["lat_dims"], P["lat_counts"],
+                              P["lat_origin"], ind, dt=P["dt"], gravity=P["gravity"],
+                              ind_v0=P["ind_v0"], threads=0)
+    s0 = sim.state()
+    ne = sim.n_elastomer
+    rng = np.random.default_rng(21)
+    v = s0["v"].copy()
+    v[ne:] += rng.uniform(-0.01, 0.01, v[ne:].shape)  # non-uniform indenter velocity
+    sim.set_state(v=v)
+    sim.step(PARTS_V, PARTS_STEPS)
+    s1 = sim.state()
+    d = sim.diag()
+    surf = sim.surface()
+    np.savez_compressed(
+        os.path.join(OUT, "parts.npz"), ind=ind, n_elastomer=ne, x0=s0["x"], v0=v,
+        mass=s0["mass"], vol0=s0["vol0"], tag=s0["tag"], x=s1["x"], v=s1["v"],
+        F=s1["F"].reshape(-1, 9), C=s1["C"].reshape(-1, 9), min_det_f=d["min_det_f"],
+        max_speed=d["max_speed"], step_count=d["step_count"], surf_particle=surf["particle"],
+        surf_geom=np.array([surf["x0"], surf["y0"], surf["sx"], surf["sy"], surf["z0"]]),
+        surf_n=np.array([surf["nx"], surf["ny"]]))
+
+
 def bridge():
     import json
     import shutil
@@ -239,13 +277,15 @@ def bridge():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge", "harness"]
+    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge", "harness", "parts"]
     if "config5" in which:
         config5()
     if "bridge" in which:
         bridge()
     if "harness" in which:
         harness()
+    if "parts" in which:
+        parts()
     if "kat" in which:
         kat()
     if "small" in which:

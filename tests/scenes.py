@@ -151,3 +151,15 @@ HARNESS = {**SMALL,
            "press_grid": {"positions_x": 2, "positions_y": 1, "step_mm": 0.5,
                           "depths_mm": [0.0, 0.005, 0.01]},
            "alignment": {"dots": {"offset_px": [3.0, -2.0], "scale": 1.05}}}
+
+
+# init_scene from explicit parts (mpm::init_scene, scene.cpp:28-87) with the
+# options the config path does not exercise: gravity, a moving indenter at
+# creation and a non-uniform indenter velocity (set after creation), on a
+# non-cubic-count lattice. Torus indenter 1 um above a 4 x 4 x 1 mm gel.
+PARTS = dict(res=(48, 48, 48), grid_edge=0.0096, lat_dims=(0.004, 0.004, 0.001),
+             lat_counts=(21, 19, 6), lat_origin=(0.0028, 0.0028, 0.0038), dt=2e-6,
+             gravity=(0.0, 0.0, -9.81), ind_v0=(0.0, 0.0, -0.02), ind_shape="torus",
+             ind_points=2500, ind_scale=0.5, gap=1e-6)
+PARTS_STEPS = 120
+PARTS_V = (0.02, -0.01, -0.1)

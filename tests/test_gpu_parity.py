@@ -306,6 +306,39 @@ def test_config5_large_gel_matches_reference(tb, golden):
     assert np.abs(img.astype(int) - g["image"]).max() <= 2
 
 
+@pytest.mark.parametrize("with_surface", [True, False])
+def test_init_scene_parts_gravity_nonuniform_indenter(tb, golden, with_surface):
+    """mpm::init_scene from explicit arrays (tests/scenes.py PARTS) with gravity,
+    an indenter moving at creation and a non-uniform indenter velocity (the
+    direct indenter scatter), 21 x 19 x 6 lattice; with the surface lattice
+    (lattice-block CTA tiling) and without (flat tiling)."""
+    from tests.scenes import PARTS, PARTS_STEPS, PARTS_V
+
+    g = golden("parts.npz")
+    P = PARTS
+    params = dict(res=P["res"], dx=P["grid_edge"] / P["res"][0], origin=(0, 0, 0), dt=P["dt"],
+                  gravity=P["gravity"])
+    particles = dict(x=g["x0"], v=g["v0"], mass=g["mass"], volume0=g["vol0"], tag=g["tag"],
+                     n_elastomer=int(g["n_elastomer"]))
+    surface = None
+    if with_surface:
+        geom = g["surf_geom"]
+        surface = dict(nx=int(g["surf_n"][0]), ny=int(g["surf_n"][1]), x0=geom[0], y0=geom[1],
+                       sx=geom[2], sy=geom[3], z0=geom[4], particle=g["surf_particle"])
+    s = tb.init_scene(params, particles, surface)
+    tb.mpm.step(s, PARTS_V, PARTS_STEPS)
+    st = s.state()
+    disp = np.abs(g["x"] - g["x0"]).max()
+    assert np.abs(st["x"] - g["x"]).max() <= 1e-8 * disp
+    ne = int(g["n_elastomer"])
+    np.testing.assert_allclose(st["F"].reshape(-1, 9)[:ne], g["F"][:ne], rtol=0, atol=1e-11)
+    np.testing.assert_allclose(st["v"], g["v"], rtol=0, atol=1e-7 * np.abs(g["v"]).max())
+    d = s.diag
+    assert d.step_count == int(g["step_count"])
+    assert d.min_det_f == pytest.approx(float(g["min_det_f"]), abs=1e-12)
+    assert d.max_speed == pytest.approx(float(g["max_speed"]), rel=1e-9)
+
+
 def test_config2a_conserves_mass_and_momentum(tb):
     """Config 2a (1,214,221 particles): size-independent P2G invariants
     (SPEC.md:147-148): sum of node mass = sum of particle mass; with zero
