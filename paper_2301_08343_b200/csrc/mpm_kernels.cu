@@ -1357,7 +1357,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     // along z) in the shared tile before the gathers.
     tile_box(T, active, st_old.base);
     staged = T.ok != 0;
-    if (staged) tile_bulk_stage(T, g, vel);
+    if (staged && g.scatter_mode != 5) tile_bulk_stage(T, g, vel);
   }
   AccSrc src;
   if (kFused) {
@@ -1381,7 +1381,10 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     }
   }
   if (active) {
-    if (staged) g2p_gather_smem(g, T, st_old, vv, Cn);
+    if (g.scatter_mode == 5) {  // A/B timing: no velocity staging / gather
+      vv[0] = vv[1] = vv[2] = 0.0;
+      for (int i = 0; i < 9; ++i) Cn[i] = 0.0;
+    } else if (staged) g2p_gather_smem(g, T, st_old, vv, Cn);
     else if (kFused) g2p_gather_acc(g, src, px0, px1, px2, vv, Cn);
     else g2p_gather(g, vel, px0, px1, px2, vv, Cn);
     double G[9];
@@ -1392,13 +1395,15 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     matmul3(G, F0, F);  // F <- (I + dt C) F  (engine.cpp:250)
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
-      Cm[i * n_el + p] = Cn[i];
+      if (g.scatter_mode != 6) Cm[i * n_el + p] = Cn[i];  // 6: A/B timing, no C / v stores
       Fm[i * n_el + p] = F[i];
     }
     if (kBoundary && tag[p] == kElastomerBottom) vv[0] = vv[1] = vv[2] = 0.0;
-    v[p] = vv[0];
-    v[n + p] = vv[1];
-    v[2 * n + p] = vv[2];
+    if (g.scatter_mode != 6) {
+      v[p] = vv[0];
+      v[n + p] = vv[1];
+      v[2 * n + p] = vv[2];
+    }
     if (kAdvect) {
       px0 = advance(px0, g.dt, vv[0]);
       px1 = advance(px1, g.dt, vv[1]);
