@@ -30,7 +30,6 @@ int launch_finalize_step(DeviceSim& s);
 int launch_call_begin(DeviceSim& s);
 int launch_ind_cols(DeviceSim& s, bool move);
 int launch_ind_catchup(DeviceSim& s);
-int launch_zero_consumed(DeviceSim& s, int sms);
 int launch_phase_g2p(DeviceSim& s);
 int launch_phase_boundary(DeviceSim& s);
 int launch_phase_advect(DeviceSim& s);
@@ -88,11 +87,11 @@ DeviceSim::~DeviceSim() {
   cudaFree(C);
   cudaFree(F);
   cudaFree(tag);
-  cudaFree(grid_mp);
-  cudaFree(grid_v);
+  cudaFree(grid_mp.lo);
+  cudaFree(grid_mp.hi);
+  cudaFree(grid_v.lo);
+  cudaFree(grid_v.hi);
   cudaFree(grid_mi);
-  cudaFree(grid_mp_alt);
-  cudaFree(grid_mi_alt);
   cudaFree(col_start);
   cudaFree(ind_moves);
   cudaFree(surf_idx);
@@ -197,7 +196,6 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   g.stress_scale = -P->dt * 4.0 * g.inv_dx * g.inv_dx;
   if (const char* m = std::getenv("TACCHI_SCATTER")) g.scatter_mode = std::atoi(m);
   if (const char* f = std::getenv("TACCHI_FULL_INDENTER")) s->full_indenter = std::atoi(f) != 0;
-  if (const char* f = std::getenv("TACCHI_FUSED_GU")) s->fused_gu = std::atoi(f) != 0;
   s->sms = sm_count(device);
 
   // Indenter particles are re-ordered by base cell so that P2G scatters from
@@ -239,11 +237,11 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
             cudaMalloc(&s->C, std::max<int64_t>(9 * n_el, 1) * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->F, std::max<int64_t>(9 * n_el, 1) * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->tag, std::max<int64_t>(n_el, 1)) == cudaSuccess &&
-            cudaMalloc(&s->grid_mp, s->n_nodes * sizeof(double4)) == cudaSuccess &&
-            cudaMalloc(&s->grid_v, s->n_nodes * sizeof(double4)) == cudaSuccess &&
+            cudaMalloc(&s->grid_mp.lo, s->n_nodes * sizeof(double2)) == cudaSuccess &&
+            cudaMalloc(&s->grid_mp.hi, s->n_nodes * sizeof(double2)) == cudaSuccess &&
+            cudaMalloc(&s->grid_v.lo, s->n_nodes * sizeof(double2)) == cudaSuccess &&
+            cudaMalloc(&s->grid_v.hi, s->n_nodes * sizeof(double2)) == cudaSuccess &&
             cudaMalloc(&s->grid_mi, s->n_nodes * sizeof(double)) == cudaSuccess &&
-            cudaMalloc(&s->grid_mp_alt, s->n_nodes * sizeof(double4)) == cudaSuccess &&
-            cudaMalloc(&s->grid_mi_alt, s->n_nodes * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->col_start, std::max<size_t>(col_starts.size(), 1) * sizeof(int64_t)) ==
                 cudaSuccess &&
             cudaMalloc(&s->ind_moves, std::max<int64_t>(n_ind, 1)) == cudaSuccess &&
@@ -254,11 +252,11 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
     delete s;
     return fail(TG_ERR_CUDA, "tg_create: device allocation failed");
   }
-  cudaMemsetAsync(s->grid_mp, 0, s->n_nodes * sizeof(double4), s->stream);
-  cudaMemsetAsync(s->grid_v, 0, s->n_nodes * sizeof(double4), s->stream);
+  cudaMemsetAsync(s->grid_mp.lo, 0, s->n_nodes * sizeof(double2), s->stream);
+  cudaMemsetAsync(s->grid_mp.hi, 0, s->n_nodes * sizeof(double2), s->stream);
+  cudaMemsetAsync(s->grid_v.lo, 0, s->n_nodes * sizeof(double2), s->stream);
+  cudaMemsetAsync(s->grid_v.hi, 0, s->n_nodes * sizeof(double2), s->stream);
   cudaMemsetAsync(s->grid_mi, 0, s->n_nodes * sizeof(double), s->stream);
-  cudaMemsetAsync(s->grid_mp_alt, 0, s->n_nodes * sizeof(double4), s->stream);
-  cudaMemsetAsync(s->grid_mi_alt, 0, s->n_nodes * sizeof(double), s->stream);
   cudaMemsetAsync(s->ind_moves, 0, std::max<int64_t>(n_ind, 1), s->stream);
   s->n_cols = col_starts.empty() ? 0 : static_cast<int>(col_starts.size()) - 1;
   if (s->n_cols > 0)
@@ -346,10 +344,9 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
   s.window_valid = false;
   // A look-ahead scatter may have started anywhere in the grid: reset the
   // accumulators wholesale (errors are rare; this keeps the invariant simple).
-  CUDA_TRY(cudaMemsetAsync(s.grid_mp, 0, s.n_nodes * sizeof(double4), s.stream));
+  CUDA_TRY(cudaMemsetAsync(s.grid_mp.lo, 0, s.n_nodes * sizeof(double2), s.stream));
+  CUDA_TRY(cudaMemsetAsync(s.grid_mp.hi, 0, s.n_nodes * sizeof(double2), s.stream));
   CUDA_TRY(cudaMemsetAsync(s.grid_mi, 0, s.n_nodes * sizeof(double), s.stream));
-  CUDA_TRY(cudaMemsetAsync(s.grid_mp_alt, 0, s.n_nodes * sizeof(double4), s.stream));
-  CUDA_TRY(cudaMemsetAsync(s.grid_mi_alt, 0, s.n_nodes * sizeof(double), s.stream));
   s.grid_dirty = false;
   s.grid_ready = false;
   CUDA_TRY(cudaStreamSynchronize(s.stream));
@@ -368,21 +365,12 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
 // (grid_ready), the standalone scatter is skipped; every substep, the last one
 // included, scatters the next substep's particles, so consecutive step() calls
 // chain without a standalone scatter.
-// One substep of the step path. Fused (default): the G2P kernel computes
-// grid_update on its staged node box from A_s / M_I_s and scatters s+1 into
-// the other buffers; the indenter kernel re-zeroes A_s / M_I_s.
+// One substep of the step path.
 static int record_substep(DeviceSim& s, int sms, bool cols) {
-  int k = 0;
-  if (!s.fused_gu) k += launch_grid_update(s, sms, true);
+  int k = launch_grid_update(s, sms, true);
   k += launch_g2p2g_gel(s, true);
-  if (cols) {
-    k += launch_ind_cols(s, true);
-  } else {
-    k += launch_ind_move(s, true);
-    if (s.fused_gu) k += launch_zero_consumed(s, sms);
-  }
+  k += cols ? launch_ind_cols(s, true) : launch_ind_move(s, true);
   k += launch_finalize_step(s);
-  if (s.fused_gu) s.swap_buffers();
   return k;
 }
 
@@ -412,7 +400,7 @@ int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
   s.window_valid = true;
   if (s.use_graphs) {
     const int key = n_substeps * 32 + (s.grid_dirty ? 1 : 0) + (s.ind_v_uniform ? 2 : 0) +
-                    (s.grid_ready ? 4 : 0) + (s.fused_gu ? 8 : 0) + (s.cur_buf ? 16 : 0);
+                    (s.grid_ready ? 4 : 0);
     auto it = s.graphs.find(key);
     const bool replay = it != s.graphs.end();
     if (!replay) {
@@ -432,8 +420,6 @@ int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
     }
     CUDA_TRY(cudaGraphLaunch(it->second, s.stream));
     s.kernel_launches += s.graph_kernels[key];
-    // recording advanced the buffer pair substep by substep; a replay does not
-    if (replay && s.fused_gu && (n_substeps & 1)) s.swap_buffers();
   } else {
     CUDA_TRY(cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double),
                              cudaMemcpyHostToDevice, s.stream));
@@ -498,20 +484,15 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
   out_ms[1] = ms;
   for (int r = 0; r < reps; ++r) {
     cudaEventRecord(ev[2], s.stream);
-    if (!s.fused_gu) launch_grid_update(s, sms, true);
+    launch_grid_update(s, sms, true);
     cudaEventRecord(ev[3], s.stream);
     launch_g2p2g_gel(s, true);
     cudaEventRecord(ev[4], s.stream);
-    if (cols) {
-      launch_ind_cols(s, true);
-    } else {
-      launch_ind_move(s, true);
-      if (s.fused_gu) launch_zero_consumed(s, sms);
-    }
+    if (cols) launch_ind_cols(s, true);
+    else launch_ind_move(s, true);
     cudaEventRecord(ev[5], s.stream);
     launch_finalize_step(s);
     cudaEventRecord(ev[6], s.stream);
-    if (s.fused_gu) s.swap_buffers();
     CUDA_TRY(cudaEventSynchronize(ev[6]));
     for (int g = 2; g < kGroups; ++g) {
       cudaEventElapsedTime(&ms, ev[g], ev[g + 1]);

@@ -49,6 +49,14 @@ struct Geometry {
   int scatter_mode;     // 0: shared-memory tile (default), 1: direct RED (A/B switch)
 };
 
+// A dense node array in split layout: two 16-byte halves per node in two
+// arrays (node (i,j,k) at (i*res1 + j)*res2 + k). Grid::mass/momentum:
+// lo = {m, px}, hi = {py, pz}; Grid::velocity: lo = {vx, vy}, hi = {vz, 0}.
+struct NodeBuf {
+  double2* lo;
+  double2* hi;
+};
+
 struct DeviceSim {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -64,19 +72,11 @@ struct DeviceSim {
   uint8_t* tag = nullptr;  // n_el (Elastomer / ElastomerBottom)
   std::vector<int64_t> perm;  // internal index -> reference index (indenter sort)
 
-  // Dense node arrays (Grid::mass/momentum packed as double4 {m, px, py, pz};
-  // Grid::velocity as double4 {vx, vy, vz, 0}).
-  double4* grid_mp = nullptr;
-  double4* grid_v = nullptr;
+  // Dense node arrays (NodeBuf split layout).
+  NodeBuf grid_mp{nullptr, nullptr};  // Grid::mass / momentum (elastomer + direct indenter)
+  NodeBuf grid_v{nullptr, nullptr};   // Grid::velocity
   double* grid_mi = nullptr;  // indenter mass (uniform-velocity indenter scatter)
-  // Fused step path (grid_update inside the G2P staging): the accumulators
-  // are double-buffered; grid_mp / grid_mi always name the current substep's
-  // buffers, *_alt the next substep's (swap_buffers after every substep).
-  double4* grid_mp_alt = nullptr;
-  double* grid_mi_alt = nullptr;
-  int cur_buf = 0;
   int sms = 148;              // multiprocessor count of `device`
-  bool fused_gu = false;      // TACCHI_FUSED_GU=1: grid_update inside the G2P staging (A/B)
   // Indenter columns: maximal runs of equal initial (bx, by) in the sorted
   // cloud (internal indices [col_start[c], col_start[c+1])), z ascending.
   int n_cols = 0;
@@ -118,11 +118,6 @@ struct DeviceSim {
   int64_t kernel_launches = 0;
   int pending_start = 0;        // first substep of the in-flight step call
 
-  void swap_buffers() {
-    std::swap(grid_mp, grid_mp_alt);
-    std::swap(grid_mi, grid_mi_alt);
-    cur_buf ^= 1;
-  }
   ~DeviceSim();
 };
 

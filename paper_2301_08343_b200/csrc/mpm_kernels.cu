@@ -184,13 +184,15 @@ constexpr int kTileCap = TACCHI_TILE_CAP;  // nodes; 2816 -> 32 B x 2816 + 4 B x
 constexpr int kGelThreads = TACCHI_GEL_THREADS;
 constexpr int kGelMinBlocks = (2 * 256) / TACCHI_GEL_THREADS;
 
-// Node tile, array of structures so that a z-row of the CTA's node box is one
-// contiguous run in both shared and global memory (node (i,j,k) at
-// (i*res1 + j)*res2 + k, k fastest): rows move with single bulk-async (TMA)
-// copies / reductions. {m, px, py, pz} while scattering, {vx, vy, vz, -}
-// while staging the grid velocity for G2P.
+// Node tile in the grid's split layout (NodeBuf: two 16-byte halves per node
+// in two arrays), so that a z-row of the CTA's node box is one contiguous run
+// per half in both shared and global memory (node (i,j,k) at
+// (i*res1 + j)*res2 + k, k fastest): rows move with bulk-async (TMA) copies /
+// reductions, and 16-byte lanes of one half fall in distinct bank slots for
+// nodes up to 8 apart.
 struct P2GTile {
-  double4 node[kTileCap];
+  double2 nlo[kTileCap];  // {m, px} / {vx, vy}
+  double2 nhi[kTileCap];  // {py, pz} / {vz, -}
   int owner[kTileCap];
   int lo[3], hi[3], dim[3];
   int ok;
@@ -207,20 +209,22 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 // Adds the CTA's node box into the global grid: one bulk-async reduction
-// (UBLKRED.ADD.F64, element-wise atomic in L2) per z-row, issued by the
-// first dim0*dim1 threads. Call after a __syncthreads that follows the last
-// tile write (and a fence_proxy_async by every writer).
+// (UBLKRED.ADD.F64, element-wise atomic in L2) per z-row and half, issued by
+// the first 2*dim0*dim1 threads. Call after a __syncthreads that follows the
+// last tile write (and a fence_proxy_async by every writer).
 __device__ __forceinline__ void tile_bulk_reduce(const P2GTile& T, const Geometry& g,
-                                                 double4* grid) {
+                                                 NodeBuf grid) {
   const int rows = T.dim[0] * T.dim[1];
   const int d2 = T.dim[2];
   bool issued = false;
-  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+  for (int t = threadIdx.x; t < 2 * rows; t += blockDim.x) {
+    const int r = t >> 1, half = t & 1;
     const int i = r / T.dim[1], j = r - i * T.dim[1];
-    double4* dst = grid + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
+    double2* dst = (half ? grid.hi : grid.lo) + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
+    const double2* src = (half ? T.nhi : T.nlo) + r * d2;
     asm volatile(
         "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
-        "r"(smem_addr(&T.node[r * d2])), "r"(static_cast<unsigned>(d2 * sizeof(double4)))
+        "r"(smem_addr(src)), "r"(static_cast<unsigned>(d2 * sizeof(double2)))
         : "memory");
     issued = true;
   }
@@ -231,11 +235,11 @@ __device__ __forceinline__ void tile_bulk_reduce(const P2GTile& T, const Geometr
   }
 }
 
-// Stages grid rows [lo, lo + dim) of `src` into T.node with bulk-async copies
-// completing on T.bar; every thread returns after the bytes landed. All
-// threads of the block must call it; T.dim / T.lo / T.ok set by tile_box.
-__device__ __forceinline__ void tile_bulk_stage(P2GTile& T, const Geometry& g,
-                                                const double4* src) {
+// Stages grid rows [lo, lo + dim) of `src` (both halves) into T with
+// bulk-async copies completing on T.bar; every thread returns after the bytes
+// landed. All threads of the block must call it; T.dim / T.lo / T.ok set by
+// tile_box.
+__device__ __forceinline__ void tile_bulk_stage(P2GTile& T, const Geometry& g, NodeBuf src) {
   const int rows = T.dim[0] * T.dim[1];
   const int d2 = T.dim[2];
   const unsigned bar = smem_addr(&T.bar);
@@ -243,17 +247,19 @@ __device__ __forceinline__ void tile_bulk_stage(P2GTile& T, const Geometry& g,
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                 "r"(static_cast<unsigned>(rows * d2 * sizeof(double4)))
+                 "r"(static_cast<unsigned>(2 * rows * d2 * sizeof(double2)))
                  : "memory");
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+  for (int t = threadIdx.x; t < 2 * rows; t += blockDim.x) {
+    const int r = t >> 1, half = t & 1;
     const int i = r / T.dim[1], j = r - i * T.dim[1];
-    const double4* s = src + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
+    const double2* sp = (half ? src.hi : src.lo) + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
+    double2* dp = (half ? T.nhi : T.nlo) + r * d2;
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_addr(&T.node[r * d2])),
-        "l"(s), "r"(static_cast<unsigned>(d2 * sizeof(double4))), "r"(bar)
+            "r"(smem_addr(dp)),
+        "l"(sp), "r"(static_cast<unsigned>(d2 * sizeof(double2))), "r"(bar)
         : "memory");
   }
   asm volatile(
@@ -274,7 +280,7 @@ struct P2GPayload {
   double aff[9];
 };
 
-__device__ __forceinline__ void scatter_direct(const Geometry& g, double4* grid, double m,
+__device__ __forceinline__ void scatter_direct(const Geometry& g, NodeBuf grid, double m,
                                                const P2GPayload& q) {
   const double dx = g.dx;
 #pragma unroll
@@ -288,16 +294,17 @@ __device__ __forceinline__ void scatter_direct(const Geometry& g, double4* grid,
       const double m0 = q.mv[0] + q.aff[0] * dxa + q.aff[1] * dxb;
       const double m1 = q.mv[1] + q.aff[3] * dxa + q.aff[4] * dxb;
       const double m2 = q.mv[2] + q.aff[6] * dxa + q.aff[7] * dxb;
-      double* row = reinterpret_cast<double*>(
-          grid + node_index(g, q.st.base[0] + a, q.st.base[1] + b, q.st.base[2]));
+      const size_t row = node_index(g, q.st.base[0] + a, q.st.base[1] + b, q.st.base[2]);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double w = wab * q.st.w[2][c];
         const double dxc = (c - q.st.fx[2]) * dx;
-        red_add(row + 4 * c + 0, w * m);
-        red_add(row + 4 * c + 1, w * (m0 + q.aff[2] * dxc));
-        red_add(row + 4 * c + 2, w * (m1 + q.aff[5] * dxc));
-        red_add(row + 4 * c + 3, w * (m2 + q.aff[8] * dxc));
+        double* lo = reinterpret_cast<double*>(grid.lo + row + c);
+        double* hi = reinterpret_cast<double*>(grid.hi + row + c);
+        red_add(lo + 0, w * m);
+        red_add(lo + 1, w * (m0 + q.aff[2] * dxc));
+        red_add(hi + 0, w * (m1 + q.aff[5] * dxc));
+        red_add(hi + 1, w * (m2 + q.aff[8] * dxc));
       }
     }
   }
@@ -374,7 +381,7 @@ __device__ void tile_box(P2GTile& T, bool active, const int* base) {
 // does; the rare duplicates (detected through the owner table) and CTAs whose
 // footprint exceeds the tile fall back to direct REDs.
 __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
-                                 const Geometry& g, double4* grid) {
+                                 const Geometry& g, NodeBuf grid) {
   const int tid = threadIdx.x;
   if (g.scatter_mode == 1) {  // A/B: per-particle REDs, no tile
     if (active) scatter_direct(g, grid, m, q);
@@ -388,9 +395,8 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
   if (use_tile) {
     const double2 z2 = make_double2(0.0, 0.0);
     for (int e = tid; e < vol; e += blockDim.x) {
-      double2* n2 = reinterpret_cast<double2*>(&T.node[e]);
-      n2[0] = z2;
-      n2[1] = z2;
+      T.nlo[e] = z2;
+      T.nhi[e] = z2;
       T.owner[e] = -1;
     }
   }
@@ -424,14 +430,13 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
           const double dxc = (c - q.st.fx[2]) * dx;
           const double w = wab * q.st.w[2][c];
           const int e = base_idx + (a * d1 + b) * d2 + c;
-          double2* n2 = reinterpret_cast<double2*>(&T.node[e]);
-          double2 lo2 = n2[0], hi2 = n2[1];
+          double2 lo2 = T.nlo[e], hi2 = T.nhi[e];
           lo2.x += w * m;
           lo2.y += w * (m0 + q.aff[2] * dxc);
           hi2.x += w * (m1 + q.aff[5] * dxc);
           hi2.y += w * (m2 + q.aff[8] * dxc);
-          n2[0] = lo2;
-          n2[1] = hi2;
+          T.nlo[e] = lo2;
+          T.nhi[e] = hi2;
         }
       }
     }
@@ -632,12 +637,12 @@ __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode)
 }
 
 // zero_grid's clear of Grid::mass / momentum over Ctl::clr (engine.cpp:72-83).
-__global__ void k_clear(double4* __restrict__ grid, double* __restrict__ mi, Ctl* ctl, Geometry g) {
+__global__ void k_clear(NodeBuf grid, double* __restrict__ mi, Ctl* ctl, Geometry g) {
   if (stale(ctl, ctl->substep)) return;
   const int lx = ctl->clr_lo[0], ly = ctl->clr_lo[1], lz = ctl->clr_lo[2];
   const int ny = ctl->clr_hi[1] - ly, nz = ctl->clr_hi[2] - lz;
   const int64_t total = static_cast<int64_t>(ctl->clr_hi[0] - lx) * ny * nz;
-  const double4 z = make_double4(0, 0, 0, 0);
+  const double2 z = make_double2(0, 0);
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int k = static_cast<int>(t % nz);
@@ -645,7 +650,8 @@ __global__ void k_clear(double4* __restrict__ grid, double* __restrict__ mi, Ctl
     const int j = static_cast<int>(r % ny);
     const int i = static_cast<int>(r / ny);
     const size_t nd = node_index(g, lx + i, ly + j, lz + k);
-    grid[nd] = z;
+    grid.lo[nd] = z;
+    grid.hi[nd] = z;
     mi[nd] = 0.0;
   }
 }
@@ -658,7 +664,7 @@ __global__ void k_clear(double4* __restrict__ grid, double* __restrict__ mi, Ctl
 __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_p2g_gel_tile(
     const double* __restrict__ x, const double* __restrict__ v, const double* __restrict__ Cm,
     const double* __restrict__ Fm, int64_t n, int64_t n_el, GelMap M, Ctl* ctl, Geometry g,
-    double4* __restrict__ grid, double m, double vol0) {
+    NodeBuf grid, double m, double vol0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   P2GTile& T = *reinterpret_cast<P2GTile*>(smem_raw);
   const int s = ctl->substep;
@@ -690,7 +696,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_p2g_gel_tile(
 __global__ void __launch_bounds__(256) k_p2g_ind_direct(const double* __restrict__ x,
                                                         const double* __restrict__ v, int64_t n,
                                                         int64_t n_el, Ctl* ctl, Geometry g,
-                                                        double4* __restrict__ grid, double m) {
+                                                        NodeBuf grid, double m) {
   if (stale(ctl, ctl->substep)) return;
   const int64_t p = n_el + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -887,34 +893,6 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
 // accumulate pending moves that k_ind_catchup applies (the same sequence of
 // rounded adds) before mpm::step returns.
 // ---------------------------------------------------------------------------
-// Re-zeroes the accumulators of the substep just consumed (A_s over the
-// elastomer and indenter node boxes, M_I_s over the indenter box; the boxes
-// are P2G(s)'s footprints, Ctl::box_* until k_finalize(s) replaces them), so
-// the buffer is clean when the scatter of substep s + 2 lands in it. Work is
-// split over `nblocks` blocks starting at block `b0`.
-__device__ __forceinline__ void zero_consumed(double4* __restrict__ mp, double* __restrict__ mi,
-                                              const Ctl* ctl, const Geometry& g, int b0,
-                                              int nblocks) {
-  const int first = (blockIdx.x - b0) * blockDim.x + threadIdx.x, step = nblocks * blockDim.x;
-  const double2 z2 = make_double2(0.0, 0.0);
-  for (int m = 0; m < 2; ++m) {
-    int lo[3], dm[3], vol = 1;
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = ctl->box_lo[m][a];
-      dm[a] = max(ctl->box_hi[m][a] - lo[a], 0);
-      vol *= dm[a];
-    }
-    if (vol <= 0) continue;
-    for (BoxIter it(first, step, dm[1], dm[2]); it.e < vol; it.next(dm[1], dm[2])) {
-      const size_t nd = node_index(g, lo[0] + it.i, lo[1] + it.j, lo[2] + it.k);
-      double2* q = reinterpret_cast<double2*>(mp + nd);
-      q[0] = z2;
-      q[1] = z2;
-      if (m == 1) mi[nd] = 0.0;
-    }
-  }
-}
-
 __global__ void k_call_begin(Ctl* ctl) { ctl->call_start = ctl->substep; }
 
 constexpr int kColWarps = 8;
@@ -925,13 +903,11 @@ struct ColSmem {
   int run_start[kColWarps][33];
 };
 
-// Blocks >= col_blocks (step path) re-zero the consumed accumulators
-// (zero_consumed) alongside the column walks.
 template <bool kMove>
 __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
     double* __restrict__ x, int64_t n, int64_t n_el, const int64_t* __restrict__ col_start,
     int n_cols, uint8_t* __restrict__ moves, Ctl* ctl, Geometry g, double* __restrict__ mi,
-    int box_from_bb, double4* __restrict__ zero_mp, double* __restrict__ zero_mi, int col_blocks) {
+    int box_from_bb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ColSmem& S = *reinterpret_cast<ColSmem*>(smem_raw);
   pdl_wait();
@@ -942,10 +918,6 @@ __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
     ctl->ind_v[0] = ctl->vind[0];  // apply_boundary (engine.cpp:260-261)
     ctl->ind_v[1] = ctl->vind[1];
     ctl->ind_v[2] = ctl->vind[2];
-  }
-  if (zero_mp != nullptr && static_cast<int>(blockIdx.x) >= col_blocks) {
-    zero_consumed(zero_mp, zero_mi, ctl, g, col_blocks, gridDim.x - col_blocks);
-    return;
   }
   const int c = blockIdx.x * kColWarps + warp;
   if (c >= n_cols) return;  // warp-uniform; only __syncwarp below
@@ -1100,12 +1072,13 @@ __device__ __forceinline__ double4 node_velocity(const Geometry& g, double4 q, d
 // Node update of the grid_update kernels; kZero also re-zeroes A / M_I.
 // with_mi: the node may hold indenter weight (inside the indenter box).
 template <bool kZero>
-__device__ __forceinline__ void update_node(double4* __restrict__ mp, double* __restrict__ mi,
-                                            double4* __restrict__ vel, const Geometry& g,
+__device__ __forceinline__ void update_node(NodeBuf mp, double* __restrict__ mi,
+                                            NodeBuf vel, const Geometry& g,
                                             double m_ind, double u0, double u1, double u2, int i,
                                             int j, int k, bool with_mi) {
   const size_t nd = node_index(g, i, j, k);
-  const double4 q = mp[nd];
+  const double2 qa = mp.lo[nd], qb = mp.hi[nd];
+  const double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
   const double wi = with_mi ? mi[nd] : 0.0;
   double4 o = node_velocity(g, q, wi, m_ind, u0, u1, u2, i, j, k);
   const bool massive = o.w != 0.0;
@@ -1113,24 +1086,23 @@ __device__ __forceinline__ void update_node(double4* __restrict__ mp, double* __
   // Step path: nodes without mass keep their (finite) stale velocity; every
   // G2P read of such a node carries B-spline weight exactly 0 (the particle's
   // own scatter would have given it mass otherwise).
-  if (!kZero || massive) vel[nd] = o;
+  if (!kZero || massive) {
+    vel.lo[nd] = make_double2(o.x, o.y);
+    vel.hi[nd] = make_double2(o.z, 0.0);
+  }
   if (kZero) {
-    if (q.x != 0.0 || q.y != 0.0 || q.z != 0.0 || q.w != 0.0) mp[nd] = make_double4(0, 0, 0, 0);
+    if (q.x != 0.0 || q.y != 0.0 || q.z != 0.0 || q.w != 0.0) {
+      mp.lo[nd] = make_double2(0, 0);
+      mp.hi[nd] = make_double2(0, 0);
+    }
     if (wi != 0.0) mi[nd] = 0.0;
   }
 }
 
-__global__ void k_zero_consumed(double4* __restrict__ mp, double* __restrict__ mi, Ctl* ctl,
-                                Geometry g) {
-  pdl_wait();
-  if (stale(ctl, ctl->substep)) return;
-  zero_consumed(mp, mi, ctl, g, 0, gridDim.x);
-}
-
 // Phase API: the full active window, as the reference (Grid::velocity is 0
 // on every massless window node).
-__global__ void k_grid_update_window(double4* __restrict__ mp, double* __restrict__ mi,
-                                     double4* __restrict__ vel, Ctl* ctl, Geometry g,
+__global__ void k_grid_update_window(NodeBuf mp, double* __restrict__ mi, NodeBuf vel,
+                                     Ctl* ctl, Geometry g,
                                      double m_ind) {
   if (stale(ctl, ctl->substep)) return;
   const int lx = ctl->win_lo[0], ly = ctl->win_lo[1], lz = ctl->win_lo[2];
@@ -1145,8 +1117,8 @@ __global__ void k_grid_update_window(double4* __restrict__ mp, double* __restric
 // Step path: only the union of the elastomer and indenter node boxes (every
 // node a scatter can have touched), re-zeroing the accumulators. M_I is read
 // only inside the indenter box.
-__global__ void k_grid_update_boxes(double4* __restrict__ mp, double* __restrict__ mi,
-                                    double4* __restrict__ vel, Ctl* ctl, Geometry g,
+__global__ void k_grid_update_boxes(NodeBuf mp, double* __restrict__ mi, NodeBuf vel,
+                                    Ctl* ctl, Geometry g,
                                     double m_ind) {
   pdl_wait();
   if (stale(ctl, ctl->substep)) return;
@@ -1184,7 +1156,7 @@ __global__ void k_grid_update_boxes(double4* __restrict__ mp, double* __restrict
 
 namespace {
 // engine.cpp:217-249 for one particle: v and C from the node velocities.
-__device__ __forceinline__ void g2p_gather(const Geometry& g, const double4* __restrict__ vel,
+__device__ __forceinline__ void g2p_gather(const Geometry& g, NodeBuf vel,
                                            double px0, double px1, double px2, double* vv,
                                            double* Cn) {
   Stencil st;
@@ -1199,13 +1171,12 @@ __device__ __forceinline__ void g2p_gather(const Geometry& g, const double4* __r
     for (int b = 0; b < 3; ++b) {
       const double wab = wa * st.w[1][b];
       const double db = b - st.fx[1];
-      const double4* row = vel + node_index(g, st.base[0] + a, st.base[1] + b, st.base[2]);
+      const size_t row = node_index(g, st.base[0] + a, st.base[1] + b, st.base[2]);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double w = wab * st.w[2][c];
         const double dc = c - st.fx[2];
-        const double2* q2 = reinterpret_cast<const double2*>(row + c);
-        const double2 qa = __ldg(q2), qb = __ldg(q2 + 1);
+        const double2 qa = __ldg(vel.lo + row + c), qb = __ldg(vel.hi + row + c);
         const double wv0 = w * qa.x, wv1 = w * qa.y, wv2 = w * qb.x;
         v0 += wv0; v1 += wv1; vz += wv2;
         b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
@@ -1224,66 +1195,8 @@ __device__ __forceinline__ void g2p_gather(const Geometry& g, const double4* __r
 }
 }  // namespace
 
-// Grid-update inputs of the fused step path: G2P computes node velocities
-// from the accumulators of substep s (A_s, and M_I_s inside the indenter's
-// P2G footprint) instead of a materialised Grid::velocity.
-struct AccSrc {
-  const double4* acc;
-  const double* mi;
-  int lo[3], hi[3];  // indenter node box of P2G(s)
-  double u[3];       // uniform indenter velocity of P2G(s)
-  double m_ind;
-};
-
-__device__ __forceinline__ bool in_ind_box(const AccSrc& A, int i, int j, int k) {
-  return i >= A.lo[0] && i < A.hi[0] && j >= A.lo[1] && j < A.hi[1] && k >= A.lo[2] &&
-         k < A.hi[2];
-}
-
-__device__ __forceinline__ double4 acc_velocity(const Geometry& g, const AccSrc& A, int i, int j,
-                                                int k) {
-  const size_t nd = node_index(g, i, j, k);
-  const double wi = in_ind_box(A, i, j, k) ? A.mi[nd] : 0.0;
-  return node_velocity(g, A.acc[nd], wi, A.m_ind, A.u[0], A.u[1], A.u[2], i, j, k);
-}
-
-// g2p_gather with node velocities computed from the accumulators (fallback
-// when the CTA footprint exceeds the shared tile).
-__device__ __forceinline__ void g2p_gather_acc(const Geometry& g, const AccSrc& A, double px0,
-                                               double px1, double px2, double* vv, double* Cn) {
-  Stencil st;
-  make_stencil(px0, px1, px2, g.origin, g.inv_dx, st);
-  double v0 = 0, v1 = 0, vz = 0;
-  double b00 = 0, b01 = 0, b02 = 0, b10 = 0, b11 = 0, b12 = 0, b20 = 0, b21 = 0, b22 = 0;
-  for (int a = 0; a < 3; ++a) {
-    const double wa = st.w[0][a];
-    const double da = a - st.fx[0];
-    for (int b = 0; b < 3; ++b) {
-      const double wab = wa * st.w[1][b];
-      const double db = b - st.fx[1];
-      for (int c = 0; c < 3; ++c) {
-        const double w = wab * st.w[2][c];
-        const double dc = c - st.fx[2];
-        const double4 q = acc_velocity(g, A, st.base[0] + a, st.base[1] + b, st.base[2] + c);
-        const double wv0 = w * q.x, wv1 = w * q.y, wv2 = w * q.z;
-        v0 += wv0; v1 += wv1; vz += wv2;
-        b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
-        b10 += wv1 * da; b11 += wv1 * db; b12 += wv1 * dc;
-        b20 += wv2 * da; b21 += wv2 * db; b22 += wv2 * dc;
-      }
-    }
-  }
-  vv[0] = v0;
-  vv[1] = v1;
-  vv[2] = vz;
-  const double k = 4.0 * g.inv_dx;
-  Cn[0] = k * b00; Cn[1] = k * b01; Cn[2] = k * b02;
-  Cn[3] = k * b10; Cn[4] = k * b11; Cn[5] = k * b12;
-  Cn[6] = k * b20; Cn[7] = k * b21; Cn[8] = k * b22;
-}
-
 // G2P gather from the CTA's node box staged in shared memory (vx, vy, vz in
-// T.node[.].x/y/z), same arithmetic as g2p_gather.
+// T.nlo[.].x/y, T.nhi[.].x), same arithmetic as g2p_gather.
 __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile& T,
                                                 const Stencil& st, double* vv, double* Cn) {
   const int d1 = T.dim[1], d2 = T.dim[2];
@@ -1303,8 +1216,8 @@ __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile
       for (int c = 0; c < 3; ++c) {
         const double w = wab * st.w[2][c];
         const double dc = c - st.fx[2];
-        const double2 vxy = *reinterpret_cast<const double2*>(&T.node[row + c]);
-        const double vzz = T.node[row + c].z;
+        const double2 vxy = T.nlo[row + c];
+        const double vzz = T.nhi[row + c].x;
         const double wv0 = w * vxy.x, wv1 = w * vxy.y, wv2 = w * vzz;
         v0 += wv0; v1 += wv1; vz += wv2;
         b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
@@ -1322,14 +1235,12 @@ __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile
   Cn[6] = k * b20; Cn[7] = k * b21; Cn[8] = k * b22;
 }
 
-// kFused (step path): `vel` is A_s and `mi_cur` M_I_s; grid_update runs on
-// the staged node box (node_velocity) instead of in a separate pass.
-template <bool kBoundary, bool kAdvect, bool kLookahead, bool kFused = false>
+template <bool kBoundary, bool kAdvect, bool kLookahead>
 __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     double* __restrict__ x, double* __restrict__ v, double* __restrict__ Cm,
     double* __restrict__ Fm, const uint8_t* __restrict__ tag, int64_t n, int64_t n_el, GelMap M,
-    Ctl* ctl, Geometry g, const double4* __restrict__ vel, double4* __restrict__ grid, double m,
-    double vol0, const double* __restrict__ mi_cur, double m_ind) {
+    Ctl* ctl, Geometry g, NodeBuf vel, NodeBuf grid, double m,
+    double vol0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   P2GTile& T = *reinterpret_cast<P2GTile*>(smem_raw);
   pdl_wait();
@@ -1359,33 +1270,11 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     staged = T.ok != 0;
     if (staged && g.scatter_mode != 5) tile_bulk_stage(T, g, vel);
   }
-  AccSrc src;
-  if (kFused) {
-    src.acc = vel;
-    src.mi = mi_cur;
-    for (int a = 0; a < 3; ++a) {
-      src.lo[a] = ctl->box_lo[1][a];
-      src.hi[a] = ctl->box_hi[1][a];
-      src.u[a] = ctl->ind_v[a];
-    }
-    src.m_ind = m_ind;
-    if (staged) {  // grid_update (engine.cpp:180-205) of the staged box, in place
-      const int d1 = T.dim[1], d2 = T.dim[2];
-      const int vol = T.dim[0] * d1 * d2;
-      for (BoxIter it(threadIdx.x, blockDim.x, d1, d2); it.e < vol; it.next(d1, d2)) {
-        const int i = T.lo[0] + it.i, j = T.lo[1] + it.j, k = T.lo[2] + it.k;
-        const double wi = in_ind_box(src, i, j, k) ? mi_cur[node_index(g, i, j, k)] : 0.0;
-        T.node[it.e] = node_velocity(g, T.node[it.e], wi, m_ind, src.u[0], src.u[1], src.u[2], i, j, k);
-      }
-      __syncthreads();
-    }
-  }
   if (active) {
     if (g.scatter_mode == 5) {  // A/B timing: no velocity staging / gather
       vv[0] = vv[1] = vv[2] = 0.0;
       for (int i = 0; i < 9; ++i) Cn[i] = 0.0;
     } else if (staged) g2p_gather_smem(g, T, st_old, vv, Cn);
-    else if (kFused) g2p_gather_acc(g, src, px0, px1, px2, vv, Cn);
     else g2p_gather(g, vel, px0, px1, px2, vv, Cn);
     double G[9];
 #pragma unroll
@@ -1502,8 +1391,8 @@ __global__ void k_p2g_done(Ctl* ctl) {
 
 // Copies a node box [lo, hi) into dense staging buffers (tg_download_grid):
 // Grid::mass / momentum as the reference holds them (elastomer + indenter).
-__global__ void k_gather_box(const double4* __restrict__ mp, const double* __restrict__ mi,
-                             const double4* __restrict__ vel, const Ctl* ctl, Geometry g,
+__global__ void k_gather_box(NodeBuf mp, const double* __restrict__ mi, NodeBuf vel,
+                             const Ctl* ctl, Geometry g,
                              double m_ind, int3 lo, int3 hi, double* __restrict__ mass,
                              double* __restrict__ mom, double* __restrict__ velo) {
   const int ny = hi.y - lo.y, nz = hi.z - lo.z;
@@ -1515,9 +1404,11 @@ __global__ void k_gather_box(const double4* __restrict__ mp, const double* __res
     const int j = lo.y + static_cast<int>(r % ny);
     const int i = lo.x + static_cast<int>(r / ny);
     const size_t nd = node_index(g, i, j, k);
-    const double4 q = mp[nd];
+    const double2 qa = mp.lo[nd], qb = mp.hi[nd];
+    const double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
     const double M = mi[nd] * m_ind;
-    const double4 u = vel[nd];
+    const double2 ua = vel.lo[nd], ub = vel.hi[nd];
+    const double4 u = make_double4(ua.x, ua.y, ub.x, 0.0);
     mass[t] = q.x + M;
     mom[3 * t] = q.y + M * ctl->ind_v[0];
     mom[3 * t + 1] = q.z + M * ctl->ind_v[1];
@@ -1582,8 +1473,6 @@ void configure_once() {
                        static_cast<int>(kTileSmem));
   cudaFuncSetAttribute(k_g2p2g_gel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(kTileSmem));
-  cudaFuncSetAttribute(k_g2p2g_gel<true, true, true, true>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTileSmem));
   cudaFuncSetAttribute(k_ind_move_p2g<false, true>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIndSmem));
   cudaFuncSetAttribute(k_ind_move_p2g<true, true>,
@@ -1698,20 +1587,14 @@ int launch_grid_update(DeviceSim& s, int sms, bool zero) {
 int launch_g2p2g_gel(DeviceSim& s, bool lookahead) {
   if (s.n_el <= 0) return 0;
   configure_once();
-  if (lookahead && s.fused_gu)
-    launch_pdl(k_g2p2g_gel<true, true, true, true>, dim3(gel_blocks(s)), dim3(kGelThreads),
-               kTileSmem, s.stream, s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl,
-               s.geo, static_cast<const double4*>(s.grid_mp), s.grid_mp_alt, s.m_el, s.vol_el,
-               static_cast<const double*>(s.grid_mi), s.m_ind);
-  else if (lookahead)
+  if (lookahead)
     launch_pdl(k_g2p2g_gel<true, true, true>, dim3(gel_blocks(s)), dim3(kGelThreads), kTileSmem,
                s.stream, s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo,
-               static_cast<const double4*>(s.grid_v), s.grid_mp, s.m_el, s.vol_el,
-               static_cast<const double*>(nullptr), 0.0);
+               s.grid_v, s.grid_mp, s.m_el, s.vol_el);
   else
     k_g2p2g_gel<true, true, false><<<gel_blocks(s), kGelThreads, 0, s.stream>>>(
         s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
-        s.m_el, s.vol_el, nullptr, 0.0);
+        s.m_el, s.vol_el);
   s.kernel_launches += 1;
   return 1;
 }
@@ -1721,19 +1604,11 @@ int launch_ind_move(DeviceSim& s, bool lookahead) {
   configure_once();
   if (lookahead)
     k_ind_move_p2g<true, true><<<ind_blocks(s), kIndThreads, kIndSmem, s.stream>>>(
-        s.x, s.n, s.n_el, s.ctl, s.geo, s.fused_gu ? s.grid_mi_alt : s.grid_mi);
+        s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   else
     k_ind_move_p2g<true, false><<<ind_blocks(s), kIndThreads, 0, s.stream>>>(
         s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
   s.ind_v_uniform = true;
-  s.kernel_launches += 1;
-  return 1;
-}
-
-// Fused step path without the column walk: re-zero the consumed buffers.
-int launch_zero_consumed(DeviceSim& s, int sms) {
-  launch_pdl(k_zero_consumed, dim3(2 * sms), dim3(kThreads), 0, s.stream, s.grid_mp, s.grid_mi,
-             s.ctl, s.geo);
   s.kernel_launches += 1;
   return 1;
 }
@@ -1759,21 +1634,13 @@ int launch_ind_cols(DeviceSim& s, bool move) {
     attr = true;
   }
   const unsigned blocks = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
-  if (move && s.fused_gu) {  // scatter into the next buffer, zero the consumed one
-    const unsigned zblocks = static_cast<unsigned>(2 * s.sms);
-    launch_pdl(k_ind_cols<true>, dim3(blocks + zblocks), dim3(kColWarps * 32), kColSmem, s.stream,
-               s.x, s.n, s.n_el, static_cast<const int64_t*>(s.col_start), s.n_cols, s.ind_moves,
-               s.ctl, s.geo, s.grid_mi_alt, 1, s.grid_mp, s.grid_mi, static_cast<int>(blocks));
-  } else if (move) {
+  if (move)
     launch_pdl(k_ind_cols<true>, dim3(blocks), dim3(kColWarps * 32), kColSmem, s.stream, s.x,
                s.n, s.n_el, static_cast<const int64_t*>(s.col_start), s.n_cols, s.ind_moves,
-               s.ctl, s.geo, s.grid_mi, 1, static_cast<double4*>(nullptr),
-               static_cast<double*>(nullptr), static_cast<int>(blocks));
-  } else {
+               s.ctl, s.geo, s.grid_mi, 1);
+  else
     k_ind_cols<false><<<blocks, kColWarps * 32, kColSmem, s.stream>>>(
-        s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 0,
-        nullptr, nullptr, static_cast<int>(blocks));
-  }
+        s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 0);
   s.ind_v_uniform = true;
   s.kernel_launches += 1;
   return 1;
@@ -1798,7 +1665,7 @@ int launch_phase_g2p(DeviceSim& s) {
   if (s.n_el <= 0) return 0;
   k_g2p2g_gel<false, false, false><<<gel_blocks(s), kGelThreads, 0, s.stream>>>(
       s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
-      s.m_el, s.vol_el, nullptr, 0.0);
+      s.m_el, s.vol_el);
   s.kernel_launches += 1;
   return 1;
 }
