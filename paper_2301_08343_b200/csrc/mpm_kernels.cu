@@ -1254,13 +1254,15 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
   Stencil st_old;
   double F0[9];
   if (active) {
-    px0 = x[p];
-    px1 = x[n + p];
-    px2 = x[2 * n + p];
+    // particle state streams through once per substep: evict-first loads and
+    // stores (ld/st .cs) keep L2 for the grid arrays the next kernels reuse
+    px0 = __ldcs(x + p);
+    px1 = __ldcs(x + n + p);
+    px2 = __ldcs(x + 2 * n + p);
     // issue the deformation-gradient loads now; they complete while the
     // footprint is reduced and the velocity tile is staged
 #pragma unroll
-    for (int i = 0; i < 9; ++i) F0[i] = Fm[i * n_el + p];
+    for (int i = 0; i < 9; ++i) F0[i] = __ldcs(Fm + i * n_el + p);
     make_stencil(px0, px1, px2, g.origin, g.inv_dx, st_old);
   }
   if (kLookahead) {
@@ -1284,22 +1286,22 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     matmul3(G, F0, F);  // F <- (I + dt C) F  (engine.cpp:250)
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
-      if (g.scatter_mode != 6) Cm[i * n_el + p] = Cn[i];  // 6: A/B timing, no C / v stores
-      Fm[i * n_el + p] = F[i];
+      if (g.scatter_mode != 6) __stcs(Cm + i * n_el + p, Cn[i]);  // 6: A/B timing, no C / v
+      __stcs(Fm + i * n_el + p, F[i]);
     }
     if (kBoundary && tag[p] == kElastomerBottom) vv[0] = vv[1] = vv[2] = 0.0;
     if (g.scatter_mode != 6) {
-      v[p] = vv[0];
-      v[n + p] = vv[1];
-      v[2 * n + p] = vv[2];
+      __stcs(v + p, vv[0]);
+      __stcs(v + n + p, vv[1]);
+      __stcs(v + 2 * n + p, vv[2]);
     }
     if (kAdvect) {
       px0 = advance(px0, g.dt, vv[0]);
       px1 = advance(px1, g.dt, vv[1]);
       px2 = advance(px2, g.dt, vv[2]);
-      x[p] = px0;
-      x[n + p] = px1;
-      x[2 * n + p] = px2;
+      __stcs(x + p, px0);
+      __stcs(x + n + p, px1);
+      __stcs(x + 2 * n + p, px2);
       v2 = vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2];
     }
   }
