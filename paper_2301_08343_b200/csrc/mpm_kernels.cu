@@ -945,7 +945,7 @@ __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
     Stencil st;
     bool beyond = false, contrib = false;
     if (valid) {
-      double px = x[p], py = x[n + p], pz = x[2 * n + p];
+      double px = __ldcs(x + p), py = __ldcs(x + n + p), pz = __ldcs(x + 2 * n + p);
       const int done = moves[p - n_el];
       if (done < target) {
         for (int k = done; k < target; ++k) {
@@ -953,9 +953,9 @@ __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
           py = add_rn(py, d[1]);
           pz = add_rn(pz, d[2]);
         }
-        x[p] = px;
-        x[n + p] = py;
-        x[2 * n + p] = pz;
+        __stcs(x + p, px);
+        __stcs(x + n + p, py);
+        __stcs(x + 2 * n + p, pz);
         moves[p - n_el] = static_cast<uint8_t>(target);
       }
       make_stencil(px, py, pz, g.origin, g.inv_dx, st);
