@@ -121,6 +121,16 @@ __device__ void reduce_motion(unsigned long long* max_v2, unsigned long long* lo
   }
 }
 
+// 16-byte store with an L2 evict_last policy (grid data reused by the next
+// kernel; the particle streams around it are evict-first).
+__device__ __forceinline__ void st_keep(double2* p, double a, double b) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b),
+               "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ size_t node_index(const Geometry& g, int i, int j, int k) {
   return (static_cast<size_t>(i) * g.res[1] + j) * g.res[2] + k;
 }
@@ -1086,14 +1096,14 @@ __device__ __forceinline__ void update_node(NodeBuf mp, double* __restrict__ mi,
   // Step path: nodes without mass keep their (finite) stale velocity; every
   // G2P read of such a node carries B-spline weight exactly 0 (the particle's
   // own scatter would have given it mass otherwise).
-  if (!kZero || massive) {
-    vel.lo[nd] = make_double2(o.x, o.y);
-    vel.hi[nd] = make_double2(o.z, 0.0);
+  if (!kZero || massive) {  // read back by the next G2P staging: keep in L2
+    st_keep(vel.lo + nd, o.x, o.y);
+    st_keep(vel.hi + nd, o.z, 0.0);
   }
   if (kZero) {
-    if (q.x != 0.0 || q.y != 0.0 || q.z != 0.0 || q.w != 0.0) {
-      mp.lo[nd] = make_double2(0, 0);
-      mp.hi[nd] = make_double2(0, 0);
+    if (q.x != 0.0 || q.y != 0.0 || q.z != 0.0 || q.w != 0.0) {  // next scatter target
+      st_keep(mp.lo + nd, 0.0, 0.0);
+      st_keep(mp.hi + nd, 0.0, 0.0);
     }
     if (wi != 0.0) mi[nd] = 0.0;
   }
