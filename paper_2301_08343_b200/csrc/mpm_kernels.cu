@@ -1023,15 +1023,15 @@ __global__ void k_ind_catchup(double* __restrict__ x, int64_t n, int64_t n_el,
   if (done < total) {
     double d[3];
     for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
-    double px = x[p], py = x[n + p], pz = x[2 * n + p];
+    double px = __ldcs(x + p), py = __ldcs(x + n + p), pz = __ldcs(x + 2 * n + p);
     for (int k = done; k < total; ++k) {
       px = add_rn(px, d[0]);
       py = add_rn(py, d[1]);
       pz = add_rn(pz, d[2]);
     }
-    x[p] = px;
-    x[n + p] = py;
-    x[2 * n + p] = pz;
+    __stcs(x + p, px);
+    __stcs(x + n + p, py);
+    __stcs(x + 2 * n + p, pz);
   }
   if (done) moves[p - n_el] = 0;
 }
