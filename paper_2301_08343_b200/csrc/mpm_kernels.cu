@@ -253,6 +253,8 @@ __device__ __forceinline__ void tile_bulk_stage(P2GTile& T, const Geometry& g, N
   const int rows = T.dim[0] * T.dim[1];
   const int d2 = T.dim[2];
   const unsigned bar = smem_addr(&T.bar);
+  unsigned long long pol;  // V is dead once the CTAs around it have staged it
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -267,9 +269,9 @@ __device__ __forceinline__ void tile_bulk_stage(P2GTile& T, const Geometry& g, N
     const double2* sp = (half ? src.hi : src.lo) + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
     double2* dp = (half ? T.nhi : T.nlo) + r * d2;
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_addr(dp)),
-        "l"(sp), "r"(static_cast<unsigned>(d2 * sizeof(double2))), "r"(bar)
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1], %2, [%3], %4;" ::"r"(smem_addr(dp)),
+        "l"(sp), "r"(static_cast<unsigned>(d2 * sizeof(double2))), "r"(bar), "l"(pol)
         : "memory");
   }
   asm volatile(
