@@ -36,6 +36,7 @@ int launch_phase_advect(DeviceSim& s);
 int launch_gather_box(DeviceSim& s, const int lo[3], const int hi[3], double* mass, double* mom,
                       double* vel);
 void configure_gel_tiling(DeviceSim& s, int nx, int ny, int nz);
+unsigned gel_block_count(const DeviceSim& s);
 constexpr int kResetAll = 7;
 // capture_kernels.cu
 int capture(DeviceSim& s, const tg_render& r, double* depth_host, uint8_t* rgb_host,
@@ -87,6 +88,7 @@ DeviceSim::~DeviceSim() {
   cudaFree(C);
   cudaFree(F);
   cudaFree(tag);
+  cudaFree(geo.cta_box);
   cudaFree(grid_mp.lo);
   cudaFree(grid_mp.hi);
   cudaFree(grid_v.lo);
@@ -315,6 +317,13 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
     const int64_t cols = static_cast<int64_t>(surf->nx) * surf->ny;
     if (n_el % cols == 0) configure_gel_tiling(*s, surf->nx, surf->ny, static_cast<int>(n_el / cols));
   }
+  // Per-CTA tile boxes carried from each P2G to the next G2P (mpm_kernels.cu).
+  const size_t ctas = std::max<size_t>(gel_block_count(*s), 1);
+  if (cudaMalloc(&s->geo.cta_box, ctas * 8 * sizeof(int)) != cudaSuccess) {
+    delete s;
+    return fail(TG_ERR_CUDA, "tg_create: device allocation failed");
+  }
+  cudaMemsetAsync(s->geo.cta_box, 0, ctas * 8 * sizeof(int), s->stream);
   const cudaError_t e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) {
     delete s;

@@ -47,6 +47,7 @@ struct Geometry {
   int with_gravity;
   double stress_scale;  // -dt * 4 * inv_dx^2 (engine.cpp:114)
   int scatter_mode;     // 0: shared-memory tile (default), 1: direct RED (A/B switch)
+  int* cta_box;         // per elastomer CTA: {lo[3], dim[3], ok} of its last P2G tile
 };
 
 // A dense node array in split layout: two 16-byte halves per node in two

@@ -395,12 +395,20 @@ __device__ void tile_box(P2GTile& T, bool active, const int* base) {
 __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
                                  const Geometry& g, NodeBuf grid) {
   const int tid = threadIdx.x;
-  if (g.scatter_mode == 1) {  // A/B: per-particle REDs, no tile
-    if (active) scatter_direct(g, grid, m, q);
-    return;
+  if (g.scatter_mode == 1 || g.scatter_mode == 3) {  // A/B switches without a tile
+    if (tid == 0 && g.cta_box) g.cta_box[8 * blockIdx.x + 6] = 0;  // next G2P: no staged box
+    if (g.scatter_mode == 1 && active) scatter_direct(g, grid, m, q);  // per-particle REDs
+    return;                                                            // (3: no scatter)
   }
-  if (g.scatter_mode == 3) return;  // A/B timing: no scatter at all
   tile_box(T, active, q.st.base);
+  if (tid == 0 && g.cta_box) {  // the next G2P of these particles stages this box
+    int* b = g.cta_box + 8 * blockIdx.x;
+    for (int a = 0; a < 3; ++a) {
+      b[a] = T.lo[a];
+      b[3 + a] = T.dim[a];
+    }
+    b[6] = T.ok;
+  }
   const int d1 = T.dim[1], d2 = T.dim[2];
   const int vol = T.dim[0] * d1 * d2;
   const bool use_tile = T.ok != 0;
@@ -1280,7 +1288,19 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
   if (kLookahead) {
     // Stage the grid velocities of the CTA's G2P footprint (coalesced rows
     // along z) in the shared tile before the gathers.
-    tile_box(T, active, st_old.base);
+    // The G2P footprint is the tile box of the P2G that scattered these
+    // particles at these positions (the previous kernel of this CTA): read it
+    // instead of reducing it, so the staging copies start right away.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int* b = g.cta_box + 8 * blockIdx.x;
+      for (int a = 0; a < 3; ++a) {
+        T.lo[a] = b[a];
+        T.dim[a] = b[3 + a];
+      }
+      T.ok = b[6];
+    }
+    __syncthreads();
     staged = T.ok != 0;
     if (staged && g.scatter_mode != 5) tile_bulk_stage(T, g, vel);
   }
@@ -1475,6 +1495,10 @@ GelMap gel_map(const DeviceSim& s) {
   return M;
 }
 
+unsigned gel_blocks(const DeviceSim& s);
+}  // namespace
+unsigned gel_block_count(const DeviceSim& s) { return gel_blocks(s); }
+namespace {
 unsigned gel_blocks(const DeviceSim& s) {
   if (s.lat[0] > 0) return static_cast<unsigned>(s.tiles[0] * s.tiles[1]);
   return static_cast<unsigned>((s.n_el + kGelThreads - 1) / kGelThreads);
