@@ -245,11 +245,10 @@ __device__ __forceinline__ void tile_bulk_reduce(const P2GTile& T, const Geometr
   }
 }
 
-// Stages grid rows [lo, lo + dim) of `src` (both halves) into T with
-// bulk-async copies completing on T.bar; every thread returns after the bytes
-// landed. All threads of the block must call it; T.dim / T.lo / T.ok set by
-// tile_box.
-__device__ __forceinline__ void tile_bulk_stage(P2GTile& T, const Geometry& g, NodeBuf src) {
+// Issues the staging of grid rows [lo, lo + dim) of `src` (both halves) into
+// T as bulk-async copies completing on T.bar (tile_bulk_wait). All threads of
+// the block must call it; T.dim / T.lo / T.ok are set.
+__device__ __forceinline__ void tile_bulk_stage_issue(P2GTile& T, const Geometry& g, NodeBuf src) {
   const int rows = T.dim[0] * T.dim[1];
   const int d2 = T.dim[2];
   const unsigned bar = smem_addr(&T.bar);
@@ -274,6 +273,11 @@ __device__ __forceinline__ void tile_bulk_stage(P2GTile& T, const Geometry& g, N
         "l"(sp), "r"(static_cast<unsigned>(d2 * sizeof(double2))), "r"(bar), "l"(pol)
         : "memory");
   }
+}
+
+// Waits until the staging copies of tile_bulk_stage_issue have landed.
+__device__ __forceinline__ void tile_bulk_wait(P2GTile& T) {
+  const unsigned bar = smem_addr(&T.bar);
   asm volatile(
       "{\n"
       ".reg .pred done;\n"
@@ -1283,7 +1287,6 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     // footprint is reduced and the velocity tile is staged
 #pragma unroll
     for (int i = 0; i < 9; ++i) F0[i] = __ldcs(Fm + i * n_el + p);
-    make_stencil(px0, px1, px2, g.origin, g.inv_dx, st_old);
   }
   if (kLookahead) {
     // Stage the grid velocities of the CTA's G2P footprint (coalesced rows
@@ -1302,8 +1305,11 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     }
     __syncthreads();
     staged = T.ok != 0;
-    if (staged && g.scatter_mode != 5) tile_bulk_stage(T, g, vel);
+    if (staged && g.scatter_mode != 5) tile_bulk_stage_issue(T, g, vel);
   }
+  // the stencil needs x: its loads complete while the staging copies fly
+  if (active) make_stencil(px0, px1, px2, g.origin, g.inv_dx, st_old);
+  if (kLookahead && staged && g.scatter_mode != 5) tile_bulk_wait(T);
   if (active) {
     if (g.scatter_mode == 5) {  // A/B timing: no velocity staging / gather
       vv[0] = vv[1] = vv[2] = 0.0;
