@@ -24,9 +24,9 @@ int launch_p2g(DeviceSim& s, bool publish_diag);
 int launch_p2g_gel(DeviceSim& s);
 int launch_p2g_ind(DeviceSim& s);
 int launch_grid_update(DeviceSim& s, int sms, bool zero);
-int launch_g2p2g_gel(DeviceSim& s, bool lookahead);
+int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter = false);
 int launch_ind_move(DeviceSim& s, bool lookahead);
-int launch_finalize_step(DeviceSim& s);
+int launch_finalize_step(DeviceSim& s, bool cfl_check = false);
 int launch_call_begin(DeviceSim& s);
 int launch_ind_cols(DeviceSim& s, bool move);
 int launch_ind_catchup(DeviceSim& s);
@@ -377,6 +377,12 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
 // One substep of the step path.
 static int record_substep(DeviceSim& s, int sms, bool cols) {
   int k = launch_grid_update(s, sms, true);
+  if (cols && s.n_el > 0) {
+    // the indenter's column walks run as extra blocks of the elastomer kernel
+    k += launch_g2p2g_gel(s, true, true);
+    k += launch_finalize_step(s, true);
+    return k;
+  }
   k += launch_g2p2g_gel(s, true);
   k += cols ? launch_ind_cols(s, true) : launch_ind_move(s, true);
   k += launch_finalize_step(s);

@@ -161,6 +161,16 @@ struct GelMap {
   int tiles[3];
 };
 
+// The rigid indenter's look-ahead column walks, run by extra blocks of the
+// elastomer kernel (blocks >= gel_ctas) instead of a kernel of their own.
+struct IndArgs {
+  const int64_t* col_start;
+  uint8_t* moves;
+  double* mi;
+  int n_cols;
+  int gel_ctas;  // 0: no indenter blocks
+};
+
 namespace {
 
 __device__ __forceinline__ int64_t gel_particle(const GelMap& M, int64_t n_el) {
@@ -546,7 +556,7 @@ __global__ void k_bbox(const double* __restrict__ x, int64_t n, int64_t begin, i
                 active ? x[2 * n + p] : 0.0);
 }
 
-enum : int { kFinAdvect = 1, kFinWindow = 2, kFinDiag = 4, kFinIndShift = 8 };
+enum : int { kFinAdvect = 1, kFinWindow = 2, kFinDiag = 4, kFinIndShift = 8, kFinCfl = 16 };
 
 // grid.cpp:29-36: in_range divides by dx.
 __device__ bool in_range(const Geometry& g, const double* x) {
@@ -590,7 +600,15 @@ __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode)
   }
   const double lo = fmin(bl, il), hi = fmax(bh, ih);
   int err = 0;  // warp-uniform
-  if (mode & kFinAdvect) {
+  if (mode & kFinCfl) {
+    // The indenter's look-ahead walks (run beside the elastomer kernel) used
+    // the previous elastomer box widened by one node: valid while no
+    // elastomer particle moves a full cell in one substep (|v| dt < dx, far
+    // inside the explicit scheme's stability bound). Otherwise: OutOfGrid.
+    const double vg2 = __longlong_as_double(static_cast<long long>(ctl->max_v2));
+    if (!(vg2 * g.dt * g.dt < g.dx * g.dx)) err = 1;
+  }
+  if (!err && (mode & kFinAdvect)) {
     // engine.cpp:279-285 (grid.cpp:29-36 per axis: xn = (x - o) / dx)
     bool ok = true;
     if (ax) {
@@ -927,36 +945,42 @@ struct ColSmem {
   int run_start[kColWarps][33];
 };
 
+// One block's column walks (blk = block index among the indenter blocks).
+// box_mode: 0 = Ctl::box[0] (the elastomer box of the substep being
+// scattered: standalone scatter), 1 = from Ctl::bb (the elastomer bbox after
+// this substep's advect), 2 = Ctl::box[0] of this substep widened by one node
+// on every side (look-ahead scatter running alongside the elastomer kernel:
+// the elastomer moves less than one cell per substep, which k_finalize checks).
 template <bool kMove>
-__global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
-    double* __restrict__ x, int64_t n, int64_t n_el, const int64_t* __restrict__ col_start,
-    int n_cols, uint8_t* __restrict__ moves, Ctl* ctl, Geometry g, double* __restrict__ mi,
-    int box_from_bb) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  ColSmem& S = *reinterpret_cast<ColSmem*>(smem_raw);
-  pdl_wait();
+__device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __restrict__ x,
+                                               int64_t n, int64_t n_el,
+                                               const int64_t* __restrict__ col_start, int n_cols,
+                                               uint8_t* __restrict__ moves, Ctl* ctl,
+                                               const Geometry& g, double* __restrict__ mi,
+                                               int box_mode, int s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = ctl->substep;
-  if (stale(ctl, s)) return;
-  if (kMove && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (kMove && blk == 0 && threadIdx.x == 0) {
     ctl->ind_v[0] = ctl->vind[0];  // apply_boundary (engine.cpp:260-261)
     ctl->ind_v[1] = ctl->vind[1];
     ctl->ind_v[2] = ctl->vind[2];
   }
-  const int c = blockIdx.x * kColWarps + warp;
+  const int c = blk * kColWarps + warp;
   if (c >= n_cols) return;  // warp-uniform; only __syncwarp below
   // Elastomer node box of the substep being scattered.
   int glo[3], ghi[3];
   for (int a = 0; a < 3; ++a) {
-    if (box_from_bb) {
+    if (box_mode == 1) {
       const double l = order_val(ctl->bb_lo[a]), h = order_val(ctl->bb_hi[a]);
       if (!(l <= h)) return;  // no elastomer: nothing reads the grid
       glo[a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(l, g.origin[a]), g.inv_dx), 0.5)));
       ghi[a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(h, g.origin[a]), g.inv_dx), 0.5))) + 3;
     } else {
+      const int widen = box_mode == 2 ? 1 : 0;
       glo[a] = ctl->box_lo[0][a];
       ghi[a] = ctl->box_hi[0][a];
       if (ghi[a] <= glo[a]) return;
+      glo[a] -= widen;
+      ghi[a] += widen;
     }
   }
   const int target = s - ctl->call_start + (kMove ? 1 : 0);  // advects this call after this kernel
@@ -1022,6 +1046,20 @@ __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
     __syncwarp();
     if (bey) break;  // the rest of the column is above the elastomer box
   }
+}
+
+template <bool kMove>
+__global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
+    double* __restrict__ x, int64_t n, int64_t n_el, const int64_t* __restrict__ col_start,
+    int n_cols, uint8_t* __restrict__ moves, Ctl* ctl, Geometry g, double* __restrict__ mi,
+    int box_mode) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ColSmem& S = *reinterpret_cast<ColSmem*>(smem_raw);
+  pdl_wait();
+  const int s = ctl->substep;
+  if (stale(ctl, s)) return;
+  ind_cols_block<kMove>(S, blockIdx.x, x, n, n_el, col_start, n_cols, moves, ctl, g, mi, box_mode,
+                        s);
 }
 
 // Applies the pending advects of the indenter particles the column walks did
@@ -1264,10 +1302,19 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     double* __restrict__ x, double* __restrict__ v, double* __restrict__ Cm,
     double* __restrict__ Fm, const uint8_t* __restrict__ tag, int64_t n, int64_t n_el, GelMap M,
     Ctl* ctl, Geometry g, NodeBuf vel, NodeBuf grid, double m,
-    double vol0) {
+    double vol0, IndArgs ia) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   P2GTile& T = *reinterpret_cast<P2GTile*>(smem_raw);
   pdl_wait();
+  if (kLookahead && ia.gel_ctas > 0 && static_cast<int>(blockIdx.x) >= ia.gel_ctas) {
+    // indenter blocks: the s+1 column walks (they touch only indenter x and
+    // M_I; the elastomer box comes from the previous finalize, widened)
+    const int s = ctl->substep;
+    if (stale(ctl, s)) return;
+    ind_cols_block<true>(*reinterpret_cast<ColSmem*>(smem_raw), blockIdx.x - ia.gel_ctas, x, n,
+                         n_el, ia.col_start, ia.n_cols, ia.moves, ctl, g, ia.mi, 2, s);
+    return;
+  }
   const int s = ctl->substep;
   if (stale_block(ctl, s)) return;
   const int64_t p = gel_particle(M, n_el);
@@ -1483,6 +1530,8 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 
 constexpr int kThreads = 256;
 constexpr size_t kTileSmem = sizeof(P2GTile);
+static_assert(sizeof(ColSmem) <= sizeof(P2GTile), "indenter blocks reuse the tile's shared memory");
+static_assert(kGelThreads == kColWarps * 32, "indenter blocks of the elastomer kernel: 8 warps");
 constexpr size_t kIndSmem = sizeof(IndSmem);
 
 inline unsigned blocks_for(int64_t n) {
@@ -1628,17 +1677,24 @@ int launch_grid_update(DeviceSim& s, int sms, bool zero) {
 }
 
 // G2P + boundary + advect for the elastomer, with the look-ahead scatter.
-int launch_g2p2g_gel(DeviceSim& s, bool lookahead) {
+int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter) {
   if (s.n_el <= 0) return 0;
   configure_once();
+  IndArgs ia{};
+  unsigned extra = 0;
+  if (with_indenter) {  // the indenter's look-ahead column walks ride along
+    ia = IndArgs{s.col_start, s.ind_moves, s.grid_mi, s.n_cols, static_cast<int>(gel_blocks(s))};
+    extra = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
+    s.ind_v_uniform = true;
+  }
   if (lookahead)
-    launch_pdl(k_g2p2g_gel<true, true, true>, dim3(gel_blocks(s)), dim3(kGelThreads), kTileSmem,
+    launch_pdl(k_g2p2g_gel<true, true, true>, dim3(gel_blocks(s) + extra), dim3(kGelThreads), kTileSmem,
                s.stream, s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo,
-               s.grid_v, s.grid_mp, s.m_el, s.vol_el);
+               s.grid_v, s.grid_mp, s.m_el, s.vol_el, ia);
   else
     k_g2p2g_gel<true, true, false><<<gel_blocks(s), kGelThreads, 0, s.stream>>>(
         s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
-        s.m_el, s.vol_el);
+        s.m_el, s.vol_el, IndArgs{});
   s.kernel_launches += 1;
   return 1;
 }
@@ -1698,9 +1754,10 @@ int launch_ind_catchup(DeviceSim& s) {
   return 1;
 }
 
-int launch_finalize_step(DeviceSim& s) {
+int launch_finalize_step(DeviceSim& s, bool cfl_check) {
   launch_pdl(k_finalize, dim3(1), dim3(32), 0, s.stream, s.ctl, s.geo,
-             static_cast<int>(kFinDiag | kFinAdvect | kFinWindow | (s.n_ind > 0 ? kFinIndShift : 0)));
+             static_cast<int>(kFinDiag | kFinAdvect | kFinWindow | (s.n_ind > 0 ? kFinIndShift : 0) |
+                              (cfl_check ? kFinCfl : 0)));
   s.kernel_launches += 1;
   return 1;
 }
@@ -1709,7 +1766,7 @@ int launch_phase_g2p(DeviceSim& s) {
   if (s.n_el <= 0) return 0;
   k_g2p2g_gel<false, false, false><<<gel_blocks(s), kGelThreads, 0, s.stream>>>(
       s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,
-      s.m_el, s.vol_el);
+      s.m_el, s.vol_el, IndArgs{});
   s.kernel_launches += 1;
   return 1;
 }
