@@ -21,9 +21,12 @@ struct Ctl {
   int err_substep;   // absolute substep index the error belongs to
   int substep;       // absolute index of the substep being executed
   int pad0;
-  unsigned long long bb_lo[3], bb_hi[3];  // order_key() of elastomer x after advect
-  unsigned long long ind_lo[3], ind_hi[3];  // order_key() of the indenter bbox
-  unsigned long long max_v2;              // bits of max |v|^2 (non-negative)
+  // Motion reductions in two slots by substep parity: slot s & 1 holds the
+  // state after the advect of substep s (so a reader of slot s & 1 and the
+  // reset of slot (s + 1) & 1 for the next advect never touch the same slot).
+  unsigned long long bb_lo[2][3], bb_hi[2][3];   // order_key() of elastomer x
+  unsigned long long ind_lo[2][3], ind_hi[2][3];  // order_key() of the indenter bbox
+  unsigned long long max_v2[2];                  // bits of max |v|^2 (non-negative)
   unsigned long long min_detf[2];         // order_key() of min det F, per substep parity
   int win_lo[3], win_hi[3];               // Grid::active_lo/hi
   int prev_lo[3], prev_hi[3];             // Grid::prev_lo/hi

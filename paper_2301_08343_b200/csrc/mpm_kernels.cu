@@ -531,27 +531,33 @@ __device__ __forceinline__ void reduce_min_detf(Ctl* ctl, int s, bool active, do
 enum : int { kResetMotion = 1, kResetIndBox = 2, kResetDetF = 4 };
 
 __global__ void k_reset(Ctl* ctl, int mask) {
-  for (int a = 0; a < 3; ++a) {
-    if (mask & kResetMotion) {
-      ctl->bb_lo[a] = order_key(INFINITY);
-      ctl->bb_hi[a] = order_key(-INFINITY);
+  for (int slot = 0; slot < 2; ++slot) {
+    for (int a = 0; a < 3; ++a) {
+      if (mask & kResetMotion) {
+        ctl->bb_lo[slot][a] = order_key(INFINITY);
+        ctl->bb_hi[slot][a] = order_key(-INFINITY);
+      }
+      if (mask & kResetIndBox) {
+        ctl->ind_lo[slot][a] = order_key(INFINITY);
+        ctl->ind_hi[slot][a] = order_key(-INFINITY);
+      }
     }
-    if (mask & kResetIndBox) {
-      ctl->ind_lo[a] = order_key(INFINITY);
-      ctl->ind_hi[a] = order_key(-INFINITY);
-    }
+    if (mask & kResetMotion) ctl->max_v2[slot] = 0ull;
   }
-  if (mask & kResetMotion) ctl->max_v2 = 0ull;
   if (mask & kResetDetF) ctl->min_detf[0] = ctl->min_detf[1] = order_key(1.0);
 }
 
 // particle_bbox (engine.cpp:31-45) over [begin, end): elastomer part into
-// bb_*, indenter part into ind_* (then advanced analytically by finalize).
+// bb_*, indenter part into ind_* (then advanced analytically by finalize),
+// slot (substep + next) & 1: next = 1 for the positions before this substep's
+// P2G (they are "after the advect of substep - 1"), 0 after an advect.
 __global__ void k_bbox(const double* __restrict__ x, int64_t n, int64_t begin, int64_t end,
-                       Ctl* ctl, int indenter) {
+                       Ctl* ctl, int indenter, int next) {
   const int64_t p = begin + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool active = p < end;
-  reduce_motion(nullptr, indenter ? ctl->ind_lo : ctl->bb_lo, indenter ? ctl->ind_hi : ctl->bb_hi,
+  const int sl = (ctl->substep + next) & 1;
+  reduce_motion(nullptr, indenter ? ctl->ind_lo[sl] : ctl->bb_lo[sl],
+                indenter ? ctl->ind_hi[sl] : ctl->bb_hi[sl],
                 active, 0.0, active ? x[p] : 0.0, active ? x[n + p] : 0.0,
                 active ? x[2 * n + p] : 0.0);
 }
@@ -584,10 +590,15 @@ __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode)
   const int a = ax ? lane : 0;
   const int s = ctl->substep;
   if (stale(ctl, s)) return;
+  // after an advect the reductions of substep s are in slot s & 1; a window
+  // of the current positions (before P2G(s)) reads slot (s + 1) & 1
+  const int cur = (mode & kFinAdvect) ? (s & 1) : ((s + 1) & 1);
+  // the indenter box is advanced from the previous slot when shifting
+  const int isl = (mode & kFinIndShift) ? (cur ^ 1) : cur;
   // per-axis inputs
-  const bool ind_any = order_val(ctl->ind_lo[0]) <= order_val(ctl->ind_hi[0]);
-  double bl = order_val(ctl->bb_lo[a]), bh = order_val(ctl->bb_hi[a]);
-  double il = order_val(ctl->ind_lo[a]), ih = order_val(ctl->ind_hi[a]);
+  const bool ind_any = order_val(ctl->ind_lo[isl][0]) <= order_val(ctl->ind_hi[isl][0]);
+  double bl = order_val(ctl->bb_lo[cur][a]), bh = order_val(ctl->bb_hi[cur][a]);
+  double il = order_val(ctl->ind_lo[isl][a]), ih = order_val(ctl->ind_hi[isl][a]);
   const double va = ctl->vind[a];
   const int pl = ctl->prev_lo[a], ph = ctl->prev_hi[a];
   const bool shift = (mode & kFinIndShift) && ind_any;
@@ -605,7 +616,7 @@ __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode)
     // the previous elastomer box widened by one node: valid while no
     // elastomer particle moves a full cell in one substep (|v| dt < dx, far
     // inside the explicit scheme's stability bound). Otherwise: OutOfGrid.
-    const double vg2 = __longlong_as_double(static_cast<long long>(ctl->max_v2));
+    const double vg2 = __longlong_as_double(static_cast<long long>(ctl->max_v2[cur]));
     if (!(vg2 * g.dt * g.dt < g.dx * g.dx)) err = 1;
   }
   if (!err && (mode & kFinAdvect)) {
@@ -637,7 +648,7 @@ __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode)
       ctl->min_detf[s & 1] = order_key(1.0);
     }
     if (mode & kFinAdvect) {
-      double v2 = __longlong_as_double(static_cast<long long>(ctl->max_v2));
+      double v2 = __longlong_as_double(static_cast<long long>(ctl->max_v2[cur]));
       if (shift) {
         const double u0 = ctl->vind[0], u1 = ctl->vind[1], u2 = ctl->vind[2];
         v2 = fmax(v2, u0 * u0 + u1 * u1 + u2 * u2);
@@ -652,8 +663,8 @@ __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode)
     }
   }
   if (ax && shift) {
-    ctl->ind_lo[a] = order_key(il);
-    ctl->ind_hi[a] = order_key(ih);
+    ctl->ind_lo[cur][a] = order_key(il);
+    ctl->ind_hi[cur][a] = order_key(ih);
   }
   if (err) return;
   if (ax && (mode & kFinWindow)) {
@@ -671,11 +682,11 @@ __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode)
     ctl->win_lo[a] = ctl->prev_lo[a] = wlo;
     ctl->win_hi[a] = ctl->prev_hi[a] = whi;
   }
-  if (ax) {
-    ctl->bb_lo[a] = order_key(INFINITY);
-    ctl->bb_hi[a] = order_key(-INFINITY);
+  if ((mode & kFinAdvect) && ax) {  // the next advect reduces into the other slot
+    ctl->bb_lo[cur ^ 1][a] = order_key(INFINITY);
+    ctl->bb_hi[cur ^ 1][a] = order_key(-INFINITY);
   }
-  if (lane == 0) ctl->max_v2 = 0ull;
+  if ((mode & kFinAdvect) && lane == 0) ctl->max_v2[cur ^ 1] = 0ull;
 }
 
 // zero_grid's clear of Grid::mass / momentum over Ctl::clr (engine.cpp:72-83).
@@ -970,7 +981,7 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
   int glo[3], ghi[3];
   for (int a = 0; a < 3; ++a) {
     if (box_mode == 1) {
-      const double l = order_val(ctl->bb_lo[a]), h = order_val(ctl->bb_hi[a]);
+      const double l = order_val(ctl->bb_lo[s & 1][a]), h = order_val(ctl->bb_hi[s & 1][a]);
       if (!(l <= h)) return;  // no elastomer: nothing reads the grid
       glo[a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(l, g.origin[a]), g.inv_dx), 0.5)));
       ghi[a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(h, g.origin[a]), g.inv_dx), 0.5))) + 3;
@@ -1390,7 +1401,9 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
       v2 = vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2];
     }
   }
-  if (kAdvect) reduce_motion(&ctl->max_v2, ctl->bb_lo, ctl->bb_hi, active, v2, px0, px1, px2);
+  if (kAdvect)
+    reduce_motion(&ctl->max_v2[s & 1], ctl->bb_lo[s & 1], ctl->bb_hi[s & 1], active, v2, px0, px1,
+                  px2);
   if (kLookahead) {
     // particle_to_grid of substep s + 1 with the state just written.
     P2GPayload q;
@@ -1437,7 +1450,8 @@ __global__ void k_gel_advect(double* __restrict__ x, const double* __restrict__ 
     x[2 * n + p] = px2;
     v2 = v0 * v0 + v1 * v1 + vz * vz;
   }
-  reduce_motion(&ctl->max_v2, ctl->bb_lo, ctl->bb_hi, active, v2, px0, px1, px2);
+  const int sl = ctl->substep & 1;
+  reduce_motion(&ctl->max_v2[sl], ctl->bb_lo[sl], ctl->bb_hi[sl], active, v2, px0, px1, px2);
 }
 
 // Indenter advect in phase mode with its current (possibly non-uniform)
@@ -1460,7 +1474,8 @@ __global__ void k_ind_advect(double* __restrict__ x, const double* __restrict__ 
   }
   const double m = warp_max(active ? v2 : 0.0);
   if ((threadIdx.x & 31) == 0 && m > 0.0)
-    atomicMax(&ctl->max_v2, static_cast<unsigned long long>(__double_as_longlong(m)));
+    atomicMax(&ctl->max_v2[ctl->substep & 1],
+              static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
 __global__ void k_ind_boundary(Ctl* ctl) {
@@ -1608,11 +1623,11 @@ int launch_window(DeviceSim& s) {
   configure_once();
   int k = launch_reset(s, kResetMotion | kResetIndBox | kResetDetF);
   if (s.n_el > 0) {
-    k_bbox<<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(s.x, s.n, 0, s.n_el, s.ctl, 0);
+    k_bbox<<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(s.x, s.n, 0, s.n_el, s.ctl, 0, 1);
     ++k;
   }
   if (s.n_ind > 0) {
-    k_bbox<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.n, s.ctl, 1);
+    k_bbox<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.n, s.ctl, 1, 1);
     ++k;
   }
   k_finalize<<<1, 32, 0, s.stream>>>(s.ctl, s.geo, kFinWindow);
@@ -1803,7 +1818,7 @@ int launch_phase_advect(DeviceSim& s) {
       k_ind_advect<false><<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.v, s.n, s.n_el,
                                                                          s.ctl, s.geo);
     k_reset<<<1, 1, 0, s.stream>>>(s.ctl, kResetIndBox);
-    k_bbox<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.n, s.ctl, 1);
+    k_bbox<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.n, s.ctl, 1, 0);
     k += 3;
   }
   k_finalize<<<1, 32, 0, s.stream>>>(s.ctl, s.geo, kFinAdvect);
