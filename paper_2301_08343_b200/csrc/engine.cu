@@ -91,8 +91,8 @@ DeviceSim::~DeviceSim() {
   cudaFree(geo.cta_box);
   cudaFree(grid_mp.lo);
   cudaFree(grid_mp.hi);
-  cudaFree(grid_v.lo);
-  cudaFree(grid_v.hi);
+  cudaFree(grid_v.xy);
+  cudaFree(grid_v.z);
   cudaFree(grid_mi);
   cudaFree(col_start);
   cudaFree(ind_moves);
@@ -241,8 +241,9 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
             cudaMalloc(&s->tag, std::max<int64_t>(n_el, 1)) == cudaSuccess &&
             cudaMalloc(&s->grid_mp.lo, s->n_nodes * sizeof(double2)) == cudaSuccess &&
             cudaMalloc(&s->grid_mp.hi, s->n_nodes * sizeof(double2)) == cudaSuccess &&
-            cudaMalloc(&s->grid_v.lo, s->n_nodes * sizeof(double2)) == cudaSuccess &&
-            cudaMalloc(&s->grid_v.hi, s->n_nodes * sizeof(double2)) == cudaSuccess &&
+            cudaMalloc(&s->grid_v.xy, s->n_nodes * sizeof(double2)) == cudaSuccess &&
+            // +2: the staging reads vz rows from an even node over an even count
+            cudaMalloc(&s->grid_v.z, (s->n_nodes + 2) * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->grid_mi, s->n_nodes * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->col_start, std::max<size_t>(col_starts.size(), 1) * sizeof(int64_t)) ==
                 cudaSuccess &&
@@ -256,8 +257,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   }
   cudaMemsetAsync(s->grid_mp.lo, 0, s->n_nodes * sizeof(double2), s->stream);
   cudaMemsetAsync(s->grid_mp.hi, 0, s->n_nodes * sizeof(double2), s->stream);
-  cudaMemsetAsync(s->grid_v.lo, 0, s->n_nodes * sizeof(double2), s->stream);
-  cudaMemsetAsync(s->grid_v.hi, 0, s->n_nodes * sizeof(double2), s->stream);
+  cudaMemsetAsync(s->grid_v.xy, 0, s->n_nodes * sizeof(double2), s->stream);
+  cudaMemsetAsync(s->grid_v.z, 0, (s->n_nodes + 2) * sizeof(double), s->stream);
   cudaMemsetAsync(s->grid_mi, 0, s->n_nodes * sizeof(double), s->stream);
   cudaMemsetAsync(s->ind_moves, 0, std::max<int64_t>(n_ind, 1), s->stream);
   s->n_cols = col_starts.empty() ? 0 : static_cast<int>(col_starts.size()) - 1;

@@ -55,10 +55,16 @@ struct Geometry {
 
 // A dense node array in split layout: two 16-byte halves per node in two
 // arrays (node (i,j,k) at (i*res1 + j)*res2 + k). Grid::mass/momentum:
-// lo = {m, px}, hi = {py, pz}; Grid::velocity: lo = {vx, vy}, hi = {vz, 0}.
+// lo = {m, px}, hi = {py, pz}.
 struct NodeBuf {
   double2* lo;
   double2* hi;
+};
+
+// Grid::velocity: xy = {vx, vy} (16 B) and z = vz (8 B) per node.
+struct VelBuf {
+  double2* xy;
+  double* z;
 };
 
 struct DeviceSim {
@@ -78,7 +84,7 @@ struct DeviceSim {
 
   // Dense node arrays (NodeBuf split layout).
   NodeBuf grid_mp{nullptr, nullptr};  // Grid::mass / momentum (elastomer + direct indenter)
-  NodeBuf grid_v{nullptr, nullptr};   // Grid::velocity
+  VelBuf grid_v{nullptr, nullptr};    // Grid::velocity
   double* grid_mi = nullptr;  // indenter mass (uniform-velocity indenter scatter)
   int sms = 148;              // multiprocessor count of `device`
   // Indenter columns: maximal runs of equal initial (bx, by) in the sorted

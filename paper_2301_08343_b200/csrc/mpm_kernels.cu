@@ -131,6 +131,12 @@ __device__ __forceinline__ void st_keep(double2* p, double a, double b) {
                : "memory");
 }
 
+__device__ __forceinline__ void st_keep1(double* p, double a) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(a), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ size_t node_index(const Geometry& g, int i, int j, int k) {
   return (static_cast<size_t>(i) * g.res[1] + j) * g.res[2] + k;
 }
@@ -212,10 +218,11 @@ constexpr int kGelMinBlocks = (2 * 256) / TACCHI_GEL_THREADS;
 // nodes up to 8 apart.
 struct P2GTile {
   double2 nlo[kTileCap];  // {m, px} / {vx, vy}
-  double2 nhi[kTileCap];  // {py, pz} / {vz, -}
+  double2 nhi[kTileCap];  // {py, pz} / vz rows (as doubles, pitch zp, offset zoff)
   int owner[kTileCap];
   int lo[3], hi[3], dim[3];
   int ok;
+  int zp, zoff;  // staged vz: node (row r, column c) at ((double*)nhi)[r * zp + zoff + c]
   unsigned long long bar;  // mbarrier of the staging copies
 };
 
@@ -258,34 +265,43 @@ __device__ __forceinline__ void tile_bulk_reduce(const P2GTile& T, const Geometr
 // Issues the staging of grid rows [lo, lo + dim) of `src` (both halves) into
 // T as bulk-async copies completing on T.bar (tile_bulk_wait). All threads of
 // the block must call it; T.dim / T.lo / T.ok are set.
-__device__ __forceinline__ void tile_bulk_stage_issue(P2GTile& T, const Geometry& g, NodeBuf src) {
+__device__ __forceinline__ void tile_bulk_stage_issue(P2GTile& T, const Geometry& g, VelBuf src) {
   const int rows = T.dim[0] * T.dim[1];
   const int d2 = T.dim[2];
   const unsigned bar = smem_addr(&T.bar);
   unsigned long long pol;  // V is dead once the CTAs around it have staged it
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  // vz rows are 8-byte elements: each row is copied from the even node at or
+  // below its start (16-byte aligned; res2 is even, so every row of the box
+  // has the same parity zoff) over an even count, into rows of pitch zp.
+  const int zoff = T.lo[2] & 1;
+  const int zcnt = (zoff + d2 + 1) & ~1;
   if (threadIdx.x == 0) {
+    T.zp = zcnt;
+    T.zoff = zoff;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                 "r"(static_cast<unsigned>(2 * rows * d2 * sizeof(double2)))
+                 "r"(static_cast<unsigned>(rows * (d2 * sizeof(double2) + zcnt * sizeof(double))))
                  : "memory");
   }
   __syncthreads();
+  double* zs = reinterpret_cast<double*>(T.nhi);
   for (int t = threadIdx.x; t < 2 * rows; t += blockDim.x) {
     const int r = t >> 1, half = t & 1;
     const int i = r / T.dim[1], j = r - i * T.dim[1];
-    const double2* sp = (half ? src.hi : src.lo) + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
-    double2* dp = (half ? T.nhi : T.nlo) + r * d2;
+    const size_t nd = node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
+    const void* sp = half ? static_cast<const void*>(src.z + (nd - zoff))
+                          : static_cast<const void*>(src.xy + nd);
+    void* dp = half ? static_cast<void*>(zs + r * zcnt) : static_cast<void*>(T.nlo + r * d2);
+    const unsigned bytes = half ? zcnt * sizeof(double) : d2 * sizeof(double2);
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
         "[%1], %2, [%3], %4;" ::"r"(smem_addr(dp)),
-        "l"(sp), "r"(static_cast<unsigned>(d2 * sizeof(double2))), "r"(bar), "l"(pol)
+        "l"(sp), "r"(bytes), "r"(bar), "l"(pol)
         : "memory");
   }
 }
-
-// Waits until the staging copies of tile_bulk_stage_issue have landed.
 __device__ __forceinline__ void tile_bulk_wait(P2GTile& T) {
   const unsigned bar = smem_addr(&T.bar);
   asm volatile(
@@ -1146,7 +1162,7 @@ __device__ __forceinline__ double4 node_velocity(const Geometry& g, double4 q, d
 // with_mi: the node may hold indenter weight (inside the indenter box).
 template <bool kZero>
 __device__ __forceinline__ void update_node(NodeBuf mp, double* __restrict__ mi,
-                                            NodeBuf vel, const Geometry& g,
+                                            VelBuf vel, const Geometry& g,
                                             double m_ind, double u0, double u1, double u2, int i,
                                             int j, int k, bool with_mi) {
   const size_t nd = node_index(g, i, j, k);
@@ -1160,8 +1176,8 @@ __device__ __forceinline__ void update_node(NodeBuf mp, double* __restrict__ mi,
   // G2P read of such a node carries B-spline weight exactly 0 (the particle's
   // own scatter would have given it mass otherwise).
   if (!kZero || massive) {  // read back by the next G2P staging: keep in L2
-    st_keep(vel.lo + nd, o.x, o.y);
-    st_keep(vel.hi + nd, o.z, 0.0);
+    st_keep(vel.xy + nd, o.x, o.y);
+    st_keep1(vel.z + nd, o.z);
   }
   if (kZero) {
     if (q.x != 0.0 || q.y != 0.0 || q.z != 0.0 || q.w != 0.0) {  // next scatter target
@@ -1174,7 +1190,7 @@ __device__ __forceinline__ void update_node(NodeBuf mp, double* __restrict__ mi,
 
 // Phase API: the full active window, as the reference (Grid::velocity is 0
 // on every massless window node).
-__global__ void k_grid_update_window(NodeBuf mp, double* __restrict__ mi, NodeBuf vel,
+__global__ void k_grid_update_window(NodeBuf mp, double* __restrict__ mi, VelBuf vel,
                                      Ctl* ctl, Geometry g,
                                      double m_ind) {
   if (stale(ctl, ctl->substep)) return;
@@ -1190,7 +1206,7 @@ __global__ void k_grid_update_window(NodeBuf mp, double* __restrict__ mi, NodeBu
 // Step path: only the union of the elastomer and indenter node boxes (every
 // node a scatter can have touched), re-zeroing the accumulators. M_I is read
 // only inside the indenter box.
-__global__ void k_grid_update_boxes(NodeBuf mp, double* __restrict__ mi, NodeBuf vel,
+__global__ void k_grid_update_boxes(NodeBuf mp, double* __restrict__ mi, VelBuf vel,
                                     Ctl* ctl, Geometry g,
                                     double m_ind) {
   pdl_wait();
@@ -1229,7 +1245,7 @@ __global__ void k_grid_update_boxes(NodeBuf mp, double* __restrict__ mi, NodeBuf
 
 namespace {
 // engine.cpp:217-249 for one particle: v and C from the node velocities.
-__device__ __forceinline__ void g2p_gather(const Geometry& g, NodeBuf vel,
+__device__ __forceinline__ void g2p_gather(const Geometry& g, VelBuf vel,
                                            double px0, double px1, double px2, double* vv,
                                            double* Cn) {
   Stencil st;
@@ -1249,7 +1265,8 @@ __device__ __forceinline__ void g2p_gather(const Geometry& g, NodeBuf vel,
       for (int c = 0; c < 3; ++c) {
         const double w = wab * st.w[2][c];
         const double dc = c - st.fx[2];
-        const double2 qa = __ldg(vel.lo + row + c), qb = __ldg(vel.hi + row + c);
+        const double2 qa = __ldg(vel.xy + row + c);
+        const double2 qb = make_double2(__ldg(vel.z + row + c), 0.0);
         const double wv0 = w * qa.x, wv1 = w * qa.y, wv2 = w * qb.x;
         v0 += wv0; v1 += wv1; vz += wv2;
         b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
@@ -1272,8 +1289,10 @@ __device__ __forceinline__ void g2p_gather(const Geometry& g, NodeBuf vel,
 // T.nlo[.].x/y, T.nhi[.].x), same arithmetic as g2p_gather.
 __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile& T,
                                                 const Stencil& st, double* vv, double* Cn) {
-  const int d1 = T.dim[1], d2 = T.dim[2];
-  const int e0 = ((st.base[0] - T.lo[0]) * d1 + (st.base[1] - T.lo[1])) * d2 + (st.base[2] - T.lo[2]);
+  const int d1 = T.dim[1], d2 = T.dim[2], zp = T.zp;
+  const int r0 = (st.base[0] - T.lo[0]) * d1 + (st.base[1] - T.lo[1]);
+  const int c0 = st.base[2] - T.lo[2];
+  const double* zs = reinterpret_cast<const double*>(T.nhi);
   double v0 = 0, v1 = 0, vz = 0;
   double b00 = 0, b01 = 0, b02 = 0, b10 = 0, b11 = 0, b12 = 0, b20 = 0, b21 = 0, b22 = 0;
 #pragma unroll
@@ -1284,13 +1303,14 @@ __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile
     for (int b = 0; b < 3; ++b) {
       const double wab = wa * st.w[1][b];
       const double db = b - st.fx[1];
-      const int row = e0 + (a * d1 + b) * d2;
+      const int r = r0 + a * d1 + b;
+      const int row = r * d2 + c0, zrow = r * zp + T.zoff + c0;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double w = wab * st.w[2][c];
         const double dc = c - st.fx[2];
         const double2 vxy = T.nlo[row + c];
-        const double vzz = T.nhi[row + c].x;
+        const double vzz = zs[zrow + c];
         const double wv0 = w * vxy.x, wv1 = w * vxy.y, wv2 = w * vzz;
         v0 += wv0; v1 += wv1; vz += wv2;
         b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
@@ -1312,7 +1332,7 @@ template <bool kBoundary, bool kAdvect, bool kLookahead>
 __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     double* __restrict__ x, double* __restrict__ v, double* __restrict__ Cm,
     double* __restrict__ Fm, const uint8_t* __restrict__ tag, int64_t n, int64_t n_el, GelMap M,
-    Ctl* ctl, Geometry g, NodeBuf vel, NodeBuf grid, double m,
+    Ctl* ctl, Geometry g, VelBuf vel, NodeBuf grid, double m,
     double vol0, IndArgs ia) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   P2GTile& T = *reinterpret_cast<P2GTile*>(smem_raw);
@@ -1359,7 +1379,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
         T.lo[a] = b[a];
         T.dim[a] = b[3 + a];
       }
-      T.ok = b[6];
+      T.ok = b[6] && (g.res[2] & 1) == 0;  // vz row staging needs an even res2
     }
     __syncthreads();
     staged = T.ok != 0;
@@ -1493,7 +1513,7 @@ __global__ void k_p2g_done(Ctl* ctl) {
 
 // Copies a node box [lo, hi) into dense staging buffers (tg_download_grid):
 // Grid::mass / momentum as the reference holds them (elastomer + indenter).
-__global__ void k_gather_box(NodeBuf mp, const double* __restrict__ mi, NodeBuf vel,
+__global__ void k_gather_box(NodeBuf mp, const double* __restrict__ mi, VelBuf vel,
                              const Ctl* ctl, Geometry g,
                              double m_ind, int3 lo, int3 hi, double* __restrict__ mass,
                              double* __restrict__ mom, double* __restrict__ velo) {
@@ -1509,8 +1529,8 @@ __global__ void k_gather_box(NodeBuf mp, const double* __restrict__ mi, NodeBuf 
     const double2 qa = mp.lo[nd], qb = mp.hi[nd];
     const double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
     const double M = mi[nd] * m_ind;
-    const double2 ua = vel.lo[nd], ub = vel.hi[nd];
-    const double4 u = make_double4(ua.x, ua.y, ub.x, 0.0);
+    const double2 ua = vel.xy[nd];
+    const double4 u = make_double4(ua.x, ua.y, vel.z[nd], 0.0);
     mass[t] = q.x + M;
     mom[3 * t] = q.y + M * ctl->ind_v[0];
     mom[3 * t + 1] = q.z + M * ctl->ind_v[1];
