@@ -1206,7 +1206,7 @@ __global__ void k_grid_update_window(NodeBuf mp, double* __restrict__ mi, VelBuf
 // Step path: only the union of the elastomer and indenter node boxes (every
 // node a scatter can have touched), re-zeroing the accumulators. M_I is read
 // only inside the indenter box.
-__global__ void k_grid_update_boxes(NodeBuf mp, double* __restrict__ mi, VelBuf vel,
+__global__ void __launch_bounds__(256, 5) k_grid_update_boxes(NodeBuf mp, double* __restrict__ mi, VelBuf vel,
                                     Ctl* ctl, Geometry g,
                                     double m_ind) {
   pdl_wait();
