@@ -1,31 +1,33 @@
 // MLS-MPM substep kernels for sm_100a.
 //
-// Step path (mpm::step, engine.cpp:288-297), per substep s:
-//   k_grid_update<true>  grid_update (engine.cpp:180-205) over the active
-//                        window; reads Grid::mass/momentum (A, M_I), writes
-//                        Grid::velocity (V) and re-zeroes A / M_I, so the next
-//                        scatter needs no separate zero_grid clear.
+// Step path (mpm::step, engine.cpp:288-297), per substep s (CUDA graph, each
+// kernel launched with programmatic stream serialization):
+//   k_grid_update_boxes  grid_update (engine.cpp:180-205) over the elastomer
+//                        and indenter node boxes; reads Grid::mass/momentum
+//                        (A, M_I), writes Grid::velocity (V) and re-zeroes A /
+//                        M_I, so the next scatter needs no zero_grid clear.
 //   k_g2p2g_gel          grid_to_particle + apply_boundary + advect for the
-//                        elastomer (engine.cpp:207-279) and, fused in the same
-//                        CTA, particle_to_grid of substep s+1 (engine.cpp:
-//                        107-178: det F, Newton polar, corotated stress, APIC)
-//                        through a shared-memory node tile: 27 barrier-
-//                        separated conflict-free accumulation phases, then one
-//                        RED.F64 per touched node and component.
-//   k_ind_move_p2g       apply_boundary + advect of the rigid indenter
-//                        (engine.cpp:260-261, 275-279) fused with its s+1
-//                        scatter: run-length accumulation of B-spline weights
-//                        in registers along z-sorted particle runs, one
-//                        RED.F64 per touched node (mass only: the indenter's
-//                        momentum is M_I * v, v uniform).
+//                        elastomer (engine.cpp:207-279) from a TMA-staged
+//                        velocity tile and, fused in the same CTA,
+//                        particle_to_grid of substep s+1 (engine.cpp:107-178:
+//                        det F, Newton polar, corotated stress, APIC) through
+//                        a shared-memory node tile: 27 barrier-separated
+//                        conflict-free accumulation phases, then one TMA bulk
+//                        reduction per tile row. Extra blocks of the same
+//                        launch run the rigid indenter's apply_boundary +
+//                        advect + s+1 scatter (ind_cols_block: warp per
+//                        z-sorted column, run-length accumulation of B-spline
+//                        weight sums, one RED.F64 per touched node into M_I;
+//                        the indenter's momentum is M_I * v, v uniform).
 //   k_finalize           advect's in_range check / step_count / max_speed and
 //                        the next zero_grid window (engine.cpp:53-68, 279-285).
-// The first substep of a call starts with a standalone scatter (k_p2g_gel_tile,
-// k_ind_move_p2g<false, true>); the last substep does no look-ahead scatter so
-// the state is complete when mpm::step returns. Errors are latched in
-// Ctl::err_code with the substep they belong to; every kernel of a later or
-// equal substep exits early, reproducing the reference's "state at the
-// throwing phase".
+// The first substep of a call without a pending look-ahead starts with a
+// standalone scatter (k_p2g_gel_tile, k_ind_cols<false>); every substep
+// scatters the next one, so consecutive calls chain; k_ind_catchup applies
+// the advects of indenter particles the column walks did not visit. Errors
+// are latched in Ctl::err_code with the substep they belong to; every kernel
+// of a later or equal substep exits early, reproducing the reference's
+// "state at the throwing phase".
 #include <climits>
 
 #include "engine.cuh"
