@@ -202,6 +202,23 @@ def test_out_of_grid_after_advect(tb):
     assert 1 <= s.step_count < 200
 
 
+def test_elastomer_moving_a_cell_per_substep_is_out_of_grid(tb):
+    """Deliberate deviation: the indenter's look-ahead walks
+    use the previous elastomer box widened by one node, valid while no
+    elastomer particle moves a full cell per substep; a step that does (here
+    an uploaded 100 m/s, dx / dt = 94 m/s) raises OutOfGrid at that substep
+    instead of continuing (the explicit scheme is far outside its stability
+    bound there)."""
+    s = tb.sim.build_sim(SMALL)
+    st = s.state()
+    v = st["v"].copy()
+    v[: s.elastomer_count, 0] = 100.0
+    s.set_state(v=v)
+    with pytest.raises(tb.OutOfGrid):
+        tb.mpm.step(s, (0, 0, 0), 5)
+    assert s.step_count <= 2
+
+
 def test_render_functions_match_reference(tb, golden):
     k = golden("kat.npz")
     r, hemi, ramp, src = render_inputs()
