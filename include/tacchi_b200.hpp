@@ -38,6 +38,10 @@ class ShapeMismatch : public Error { public: using Error::Error; };
 class ConfigError : public Error { public: using Error::Error; };
 class IoError : public Error { public: using Error::Error; };
 class CudaError : public Error { public: using Error::Error; };
+class SessionNotInitialized : public Error { public: using Error::Error; };
+class NonMonotonicTime : public Error { public: using Error::Error; };
+class ProtocolError : public Error { public: using Error::Error; };
+class ManifestMismatch : public Error { public: using Error::Error; };
 
 inline void check(int rc) {
   if (rc == TG_OK) return;
@@ -54,6 +58,10 @@ inline void check(int rc) {
     case TG_ERR_EMPTY_CLOUD: throw EmptyCloud(m);
     case TG_ERR_PARSE: throw ParseError(m);
     case TG_ERR_IO: throw IoError(m);
+    case TG_ERR_SESSION_NOT_INITIALIZED: throw SessionNotInitialized(m);
+    case TG_ERR_NON_MONOTONIC_TIME: throw NonMonotonicTime(m);
+    case TG_ERR_PROTOCOL: throw ProtocolError(m);
+    case TG_ERR_MANIFEST_MISMATCH: throw ManifestMismatch(m);
     case TG_ERR_CUDA: throw CudaError(m);
     default: throw Error(m);
   }
@@ -171,5 +179,77 @@ inline Capture capture(const mpm::SimState& s, const std::string& config_json,
   return c;
 }
 
+// One Session control step (session.cpp:86 + 42): mpm::step then capture,
+// submitted together with one host synchronisation.
+inline Capture step_capture(mpm::SimState& s, const Vec3& indenter_velocity, int n_substeps,
+                            const std::string& config_json, const std::string& object) {
+  tg_render r;
+  check(tg_render_from_config(config_json.c_str(), object.c_str(), &r));
+  Capture c;
+  c.depth.width = c.image.width = r.width;
+  c.depth.height = c.image.height = r.height;
+  c.depth.pixel_to_meter = r.pixel_to_meter * r.crop_scale;
+  c.depth.values.resize(static_cast<size_t>(r.width) * r.height);
+  c.image.data.resize(static_cast<size_t>(r.width) * r.height * 3);
+  check(tg_step_capture(s.handle(), indenter_velocity.data(), n_substeps, &r,
+                        c.depth.values.data(), c.image.data.data()));
+  return c;
+}
+
 }  // namespace sim
+
+// ---- bridge (server.hpp:13-40), dataset (harness.hpp), metrics ------------
+namespace bridge {
+// run_protocol over newline-separated JSON messages; returns the reply lines.
+inline std::string run_protocol(const std::string& input, const std::string& base_config_json,
+                                const std::string& session_root, int device = 0) {
+  char* out = nullptr;
+  check(tg_bridge_run(device, base_config_json.c_str(), session_root.c_str(), input.c_str(), &out));
+  std::string replies(out);
+  tg_free(out);
+  return replies;
+}
+// serve_stdio (port < 0) / serve_tcp on 127.0.0.1:port
+inline void serve(const std::string& base_config_json, const std::string& session_root,
+                  int port = -1, int max_connections = 0, int device = 0) {
+  check(tg_bridge_serve(device, base_config_json.c_str(), session_root.c_str(), port,
+                        max_connections));
+}
+}  // namespace bridge
+
+namespace dataset {
+struct DatasetResult {
+  int64_t rows = 0, skipped_positions = 0;
+};
+inline DatasetResult run_press_dataset(const std::string& config_json, const std::string& out_dir,
+                                       int device = 0, int batch = 0) {
+  DatasetResult r;
+  check(tg_run_press_dataset(device, config_json.c_str(), out_dir.c_str(), batch, &r.rows,
+                             &r.skipped_positions));
+  return r;
+}
+struct CompareAggregate {
+  int64_t pairs = 0;
+  double ssim_mean = 0, ssim_std = 0, psnr_mean = 0, psnr_std = 0, mae_mean = 0, mae_std = 0;
+};
+inline CompareAggregate compare_datasets(const std::string& dir_a, const std::string& dir_b,
+                                         const std::string& csv_out = "", int device = 0) {
+  double o[7];
+  check(tg_compare_datasets(device, dir_a.c_str(), dir_b.c_str(), csv_out.c_str(), o));
+  return {static_cast<int64_t>(o[0]), o[1], o[2], o[3], o[4], o[5], o[6]};
+}
+}  // namespace dataset
+
+namespace metrics {
+struct MetricReport {
+  double ssim = 0, psnr_db = 0, mae_pct = 0;
+};
+inline MetricReport compare(const render::Image8& a, const render::Image8& b, int device = 0) {
+  if (a.width != b.width || a.height != b.height)
+    throw ShapeMismatch("image shapes differ");
+  double o[3];
+  check(tg_image_metrics(device, a.data.data(), b.data.data(), a.width, a.height, 1, o));
+  return {o[0], o[1], o[2]};
+}
+}  // namespace metrics
 }  // namespace tacchi_b200
