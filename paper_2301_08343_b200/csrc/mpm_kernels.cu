@@ -224,6 +224,7 @@ struct P2GTile {
   int owner[kTileCap];
   int lo[3], hi[3], dim[3];
   int ok;
+  int pitch;     // node row pitch (>= dim[2], = 1 mod 8: rows shift the 16-byte bank slot)
   int zp, zoff;  // staged vz: node (row r, column c) at ((double*)nhi)[r * zp + zoff + c]
   unsigned long long bar;  // mbarrier of the staging copies
 };
@@ -236,6 +237,12 @@ __device__ __forceinline__ unsigned smem_addr(const void* p) {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+
+// Row pitches of the tile: nodes of the same z in neighbouring rows land in
+// different 16-byte bank slots (pitch = 1 mod 8 nodes); the staged vz rows
+// (8-byte elements, 16-byte aligned starts) use an even pitch = 2 mod 16.
+__host__ __device__ __forceinline__ int tile_pitch(int d2) { return ((d2 + 6) & ~7) + 1; }
+__host__ __device__ __forceinline__ int tile_zpitch(int zcnt) { return ((zcnt + 13) & ~15) + 2; }
 
 // Adds the CTA's node box into the global grid: one bulk-async reduction
 // (UBLKRED.ADD.F64, element-wise atomic in L2) per z-row and half, issued by
@@ -250,7 +257,7 @@ __device__ __forceinline__ void tile_bulk_reduce(const P2GTile& T, const Geometr
     const int r = t >> 1, half = t & 1;
     const int i = r / T.dim[1], j = r - i * T.dim[1];
     double2* dst = (half ? grid.hi : grid.lo) + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
-    const double2* src = (half ? T.nhi : T.nlo) + r * d2;
+    const double2* src = (half ? T.nhi : T.nlo) + r * T.pitch;
     asm volatile(
         "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
         "r"(smem_addr(src)), "r"(static_cast<unsigned>(d2 * sizeof(double2)))
@@ -278,8 +285,9 @@ __device__ __forceinline__ void tile_bulk_stage_issue(P2GTile& T, const Geometry
   // has the same parity zoff) over an even count, into rows of pitch zp.
   const int zoff = T.lo[2] & 1;
   const int zcnt = (zoff + d2 + 1) & ~1;
+  const int zp = tile_zpitch(zcnt);
   if (threadIdx.x == 0) {
-    T.zp = zcnt;
+    T.zp = zp;
     T.zoff = zoff;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -295,7 +303,7 @@ __device__ __forceinline__ void tile_bulk_stage_issue(P2GTile& T, const Geometry
     const size_t nd = node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
     const void* sp = half ? static_cast<const void*>(src.z + (nd - zoff))
                           : static_cast<const void*>(src.xy + nd);
-    void* dp = half ? static_cast<void*>(zs + r * zcnt) : static_cast<void*>(T.nlo + r * d2);
+    void* dp = half ? static_cast<void*>(zs + r * zp) : static_cast<void*>(T.nlo + r * T.pitch);
     const unsigned bytes = half ? zcnt * sizeof(double) : d2 * sizeof(double2);
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
@@ -407,13 +415,11 @@ __device__ void tile_box(P2GTile& T, bool active, const int* base) {
   }
   __syncthreads();
   if (tid == 0) {
-    int vol = 1;
     const bool any = T.lo[0] != INT_MAX;
-    for (int a = 0; a < 3; ++a) {
-      T.dim[a] = any ? T.hi[a] - T.lo[a] + 3 : 0;
-      vol *= T.dim[a];
-    }
-    T.ok = any && vol <= kTileCap;
+    for (int a = 0; a < 3; ++a) T.dim[a] = any ? T.hi[a] - T.lo[a] + 3 : 0;
+    T.pitch = tile_pitch(T.dim[2]);
+    const int rows = T.dim[0] * T.dim[1];
+    T.ok = any && rows * T.pitch <= kTileCap && rows * tile_zpitch(T.dim[2] + 2) <= 2 * kTileCap;
   }
   __syncthreads();
 }
@@ -441,7 +447,7 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
     }
     b[6] = T.ok;
   }
-  const int d1 = T.dim[1], d2 = T.dim[2];
+  const int d1 = T.dim[1], d2 = T.pitch;  // row pitch
   const int vol = T.dim[0] * d1 * d2;
   const bool use_tile = T.ok != 0;
   if (use_tile) {
@@ -1291,7 +1297,7 @@ __device__ __forceinline__ void g2p_gather(const Geometry& g, VelBuf vel,
 // T.nlo[.].x/y, T.nhi[.].x), same arithmetic as g2p_gather.
 __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile& T,
                                                 const Stencil& st, double* vv, double* Cn) {
-  const int d1 = T.dim[1], d2 = T.dim[2], zp = T.zp;
+  const int d1 = T.dim[1], d2 = T.pitch, zp = T.zp;
   const int r0 = (st.base[0] - T.lo[0]) * d1 + (st.base[1] - T.lo[1]);
   const int c0 = st.base[2] - T.lo[2];
   const double* zs = reinterpret_cast<const double*>(T.nhi);
@@ -1382,6 +1388,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
         T.dim[a] = b[3 + a];
       }
       T.ok = b[6] && (g.res[2] & 1) == 0;  // vz row staging needs an even res2
+      T.pitch = tile_pitch(T.dim[2]);
     }
     __syncthreads();
     staged = T.ok != 0;
