@@ -17,6 +17,9 @@ Fixtures (all numpy .npz):
                    full particle state, diagnostics, capture depth + image.
   config3.npz      SMALL3 scene per config-3 shape (cylinder, ring, wave,
                    dots): press then slide; full positions, F, image.
+  config1_deep.npz default config, 10,000 substeps (1000 frames) at the default
+                   press velocity: 0.1 mm into the gel; elastomer subset, surface
+                   positions, image and depth.
   config5.npz      large-area gel (848,421 + 1e5 particles, 512^3 grid):
                    50 substeps pressing + 30 moving laterally; seeded
                    4096-particle subset, every 7th surface particle, image.
@@ -47,7 +50,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import refpy as R  # noqa: E402
-from tests.scenes import (BAD_CONFIGS, HARNESS, PARTS, PARTS_STEPS, PARTS_V, CONFIG1, CONFIG5, CONFIG5_MOVE, CONFIG5_PRESS, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
+from tests.scenes import (BAD_CONFIGS, CONFIG1_DEEP_STEPS, HARNESS, PARTS, PARTS_STEPS, PARTS_V, CONFIG1, CONFIG5, CONFIG5_MOVE, CONFIG5_PRESS, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
                           SMALL, SMALL3, SMALL3_PRESS, SMALL3_SHAPES, SMALL3_SLIDE, SMALL_STEPS,
                           SMALL_V, render_inputs, sha)
 
@@ -155,6 +158,24 @@ def config1():
         x_surface=s1["x"][surf["particle"]], min_det_f=d["min_det_f"], max_speed=d["max_speed"],
         step_count=d["step_count"], image=img, depth_sha=sha(depth),
         depth_sample=depth[::16, ::16])
+
+
+def config1_deep():
+    sim = R.RefSim.from_config(CONFIG1, "", threads=0)
+    s0 = sim.state()
+    sim.step(CONFIG1_V, CONFIG1_DEEP_STEPS)
+    s1 = sim.state()
+    d = sim.diag()
+    depth, img = sim.capture(CONFIG1)
+    surf = sim.surface()
+    rng = np.random.default_rng(2)
+    subset = np.sort(rng.choice(sim.n_elastomer, 4096, replace=False))
+    np.savez_compressed(
+        os.path.join(OUT, "config1_deep.npz"), x0_hash=sha(s0["x"]), subset=subset,
+        x0_subset=s0["x"][subset], x_subset=s1["x"][subset],
+        F_subset=s1["F"].reshape(-1, 9)[subset], x_surface=s1["x"][surf["particle"]],
+        min_det_f=d["min_det_f"], max_speed=d["max_speed"], step_count=d["step_count"],
+        image=img, depth_sample=depth[::8, ::8], depth_max=depth.max())
 
 
 def config5():
@@ -280,6 +301,8 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge", "harness", "parts"]
     if "config5" in which:
         config5()
+    if "config1_deep" in which:
+        config1_deep()
     if "bridge" in which:
         bridge()
     if "harness" in which:

@@ -23,6 +23,9 @@ SMALL_V = (0.0, 0.0, -0.05)
 CONFIG1 = {"time": {"dt_s": 2e-6}}
 CONFIG1_STEPS = 1000  # 100 frames (SURVEY §8(d) CI parity)
 CONFIG1_V = (0.0, 0.0, -0.01)
+# 1000 frames: the indenter crosses the 0.1 mm gap after 500 and presses
+# 0.1 mm into the gel by the end (contact, the part 100 frames never reach).
+CONFIG1_DEEP_STEPS = 10000
 
 # Config 2a (BASELINE.json configs[1]): same gel, sphere at the reference's
 # finest indenter density (1e6 points, no subsampling) -> 1,214,221 particles.

@@ -262,6 +262,34 @@ def test_config1_hundred_frames_match_reference(tb, golden):
     assert np.abs(img.astype(int) - g["image"]).max() <= 2
 
 
+def test_config1_thousand_frames_pressing_matches_reference(tb, golden):
+    """Config 1 for 1000 frames (10,000 substeps): the indenter crosses the
+    0.1 mm gap and presses 0.1 mm into the gel; positions, F, height map and
+    image vs the reference."""
+    from tests.scenes import CONFIG1_DEEP_STEPS
+
+    g = golden("config1_deep.npz")
+    s = tb.sim.build_sim(CONFIG1)
+    x0 = s.positions()
+    assert sha(x0) == str(g["x0_hash"])
+    for _ in range(CONFIG1_DEEP_STEPS // 10):
+        tb.mpm.step(s, CONFIG1_V, 10)
+    st = s.state()
+    sub = g["subset"]
+    disp = np.abs(g["x_subset"] - g["x0_subset"]).max()
+    err = np.abs(st["x"][sub] - g["x_subset"]).max()
+    print(f"config1 deep: err {err:.3e} m, displacement {disp:.3e} m")
+    assert err <= 1e-9 * disp, (err, disp)  # measured ~5e-12 of the displacement
+    assert np.abs(st["x"][_default_surface()] - g["x_surface"]).max() <= 1e-9 * disp
+    np.testing.assert_allclose(st["F"].reshape(-1, 9)[sub], g["F_subset"], rtol=0, atol=1e-9)
+    d = s.diag
+    assert d.step_count == int(g["step_count"])
+    assert d.min_det_f == pytest.approx(float(g["min_det_f"]), abs=1e-9)
+    depth, img = tb.sim.capture(s, CONFIG1)
+    assert np.abs(depth[::8, ::8] - g["depth_sample"]).max() <= 1e-7
+    assert np.abs(img.astype(int) - g["image"]).max() <= 2
+
+
 def _default_surface(nx=101, ny=101, nz=21):
     return np.array([(i * ny + j) * nz + nz - 1 for i in range(nx) for j in range(ny)])
 
