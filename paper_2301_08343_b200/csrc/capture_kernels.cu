@@ -552,7 +552,7 @@ int render_standalone(int mode, const double* src, int sw, int sh, double r, dou
   cudaFree(d_u8);
   cudaFree(d_bg);
   cudaStreamDestroy(st);
-  return ok ? kOk : TG_ERR_CUDA;
+  return ok ? static_cast<int>(kOk) : static_cast<int>(TG_ERR_CUDA);
 }
 
 }  // namespace tacchi_b200
