@@ -252,7 +252,7 @@ void tg_free(void* p);
  * dataset::run_press_dataset (harness.cpp:159-245): every object of the
  * SceneConfig at every press-grid position, pressed at press_speed_mm_s with
  * one capture per depth level -> out_dir/{config.json, manifest.csv,
- * images/*.png, depth/*.depth}; complete (object, position) groups of an
+ * images/<stem>.png, depth/<stem>.depth}; complete (object, position) groups of an
  * existing manifest are kept (resume). `batch` simulations are stepped
  * together on `device` (0: config "workers", else 16). */
 int tg_run_press_dataset(int device, const char* config_json, const char* out_dir, int batch,
