@@ -210,6 +210,7 @@ def run_ours(args):
                   (phase_ms.get("p2g_elastomer_first", 0) + phase_ms.get("p2g_indenter_first", 0)) /
                   SUBSTEPS_PER_FRAME)
     traffic = None
+    shared = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f)
@@ -217,6 +218,12 @@ def run_ours(args):
                  "indenter_move_p2g": "k_ind_cols"}.get(dom)
         if kname in tr:
             traffic = tr[kname]["dram_bytes_per_launch"]
+            if "shared_wavefronts_per_launch" in tr[kname]:
+                shared = {"wavefronts_per_launch": tr[kname]["shared_wavefronts_per_launch"],
+                          "pct_of_peak_sustained": tr[kname]["shared_wavefronts_pct_of_peak"],
+                          "source": "profiles/traffic.json (ncu l1tex__data_pipe_lsu_wavefronts_"
+                                    "mem_shared): the elastomer kernel is bound by shared memory "
+                                    "and latency, not HBM (DESIGN.md 4.2)"}
     except Exception:
         traffic = None
     line = {
@@ -239,6 +246,7 @@ def run_ours(args):
                      "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write per launch)",
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": per_kernel[dom],
+                     "shared_memory": shared,
                      "kernel_ms": dom_ms,
                      "substep": {"ms": substep_ms,
                                  "ms_measured_in_frames": dev_ms / (args.steps * SUBSTEPS_PER_FRAME),

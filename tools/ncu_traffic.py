@@ -1,6 +1,7 @@
 """Per-kernel DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum, per
-launch, averaged over the captured launches) from an ncu --set full report,
-written as JSON for bench.py's roofline "traffic" field.
+launch, averaged over the captured launches) and shared-memory wavefronts
+(l1tex__data_pipe_lsu_wavefronts_mem_shared) from an ncu --set full report,
+written as JSON for bench.py's roofline "traffic" / "shared_memory" fields.
 
     python tools/ncu_traffic.py gpurun_out/prof.ncu-rep > profiles/traffic.json
 """
@@ -26,14 +27,19 @@ def main(path):
     raw2 = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--print-units", "base"],
                           capture_output=True, text=True, check=True).stdout
     rows2 = list(csv.reader(io.StringIO(raw2)))[2:]
-    acc = defaultdict(lambda: [0.0, 0.0, 0])
+    si = hdr.index("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
+    sp = hdr.index("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")
+    acc = defaultdict(lambda: [0.0, 0.0, 0, 0.0, 0.0])
     for r in rows2:
         name = r[name_i].split("(")[0].replace("void ", "").split("<")[0].strip()
         acc[name][0] += float(r[ri]) + float(r[wi])
         acc[name][1] += float(r[ti])
         acc[name][2] += 1
+        acc[name][3] += float(r[si] or 0)
+        acc[name][4] += float(r[sp] or 0)
     out = {k: {"dram_bytes_per_launch": v[0] / v[2], "ncu_time_ns": v[1] / v[2], "launches": v[2],
-               "report": path}
+               "shared_wavefronts_per_launch": v[3] / v[2],
+               "shared_wavefronts_pct_of_peak": v[4] / v[2], "report": path}
            for k, v in acc.items()}
     json.dump(out, sys.stdout, indent=1)
     print()
