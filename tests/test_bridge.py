@@ -195,3 +195,24 @@ def test_default_terminal_is_deepest_press_level(tmp_path):
     assert [m["step"] for m in out[1:9]] == [1, 2, 3, 3, 3, 3, 3, 3]
     assert out[-1] == {"type": "done", "steps": 3}
     assert os.path.exists(os.path.join(out[0]["session_dir"], "steps.jsonl"))
+
+
+@pytest.mark.gpu
+def test_serve_tcp_session_matches_in_process(golden, tmp_path):
+    """The same scripted session over loopback TCP (serve_tcp) gives the
+    reference's replies, like the in-process transport."""
+    tb = _tb()
+    port = _free_port()
+    sdir = str(tmp_path / "tcp")
+    th = threading.Thread(target=tb.bridge.serve,
+                          kwargs=dict(session_root=str(tmp_path), port=port, max_connections=1))
+    th.start()
+    try:
+        script = [m for m in bridge_script(sdir) if not isinstance(m, str)]
+        got = _tcp_session(port, script)
+    finally:
+        th.join(timeout=120)
+    ref = [r for r in json.loads(str(golden["replies"]).replace("<dir>", sdir))
+           if r.get("echo") != "not json"]
+    assert got == ref
+    assert not th.is_alive()

@@ -11,7 +11,6 @@ Prints one JSON line.
 """
 import argparse
 import json
-import math
 import os
 import shutil
 import sys
