@@ -58,8 +58,21 @@ void save_png(const Image8& image, const std::filesystem::path& path) {
   std::fwrite(image.data.data(), 1, image.data.size(), f);
   std::fclose(f);
 }
+// ... and load_png reads that PPM back (render_params_struct's background).
 Image8 load_png(const std::filesystem::path& path) {
-  throw IoError("load_png unavailable in the oracle build: " + path.string());
+  std::FILE* f = std::fopen(path.string().c_str(), "rb");
+  if (!f) throw IoError("cannot open " + path.string());
+  int w = 0, h = 0, maxv = 0;
+  if (std::fscanf(f, "P6 %d %d %d", &w, &h, &maxv) != 3 || maxv != 255 || w <= 0 || h <= 0) {
+    std::fclose(f);
+    throw ParseError("not a binary PPM (oracle build): " + path.string());
+  }
+  std::fgetc(f);  // the single whitespace after the header
+  Image8 img(w, h);
+  const size_t got = std::fread(img.data.data(), 1, img.data.size(), f);
+  std::fclose(f);
+  if (got != img.data.size()) throw ParseError("truncated PPM: " + path.string());
+  return img;
 }
 }  // namespace tacchi::render
 

@@ -8,7 +8,10 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <filesystem>
 #include <functional>
+#include <memory>
+#include <mutex>
 #include <map>
 #include <numeric>
 #include <random>
@@ -622,6 +625,37 @@ std::string to_json_string(const Config& c) {
   return j.dump(2) + "\n";
 }
 
+// Background images of render configs, decoded once per (path, size, mtime)
+// and kept for the process (tg_render::background points into the cache).
+const uint8_t* background_pixels(const std::string& path, int& w, int& h) {
+  struct Entry {
+    std::vector<uint8_t> rgb;
+    int w = 0, h = 0;
+    std::uintmax_t size = 0;
+    std::filesystem::file_time_type mtime{};
+  };
+  static std::mutex mu;
+  static std::map<std::string, std::unique_ptr<Entry>> cache;
+  static std::vector<std::unique_ptr<Entry>> retired;  // earlier tg_render may still point here
+  std::error_code ec;
+  const auto size = std::filesystem::file_size(path, ec);
+  if (ec) raise(TG_ERR_IO, "cannot open " + path);
+  const auto mtime = std::filesystem::last_write_time(path, ec);
+  std::lock_guard<std::mutex> lk(mu);
+  auto& e = cache[path];
+  if (!e || e->size != size || e->mtime != mtime) {
+    auto fresh = std::make_unique<Entry>();
+    fresh->rgb = load_png(path, fresh->w, fresh->h);
+    fresh->size = size;
+    fresh->mtime = mtime;
+    if (e) retired.push_back(std::move(e));
+    e = std::move(fresh);
+  }
+  w = e->w;
+  h = e->h;
+  return e->rgb.data();
+}
+
 template <typename F>
 int guarded(F&& f) {
   try {
@@ -651,9 +685,15 @@ int tg_build_sim(int device, const char* config_json, const char* object, double
 int tg_render_from_config(const char* config_json, const char* object, tg_render* r) {
   return guarded([&] {
     const Config c = parse_config(config_json);
-    if (!c.background_image.empty())
-      raise(TG_ERR_IO, "background_image PNG loading is not supported by this build; pass "
-                       "tg_render::background instead");
+    const uint8_t* background = nullptr;
+    if (!c.background_image.empty()) {
+      // render_params_struct loads the PNG (scene_config.cpp:77-78); phong
+      // requires its size to be the image's (phong.cpp:46-48)
+      int bw = 0, bh = 0;
+      background = background_pixels(c.background_image, bw, bh);
+      if (bw != c.image_w || bh != c.image_h)
+        raise(TG_ERR_SHAPE_MISMATCH, "phong_render: background image size differs from the depth map");
+    }
     std::memset(r, 0, sizeof(*r));
     r->pixel_to_meter = c.pixel_to_meter;
     const auto it = c.alignment.find(object ? object : "");
@@ -680,7 +720,7 @@ int tg_render_from_config(const char* config_json, const char* object, tg_render
         r->lights[l][3 + k] = c.lights[l].diffuse[k];
         r->lights[l][6 + k] = c.lights[l].specular[k];
       }
-    r->background = nullptr;
+    r->background = background;
     return TG_OK;
   });
 }

@@ -27,6 +27,7 @@ Fixtures (all numpy .npz):
                    by tests/scenes.bridge_script on the SMALL scene, plus the
                    init errors of BAD_CONFIGS: replies, steps.jsonl, the
                    .depth files (bytes) and the images (pixels).
+  background.npz   sim::capture with a render background image (SMALL scene).
   parts.npz        mpm::init_scene from explicit parts (PARTS: gravity, moving
                    indenter at creation, then a non-uniform indenter velocity):
                    initial arrays and the state after PARTS_STEPS substeps.
@@ -269,6 +270,29 @@ def parts():
         surf_n=np.array([surf["nx"], surf["ny"]]))
 
 
+def background_pixels(h=120, w=160):
+    yy, xx = np.mgrid[0:h, 0:w]
+    return np.stack([(xx * 7 + yy * 3) % 256, (xx * 2 + yy * 11) % 256, (xx * yy) % 256],
+                    axis=2).astype(np.uint8)
+
+
+def background():
+    """sim::capture with a render background image (render_params_struct loads
+    it, phong_render starts from k_a * background): SMALL scene at creation."""
+    import tempfile
+
+    bg = background_pixels()
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "bg.png")
+        with open(path, "wb") as f:  # binary PPM under the .png name (ref_driver load_png)
+            f.write(b"P6\n160 120\n255\n" + bg.tobytes())
+        cfg = {**SMALL, "render": {**SMALL["render"], "background_image": path}}
+        sim = R.RefSim.from_config(cfg, "", threads=0)
+        depth, img = sim.capture(cfg)
+    np.savez_compressed(os.path.join(OUT, "background.npz"), background=bg, image=img,
+                        depth_sha=sha(depth))
+
+
 def bridge():
     import json
     import shutil
@@ -298,7 +322,7 @@ def bridge():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge", "harness", "parts"]
+    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge", "harness", "parts", "background"]
     if "config5" in which:
         config5()
     if "config1_deep" in which:
@@ -309,6 +333,8 @@ if __name__ == "__main__":
         harness()
     if "parts" in which:
         parts()
+    if "background" in which:
+        background()
     if "kat" in which:
         kat()
     if "small" in which:

@@ -90,3 +90,30 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(tb.CudaError):
         tb.sim.build_sim({"time": {"dt_s": 2e-6}, "indenter": {"source_points": 2000,
                                                                  "target_points": 1000}})
+
+
+def test_render_background_image_from_config(tmp_path):
+    """render_params_struct's background_image (scene_config.cpp:77-78): loaded
+    once, passed to the capture; a size other than the image's is the
+    reference's ShapeMismatch (phong.cpp:46-48)."""
+    import ctypes
+
+    import numpy as np
+
+    import paper_2301_08343_b200 as tb
+    from tests.scenes import SMALL
+
+    bg = np.random.default_rng(4).integers(0, 256, (120, 160, 3), dtype=np.uint8)
+    path = str(tmp_path / "bg.png")
+    tb.save_png(bg, path)
+    cfg = {**SMALL, "render": {**SMALL["render"], "background_image": path}}
+    rp = tb.render_params(cfg, "")
+    assert rp.background
+    got = np.ctypeslib.as_array(ctypes.cast(rp.background, ctypes.POINTER(ctypes.c_uint8)),
+                                shape=(120, 160, 3))
+    np.testing.assert_array_equal(got, bg)
+    tb.save_png(bg[:60], path)  # rewritten with another size: reloaded, rejected
+    with pytest.raises(tb.ShapeMismatch):
+        tb.render_params(cfg, "")
+    with pytest.raises(tb.IoError):
+        tb.render_params({**cfg, "render": {"background_image": str(tmp_path / "none.png")}}, "")

@@ -219,6 +219,19 @@ def test_elastomer_moving_a_cell_per_substep_is_out_of_grid(tb):
     assert s.step_count <= 2
 
 
+def test_capture_with_background_image_matches_reference(tb, golden, tmp_path):
+    """sim::capture with render.background_image (the image starts from
+    k_a * background, phong.cpp:61-64), bit-exact on identical positions."""
+    g = golden("background.npz")
+    path = str(tmp_path / "bg.png")
+    tb.save_png(g["background"], path)
+    cfg = {**SMALL, "render": {**SMALL["render"], "background_image": path}}
+    s = tb.sim.build_sim(cfg)
+    depth, img = tb.sim.capture(s, cfg)
+    assert sha(depth) == str(g["depth_sha"])
+    np.testing.assert_array_equal(img, g["image"])
+
+
 def test_render_functions_match_reference(tb, golden):
     k = golden("kat.npz")
     r, hemi, ramp, src = render_inputs()
