@@ -8,7 +8,10 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <charconv>
 #include <filesystem>
+#include <fstream>
+#include <string_view>
 #include <functional>
 #include <memory>
 #include <mutex>
@@ -403,16 +406,141 @@ std::vector<V3> place(const std::vector<V3>& cloud, const V3& t, double rot) {
   return out;
 }
 
-// indenter_cloud_for (scene_builder.cpp:33-46): generated shape (or
-// cloud_path, unsupported here), subsampled to target_points.
+// ---- point-cloud files (geo/point_cloud_io.cpp:14-141): plain XYZ or ASCII
+// PLY, coordinates in millimetres -----------------------------------------
+namespace {
+
+std::vector<std::string_view> split_ws(std::string_view line) {
+  std::vector<std::string_view> toks;
+  size_t i = 0;
+  while (i < line.size()) {
+    while (i < line.size() && (line[i] == ' ' || line[i] == '\t' || line[i] == '\r')) ++i;
+    size_t j = i;
+    while (j < line.size() && line[j] != ' ' && line[j] != '\t' && line[j] != '\r') ++j;
+    if (j > i) toks.push_back(line.substr(i, j - i));
+    i = j;
+  }
+  return toks;
+}
+
+bool parse_double(std::string_view tok, double& out) {
+  const auto r = std::from_chars(tok.data(), tok.data() + tok.size(), out);
+  return r.ec == std::errc{} && r.ptr == tok.data() + tok.size();
+}
+
+bool parse_size(std::string_view tok, size_t& out) {
+  const auto r = std::from_chars(tok.data(), tok.data() + tok.size(), out);
+  return r.ec == std::errc{} && r.ptr == tok.data() + tok.size();
+}
+
+[[noreturn]] void cloud_fail(const std::string& path, size_t line_no, const std::string& what) {
+  raise(TG_ERR_PARSE, path + ":" + std::to_string(line_no) + ": " + what);
+}
+
+constexpr double kFileUnitToMeter = 1e-3;
+
+std::vector<V3> load_ply(std::ifstream& in, const std::string& path) {
+  std::string line;
+  size_t line_no = 1;
+  bool ascii = false, in_vertex = false;
+  size_t vertex_count = 0;
+  int xi = -1, yi = -1, zi = -1, props = 0;
+  while (std::getline(in, line)) {
+    ++line_no;
+    const auto t = split_ws(line);
+    if (t.empty() || t[0] == "comment") continue;
+    if (t[0] == "format") {
+      if (t.size() < 2 || t[1] != "ascii") cloud_fail(path, line_no, "only ascii PLY is supported");
+      ascii = true;
+    } else if (t[0] == "element") {
+      if (t.size() < 3) cloud_fail(path, line_no, "malformed element line");
+      in_vertex = t[1] == "vertex";
+      if (in_vertex && !parse_size(t[2], vertex_count)) cloud_fail(path, line_no, "bad vertex count");
+    } else if (t[0] == "property") {
+      if (!in_vertex) continue;
+      if (t.size() >= 3 && t[1] == "list") cloud_fail(path, line_no, "list property in vertex element");
+      const std::string_view name = t.back();
+      if (name == "x") xi = props;
+      else if (name == "y") yi = props;
+      else if (name == "z") zi = props;
+      ++props;
+    } else if (t[0] == "end_header") {
+      break;
+    }
+  }
+  if (!ascii) cloud_fail(path, line_no, "missing 'format ascii 1.0' header");
+  if (xi < 0 || yi < 0 || zi < 0) cloud_fail(path, line_no, "vertex element lacks x/y/z properties");
+  std::vector<V3> pts;
+  pts.reserve(vertex_count);
+  for (size_t v = 0; v < vertex_count; ++v) {
+    if (!std::getline(in, line)) cloud_fail(path, line_no, "unexpected end of file in vertex data");
+    ++line_no;
+    const auto t = split_ws(line);
+    if (t.empty()) {
+      --v;
+      continue;
+    }
+    if (static_cast<int>(t.size()) < props) cloud_fail(path, line_no, "short vertex line");
+    double c[3];
+    for (int a = 0; a < 3; ++a)
+      if (!parse_double(t[a == 0 ? xi : (a == 1 ? yi : zi)], c[a]))
+        cloud_fail(path, line_no, "bad coordinate");
+    pts.push_back({c[0] * kFileUnitToMeter, c[1] * kFileUnitToMeter, c[2] * kFileUnitToMeter});
+  }
+  if (pts.empty()) raise(TG_ERR_EMPTY_CLOUD, path + ": no vertices");
+  return pts;
+}
+
+}  // namespace
+
+// geo::load_point_cloud (point_cloud_io.cpp:108-141)
+std::vector<V3> load_point_cloud(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) raise(TG_ERR_IO, "cannot open " + path);
+  std::string line;
+  size_t line_no = 0;
+  std::streampos first_pos = in.tellg();
+  while (std::getline(in, line)) {
+    ++line_no;
+    if (!split_ws(line).empty()) break;
+    first_pos = in.tellg();
+  }
+  const auto toks = split_ws(line);
+  if (toks.empty()) raise(TG_ERR_EMPTY_CLOUD, path + ": empty file");
+  if (toks[0] == "ply") return load_ply(in, path);
+  in.clear();
+  in.seekg(first_pos);
+  line_no -= 1;
+  std::vector<V3> pts;
+  while (std::getline(in, line)) {
+    ++line_no;
+    const auto t = split_ws(line);
+    if (t.empty()) continue;
+    if (t.size() < 3) cloud_fail(path, line_no, "expected 3 coordinates");
+    double x, y, z;
+    if (!parse_double(t[0], x) || !parse_double(t[1], y) || !parse_double(t[2], z))
+      cloud_fail(path, line_no, "bad coordinate");
+    pts.push_back({x * kFileUnitToMeter, y * kFileUnitToMeter, z * kFileUnitToMeter});
+  }
+  if (pts.empty()) raise(TG_ERR_EMPTY_CLOUD, path + ": no points");
+  return pts;
+}
+
+// indenter_cloud_for (scene_builder.cpp:33-50): cloud_path, else the
+// generated shape, else the object name as a file; subsampled to
+// target_points.
 std::vector<V3> indenter_cloud_for(const Config& c, const std::string& object) {
-  if (!c.cloud_path.empty() && (object.empty() || object == c.cloud_path))
-    raise(TG_ERR_IO, "point-cloud files are not supported by this build: " + c.cloud_path);
-  const std::string shape = object.empty() ? c.generated_shape : object;
-  Shape probe;
-  if (!make_shape(shape, probe))
-    raise(TG_ERR_IO, "point-cloud files are not supported by this build: " + shape);
-  std::vector<V3> cloud = generate_cloud(shape, c.source_points, c.seed);
+  std::vector<V3> cloud;
+  if (!c.cloud_path.empty() && (object.empty() || object == c.cloud_path)) {
+    cloud = load_point_cloud(c.cloud_path);
+  } else {
+    const std::string shape = object.empty() ? c.generated_shape : object;
+    Shape probe;
+    if (!make_shape(shape, probe))
+      cloud = load_point_cloud(shape);  // the object name as a file path
+    else
+      cloud = generate_cloud(shape, c.source_points, c.seed);
+  }
   if (c.target_points < cloud.size()) cloud = subsample(cloud, c.target_points, c.seed);
   return cloud;
 }

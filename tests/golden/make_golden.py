@@ -27,6 +27,8 @@ Fixtures (all numpy .npz):
                    by tests/scenes.bridge_script on the SMALL scene, plus the
                    init errors of BAD_CONFIGS: replies, steps.jsonl, the
                    .depth files (bytes) and the images (pixels).
+  clouds.npz       indenters from point-cloud files (ASCII PLY, XYZ) and the
+                   reference's errors for malformed files.
   background.npz   sim::capture with a render background image (SMALL scene).
   parts.npz        mpm::init_scene from explicit parts (PARTS: gravity, moving
                    indenter at creation, then a non-uniform indenter velocity):
@@ -293,6 +295,53 @@ def background():
                         depth_sha=sha(depth))
 
 
+def cloud_files():
+    """Point-cloud files as indenters (geo::load_point_cloud, scene_builder.cpp:
+    33-50): an ASCII PLY with extra properties and comments, a plain XYZ file
+    with blank lines; the placed indenters the reference builds from them and
+    its errors for malformed files."""
+    import tempfile
+
+    rng = np.random.default_rng(9)
+    pts = rng.uniform(-2.0, 2.0, (3000, 3))
+    pts = (pts[np.linalg.norm(pts, axis=1) < 2.0] * np.array([1.0, 1.0, 0.5])).tolist()
+    ply = ["ply", "format ascii 1.0", "comment test cloud", f"element vertex {len(pts)}",
+           "property float nx", "property double x", "property double y", "property double z",
+           "element face 0", "property list uchar int vertex_indices", "end_header"]
+    ply += [f"0.5 {x!r} {y!r} {z!r}" for x, y, z in pts]
+    xyz = ["", "  "] + [f"{x:.9f}\t{y:.9f} {z:.9f}" + ("" if k % 7 else "\n") for k, (x, y, z) in
+                         enumerate(pts)]
+    texts = {"ply": "\n".join(ply) + "\n", "xyz": "\n".join(xyz) + "\n",
+             "binary": "ply\nformat binary_little_endian 1.0\nelement vertex 1\nend_header\n",
+             "empty": "\n\n", "short": "1.0 2.0\n"}
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        paths = {}
+        for k, t in texts.items():
+            paths[k] = os.path.join(d, f"cloud_{k}.{'ply' if k in ('ply', 'binary') else 'xyz'}")
+            with open(paths[k], "w") as f:
+                f.write(t)
+        for k in ("ply", "xyz"):
+            cfg = {"indenter": {"cloud_path": paths[k], "target_points": 2000}}
+            placed = R.placed_indenter(cfg, "")
+            out[f"{k}_hash"] = sha(placed)
+            out[f"{k}_n"] = len(placed)
+            # the object name as a file path (no cloud_path)
+            placed2 = R.placed_indenter({"indenter": {"target_points": 2000}}, paths[k])
+            out[f"{k}_obj_hash"] = sha(placed2)
+            sub = R.placed_indenter({"indenter": {"cloud_path": paths[k], "target_points": 1000,
+                                                  "z_rotation_rad": 0.3}}, "")
+            out[f"{k}_sub_hash"] = sha(sub)
+        for k in ("binary", "empty", "short"):
+            try:
+                R.placed_indenter({"indenter": {"cloud_path": paths[k]}}, "")
+                out[f"{k}_err"] = "none"
+            except R.RefError as e:
+                out[f"{k}_err"] = f"{e.code}:" + e.msg.replace(paths[k], "<path>")
+    np.savez_compressed(os.path.join(OUT, "clouds.npz"), **{f"text_{k}": v for k, v in texts.items()},
+                        **out)
+
+
 def bridge():
     import json
     import shutil
@@ -322,7 +371,7 @@ def bridge():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge", "harness", "parts", "background"]
+    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge", "harness", "parts", "background", "clouds"]
     if "config5" in which:
         config5()
     if "config1_deep" in which:
@@ -335,6 +384,8 @@ if __name__ == "__main__":
         parts()
     if "background" in which:
         background()
+    if "clouds" in which:
+        cloud_files()
     if "kat" in which:
         kat()
     if "small" in which:

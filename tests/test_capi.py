@@ -117,3 +117,33 @@ def test_render_background_image_from_config(tmp_path):
         tb.render_params(cfg, "")
     with pytest.raises(tb.IoError):
         tb.render_params({**cfg, "render": {"background_image": str(tmp_path / "none.png")}}, "")
+
+
+def test_point_cloud_files_match_reference(golden, tmp_path):
+    """Indenters from point-cloud files (geo::load_point_cloud, ASCII PLY and
+    plain XYZ in millimetres; scene_builder.cpp:33-50: cloud_path, or the
+    object name as a path), placed bit-identically to the reference; its
+    errors for malformed files."""
+    import paper_2301_08343_b200 as tb
+
+    g = golden("clouds.npz")
+    paths = {}
+    for k in ("ply", "xyz", "binary", "empty", "short"):
+        paths[k] = str(tmp_path / f"cloud_{k}.{'ply' if k in ('ply', 'binary') else 'xyz'}")
+        with open(paths[k], "w") as f:
+            f.write(str(g[f"text_{k}"]))
+    for k in ("ply", "xyz"):
+        placed = tb.geo.placed_indenter({"indenter": {"cloud_path": paths[k],
+                                                      "target_points": 2000}})
+        assert len(placed) == int(g[f"{k}_n"]) and sha(placed) == str(g[f"{k}_hash"])
+        obj = tb.geo.placed_indenter({"indenter": {"target_points": 2000}}, paths[k])
+        assert sha(obj) == str(g[f"{k}_obj_hash"])
+        sub = tb.geo.placed_indenter({"indenter": {"cloud_path": paths[k], "target_points": 1000,
+                                                   "z_rotation_rad": 0.3}})
+        assert sha(sub) == str(g[f"{k}_sub_hash"])
+    errors = {10: tb.ParseError, 9: tb.EmptyCloud}
+    for k in ("binary", "empty", "short"):
+        code, msg = str(g[f"{k}_err"]).split(":", 1)
+        with pytest.raises(errors[int(code)]) as e:
+            tb.geo.placed_indenter({"indenter": {"cloud_path": paths[k]}})
+        assert str(e.value).replace(paths[k], "<path>") == msg
