@@ -70,6 +70,28 @@ def test_small_scene_matches_reference(tb, golden):
     assert np.abs(img.astype(int) - g["image"]).max() <= 2
 
 
+@pytest.mark.parametrize("env", [{"TACCHI_FULL_INDENTER": "1"}, {"TACCHI_SCATTER": "1"},
+                                 {"TACCHI_FULL_INDENTER": "1", "TACCHI_SCATTER": "1"}])
+def test_alternative_scatter_paths_match_reference(tb, golden, monkeypatch, env):
+    """The alternative device paths (read at tg_create): every indenter
+    particle scattered by k_ind_move_p2g instead of the column walks, and the
+    per-particle RED.F64 elastomer scatter instead of the shared tile."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = golden("small_scene.npz")
+    s = tb.sim.build_sim(SMALL)
+    tb.mpm.step(s, SMALL_V, SMALL_STEPS // 2)
+    tb.mpm.step(s, SMALL_V, SMALL_STEPS // 2)
+    st = s.state()
+    disp = np.abs(g["x"] - g["x0"]).max()
+    assert np.abs(st["x"] - g["x"]).max() <= 1e-9 * disp
+    np.testing.assert_allclose(st["F"], g["F"], rtol=0, atol=1e-11)
+    assert s.diag.step_count == int(g["step_count"])
+    depth, img = tb.sim.capture(s, SMALL)
+    assert np.abs(depth - g["depth"]).max() <= 1e-7
+    assert np.abs(img.astype(int) - g["image"]).max() <= 2
+
+
 def test_capture_bit_exact_for_identical_positions(tb, golden, oracle):
     g = golden("small_scene.npz")
     s = tb.sim.build_sim(SMALL)
