@@ -185,6 +185,34 @@ def test_step_capture_matches_step_then_capture(tb):
     assert none is None and b.step_count == a.step_count + 250
 
 
+def test_handles_stepped_from_concurrent_threads(tb, golden):
+    """One control thread per handle: four host threads each
+    drive their own simulation at the same time; each matches the reference."""
+    import threading
+
+    g = golden("small_scene.npz")
+    results, errors = {}, []
+
+    def run(i):
+        try:
+            s = tb.sim.build_sim(SMALL)
+            for _ in range(SMALL_STEPS // 10):
+                tb.mpm.step(s, SMALL_V, 10)
+            results[i] = s.state()["x"]
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    disp = np.abs(g["x"] - g["x0"]).max()
+    for x in results.values():
+        assert np.abs(x - g["x"]).max() <= 1e-9 * disp
+
+
 def test_step_many_matches_individual_steps(tb):
     sims = [tb.sim.build_sim(SMALL, "", 1e-4 * i, 0.0) for i in range(3)]
     ref = [tb.sim.build_sim(SMALL, "", 1e-4 * i, 0.0) for i in range(3)]
