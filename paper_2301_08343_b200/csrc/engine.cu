@@ -27,7 +27,7 @@ int launch_grid_update(DeviceSim& s, int sms, bool zero);
 int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter = false);
 int launch_ind_move(DeviceSim& s, bool lookahead);
 int launch_finalize_step(DeviceSim& s, bool cfl_check = false);
-int launch_call_begin(DeviceSim& s);
+int launch_chain_begin(DeviceSim& s);
 int launch_ind_cols(DeviceSim& s, bool move);
 int launch_ind_catchup(DeviceSim& s);
 int launch_phase_g2p(DeviceSim& s);
@@ -334,6 +334,14 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   return TG_OK;
 }
 
+// Applies the open indenter chain's pending advects and closes the chain.
+static void flush_indenter(DeviceSim& s) {
+  if (!s.chain_open) return;
+  if (s.n_cols > 0 && !s.full_indenter) launch_ind_catchup(s);
+  s.chain_open = false;
+  s.chain_len = 0;
+}
+
 // Reads back the control block and converts a latched device error into the
 // reference's exception semantics. `end_substep` is the absolute substep index
 // one past the last substep this call asked for: an error raised for a later
@@ -346,6 +354,7 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
   const Ctl& c = *s.h_ctl;
   s.host_substep = c.substep;
   if (c.err_code == 0) return TG_OK;
+  flush_indenter(s);  // the state at the throw includes the indenter's advects
   const int code = c.err_code;
   const int at = c.err_substep;
   // Clear the latch; the next call re-derives the window from the state.
@@ -391,7 +400,7 @@ static int record_substep(DeviceSim& s, int sms, bool cols) {
 }
 
 static int record_substeps(DeviceSim& s, int n_substeps) {
-  int k = launch_call_begin(s);
+  int k = 0;
   const int sms = sm_count(s.device);
   const bool cols = s.n_cols > 0 && !s.full_indenter;
   if (!s.grid_ready) {
@@ -400,7 +409,6 @@ static int record_substeps(DeviceSim& s, int n_substeps) {
     k += (cols && s.ind_v_uniform) ? launch_ind_cols(s, false) : launch_p2g_ind(s);
   }
   for (int i = 0; i < n_substeps; ++i) k += record_substep(s, sms, cols);
-  if (cols) k += launch_ind_catchup(s);
   return k;
 }
 
@@ -410,10 +418,24 @@ int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
   s.pending_start = s.host_substep;
   if (n_substeps <= 0) return TG_OK;
   for (int a = 0; a < 3; ++a) s.h_vind[a] = vind[a];
+  // the indenter chain continues only with the same velocity (bitwise) and
+  // while the per-particle 8-bit move counters cannot overflow
+  if (s.chain_open && (std::memcmp(s.chain_vind, vind, sizeof(s.chain_vind)) != 0 ||
+                       s.chain_len + n_substeps > 255))
+    flush_indenter(s);
   // zero_grid of the first substep (a failing window latches OutOfGrid for
-  // this substep and every later kernel exits early).
-  if (!s.window_valid) launch_window(s);
+  // this substep and every later kernel exits early); it reads positions.
+  if (!s.window_valid) {
+    flush_indenter(s);
+    launch_window(s);
+  }
   s.window_valid = true;
+  if (!s.chain_open) {
+    launch_chain_begin(s);
+    s.chain_open = true;
+    std::memcpy(s.chain_vind, vind, sizeof(s.chain_vind));
+  }
+  s.chain_len += n_substeps;
   if (s.use_graphs) {
     const int key = n_substeps * 32 + (s.grid_dirty ? 1 : 0) + (s.ind_v_uniform ? 2 : 0) +
                     (s.grid_ready ? 4 : 0);
@@ -475,6 +497,7 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
   for (int g = 0; g < kGroups; ++g) out_ms[g] = 0.0;
   for (int a = 0; a < 3; ++a) s.h_vind[a] = vind[a];
   const int start = s.host_substep;
+  flush_indenter(s);
   if (!s.window_valid) launch_window(s);
   s.window_valid = true;
   CUDA_TRY(cudaMemcpyAsync(&s.ctl->vind[0], s.h_vind, 3 * sizeof(double), cudaMemcpyHostToDevice,
@@ -485,7 +508,7 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
   }
   if (s.grid_dirty) launch_clear(s, sms);
   const bool cols = s.n_cols > 0 && !s.full_indenter;
-  launch_call_begin(s);
+  launch_chain_begin(s);
   float ms = 0.f;
   cudaEventRecord(ev[0], s.stream);
   launch_p2g_gel(s);
@@ -523,6 +546,7 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
 
 int phase(DeviceSim& s, int ph, const double vind[3]) {
   CUDA_TRY(cudaSetDevice(s.device));
+  flush_indenter(s);  // the phases read and move every particle
   if (s.grid_ready) {  // phases drive zero_grid / P2G themselves
     s.grid_ready = false;
     s.grid_dirty = true;
@@ -564,6 +588,7 @@ static void to_component_major(const double* src, int64_t n, int ncomp, const st
 int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, const double* Fm,
            bool init) {
   CUDA_TRY(cudaSetDevice(s.device));
+  flush_indenter(s);
   CUDA_TRY(cudaStreamSynchronize(s.stream));
   std::vector<double> buf;
   auto put3 = [&](const double* src, double* dst) -> int {
@@ -609,6 +634,7 @@ int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, con
 
 int download(DeviceSim& s, double* x, double* v, double* Cm, double* Fm) {
   CUDA_TRY(cudaSetDevice(s.device));
+  flush_indenter(s);
   CUDA_TRY(cudaStreamSynchronize(s.stream));
   std::vector<double> buf;
   auto get3 = [&](const double* src, double* dst) -> int {

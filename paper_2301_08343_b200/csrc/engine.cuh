@@ -34,7 +34,7 @@ struct Ctl {
   int box_lo[2][3], box_hi[2][3];         // per-material node boxes (elastomer, indenter)
   double vind[3];                         // commanded indenter velocity
   double ind_v[3];                        // uniform indenter velocity (P2G input)
-  int call_start;                         // substep index at the start of the step() call
+  int chain_start;                        // first substep of the open indenter chain
   double diag_min_det_f, diag_max_speed;  // StepDiagnostics
   long long step_count;                   // SimState::step_count
 };
@@ -127,6 +127,13 @@ struct DeviceSim {
   std::map<int, int> graph_kernels;       // n_substeps -> kernels in graph
   int64_t kernel_launches = 0;
   int pending_start = 0;        // first substep of the in-flight step call
+  // Indenter chain: consecutive step calls with one commanded velocity; the
+  // advects of indenter particles the column walks skip stay pending (per-
+  // particle counters since Ctl::chain_start) until the chain is flushed by
+  // k_ind_catchup (velocity change, state access, 255 substeps).
+  bool chain_open = false;
+  int chain_len = 0;
+  double chain_vind[3] = {0, 0, 0};
 
   ~DeviceSim();
 };

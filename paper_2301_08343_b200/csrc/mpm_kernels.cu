@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
 // accumulate pending moves that k_ind_catchup applies (the same sequence of
 // rounded adds) before mpm::step returns.
 // ---------------------------------------------------------------------------
-__global__ void k_call_begin(Ctl* ctl) { ctl->call_start = ctl->substep; }
+__global__ void k_chain_begin(Ctl* ctl) { ctl->chain_start = ctl->substep; }
 
 constexpr int kColWarps = 8;
 
@@ -1018,7 +1018,7 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
       ghi[a] += widen;
     }
   }
-  const int target = s - ctl->call_start + (kMove ? 1 : 0);  // advects this call after this kernel
+  const int target = s - ctl->chain_start + (kMove ? 1 : 0);  // chain advects after this kernel
   double d[3] = {0, 0, 0};
   for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
   const int64_t a0 = col_start[c], a1 = col_start[c + 1];
@@ -1105,7 +1105,7 @@ __global__ void k_ind_catchup(double* __restrict__ x, int64_t n, int64_t n_el,
   pdl_wait();
   const int64_t p = n_el + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const int total = ctl->substep - ctl->call_start;  // advects that completed in this call
+  const int total = ctl->substep - ctl->chain_start;  // advects completed in the chain
   const int done = moves[p - n_el];
   if (done < total) {
     double d[3];
@@ -1759,8 +1759,8 @@ int launch_ind_move(DeviceSim& s, bool lookahead) {
 
 constexpr size_t kColSmem = sizeof(ColSmem);
 
-int launch_call_begin(DeviceSim& s) {
-  k_call_begin<<<1, 1, 0, s.stream>>>(s.ctl);
+int launch_chain_begin(DeviceSim& s) {
+  k_chain_begin<<<1, 1, 0, s.stream>>>(s.ctl);
   s.kernel_launches += 1;
   return 1;
 }
