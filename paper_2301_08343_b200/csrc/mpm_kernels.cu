@@ -24,7 +24,8 @@
 // The first substep of a call without a pending look-ahead starts with a
 // standalone scatter (k_p2g_gel_tile, k_ind_cols<false>); every substep
 // scatters the next one, so consecutive calls chain; k_ind_catchup applies
-// the advects of indenter particles the column walks did not visit. Errors
+// the advects of indenter particles the column walks did not visit once the
+// chain of same-velocity calls ends. Errors
 // are latched in Ctl::err_code with the substep they belong to; every kernel
 // of a later or equal substep exits early, reproducing the reference's
 // "state at the throwing phase".
@@ -968,7 +969,9 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
 // first particle above the box. Particles are still advected every substep in
 // exact arithmetic: the ones visited here are moved in place, the others
 // accumulate pending moves that k_ind_catchup applies (the same sequence of
-// rounded adds) before mpm::step returns.
+// rounded adds) when the chain of same-velocity step calls ends (engine.cu
+// flush_indenter: a velocity change, any access to the particle state, an
+// error, or 255 substeps).
 // ---------------------------------------------------------------------------
 __global__ void k_chain_begin(Ctl* ctl) { ctl->chain_start = ctl->substep; }
 
@@ -1098,8 +1101,8 @@ __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
 }
 
 // Applies the pending advects of the indenter particles the column walks did
-// not visit, so every particle has moved exactly (completed substeps of this
-// call) times, then resets the per-call move counters.
+// not visit, so every particle has moved exactly (completed substeps of the
+// chain) times, then resets the move counters.
 __global__ void k_ind_catchup(double* __restrict__ x, int64_t n, int64_t n_el,
                               uint8_t* __restrict__ moves, Ctl* ctl, Geometry g) {
   pdl_wait();
