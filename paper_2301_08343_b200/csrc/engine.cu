@@ -198,8 +198,6 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   g.stress_scale = -P->dt * 4.0 * g.inv_dx * g.inv_dx;
   if (const char* m = std::getenv("TACCHI_SCATTER")) g.scatter_mode = std::atoi(m);
   if (const char* f = std::getenv("TACCHI_FULL_INDENTER")) s->full_indenter = std::atoi(f) != 0;
-  g.runs = 1;
-  if (const char* f = std::getenv("TACCHI_NO_RUNS")) g.runs = std::atoi(f) != 0 ? 0 : 1;
   s->sms = sm_count(device);
 
   // Indenter particles are re-ordered by base cell so that P2G scatters from

@@ -51,7 +51,6 @@ struct Geometry {
   double stress_scale;  // -dt * 4 * inv_dx^2 (engine.cpp:114)
   int scatter_mode;     // 0: shared-memory tile (default), 1: direct RED (A/B switch)
   int* cta_box;         // per elastomer CTA: {lo[3], dim[3], ok} of its last P2G tile
-  int runs;             // run-mode elastomer scatter (TACCHI_NO_RUNS=1: 27-phase only)
 };
 
 // A dense node array in split layout: two 16-byte halves per node in two

@@ -222,19 +222,7 @@ constexpr int kGelMinBlocks = (2 * 256) / TACCHI_GEL_THREADS;
 struct P2GTile {
   double2 nlo[kTileCap];  // {m, px} / {vx, vy}
   double2 nhi[kTileCap];  // {py, pz} / vz rows (as doubles, pitch zp, offset zoff)
-  // the owner table is dead once the duplicates are known: the run-mode
-  // scatter (p2g_runs) reuses its storage
-  union {
-    int owner[kTileCap];
-    struct {
-      struct Edge {
-        int ck[3], z[3];  // lanes 0, 30, 31: column key (-1: not tiled), base z
-        double c[9][12];  // per (a, b): lane 31's C1, C2 and lane 30's C2
-      } edge[kGelThreads / 32];
-      int col_run[320];  // head thread of the run owning each (bx, by) column
-      int runs_bad;
-    } run;
-  };
+  int owner[kTileCap];
   int lo[3], hi[3], dim[3];
   int ok;
   int pitch;     // node row pitch (>= dim[2], = 1 mod 8: rows shift the 16-byte bank slot)
@@ -437,159 +425,6 @@ __device__ void tile_box(P2GTile& T, bool active, const int* base) {
   __syncthreads();
 }
 
-// One particle's contribution vector {w m, w p} to node base + (a, b, c).
-__device__ __forceinline__ void contrib(const P2GPayload& q, double m, double wab, double m0,
-                                        double m1, double m2, int c, double dx, double* o) {
-  const double dxc = (c - q.st.fx[2]) * dx;
-  const double w = wab * q.st.w[2][c];
-  o[0] = w * m;
-  o[1] = w * (m0 + q.aff[2] * dxc);
-  o[2] = w * (m1 + q.aff[5] * dxc);
-  o[3] = w * (m2 + q.aff[8] * dxc);
-}
-
-__device__ __forceinline__ void tile_add(P2GTile& T, int e, const double* v) {
-  double2 lo2 = T.nlo[e], hi2 = T.nhi[e];
-  lo2.x += v[0];
-  lo2.y += v[1];
-  hi2.x += v[2];
-  hi2.y += v[3];
-  T.nlo[e] = lo2;
-  T.nhi[e] = hi2;
-}
-
-// Run-mode tile scatter: 9 block-wide (a, b) phases instead of 27. The
-// particles of one lattice column are consecutive threads with z-ascending
-// bases 1-2 nodes apart ("runs"); in phase (a, b) each thread adds the full
-// sum of its own nodes [z, z_next) of node column (bx + a, by + b), its
-// predecessors' contributions arriving by warp shuffles (through shared
-// memory across a warp boundary). Each (bx, by) column key must belong to a
-// single run and no particle may be a duplicate; otherwise (block-uniform)
-// returns false and the caller runs the 27-phase scheme. All threads of the
-// block must call it.
-__device__ bool p2g_runs(P2GTile& T, bool active, bool tiled, const P2GPayload& q, double m,
-                         const Geometry& g, int d1, int d2, int base_idx) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const unsigned full = 0xffffffffu;
-  const int ck = tiled ? (q.st.base[0] - T.lo[0]) * d1 + (q.st.base[1] - T.lo[1]) : -1;
-  const int zb = q.st.base[2] - T.lo[2];
-  const int rows = T.dim[0] * d1;
-  __syncthreads();  // the owner table (same storage) is done
-  for (int r = tid; r < rows; r += blockDim.x) T.run.col_run[r] = -1;
-  if (tid == 0) T.run.runs_bad = 0;
-  if (lane == 0 || lane >= 30) {
-    const int slot = lane == 0 ? 0 : lane - 29;
-    T.run.edge[warp].ck[slot] = ck;
-    T.run.edge[warp].z[slot] = zb;
-  }
-  __syncthreads();
-  // links to the predecessors (lane - 1, lane - 2) of the same run
-  int ck1 = __shfl_up_sync(full, ck, 1), z1 = __shfl_up_sync(full, zb, 1);
-  int ck2 = __shfl_up_sync(full, ck, 2), z2 = __shfl_up_sync(full, zb, 2);
-  if (lane == 0) {
-    ck1 = warp > 0 ? T.run.edge[warp - 1].ck[2] : -1;
-    z1 = warp > 0 ? T.run.edge[warp - 1].z[2] : 0;
-    ck2 = warp > 0 ? T.run.edge[warp - 1].ck[1] : -1;
-    z2 = warp > 0 ? T.run.edge[warp - 1].z[1] : 0;
-  } else if (lane == 1) {
-    ck2 = warp > 0 ? T.run.edge[warp - 1].ck[2] : -1;
-    z2 = warp > 0 ? T.run.edge[warp - 1].z[2] : 0;
-  }
-  const int dz1 = zb - z1;
-  const bool link1 = tiled && ck1 == ck && (dz1 == 1 || dz1 == 2);
-  const bool link2 = link1 && dz1 == 1 && ck2 == ck && zb - z2 == 2;
-  // the successor's link decides how many nodes this thread owns
-  int lnk_n = __shfl_down_sync(full, link1 ? 1 : 0, 1), z_n = __shfl_down_sync(full, zb, 1);
-  if (lane == 31) {
-    lnk_n = 0;
-    if (warp + 1 < nw) {
-      const int ckn = T.run.edge[warp + 1].ck[0], zn = T.run.edge[warp + 1].z[0];
-      lnk_n = tiled && ckn == ck && (zn - zb == 1 || zn - zb == 2);
-      z_n = zn;
-    }
-  }
-  const int own_n = lnk_n ? z_n - zb : 3;
-  bool bad = active && !tiled;  // a duplicate base: scattered directly, breaks the runs
-  if (tiled && !link1 && atomicCAS(&T.run.col_run[ck], -1, tid) != -1) bad = true;
-  if (bad) T.run.runs_bad = 1;
-  __syncthreads();
-  if (T.run.runs_bad) return false;  // block-uniform
-  const double dx = g.dx;
-  // contributions that cross a warp boundary, for every (a, b)
-  if (lane >= 30 && warp + 1 < nw) {
-    for (int a = 0; a < 3; ++a) {
-      const double dxa = (a - q.st.fx[0]) * dx;
-      for (int b = 0; b < 3; ++b) {
-        const double dxb = (b - q.st.fx[1]) * dx;
-        const double wab = q.st.w[0][a] * q.st.w[1][b];
-        const double m0 = q.mv[0] + q.aff[0] * dxa + q.aff[1] * dxb;
-        const double m1 = q.mv[1] + q.aff[3] * dxa + q.aff[4] * dxb;
-        const double m2 = q.mv[2] + q.aff[6] * dxa + q.aff[7] * dxb;
-        double* dst = T.run.edge[warp].c[3 * a + b];
-        if (lane == 31) {
-          contrib(q, m, wab, m0, m1, m2, 1, dx, dst);
-          contrib(q, m, wab, m0, m1, m2, 2, dx, dst + 4);
-        } else {
-          contrib(q, m, wab, m0, m1, m2, 2, dx, dst + 8);
-        }
-      }
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double dxa = (a - q.st.fx[0]) * dx;
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      const double dxb = (b - q.st.fx[1]) * dx;
-      const double wab = q.st.w[0][a] * q.st.w[1][b];
-      const double m0 = q.mv[0] + q.aff[0] * dxa + q.aff[1] * dxb;
-      const double m1 = q.mv[1] + q.aff[3] * dxa + q.aff[4] * dxb;
-      const double m2 = q.mv[2] + q.aff[6] * dxa + q.aff[7] * dxb;
-      double c0[4], c1[4], c2[4], p1c1[4], p1c2[4], p2c2[4];
-      contrib(q, m, wab, m0, m1, m2, 0, dx, c0);
-      contrib(q, m, wab, m0, m1, m2, 1, dx, c1);
-      contrib(q, m, wab, m0, m1, m2, 2, dx, c2);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        p1c1[k] = __shfl_up_sync(full, c1[k], 1);
-        p1c2[k] = __shfl_up_sync(full, c2[k], 1);
-        p2c2[k] = __shfl_up_sync(full, c2[k], 2);
-      }
-      if (warp > 0 && lane < 2) {
-        const double* e = T.run.edge[warp - 1].c[3 * a + b];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (lane == 0) {
-            p1c1[k] = e[k];
-            p1c2[k] = e[4 + k];
-            p2c2[k] = e[8 + k];
-          } else {
-            p2c2[k] = e[4 + k];
-          }
-        }
-      }
-      __syncthreads();  // the previous (a, b) phase is complete
-      if (tiled) {
-        const int e0 = base_idx + (a * d1 + b) * d2;
-        double n0[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          n0[k] = c0[k] + (link1 ? (dz1 == 1 ? p1c1[k] : p1c2[k]) : 0.0) + (link2 ? p2c2[k] : 0.0);
-        tile_add(T, e0, n0);
-        if (own_n >= 2) {
-          double n1[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) n1[k] = c1[k] + (link1 && dz1 == 1 ? p1c2[k] : 0.0);
-          tile_add(T, e0 + 1, n1);
-        }
-        if (own_n >= 3) tile_add(T, e0 + 2, c2);
-      }
-    }
-  }
-  return true;
-}
-
 // CTA-cooperative scatter. All threads of the block must call it.
 // Phase (a,b,c) adds each particle's contribution to node base + (a,b,c);
 // two particles of the CTA collide in a phase only if they share a base cell,
@@ -636,13 +471,6 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
     if (!tiled) scatter_direct(g, grid, m, q);
   }
   if (!use_tile) return;  // block-uniform
-  if (g.runs && g.scatter_mode == 0 && T.dim[0] * d1 <= 320 &&
-      p2g_runs(T, active, tiled, q, m, g, d1, d2, base_idx)) {
-    fence_proxy_async();
-    __syncthreads();
-    tile_bulk_reduce(T, g, grid);
-    return;
-  }
   const double dx = g.dx;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -1750,7 +1578,6 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 constexpr int kThreads = 256;
 constexpr size_t kTileSmem = sizeof(P2GTile);
 static_assert(sizeof(ColSmem) <= sizeof(P2GTile), "indenter blocks reuse the tile's shared memory");
-static_assert(sizeof(P2GTile::run) <= sizeof(int) * kTileCap, "run-mode data fits the owner table");
 static_assert(kGelThreads == kColWarps * 32, "indenter blocks of the elastomer kernel: 8 warps");
 constexpr size_t kIndSmem = sizeof(IndSmem);
 
