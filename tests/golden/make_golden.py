@@ -53,7 +53,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import refpy as R  # noqa: E402
-from tests.scenes import (BAD_CONFIGS, CONFIG1_DEEP_STEPS, HARNESS, PARTS, PARTS_STEPS, PARTS_V, CONFIG1, CONFIG5, CONFIG5_MOVE, CONFIG5_PRESS, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
+from tests.scenes import (BAD_CONFIGS, CONFIG1_DEEP_STEPS, HARNESS, PARTS, PARTS_STEPS, PARTS_V, CONFIG1, CONFIG2B, CONFIG2B_PRESS, CONFIG2B_SLIDE, CONFIG5, CONFIG5_MOVE, CONFIG5_PRESS, bridge_script, CONFIG1_STEPS, CONFIG1_V, LIGHT_CFG, PLACED_ROT, SHAPES,  # noqa: E402
                           SMALL, SMALL3, SMALL3_PRESS, SMALL3_SHAPES, SMALL3_SLIDE, SMALL_STEPS,
                           SMALL_V, render_inputs, sha)
 
@@ -199,6 +199,25 @@ def config5():
         x_surface=s1["x"][surf["particle"]][::7], min_det_f=d["min_det_f"],
         max_speed=d["max_speed"], step_count=d["step_count"], image=img,
         depth_sample=depth[::16, ::16])
+
+
+def config2b():
+    sim = R.RefSim.from_config(CONFIG2B, "", threads=0)
+    s0 = sim.state()
+    sim.step(CONFIG2B_PRESS[1], CONFIG2B_PRESS[0])
+    sim.step(CONFIG2B_SLIDE[1], CONFIG2B_SLIDE[0])
+    s1 = sim.state()
+    d = sim.diag()
+    depth, img = sim.capture(CONFIG2B)
+    surf = sim.surface()
+    rng = np.random.default_rng(6)
+    subset = np.sort(rng.choice(sim.n, 4096, replace=False))
+    np.savez_compressed(
+        os.path.join(OUT, "config2b.npz"), n=sim.n, n_elastomer=sim.n_elastomer,
+        x0_hash=sha(s0["x"]), subset=subset, x_subset=s1["x"][subset],
+        F_subset=s1["F"][subset], x_surface=s1["x"][surf["particle"]][::7],
+        min_det_f=d["min_det_f"], max_speed=d["max_speed"], step_count=d["step_count"],
+        image=img, depth_sample=depth[::16, ::16])
 
 
 def harness():
@@ -371,7 +390,9 @@ def bridge():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "bridge", "harness", "parts", "background", "clouds"]
+    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "config2b", "bridge", "harness", "parts", "background", "clouds"]
+    if "config2b" in which:
+        config2b()
     if "config5" in which:
         config5()
     if "config1_deep" in which:

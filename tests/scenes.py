@@ -32,6 +32,16 @@ CONFIG1_DEEP_STEPS = 10000
 CONFIG2A = {"time": {"dt_s": 2e-6}, "indenter": {"target_points": 1000000}}
 CONFIG2A_V = (0.0, 0.0, -0.01)
 
+# Config 2b (BASELINE.json configs[2]): isotropic 0.1176 mm gel spacing,
+# 171 x 171 x 35 = 1,023,435 gel particles + sphere 1e5 = 1,123,435. The gel
+# spacing is 0.91 grid cells, so about a quarter of the gel particles share a
+# base cell with a neighbour (the scatter's duplicate path). Parity slice:
+# gap 2 um, press at 0.3 m/s, then slide while pressed.
+CONFIG2B = {"elastomer": {"particle_counts": [171, 171, 35]}, "time": {"dt_s": 2e-6},
+            "indenter": {"gap_mm": 0.002}}
+CONFIG2B_PRESS = (40, (0.0, 0.0, -0.3))
+CONFIG2B_SLIDE = (20, (0.2, -0.1, 0.0))
+
 SUBSTEPS_PER_FRAME = 10  # scene_config.hpp:36, session.cpp:86
 
 # Config 5 (BASELINE.json configs[4]): large-area gel 40 x 40 x 4 mm at the

@@ -414,6 +414,37 @@ def test_config5_large_gel_matches_reference(tb, golden):
     assert np.abs(img.astype(int) - g["image"]).max() <= 2
 
 
+def test_config2b_dense_gel_matches_reference(tb, golden):
+    """Config 2b (171 x 171 x 35 gel at 0.91 grid cells spacing + sphere 1e5,
+    1,123,435 particles): a quarter of the gel particles share a base cell, so
+    the scatter's duplicate path carries real load. Press then slide vs the
+    reference (tests/scenes.py CONFIG2B)."""
+    from tests.scenes import CONFIG2B, CONFIG2B_PRESS, CONFIG2B_SLIDE
+
+    g = golden("config2b.npz")
+    s = tb.sim.build_sim(CONFIG2B)
+    assert s.n == int(g["n"]) and s.elastomer_count == int(g["n_elastomer"])
+    x0 = s.positions()
+    assert sha(x0) == str(g["x0_hash"])
+    tb.mpm.step(s, CONFIG2B_PRESS[1], CONFIG2B_PRESS[0])
+    tb.mpm.step(s, CONFIG2B_SLIDE[1], CONFIG2B_SLIDE[0])
+    st = s.state()
+    sub = g["subset"]
+    disp = np.abs(g["x_subset"] - x0[sub]).max()
+    assert disp > 1e-5
+    assert np.abs(st["x"][sub] - g["x_subset"]).max() <= 1e-8 * disp
+    surf = _default_surface(171, 171, 35)[::7]
+    assert np.abs(st["x"][surf] - g["x_surface"]).max() <= 1e-8 * disp
+    np.testing.assert_allclose(st["F"][sub], g["F_subset"], rtol=0, atol=1e-11)
+    d = s.diag
+    assert d.step_count == int(g["step_count"])
+    assert d.min_det_f == pytest.approx(float(g["min_det_f"]), abs=1e-12)
+    assert d.max_speed == pytest.approx(float(g["max_speed"]), rel=1e-9)
+    depth, img = tb.sim.capture(s, CONFIG2B)
+    assert np.abs(depth[::16, ::16] - g["depth_sample"]).max() <= 1e-7
+    assert np.abs(img.astype(int) - g["image"]).max() <= 2
+
+
 @pytest.mark.parametrize("with_surface", [True, False])
 def test_init_scene_parts_gravity_nonuniform_indenter(tb, golden, with_surface):
     """mpm::init_scene from explicit arrays (tests/scenes.py PARTS) with gravity,

@@ -1,6 +1,6 @@
 """Throughput of the step + capture frame on each BASELINE.json config shape
 (one episode per GPU): config 1 (default gel, sphere 1e5), config 2a (sphere
-1e6), config 3 (default gel, cylinder / ring / wave / dot-grid indenters,
+1e6), config 2b (171 x 171 x 35 gel), config 3 (default gel, cylinder / ring / wave / dot-grid indenters,
 1e5 points), config 5 (large-area gel on 512^3). Prints one JSON line each.
 
     python tools/bench_configs.py [--frames F]
@@ -17,11 +17,12 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_2301_08343_b200 as tb  # noqa: E402
-from tests.scenes import CONFIG1, CONFIG2A, CONFIG5, SUBSTEPS_PER_FRAME  # noqa: E402
+from tests.scenes import CONFIG1, CONFIG2A, CONFIG2B, CONFIG5, SUBSTEPS_PER_FRAME  # noqa: E402
 
 CASES = [
     ("config1", CONFIG1, "", (0.0, 0.0, -0.01)),
     ("config2a", CONFIG2A, "", (0.0, 0.0, -0.01)),
+    ("config2b", CONFIG2B, "", (0.0, 0.0, -0.01)),
     ("config3-cylinder", CONFIG1, "cylinder", (0.0, 0.0, -0.01)),
     ("config3-ring", CONFIG1, "cylinder_shell", (0.0, 0.0, -0.01)),
     ("config3-wave", CONFIG1, "wave1", (0.0, 0.0, -0.01)),
