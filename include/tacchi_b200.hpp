@@ -196,6 +196,38 @@ inline Capture step_capture(mpm::SimState& s, const Vec3& indenter_velocity, int
   return c;
 }
 
+// Batched control step over independent episodes (config 4): every state
+// steps with its velocity and is captured, all submitted before any wait.
+// Throws the first failing episode's error after all were processed.
+inline std::vector<Capture> step_capture_many(std::vector<mpm::SimState*>& states,
+                                              const std::vector<Vec3>& velocities,
+                                              int n_substeps, const std::string& config_json,
+                                              const std::string& object) {
+  tg_render r;
+  check(tg_render_from_config(config_json.c_str(), object.c_str(), &r));
+  const size_t n = states.size();
+  std::vector<Capture> out(n);
+  std::vector<tg_handle> hs(n);
+  std::vector<double> v(3 * n);
+  std::vector<double*> dp(n);
+  std::vector<uint8_t*> cp(n);
+  for (size_t i = 0; i < n; ++i) {
+    Capture& c = out[i];
+    c.depth.width = c.image.width = r.width;
+    c.depth.height = c.image.height = r.height;
+    c.depth.pixel_to_meter = r.pixel_to_meter * r.crop_scale;
+    c.depth.values.resize(static_cast<size_t>(r.width) * r.height);
+    c.image.data.resize(static_cast<size_t>(r.width) * r.height * 3);
+    hs[i] = states[i]->handle();
+    for (int a = 0; a < 3; ++a) v[3 * i + a] = velocities[i][a];
+    dp[i] = c.depth.values.data();
+    cp[i] = c.image.data.data();
+  }
+  check(tg_step_capture_many(hs.data(), static_cast<int>(n), v.data(), n_substeps, &r, 1,
+                             dp.data(), cp.data(), nullptr));
+  return out;
+}
+
 }  // namespace sim
 
 // ---- bridge (server.hpp:13-40), dataset (harness.hpp), metrics ------------

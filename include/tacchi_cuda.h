@@ -210,6 +210,16 @@ int tg_phong_render(int device, const double* depth, int w, int hgt, double r,
  * launches (one stream each, submitted back to back). */
 int tg_step_many(tg_handle* hs, int n_handles, const double* velocities /* n x 3 */,
                  int n_substeps);
+/* Batched control step (config 4 / the harness's capture levels): for every
+ * handle mpm::step(v_i, n_substeps) then sim::capture with renders[i] (or
+ * renders[0] when n_renders == 1), all submitted before any wait. depth_outs /
+ * rgb_outs: n pointers each (or NULL), entries as tg_capture's outputs (NULL =
+ * not read back). status (optional, n ints) receives each handle's code; the
+ * return value is the first failing handle's, with its message. A failing
+ * handle does not stop the others. n_substeps <= 200 (the harness's chunk). */
+int tg_step_capture_many(tg_handle* hs, int n_handles, const double* velocities /* n x 3 */,
+                         int n_substeps, const tg_render* renders, int n_renders,
+                         double** depth_outs, uint8_t** rgb_outs, int* status);
 
 /* ---- runtime ------------------------------------------------------------ */
 

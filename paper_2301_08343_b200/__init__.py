@@ -99,7 +99,7 @@ EXPORTED = [
     "tg_create", "tg_build_sim", "tg_destroy", "tg_step", "tg_phase", "tg_num_particles",
     "tg_num_elastomer", "tg_download", "tg_upload", "tg_diag", "tg_grid_window",
     "tg_download_grid", "tg_render_from_config", "tg_capture", "tg_extract_depth",
-    "tg_crop_align", "tg_surface_normals", "tg_phong_render", "tg_step_many", "tg_sync",
+    "tg_crop_align", "tg_surface_normals", "tg_phong_render", "tg_step_many", "tg_step_capture_many", "tg_sync",
     "tg_stream", "tg_kernel_launches", "tg_set_graphs", "tg_last_error", "tg_version",
     "tg_generate_cloud", "tg_placed_indenter", "tg_time_phases",
 ]
@@ -149,6 +149,10 @@ def lib():
         L.tg_phong_render.argtypes = [C.c_int, _dp, C.c_int, C.c_int, C.c_double,
                                       C.POINTER(TgRender), _u8p]
         L.tg_step_many.argtypes = [C.POINTER(C.c_void_p), C.c_int, _dp, C.c_int]
+        L.tg_step_capture_many.argtypes = [C.POINTER(C.c_void_p), C.c_int, _dp, C.c_int,
+                                           C.POINTER(TgRender), C.c_int,
+                                           C.POINTER(_dp), C.POINTER(_u8p),
+                                           C.POINTER(C.c_int)]
         L.tg_sync.argtypes = [C.c_void_p]
         L.tg_stream.argtypes = [C.c_void_p]
         L.tg_stream.restype = C.c_void_p
@@ -477,6 +481,39 @@ class sim:  # noqa: N801 — mirrors tacchi::sim
         _check(lib().tg_step_capture(state.handle, _p(_vec(indenter_velocity)), int(n_substeps),
                                      C.byref(rp), _p(depth), _p(img, _u8p)))
         return depth, img
+
+
+    @staticmethod
+    def step_capture_many(states, velocities, n_substeps: int, params, want_depth: bool = True,
+                          want_image: bool = True):
+        """Batched control step (tg_step_capture_many): every state steps with
+        its velocity row and is captured with `params` (one TgRender for all,
+        or one per state); all submitted before any wait. Returns
+        (outputs, status): outputs[i] = (depth, image) (None where not
+        wanted), status[i] = the handle's error code (0 = OK). Raises the
+        first failing handle's error after every handle was processed."""
+        n = len(states)
+        ps = list(params) if isinstance(params, (list, tuple)) else [params]
+        if len(ps) not in (1, n):
+            raise ValueError("params: one TgRender or one per state")
+        renders = (TgRender * len(ps))(*ps)
+        v = _d(velocities, (n, 3))
+        outs, dptr, iptr = [], (_dp * n)(), (_u8p * n)()
+        for i in range(n):
+            rp = ps[0] if len(ps) == 1 else ps[i]
+            d = np.empty((rp.height, rp.width)) if want_depth else None
+            im = np.empty((rp.height, rp.width, 3), np.uint8) if want_image else None
+            dptr[i] = _p(d)
+            iptr[i] = _p(im, _u8p)
+            outs.append((d, im))
+        hs = (C.c_void_p * n)(*[s.handle.value for s in states])
+        status = (C.c_int * n)()
+        rc = lib().tg_step_capture_many(hs, n, _p(v), int(n_substeps), renders, len(ps), dptr,
+                                        iptr, status)
+        st = list(status)
+        if rc:
+            _check(rc)
+        return outs, st
 
 
 class geo:  # noqa: N801 — mirrors tacchi::geo (host setup)

@@ -875,20 +875,68 @@ int tg_phong_render(int device, const double* depth, int w, int hgt, double r,
   return rc ? fail(rc, msg) : TG_OK;
 }
 
+// Submits every handle's work before waiting on any of them; a handle whose
+// submission fails is still accounted for, the others are finished normally.
+// Returns the first failing handle's code and message; per-handle codes go to
+// `status` when given.
+static int many(tg_handle* hs, int n_handles, const double* velocities, int n_substeps,
+                const tg_render* renders, int n_renders, double** depth_outs,
+                uint8_t** rgb_outs, int* status, const char* who) {
+  if (!hs || !velocities || n_handles < 0)
+    return fail(TG_ERR_INVALID_ARGUMENT, std::string(who) + ": null argument");
+  if (n_substeps < 0 || n_substeps > 200)
+    return fail(TG_ERR_INVALID_ARGUMENT, std::string(who) + ": n_substeps outside [0, 200]");
+  for (int i = 0; i < n_handles; ++i)
+    if (!hs[i]) return fail(TG_ERR_INVALID_ARGUMENT, std::string(who) + ": null handle");
+  std::vector<int> rc(n_handles, TG_OK), crc(n_handles, TG_OK);
+  std::vector<std::string> msg(n_handles);
+  std::vector<char> submitted(n_handles, 0);
+  for (int i = 0; i < n_handles; ++i) {
+    DeviceSim& s = *H(hs[i]);
+    rc[i] = tacchi_b200::step_submit(s, velocities + 3 * i, n_substeps);
+    if (rc[i]) {
+      msg[i] = g_last_error;
+      continue;
+    }
+    submitted[i] = 1;
+    if (renders) {
+      const tg_render& r = renders[n_renders == 1 ? 0 : i];
+      crc[i] = tacchi_b200::capture_enqueue(s, r, depth_outs && depth_outs[i],
+                                            rgb_outs && rgb_outs[i], msg[i]);
+    }
+  }
+  int first = -1;
+  for (int i = 0; i < n_handles; ++i) {
+    if (submitted[i]) {
+      DeviceSim& s = *H(hs[i]);
+      rc[i] = tacchi_b200::step_finish(s, n_substeps);  // the step's error wins
+      if (rc[i]) {
+        msg[i] = g_last_error;
+      } else if (crc[i]) {
+        rc[i] = crc[i];
+      } else if (renders) {
+        tacchi_b200::capture_collect(s, depth_outs ? depth_outs[i] : nullptr,
+                                     rgb_outs ? rgb_outs[i] : nullptr);
+      }
+    }
+    if (status) status[i] = rc[i];
+    if (rc[i] && first < 0) first = i;
+  }
+  return first < 0 ? TG_OK : fail(rc[first], msg[first]);
+}
+
 int tg_step_many(tg_handle* hs, int n_handles, const double* velocities, int n_substeps) {
-  if (!hs || !velocities) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_many: null argument");
-  // Submit every handle's graph before waiting on any of them.
-  if (n_substeps > 200) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_many: n_substeps > 200");
-  for (int i = 0; i < n_handles; ++i) {
-    const int rc = tacchi_b200::step_submit(*H(hs[i]), velocities + 3 * i, n_substeps);
-    if (rc) return rc;
-  }
-  int first = TG_OK;
-  for (int i = 0; i < n_handles; ++i) {
-    const int rc = tacchi_b200::step_finish(*H(hs[i]), n_substeps);
-    if (rc && !first) first = rc;
-  }
-  return first;
+  return many(hs, n_handles, velocities, n_substeps, nullptr, 0, nullptr, nullptr, nullptr,
+              "tg_step_many");
+}
+
+int tg_step_capture_many(tg_handle* hs, int n_handles, const double* velocities, int n_substeps,
+                         const tg_render* renders, int n_renders, double** depth_outs,
+                         uint8_t** rgb_outs, int* status) {
+  if (!renders || (n_renders != 1 && n_renders != n_handles))
+    return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture_many: renders must hold 1 or n entries");
+  return many(hs, n_handles, velocities, n_substeps, renders, n_renders, depth_outs, rgb_outs,
+              status, "tg_step_capture_many");
 }
 
 int tg_sync(tg_handle h) {

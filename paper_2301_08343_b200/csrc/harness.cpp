@@ -333,13 +333,27 @@ DatasetResult run_press_dataset(const std::string& cfg_json, const fs::path& out
         vel[3 * i + 1] = 0.0;
         vel[3 * i + 2] = -v;
       }
-      auto capture_levels = [&](const std::vector<int>& levels) {
+      // The chunk that reaches a capture level is submitted together with
+      // every handle's capture (tg_step_capture_many: one wait per handle).
+      std::vector<tg_render> rs(nb);
+      for (size_t i = 0; i < nb; ++i) rs[i] = renders.at(jobs[b0 + i].object);
+      auto step_and_capture = [&](int n, const std::vector<int>& levels) {
+        std::vector<std::shared_ptr<std::vector<double>>> depth(nb);
+        std::vector<std::shared_ptr<std::vector<uint8_t>>> rgb(nb);
+        std::vector<double*> dp(nb);
+        std::vector<uint8_t*> cp(nb);
+        for (size_t i = 0; i < nb; ++i) {
+          const size_t px = static_cast<size_t>(rs[i].width) * rs[i].height;
+          depth[i] = std::make_shared<std::vector<double>>(px);
+          rgb[i] = std::make_shared<std::vector<uint8_t>>(px * 3);
+          dp[i] = depth[i]->data();
+          cp[i] = rgb[i]->data();
+        }
+        check(tg_step_capture_many(hs.data(), static_cast<int>(nb), vel.data(), n, rs.data(),
+                                   static_cast<int>(nb), dp.data(), cp.data(), nullptr));
         for (size_t i = 0; i < nb; ++i) {
           const PositionJob& job = jobs[b0 + i];
-          const tg_render& r = renders.at(job.object);
-          auto depth = std::make_shared<std::vector<double>>(static_cast<size_t>(r.width) * r.height);
-          auto rgb = std::make_shared<std::vector<uint8_t>>(static_cast<size_t>(r.width) * r.height * 3);
-          check(tg_capture(hs[i], &r, depth->data(), rgb->data()));
+          const tg_render& r = rs[i];
           for (int k : levels) {
             ManifestRow row;
             row.object = job.object;
@@ -357,9 +371,9 @@ DatasetResult run_press_dataset(const std::string& cfg_json, const fs::path& out
             const std::string dep = (out_dir / row.depth_map).string();
             const int w = r.width, h = r.height;
             const double ptm = r.pixel_to_meter * r.crop_scale;
-            writers.submit([png, dep, w, h, ptm, depth, rgb] {
-              host::save_png(png, w, h, rgb->data());
-              host::save_depth_map(dep, w, h, ptm, depth->data());
+            writers.submit([png, dep, w, h, ptm, d = depth[i], c = rgb[i]] {
+              host::save_png(png, w, h, c->data());
+              host::save_depth_map(dep, w, h, ptm, d->data());
             });
             std::lock_guard<std::mutex> lk(rows_mutex);
             fresh.push_back(std::move(row));
@@ -368,12 +382,12 @@ DatasetResult run_press_dataset(const std::string& cfg_json, const fs::path& out
       };
       int64_t cur = 0;
       for (const auto& [s, levels] : schedule) {
-        while (cur < s) {
-          const int n = static_cast<int>(std::min<int64_t>(200, s - cur));
-          check(tg_step_many(hs.data(), static_cast<int>(nb), vel.data(), n));
-          cur += n;
+        while (s - cur > 200) {
+          check(tg_step_many(hs.data(), static_cast<int>(nb), vel.data(), 200));
+          cur += 200;
         }
-        capture_levels(levels);
+        step_and_capture(static_cast<int>(s - cur), levels);
+        cur = s;
       }
     }
   } catch (...) {

@@ -240,6 +240,36 @@ def test_degenerate_f_leaves_state_at_failing_substep(tb):
         tb.mpm.step(s, SMALL_V, 1)
 
 
+def test_step_capture_many_matches_single_handles(tb):
+    """tg_step_capture_many (every handle submitted before any wait) == one
+    tg_step_capture per handle; per-handle status, and a failing handle
+    (OutOfGrid, the out-of-grid setup below) does not stop the others."""
+    rp = tb.render_params(SMALL, "")
+    vs = np.array([SMALL_V, (0.002, 0.0, -0.04), (0.0, -0.003, -0.02)])
+    batch = [tb.sim.build_sim(SMALL) for _ in vs]
+    single = [tb.sim.build_sim(SMALL) for _ in vs]
+    for _ in range(3):
+        outs, status = tb.sim.step_capture_many(batch, vs, 10, rp)
+        assert status == [0, 0, 0]
+        for s, v, (d, im) in zip(single, vs, outs):
+            ds, ims = tb.sim.step_capture(s, v, 10, params=rp)
+            np.testing.assert_allclose(d, ds, rtol=0, atol=1e-12)
+            assert np.abs(im.astype(int) - ims).max() <= 1
+    outs, status = tb.sim.step_capture_many(batch, vs, 5, [rp] * 3, want_depth=False)
+    assert all(d is None and im is not None for d, im in outs)
+    # handle 1 runs out of the grid; 0 and 2 still step and capture
+    x = batch[1].positions()
+    x[-1, 2] = (64 - 3) * (12e-3 / 64) + 0.49 * (12e-3 / 64)
+    batch[1].set_state(x=x)
+    before = [s.step_count for s in batch]
+    up = vs.copy()
+    up[1] = (0.0, 0.0, 1.0)
+    with pytest.raises(tb.OutOfGrid):
+        tb.sim.step_capture_many(batch, up, 200, rp)
+    assert batch[0].step_count == before[0] + 200 and batch[2].step_count == before[2] + 200
+    assert before[1] < batch[1].step_count < before[1] + 200
+
+
 def test_out_of_grid_after_advect(tb):
     s = tb.sim.build_sim(SMALL)
     x = s.positions()

@@ -1,7 +1,7 @@
 """Batched independent episodes on one GPU:
 K config-1 episodes with the config-4 pose draws (episodes.make_episode),
-stepped together with tg_step_many (every handle's substep graph submitted
-before any wait) and captured every frame. Prints one JSON line per K.
+stepped and captured together with tg_step_capture_many (every handle's
+substep graph and capture submitted before any wait), every frame. Prints one JSON line per K.
 
     python tools/bench_batch.py [K ...] [--frames F] [--warmup W]
 
@@ -36,9 +36,8 @@ def run(k, frames, warmup):
     v = np.tile(np.asarray(CONFIG1_V, dtype=np.float64), (k, 1))
 
     def frame():
-        tb.mpm.step_many(sims, v, SUBSTEPS_PER_FRAME)
-        for s in sims:
-            tb.sim.capture(s, params=rp, want_depth=False, want_image=False)
+        tb.sim.step_capture_many(sims, v, SUBSTEPS_PER_FRAME, rp, want_depth=False,
+                                 want_image=False)
 
     for _ in range(warmup):
         frame()
@@ -52,7 +51,7 @@ def run(k, frames, warmup):
     n = sims[0].n
     units = float(n) * k * SUBSTEPS_PER_FRAME * frames
     return {"workload": f"config4-style: {k} x config1 ({n} particles each), 10 substeps + capture "
-                        "per frame, tg_step_many",
+                        "per frame, tg_step_capture_many",
             "episodes": k, "frames": frames, "ms": ms,
             "particle_substeps_per_s": units / (ms * 1e-3),
             "episode_frames_per_s": k * frames / (ms * 1e-3)}
