@@ -290,10 +290,30 @@ def cpu_baseline(frames: int = 2):
     sim.capture(CONFIG2A)
     cap = time.perf_counter() - t1
     n = sim.n
+    del sim
+    # the same engine on one thread (nproc and 1), 2 substeps
+    one = refpy.RefSim.from_config(CONFIG2A, "", threads=1)
+    one.step(CONFIG2A_V, 1)
+    t2 = time.perf_counter()
+    one.step(CONFIG2A_V, 2)
+    dt1 = time.perf_counter() - t2
     return {"value": n * SUBSTEPS_PER_FRAME * frames / dt, "unit": UNIT, "cores": threads,
-            "kind": "reference", "capture_ms": cap * 1e3,
+            "kind": "reference", "capture_ms": cap * 1e3, "value_1_thread": n * 2 / dt1,
+            "cpu_model": _cpu_model(),
             "sample": f"{frames * SUBSTEPS_PER_FRAME} substeps of config2a ({n} particles), "
-                      f"mpm::step wall time, OMP threads={threads}"}
+                      f"mpm::step wall time, OMP threads={threads}; value_1_thread: 2 "
+                      f"substeps on one thread"}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 REF_BUDGET_S = 90.0
@@ -337,6 +357,7 @@ def run_reference(args):
         "config": {"workload": WORKLOAD, "particles_per_gpu": n, "substeps_per_step": SUBSTEPS_PER_FRAME},
         "frames_per_sec": steps / dt,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "cpu_model": _cpu_model(),
                          "sample": f"{steps} frames (10 substeps + capture) of config2a "
                                    f"(of {args.steps} requested; {REF_BUDGET_S:.0f} s budget), "
                                    f"OMP threads={threads}"},
