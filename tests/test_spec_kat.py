@@ -1,0 +1,304 @@
+"""The reference's specified known-answer tests (SPEC.md examples and
+invariants: the reference ships them as empty stubs) run
+on the CUDA path through the C-ABI. Needs a B200: `pytest -m gpu`.
+
+Scenes are built with mpm::init_scene from explicit arrays on a grid of
+dx = 2^-10 m, so node positions and B-spline fractions are exact binary
+numbers and the closed forms below hold to rounding.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+DX = 2.0 ** -10
+RES = (32, 32, 32)
+E, NU = 1.45e5, 0.45
+MU = E / (2 * (1 + NU))
+LAM = E * NU / ((1 + NU) * (1 - 2 * NU))
+
+
+@pytest.fixture(scope="module")
+def tb():
+    import paper_2301_08343_b200 as tb
+
+    return tb
+
+
+def _scene(tb, x_el, v_el=None, C_el=None, F_el=None, tag_el=None, x_ind=None, dt=1e-5,
+           m_el=1e-3, vol_el=1e-9, m_ind=1.0, indenter_velocity=(0, 0, 0)):
+    """Elastomer particles x_el (+ one far indenter particle unless x_ind)."""
+    x_el = np.atleast_2d(np.asarray(x_el, float))
+    ne = len(x_el)
+    if x_ind is None:
+        x_ind = np.array([[4.3, 4.3, 4.3]]) * DX  # stencil nodes 3..5, far from the gel
+    x_ind = np.atleast_2d(np.asarray(x_ind, float))
+    n = ne + len(x_ind)
+    v = np.zeros((n, 3))
+    if v_el is not None:
+        v[:ne] = v_el
+    Cm = np.zeros((n, 9))
+    if C_el is not None:
+        Cm[:ne] = np.asarray(C_el, float).reshape(-1, 9)
+    F = np.tile(np.eye(3).ravel(), (n, 1))
+    if F_el is not None:
+        F[:ne] = np.asarray(F_el, float).reshape(-1, 9)
+    tag = np.full(n, 2, np.uint8)
+    tag[:ne] = 0 if tag_el is None else tag_el
+    mass = np.concatenate([np.full(ne, m_el), np.full(len(x_ind), m_ind)])
+    vol = np.concatenate([np.full(ne, vol_el), np.full(len(x_ind), 1e-9)])
+    params = dict(res=RES, dx=DX, origin=(0, 0, 0), dt=dt, E=E, nu=NU)
+    parts = dict(x=np.vstack([x_el, x_ind]), v=v, C=Cm, F=F, mass=mass, volume0=vol, tag=tag,
+                 n_elastomer=ne, indenter_velocity=indenter_velocity)
+    return tb.init_scene(params, parts)
+
+
+def _p2g(tb, s):
+    tb.mpm.zero_grid(s)
+    tb.mpm.particle_to_grid(s)
+    lo, hi = s.grid_window()
+    m, mom, _ = s.grid(lo, hi)
+    return lo, m, mom
+
+
+def test_bspline_weights_at_a_node_center(tb):
+    """SPEC bspline_weights / particle_to_grid examples: a particle exactly at
+    a node centre -> per-axis weights (0.125, 0.75, 0.125); with v = (1,0,0),
+    C = 0, F = I the centre node's momentum is 0.75^3 m (1, 0, 0)."""
+    node = np.array([16, 15, 17])
+    m = 1e-3
+    s = _scene(tb, node * DX, v_el=[1.0, 0.0, 0.0], m_el=m)
+    lo, M, MG = _p2g(tb, s)
+    w = np.array([0.125, 0.75, 0.125])
+    for a in range(3):
+        for b in range(3):
+            for c in range(3):
+                i = tuple(node + (a - 1, b - 1, c - 1) - lo)
+                assert M[i] == pytest.approx(w[a] * w[b] * w[c] * m, rel=1e-15)
+    ctr = tuple(node - lo)
+    np.testing.assert_allclose(MG[ctr], [0.75 ** 3 * m, 0, 0], rtol=1e-15, atol=0)
+    assert M.sum() == pytest.approx(m + 1.0, rel=1e-14)
+    # the particle halfway between two nodes in x: x-weights (0.5, 0.5, 0)
+    s2 = _scene(tb, (node + (0.5, 0, 0)) * DX, m_el=m)
+    lo2, M2, _ = _p2g(tb, s2)
+    row = M2[:, node[1] - lo2[1], node[2] - lo2[2]] / (0.75 * 0.75 * m)
+    got = row[row > 0]
+    np.testing.assert_allclose(np.sort(got)[::-1][:2], [0.5, 0.5], rtol=1e-15)
+
+
+def _stress_from_momentum(MG, fx_nodes, k):
+    """Solves MG_i = w_i k S (X_i - x_p) for S over the 27 stencil nodes."""
+    rows, rhs = [], []
+    for (i, w, d) in fx_nodes:
+        rows.append(w * k * d)
+        rhs.append(MG[i])
+    A = np.array(rows)  # 27 x 3
+    Y = np.array(rhs)   # 27 x 3
+    St, *_ = np.linalg.lstsq(A, Y, rcond=None)
+    return St.T
+
+
+@pytest.mark.parametrize("case", ["identity", "rotation", "stretch"])
+def test_corotated_stress_known_answers(tb, case):
+    """SPEC compute_stress examples through P2G (v = 0, C = 0): the momentum a
+    particle scatters is w_i (-dt 4/dx^2 V0) S (X_i - x_p). F = I -> S = 0;
+    F = rotation -> S = 0 within 1e-9; F = diag(0.9, 1, 1) -> the corotated
+    formula (R = I) to 1e-10 relative."""
+    node = np.array([16, 16, 16])
+    x = (node + 0.25) * DX  # fx = 1.25 per axis
+    if case == "identity":
+        F = np.eye(3)
+    elif case == "rotation":
+        t = 0.3
+        F = np.array([[np.cos(t), -np.sin(t), 0], [np.sin(t), np.cos(t), 0], [0, 0, 1]])
+        F = F @ np.array([[1, 0, 0], [0, np.cos(0.2), -np.sin(0.2)], [0, np.sin(0.2), np.cos(0.2)]])
+    else:
+        F = np.diag([0.9, 1.0, 1.0])
+    dt, vol = 1e-5, 1e-9
+    s = _scene(tb, x, F_el=F, dt=dt, vol_el=vol)
+    lo, M, MG = _p2g(tb, s)
+    fx = 1.25
+    w1 = [0.5 * (1.5 - fx) ** 2, 0.75 - (fx - 1) ** 2, 0.5 * (fx - 0.5) ** 2]
+    base = np.floor(x / DX - 0.5).astype(int)  # 15: fx = 1.25 per axis
+    nodes = []
+    for a in range(3):
+        for b in range(3):
+            for c in range(3):
+                i = tuple(base + (a, b, c) - lo)
+                d = (np.array([a, b, c]) - fx) * DX
+                nodes.append((i, w1[a] * w1[b] * w1[c], d))
+    k = -dt * 4 / DX ** 2 * vol
+    S = _stress_from_momentum(MG, nodes, k)
+    if case == "identity":
+        assert np.abs(MG).max() == 0.0
+    elif case == "rotation":
+        assert np.abs(S).max() < 1e-9
+    else:
+        J = 0.9
+        expect = 2 * MU * (F - np.eye(3)) @ F.T + LAM * (J - 1) * J * np.eye(3)
+        np.testing.assert_allclose(S, expect, rtol=1e-10, atol=1e-10 * np.abs(expect).max())
+
+
+def _block(n=6, spacing=0.6, origin=(12.3, 12.1, 12.2)):
+    g = np.stack(np.meshgrid(*[np.arange(n)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    return (np.asarray(origin) + spacing * g) * DX
+
+
+def test_p2g_conserves_mass_and_momentum_random_particles(tb):
+    """SPEC invariants: 1000 random in-range particles, zero stress -> sum of
+    node mass = sum m (1e-10) and sum of node momentum = sum m v (1e-10)."""
+    rng = np.random.default_rng(7)
+    x = (10 + 10 * rng.random((1000, 3))) * DX
+    v = rng.standard_normal((1000, 3))
+    s = _scene(tb, x, v_el=v, m_el=1e-3)
+    st = s.state()
+    assert np.array_equal(st["x"][:1000], x)
+    lo, M, MG = _p2g(tb, s)
+    total = 1000 * 1e-3 + 1.0
+    assert M.sum() == pytest.approx(total, rel=1e-10)
+    pm = (1e-3 * v).sum(0)
+    np.testing.assert_allclose(MG.reshape(-1, 3).sum(0), pm, rtol=1e-10,
+                               atol=1e-12 * np.abs(pm).max())
+
+
+def test_g2p_reproduces_uniform_and_linear_fields(tb):
+    """SPEC grid_to_particle examples: with APIC state v_p = c + A x_p, C_p = A
+    and zero stress, P2G builds the grid field V_i = c + A X_i, and G2P gives
+    back v_p = c + A x_p and C_p = A (within 1e-6; uniform field: A = 0,
+    C_p = 0)."""
+    x = _block()
+    n = len(x)
+    for A in (np.zeros((3, 3)), np.array([[0.3, -0.2, 0.1], [0.05, -0.4, 0.2], [0.1, 0.0, 0.25]])):
+        c = np.array([0.01, -0.02, 0.005])
+        v = c + x @ A.T
+        s = _scene(tb, x, v_el=v, C_el=np.tile(A.ravel(), (n, 1)))
+        lo, M, MG = _p2g(tb, s)
+        tb.mpm.grid_update(s)
+        _, _, V = s.grid(lo, lo + np.array(M.shape))
+        has = M > 0
+        X = (np.stack(np.meshgrid(*[np.arange(k) for k in M.shape], indexing="ij"), -1) + lo) * DX
+        lin = c + X @ A.T
+        # nodes carrying only elastomer mass hold the linear field
+        el = has & (np.abs(X - x.mean(0)).max(-1) < 6 * DX)
+        np.testing.assert_allclose(V[el], lin[el], rtol=0, atol=1e-12)
+        tb.mpm.grid_to_particle(s)
+        st = s.state()
+        np.testing.assert_allclose(st["v"][:n], v, rtol=0, atol=1e-12)
+        np.testing.assert_allclose(st["C"][:n].reshape(n, 9), np.tile(A.ravel(), (n, 1)),
+                                   rtol=0, atol=1e-6)
+        if not A.any():
+            assert np.abs(st["C"][:n]).max() < 1e-9
+
+
+def test_grid_update_division_and_empty_nodes(tb):
+    """SPEC grid_update: V = MG / M where M > 0, V = 0 on empty nodes."""
+    x = _block(n=3, spacing=2.2)
+    rng = np.random.default_rng(3)
+    s = _scene(tb, x, v_el=rng.standard_normal((len(x), 3)))
+    lo, M, MG = _p2g(tb, s)
+    tb.mpm.grid_update(s)
+    _, _, V = s.grid(lo, lo + np.array(M.shape))
+    has = M > 0
+    np.testing.assert_array_equal(V[has], MG[has] / M[has][:, None])
+    assert not V[~has].any()
+    assert (~has).any()
+
+
+def test_boundary_and_advect_closed_forms(tb):
+    """SPEC apply_boundary / advect examples: indenter velocity exactly the
+    command; bottom particles keep their positions; x += dt v (1e-4 m for
+    v = (1, 0, 0), dt = 1e-4); an indenter at z0 driven at (0, 0, -0.001) for
+    N substeps ends at z0 - 0.001 N dt (1e-12)."""
+    x = _block(n=4, spacing=0.6)
+    n = len(x)
+    tag = np.zeros(n, np.uint8)
+    tag[:16] = 1  # a bottom layer (ELASTOMER_BOTTOM)
+    ind = np.array([[20.3, 20.6, 24.1], [21.1, 20.4, 24.9]]) * DX
+    s = _scene(tb, x, tag_el=tag, x_ind=ind, dt=1e-4)
+    vcmd = (0.0, 0.0, -0.001)
+    tb.mpm.zero_grid(s)
+    tb.mpm.particle_to_grid(s)
+    tb.mpm.grid_update(s)
+    tb.mpm.grid_to_particle(s)
+    tb.mpm.apply_boundary(s, vcmd)
+    st = s.state()
+    np.testing.assert_array_equal(st["v"][n:], np.tile(vcmd, (2, 1)))
+    assert not st["v"][:16].any()
+    # advect with a uniform v = (1, 0, 0) uploaded on the elastomer
+    v = st["v"].copy()
+    v[:n] = (1.0, 0.0, 0.0)
+    s.set_state(v=v)
+    x0 = s.positions()
+    tb.mpm.advect(s)
+    np.testing.assert_allclose(s.positions()[:n] - x0[:n], np.tile([1e-4, 0, 0], (n, 1)),
+                               rtol=0, atol=1e-17)
+    # closed-form indenter integration over N substeps
+    s2 = _scene(tb, x, tag_el=tag, x_ind=ind, dt=1e-5)
+    z0 = s2.positions()[n:, 2].copy()
+    N = 100
+    tb.mpm.step(s2, vcmd, N)
+    xs = s2.positions()
+    np.testing.assert_allclose(xs[n:, 2], z0 - 0.001 * N * 1e-5, rtol=0, atol=1e-12)
+    np.testing.assert_array_equal(xs[:16], x[:16])  # bottom layer pinned
+
+
+def test_indenter_translates_rigidly(tb):
+    """SPEC invariant: indenter particles keep their relative positions (1e-12)."""
+    x = _block(n=4, spacing=0.6)
+    rng = np.random.default_rng(11)
+    ind = (np.array([20.0, 20.0, 22.0]) + 3 * rng.random((50, 3))) * DX
+    s = _scene(tb, x, x_ind=ind, dt=1e-5)
+    tb.mpm.step(s, (0.01, -0.02, -0.005), 150)
+    xi = s.positions()[len(x):]
+    rel0 = ind - ind[0]
+    np.testing.assert_allclose(xi - xi[0], rel0, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(xi[0] - ind[0], np.array([0.01, -0.02, -0.005]) * 150 * 1e-5,
+                               rtol=0, atol=1e-12)
+
+
+def _flat_render(tb, ka=0.0, kd=0.55, ks=0.25, lights=None, shininess=24.0):
+    r = tb.render_params()
+    r.ambient_k, r.diffuse_k, r.specular_k, r.shininess = ka, kd, ks, shininess
+    r.view_dir[:] = [0.0, 0.0, -1.0]
+    lights = lights or [((0, 0, -1), (0.8, 0.6, 0.4), (0.5, 0.3, 0.2))]
+    r.n_lights = len(lights)
+    for i, (d, diff, spec) in enumerate(lights):
+        r.lights[i][:] = list(d) + list(diff) + list(spec)
+    return r
+
+
+def test_render_known_answers(tb):
+    """SPEC render examples: flat depth -> normals (0, 0, -1); flat depth with
+    one overhead light -> uniform k_d i_d + k_s i_s; k_d = k_s = 0 -> k_a i_a;
+    a linear ramp -> constant normals; unit normals; zero-offset crop of a
+    480 x 640 map is the identity; the diffuse term is linear in i_d."""
+    h, w, r = 48, 64, 3e-5
+    flat = np.zeros((h, w))
+    nrm = tb.render.surface_normals(flat, r)
+    np.testing.assert_array_equal(nrm, np.broadcast_to([0.0, 0.0, -1.0], nrm.shape))
+    img = tb.render.phong_render(flat, r, _flat_render(tb))
+    expect = np.round(np.clip(0.55 * np.array([0.8, 0.6, 0.4]) + 0.25 * np.array([0.5, 0.3, 0.2]),
+                              0, 1) * 255)
+    np.testing.assert_array_equal(img, np.broadcast_to(expect.astype(np.uint8), img.shape))
+    amb = _flat_render(tb, ka=0.7, kd=0.0, ks=0.0)
+    amb.ambient_rgb[:] = [0.2, 0.5, 0.9]
+    img = tb.render.phong_render(flat, r, amb)
+    np.testing.assert_array_equal(img, np.broadcast_to(np.round(0.7 * np.array([0.2, 0.5, 0.9]) * 255)
+                                                       .astype(np.uint8), img.shape))
+    c = 0.3
+    ramp = c * r * np.arange(w)[None, :].repeat(h, 0)  # depth grows by c per pixel in x
+    nrm = tb.render.surface_normals(ramp, r)
+    n_exp = np.array([-c, 0.0, -1.0]) / np.sqrt(1 + c * c)  # H = -depth
+    np.testing.assert_allclose(nrm, np.broadcast_to(n_exp, nrm.shape), rtol=0, atol=1e-12)
+    rng = np.random.default_rng(2)
+    bumpy = rng.random((h, w)) * 1e-4
+    nrm = tb.render.surface_normals(bumpy, r)
+    assert np.abs(np.linalg.norm(nrm, axis=-1) - 1).max() < 1e-6
+    src = rng.random((480, 640))
+    np.testing.assert_array_equal(tb.render.crop_align(src, (0.0, 0.0, 1.0)), src)
+    # diffuse linearity (k_a = k_s = 0): doubling i_d doubles the pre-clamp value
+    tilt = [((0.3, 0.2, -0.9), (0.2, 0.15, 0.1), (0, 0, 0))]
+    one = tb.render.phong_render(bumpy, r, _flat_render(tb, kd=0.5, ks=0.0, lights=tilt))
+    tilt2 = [((0.3, 0.2, -0.9), (0.4, 0.3, 0.2), (0, 0, 0))]
+    two = tb.render.phong_render(bumpy, r, _flat_render(tb, kd=0.5, ks=0.0, lights=tilt2))
+    assert np.abs(two.astype(int) - 2 * one.astype(int)).max() <= 1
