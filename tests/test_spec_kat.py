@@ -302,3 +302,20 @@ def test_render_known_answers(tb):
     tilt2 = [((0.3, 0.2, -0.9), (0.4, 0.3, 0.2), (0, 0, 0))]
     two = tb.render.phong_render(bumpy, r, _flat_render(tb, kd=0.5, ks=0.0, lights=tilt2))
     assert np.abs(two.astype(int) - 2 * one.astype(int)).max() <= 1
+
+
+def test_indenter_particle_density_ordering(tb):
+    """SPEC acceptance 8 (the paper's Fig. 6): the config-1 sphere at 1e4 / 1e5
+    / 1e6 indenter points pressed 0.5 mm: MAE(1e4 vs 1e6) > MAE(1e5 vs 1e6) >
+    0, and SSIM orders the same way (tools/density_ordering.py)."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    from density_ordering import press_images
+
+    imgs = press_images(depth_mm=0.5)
+    s4, _, m4 = tb.metrics.compare(imgs[10000], imgs[1000000])
+    s5, _, m5 = tb.metrics.compare(imgs[100000], imgs[1000000])
+    assert m4 > m5 > 0
+    assert s4 < s5 < 1
