@@ -220,6 +220,32 @@ def config2b():
         image=img, depth_sample=depth[::16, ::16])
 
 
+def acceptance3():
+    """SPEC acceptance 3 scene: 60 particles on an 8^3 grid, one step of the
+    reference's serial SVD oracle (tests/oracle/reference_mpm.cpp)."""
+    rng = np.random.default_rng(3)
+    n = 60
+    dx = 1e-3
+    x = 2.5e-3 + rng.random((n, 3)) * 3e-3
+    v = rng.standard_normal((n, 3)) * 0.01
+    Cm = rng.standard_normal((n, 3, 3)) * 0.5
+    F = np.eye(3) + rng.standard_normal((n, 3, 3)) * 0.02
+    tag = np.where(np.arange(n) < 40, 0, 2).astype(np.uint8)
+    tag[:5] = 1
+    Cm[tag == 2] = 0
+    F[tag == 2] = np.eye(3)
+    mass = np.where(tag == 2, 2e-6, 1e-6)
+    vol0 = np.full(n, 1e-9)
+    E, nu, dt = 1.45e5, 0.45, 1e-5
+    mu = E / (2 * (1 + nu))
+    lam = E * nu / ((1 + nu) * (1 - 2 * nu))
+    st = dict(x=x, v=v, C=Cm, F=F, mass=mass, vol0=vol0, tag=tag)
+    ref, _ = R.oracle_step(st, (8, 8, 8), dx, (0, 0, 0), mu, lam, dt, (0, 0, -0.01))
+    np.savez_compressed(os.path.join(OUT, "acceptance3.npz"), dx=dx, dt=dt, E=E, nu=nu,
+                        vind=np.array([0, 0, -0.01]), x0=x, v0=v, C0=Cm, F0=F, tag=tag,
+                        mass=mass, vol0=vol0, x=ref["x"], v=ref["v"], C=ref["C"], F=ref["F"])
+
+
 def harness():
     import shutil
     import tempfile
@@ -390,9 +416,11 @@ def bridge():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "config2b", "bridge", "harness", "parts", "background", "clouds"]
+    which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "config2b", "acceptance3", "bridge", "harness", "parts", "background", "clouds"]
     if "config2b" in which:
         config2b()
+    if "acceptance3" in which:
+        acceptance3()
     if "config5" in which:
         config5()
     if "config1_deep" in which:

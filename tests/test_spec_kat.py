@@ -319,3 +319,24 @@ def test_indenter_particle_density_ordering(tb):
     s5, _, m5 = tb.metrics.compare(imgs[100000], imgs[1000000])
     assert m4 > m5 > 0
     assert s4 < s5 < 1
+
+
+def test_one_step_matches_the_reference_serial_oracle(tb, golden):
+    """SPEC acceptance 3: <= 100 particles on an 8^3 grid, one full step of the
+    CUDA path vs the reference's own serial triple-loop oracle with SVD polar
+    decomposition (tests/oracle/reference_mpm.cpp, fixture acceptance3.npz),
+    1e-10 relative on every particle quantity."""
+    g = golden("acceptance3.npz")
+    n = len(g["mass"])
+    ne = int((g["tag"] != 2).sum())
+    params = dict(res=(8, 8, 8), dx=float(g["dx"]), origin=(0, 0, 0), dt=float(g["dt"]),
+                  E=float(g["E"]), nu=float(g["nu"]))
+    parts = dict(x=g["x0"], v=g["v0"], C=g["C0"].reshape(n, 9), F=g["F0"].reshape(n, 9),
+                 mass=g["mass"], volume0=g["vol0"], tag=g["tag"], n_elastomer=ne)
+    s = tb.init_scene(params, parts)
+    tb.mpm.step(s, g["vind"], 1)
+    st = s.state()
+    for k in ("x", "v", "C", "F"):
+        ref = g[k]
+        got = st[k]
+        assert np.abs(got - ref).max() <= 1e-10 * np.abs(ref).max(), k
