@@ -89,11 +89,7 @@ DeviceSim::~DeviceSim() {
   cudaFree(F);
   cudaFree(tag);
   cudaFree(geo.cta_box);
-  cudaFree(grid_mp.lo);
-  cudaFree(grid_mp.hi);
-  cudaFree(grid_v.xy);
-  cudaFree(grid_v.z);
-  cudaFree(grid_mi);
+  cudaFree(grid_slab);  // grid_mp, grid_v, grid_mi live in one allocation
   cudaFree(col_start);
   cudaFree(ind_moves);
   cudaFree(surf_idx);
@@ -141,6 +137,24 @@ static int host_base(double x, double origin, double inv_dx) {
 
 int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, const double* Fm,
            bool init);
+
+// The grid arrays in one allocation (A.lo | A.hi | V.xy | V.z | M_I).
+static bool alloc_grid(DeviceSim& s) {
+  const size_t n = s.n_nodes;
+  const size_t b2 = n * sizeof(double2);
+  // +2: the staging reads vz rows from an even node over an even count
+  const size_t bz = ((n + 2) * sizeof(double) + 255) & ~size_t(255);
+  const size_t b1 = n * sizeof(double);
+  s.grid_slab_bytes = 3 * b2 + bz + b1;
+  if (cudaMalloc(&s.grid_slab, s.grid_slab_bytes) != cudaSuccess) return false;
+  char* p = static_cast<char*>(s.grid_slab);
+  s.grid_mp.lo = reinterpret_cast<double2*>(p);
+  s.grid_mp.hi = reinterpret_cast<double2*>(p + b2);
+  s.grid_v.xy = reinterpret_cast<double2*>(p + 2 * b2);
+  s.grid_v.z = reinterpret_cast<double*>(p + 3 * b2);
+  s.grid_mi = reinterpret_cast<double*>(p + 3 * b2 + bz);
+  return true;
+}
 
 int create(int device, const tg_params* P, const tg_particles* in, const tg_surface* surf,
            DeviceSim** out) {
@@ -239,12 +253,7 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
             cudaMalloc(&s->C, std::max<int64_t>(9 * n_el, 1) * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->F, std::max<int64_t>(9 * n_el, 1) * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->tag, std::max<int64_t>(n_el, 1)) == cudaSuccess &&
-            cudaMalloc(&s->grid_mp.lo, s->n_nodes * sizeof(double2)) == cudaSuccess &&
-            cudaMalloc(&s->grid_mp.hi, s->n_nodes * sizeof(double2)) == cudaSuccess &&
-            cudaMalloc(&s->grid_v.xy, s->n_nodes * sizeof(double2)) == cudaSuccess &&
-            // +2: the staging reads vz rows from an even node over an even count
-            cudaMalloc(&s->grid_v.z, (s->n_nodes + 2) * sizeof(double)) == cudaSuccess &&
-            cudaMalloc(&s->grid_mi, s->n_nodes * sizeof(double)) == cudaSuccess &&
+            alloc_grid(*s) &&
             cudaMalloc(&s->col_start, std::max<size_t>(col_starts.size(), 1) * sizeof(int64_t)) ==
                 cudaSuccess &&
             cudaMalloc(&s->ind_moves, std::max<int64_t>(n_ind, 1)) == cudaSuccess &&

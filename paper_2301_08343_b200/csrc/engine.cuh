@@ -99,6 +99,8 @@ struct DeviceSim {
   int tile[3] = {0, 0, 0};   // lattice block per CTA (ti, tj, tk)
   int tiles[3] = {0, 0, 0};  // blocks per axis
   bool grid_dirty = false;   // A / M_I may hold a phase-mode P2G (needs k_clear)
+  void* grid_slab = nullptr;  // one allocation holding grid_mp, grid_v, grid_mi
+  size_t grid_slab_bytes = 0;
   bool full_indenter = false; // scatter every indenter particle (TACCHI_FULL_INDENTER=1)
   bool grid_ready = false;   // A / M_I hold the scatter of the next substep (look-ahead
                              // of the previous mpm::step call); skip the standalone P2G
