@@ -233,7 +233,10 @@ def run_ours(args):
         "config": {"workload": WORKLOAD, "particles_per_gpu": n, "elastomer": n_el,
                    "grid": [256, 256, 256], "substeps_per_step": SUBSTEPS_PER_FRAME,
                    "dt_s": 2e-6, "parallelism": f"episodes x{world} (one per GPU)",
-                   "l2": "working set > L2 (particles ~90 MB + active grid window ~130 MB per substep)"},
+                   "l2": "no flush; per substep the particle state streams ~62 MB and the "
+                         "grid box ~60 MB (126 MB L2): measured in-pipeline DRAM traffic "
+                         "~240 MB per substep (ncu --cache-control none, DESIGN 4.4), so "
+                         "the inputs are not L2-resident between iterations"},
         "frames_per_sec": args.steps * world / (dev_ms * 1e-3),
         "e2e": {"value": e2e_value, "unit": UNIT, "frames_per_sec": args.steps * world / (e2e_ms * 1e-3),
                 "h2d_bytes_per_step": 3 * 8, "d2h_bytes_per_step": depth.nbytes + img.nbytes,
