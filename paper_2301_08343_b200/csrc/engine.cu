@@ -212,6 +212,13 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   g.stress_scale = -P->dt * 4.0 * g.inv_dx * g.inv_dx;
   if (const char* m = std::getenv("TACCHI_SCATTER")) g.scatter_mode = std::atoi(m);
   if (const char* f = std::getenv("TACCHI_FULL_INDENTER")) s->full_indenter = std::atoi(f) != 0;
+  // launch-shape A/B switches (tools/README.md); defaults are the measured best
+  g.gu_bps = 10;
+  g.pdl_early = 1;
+  g.ind_first = 1;
+  if (const char* e = std::getenv("TACCHI_GU_BPS")) g.gu_bps = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("TACCHI_PDL_EARLY")) g.pdl_early = std::atoi(e);
+  if (const char* e = std::getenv("TACCHI_IND_FIRST")) g.ind_first = std::atoi(e);
   s->sms = sm_count(device);
 
   // Indenter particles are re-ordered by base cell so that P2G scatters from

@@ -41,6 +41,41 @@ namespace {
 // programmatic stream serialization so each is dispatched while its
 // predecessor drains; this waits until the predecessor's writes are visible
 // (a no-op for ordinary launches).
+#ifdef TACCHI_TRACE
+// Per-CTA stage timestamps of the elastomer kernel (diagnostic builds only,
+// tools/trace_gel.py): [0] globaltimer at entry, [1] smid, [2..13] clock64 at
+// the stage marks, [14] globaltimer at exit, [15] block kind.
+__device__ unsigned long long g_trace[16384 * 16];
+__device__ __forceinline__ unsigned long long trace_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE_MARK(i)                                                                   \
+  do {                                                                                 \
+    if (threadIdx.x == 0 && blockIdx.x < 16384) g_trace[blockIdx.x * 16 + 2 + (i)] = clock64(); \
+  } while (0)
+#define TRACE_BEGIN(kind)                                                               \
+  do {                                                                                 \
+    if (threadIdx.x == 0 && blockIdx.x < 16384) {                                      \
+      unsigned sm;                                                                     \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));                                  \
+      g_trace[blockIdx.x * 16 + 0] = trace_gtime();                                    \
+      g_trace[blockIdx.x * 16 + 1] = sm;                                               \
+      g_trace[blockIdx.x * 16 + 15] = (kind);                                          \
+      g_trace[blockIdx.x * 16 + 2] = clock64();                                        \
+    }                                                                                  \
+  } while (0)
+#define TRACE_END()                                                                     \
+  do {                                                                                 \
+    if (threadIdx.x == 0 && blockIdx.x < 16384) g_trace[blockIdx.x * 16 + 14] = trace_gtime(); \
+  } while (0)
+#else
+#define TRACE_MARK(i)
+#define TRACE_BEGIN(kind)
+#define TRACE_END()
+#endif
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ void raise(Ctl* ctl, int code, int substep) {
@@ -178,11 +213,14 @@ struct IndArgs {
   double* mi;
   int n_cols;
   int gel_ctas;  // 0: no indenter blocks
+  int gel_lo;    // first elastomer block (the indenter blocks come first: they are
+                 // short, and the elastomer CTAs then end the kernel in full waves)
+  int ind_lo;    // first indenter block
 };
 
 namespace {
 
-__device__ __forceinline__ int64_t gel_particle(const GelMap& M, int64_t n_el) {
+__device__ __forceinline__ int64_t gel_particle(const GelMap& M, int64_t n_el, int cta) {
   if (M.lat[0] > 0) {
     const int t = threadIdx.x;
     const int per_col = M.tile[2];
@@ -190,13 +228,13 @@ __device__ __forceinline__ int64_t gel_particle(const GelMap& M, int64_t n_el) {
     const int jj = (t / per_col) % M.tile[1];
     const int ii = t / (per_col * M.tile[1]);
     if (ii >= M.tile[0]) return -1;
-    const int bj = blockIdx.x % M.tiles[1];
-    const int bi = blockIdx.x / M.tiles[1];
+    const int bj = cta % M.tiles[1];
+    const int bi = cta / M.tiles[1];
     const int i = bi * M.tile[0] + ii, j = bj * M.tile[1] + jj;
     if (i >= M.lat[0] || j >= M.lat[1] || kk >= M.lat[2]) return -1;
     return (static_cast<int64_t>(i) * M.lat[1] + j) * M.lat[2] + kk;
   }
-  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t p = static_cast<int64_t>(cta) * blockDim.x + threadIdx.x;
   return p < n_el ? p : -1;
 }
 
@@ -432,16 +470,16 @@ __device__ void tile_box(P2GTile& T, bool active, const int* base) {
 // does; the rare duplicates (detected through the owner table) and CTAs whose
 // footprint exceeds the tile fall back to direct REDs.
 __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
-                                 const Geometry& g, NodeBuf grid) {
+                                 const Geometry& g, NodeBuf grid, int cta) {
   const int tid = threadIdx.x;
   if (g.scatter_mode == 1 || g.scatter_mode == 3) {  // A/B switches without a tile
-    if (tid == 0 && g.cta_box) g.cta_box[8 * blockIdx.x + 6] = 0;  // next G2P: no staged box
+    if (tid == 0 && g.cta_box) g.cta_box[8 * cta + 6] = 0;  // next G2P: no staged box
     if (g.scatter_mode == 1 && active) scatter_direct(g, grid, m, q);  // per-particle REDs
     return;                                                            // (3: no scatter)
   }
   tile_box(T, active, q.st.base);
   if (tid == 0 && g.cta_box) {  // the next G2P of these particles stages this box
-    int* b = g.cta_box + 8 * blockIdx.x;
+    int* b = g.cta_box + 8 * cta;
     for (int a = 0; a < 3; ++a) {
       b[a] = T.lo[a];
       b[3 + a] = T.dim[a];
@@ -462,6 +500,7 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
   __syncthreads();
   int base_idx = 0;
   bool tiled = false;
+  TRACE_MARK(5);
   if (active) {
     if (use_tile) {
       base_idx = ((q.st.base[0] - T.lo[0]) * d1 + (q.st.base[1] - T.lo[1])) * d2 +
@@ -500,9 +539,11 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
       }
     }
   }
+  TRACE_MARK(6);
   fence_proxy_async();
   __syncthreads();
   tile_bulk_reduce(T, g, grid);
+  TRACE_MARK(7);
 }
 
 // det F check + polar + stress + affine (engine.cpp:130-139). Returns false
@@ -747,7 +788,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_p2g_gel_tile(
   P2GTile& T = *reinterpret_cast<P2GTile*>(smem_raw);
   const int s = ctl->substep;
   if (stale_block(ctl, s)) return;
-  const int64_t p = gel_particle(M, n_el);
+  const int64_t p = gel_particle(M, n_el, blockIdx.x);
   bool active = p >= 0;
   P2GPayload q;
   double J = 1.0;
@@ -765,7 +806,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_p2g_gel_tile(
     if (active && !stencil_in_grid(g, q.st)) active = false;  // zero_grid already raised
   }
   reduce_min_detf(ctl, s, active, J);
-  p2g_tile_scatter(T, active, q, m, g, grid);
+  p2g_tile_scatter(T, active, q, m, g, grid, blockIdx.x);
 }
 
 // Indenter scatter with a non-uniform velocity (only possible before the
@@ -1221,6 +1262,9 @@ __global__ void __launch_bounds__(256, 5) k_grid_update_boxes(NodeBuf mp, double
                                     Ctl* ctl, Geometry g,
                                     double m_ind) {
   pdl_wait();
+  // The elastomer kernel that follows reads its particle state (written two
+  // kernels back, complete now) before its own wait: let it launch early.
+  if (g.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (stale(ctl, ctl->substep)) return;
   int lo[2][3], dm[2][3], vol[2];
   for (int m = 0; m < 2; ++m) {
@@ -1347,65 +1391,85 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     double vol0, IndArgs ia) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   P2GTile& T = *reinterpret_cast<P2GTile*>(smem_raw);
+  const bool with_ind = kLookahead && ia.gel_ctas > 0;
+  const int cta = with_ind ? static_cast<int>(blockIdx.x) - ia.gel_lo : static_cast<int>(blockIdx.x);
+  const bool gel_block = !with_ind || (cta >= 0 && cta < ia.gel_ctas);
+  TRACE_BEGIN(gel_block ? 1 : 2);
+  const int64_t p = gel_block ? gel_particle(M, n_el, cta) : -1;
+  const bool active = p >= 0;
+  double px0 = 0, px1 = 0, px2 = 0, v2 = 0;
+  bool bottom = false;
+  if (active) {
+    // particle state streams through once per substep: evict-first loads and
+    // stores (ld/st .cs) keep L2 for the grid arrays the next kernels reuse.
+    // x, F and cta_box were last written by the previous launch of this
+    // kernel, which is complete once the kernel before this one passed its
+    // own griddepcontrol.wait (the only way this grid can have been
+    // launched), so they are read before this grid's wait, overlapping the
+    // tail of grid_update. F is only prefetched into L2 here (held in
+    // registers across the gather it would be spilled, and the spill store
+    // would wait for the load); it is loaded after the gather.
+    px0 = __ldcs(x + p);
+    px1 = __ldcs(x + n + p);
+    px2 = __ldcs(x + 2 * n + p);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) asm volatile("prefetch.global.L2 [%0];" ::"l"(Fm + i * n_el + p));
+    if (kBoundary) bottom = __ldg(tag + p) == kElastomerBottom;
+  }
+  if (kLookahead && gel_block && threadIdx.x == 0) {
+    // The G2P footprint is the tile box of the P2G that scattered these
+    // particles at these positions (the previous kernel of this CTA).
+    const int* b = g.cta_box + 8 * cta;
+    for (int a = 0; a < 3; ++a) {
+      T.lo[a] = b[a];
+      T.dim[a] = b[3 + a];
+    }
+    T.ok = b[6] && (g.res[2] & 1) == 0;  // vz row staging needs an even res2
+    T.pitch = tile_pitch(T.dim[2]);
+  }
   pdl_wait();
-  if (kLookahead && ia.gel_ctas > 0 && static_cast<int>(blockIdx.x) >= ia.gel_ctas) {
+  TRACE_MARK(1);
+  if (!gel_block) {
     // indenter blocks: the s+1 column walks (they touch only indenter x and
     // M_I; the elastomer box comes from the previous finalize, widened)
     const int s = ctl->substep;
     if (stale(ctl, s)) return;
-    ind_cols_block<true>(*reinterpret_cast<ColSmem*>(smem_raw), blockIdx.x - ia.gel_ctas, x, n,
+    ind_cols_block<true>(*reinterpret_cast<ColSmem*>(smem_raw), blockIdx.x - ia.ind_lo, x, n,
                          n_el, ia.col_start, ia.n_cols, ia.moves, ctl, g, ia.mi, 2, s);
+    TRACE_END();
     return;
   }
-  const int s = ctl->substep;
-  if (stale_block(ctl, s)) return;
-  const int64_t p = gel_particle(M, n_el);
-  const bool active = p >= 0;
-  double px0 = 0, px1 = 0, px2 = 0, v2 = 0;
   double F[9], vv[3] = {0, 0, 0}, Cn[9];
   bool staged = false;
   Stencil st_old;
-  double F0[9];
-  if (active) {
-    // particle state streams through once per substep: evict-first loads and
-    // stores (ld/st .cs) keep L2 for the grid arrays the next kernels reuse
-    px0 = __ldcs(x + p);
-    px1 = __ldcs(x + n + p);
-    px2 = __ldcs(x + 2 * n + p);
-    // issue the deformation-gradient loads now; they complete while the
-    // footprint is reduced and the velocity tile is staged
-#pragma unroll
-    for (int i = 0; i < 9; ++i) F0[i] = __ldcs(Fm + i * n_el + p);
-  }
   if (kLookahead) {
     // Stage the grid velocities of the CTA's G2P footprint (coalesced rows
-    // along z) in the shared tile before the gathers.
-    // The G2P footprint is the tile box of the P2G that scattered these
-    // particles at these positions (the previous kernel of this CTA): read it
-    // instead of reducing it, so the staging copies start right away.
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int* b = g.cta_box + 8 * blockIdx.x;
-      for (int a = 0; a < 3; ++a) {
-        T.lo[a] = b[a];
-        T.dim[a] = b[3 + a];
-      }
-      T.ok = b[6] && (g.res[2] & 1) == 0;  // vz row staging needs an even res2
-      T.pitch = tile_pitch(T.dim[2]);
-    }
-    __syncthreads();
+    // along z) in the shared tile before the gathers; the copies are in
+    // flight while the control block is read.
+    __syncthreads();  // T.lo / dim / ok from thread 0
     staged = T.ok != 0;
     if (staged && g.scatter_mode != 5) tile_bulk_stage_issue(T, g, vel);
   }
+  const bool staging = kLookahead && staged && g.scatter_mode != 5;
+  const int s = ctl->substep;
+  if (stale_block(ctl, s)) {
+    if (staging) tile_bulk_wait(T);  // no bulk copy may land in a retired CTA's smem
+    return;
+  }
   // the stencil needs x: its loads complete while the staging copies fly
   if (active) make_stencil(px0, px1, px2, g.origin, g.inv_dx, st_old);
-  if (kLookahead && staged && g.scatter_mode != 5) tile_bulk_wait(T);
+  if (staging) tile_bulk_wait(T);
+  TRACE_MARK(2);
   if (active) {
     if (g.scatter_mode == 5) {  // A/B timing: no velocity staging / gather
       vv[0] = vv[1] = vv[2] = 0.0;
       for (int i = 0; i < 9; ++i) Cn[i] = 0.0;
     } else if (staged) g2p_gather_smem(g, T, st_old, vv, Cn);
     else g2p_gather(g, vel, px0, px1, px2, vv, Cn);
+    TRACE_MARK(8);
+    double F0[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) F0[i] = __ldcs(Fm + i * n_el + p);
     double G[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -1417,7 +1481,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
       if (g.scatter_mode != 6) __stcs(Cm + i * n_el + p, Cn[i]);  // 6: A/B timing, no C / v
       __stcs(Fm + i * n_el + p, F[i]);
     }
-    if (kBoundary && tag[p] == kElastomerBottom) vv[0] = vv[1] = vv[2] = 0.0;
+    if (bottom) vv[0] = vv[1] = vv[2] = 0.0;
     if (g.scatter_mode != 6) {
       __stcs(v + p, vv[0]);
       __stcs(v + n + p, vv[1]);
@@ -1433,9 +1497,11 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
       v2 = vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2];
     }
   }
+  TRACE_MARK(9);
   if (kAdvect)
     reduce_motion(&ctl->max_v2[s & 1], ctl->bb_lo[s & 1], ctl->bb_hi[s & 1], active, v2, px0, px1,
                   px2);
+  TRACE_MARK(3);
   if (kLookahead) {
     // particle_to_grid of substep s + 1 with the state just written.
     P2GPayload q;
@@ -1450,8 +1516,10 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
       if (go && !stencil_in_grid(g, q.st)) go = false;  // finalize raises OutOfGrid
     }
     reduce_min_detf(ctl, s + 1, go, J);
-    p2g_tile_scatter(T, go, q, m, g, grid);
+    TRACE_MARK(4);
+    p2g_tile_scatter(T, go, q, m, g, grid, cta);
   }
+  TRACE_END();
 }
 
 // Phase-API pieces (engine.cpp:254-286).
@@ -1714,7 +1782,7 @@ int launch_p2g(DeviceSim& s, bool publish_diag) {
 
 int launch_grid_update(DeviceSim& s, int sms, bool zero) {
   if (zero)
-    launch_pdl(k_grid_update_boxes, dim3(window_blocks(sms)), dim3(kThreads), 0, s.stream,
+    launch_pdl(k_grid_update_boxes, dim3(static_cast<unsigned>(sms * s.geo.gu_bps)), dim3(kThreads), 0, s.stream,
                s.grid_mp, s.grid_mi, s.grid_v, s.ctl, s.geo, s.m_ind);
   else
     k_grid_update_window<<<window_blocks(sms), kThreads, 0, s.stream>>>(
@@ -1730,8 +1798,11 @@ int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter) {
   IndArgs ia{};
   unsigned extra = 0;
   if (with_indenter) {  // the indenter's look-ahead column walks ride along
-    ia = IndArgs{s.col_start, s.ind_moves, s.grid_mi, s.n_cols, static_cast<int>(gel_blocks(s))};
     extra = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
+    const int gel = static_cast<int>(gel_blocks(s));
+    const bool ind_first = s.geo.ind_first != 0;
+    ia = IndArgs{s.col_start, s.ind_moves, s.grid_mi, s.n_cols, gel,
+                 ind_first ? static_cast<int>(extra) : 0, ind_first ? 0 : gel};
     s.ind_v_uniform = true;
   }
   if (lookahead)
@@ -1869,3 +1940,14 @@ int launch_gather_box(DeviceSim& s, const int lo[3], const int hi[3], double* ma
 }
 
 }  // namespace tacchi_b200
+
+#ifdef TACCHI_TRACE
+// Diagnostic builds only: copies the elastomer kernel's per-CTA stage marks.
+extern "C" int tg_debug_trace(unsigned long long* out, int n_ctas) {
+  if (n_ctas > 16384) n_ctas = 16384;
+  return cudaMemcpyFromSymbol(out, tacchi_b200::g_trace, sizeof(unsigned long long) * 16 * n_ctas) ==
+                 cudaSuccess
+             ? n_ctas
+             : -1;
+}
+#endif
