@@ -463,6 +463,88 @@ __device__ void tile_box(P2GTile& T, bool active, const int* base) {
   __syncthreads();
 }
 
+// The look-ahead kernel's block reductions in one pass (2 barriers instead of
+// the 2 + 4 of reduce_motion + tile_box): advect's max |v|^2 and bbox of x
+// (engine.cpp:273-282) into the substep-s slots of the control block, the
+// min det F of substep s + 1 (engine.cpp:119,135), and the CTA's P2G node box
+// into T (as tile_box). All threads of the block must call it; the first
+// barrier also retires every earlier reader of T (the G2P gathers).
+__device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double v2, double x0,
+                                 double x1, double x2, bool go, double J, const int* base) {
+  __shared__ double redd[8][kGelThreads / 32];
+  __shared__ int redi[6][kGelThreads / 32];
+  double r[8];
+  r[0] = moved ? v2 : 0.0;
+  r[1] = moved ? x0 : INFINITY;
+  r[2] = moved ? x1 : INFINITY;
+  r[3] = moved ? x2 : INFINITY;
+  r[4] = moved ? x0 : -INFINITY;
+  r[5] = moved ? x1 : -INFINITY;
+  r[6] = moved ? x2 : -INFINITY;
+  r[7] = go ? J : 1.0;
+  r[0] = warp_max(r[0]);
+#pragma unroll
+  for (int a = 1; a < 4; ++a) r[a] = warp_min(r[a]);
+#pragma unroll
+  for (int a = 4; a < 7; ++a) r[a] = warp_max(r[a]);
+  r[7] = warp_min(r[7]);
+  int bi[6];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    bi[a] = __reduce_min_sync(0xffffffffu, go ? base[a] : INT_MAX);
+    bi[3 + a] = __reduce_max_sync(0xffffffffu, go ? base[a] : INT_MIN);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kGelThreads / 32;
+  if (lane == 0) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a) redd[a][warp] = r[a];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) redi[a][warp] = bi[a];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const double ident = (a == 0) ? 0.0 : (a < 4 ? INFINITY : (a < 7 ? -INFINITY : 1.0));
+      r[a] = lane < kWarps ? redd[a][lane] : ident;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      bi[a] = __reduce_min_sync(0xffffffffu, lane < kWarps ? redi[a][lane] : INT_MAX);
+      bi[3 + a] = __reduce_max_sync(0xffffffffu, lane < kWarps ? redi[3 + a][lane] : INT_MIN);
+    }
+    r[0] = warp_max(r[0]);
+#pragma unroll
+    for (int a = 1; a < 4; ++a) r[a] = warp_min(r[a]);
+#pragma unroll
+    for (int a = 4; a < 7; ++a) r[a] = warp_max(r[a]);
+    r[7] = warp_min(r[7]);
+    if (lane == 0) {
+      if (r[1] <= r[4]) {
+        atomicMax(&ctl->max_v2[s & 1], static_cast<unsigned long long>(__double_as_longlong(r[0])));
+        atomicMin(&ctl->bb_lo[s & 1][0], order_key(r[1]));
+        atomicMin(&ctl->bb_lo[s & 1][1], order_key(r[2]));
+        atomicMin(&ctl->bb_lo[s & 1][2], order_key(r[3]));
+        atomicMax(&ctl->bb_hi[s & 1][0], order_key(r[4]));
+        atomicMax(&ctl->bb_hi[s & 1][1], order_key(r[5]));
+        atomicMax(&ctl->bb_hi[s & 1][2], order_key(r[6]));
+      }
+      if (r[7] < 1.0) atomicMin(&ctl->min_detf[(s + 1) & 1], order_key(r[7]));
+      const bool any = bi[0] != INT_MAX;
+      for (int a = 0; a < 3; ++a) {
+        T.lo[a] = bi[a];
+        T.hi[a] = bi[3 + a];
+        T.dim[a] = any ? bi[3 + a] - bi[a] + 3 : 0;
+      }
+      T.pitch = tile_pitch(T.dim[2]);
+      const int rows = T.dim[0] * T.dim[1];
+      T.ok = any && rows * T.pitch <= kTileCap && rows * tile_zpitch(T.dim[2] + 2) <= 2 * kTileCap;
+    }
+  }
+  __syncthreads();
+}
+
 // CTA-cooperative scatter. All threads of the block must call it.
 // Phase (a,b,c) adds each particle's contribution to node base + (a,b,c);
 // two particles of the CTA collide in a phase only if they share a base cell,
@@ -470,14 +552,14 @@ __device__ void tile_box(P2GTile& T, bool active, const int* base) {
 // does; the rare duplicates (detected through the owner table) and CTAs whose
 // footprint exceeds the tile fall back to direct REDs.
 __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
-                                 const Geometry& g, NodeBuf grid, int cta) {
+                                 const Geometry& g, NodeBuf grid, int cta, bool box_done) {
   const int tid = threadIdx.x;
   if (g.scatter_mode == 1 || g.scatter_mode == 3) {  // A/B switches without a tile
     if (tid == 0 && g.cta_box) g.cta_box[8 * cta + 6] = 0;  // next G2P: no staged box
     if (g.scatter_mode == 1 && active) scatter_direct(g, grid, m, q);  // per-particle REDs
     return;                                                            // (3: no scatter)
   }
-  tile_box(T, active, q.st.base);
+  if (!box_done) tile_box(T, active, q.st.base);
   if (tid == 0 && g.cta_box) {  // the next G2P of these particles stages this box
     int* b = g.cta_box + 8 * cta;
     for (int a = 0; a < 3; ++a) {
@@ -806,7 +888,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_p2g_gel_tile(
     if (active && !stencil_in_grid(g, q.st)) active = false;  // zero_grid already raised
   }
   reduce_min_detf(ctl, s, active, J);
-  p2g_tile_scatter(T, active, q, m, g, grid, blockIdx.x);
+  p2g_tile_scatter(T, active, q, m, g, grid, blockIdx.x, false);
 }
 
 // Indenter scatter with a non-uniform velocity (only possible before the
@@ -1498,11 +1580,12 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     }
   }
   TRACE_MARK(9);
-  if (kAdvect)
+  if (kAdvect && !kLookahead)
     reduce_motion(&ctl->max_v2[s & 1], ctl->bb_lo[s & 1], ctl->bb_hi[s & 1], active, v2, px0, px1,
                   px2);
   TRACE_MARK(3);
   if (kLookahead) {
+    static_assert(!kLookahead || kAdvect, "the look-ahead scatter follows an advect");
     // particle_to_grid of substep s + 1 with the state just written.
     P2GPayload q;
     double J = 1.0;
@@ -1515,9 +1598,10 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
       go = make_payload(g, ctl, s + 1, m, vol0, F, Cn, vv, px0, px1, px2, q, J);
       if (go && !stencil_in_grid(g, q.st)) go = false;  // finalize raises OutOfGrid
     }
-    reduce_min_detf(ctl, s + 1, go, J);
     TRACE_MARK(4);
-    p2g_tile_scatter(T, go, q, m, g, grid, cta);
+    // advect's motion reductions, min det F of s + 1 and the tile box together
+    block_motion_box(T, ctl, s, active, v2, px0, px1, px2, go, J, q.st.base);
+    p2g_tile_scatter(T, go, q, m, g, grid, cta, true);
   }
   TRACE_END();
 }
