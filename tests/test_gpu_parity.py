@@ -147,6 +147,48 @@ def test_phases_match_oracle(tb, golden, oracle):
     assert s.diag.max_speed == pytest.approx(o.diag.max_speed, rel=1e-15)
 
 
+def test_step_chains_with_uploads_match_oracle(tb, golden, oracle):
+    """Step calls interleaved with state uploads, velocity changes and odd
+    substep counts vs the serial oracle on the same inputs. The step path
+    carries the next substep's scatter, each tile's staging box and (before
+    each elastomer kernel's grid-dependency wait) the particle state from one
+    launch to the next; an upload must discard all of it."""
+    g = golden("small_scene.npz")
+    s = tb.sim.build_sim(SMALL)
+    o = _small_oracle(oracle, g)
+    rng = np.random.default_rng(7)
+    plan = [(SMALL_V, 10, None), (SMALL_V, 7, "x"), ((0.0, 0.0, -0.02), 13, None),
+            ((0.001, 0.0, -0.01), 1, "F"), (SMALL_V, 20, "v"), (SMALL_V, 9, None)]
+    for vind, n, upload in plan:
+        el = o.tag != 2  # elastomer (the indenter stays rigid)
+        if upload == "x":
+            x = s.state()["x"].copy()
+            x[el] += rng.uniform(-2e-7, 2e-7, (int(el.sum()), 3))
+            s.set_state(x=x)
+            o.x = x.copy()
+        elif upload == "F":
+            st = s.state()
+            F = st["F"].reshape(-1, 3, 3).copy()
+            F[el] += rng.uniform(-1e-6, 1e-6, (int(el.sum()), 3, 3))
+            s.set_state(F=F.reshape(-1, 9))
+            o.F = F.copy()
+        elif upload == "v":
+            st = s.state()
+            v = st["v"].copy()
+            v[el] += rng.uniform(-1e-4, 1e-4, (int(el.sum()), 3))
+            s.set_state(v=v)
+            o.v = v.copy()
+        tb.mpm.step(s, vind, n)
+        o.step(vind, n)
+        x = s.positions()
+        disp = np.abs(o.x - g["x0"]).max()
+        err = np.abs(x - o.x).max()
+        assert err <= 1e-8 * disp, (upload, n, err, disp)
+        st = s.state()
+        np.testing.assert_allclose(st["F"].reshape(-1, 3, 3), o.F, rtol=0, atol=1e-11)
+        assert s.step_count == o.diag.step_count
+
+
 def test_step_graph_and_plain_launches_agree(tb):
     a = tb.sim.build_sim(SMALL)
     b = tb.sim.build_sim(SMALL)
