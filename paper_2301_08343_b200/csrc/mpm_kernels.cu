@@ -14,13 +14,18 @@
 //                        a shared-memory node tile: 27 barrier-separated
 //                        conflict-free accumulation phases, then one TMA bulk
 //                        reduction per tile row. Extra blocks of the same
-//                        launch run the rigid indenter's apply_boundary +
+//                        launch (the lowest block indices) run the rigid
+//                        indenter's apply_boundary +
 //                        advect + s+1 scatter (ind_cols_block: warp per
 //                        z-sorted column, run-length accumulation of B-spline
 //                        weight sums, one RED.F64 per touched node into M_I;
 //                        the indenter's momentum is M_I * v, v uniform).
 //   k_finalize           advect's in_range check / step_count / max_speed and
 //                        the next zero_grid window (engine.cpp:53-68, 279-285).
+// grid_update triggers the elastomer kernel's launch right after its own
+// griddepcontrol.wait, and the elastomer kernel reads its particle state and
+// staging box (written by its previous launch, complete by then) before its
+// own wait.
 // The first substep of a call without a pending look-ahead starts with a
 // standalone scatter (k_p2g_gel_tile, k_ind_cols<false>); every substep
 // scatters the next one, so consecutive calls chain; k_ind_catchup applies
@@ -206,7 +211,8 @@ struct GelMap {
 };
 
 // The rigid indenter's look-ahead column walks, run by extra blocks of the
-// elastomer kernel (blocks >= gel_ctas) instead of a kernel of their own.
+// elastomer kernel (blocks [ind_lo, ind_lo + walk blocks)) instead of a kernel
+// of their own.
 struct IndArgs {
   const int64_t* col_start;
   uint8_t* moves;
