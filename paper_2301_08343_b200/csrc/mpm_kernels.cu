@@ -1494,9 +1494,9 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     // kernel, which is complete once the kernel before this one passed its
     // own griddepcontrol.wait (the only way this grid can have been
     // launched), so they are read before this grid's wait, overlapping the
-    // tail of grid_update. F is only prefetched into L2 here (held in
-    // registers across the gather it would be spilled, and the spill store
-    // would wait for the load); it is loaded after the gather.
+    // tail of grid_update. F is only prefetched into L2 here (loaded into
+    // registers this early it is spilled, and the spill store waits for the
+    // load); it is loaded once the stencil is computed.
     px0 = __ldcs(x + p);
     px1 = __ldcs(x + n + p);
     px2 = __ldcs(x + 2 * n + p);
@@ -1546,6 +1546,14 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
   }
   // the stencil needs x: its loads complete while the staging copies fly
   if (active) make_stencil(px0, px1, px2, g.origin, g.inv_dx, st_old);
+  // F (prefetched into L2 at entry) is loaded while the staging copies
+  // complete: loaded at entry it was spilled (the spill store waited for the
+  // load), loaded after the gather its L2 latency was exposed (DESIGN 4.5)
+  double F0[9];
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) F0[i] = __ldcs(Fm + i * n_el + p);
+  }
   if (staging) tile_bulk_wait(T);
   TRACE_MARK(2);
   if (active) {
@@ -1555,9 +1563,6 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     } else if (staged) g2p_gather_smem(g, T, st_old, vv, Cn);
     else g2p_gather(g, vel, px0, px1, px2, vv, Cn);
     TRACE_MARK(8);
-    double F0[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) F0[i] = __ldcs(Fm + i * n_el + p);
     double G[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
