@@ -1527,7 +1527,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     TRACE_END();
     return;
   }
-  double F[9], vv[3] = {0, 0, 0}, Cn[9];
+  double F[9], vv[3], Cn[9];  // defined for active particles only
   bool staged = false;
   Stencil st_old;
   if (kLookahead) {
