@@ -8,6 +8,9 @@ SURVEY.md §8(d) (the tests run the same scenes over shorter slices):
                  slide at (+0.005, 0, 0) m/s for 200 frames
   config5      : 40 x 40 mm gel on 512^3, press 2000 frames, then move at
                  (0.01, 0, 0) m/s for 500 frames
+  config2a     : config 1 with the 1e6-point sphere, press 2000 frames
+  config2b     : 171 x 171 x 35 gel (0.91 grid cells spacing: duplicate base
+                 cells), press 2000 frames, then slide 200 frames
 
 The reference (oracle/_ref, all host threads) and the CUDA path run the same
 step calls (10 substeps per frame); at every checkpoint both are captured and
@@ -27,11 +30,12 @@ import numpy as np  # noqa: E402
 
 import paper_2301_08343_b200 as tb  # noqa: E402
 from oracle import refpy  # noqa: E402  (checker only)
-from tests.scenes import CONFIG1  # noqa: E402
+from tests.scenes import CONFIG1, CONFIG2A  # noqa: E402
 
 CONFIG5_FULL = {"elastomer": {"size_mm": [40, 40, 4], "particle_counts": [201, 201, 21]},
                 "grid": {"nodes_per_axis": [512, 512, 512], "edge_mm": 66.0},
                 "time": {"dt_s": 2e-6}}
+CONFIG2B_FULL = {"elastomer": {"particle_counts": [171, 171, 35]}, "time": {"dt_s": 2e-6}}
 PRESS = (0.0, 0.0, -0.01)
 
 
@@ -40,6 +44,8 @@ def cases():
     for shape in ("cylinder", "cylinder_shell", "wave1", "dots"):
         yield f"config3-{shape}", CONFIG1, shape, [(2000, PRESS), (200, (0.005, 0.0, 0.0))], 550
     yield "config5", CONFIG5_FULL, "", [(2000, PRESS), (500, (0.01, 0.0, 0.0))], 500
+    yield "config2a", CONFIG2A, "", [(2000, PRESS)], 500
+    yield "config2b", CONFIG2B_FULL, "", [(2000, PRESS), (200, (0.005, 0.0, 0.0))], 550
 
 
 def main(selected):
