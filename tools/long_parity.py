@@ -11,6 +11,9 @@ SURVEY.md §8(d) (the tests run the same scenes over shorter slices):
   config2a     : config 1 with the 1e6-point sphere, press 2000 frames
   config2b     : 171 x 171 x 35 gel (0.91 grid cells spacing: duplicate base
                  cells), press 2000 frames, then slide 200 frames
+  config4-<e>  : config 1 with episode e's config-4 draw (lateral offset,
+                 z-rotation; a non-symmetric "dots" indenter so the rotation
+                 matters), pressed 700 frames (0.14 mm of travel, 0.04 mm into the gel)
 
 The reference (oracle/_ref, all host threads) and the CUDA path run the same
 step calls (10 substeps per frame); at every checkpoint both are captured and
@@ -45,6 +48,11 @@ def cases():
         yield f"config3-{shape}", CONFIG1, shape, [(2000, PRESS), (200, (0.005, 0.0, 0.0))], 550
     yield "config5", CONFIG5_FULL, "", [(2000, PRESS), (500, (0.01, 0.0, 0.0))], 500
     yield "config2a", CONFIG2A, "", [(2000, PRESS)], 500
+    from paper_2301_08343_b200 import episodes
+    for e in range(8):
+        ep = episodes.make_episode(e)
+        cfg = episodes.episode_config(CONFIG1, ep)
+        yield f"config4-{e}", cfg, ("dots", ep.offset_x_m, ep.offset_y_m), [(700, PRESS)], 700
     yield "config2b", CONFIG2B_FULL, "", [(2000, PRESS), (200, (0.005, 0.0, 0.0))], 550
 
 
@@ -52,13 +60,16 @@ def main(selected):
     threads = os.cpu_count() or 1
     div = int(os.environ.get("LP_DIV", "1"))  # shrink every phase (smoke runs)
     for name, cfg, obj, plan, every in cases():
-        if selected and name not in selected:
+        if selected and name not in selected and name.split("-")[0] not in selected:
             continue
         plan = [(max(f // div, 1), v) for f, v in plan]
         every = max(every // div, 1)
         t0 = time.perf_counter()
-        ref = refpy.RefSim.from_config(cfg, obj, threads=threads)
-        gpu = tb.sim.build_sim(cfg, obj)
+        ox = oy = 0.0
+        if isinstance(obj, tuple):
+            obj, ox, oy = obj
+        ref = refpy.RefSim.from_config(cfg, obj, ox, oy, threads=threads)
+        gpu = tb.sim.build_sim(cfg, obj, ox, oy)
         x0 = ref.state()["x"]
         assert np.array_equal(gpu.positions(), x0), "setup differs"
         frame = 0
