@@ -739,6 +739,10 @@ __device__ __forceinline__ int base_of(const Geometry& g, int a, double x) {
 
 __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode) {
   pdl_wait();
+  // every kernel that follows finalize in a step plan (grid_update,
+  // k_ind_catchup) reads nothing before its own wait: let it launch while
+  // this warp runs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x;
   const bool ax = lane < 3;
   const int a = ax ? lane : 0;
