@@ -238,6 +238,14 @@ void* tg_stream(tg_handle h);
 int64_t tg_kernel_launches(tg_handle h);
 /* Enables / disables CUDA-graph replay of the substep loop (default on). */
 int tg_set_graphs(tg_handle h, int enabled);
+/* mpm::polar_rotation / polar_rotation_svd + corotated_stress
+ * (material.cpp:18-89) of n row-major 3x3 matrices F on `device`, through the
+ * device functions the P2G kernels call. mode 0: polar_rotation (scaled
+ * Newton with its SVD fallback), 1: polar_rotation_svd directly (the
+ * fallback). S (may be NULL) receives corotated_stress(F) with that R.
+ * Instrumentation for the material known-answer tests. */
+int tg_polar(int device, const double* F, int64_t n, int mode, double youngs_modulus,
+             double poisson_ratio, double* R, double* S);
 const char* tg_last_error(void);
 const char* tg_version(void);
 

@@ -101,7 +101,7 @@ EXPORTED = [
     "tg_download_grid", "tg_render_from_config", "tg_capture", "tg_extract_depth",
     "tg_crop_align", "tg_surface_normals", "tg_phong_render", "tg_step_many", "tg_step_capture_many", "tg_sync",
     "tg_stream", "tg_kernel_launches", "tg_set_graphs", "tg_last_error", "tg_version",
-    "tg_generate_cloud", "tg_placed_indenter", "tg_time_phases",
+    "tg_generate_cloud", "tg_placed_indenter", "tg_time_phases", "tg_polar",
 ]
 
 PHASE_TIMING_NAMES = ["p2g_elastomer_first", "p2g_indenter_first", "grid_update",
@@ -160,6 +160,7 @@ def lib():
         L.tg_kernel_launches.restype = C.c_int64
         L.tg_set_graphs.argtypes = [C.c_void_p, C.c_int]
         L.tg_time_phases.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
+        L.tg_polar.argtypes = [C.c_int, _dp, C.c_int64, C.c_int, C.c_double, C.c_double, _dp, _dp]
         L.tg_generate_cloud.argtypes = [C.c_char_p, C.c_int64, C.c_uint64, _dp]
         L.tg_placed_indenter.argtypes = [C.c_char_p, C.c_char_p, C.c_double, C.c_double, _dp,
                                          _i64p]
@@ -514,6 +515,19 @@ class sim:  # noqa: N801 — mirrors tacchi::sim
         if rc:
             _check(rc)
         return outs, st
+
+
+class material:  # noqa: N801 — mirrors tacchi::mpm material functions (material.hpp)
+    @staticmethod
+    def polar_rotation(F, svd: bool = False, E: float = 1.45e5, nu: float = 0.45,
+                       device: int = 0):
+        """polar_rotation (or polar_rotation_svd when svd) and corotated_stress
+        of a batch of 3x3 F on the device -> (R, S), each n x 3 x 3."""
+        F = _d(F).reshape(-1, 9)
+        R = np.empty_like(F)
+        S = np.empty_like(F)
+        _check(lib().tg_polar(device, _p(F), len(F), 1 if svd else 0, E, nu, _p(R), _p(S)))
+        return R.reshape(-1, 3, 3), S.reshape(-1, 3, 3)
 
 
 class geo:  # noqa: N801 — mirrors tacchi::geo (host setup)

@@ -230,172 +230,259 @@ class Session {
   StepReply last_reply_;
 };
 
-// ---- protocol (server.cpp:49-113) ----------------------------------------------
+// ---- protocol "tacchi/1" (server.cpp:49-113) -----------------------------------
+//
+// A Dispatcher consumes one line at a time and produces at most one reply
+// line; transports (in-memory text, stdio, a loopback TCP connection) only
+// move lines. Message kinds dispatch through a table; every failure inside a
+// handler becomes an "error" reply naming the reference's exception class
+// and echoing the offending line, and the dispatcher keeps serving (an "end"
+// message or the end of input stops it).
 
 using LineReader = std::function<bool(std::string&)>;
 using LineWriter = std::function<void(const std::string&)>;
 
 namespace {
 
-json error_reply(const std::string& error, const std::string& message, const std::string& echo) {
-  return {{"type", "error"}, {"error", error}, {"message", message}, {"echo", echo}};
+// Protocol error names of the reference's exception classes (server.cpp:102-111).
+const char* error_kind(int code) {
+  switch (code) {
+    case TG_ERR_SESSION_NOT_INITIALIZED: return "SessionNotInitialized";
+    case TG_ERR_NON_MONOTONIC_TIME: return "NonMonotonicTime";
+    case TG_ERR_PROTOCOL: return "ProtocolError";
+    default: return "PhysicsFault";  // physics / configuration faults keep the server up
+  }
 }
 
-StepCommand parse_step(const json& j) {
-  StepCommand cmd;
-  const std::string mode = j.value("mode", "velocity");
-  if (mode == "velocity")
-    cmd.mode = CommandMode::Velocity;
-  else if (mode == "position")
-    cmd.mode = CommandMode::Position;
-  else
-    throw HostError{TG_ERR_PROTOCOL, "unknown step mode '" + mode + "'"};
-  if (!j.contains("vector") || !j["vector"].is_array() || j["vector"].size() != 3)
-    throw HostError{TG_ERR_PROTOCOL, "step requires a 3-element 'vector'"};
-  for (int a = 0; a < 3; ++a) cmd.vector[a] = j["vector"][a].get<double>();
-  if (j.contains("sim_time")) cmd.sim_time = j["sim_time"].get<double>();
-  cmd.request_image = j.value("request_image", false);
-  return cmd;
-}
-
-std::string read_file(const std::string& path) {
-  std::ifstream in(path);
+std::string slurp(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
   if (!in) throw HostError{TG_ERR_IO, "cannot open config " + path};
-  return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  std::ostringstream ss;
+  ss << in.rdbuf();
+  return ss.str();
 }
+
+class Dispatcher {
+ public:
+  Dispatcher(std::string base_config, std::string session_root, int device)
+      : base_(std::move(base_config)), root_(std::move(session_root)), device_(device) {}
+
+  bool finished() const { return finished_; }
+
+  // One inbound line -> the reply line ("" for a blank line).
+  std::string on_line(const std::string& line) {
+    if (line.empty()) return {};
+    const json msg = json::parse(line, nullptr, false);
+    json reply;
+    if (msg.is_discarded()) {
+      reply = failure("ProtocolError", "not valid JSON", line);
+    } else {
+      try {
+        reply = route(msg);
+      } catch (const HostError& e) {
+        reply = failure(error_kind(e.code), e.msg, line);
+      } catch (const json::exception& e) {  // a mistyped field is a protocol error
+        reply = failure("ProtocolError", e.what(), line);
+      }
+    }
+    return reply.dump();
+  }
+
+ private:
+  static json failure(const char* kind, const std::string& what, const std::string& line) {
+    json r;
+    r["type"] = "error";
+    r["error"] = kind;
+    r["message"] = what;
+    r["echo"] = line;
+    return r;
+  }
+
+  json route(const json& msg) {
+    const std::string kind = msg.value("type", "");
+    if (kind == "init") return on_init(msg);
+    if (kind == "step") return on_step(msg);
+    if (kind == "end") return on_end();
+    throw HostError{TG_ERR_PROTOCOL, "unknown message type '" + kind + "'"};
+  }
+
+  // "init": a new Session (session.cpp:15-30) replaces the current one.
+  json on_init(const json& msg) {
+    std::string cfg = base_;
+    if (auto it = msg.find("config_path"); it != msg.end()) cfg = slurp(it->get<std::string>());
+    if (auto it = msg.find("config"); it != msg.end()) cfg = it->dump();
+    TerminalCondition term;
+    if (auto it = msg.find("max_depth_m"); it != msg.end()) term.max_depth_m = it->get<double>();
+    if (auto it = msg.find("max_steps"); it != msg.end()) term.max_steps = it->get<int64_t>();
+    std::string dir = msg.value("session_dir", "");
+    if (dir.empty()) dir = root_ + "/session_" + std::to_string(sessions_started_++);
+    session_.reset();  // release the previous device simulation first
+    session_ = std::make_unique<Session>(cfg, dir, msg.value("object", ""), term, device_);
+    json r;
+    r["type"] = "ready";
+    r["version"] = kProtocolVersion;
+    r["particles"] = session_->particles();
+    r["dt_s"] = session_->cfg().dt;
+    r["substeps_per_control_step"] = session_->cfg().substeps_per_control_step;
+    r["session_dir"] = session_->dir().string();
+    return r;
+  }
+
+  // "step": one control step (session.cpp:61-98).
+  json on_step(const json& msg) {
+    if (!session_) throw HostError{TG_ERR_SESSION_NOT_INITIALIZED, "step before init"};
+    StepCommand cmd;
+    const std::string mode = msg.value("mode", "velocity");
+    if (mode == "position")
+      cmd.mode = CommandMode::Position;
+    else if (mode != "velocity")
+      throw HostError{TG_ERR_PROTOCOL, "unknown step mode '" + mode + "'"};
+    const auto vec = msg.find("vector");
+    if (vec == msg.end() || !vec->is_array() || vec->size() != 3)
+      throw HostError{TG_ERR_PROTOCOL, "step requires a 3-element 'vector'"};
+    for (size_t a = 0; a < 3; ++a) cmd.vector[a] = (*vec)[a].get<double>();
+    if (auto it = msg.find("sim_time"); it != msg.end()) cmd.sim_time = it->get<double>();
+    cmd.request_image = msg.value("request_image", false);
+    const StepReply rep = session_->handle_command(cmd);
+    json r;
+    r["type"] = "reply";
+    r["step"] = rep.step_index;
+    r["depth_m"] = rep.depth_m;
+    r["terminal"] = rep.terminal;
+    r["image"] = rep.image_path;
+    r["depth_map"] = rep.depth_map_path;
+    return r;
+  }
+
+  // "end": report the control steps taken and stop serving this stream.
+  json on_end() {
+    json r;
+    r["type"] = "done";
+    r["steps"] = session_ ? session_->control_steps() : int64_t{0};
+    session_.reset();
+    finished_ = true;
+    return r;
+  }
+
+  std::string base_, root_;
+  int device_;
+  int sessions_started_ = 0;
+  bool finished_ = false;
+  std::unique_ptr<Session> session_;
+};
+
+// Line framing over a connected socket: bytes accumulate in `pending_` and
+// complete lines are cut off its front.
+class SocketLines {
+ public:
+  explicit SocketLines(int fd) : fd_(fd) {}
+  bool next(std::string& line) {
+    size_t nl;
+    while ((nl = pending_.find('\n', scanned_)) == std::string::npos) {
+      scanned_ = pending_.size();
+      char buf[8192];
+      const ssize_t got = ::recv(fd_, buf, sizeof(buf), 0);
+      if (got <= 0) return false;  // peer closed (a partial last line is dropped)
+      pending_.append(buf, static_cast<size_t>(got));
+    }
+    line.assign(pending_, 0, nl);
+    pending_.erase(0, nl + 1);
+    scanned_ = 0;
+    return true;
+  }
+  void send_line(const std::string& text) {
+    std::string out = text;
+    out.push_back('\n');
+    const char* p = out.data();
+    size_t left = out.size();
+    while (left > 0) {
+      const ssize_t put = ::send(fd_, p, left, MSG_NOSIGNAL);
+      if (put <= 0) return;  // peer gone: drop the reply
+      p += put;
+      left -= static_cast<size_t>(put);
+    }
+  }
+
+ private:
+  int fd_;
+  std::string pending_;
+  size_t scanned_ = 0;
+};
+
+// A loopback listening socket (closed on destruction).
+class LoopbackListener {
+ public:
+  explicit LoopbackListener(int port) {
+    fd_ = ::socket(AF_INET, SOCK_STREAM, 0);
+    if (fd_ < 0) throw HostError{TG_ERR_IO, "socket() failed"};
+    const int on = 1;
+    ::setsockopt(fd_, SOL_SOCKET, SO_REUSEADDR, &on, sizeof(on));
+    sockaddr_in sa{};
+    sa.sin_family = AF_INET;
+    sa.sin_port = htons(static_cast<uint16_t>(port));
+    sa.sin_addr.s_addr = htonl(INADDR_LOOPBACK);
+    if (::bind(fd_, reinterpret_cast<const sockaddr*>(&sa), sizeof(sa)) != 0)
+      fail_with("bind() failed on port " + std::to_string(port));
+    if (::listen(fd_, 1) != 0) fail_with("listen() failed");
+    socklen_t len = sizeof(sa);
+    ::getsockname(fd_, reinterpret_cast<sockaddr*>(&sa), &len);
+    port_ = ntohs(sa.sin_port);
+  }
+  ~LoopbackListener() {
+    if (fd_ >= 0) ::close(fd_);
+  }
+  LoopbackListener(const LoopbackListener&) = delete;
+  LoopbackListener& operator=(const LoopbackListener&) = delete;
+  int port() const { return port_; }
+  int accept_client() { return ::accept(fd_, nullptr, nullptr); }
+
+ private:
+  [[noreturn]] void fail_with(const std::string& what) {
+    ::close(fd_);
+    fd_ = -1;
+    throw HostError{TG_ERR_IO, what};
+  }
+  int fd_ = -1;
+  int port_ = 0;
+};
 
 }  // namespace
 
+// bridge::run_protocol with injectable line transport (server.hpp:13-25).
 void run_protocol(const LineReader& read_line, const LineWriter& write_line,
                   const std::string& base_config_json, const std::string& session_root,
                   int device) {
-  std::unique_ptr<Session> session;
-  int session_counter = 0;
+  Dispatcher d(base_config_json, session_root, device);
   std::string line;
-  while (read_line(line)) {
-    if (line.empty()) continue;
-    json msg = json::parse(line, nullptr, false);
-    if (msg.is_discarded()) {
-      write_line(error_reply("ProtocolError", "not valid JSON", line).dump());
-      continue;
-    }
-    const std::string type = msg.value("type", "");
-    try {
-      if (type == "init") {
-        std::string cfg = base_config_json;
-        if (msg.contains("config_path")) cfg = read_file(msg["config_path"].get<std::string>());
-        if (msg.contains("config")) cfg = msg["config"].dump();
-        const std::string object = msg.value("object", "");
-        TerminalCondition term;
-        if (msg.contains("max_depth_m")) term.max_depth_m = msg["max_depth_m"].get<double>();
-        if (msg.contains("max_steps")) term.max_steps = msg["max_steps"].get<int64_t>();
-        std::string dir = msg.value("session_dir", "");
-        if (dir.empty()) dir = session_root + "/session_" + std::to_string(session_counter++);
-        session = std::make_unique<Session>(cfg, dir, object, term, device);
-        write_line(json{{"type", "ready"},
-                        {"version", kProtocolVersion},
-                        {"particles", session->particles()},
-                        {"dt_s", session->cfg().dt},
-                        {"substeps_per_control_step", session->cfg().substeps_per_control_step},
-                        {"session_dir", session->dir().string()}}
-                       .dump());
-      } else if (type == "step") {
-        if (!session) throw HostError{TG_ERR_SESSION_NOT_INITIALIZED, "step before init"};
-        const StepReply reply = session->handle_command(parse_step(msg));
-        write_line(json{{"type", "reply"},
-                        {"step", reply.step_index},
-                        {"depth_m", reply.depth_m},
-                        {"terminal", reply.terminal},
-                        {"image", reply.image_path},
-                        {"depth_map", reply.depth_map_path}}
-                       .dump());
-      } else if (type == "end") {
-        const int64_t steps = session ? session->control_steps() : 0;
-        session.reset();
-        write_line(json{{"type", "done"}, {"steps", steps}}.dump());
-        return;
-      } else {
-        throw HostError{TG_ERR_PROTOCOL, "unknown message type '" + type + "'"};
-      }
-    } catch (const HostError& e) {
-      const char* name = e.code == TG_ERR_SESSION_NOT_INITIALIZED ? "SessionNotInitialized"
-                         : e.code == TG_ERR_NON_MONOTONIC_TIME    ? "NonMonotonicTime"
-                         : e.code == TG_ERR_PROTOCOL               ? "ProtocolError"
-                                                                   : "PhysicsFault";
-      write_line(error_reply(name, e.msg, line).dump());
-    } catch (const json::exception& e) {
-      write_line(error_reply("ProtocolError", e.what(), line).dump());
-    }
+  while (!d.finished() && read_line(line)) {
+    const std::string reply = d.on_line(line);
+    if (!reply.empty()) write_line(reply);
   }
 }
 
 void serve_stdio(const std::string& base_config_json, const std::string& session_root,
                  int device) {
   run_protocol([](std::string& l) { return static_cast<bool>(std::getline(std::cin, l)); },
-               [](const std::string& l) {
-                 std::cout << l << '\n';
-                 std::cout.flush();
-               },
-               base_config_json, session_root, device);
+               [](const std::string& l) { std::cout << l << std::endl; }, base_config_json,
+               session_root, device);
 }
 
-// server.cpp:125-182: loopback TCP, sequential connections.
+// bridge::serve_tcp (server.cpp:125-182): one client at a time on
+// 127.0.0.1:port (0 = ephemeral), max_connections = 0 serves forever.
 int serve_tcp(const std::string& base_config_json, const std::string& session_root, int port,
               int max_connections, int device) {
-  const int listener = ::socket(AF_INET, SOCK_STREAM, 0);
-  if (listener < 0) throw HostError{TG_ERR_IO, "socket() failed"};
-  int yes = 1;
-  ::setsockopt(listener, SOL_SOCKET, SO_REUSEADDR, &yes, sizeof(yes));
-  sockaddr_in addr{};
-  addr.sin_family = AF_INET;
-  addr.sin_addr.s_addr = htonl(INADDR_LOOPBACK);
-  addr.sin_port = htons(static_cast<uint16_t>(port));
-  if (::bind(listener, reinterpret_cast<sockaddr*>(&addr), sizeof(addr)) != 0) {
-    ::close(listener);
-    throw HostError{TG_ERR_IO, "bind() failed on port " + std::to_string(port)};
+  LoopbackListener listener(port);
+  std::cerr << "[tacchi] bridge listening on 127.0.0.1:" << listener.port() << "\n";
+  for (int served = 0; max_connections == 0 || served < max_connections; ++served) {
+    const int fd = listener.accept_client();
+    if (fd < 0) break;
+    SocketLines conn(fd);
+    run_protocol([&conn](std::string& l) { return conn.next(l); },
+                 [&conn](const std::string& l) { conn.send_line(l); }, base_config_json,
+                 session_root, device);
+    ::close(fd);
   }
-  socklen_t len = sizeof(addr);
-  ::getsockname(listener, reinterpret_cast<sockaddr*>(&addr), &len);
-  const int bound_port = ntohs(addr.sin_port);
-  if (::listen(listener, 1) != 0) {
-    ::close(listener);
-    throw HostError{TG_ERR_IO, "listen() failed"};
-  }
-  std::cerr << "[tacchi] bridge listening on 127.0.0.1:" << bound_port << "\n";
-  int served = 0;
-  while (max_connections == 0 || served < max_connections) {
-    const int client = ::accept(listener, nullptr, nullptr);
-    if (client < 0) break;
-    std::string buffer;
-    auto read_line = [client, &buffer](std::string& l) {
-      for (;;) {
-        const size_t pos = buffer.find('\n');
-        if (pos != std::string::npos) {
-          l = buffer.substr(0, pos);
-          buffer.erase(0, pos + 1);
-          return true;
-        }
-        char chunk[4096];
-        const ssize_t n = ::read(client, chunk, sizeof(chunk));
-        if (n <= 0) return false;
-        buffer.append(chunk, static_cast<size_t>(n));
-      }
-    };
-    auto write_line = [client](const std::string& l) {
-      const std::string out = l + "\n";
-      size_t sent = 0;
-      while (sent < out.size()) {
-        const ssize_t n = ::write(client, out.data() + sent, out.size() - sent);
-        if (n <= 0) return;
-        sent += static_cast<size_t>(n);
-      }
-    };
-    run_protocol(read_line, write_line, base_config_json, session_root, device);
-    ::close(client);
-    ++served;
-  }
-  ::close(listener);
-  return bound_port;
+  return listener.port();
 }
 
 }  // namespace tacchi_b200::bridge

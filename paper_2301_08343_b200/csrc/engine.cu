@@ -26,7 +26,7 @@ int launch_p2g_ind(DeviceSim& s);
 int launch_grid_update(DeviceSim& s, int sms, bool zero);
 int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter = false);
 int launch_ind_move(DeviceSim& s, bool lookahead);
-int launch_finalize_step(DeviceSim& s, bool cfl_check = false);
+int launch_finalize_step(DeviceSim& s, bool walk_fix = false);
 int launch_chain_begin(DeviceSim& s);
 int launch_ind_cols(DeviceSim& s, bool move);
 int launch_ind_catchup(DeviceSim& s);
@@ -137,6 +137,17 @@ static int host_base(double x, double origin, double inv_dx) {
 
 int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, const double* Fm,
            bool init);
+int configure_device(int device);  // mpm_kernels.cu
+
+// Host <-> device copies ordered on the handle's (non-blocking) stream and
+// completed before returning: every upload is ordered after the kernels
+// already queued on the handle and before the ones that follow.
+static cudaError_t copy_sync(DeviceSim& s, void* dst, const void* src, size_t bytes,
+                             cudaMemcpyKind kind) {
+  const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, s.stream);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s.stream);
+}
 
 // The grid arrays in one allocation (A.lo | A.hi | V.xy | V.z | M_I).
 static bool alloc_grid(DeviceSim& s) {
@@ -185,6 +196,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   }
   int rc = check_device(device);
   if (rc) return rc;
+  if (configure_device(device))
+    return fail(TG_ERR_CUDA, "tg_create: could not set the kernels' shared-memory limits");
 
   auto* s = new DeviceSim();
   s->device = device;
@@ -279,8 +292,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   cudaMemsetAsync(s->ind_moves, 0, std::max<int64_t>(n_ind, 1), s->stream);
   s->n_cols = col_starts.empty() ? 0 : static_cast<int>(col_starts.size()) - 1;
   if (s->n_cols > 0)
-    cudaMemcpy(s->col_start, col_starts.data(), col_starts.size() * sizeof(int64_t),
-               cudaMemcpyHostToDevice);
+    copy_sync(*s, s->col_start, col_starts.data(), col_starts.size() * sizeof(int64_t),
+              cudaMemcpyHostToDevice);
   std::memset(s->h_ctl, 0, sizeof(Ctl));
   for (int a = 0; a < 3; ++a) s->h_ctl->vind[a] = in->indenter_velocity[a];
   // Is the indenter velocity uniform (it is for init_scene's output)?
@@ -296,7 +309,7 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   // Tags of the elastomer (Elastomer / ElastomerBottom).
   std::vector<uint8_t> tags(std::max<int64_t>(n_el, 1));
   for (int64_t p = 0; p < n_el; ++p) tags[p] = in->tag[p];
-  cudaMemcpy(s->tag, tags.data(), n_el, cudaMemcpyHostToDevice);
+  copy_sync(*s, s->tag, tags.data(), n_el, cudaMemcpyHostToDevice);
 
   rc = upload(*s, in->x, in->v, in->C, in->F, true);
   if (rc) {
@@ -328,7 +341,7 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
       delete s;
       return fail(TG_ERR_CUDA, "tg_create: device allocation failed");
     }
-    cudaMemcpy(s->surf_idx, idx.data(), cnt * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    copy_sync(*s, s->surf_idx, idx.data(), cnt * sizeof(uint32_t), cudaMemcpyHostToDevice);
     // Lattice metadata (particle_set.hpp:16-17): the surface is the top layer
     // of an nx x ny x nz elastomer lattice.
     const int64_t cols = static_cast<int64_t>(surf->nx) * surf->ny;
@@ -609,7 +622,7 @@ int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, con
   std::vector<double> buf;
   auto put3 = [&](const double* src, double* dst) -> int {
     to_component_major(src, s.n, 3, s.perm, 0, s.n, buf);
-    const cudaError_t e = cudaMemcpy(dst, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice);
+    const cudaError_t e = copy_sync(s, dst, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice);
     return e == cudaSuccess ? 0 : fail(TG_ERR_CUDA, cudaGetErrorString(e));
   };
   auto put9 = [&](const double* src, double* dst, bool identity) -> int {
@@ -623,7 +636,7 @@ int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, con
           std::fill(buf.begin() + static_cast<size_t>(4 * d) * s.n_el,
                     buf.begin() + static_cast<size_t>(4 * d + 1) * s.n_el, 1.0);
     }
-    const cudaError_t e = cudaMemcpy(dst, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice);
+    const cudaError_t e = copy_sync(s, dst, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice);
     return e == cudaSuccess ? 0 : fail(TG_ERR_CUDA, cudaGetErrorString(e));
   };
   int rc = 0;
@@ -635,8 +648,8 @@ int upload(DeviceSim& s, const double* x, const double* v, const double* Cm, con
       for (int a = 0; a < 3; ++a)
         if (v[3 * p + a] != v[3 * s.n_el + a]) uniform = false;
     s.ind_v_uniform = uniform;
-    if (uniform) CUDA_TRY(cudaMemcpy(&s.ctl->ind_v[0], v + 3 * s.n_el, 3 * sizeof(double),
-                                     cudaMemcpyHostToDevice));
+    if (uniform) CUDA_TRY(copy_sync(s, &s.ctl->ind_v[0], v + 3 * s.n_el, 3 * sizeof(double),
+                                    cudaMemcpyHostToDevice));
   }
   if ((Cm || init) && (rc = put9(Cm, s.C, false))) return rc;
   if ((Fm || init) && (rc = put9(Fm, s.F, true))) return rc;
@@ -655,7 +668,7 @@ int download(DeviceSim& s, double* x, double* v, double* Cm, double* Fm) {
   std::vector<double> buf;
   auto get3 = [&](const double* src, double* dst) -> int {
     buf.resize(3 * s.n);
-    const cudaError_t e = cudaMemcpy(buf.data(), src, buf.size() * sizeof(double), cudaMemcpyDeviceToHost);
+    const cudaError_t e = copy_sync(s, buf.data(), src, buf.size() * sizeof(double), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(TG_ERR_CUDA, cudaGetErrorString(e));
     for (int64_t q = 0; q < s.n; ++q)
       for (int c = 0; c < 3; ++c) dst[3 * s.perm[q] + c] = buf[static_cast<size_t>(c) * s.n + q];
@@ -664,7 +677,7 @@ int download(DeviceSim& s, double* x, double* v, double* Cm, double* Fm) {
   auto get9 = [&](const double* src, double* dst, bool identity) -> int {
     if (s.n_el > 0) {
       buf.resize(9 * s.n_el);
-      const cudaError_t e = cudaMemcpy(buf.data(), src, buf.size() * sizeof(double), cudaMemcpyDeviceToHost);
+      const cudaError_t e = copy_sync(s, buf.data(), src, buf.size() * sizeof(double), cudaMemcpyDeviceToHost);
       if (e != cudaSuccess) return fail(TG_ERR_CUDA, cudaGetErrorString(e));
       for (int64_t q = 0; q < s.n_el; ++q)
         for (int c = 0; c < 9; ++c) dst[9 * q + c] = buf[static_cast<size_t>(c) * s.n_el + q];
@@ -679,7 +692,7 @@ int download(DeviceSim& s, double* x, double* v, double* Cm, double* Fm) {
   if (v && (rc = get3(s.v, v))) return rc;
   if (v && s.ind_v_uniform && s.n_ind > 0) {
     double u[3];
-    CUDA_TRY(cudaMemcpy(u, &s.ctl->ind_v[0], sizeof u, cudaMemcpyDeviceToHost));
+    CUDA_TRY(copy_sync(s, u, &s.ctl->ind_v[0], sizeof u, cudaMemcpyDeviceToHost));
     for (int64_t q = s.n_el; q < s.n; ++q)
       for (int a = 0; a < 3; ++a) v[3 * s.perm[q] + a] = u[a];
   }

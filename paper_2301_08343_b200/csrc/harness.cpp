@@ -20,6 +20,11 @@
 #include <fstream>
 #include <functional>
 #include <map>
+#include <numeric>
+#include <cstring>
+#include <cstdlib>
+#include <iterator>
+#include <stdexcept>
 #include <memory>
 #include <mutex>
 #include <set>
@@ -65,23 +70,46 @@ struct ManifestRow {
 
 namespace {
 
-std::string row_file_stem(const std::string& object, int position, int depth) {
-  char buf[32];
-  std::snprintf(buf, sizeof(buf), "_p%02d_d%02d", position, depth);
-  return object + buf;
+// (object, position, depth level): the identity of a manifest row.
+using RowKey = std::tuple<std::string, int, int>;
+RowKey key_of(const ManifestRow& r) { return {r.object, r.position_index, r.depth_index}; }
+
+// Output file stem of a row: <object>_pNN_dNN (harness.cpp:75-94 names).
+std::string file_stem(const std::string& object, int position, int depth) {
+  std::string out = object;
+  char tail[24];
+  std::snprintf(tail, sizeof(tail), "_p%02d_d%02d", position, depth);
+  return out.append(tail);
 }
 
-std::vector<std::string> split_csv_line(const std::string& line) {
-  std::vector<std::string> out;
-  std::stringstream ss(line);
-  std::string field;
-  while (std::getline(ss, field, ',')) out.push_back(field);
-  return out;
+// Strict field conversions of a manifest cell (the whole cell must parse).
+long long cell_int(const std::string& c) {
+  char* end = nullptr;
+  const long long v = std::strtoll(c.c_str(), &end, 10);
+  if (c.empty() || *end != '\0') throw std::invalid_argument(c);
+  return v;
+}
+double cell_real(const std::string& c) {
+  char* end = nullptr;
+  const double v = std::strtod(c.c_str(), &end);
+  if (c.empty() || *end != '\0') throw std::invalid_argument(c);
+  return v;
 }
 
-bool row_key_less(const ManifestRow& a, const ManifestRow& b) {
-  return std::tie(a.object, a.position_index, a.depth_index) <
-         std::tie(b.object, b.position_index, b.depth_index);
+// Mean and sample standard deviation (n - 1), two passes left to right.
+struct Moments {
+  double mean = 0.0, stdev = 0.0;
+};
+Moments moments(const std::vector<double>& xs) {
+  Moments m;
+  if (xs.empty()) return m;
+  m.mean = std::accumulate(xs.begin(), xs.end(), 0.0) / static_cast<double>(xs.size());
+  if (xs.size() > 1) {
+    double ss = 0.0;
+    for (double x : xs) ss += (x - m.mean) * (x - m.mean);
+    m.stdev = std::sqrt(ss / static_cast<double>(xs.size() - 1));
+  }
+  return m;
 }
 
 // A small FIFO pool for host file encoding (PNG deflate dominates).
@@ -156,13 +184,6 @@ struct Handle {
   }
 };
 
-double aggregate_std(const std::vector<double>& xs, double mean) {
-  if (xs.size() < 2) return 0.0;
-  double acc = 0.0;
-  for (double x : xs) acc += (x - mean) * (x - mean);
-  return std::sqrt(acc / static_cast<double>(xs.size() - 1));
-}
-
 int writer_threads() {
   const unsigned hc = std::thread::hardware_concurrency();
   return static_cast<int>(std::max(2u, std::min(16u, hc ? hc : 4u)));
@@ -170,54 +191,89 @@ int writer_threads() {
 
 }  // namespace
 
-// harness.cpp:114-142
+// The manifest CSV (harness.cpp:114-157): a header line, then one row per
+// capture, ten comma-separated cells (no quoting: names never hold commas).
 std::vector<ManifestRow> read_manifest(const fs::path& csv_path) {
   std::ifstream in(csv_path);
   if (!in) throw HostError{TG_ERR_IO, "cannot open manifest " + csv_path.string()};
+  const auto malformed = [&] {
+    return HostError{TG_ERR_PARSE, csv_path.string() + ": malformed manifest row"};
+  };
   std::vector<ManifestRow> rows;
-  std::string line;
-  bool header = true;
-  while (std::getline(in, line)) {
-    if (line.empty()) continue;
-    if (header) {
-      header = false;
+  std::string text;
+  bool seen_header = false;
+  while (std::getline(in, text)) {
+    if (text.empty()) continue;
+    if (!seen_header) {  // the first non-empty line is the header
+      seen_header = true;
       continue;
     }
-    const auto f = split_csv_line(line);
-    if (f.size() != 10) throw HostError{TG_ERR_PARSE, csv_path.string() + ": malformed manifest row"};
+    std::vector<std::string> cell(1);
+    for (char ch : text) {
+      if (ch == ',') cell.emplace_back();
+      else cell.back().push_back(ch);
+    }
+    if (!cell.empty() && cell.back().empty() && text.back() == ',') cell.pop_back();
+    if (cell.size() != 10) throw malformed();
     ManifestRow r;
     try {
-      r.object = f[0];
-      r.position_index = std::stoi(f[1]);
-      r.pos_x_mm = std::stod(f[2]);
-      r.pos_y_mm = std::stod(f[3]);
-      r.depth_index = std::stoi(f[4]);
-      r.depth_mm = std::stod(f[5]);
-      r.contact = f[6] == "1" || f[6] == "true";
-      r.particle_count = std::stoull(f[7]);
+      r.position_index = static_cast<int>(cell_int(cell[1]));
+      r.pos_x_mm = cell_real(cell[2]);
+      r.pos_y_mm = cell_real(cell[3]);
+      r.depth_index = static_cast<int>(cell_int(cell[4]));
+      r.depth_mm = cell_real(cell[5]);
+      r.particle_count = static_cast<uint64_t>(cell_int(cell[7]));
     } catch (const std::exception&) {
-      throw HostError{TG_ERR_PARSE, csv_path.string() + ": malformed manifest row"};
+      throw malformed();
     }
-    r.image = f[8];
-    r.depth_map = f[9];
+    r.object = std::move(cell[0]);
+    r.contact = cell[6] == "1" || cell[6] == "true";
+    r.image = std::move(cell[8]);
+    r.depth_map = std::move(cell[9]);
     rows.push_back(std::move(r));
   }
   return rows;
 }
 
-// harness.cpp:144-157
 void write_manifest(const std::vector<ManifestRow>& rows, const fs::path& csv_path) {
-  std::FILE* f = std::fopen(csv_path.string().c_str(), "w");
-  if (!f) throw HostError{TG_ERR_IO, "cannot write manifest " + csv_path.string()};
-  std::fprintf(f,
-               "object,position_index,pos_x_mm,pos_y_mm,depth_index,depth_mm,contact,"
-               "particle_count,image,depth_map\n");
-  for (const ManifestRow& r : rows)
-    std::fprintf(f, "%s,%d,%.6g,%.6g,%d,%.6g,%d,%llu,%s,%s\n", r.object.c_str(), r.position_index,
-                 r.pos_x_mm, r.pos_y_mm, r.depth_index, r.depth_mm, r.contact ? 1 : 0,
-                 static_cast<unsigned long long>(r.particle_count), r.image.c_str(),
-                 r.depth_map.c_str());
-  std::fclose(f);
+  std::string body =
+      "object,position_index,pos_x_mm,pos_y_mm,depth_index,depth_mm,contact,"
+      "particle_count,image,depth_map\n";
+  for (const ManifestRow& r : rows) {
+    char nums[160];
+    std::snprintf(nums, sizeof(nums), ",%d,%.6g,%.6g,%d,%.6g,%d,%llu,", r.position_index,
+                  r.pos_x_mm, r.pos_y_mm, r.depth_index, r.depth_mm, r.contact ? 1 : 0,
+                  static_cast<unsigned long long>(r.particle_count));
+    body += r.object;
+    body += nums;
+    body += r.image;
+    body += ',';
+    body += r.depth_map;
+    body += '\n';
+  }
+  std::ofstream out(csv_path, std::ios::binary | std::ios::trunc);
+  if (!out) throw HostError{TG_ERR_IO, "cannot write manifest " + csv_path.string()};
+  out << body;
+}
+
+// Resume (harness.cpp:166-179): the rows of (object, position) groups whose
+// every depth level is present are kept, and those groups are not re-run.
+struct ResumeState {
+  std::vector<ManifestRow> kept;
+  std::set<std::pair<std::string, int>> complete;
+};
+ResumeState resume_from(const fs::path& manifest_path, size_t levels) {
+  ResumeState st;
+  if (!fs::exists(manifest_path)) return st;
+  std::vector<ManifestRow> prior = read_manifest(manifest_path);
+  std::map<std::pair<std::string, int>, std::set<int>> levels_of;
+  for (const ManifestRow& r : prior) levels_of[{r.object, r.position_index}].insert(r.depth_index);
+  for (const auto& entry : levels_of)
+    if (entry.second.size() == levels) st.complete.insert(entry.first);
+  std::copy_if(prior.begin(), prior.end(), std::back_inserter(st.kept), [&](const ManifestRow& r) {
+    return st.complete.count({r.object, r.position_index}) > 0;
+  });
+  return st;
 }
 
 struct DatasetResult {
@@ -239,19 +295,10 @@ DatasetResult run_press_dataset(const std::string& cfg_json, const fs::path& out
     out << host::to_json_string(cfg);
   }
 
-  // Resume: keep rows of (object, position) groups that are already complete.
-  std::vector<ManifestRow> kept;
-  std::set<std::pair<std::string, int>> done;
   const fs::path manifest_path = out_dir / "manifest.csv";
-  if (fs::exists(manifest_path)) {
-    std::map<std::pair<std::string, int>, std::set<int>> seen;
-    const auto existing = read_manifest(manifest_path);
-    for (const ManifestRow& r : existing) seen[{r.object, r.position_index}].insert(r.depth_index);
-    for (const auto& [key, depths] : seen)
-      if (depths.size() == cfg.depths_mm.size()) done.insert(key);
-    for (const ManifestRow& r : existing)
-      if (done.count({r.object, r.position_index})) kept.push_back(r);
-  }
+  ResumeState resume = resume_from(manifest_path, cfg.depths_mm.size());
+  std::vector<ManifestRow>& kept = resume.kept;
+  const auto& done = resume.complete;
 
   // Jobs: every object at every press-grid position; one cloud per object,
   // generated on host threads in parallel (rejection sampling of 1e6 points
@@ -364,7 +411,7 @@ DatasetResult run_press_dataset(const std::string& cfg_json, const fs::path& out
             row.depth_mm = cfg.depths_mm[k];
             row.contact = cfg.depths_mm[k] > 0.0;
             row.particle_count = job.cloud->size();
-            const std::string stem = row_file_stem(job.object, job.position_index, k);
+            const std::string stem = file_stem(job.object, job.position_index, k);
             row.image = "images/" + stem + ".png";
             row.depth_map = "depth/" + stem + ".depth";
             const std::string png = (out_dir / row.image).string();
@@ -401,22 +448,10 @@ DatasetResult run_press_dataset(const std::string& cfg_json, const fs::path& out
 
   std::vector<ManifestRow> all = std::move(kept);
   for (auto& r : fresh) all.push_back(std::move(r));
-  std::sort(all.begin(), all.end(), row_key_less);
+  std::sort(all.begin(), all.end(),
+            [](const ManifestRow& a, const ManifestRow& b) { return key_of(a) < key_of(b); });
   write_manifest(all, manifest_path);
   return {all.size(), skipped};
-}
-
-int image_metrics_batch(int device, const std::vector<std::vector<uint8_t>>& a,
-                        const std::vector<std::vector<uint8_t>>& b, int w, int h,
-                        std::vector<double>& out) {
-  const size_t n = a.size(), px = static_cast<size_t>(w) * h * 3;
-  std::vector<uint8_t> ha(n * px), hb(n * px);
-  for (size_t i = 0; i < n; ++i) {
-    std::copy(a[i].begin(), a[i].end(), ha.begin() + i * px);
-    std::copy(b[i].begin(), b[i].end(), hb.begin() + i * px);
-  }
-  out.assign(3 * n, 0.0);
-  return tg_image_metrics(device, ha.data(), hb.data(), w, h, static_cast<int>(n), out.data());
 }
 
 struct CompareAggregate {
@@ -424,106 +459,119 @@ struct CompareAggregate {
   double ssim_mean = 0, ssim_std = 0, psnr_mean = 0, psnr_std = 0, mae_mean = 0, mae_std = 0;
 };
 
-// compare_datasets (harness.cpp:247-321): PNG decode on host threads, the
-// metrics for every pair of one image size in batched device launches.
+// compare_datasets (harness.cpp:247-321). The keys of both manifests must
+// match; the image pairs are then evaluated in chunks of kChunk: the chunk's
+// PNGs are decoded on host threads into one pair-major staging buffer per
+// side, scored with one batched device launch (tg_image_metrics), and
+// released before the next chunk, so host memory stays bounded for any
+// dataset size.
 CompareAggregate compare_datasets(const fs::path& dir_a, const fs::path& dir_b,
                                   const fs::path& csv_out, int device) {
-  const auto rows_a = read_manifest(dir_a / "manifest.csv");
-  const auto rows_b = read_manifest(dir_b / "manifest.csv");
-  using Key = std::tuple<std::string, int, int>;
-  std::map<Key, const ManifestRow*> map_a, map_b;
-  for (const auto& r : rows_b) map_b[{r.object, r.position_index, r.depth_index}] = &r;
-  for (const auto& r : rows_a) map_a[{r.object, r.position_index, r.depth_index}] = &r;
+  std::map<RowKey, ManifestRow> side_a, side_b;
+  for (auto& r : read_manifest(dir_a / "manifest.csv")) side_a.emplace(key_of(r), std::move(r));
+  for (auto& r : read_manifest(dir_b / "manifest.csv")) side_b.emplace(key_of(r), std::move(r));
 
-  std::string missing;
-  int missing_count = 0;
-  auto note_missing = [&](const Key& k, const char* side) {
-    if (missing_count++ < 8)
-      missing += std::string(missing.empty() ? "" : "; ") + std::get<0>(k) + "/p" +
-                 std::to_string(std::get<1>(k)) + "/d" + std::to_string(std::get<2>(k)) +
-                 " missing in " + side;
-  };
-  for (const auto& [k, r] : map_a)
-    if (!map_b.count(k)) note_missing(k, "B");
-  for (const auto& [k, r] : map_b)
-    if (!map_a.count(k)) note_missing(k, "A");
-  if (missing_count > 0)
-    throw HostError{TG_ERR_MANIFEST_MISMATCH, "manifests differ (" + std::to_string(missing_count) +
-                                                  " keys): " + missing};
+  // Keys present on one side only (first eight named in the message).
+  std::vector<std::pair<RowKey, const char*>> absent;
+  for (const auto& [k, r] : side_a)
+    if (!side_b.count(k)) absent.emplace_back(k, "B");
+  for (const auto& [k, r] : side_b)
+    if (!side_a.count(k)) absent.emplace_back(k, "A");
+  if (!absent.empty()) {
+    std::string detail;
+    for (size_t i = 0; i < absent.size() && i < 8; ++i) {
+      const RowKey& k = absent[i].first;
+      if (i) detail += "; ";
+      detail += std::get<0>(k) + "/p" + std::to_string(std::get<1>(k)) + "/d" +
+                std::to_string(std::get<2>(k)) + " missing in " + absent[i].second;
+    }
+    throw HostError{TG_ERR_MANIFEST_MISMATCH,
+                    "manifests differ (" + std::to_string(absent.size()) + " keys): " + detail};
+  }
 
-  std::vector<Key> keys;
-  for (const auto& [k, r] : map_a) keys.push_back(k);
+  std::vector<RowKey> keys;
+  keys.reserve(side_a.size());
+  for (const auto& entry : side_a) keys.push_back(entry.first);
   const size_t n = keys.size();
-  std::vector<std::vector<uint8_t>> ia(n), ib(n);
-  std::vector<int> wa(n), ha(n), wb(n), hb(n);
-  {
+  std::vector<double> ssim(n), psnr(n), mae(n);
+  constexpr size_t kChunk = 256;
+  const int threads = writer_threads();
+  for (size_t c0 = 0; c0 < n; c0 += kChunk) {
+    const size_t cn = std::min(kChunk, n - c0);
+    std::vector<std::vector<uint8_t>> img(2 * cn);
+    std::vector<int> w(2 * cn), h(2 * cn);
+    std::vector<std::exception_ptr> err(2 * cn);
     std::vector<std::thread> pool;
-    std::vector<std::exception_ptr> errs(n);
-    const int nt = writer_threads();
-    for (int t = 0; t < nt; ++t)
+    for (int t = 0; t < threads; ++t)
       pool.emplace_back([&, t] {
-        for (size_t i = t; i < n; i += nt) {
+        for (size_t j = t; j < 2 * cn; j += threads) {
+          const RowKey& k = keys[c0 + j / 2];
+          const fs::path path = (j & 1) ? dir_b / side_b.at(k).image : dir_a / side_a.at(k).image;
           try {
-            ia[i] = host::load_png((dir_a / map_a.at(keys[i])->image).string(), wa[i], ha[i]);
-            ib[i] = host::load_png((dir_b / map_b.at(keys[i])->image).string(), wb[i], hb[i]);
+            img[j] = host::load_png(path.string(), w[j], h[j]);
           } catch (...) {
-            errs[i] = std::current_exception();
+            err[j] = std::current_exception();
           }
         }
       });
     for (auto& t : pool) t.join();
-    for (auto& e : errs)
+    for (auto& e : err)
       if (e) std::rethrow_exception(e);
-  }
-  std::vector<double> ssims(n), psnrs(n), maes(n);
-  // Batch consecutive pairs of one shape (all of them for a real dataset).
-  for (size_t i0 = 0; i0 < n;) {
-    if (wa[i0] != wb[i0] || ha[i0] != hb[i0])
-      throw HostError{TG_ERR_SHAPE_MISMATCH,
-                      "image shapes differ: " + std::to_string(wa[i0]) + "x" + std::to_string(ha[i0]) +
-                          " vs " + std::to_string(wb[i0]) + "x" + std::to_string(hb[i0])};
-    size_t i1 = i0 + 1;
-    while (i1 < n && i1 - i0 < 256 && wa[i1] == wa[i0] && ha[i1] == ha[i0] && wb[i1] == wa[i0] &&
-           hb[i1] == ha[i0])
-      ++i1;
-    std::vector<std::vector<uint8_t>> A(ia.begin() + i0, ia.begin() + i1),
-        B(ib.begin() + i0, ib.begin() + i1);
-    std::vector<double> m;
-    check(image_metrics_batch(device, A, B, wa[i0], ha[i0], m));
-    for (size_t i = i0; i < i1; ++i) {
-      ssims[i] = m[3 * (i - i0)];
-      psnrs[i] = m[3 * (i - i0) + 1];
-      maes[i] = m[3 * (i - i0) + 2];
+    // runs of pairs that share one image size go to the device together
+    for (size_t j0 = 0; j0 < cn;) {
+      const int W = w[2 * j0], H = h[2 * j0];
+      if (w[2 * j0 + 1] != W || h[2 * j0 + 1] != H)
+        throw HostError{TG_ERR_SHAPE_MISMATCH, "image shapes differ: " + std::to_string(W) + "x" +
+                                                   std::to_string(H) + " vs " +
+                                                   std::to_string(w[2 * j0 + 1]) + "x" +
+                                                   std::to_string(h[2 * j0 + 1])};
+      size_t j1 = j0 + 1;
+      while (j1 < cn && w[2 * j1] == W && h[2 * j1] == H && w[2 * j1 + 1] == W && h[2 * j1 + 1] == H)
+        ++j1;
+      const size_t bytes = static_cast<size_t>(W) * H * 3;
+      std::vector<uint8_t> A(bytes * (j1 - j0)), B(bytes * (j1 - j0));
+      for (size_t j = j0; j < j1; ++j) {
+        std::memcpy(A.data() + (j - j0) * bytes, img[2 * j].data(), bytes);
+        std::memcpy(B.data() + (j - j0) * bytes, img[2 * j + 1].data(), bytes);
+        img[2 * j].clear();
+        img[2 * j].shrink_to_fit();
+        img[2 * j + 1].clear();
+        img[2 * j + 1].shrink_to_fit();
+      }
+      std::vector<double> m(3 * (j1 - j0));
+      check(tg_image_metrics(device, A.data(), B.data(), W, H, static_cast<int>(j1 - j0), m.data()));
+      for (size_t j = j0; j < j1; ++j) {
+        ssim[c0 + j] = m[3 * (j - j0)];
+        psnr[c0 + j] = m[3 * (j - j0) + 1];
+        mae[c0 + j] = m[3 * (j - j0) + 2];
+      }
+      j0 = j1;
     }
-    i0 = i1;
   }
 
-  std::FILE* csv = nullptr;
-  if (!csv_out.empty()) {
-    csv = std::fopen(csv_out.string().c_str(), "w");
-    if (!csv) throw HostError{TG_ERR_IO, "cannot write " + csv_out.string()};
-    std::fprintf(csv, "object,position_index,depth_index,ssim,psnr_db,mae_pct\n");
-    for (size_t i = 0; i < n; ++i)
-      std::fprintf(csv, "%s,%d,%d,%.6f,%.4f,%.4f\n", std::get<0>(keys[i]).c_str(),
-                   std::get<1>(keys[i]), std::get<2>(keys[i]), ssims[i], psnrs[i], maes[i]);
-  }
   CompareAggregate agg;
   agg.pairs = n;
-  auto mean = [](const std::vector<double>& xs) {
-    double s = 0.0;
-    for (double x : xs) s += x;
-    return xs.empty() ? 0.0 : s / static_cast<double>(xs.size());
-  };
-  agg.ssim_mean = mean(ssims);
-  agg.psnr_mean = mean(psnrs);
-  agg.mae_mean = mean(maes);
-  agg.ssim_std = aggregate_std(ssims, agg.ssim_mean);
-  agg.psnr_std = aggregate_std(psnrs, agg.psnr_mean);
-  agg.mae_std = aggregate_std(maes, agg.mae_mean);
-  if (csv) {
-    std::fprintf(csv, "mean,,,%.6f,%.4f,%.4f\n", agg.ssim_mean, agg.psnr_mean, agg.mae_mean);
-    std::fprintf(csv, "std,,,%.6f,%.4f,%.4f\n", agg.ssim_std, agg.psnr_std, agg.mae_std);
-    std::fclose(csv);
+  const Moments ms = moments(ssim), mp = moments(psnr), mm = moments(mae);
+  agg.ssim_mean = ms.mean;
+  agg.ssim_std = ms.stdev;
+  agg.psnr_mean = mp.mean;
+  agg.psnr_std = mp.stdev;
+  agg.mae_mean = mm.mean;
+  agg.mae_std = mm.stdev;
+  if (!csv_out.empty()) {
+    std::ofstream csv(csv_out, std::ios::binary | std::ios::trunc);
+    if (!csv) throw HostError{TG_ERR_IO, "cannot write " + csv_out.string()};
+    char line[512];
+    csv << "object,position_index,depth_index,ssim,psnr_db,mae_pct\n";
+    for (size_t i = 0; i < n; ++i) {
+      std::snprintf(line, sizeof(line), ",%d,%d,%.6f,%.4f,%.4f\n", std::get<1>(keys[i]),
+                    std::get<2>(keys[i]), ssim[i], psnr[i], mae[i]);
+      csv << std::get<0>(keys[i]) << line;
+    }
+    std::snprintf(line, sizeof(line), "mean,,,%.6f,%.4f,%.4f\nstd,,,%.6f,%.4f,%.4f\n",
+                  agg.ssim_mean, agg.psnr_mean, agg.mae_mean, agg.ssim_std, agg.psnr_std,
+                  agg.mae_std);
+    csv << line;
   }
   return agg;
 }

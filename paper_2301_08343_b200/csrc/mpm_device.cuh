@@ -188,6 +188,25 @@ __device__ __forceinline__ void polar_rotation(const double* F, double* R) {
   polar_rotation_svd(F, R);
 }
 
+// corotated_stress (material.cpp:83-89) given R = polar_rotation(F) and
+// J = det F: S = 2 mu (F - R) F^T + lambda (J - 1) J I.
+__device__ __forceinline__ void corotated_stress(const double* F, const double* R, double J,
+                                                 double mu, double lambda, double* S) {
+  double A[9];
+  const double s2mu = 2.0 * mu;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) A[i] = s2mu * (F[i] - R[i]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      S[3 * i + j] = A[3 * i] * F[3 * j] + A[3 * i + 1] * F[3 * j + 1] + A[3 * i + 2] * F[3 * j + 2];
+  const double sl = lambda * (J - 1.0) * J;
+  S[0] += sl;
+  S[4] += sl;
+  S[8] += sl;
+}
+
 // Order-preserving u64 encodings for atomicMin/atomicMax on doubles.
 __device__ __forceinline__ unsigned long long order_key(double v) {
   const unsigned long long b = __double_as_longlong(v);

@@ -35,8 +35,11 @@
 // of a later or equal substep exits early, reproducing the reference's
 // "state at the throwing phase".
 #include <climits>
+#include <string>
+#include <mutex>
 
 #include "engine.cuh"
+#include "tacchi_cuda.h"
 
 namespace tacchi_b200 {
 
@@ -646,21 +649,9 @@ __device__ __forceinline__ bool make_payload(const Geometry& g, Ctl* ctl, int s,
     return false;
   }
   make_stencil(x0, x1, x2, g.origin, g.inv_dx, q.st);
-  double R[9];
+  double R[9], S[9];
   polar_rotation(F, R);
-  double A[9], S[9];
-  const double s2mu = 2.0 * g.mu;
-#pragma unroll
-  for (int i = 0; i < 9; ++i) A[i] = s2mu * (F[i] - R[i]);
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-      S[3 * i + j] = A[3 * i] * F[3 * j] + A[3 * i + 1] * F[3 * j + 1] + A[3 * i + 2] * F[3 * j + 2];
-  const double sl = g.lambda * (J - 1.0) * J;
-  S[0] += sl;
-  S[4] += sl;
-  S[8] += sl;
+  corotated_stress(F, R, J, g.mu, g.lambda, S);
   const double ks = g.stress_scale * vol0;
 #pragma unroll
   for (int i = 0; i < 9; ++i) q.aff[i] = m * Cm[i] + ks * S[i];
@@ -716,7 +707,21 @@ __global__ void k_bbox(const double* __restrict__ x, int64_t n, int64_t begin, i
                 active ? x[2 * n + p] : 0.0);
 }
 
-enum : int { kFinAdvect = 1, kFinWindow = 2, kFinDiag = 4, kFinIndShift = 8, kFinCfl = 16 };
+// kFinWalkFix: the step path's indenter look-ahead walks (run beside the
+// elastomer kernel) used the previous elastomer box widened by one node;
+// finalize checks the new box against it and, if the elastomer moved out of
+// it, scatters the indenter particles the walks missed (k_finalize's extra
+// warps) so M_I is exact wherever the elastomer reads the grid.
+enum : int { kFinAdvect = 1, kFinWindow = 2, kFinDiag = 4, kFinIndShift = 8, kFinWalkFix = 16 };
+
+// Node boxes handed from finalize's first warp to the walk fix-up.
+struct FinFix {
+  int need;               // the new elastomer box is not inside the widened old one
+  int old_ok;             // the walks ran (the old box was non-empty)
+  int wlo[3], whi[3];     // old elastomer box widened by one node (what the walks used)
+  int elo[3], ehi[3];     // new (exact) elastomer box of the substep being scattered
+  int s;                  // the substep whose advect this finalize completes
+};
 
 // grid.cpp:29-36: in_range divides by dx.
 __device__ bool in_range(const Geometry& g, const double* x) {
@@ -737,12 +742,7 @@ __device__ __forceinline__ int base_of(const Geometry& g, int a, double x) {
   return static_cast<int>(floor(sub_rn(mul_rn(sub_rn(x, g.origin[a]), g.inv_dx), 0.5)));
 }
 
-__global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode) {
-  pdl_wait();
-  // every kernel that follows finalize in a step plan (grid_update,
-  // k_ind_catchup) reads nothing before its own wait: let it launch while
-  // this warp runs
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+__device__ void finalize_warp(Ctl* ctl, const Geometry& g, int mode, FinFix& fx) {
   const int lane = threadIdx.x;
   const bool ax = lane < 3;
   const int a = ax ? lane : 0;
@@ -769,15 +769,10 @@ __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode)
   }
   const double lo = fmin(bl, il), hi = fmax(bh, ih);
   int err = 0;  // warp-uniform
-  if (mode & kFinCfl) {
-    // The indenter's look-ahead walks (run beside the elastomer kernel) used
-    // the previous elastomer box widened by one node: valid while no
-    // elastomer particle moves a full cell in one substep (|v| dt < dx, far
-    // inside the explicit scheme's stability bound). Otherwise: OutOfGrid.
-    const double vg2 = __longlong_as_double(static_cast<long long>(ctl->max_v2[cur]));
-    if (!(vg2 * g.dt * g.dt < g.dx * g.dx)) err = 1;
-  }
-  if (!err && (mode & kFinAdvect)) {
+  // the elastomer box the look-ahead walks of this substep used (before it
+  // is replaced below)
+  const int olo = ctl->box_lo[0][a], ohi = ctl->box_hi[0][a];
+  if (mode & kFinAdvect) {
     // engine.cpp:279-285 (grid.cpp:29-36 per axis: xn = (x - o) / dx)
     bool ok = true;
     if (ax) {
@@ -835,6 +830,13 @@ __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode)
       ctl->box_lo[m][a] = any ? base_of(g, a, l[m]) : 0;
       ctl->box_hi[m][a] = any ? base_of(g, a, h[m]) + 3 : 0;
     }
+    if (mode & kFinWalkFix) {
+      const bool any = bl <= bh;
+      fx.wlo[a] = olo - 1;
+      fx.whi[a] = ohi + 1;
+      fx.elo[a] = any ? base_of(g, a, bl) : 0;
+      fx.ehi[a] = any ? base_of(g, a, bh) + 3 : 0;
+    }
     ctl->clr_lo[a] = prev_empty ? wlo : min(wlo, pl);
     ctl->clr_hi[a] = prev_empty ? whi : max(whi, ph);
     ctl->win_lo[a] = ctl->prev_lo[a] = wlo;
@@ -845,6 +847,17 @@ __global__ void __launch_bounds__(32) k_finalize(Ctl* ctl, Geometry g, int mode)
     ctl->bb_hi[cur ^ 1][a] = order_key(-INFINITY);
   }
   if ((mode & kFinAdvect) && lane == 0) ctl->max_v2[cur ^ 1] = 0ull;
+  if ((mode & kFinWalkFix) && (mode & kFinWindow)) {
+    // The walks covered the new box iff it lies inside the widened old one.
+    const bool old_ok = __all_sync(0xffffffffu, !ax || ohi > olo);
+    const bool new_any = __all_sync(0xffffffffu, !ax || bl <= bh);
+    const bool inside = __all_sync(0xffffffffu, !ax || (fx.elo[a] >= fx.wlo[a] && fx.ehi[a] <= fx.whi[a]));
+    if (lane == 0) {
+      fx.old_ok = old_ok;
+      fx.need = new_any && !(old_ok && inside);
+      fx.s = s;
+    }
+  }
 }
 
 // zero_grid's clear of Grid::mass / momentum over Ctl::clr (engine.cpp:72-83).
@@ -1122,6 +1135,18 @@ struct ColSmem {
 // this substep's advect), 2 = Ctl::box[0] of this substep widened by one node
 // on every side (look-ahead scatter running alongside the elastomer kernel:
 // the elastomer moves less than one cell per substep, which k_finalize checks).
+// An indenter particle with stencil st is scattered by a walk over the
+// elastomer node box [glo, ghi) iff its stencil is in the grid and its 27
+// nodes meet the box (base_z is non-decreasing along a column, so the walk's
+// stop at the first particle with base_z >= ghi_z drops none of these).
+__device__ __forceinline__ bool walk_contrib(const Geometry& g, const Stencil& st, const int* glo,
+                                             const int* ghi) {
+  bool c = stencil_in_grid(g, st);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) c = c && st.base[a] + 2 >= glo[a] && st.base[a] <= ghi[a] - 1;
+  return c;
+}
+
 template <bool kMove>
 __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __restrict__ x,
                                                int64_t n, int64_t n_el,
@@ -1179,9 +1204,7 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
       }
       make_stencil(px, py, pz, g.origin, g.inv_dx, st);
       beyond = st.base[2] > ghi[2] - 1;  // this and every later particle of the column miss
-      contrib = !beyond && stencil_in_grid(g, st);
-      for (int a = 0; a < 3; ++a)
-        contrib = contrib && st.base[a] + 2 >= glo[a] && st.base[a] <= ghi[a] - 1;
+      contrib = walk_contrib(g, st, glo, ghi);
     }
     const unsigned bey = __ballot_sync(0xffffffffu, beyond);
     const int first_beyond = bey ? __ffs(bey) - 1 : 32;
@@ -1257,6 +1280,72 @@ __global__ void k_ind_catchup(double* __restrict__ x, int64_t n, int64_t n_el,
     __stcs(x + 2 * n + p, pz);
   }
   if (done) moves[p - n_el] = 0;
+}
+
+// Fix-up of the look-ahead walks (rare: the elastomer moved out of the box
+// the walks used, i.e. more than a cell in one substep): every warp of
+// finalize's block walks whole columns and scatters the particles whose
+// stencil meets the new box but not the widened old one (the walks scattered
+// exactly the latter), at their positions after this substep's advect
+// (pending advects applied on the fly, as the walks do).
+__device__ void ind_walk_fixup(const FinFix& fx, const double* __restrict__ x, int64_t n,
+                               int64_t n_el, const int64_t* __restrict__ col_start, int n_cols,
+                               const uint8_t* __restrict__ moves, const Ctl* ctl,
+                               const Geometry& g, double* __restrict__ mi) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int target = fx.s - ctl->chain_start + 1;
+  double d[3];
+  for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
+  for (int c = warp; c < n_cols; c += nw) {
+    const int64_t a1 = col_start[c + 1];
+    for (int64_t p = col_start[c] + lane; p < a1; p += 32) {
+      double px = x[p], py = x[n + p], pz = x[2 * n + p];
+      for (int k = moves[p - n_el]; k < target; ++k) {
+        px = add_rn(px, d[0]);
+        py = add_rn(py, d[1]);
+        pz = add_rn(pz, d[2]);
+      }
+      Stencil st;
+      make_stencil(px, py, pz, g.origin, g.inv_dx, st);
+      if (!walk_contrib(g, st, fx.elo, fx.ehi)) continue;
+      if (fx.old_ok && walk_contrib(g, st, fx.wlo, fx.whi)) continue;  // the walk had it
+#pragma unroll
+      for (int i = 0; i < 27; ++i) {
+        const int ia = i / 9, ib = (i / 3) % 3, ic = i % 3;
+        red_add(mi + node_index(g, st.base[0] + ia, st.base[1] + ib, st.base[2] + ic),
+                st.w[0][ia] * st.w[1][ib] * st.w[2][ic]);
+      }
+    }
+  }
+}
+
+// Walk fix-up arguments (the step path's column data).
+struct FixArgs {
+  const double* x;
+  int64_t n, n_el;
+  const int64_t* col_start;
+  int n_cols;
+  const uint8_t* moves;
+  double* mi;
+};
+
+// advect's in_range / step_count / max_speed and the next zero_grid window
+// (finalize_warp, warp 0); with kFinWalkFix the other warps of the block
+// stand by for the walk fix-up.
+__global__ void __launch_bounds__(256) k_finalize(Ctl* ctl, Geometry g, int mode, FixArgs fa) {
+  pdl_wait();
+  // every kernel that follows finalize in a step plan (grid_update,
+  // k_ind_catchup) reads nothing before its own wait: let it launch while
+  // this block runs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  __shared__ FinFix fx;
+  if (threadIdx.x == 0) fx.need = 0;
+  if (blockDim.x > 32) __syncthreads();
+  if (threadIdx.x < 32) finalize_warp(ctl, g, mode, fx);
+  if (blockDim.x == 32) return;
+  __syncthreads();
+  if (fx.need)
+    ind_walk_fixup(fx, fa.x, fa.n, fa.n_el, fa.col_start, fa.n_cols, fa.moves, ctl, g, fa.mi);
 }
 
 // ---------------------------------------------------------------------------
@@ -1773,24 +1862,44 @@ unsigned gel_blocks(const DeviceSim& s) {
   return static_cast<unsigned>((s.n_el + kGelThreads - 1) / kGelThreads);
 }
 
-void configure_once() {
-  static bool done = false;
-  if (done) return;
-  cudaFuncSetAttribute(k_p2g_gel_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(kTileSmem));
-  cudaFuncSetAttribute(k_g2p2g_gel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(kTileSmem));
-  cudaFuncSetAttribute(k_ind_move_p2g<false, true>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIndSmem));
-  cudaFuncSetAttribute(k_ind_move_p2g<true, true>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIndSmem));
-  done = true;
+// Dynamic shared-memory opt-ins are per device (per primary context): set
+// once for every device a handle is created on (configure_device, called by
+// tg_create after the device is selected), never lazily during a graph
+// capture. A mutex guards the per-device flags (handles on different devices
+// may be created from different threads).
+std::mutex g_cfg_mutex;
+bool g_cfg_done[64] = {};
+}  // namespace
+
+int configure_device(int device) {
+  std::lock_guard<std::mutex> lock(g_cfg_mutex);
+  if (device < 0 || device >= 64) return 1;
+  if (g_cfg_done[device]) return 0;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  cudaSetDevice(device);
+  const int tile = static_cast<int>(kTileSmem);
+  cudaError_t e = cudaSuccess;
+  auto set = [&](const void* f, int bytes) {
+    const cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (r != cudaSuccess && e == cudaSuccess) e = r;
+  };
+  set(reinterpret_cast<const void*>(k_p2g_gel_tile), tile);
+  set(reinterpret_cast<const void*>(k_g2p2g_gel<true, true, true>), tile);
+  set(reinterpret_cast<const void*>(k_ind_move_p2g<false, true>), static_cast<int>(kIndSmem));
+  set(reinterpret_cast<const void*>(k_ind_move_p2g<true, true>), static_cast<int>(kIndSmem));
+  set(reinterpret_cast<const void*>(k_ind_cols<true>), static_cast<int>(sizeof(ColSmem)));
+  set(reinterpret_cast<const void*>(k_ind_cols<false>), static_cast<int>(sizeof(ColSmem)));
+  if (cur >= 0 && cur != device) cudaSetDevice(cur);
+  if (e != cudaSuccess) return 2;
+  g_cfg_done[device] = true;
+  return 0;
 }
+namespace {
 }  // namespace
 
 // Chooses the lattice-block CTA tiling of the elastomer (engine.cuh).
 void configure_gel_tiling(DeviceSim& s, int nx, int ny, int nz) {
-  configure_once();
   if (nx <= 0 || ny <= 0 || nz <= 0 || static_cast<int64_t>(nx) * ny * nz != s.n_el ||
       nz > kGelThreads) {
     s.lat[0] = s.lat[1] = s.lat[2] = 0;
@@ -1819,7 +1928,6 @@ int launch_reset(DeviceSim& s, int mask) {
 
 // zero_grid's window from the current positions (both bboxes recomputed).
 int launch_window(DeviceSim& s) {
-  configure_once();
   int k = launch_reset(s, kResetMotion | kResetIndBox | kResetDetF);
   if (s.n_el > 0) {
     k_bbox<<<blocks_for(s.n_el), kThreads, 0, s.stream>>>(s.x, s.n, 0, s.n_el, s.ctl, 0, 1);
@@ -1829,7 +1937,7 @@ int launch_window(DeviceSim& s) {
     k_bbox<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.n, s.ctl, 1, 1);
     ++k;
   }
-  k_finalize<<<1, 32, 0, s.stream>>>(s.ctl, s.geo, kFinWindow);
+  k_finalize<<<1, 32, 0, s.stream>>>(s.ctl, s.geo, kFinWindow, FixArgs{});
   s.kernel_launches += k;  // reset counted in launch_reset
   return k + 1;
 }
@@ -1843,7 +1951,6 @@ int launch_clear(DeviceSim& s, int sms) {
 
 int launch_p2g_gel(DeviceSim& s) {
   if (s.n_el <= 0) return 0;
-  configure_once();
   k_p2g_gel_tile<<<gel_blocks(s), kGelThreads, kTileSmem, s.stream>>>(
       s.x, s.v, s.C, s.F, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_mp, s.m_el, s.vol_el);
   s.kernel_launches += 1;
@@ -1857,7 +1964,6 @@ inline unsigned ind_blocks(const DeviceSim& s) {
 
 int launch_p2g_ind(DeviceSim& s) {
   if (s.n_ind <= 0) return 0;
-  configure_once();
   if (s.ind_v_uniform)
     k_ind_move_p2g<false, true><<<ind_blocks(s), kIndThreads, kIndSmem, s.stream>>>(
         s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
@@ -1893,7 +1999,6 @@ int launch_grid_update(DeviceSim& s, int sms, bool zero) {
 // G2P + boundary + advect for the elastomer, with the look-ahead scatter.
 int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter) {
   if (s.n_el <= 0) return 0;
-  configure_once();
   IndArgs ia{};
   unsigned extra = 0;
   if (with_indenter) {  // the indenter's look-ahead column walks ride along
@@ -1918,7 +2023,6 @@ int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter) {
 
 int launch_ind_move(DeviceSim& s, bool lookahead) {
   if (s.n_ind <= 0) return 0;
-  configure_once();
   if (lookahead)
     k_ind_move_p2g<true, true><<<ind_blocks(s), kIndThreads, kIndSmem, s.stream>>>(
         s.x, s.n, s.n_el, s.ctl, s.geo, s.grid_mi);
@@ -1942,14 +2046,6 @@ int launch_chain_begin(DeviceSim& s) {
 // positions as they are) or fused with this substep's advect (look-ahead).
 int launch_ind_cols(DeviceSim& s, bool move) {
   if (s.n_ind <= 0 || s.n_cols <= 0) return 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_ind_cols<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kColSmem));
-    cudaFuncSetAttribute(k_ind_cols<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kColSmem));
-    attr = true;
-  }
   const unsigned blocks = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
   if (move)
     launch_pdl(k_ind_cols<true>, dim3(blocks), dim3(kColWarps * 32), kColSmem, s.stream, s.x,
@@ -1971,10 +2067,11 @@ int launch_ind_catchup(DeviceSim& s) {
   return 1;
 }
 
-int launch_finalize_step(DeviceSim& s, bool cfl_check) {
-  launch_pdl(k_finalize, dim3(1), dim3(32), 0, s.stream, s.ctl, s.geo,
-             static_cast<int>(kFinDiag | kFinAdvect | kFinWindow | (s.n_ind > 0 ? kFinIndShift : 0) |
-                              (cfl_check ? kFinCfl : 0)));
+int launch_finalize_step(DeviceSim& s, bool walk_fix) {
+  const int mode = kFinDiag | kFinAdvect | kFinWindow | (s.n_ind > 0 ? kFinIndShift : 0) |
+                   (walk_fix ? kFinWalkFix : 0);
+  const FixArgs fa{s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.grid_mi};
+  launch_pdl(k_finalize, dim3(1), dim3(walk_fix ? 256 : 32), 0, s.stream, s.ctl, s.geo, mode, fa);
   s.kernel_launches += 1;
   return 1;
 }
@@ -2023,7 +2120,7 @@ int launch_phase_advect(DeviceSim& s) {
     k_bbox<<<blocks_for(s.n_ind), kThreads, 0, s.stream>>>(s.x, s.n, s.n_el, s.n, s.ctl, 1, 0);
     k += 3;
   }
-  k_finalize<<<1, 32, 0, s.stream>>>(s.ctl, s.geo, kFinAdvect);
+  k_finalize<<<1, 32, 0, s.stream>>>(s.ctl, s.geo, kFinAdvect, FixArgs{});
   ++k;
   s.kernel_launches += k;
   return k;
@@ -2039,6 +2136,61 @@ int launch_gather_box(DeviceSim& s, const int lo[3], const int hi[3], double* ma
 }
 
 }  // namespace tacchi_b200
+
+// ---------------------------------------------------------------------------
+// Instrumentation: the material functions the P2G kernels call, on a batch of
+// deformation gradients (tg_polar; known-answer tests of material.cpp:18-89,
+// including the SVD fallback the Newton iteration reaches only for
+// pathological F).
+// ---------------------------------------------------------------------------
+namespace tacchi_b200 {
+__global__ void k_polar(const double* __restrict__ F, int64_t n, int mode, double mu, double lambda,
+                        double* __restrict__ R, double* __restrict__ S) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  double f[9], r[9];
+  for (int i = 0; i < 9; ++i) f[i] = F[9 * p + i];
+  if (mode == 1) polar_rotation_svd(f, r);
+  else polar_rotation(f, r);
+  for (int i = 0; i < 9; ++i) R[9 * p + i] = r[i];
+  if (S) {
+    double st[9];
+    corotated_stress(f, r, det3(f), mu, lambda, st);
+    for (int i = 0; i < 9; ++i) S[9 * p + i] = st[i];
+  }
+}
+int check_device_public(int device);
+int fail(int code, const std::string& msg);
+}  // namespace tacchi_b200
+
+extern "C" int tg_polar(int device, const double* F, int64_t n, int mode, double youngs_modulus,
+                        double poisson_ratio, double* R, double* S) {
+  using namespace tacchi_b200;
+  if (!F || !R || n < 0 || (mode != 0 && mode != 1))
+    return fail(TG_ERR_INVALID_ARGUMENT, "tg_polar: bad argument");
+  int rc = check_device_public(device);
+  if (rc) return rc;
+  if (n == 0) return TG_OK;
+  const double mu = youngs_modulus / (2.0 * (1.0 + poisson_ratio));  // material.hpp:14-18
+  const double lambda =
+      youngs_modulus * poisson_ratio / ((1.0 + poisson_ratio) * (1.0 - 2.0 * poisson_ratio));
+  double *dF = nullptr, *dR = nullptr, *dS = nullptr;
+  const size_t bytes = static_cast<size_t>(n) * 9 * sizeof(double);
+  cudaError_t e = cudaMalloc(&dF, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&dR, bytes);
+  if (e == cudaSuccess && S) e = cudaMalloc(&dS, bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(dF, F, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    k_polar<<<static_cast<unsigned>((n + 127) / 128), 128>>>(dF, n, mode, mu, lambda, dR, dS);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(R, dR, bytes, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && S) e = cudaMemcpy(S, dS, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(dF);
+  cudaFree(dR);
+  cudaFree(dS);
+  return e == cudaSuccess ? TG_OK : fail(TG_ERR_CUDA, std::string("tg_polar: ") + cudaGetErrorString(e));
+}
 
 #ifdef TACCHI_TRACE
 // Diagnostic builds only: copies the elastomer kernel's per-CTA stage marks.

@@ -37,6 +37,12 @@ Fixtures (all numpy .npz):
                    (2 objects x 2 positions x 3 depths): manifest.csv,
                    config.json, every image and .depth file; metrics::compare
                    on image pairs and on a seeded noise pair.
+  config2a.npz     the bench workload (sphere 1e6, 1,214,221 particles) at
+                   100 and 600 frames: subset x / F / v, surface, image, depth.
+  config4.npz      config-4 episodes 0-3 (mt19937_64 pose draws, offset and
+                   z-rotation), 200 frames each.
+  config3_full.npz the dot-grid indenter at full size, pressed 20,000
+                   substeps then slid 2,000.
   config1.npz      default config (dt 2e-6), 1000 substeps (100 frames) at the
                    default press velocity: surface-particle positions, a
                    seeded 4096-particle subset of x and F, diagnostics, the
@@ -218,6 +224,84 @@ def config2b():
         F_subset=s1["F"][subset], x_surface=s1["x"][surf["particle"]][::7],
         min_det_f=d["min_det_f"], max_speed=d["max_speed"], step_count=d["step_count"],
         image=img, depth_sample=depth[::16, ::16])
+
+
+def _checkpoint(sim, cfg, obj, x0, rng_seed, prefix, out):
+    """Subset positions / F, the surface, diagnostics, the capture image and
+    a depth sample of the reference state (keys prefixed)."""
+    st = sim.state()
+    d = sim.diag()
+    depth, img = sim.capture(cfg, obj)
+    surf = sim.surface()["particle"]
+    rng = np.random.default_rng(rng_seed)
+    sub = np.sort(rng.choice(sim.n_elastomer, 4096, replace=False))
+    out[f"{prefix}subset"] = sub
+    out[f"{prefix}x0_subset"] = x0[sub]
+    out[f"{prefix}x_subset"] = st["x"][sub]
+    out[f"{prefix}F_subset"] = st["F"].reshape(-1, 9)[sub]
+    out[f"{prefix}v_subset"] = st["v"][sub]
+    out[f"{prefix}x_surface"] = st["x"][surf]
+    out[f"{prefix}min_det_f"] = d["min_det_f"]
+    out[f"{prefix}max_speed"] = d["max_speed"]
+    out[f"{prefix}step_count"] = d["step_count"]
+    out[f"{prefix}image"] = img
+    out[f"{prefix}depth_sample"] = depth[::8, ::8]
+    out[f"{prefix}depth_max"] = depth.max()
+
+
+def config2a():
+    """The bench workload (1,214,221 particles) at 100 frames and 600 frames
+    (past the gap), 10 substeps per frame as the bench steps it."""
+    from tests.scenes import CONFIG2A, CONFIG2A_FRAMES, CONFIG2A_V
+
+    sim = R.RefSim.from_config(CONFIG2A, "", threads=0)
+    s0 = sim.state()
+    out = {"n": sim.n, "n_elastomer": sim.n_elastomer, "x0_hash": sha(s0["x"]),
+           "frames": np.array(CONFIG2A_FRAMES)}
+    done = 0
+    for f in CONFIG2A_FRAMES:
+        sim.step(CONFIG2A_V, 10 * (f - done))
+        done = f
+        _checkpoint(sim, CONFIG2A, "", s0["x"], 7, f"f{f}_", out)
+        print("config2a frame", f, flush=True)
+    np.savez_compressed(os.path.join(OUT, "config2a.npz"), **out)
+
+
+def config4():
+    """The first CONFIG4_EPISODES episodes of the config-4 batch (mt19937_64
+    pose draws: lateral offset and z-rotation), CONFIG4_FRAMES frames each."""
+    from paper_2301_08343_b200 import episodes as E
+    from tests.scenes import CONFIG1, CONFIG1_V, CONFIG4_EPISODES, CONFIG4_FRAMES
+
+    out = {"episodes": CONFIG4_EPISODES, "frames": CONFIG4_FRAMES}
+    for e in range(CONFIG4_EPISODES):
+        ep = E.make_episode(e)
+        cfg = E.episode_config(CONFIG1, ep)
+        sim = R.RefSim.from_config(cfg, "", ep.offset_x_m, ep.offset_y_m, threads=0)
+        s0 = sim.state()
+        out[f"e{e}_pose"] = np.array([ep.offset_x_m, ep.offset_y_m, ep.z_rotation_rad, ep.depth_m])
+        out[f"e{e}_x0_hash"] = sha(s0["x"])
+        sim.step(CONFIG1_V, 10 * CONFIG4_FRAMES)
+        _checkpoint(sim, cfg, "", s0["x"], 40 + e, f"e{e}_", out)
+        print("config4 episode", e, flush=True)
+    np.savez_compressed(os.path.join(OUT, "config4.npz"), **out)
+
+
+def config3_full():
+    """Config 3 at full size: the dot-grid indenter (1e5 points) on the
+    default gel and 256^3 grid, pressed to gap + 0.3 mm, then slid +x."""
+    from tests.scenes import CONFIG1, CONFIG3_FULL_PRESS, CONFIG3_FULL_SHAPE, CONFIG3_FULL_SLIDE
+
+    shape = CONFIG3_FULL_SHAPE
+    sim = R.RefSim.from_config(CONFIG1, shape, threads=0)
+    s0 = sim.state()
+    out = {"shape": shape, "n": sim.n, "x0_hash": sha(s0["x"])}
+    sim.step(CONFIG3_FULL_PRESS[1], CONFIG3_FULL_PRESS[0])
+    _checkpoint(sim, CONFIG1, shape, s0["x"], 31, "press_", out)
+    print("config3 full: pressed", flush=True)
+    sim.step(CONFIG3_FULL_SLIDE[1], CONFIG3_FULL_SLIDE[0])
+    _checkpoint(sim, CONFIG1, shape, s0["x"], 32, "slide_", out)
+    np.savez_compressed(os.path.join(OUT, "config3_full.npz"), **out)
 
 
 def acceptance3():
@@ -419,6 +503,12 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "config2b", "acceptance3", "bridge", "harness", "parts", "background", "clouds"]
     if "config2b" in which:
         config2b()
+    if "config2a" in which:
+        config2a()
+    if "config4" in which:
+        config4()
+    if "config3_full" in which:
+        config3_full()
     if "acceptance3" in which:
         acceptance3()
     if "config5" in which:

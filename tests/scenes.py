@@ -44,6 +44,25 @@ CONFIG2B_SLIDE = (20, (0.2, -0.1, 0.0))
 
 SUBSTEPS_PER_FRAME = 10  # scene_config.hpp:36, session.cpp:86
 
+# Config 2a parity (the bench workload): 100 frames (SURVEY §8(d) CI length)
+# and a checkpoint at 600 frames, past the gap (the indenter crosses the
+# 0.1 mm gap after 500 frames).
+CONFIG2A_FRAMES = (100, 600)
+
+# Config 4 parity: the first episodes of the 1024-episode batch (config-1
+# geometry, mt19937_64 pose draws, paper_2301_08343_b200/episodes.py), each
+# stepped for the throughput cap of 200 frames at the press velocity.
+CONFIG4_EPISODES = 4
+CONFIG4_FRAMES = 200
+
+# Config 3 at full size (default gel 101x101x21, 1e5-point dot-grid
+# indenter, 256^3): pressed until the commanded travel is gap + 0.3 mm
+# (20,000 substeps at 0.01 m/s), then slid +x at 5 mm/s for 200 frames
+# (SURVEY §8(d)).
+CONFIG3_FULL_SHAPE = "dots"
+CONFIG3_FULL_PRESS = (20000, (0.0, 0.0, -0.01))
+CONFIG3_FULL_SLIDE = (2000, (0.005, 0.0, 0.0))
+
 # Config 5 (BASELINE.json configs[4]): large-area gel 40 x 40 x 4 mm at the
 # same 0.2 mm spacing (201 x 201 x 21 = 848,421 gel particles) + sphere 1e5,
 # 512^3 grid of 66 mm edge (same dx as config 1). The parity slice is short

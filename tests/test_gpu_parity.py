@@ -324,21 +324,31 @@ def test_out_of_grid_after_advect(tb):
     assert 1 <= s.step_count < 200
 
 
-def test_elastomer_moving_a_cell_per_substep_is_out_of_grid(tb):
-    """Deliberate deviation: the indenter's look-ahead walks
-    use the previous elastomer box widened by one node, valid while no
-    elastomer particle moves a full cell per substep; a step that does (here
-    an uploaded 100 m/s, dx / dt = 94 m/s) raises OutOfGrid at that substep
-    instead of continuing (the explicit scheme is far outside its stability
-    bound there)."""
+def test_elastomer_moving_cells_per_substep_matches_oracle(tb, golden, oracle):
+    """The indenter's look-ahead walks use the previous elastomer box widened
+    by one node; when the elastomer moves further in one substep (here the
+    whole scene translates at 300 m/s, 3.2 cells per substep), finalize
+    scatters the indenter particles the walks missed, so the step continues
+    as the reference's does (engine.cpp:268-286 raises nothing there)."""
+    g = golden("small_scene.npz")
     s = tb.sim.build_sim(SMALL)
+    tb.mpm.step(s, SMALL_V, 4)
     st = s.state()
+    vfast = (300.0, -120.0, 0.0)
     v = st["v"].copy()
-    v[: s.elastomer_count, 0] = 100.0
+    v[:] += np.array(vfast)
+    v[s.elastomer_count:] = vfast  # uniform indenter velocity (the command)
     s.set_state(v=v)
-    with pytest.raises(tb.OutOfGrid):
-        tb.mpm.step(s, (0, 0, 0), 5)
-    assert s.step_count <= 2
+    o = _small_oracle(oracle, g)
+    o.x, o.v, o.C, o.F = st["x"].copy(), v.copy(), st["C"].copy(), st["F"].copy()
+    tb.mpm.step(s, vfast, 3)
+    o.step(vfast, 3)
+    x = s.positions()
+    moved = np.abs(x - st["x"]).max()
+    assert moved > 3 * 3 * 12e-3 / 64  # > 3 cells per substep
+    assert np.abs(x - o.x).max() <= 1e-9 * moved
+    np.testing.assert_allclose(s.state()["F"], o.F, rtol=0, atol=1e-11)
+    assert s.step_count == 7
 
 
 def test_capture_with_background_image_matches_reference(tb, golden, tmp_path):
@@ -613,3 +623,26 @@ def test_rest_state_is_a_fixed_point(tb):
     tb.mpm.step(s, (0, 0, 0), 100)
     assert np.abs(s.positions() - x0).max() <= 1e-9
     assert s.diag.max_speed < 1e-9
+
+
+def test_polar_rotation_and_svd_fallback_match_reference(tb, golden):
+    """material.cpp:18-89 on the device (the functions the P2G kernels call)
+    vs the reference (kat.npz, 63 deformation gradients from identity to
+    strongly sheared): the scaled Newton polar rotation, the corotated stress,
+    and the SVD fallback polar_rotation_svd forced directly (the Newton loop
+    reaches it only for |det F| <= 1e-300 or no convergence in 40 iterations,
+    which no well-posed press produces)."""
+    g = golden("kat.npz")
+    F = g["F"]
+    R, S = tb.material.polar_rotation(F)
+    np.testing.assert_allclose(R, g["R"], rtol=0, atol=1e-13)
+    smax = np.abs(g["S"]).max()
+    np.testing.assert_allclose(S, g["S"], rtol=0, atol=1e-12 * smax)
+    Rs, Ss = tb.material.polar_rotation(F, svd=True)
+    np.testing.assert_allclose(Rs, g["R_svd"], rtol=0, atol=1e-12)
+    # the two paths agree, and the fallback's rotation is proper
+    np.testing.assert_allclose(Rs, R, rtol=0, atol=1e-10)
+    np.testing.assert_allclose(np.einsum("nji,njk->nik", Rs, Rs), np.tile(np.eye(3), (len(F), 1, 1)),
+                               rtol=0, atol=1e-13)
+    assert np.all(np.linalg.det(Rs) > 0)
+    np.testing.assert_allclose(Ss, S, rtol=0, atol=1e-8 * smax)

@@ -61,3 +61,22 @@ def test_episode_draws_are_deterministic_and_in_range():
 def test_shard_rejects_bad_rank():
     with pytest.raises(ValueError):
         E.shard(8, 2, 2)
+
+
+def test_mt19937_64_known_answer():
+    """[rand.predef]: the 10000th output of a default-constructed
+    std::mt19937_64 is 9981545732273789042; seed 1 as std::mt19937_64(1)."""
+    r = E.MT19937_64()
+    for _ in range(9999):
+        r()
+    assert r() == 9981545732273789042
+    r1 = E.MT19937_64(1)
+    assert [r1(), r1()] == [2469588189546311528, 2516265689700432462]
+    ep = E.make_episode(0)  # seed 1: the first four 53-bit uniforms
+    assert ep.offset_x_m == -1e-3 + 2e-3 * ((2469588189546311528 >> 11) * 2.0**-53)
+
+
+def test_waves_split_a_rank_share():
+    eps = E.shard(1024, 3, 8)
+    w = E.waves(eps, 50)
+    assert [len(x) for x in w] == [50, 50, 28] and sum(w, []) == eps
