@@ -125,10 +125,94 @@ class SimState {
   void upload(const double* x, const double* v, const double* C, const double* F) {
     check(tg_upload(h_.get(), x, v, C, F));
   }
+  // ParticleStore::mass / volume0 / tag (reference order).
+  void constants(std::vector<double>* mass, std::vector<double>* volume0,
+                 std::vector<uint8_t>* tag) const {
+    const size_t n = static_cast<size_t>(size());
+    if (mass) mass->resize(n);
+    if (volume0) volume0->resize(n);
+    if (tag) tag->resize(n);
+    check(tg_download_constants(h_.get(), mass ? mass->data() : nullptr,
+                                volume0 ? volume0->data() : nullptr, tag ? tag->data() : nullptr));
+  }
+  // Grid::active_lo / active_hi (grid.hpp:25-26).
+  std::array<std::array<int, 3>, 2> grid_window() const {
+    std::array<std::array<int, 3>, 2> w{};
+    check(tg_grid_window(h_.get(), w[0].data(), w[1].data()));
+    return w;
+  }
+  // Grid::mass / momentum / velocity over the node box [lo, hi), k fastest
+  // (momentum / velocity: 3 per node). After a step this needs
+  // set_keep_grid(true) before stepping (tg_download_grid).
+  struct GridBox {
+    std::vector<double> mass, momentum, velocity;
+  };
+  GridBox grid(const std::array<int, 3>& lo, const std::array<int, 3>& hi) const {
+    const size_t cnt = static_cast<size_t>(hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]);
+    GridBox g;
+    g.mass.resize(cnt);
+    g.momentum.resize(3 * cnt);
+    g.velocity.resize(3 * cnt);
+    check(tg_download_grid(h_.get(), lo.data(), hi.data(), g.mass.data(), g.momentum.data(),
+                           g.velocity.data()));
+    return g;
+  }
+  void set_keep_grid(bool on) { check(tg_set_keep_grid(h_.get(), on ? 1 : 0)); }
 
  private:
   std::unique_ptr<tg_sim, void (*)(tg_handle)> h_;
 };
+
+// mpm::SceneParams (sim_state.hpp:81-98).
+struct SceneParams {
+  std::array<int, 3> grid_resolution = {256, 256, 256};
+  double grid_edge = 0.033;
+  Vec3 grid_origin = {0.0, 0.0, 0.0};
+  double youngs_modulus = 1.45e5, poisson_ratio = 0.45, density = 1000.0;
+  double dt = 1e-4;
+  int fixed_bottom_layers = 2;
+  Vec3 gravity = {0.0, 0.0, 0.0};
+  double indenter_mass_scale = 80.0;
+};
+
+// An elastomer geo::ParticleSet with LatticeMeta (particle_set.hpp:18-30);
+// empty positions = make_elastomer_lattice(dims, counts, origin).
+struct ElastomerLattice {
+  std::array<int, 3> counts = {101, 101, 21};
+  Vec3 dims = {0.02, 0.02, 0.004};
+  Vec3 origin = {0.0, 0.0, 0.0};
+  std::vector<Vec3> positions;
+};
+
+// mpm::init_scene (sim_state.hpp:102-104, scene.cpp:28-87).
+inline SimState init_scene(const SceneParams& p, const ElastomerLattice& elastomer,
+                           const std::vector<Vec3>& indenter,
+                           const Vec3& indenter_velocity = {0.0, 0.0, 0.0}, int device = 0) {
+  tg_scene_params sp{};
+  for (int a = 0; a < 3; ++a) {
+    sp.grid_resolution[a] = p.grid_resolution[a];
+    sp.grid_origin[a] = p.grid_origin[a];
+    sp.gravity[a] = p.gravity[a];
+  }
+  sp.grid_edge = p.grid_edge;
+  sp.youngs_modulus = p.youngs_modulus;
+  sp.poisson_ratio = p.poisson_ratio;
+  sp.density = p.density;
+  sp.dt = p.dt;
+  sp.fixed_bottom_layers = p.fixed_bottom_layers;
+  sp.indenter_mass_scale = p.indenter_mass_scale;
+  tg_lattice lat{};
+  for (int a = 0; a < 3; ++a) {
+    lat.counts[a] = elastomer.counts[a];
+    lat.dims[a] = elastomer.dims[a];
+    lat.origin[a] = elastomer.origin[a];
+  }
+  lat.positions = elastomer.positions.empty() ? nullptr : elastomer.positions.front().data();
+  tg_handle h = nullptr;
+  check(tg_init_scene(device, &sp, &lat, indenter.empty() ? nullptr : indenter.front().data(),
+                      static_cast<int64_t>(indenter.size()), indenter_velocity.data(), &h));
+  return SimState(h);
+}
 
 // engine.hpp:10-35
 inline void zero_grid(SimState& s) { check(tg_phase(s.handle(), TG_PHASE_ZERO_GRID, nullptr)); }
@@ -159,10 +243,46 @@ inline mpm::SimState build_sim(const std::string& config_json, const std::string
   return mpm::SimState(h);
 }
 
+// sim::build_sim(cfg, indenter) (scene_builder.hpp:29-30) with caller-placed
+// indenter points (m).
+inline mpm::SimState build_sim(const std::string& config_json, const std::vector<Vec3>& indenter,
+                               int device = 0) {
+  tg_handle h = nullptr;
+  check(tg_build_sim_points(device, config_json.c_str(),
+                            indenter.empty() ? nullptr : indenter.front().data(),
+                            static_cast<int64_t>(indenter.size()), &h));
+  return mpm::SimState(h);
+}
+
 struct Capture {
   render::DepthMap depth;
   render::Image8 image;
 };
+
+// capture's render inputs (lights, RenderParams, alignment_for(object)),
+// resolved from the SceneConfig once (scene_config.cpp:70-81) and reused for
+// every frame.
+struct RenderSetup {
+  tg_render r{};
+  static RenderSetup from_config(const std::string& config_json, const std::string& object) {
+    RenderSetup rs;
+    check(tg_render_from_config(config_json.c_str(), object.c_str(), &rs.r));
+    return rs;
+  }
+};
+
+// sim::capture (scene_builder.cpp:80-89) with resolved render inputs.
+inline Capture capture(const mpm::SimState& s, const RenderSetup& rs) {
+  const tg_render& r = rs.r;
+  Capture c;
+  c.depth.width = c.image.width = r.width;
+  c.depth.height = c.image.height = r.height;
+  c.depth.pixel_to_meter = r.pixel_to_meter * r.crop_scale;
+  c.depth.values.resize(static_cast<size_t>(r.width) * r.height);
+  c.image.data.resize(static_cast<size_t>(r.width) * r.height * 3);
+  check(tg_capture(s.handle(), &r, c.depth.values.data(), c.image.data.data()));
+  return c;
+}
 
 // sim::capture (scene_builder.cpp:80-89)
 inline Capture capture(const mpm::SimState& s, const std::string& config_json,

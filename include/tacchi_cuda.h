@@ -114,7 +114,45 @@ typedef struct {
   const uint8_t* background;/* optional height x width x 3 RGB, or NULL */
 } tg_render;
 
+/* mpm::SceneParams (sim_state.hpp:81-98): init_scene's own parameters. */
+typedef struct {
+  int grid_resolution[3];     /* nodes per axis */
+  double grid_edge;           /* m; node spacing = grid_edge / grid_resolution[0] */
+  double grid_origin[3];
+  double youngs_modulus, poisson_ratio, density;  /* MaterialParams */
+  double dt;
+  int fixed_bottom_layers;    /* lattice layers k < this are ElastomerBottom */
+  double gravity[3];
+  double indenter_mass_scale; /* default 80 */
+} tg_scene_params;
+
+/* An elastomer geo::ParticleSet with its LatticeMeta (particle_set.hpp:18-30). */
+typedef struct {
+  int counts[3];              /* particles per axis, >= 2 */
+  double dims[3];             /* extent spanned by the lattice, m */
+  double origin[3];           /* position of particle (0, 0, 0), m */
+  const double* positions;    /* counts[0]*counts[1]*counts[2] x 3 in lattice order
+                                 ((i*ny + j)*nz + k), or NULL for
+                                 make_elastomer_lattice(dims, counts, origin) */
+} tg_lattice;
+
 /* ---- scene setup ------------------------------------------------------- */
+
+/* mpm::init_scene(params, elastomer, indenter, indenter_velocity)
+ * (sim_state.hpp:102-104, scene.cpp:28-87) from its own inputs: margins,
+ * rest volumes and masses (indenter mass x indenter_mass_scale), bottom-layer
+ * tags, the surface lattice and the initial velocities are computed here.
+ * indenter: n_indenter x 3 placed points (m); indenter_velocity may be NULL
+ * (zero). Errors: EmptyScene, GridTooSmall, ConfigError. */
+int tg_init_scene(int device, const tg_scene_params* params, const tg_lattice* elastomer,
+                  const double* indenter, int64_t n_indenter, const double indenter_velocity[3],
+                  tg_handle* out);
+
+/* sim::build_sim(cfg, indenter) (scene_builder.hpp:29-30,
+ * scene_builder.cpp:63-78) with a caller's placed indenter points
+ * (n_indenter x 3, m), e.g. a co-simulation's own object geometry. */
+int tg_build_sim_points(int device, const char* config_json, const double* indenter,
+                        int64_t n_indenter, tg_handle* out);
 
 /* mpm::init_scene (sim_state.hpp:102-104) from explicit arrays. */
 int tg_create(int device, const tg_params* params, const tg_particles* particles,
@@ -126,6 +164,14 @@ int tg_create(int device, const tg_params* params, const tg_particles* particles
  * scene_config.cpp:118-257). */
 int tg_build_sim(int device, const char* config_json, const char* object, double offset_x,
                  double offset_y, tg_handle* out);
+
+/* Config-4 episodes / harness positions of one object: the indenter cloud
+ * (indenter_cloud_for, scene_builder.cpp:33-46) is built once and shared;
+ * episode e is build_sim(cfg with z_rotation_rad = poses[3e+2],
+ * place_for_press(cfg, cloud, poses[3e], poses[3e+1])) on `device`.
+ * out: n_episodes handles (all destroyed again if any creation fails). */
+int tg_build_episodes(int device, const char* config_json, const char* object, int n_episodes,
+                      const double* poses, tg_handle* out);
 
 void tg_destroy(tg_handle h);
 
@@ -158,13 +204,25 @@ int tg_upload(tg_handle h, const double* x, const double* v, const double* C, co
 /* StepDiagnostics + step_count + indenter_velocity (sim_state.hpp:54-73). */
 int tg_diag(tg_handle h, double* min_det_f, double* max_speed, int64_t* step_count,
             double indenter_velocity[3]);
-/* Grid::active_lo / active_hi (grid.hpp:25-26). */
+/* ParticleStore::mass / volume0 / tag (sim_state.hpp:17-37), reference order;
+ * any output may be NULL. */
+int tg_download_constants(tg_handle h, double* mass, double* volume0, uint8_t* tag);
+/* Grid::active_lo / active_hi (grid.hpp:25-26): the window of the last
+ * zero_grid (after mpm::step, the last substep's). */
 int tg_grid_window(tg_handle h, int lo[3], int hi[3]);
-/* Node box [lo, hi) (k fastest) of Grid::mass / momentum / velocity; any
- * output may be NULL. Momentum is available after particle_to_grid and before
- * grid_update; velocity after grid_update. */
+/* Node box [lo, hi) (k fastest) of Grid::mass / momentum / velocity as the
+ * reference holds them (zero outside the active window); any output may be
+ * NULL. Valid after the phase functions, after creation, and after tg_step /
+ * tg_step_capture on a handle with tg_set_keep_grid(h, 1); after a fused step
+ * (the default) it returns TG_ERR_INVALID_ARGUMENT: that grid holds the next
+ * substep's look-ahead scatter. */
 int tg_download_grid(tg_handle h, const int lo[3], const int hi[3], double* mass, double* momentum,
                      double* velocity);
+/* With enabled != 0 the last substep of every tg_step / tg_step_capture runs
+ * the six phases (engine.cpp:288-297) instead of the fused plan, so the grid
+ * afterwards is the reference's post-step grid (engine.cpp:180-205). Default
+ * off (the fused plan is faster and its particle results are the same). */
+int tg_set_keep_grid(tg_handle h, int enabled);
 
 /* ---- capture (render) -------------------------------------------------- */
 
@@ -232,6 +290,13 @@ int tg_sync(tg_handle h);
  * indenter_move_p2g, finalize]. The state advances exactly as tg_step
  * would. Instrumentation for the roofline in bench.py. */
 int tg_time_phases(tg_handle h, const double indenter_velocity[3], int reps, double* out_ms);
+/* Instrumentation counters of a handle: [0] kernels launched, [1] node-array
+ * reallocations (the grid arrays cover a box of the logical grid and grow
+ * on demand), [2] bytes of the node arrays, [3] substeps whose indenter
+ * look-ahead walks finalize completed (the elastomer left the walks' box),
+ * [4] allocated nodes, [5] cached substep graphs, [6] indenter particles
+ * advected by the column walks so far (the rest are caught up in bulk). */
+int tg_stats(tg_handle h, int64_t out[7]);
 /* cudaStream_t of the handle (for event timing by the caller). */
 void* tg_stream(tg_handle h);
 /* Number of kernels this handle has launched so far (graph nodes count). */

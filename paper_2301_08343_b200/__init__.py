@@ -85,6 +85,21 @@ class TgSurface(C.Structure):
                 ("particle", C.POINTER(C.c_uint32))]
 
 
+class TgSceneParams(C.Structure):
+    """mpm::SceneParams (sim_state.hpp:81-98)."""
+    _fields_ = [("grid_resolution", C.c_int * 3), ("grid_edge", C.c_double),
+                ("grid_origin", C.c_double * 3), ("youngs_modulus", C.c_double),
+                ("poisson_ratio", C.c_double), ("density", C.c_double), ("dt", C.c_double),
+                ("fixed_bottom_layers", C.c_int), ("gravity", C.c_double * 3),
+                ("indenter_mass_scale", C.c_double)]
+
+
+class TgLattice(C.Structure):
+    """An elastomer ParticleSet with its LatticeMeta (particle_set.hpp:18-30)."""
+    _fields_ = [("counts", C.c_int * 3), ("dims", C.c_double * 3), ("origin", C.c_double * 3),
+                ("positions", _dp)]
+
+
 class TgRender(C.Structure):
     _fields_ = [("pixel_to_meter", C.c_double), ("crop_offset", C.c_double * 2),
                 ("crop_scale", C.c_double), ("width", C.c_int), ("height", C.c_int),
@@ -101,7 +116,9 @@ EXPORTED = [
     "tg_download_grid", "tg_render_from_config", "tg_capture", "tg_extract_depth",
     "tg_crop_align", "tg_surface_normals", "tg_phong_render", "tg_step_many", "tg_step_capture_many", "tg_sync",
     "tg_stream", "tg_kernel_launches", "tg_set_graphs", "tg_last_error", "tg_version",
-    "tg_generate_cloud", "tg_placed_indenter", "tg_time_phases", "tg_polar",
+    "tg_generate_cloud", "tg_placed_indenter", "tg_time_phases", "tg_polar", "tg_init_scene",
+    "tg_build_sim_points", "tg_download_constants", "tg_set_keep_grid", "tg_stats",
+    "tg_build_episodes",
 ]
 
 PHASE_TIMING_NAMES = ["p2g_elastomer_first", "p2g_indenter_first", "grid_update",
@@ -160,6 +177,15 @@ def lib():
         L.tg_kernel_launches.restype = C.c_int64
         L.tg_set_graphs.argtypes = [C.c_void_p, C.c_int]
         L.tg_time_phases.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
+        L.tg_init_scene.argtypes = [C.c_int, C.POINTER(TgSceneParams), C.POINTER(TgLattice), _dp,
+                                    C.c_int64, _dp, C.POINTER(C.c_void_p)]
+        L.tg_build_sim_points.argtypes = [C.c_int, C.c_char_p, _dp, C.c_int64,
+                                          C.POINTER(C.c_void_p)]
+        L.tg_download_constants.argtypes = [C.c_void_p, _dp, _dp, _u8p]
+        L.tg_set_keep_grid.argtypes = [C.c_void_p, C.c_int]
+        L.tg_stats.argtypes = [C.c_void_p, _i64p]
+        L.tg_build_episodes.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_int, _dp,
+                                        C.POINTER(C.c_void_p)]
         L.tg_polar.argtypes = [C.c_int, _dp, C.c_int64, C.c_int, C.c_double, C.c_double, _dp, _dp]
         L.tg_generate_cloud.argtypes = [C.c_char_p, C.c_int64, C.c_uint64, _dp]
         L.tg_placed_indenter.argtypes = [C.c_char_p, C.c_char_p, C.c_double, C.c_double, _dp,
@@ -246,6 +272,27 @@ class SimState:
         n = self.n
         arrs = [None if a is None else _d(a, (n, k)) for a, k in ((x, 3), (v, 3), (Cm, 9), (F, 9))]
         _check(lib().tg_upload(self._h, *[_p(a) for a in arrs]))
+
+    def constants(self) -> dict:
+        """ParticleStore::mass / volume0 / tag (reference order)."""
+        n = self.n
+        out = dict(mass=np.empty(n), volume0=np.empty(n), tag=np.empty(n, np.uint8))
+        _check(lib().tg_download_constants(self._h, _p(out["mass"]), _p(out["volume0"]),
+                                           _p(out["tag"], _u8p)))
+        return out
+
+    def stats(self) -> dict:
+        """Instrumentation counters (tg_stats)."""
+        out = np.zeros(7, np.int64)
+        _check(lib().tg_stats(self._h, _p(out, _i64p)))
+        keys = ["kernel_launches", "regrows", "grid_bytes", "walk_fixups", "grid_nodes",
+                "graphs", "indenter_walked"]
+        return dict(zip(keys, (int(v) for v in out)))
+
+    def set_keep_grid(self, enabled: bool = True):
+        """Keep the reference's post-step grid (tg_set_keep_grid): the last
+        substep of each step runs the phase path."""
+        _check(lib().tg_set_keep_grid(self._h, int(bool(enabled))))
 
     @property
     def diag(self) -> SimpleNamespace:
@@ -343,7 +390,42 @@ def _vec(v):
 
 
 class mpm:  # noqa: N801 — mirrors tacchi::mpm
-    """engine.hpp:10-35"""
+    """engine.hpp:10-35, sim_state.hpp:102-104"""
+
+    @staticmethod
+    def init_scene(params: dict, elastomer: dict, indenter, indenter_velocity=(0.0, 0.0, 0.0),
+                   device: int = 0) -> SimState:
+        """mpm::init_scene(SceneParams, elastomer lattice, indenter points, v0)
+        (scene.cpp:28-87): masses, rest volumes, tags and the surface lattice
+        are derived here as the reference does.
+
+        params: grid_resolution, grid_edge, [grid_origin], [E, nu, rho], dt,
+        [fixed_bottom_layers = 2], [gravity], [indenter_mass_scale = 80].
+        elastomer: counts, dims, origin, [positions] (lattice order; default
+        make_elastomer_lattice). indenter: n x 3 placed points (m)."""
+        P = TgSceneParams()
+        P.grid_resolution[:] = [int(r) for r in params["grid_resolution"]]
+        P.grid_edge = float(params["grid_edge"])
+        P.grid_origin[:] = list(params.get("grid_origin", (0.0, 0.0, 0.0)))
+        P.youngs_modulus = float(params.get("E", 1.45e5))
+        P.poisson_ratio = float(params.get("nu", 0.45))
+        P.density = float(params.get("rho", 1000.0))
+        P.dt = float(params["dt"])
+        P.fixed_bottom_layers = int(params.get("fixed_bottom_layers", 2))
+        P.gravity[:] = list(params.get("gravity", (0.0, 0.0, 0.0)))
+        P.indenter_mass_scale = float(params.get("indenter_mass_scale", 80.0))
+        L = TgLattice()
+        L.counts[:] = [int(c) for c in elastomer["counts"]]
+        L.dims[:] = list(elastomer["dims"])
+        L.origin[:] = list(elastomer["origin"])
+        pos = elastomer.get("positions")
+        pos = None if pos is None else _d(pos, (-1, 3))
+        L.positions = _p(pos)
+        ind = _d(indenter, (-1, 3))
+        h = C.c_void_p()
+        _check(lib().tg_init_scene(device, C.byref(P), C.byref(L), _p(ind), len(ind),
+                                   _p(_vec(indenter_velocity)), C.byref(h)))
+        return SimState(h.value, device)
 
     @staticmethod
     def zero_grid(state: SimState):
@@ -441,6 +523,24 @@ class sim:  # noqa: N801 — mirrors tacchi::sim
         h = C.c_void_p()
         _check(lib().tg_build_sim(device, _cfg(cfg), obj.encode(), offset_x, offset_y,
                                   C.byref(h)))
+        return SimState(h.value, device)
+
+    @staticmethod
+    def build_episodes(cfg, obj: str, poses, device: int = 0) -> list:
+        """Episodes of one object sharing one indenter cloud (tg_build_episodes):
+        poses is n x 3 (offset_x, offset_y, z_rotation_rad)."""
+        P = _d(poses, (-1, 3))
+        hs = (C.c_void_p * len(P))()
+        _check(lib().tg_build_episodes(device, _cfg(cfg), obj.encode(), len(P), _p(P), hs))
+        return [SimState(h, device) for h in hs]
+
+    @staticmethod
+    def build_sim_points(cfg, indenter, device: int = 0) -> SimState:
+        """sim::build_sim(cfg, indenter) with caller-placed indenter points
+        (scene_builder.cpp:63-78)."""
+        ind = _d(indenter, (-1, 3))
+        h = C.c_void_p()
+        _check(lib().tg_build_sim_points(device, _cfg(cfg), _p(ind), len(ind), C.byref(h)))
         return SimState(h.value, device)
 
     @staticmethod

@@ -142,29 +142,107 @@ int configure_device(int device);  // mpm_kernels.cu
 // Host <-> device copies ordered on the handle's (non-blocking) stream and
 // completed before returning: every upload is ordered after the kernels
 // already queued on the handle and before the ones that follow.
-static cudaError_t copy_sync(DeviceSim& s, void* dst, const void* src, size_t bytes,
+cudaError_t copy_sync(DeviceSim& s, void* dst, const void* src, size_t bytes,
                              cudaMemcpyKind kind) {
   const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, s.stream);
   if (e != cudaSuccess) return e;
   return cudaStreamSynchronize(s.stream);
 }
 
-// The grid arrays in one allocation (A.lo | A.hi | V.xy | V.z | M_I).
-static bool alloc_grid(DeviceSim& s) {
-  const size_t n = s.n_nodes;
+// The grid arrays in one allocation (A.lo | A.hi | V.xy | V.z | M_I) over
+// the node box [lo, lo + dim) of the logical grid, zeroed on the stream.
+static bool alloc_grid(DeviceSim& s, const int lo[3], const int dim[3]) {
+  const size_t n = static_cast<size_t>(dim[0]) * dim[1] * dim[2];
   const size_t b2 = n * sizeof(double2);
   // +2: the staging reads vz rows from an even node over an even count
   const size_t bz = ((n + 2) * sizeof(double) + 255) & ~size_t(255);
   const size_t b1 = n * sizeof(double);
+  void* slab = nullptr;
+  if (cudaMalloc(&slab, 3 * b2 + bz + b1) != cudaSuccess) return false;
+  cudaFree(s.grid_slab);
+  s.grid_slab = slab;
   s.grid_slab_bytes = 3 * b2 + bz + b1;
-  if (cudaMalloc(&s.grid_slab, s.grid_slab_bytes) != cudaSuccess) return false;
-  char* p = static_cast<char*>(s.grid_slab);
+  s.n_nodes = n;
+  for (int a = 0; a < 3; ++a) {
+    s.geo.ga_lo[a] = lo[a];
+    s.geo.ga_dim[a] = dim[a];
+  }
+  char* p = static_cast<char*>(slab);
   s.grid_mp.lo = reinterpret_cast<double2*>(p);
   s.grid_mp.hi = reinterpret_cast<double2*>(p + b2);
   s.grid_v.xy = reinterpret_cast<double2*>(p + 2 * b2);
   s.grid_v.z = reinterpret_cast<double*>(p + 3 * b2);
   s.grid_mi = reinterpret_cast<double*>(p + 3 * b2 + bz);
+  cudaMemsetAsync(slab, 0, s.grid_slab_bytes, s.stream);
   return true;
+}
+
+// Node margin around the boxes the step path scatters into when the
+// allocation is (re)sized: room for the elastomer to deform and move before
+// the next regrow.
+constexpr int kAllocMargin = 4;
+// The indenter's look-ahead walks touch nodes up to 3 outside the elastomer
+// node box (its box widened by one node, plus the 3-node stencil).
+constexpr int kWalkReach = 3;
+
+// The allocation box that covers [lo, hi) with kAllocMargin (clamped to the
+// logical grid, z start and length even where the grid allows: the velocity
+// staging copies vz rows in 16-byte units).
+static void alloc_box_for(const DeviceSim& s, const int lo[3], const int hi[3], int out_lo[3],
+                          int out_dim[3]) {
+  for (int a = 0; a < 3; ++a) {
+    int l = std::max(lo[a] - kAllocMargin, 0);
+    int h = std::min(hi[a] + kAllocMargin, s.geo.res[a]);
+    if (a == 2) {
+      // z rows padded to a multiple of kZPad nodes (128-byte aligned rows of
+      // the 8-byte arrays), even start
+      l &= ~1;
+      const int pad = s.zpad;
+      int d = ((h - l + pad - 1) / pad) * pad;
+      if (l + d > s.geo.res[a]) l = std::max(s.geo.res[a] - d, 0) & ~1;
+      h = std::min(l + d, s.geo.res[a]);
+      if ((h - l) & 1) h = h < s.geo.res[a] ? h + 1 : h;
+    }
+    out_lo[a] = l;
+    out_dim[a] = std::max(h - l, 1);
+  }
+  if (const char* e = std::getenv("TACCHI_DENSE_GRID"))
+    if (std::atoi(e))
+      for (int a = 0; a < 3; ++a) {
+        out_lo[a] = 0;
+        out_dim[a] = s.geo.res[a];
+      }
+}
+
+static void drop_graphs(DeviceSim& s) {
+  for (auto& kv : s.graphs) cudaGraphExecDestroy(kv.second);
+  s.graphs.clear();
+  s.graph_kernels.clear();
+}
+
+// Grows the node arrays so that they cover [lo, hi) (and what they covered
+// before). The arrays come back zeroed: any look-ahead scatter is dropped.
+// Kernel parameters (pointers, Geometry) change, so the cached graphs go.
+static int ensure_alloc(DeviceSim& s, const int lo[3], const int hi[3]) {
+  bool inside = true;
+  for (int a = 0; a < 3; ++a)
+    inside = inside && lo[a] >= s.geo.ga_lo[a] && hi[a] <= s.geo.ga_lo[a] + s.geo.ga_dim[a];
+  if (inside && s.grid_slab) return TG_OK;
+  int want_lo[3], want_hi[3];
+  for (int a = 0; a < 3; ++a) {
+    want_lo[a] = s.grid_slab ? std::min(lo[a], s.geo.ga_lo[a]) : lo[a];
+    want_hi[a] = s.grid_slab ? std::max(hi[a], s.geo.ga_lo[a] + s.geo.ga_dim[a]) : hi[a];
+  }
+  int blo[3], bdim[3];
+  alloc_box_for(s, want_lo, want_hi, blo, bdim);
+  CUDA_TRY(cudaStreamSynchronize(s.stream));
+  if (!alloc_grid(s, blo, bdim)) return fail(TG_ERR_CUDA, "grid allocation failed");
+  drop_graphs(s);
+  s.grid_ready = false;
+  s.grid_dirty = false;
+  s.grid_ref = false;
+  s.regrows += 1;
+  return TG_OK;
 }
 
 int create(int device, const tg_params* P, const tg_particles* in, const tg_surface* surf,
@@ -226,6 +304,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   if (const char* m = std::getenv("TACCHI_SCATTER")) g.scatter_mode = std::atoi(m);
   if (const char* f = std::getenv("TACCHI_FULL_INDENTER")) s->full_indenter = std::atoi(f) != 0;
   // launch-shape A/B switches (tools/README.md); defaults are the measured best
+  s->zpad = 16;
+  if (const char* e = std::getenv("TACCHI_ZPAD")) s->zpad = std::max(2, std::atoi(e) & ~1);
   g.gu_bps = 10;
   g.pdl_early = 1;
   g.ind_first = 1;
@@ -267,13 +347,29 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
     col_starts = {n_el, n};
   }
   cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
-  s->n_nodes = static_cast<size_t>(g.res[0]) * g.res[1] * g.res[2];
+  // Node arrays over the elastomer's node box plus the walks' reach (the
+  // step path touches nothing else); the whole window when there is no
+  // elastomer. They grow on demand (ensure_alloc).
+  int alo[3], ahi[3], adim[3];
+  {
+    const int64_t b = n_el > 0 ? 0 : n_el, e = n_el > 0 ? n_el : n;
+    for (int a = 0; a < 3; ++a) {
+      double lo = in->x[3 * b + a], hi = lo;
+      for (int64_t p = b; p < e; ++p) {
+        lo = std::min(lo, in->x[3 * p + a]);
+        hi = std::max(hi, in->x[3 * p + a]);
+      }
+      alo[a] = host_base(lo, g.origin[a], g.inv_dx) - kWalkReach;
+      ahi[a] = host_base(hi, g.origin[a], g.inv_dx) + 3 + kWalkReach;
+    }
+    alloc_box_for(*s, alo, ahi, alo, adim);
+  }
   bool ok = cudaMalloc(&s->x, 3 * n * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->v, 3 * n * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->C, std::max<int64_t>(9 * n_el, 1) * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->F, std::max<int64_t>(9 * n_el, 1) * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&s->tag, std::max<int64_t>(n_el, 1)) == cudaSuccess &&
-            alloc_grid(*s) &&
+            alloc_grid(*s, alo, adim) &&
             cudaMalloc(&s->col_start, std::max<size_t>(col_starts.size(), 1) * sizeof(int64_t)) ==
                 cudaSuccess &&
             cudaMalloc(&s->ind_moves, std::max<int64_t>(n_ind, 1)) == cudaSuccess &&
@@ -284,17 +380,13 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
     delete s;
     return fail(TG_ERR_CUDA, "tg_create: device allocation failed");
   }
-  cudaMemsetAsync(s->grid_mp.lo, 0, s->n_nodes * sizeof(double2), s->stream);
-  cudaMemsetAsync(s->grid_mp.hi, 0, s->n_nodes * sizeof(double2), s->stream);
-  cudaMemsetAsync(s->grid_v.xy, 0, s->n_nodes * sizeof(double2), s->stream);
-  cudaMemsetAsync(s->grid_v.z, 0, (s->n_nodes + 2) * sizeof(double), s->stream);
-  cudaMemsetAsync(s->grid_mi, 0, s->n_nodes * sizeof(double), s->stream);
   cudaMemsetAsync(s->ind_moves, 0, std::max<int64_t>(n_ind, 1), s->stream);
   s->n_cols = col_starts.empty() ? 0 : static_cast<int>(col_starts.size()) - 1;
   if (s->n_cols > 0)
     copy_sync(*s, s->col_start, col_starts.data(), col_starts.size() * sizeof(int64_t),
               cudaMemcpyHostToDevice);
   std::memset(s->h_ctl, 0, sizeof(Ctl));
+  s->h_ctl->err = kNoError;
   for (int a = 0; a < 3; ++a) s->h_ctl->vind[a] = in->indenter_velocity[a];
   // Is the indenter velocity uniform (it is for init_scene's output)?
   s->ind_v_uniform = true;
@@ -382,21 +474,35 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
   CUDA_TRY(cudaGetLastError());
   const Ctl& c = *s.h_ctl;
   s.host_substep = c.substep;
-  if (c.err_code == 0) return TG_OK;
+  if (c.err == kNoError) return TG_OK;
   flush_indenter(s);  // the state at the throw includes the indenter's advects
-  const int code = c.err_code;
-  const int at = c.err_substep;
+  const int code = err_code_of(c.err);
+  const int at = err_substep_of(c.err);
   // Clear the latch; the next call re-derives the window from the state.
-  CUDA_TRY(cudaMemsetAsync(&s.ctl->err_code, 0, sizeof(int), s.stream));
+  static const unsigned long long clear = kNoError;
+  CUDA_TRY(cudaMemcpyAsync(&s.ctl->err, &clear, sizeof(clear), cudaMemcpyHostToDevice, s.stream));
   launch_reset(s, kResetAll);
   s.window_valid = false;
-  // A look-ahead scatter may have started anywhere in the grid: reset the
-  // accumulators wholesale (errors are rare; this keeps the invariant simple).
-  CUDA_TRY(cudaMemsetAsync(s.grid_mp.lo, 0, s.n_nodes * sizeof(double2), s.stream));
-  CUDA_TRY(cudaMemsetAsync(s.grid_mp.hi, 0, s.n_nodes * sizeof(double2), s.stream));
-  CUDA_TRY(cudaMemsetAsync(s.grid_mi, 0, s.n_nodes * sizeof(double), s.stream));
   s.grid_dirty = false;
   s.grid_ready = false;
+  if (code == kErrRegrow) {
+    // A scatter of substep `at` would have left the node arrays: every
+    // substep before `at` is complete; grow the arrays over the boxes of
+    // substep `at` (finalize wrote them) and let the caller run the rest.
+    int lo[3], hi[3];
+    const bool walks = s.n_cols > 0 && !s.full_indenter && s.ind_v_uniform && s.n_el > 0;
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = walks ? c.box_lo[0][a] - kWalkReach : c.win_lo[a];
+      hi[a] = walks ? c.box_hi[0][a] + kWalkReach : c.win_hi[a];
+    }
+    const int rc = ensure_alloc(s, lo, hi);
+    if (rc) return rc;
+    s.resume_substeps = std::max(end_substep - at, 0);
+    return kResume;
+  }
+  // A look-ahead scatter may have started anywhere in the grid: reset the
+  // accumulators wholesale (errors are rare; this keeps the invariant simple).
+  CUDA_TRY(cudaMemsetAsync(s.grid_slab, 0, s.grid_slab_bytes, s.stream));
   CUDA_TRY(cudaStreamSynchronize(s.stream));
   if (at >= end_substep) return TG_OK;
   const char* what = code == kErrOutOfGrid
@@ -495,6 +601,7 @@ int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
   s.grid_dirty = false;
   s.ind_v_uniform = true;
   s.grid_ready = true;
+  s.grid_ref = false;  // the grid now holds the next substep's look-ahead scatter
   return TG_OK;
 }
 
@@ -503,10 +610,38 @@ int step_finish(DeviceSim& s, int n_substeps) {
   return sync_and_check(s, s.pending_start + std::max(n_substeps, 0));
 }
 
+int phase(DeviceSim& s, int ph, const double vind[3]);
+
 int step(DeviceSim& s, const double vind[3], int n_substeps) {
-  const int rc = step_submit(s, vind, n_substeps);
-  if (rc) return rc;
-  return step_finish(s, n_substeps);
+  if (s.keep_grid && n_substeps > 0) {
+    // The fused plan leaves a look-ahead scatter in the grid; with keep_grid
+    // the last substep runs the six phases (engine.cpp:288-297) so that the
+    // grid afterwards holds that substep's P2G and grid_update, as the
+    // reference's does.
+    for (int left = n_substeps - 1; left > 0;) {  // chunks as tg_step's
+      const int c = left > 200 ? 200 : left;
+      const int rc = step_submit(s, vind, c);
+      if (rc) return rc;
+      const int e = step_finish(s, c);
+      if (e == kResume) {  // node arrays grown mid-chunk: run the rest of it
+        left -= c - s.resume_substeps;
+        continue;
+      }
+      if (e) return e;
+      left -= c;
+    }
+    for (int ph = TG_PHASE_ZERO_GRID; ph <= TG_PHASE_ADVECT; ++ph)
+      if (const int e = phase(s, ph, vind)) return e;
+    return TG_OK;
+  }
+  for (int left = n_substeps;;) {
+    const int rc = step_submit(s, vind, left);
+    if (rc) return rc;
+    const int e = step_finish(s, left);
+    if (e != kResume) return e;
+    left = s.resume_substeps;  // node arrays grown mid-call: run the rest
+    if (left <= 0) return TG_OK;
+  }
 }
 
 int check_device_public(int device) { return check_device(device); }
@@ -570,7 +705,10 @@ int time_phases(DeviceSim& s, const double vind[3], int reps, double* out_ms) {
   if (cols) launch_ind_catchup(s);
   for (auto& e : ev) cudaEventDestroy(e);
   s.grid_ready = true;  // the last substep scattered the next one, as in step()
-  return sync_and_check(s, start + reps);
+  s.grid_ref = false;
+  const int rc = sync_and_check(s, start + reps);
+  // grown mid-run: the timings cover a partial run; the state is consistent
+  return rc == kResume ? TG_OK : rc;
 }
 
 int phase(DeviceSim& s, int ph, const double vind[3]) {
@@ -582,12 +720,33 @@ int phase(DeviceSim& s, int ph, const double vind[3]) {
   }
   const int start = s.host_substep;
   const int sms = sm_count(s.device);
+  // The phase path touches the whole active window (every indenter particle
+  // scatters): grow the node arrays over it and the box zero_grid clears.
+  auto cover_window = [&]() -> int {
+    CUDA_TRY(cudaMemcpyAsync(s.h_ctl, s.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s.stream));
+    CUDA_TRY(cudaStreamSynchronize(s.stream));
+    const Ctl& c = *s.h_ctl;
+    if (c.err != kNoError) return TG_OK;  // reported by sync_and_check below
+    int lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+      const bool clr = c.clr_hi[a] > c.clr_lo[a];
+      lo[a] = clr ? std::min(c.win_lo[a], c.clr_lo[a]) : c.win_lo[a];
+      hi[a] = clr ? std::max(c.win_hi[a], c.clr_hi[a]) : c.win_hi[a];
+      if (hi[a] <= lo[a]) return TG_OK;  // no window yet
+    }
+    return ensure_alloc(s, lo, hi);
+  };
   switch (ph) {
-    case TG_PHASE_ZERO_GRID:
+    case TG_PHASE_ZERO_GRID: {
       launch_window(s);
+      if (const int rc = cover_window()) return rc;
       launch_clear(s, sms);
       break;
-    case TG_PHASE_PARTICLE_TO_GRID: launch_p2g(s, true); break;
+    }
+    case TG_PHASE_PARTICLE_TO_GRID:
+      if (const int rc = cover_window()) return rc;
+      launch_p2g(s, true);
+      break;
     case TG_PHASE_GRID_UPDATE: launch_grid_update(s, sms, false); break;
     case TG_PHASE_GRID_TO_PARTICLE: launch_phase_g2p(s); break;
     case TG_PHASE_APPLY_BOUNDARY:
@@ -600,7 +759,12 @@ int phase(DeviceSim& s, int ph, const double vind[3]) {
     default: return fail(TG_ERR_INVALID_ARGUMENT, "tg_phase: bad phase id");
   }
   s.window_valid = false;  // phases drive zero_grid explicitly
-  return sync_and_check(s, start + 1);
+  s.grid_ref = true;       // the phases keep the grid exactly as the reference's
+  const int rc = sync_and_check(s, start + 1);
+  if (rc == kResume)  // a scatter outside the node arrays (P2G without zero_grid)
+    return fail(TG_ERR_INVALID_ARGUMENT,
+                "particle_to_grid: particles outside the grid window; call zero_grid first");
+  return rc;
 }
 
 static void to_component_major(const double* src, int64_t n, int ncomp, const std::vector<int64_t>& perm,
@@ -733,6 +897,7 @@ void tg_destroy(tg_handle h) { delete H(h); }
 
 int tg_step(tg_handle h, const double v[3], int n) {
   if (!h || !v) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step: null argument");
+  if (H(h)->keep_grid) return tacchi_b200::step(*H(h), v, n);
   // The per-call indenter move counters are 8-bit: long calls run in chunks
   // (identical results; one extra host sync per 200 substeps).
   while (n > 0) {
@@ -787,8 +952,8 @@ int tg_grid_window(tg_handle h, int lo[3], int hi[3]) {
   cudaMemcpyAsync(s.h_ctl, s.ctl, sizeof(tacchi_b200::Ctl), cudaMemcpyDeviceToHost, s.stream);
   if (cudaStreamSynchronize(s.stream) != cudaSuccess) return fail(TG_ERR_CUDA, "readback failed");
   for (int a = 0; a < 3; ++a) {
-    lo[a] = s.h_ctl->win_lo[a];
-    hi[a] = s.h_ctl->win_hi[a];
+    lo[a] = s.h_ctl->ref_lo[a];
+    hi[a] = s.h_ctl->ref_hi[a];
   }
   return TG_OK;
 }
@@ -800,6 +965,11 @@ int tg_download_grid(tg_handle h, const int lo[3], const int hi[3], double* mass
   for (int a = 0; a < 3; ++a)
     if (lo[a] < 0 || hi[a] > s.geo.res[a] || hi[a] <= lo[a])
       return fail(TG_ERR_INVALID_ARGUMENT, "tg_download_grid: box outside the grid");
+  if (!s.grid_ref)
+    return fail(TG_ERR_INVALID_ARGUMENT,
+                "tg_download_grid: the last tg_step ran the fused substep plan, whose grid holds "
+                "the next substep's look-ahead scatter; call tg_set_keep_grid(h, 1) before "
+                "stepping to keep the reference's post-step grid");
   cudaSetDevice(s.device);
   const size_t cnt = static_cast<size_t>(hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]);
   double* d = nullptr;
@@ -841,6 +1011,13 @@ int tg_step_capture(tg_handle h, const double v[3], int n, const tg_render* r, d
                     uint8_t* rgb_out) {
   if (!h || !v || !r) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture: null argument");
   DeviceSim& s = *H(h);
+  if (s.keep_grid) {  // the step ends on the phase path; capture afterwards
+    const int rc = tacchi_b200::step(s, v, n);
+    if (rc) return rc;
+    std::string msg;
+    const int crc = tacchi_b200::capture(s, *r, depth_out, rgb_out, msg);
+    return crc ? fail(crc, msg) : TG_OK;
+  }
   while (n > 200) {  // long calls: chunks as tg_step
     const int rc = tacchi_b200::step(s, v, 200);
     if (rc) return rc;
@@ -851,6 +1028,12 @@ int tg_step_capture(tg_handle h, const double v[3], int n, const tg_render* r, d
   std::string msg;
   const int crc = tacchi_b200::capture_enqueue(s, *r, depth_out != nullptr, rgb_out != nullptr, msg);
   rc = tacchi_b200::step_finish(s, n);  // syncs the stream; the step's error wins
+  if (rc == tacchi_b200::kResume) {  // node arrays grown mid-call: finish, capture again
+    rc = tacchi_b200::step(s, v, s.resume_substeps);
+    if (rc) return rc;
+    const int c2 = tacchi_b200::capture(s, *r, depth_out, rgb_out, msg);
+    return c2 ? fail(c2, msg) : TG_OK;
+  }
   if (rc) return rc;
   if (crc) return fail(crc, msg);
   tacchi_b200::capture_collect(s, depth_out, rgb_out);
@@ -919,10 +1102,14 @@ static int many(tg_handle* hs, int n_handles, const double* velocities, int n_su
     if (!hs[i]) return fail(TG_ERR_INVALID_ARGUMENT, std::string(who) + ": null handle");
   std::vector<int> rc(n_handles, TG_OK), crc(n_handles, TG_OK);
   std::vector<std::string> msg(n_handles);
-  std::vector<char> submitted(n_handles, 0);
+  std::vector<char> submitted(n_handles, 0), stepped(n_handles, 0);
   for (int i = 0; i < n_handles; ++i) {
     DeviceSim& s = *H(hs[i]);
-    rc[i] = tacchi_b200::step_submit(s, velocities + 3 * i, n_substeps);
+    // keep_grid handles step to completion here (their last substep runs
+    // the phase path), the others are only submitted
+    stepped[i] = s.keep_grid;
+    rc[i] = s.keep_grid ? tacchi_b200::step(s, velocities + 3 * i, n_substeps)
+                        : tacchi_b200::step_submit(s, velocities + 3 * i, n_substeps);
     if (rc[i]) {
       msg[i] = g_last_error;
       continue;
@@ -938,12 +1125,26 @@ static int many(tg_handle* hs, int n_handles, const double* velocities, int n_su
   for (int i = 0; i < n_handles; ++i) {
     if (submitted[i]) {
       DeviceSim& s = *H(hs[i]);
-      rc[i] = tacchi_b200::step_finish(s, n_substeps);  // the step's error wins
+      if (stepped[i])
+        rc[i] = cudaStreamSynchronize(s.stream) == cudaSuccess
+                    ? TG_OK
+                    : fail(TG_ERR_CUDA, "capture failed on the device");
+      else
+        rc[i] = tacchi_b200::step_finish(s, n_substeps);  // the step's error wins
+      if (rc[i] == tacchi_b200::kResume) {  // node arrays grown mid-call
+        rc[i] = tacchi_b200::step(s, velocities + 3 * i, s.resume_substeps);
+        if (!rc[i] && renders && !crc[i]) {
+          const tg_render& r = renders[n_renders == 1 ? 0 : i];
+          crc[i] = tacchi_b200::capture(s, r, depth_outs ? depth_outs[i] : nullptr,
+                                        rgb_outs ? rgb_outs[i] : nullptr, msg[i]);
+          if (!crc[i]) stepped[i] = 2;  // outputs already delivered
+        }
+      }
       if (rc[i]) {
         msg[i] = g_last_error;
       } else if (crc[i]) {
         rc[i] = crc[i];
-      } else if (renders) {
+      } else if (renders && stepped[i] != 2) {
         tacchi_b200::capture_collect(s, depth_outs ? depth_outs[i] : nullptr,
                                      rgb_outs ? rgb_outs[i] : nullptr);
       }
@@ -984,6 +1185,49 @@ int tg_time_phases(tg_handle h, const double v[3], int reps, double* out_ms) {
 
 void* tg_stream(tg_handle h) { return h ? static_cast<void*>(H(h)->stream) : nullptr; }
 int64_t tg_kernel_launches(tg_handle h) { return h ? H(h)->kernel_launches : 0; }
+int tg_stats(tg_handle h, int64_t out[7]) {
+  if (!h || !out) return fail(TG_ERR_INVALID_ARGUMENT, "tg_stats: null argument");
+  DeviceSim& s = *H(h);
+  cudaSetDevice(s.device);
+  if (cudaMemcpyAsync(s.h_ctl, s.ctl, sizeof(tacchi_b200::Ctl), cudaMemcpyDeviceToHost, s.stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(s.stream) != cudaSuccess)
+    return fail(TG_ERR_CUDA, "tg_stats: readback failed");
+  out[0] = s.kernel_launches;
+  out[1] = s.regrows;
+  out[2] = static_cast<int64_t>(s.grid_slab_bytes);
+  out[3] = s.h_ctl->walk_fixups;
+  out[4] = static_cast<int64_t>(s.n_nodes);
+  out[5] = static_cast<int64_t>(s.graphs.size());
+  out[6] = static_cast<int64_t>(s.h_ctl->ind_walked);
+  return TG_OK;
+}
+
+int tg_set_keep_grid(tg_handle h, int enabled) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_set_keep_grid: null handle");
+  H(h)->keep_grid = enabled != 0;
+  return TG_OK;
+}
+
+int tg_download_constants(tg_handle h, double* mass, double* volume0, uint8_t* tag) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_download_constants: null handle");
+  DeviceSim& s = *H(h);
+  cudaSetDevice(s.device);
+  std::vector<uint8_t> el_tag(static_cast<size_t>(std::max<int64_t>(s.n_el, 1)));
+  if (tag && s.n_el > 0) {
+    const cudaError_t e = tacchi_b200::copy_sync(s, el_tag.data(), s.tag, s.n_el, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(TG_ERR_CUDA, cudaGetErrorString(e));
+  }
+  for (int64_t q = 0; q < s.n; ++q) {
+    const int64_t r = s.perm[q];  // reference index
+    const bool el = q < s.n_el;
+    if (mass) mass[r] = el ? s.m_el : s.m_ind;
+    if (volume0) volume0[r] = el ? s.vol_el : s.vol_ind;
+    if (tag) tag[r] = el ? el_tag[q] : tacchi_b200::kIndenter;
+  }
+  return TG_OK;
+}
+
 int tg_set_graphs(tg_handle h, int enabled) {
   if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_set_graphs: null handle");
   H(h)->use_graphs = enabled != 0;

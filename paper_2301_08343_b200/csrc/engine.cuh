@@ -17,8 +17,11 @@ namespace tacchi_b200 {
 // Device-resident control block: latched error, reductions, active windows,
 // diagnostics and the commanded velocity. One per handle.
 struct Ctl {
-  int err_code;      // first error wins (atomicCAS from 0)
-  int err_substep;   // absolute substep index the error belongs to
+  // Latched error: (substep << 8) | code, ~0 when clear. atomicMin keeps the
+  // earliest substep's error (and, within a substep, the lowest code: a real
+  // error before an allocation regrow). One word, so a reader never sees a
+  // code without its substep.
+  unsigned long long err;
   int substep;       // absolute index of the substep being executed
   int pad0;
   // Motion reductions in two slots by substep parity: slot s & 1 holds the
@@ -28,7 +31,9 @@ struct Ctl {
   unsigned long long ind_lo[2][3], ind_hi[2][3];  // order_key() of the indenter bbox
   unsigned long long max_v2[2];                  // bits of max |v|^2 (non-negative)
   unsigned long long min_detf[2];         // order_key() of min det F, per substep parity
-  int win_lo[3], win_hi[3];               // Grid::active_lo/hi
+  int win_lo[3], win_hi[3];               // window of the next zero_grid (P2G of ctl->substep)
+  int ref_lo[3], ref_hi[3];               // Grid::active_lo/hi as the reference holds them:
+                                          // the window of the last zero_grid that ran
   int prev_lo[3], prev_hi[3];             // Grid::prev_lo/hi
   int clr_lo[3], clr_hi[3];               // node box to clear before P2G
   int box_lo[2][3], box_hi[2][3];         // per-material node boxes (elastomer, indenter)
@@ -37,10 +42,16 @@ struct Ctl {
   int chain_start;                        // first substep of the open indenter chain
   double diag_min_det_f, diag_max_speed;  // StepDiagnostics
   long long step_count;                   // SimState::step_count
+  long long walk_fixups;                  // substeps whose walks finalize completed
+  unsigned long long ind_walked;          // indenter particles advected by the column walks
 };
 
 struct Geometry {
   int res[3];
+  // Node arrays cover the allocation box [ga_lo, ga_lo + ga_dim) of the
+  // logical res^3 grid (node (i,j,k) at ((i-lo0)*d1 + (j-lo1))*d2 + (k-lo2)),
+  // grown on demand (engine.cu ensure_alloc / regrow).
+  int ga_lo[3], ga_dim[3];
   double dx, inv_dx;
   double origin[3];
   double mu, lambda;
@@ -71,6 +82,10 @@ struct VelBuf {
   double2* xy;
   double* z;
 };
+
+// Internal return code of step_finish / phase: the node arrays were grown
+// mid-call; DeviceSim::resume_substeps substeps remain (engine.cu).
+constexpr int kResume = -100;
 
 struct DeviceSim {
   int device = 0;
@@ -109,6 +124,13 @@ struct DeviceSim {
   bool full_indenter = false; // scatter every indenter particle (TACCHI_FULL_INDENTER=1)
   bool grid_ready = false;   // A / M_I hold the scatter of the next substep (look-ahead
                              // of the previous mpm::step call); skip the standalone P2G
+  bool keep_grid = false;    // tg_set_keep_grid: the last substep of a step runs the phase
+                             // path so the grid afterwards is the reference's (engine.cpp:288-297)
+  int regrows = 0;            // node-array reallocations so far
+  int zpad = 16;              // allocation z-row length multiple (TACCHI_ZPAD)
+  int resume_substeps = 0;    // after kResume: substeps of the call still to run
+  bool grid_ref = true;      // the node arrays hold the reference's Grid state (not a
+                             // fused look-ahead): tg_download_grid may read them
 
   // Surface lattice (sim_state.hpp:41-52) + capture scratch.
   int surf_nx = 0, surf_ny = 0;

@@ -20,6 +20,8 @@
 #include <random>
 #include <string>
 #include <vector>
+#include <thread>
+#include <atomic>
 
 #include <nlohmann/json.hpp>
 
@@ -573,6 +575,7 @@ struct Scene {
   std::vector<uint32_t> surf;
   tg_surface S{};
   int64_t n_el = 0;
+  double v0[3] = {0.0, 0.0, 0.0};  // init_scene's indenter_velocity
 };
 
 void check_margin(const tg_params& P, const V3& lo, const V3& hi, const char* label) {
@@ -587,105 +590,133 @@ void check_margin(const tg_params& P, const V3& lo, const V3& hi, const char* la
   }
 }
 
-Scene build_scene(const Config& c, const std::vector<V3>& indenter) {
+// mpm::init_scene (scene.cpp:28-87) from its own inputs: SceneParams, the
+// elastomer lattice (positions in lattice order, or make_elastomer_lattice's
+// when `lattice.positions` is NULL) and the placed indenter points.
+Scene init_scene_arrays(const tg_scene_params& sp, const tg_lattice& lat,
+                        const std::vector<V3>& indenter, const double v0[3]) {
   Scene sc;
-  tg_params& P = sc.P;
-  for (int a = 0; a < 3; ++a) {
-    P.res[a] = c.nodes[a];
-    P.origin[a] = 0.0;
-  }
-  const double edge = c.edge_mm * 1e-3;
-  P.dx = edge / c.nodes[0];  // scene.cpp:41-42
-  P.youngs_modulus = c.E;
-  P.poisson_ratio = c.nu;
-  P.density = c.rho;
-  P.dt = c.dt;
-  P.gravity[0] = 0.0;
-  P.gravity[1] = 0.0;
-  P.gravity[2] = -c.gravity_mps2;
-
   for (int a = 0; a < 3; ++a)
-    if (c.counts[a] < 2) raise(TG_ERR_CONFIG, "make_elastomer_lattice: counts must be >= 2 per axis");
-  // elastomer_for (scene_builder.cpp:26-31) + make_elastomer_lattice.
-  const double dims[3] = {c.size_mm[0] * 1e-3, c.size_mm[1] * 1e-3, c.size_mm[2] * 1e-3};
-  double origin[3], h[3];
-  for (int a = 0; a < 3; ++a) {
-    origin[a] = 0.5 * edge - 0.5 * dims[a];
-    h[a] = dims[a] / (c.counts[a] - 1);
-  }
-  const int64_t nx = c.counts[0], ny = c.counts[1], nz = c.counts[2];
+    if (lat.counts[a] < 2) raise(TG_ERR_CONFIG, "make_elastomer_lattice: counts must be >= 2 per axis");
+  const int64_t nx = lat.counts[0], ny = lat.counts[1], nz = lat.counts[2];
   const int64_t n_el = nx * ny * nz;
   if (n_el == 0 || indenter.empty())
     raise(TG_ERR_EMPTY_SCENE, "init_scene: both elastomer and indenter particle sets must be non-empty");
   // MaterialParams::validate (material.cpp:11-16), dt (scene.cpp:33)
-  if (!(c.E > 0.0)) raise(TG_ERR_CONFIG, "youngs_modulus must be > 0");
-  if (!(c.nu >= 0.0 && c.nu < 0.5)) raise(TG_ERR_CONFIG, "poisson_ratio must be in [0, 0.5)");
-  if (!(c.rho > 0.0)) raise(TG_ERR_CONFIG, "density must be > 0");
-  if (!(c.dt > 0.0)) raise(TG_ERR_CONFIG, "dt must be > 0");
+  if (!(sp.youngs_modulus > 0.0)) raise(TG_ERR_CONFIG, "youngs_modulus must be > 0");
+  if (!(sp.poisson_ratio >= 0.0 && sp.poisson_ratio < 0.5))
+    raise(TG_ERR_CONFIG, "poisson_ratio must be in [0, 0.5)");
+  if (!(sp.density > 0.0)) raise(TG_ERR_CONFIG, "density must be > 0");
+  if (!(sp.dt > 0.0)) raise(TG_ERR_CONFIG, "dt must be > 0");
+  tg_params& P = sc.P;
+  for (int a = 0; a < 3; ++a) {
+    P.res[a] = sp.grid_resolution[a];
+    P.origin[a] = sp.grid_origin[a];
+    P.gravity[a] = sp.gravity[a];
+  }
   if (P.res[0] < 4 || P.res[1] < 4 || P.res[2] < 4)
     raise(TG_ERR_CONFIG, "grid resolution must be >= 4 per axis");
+  P.dx = sp.grid_edge / P.res[0];  // scene.cpp:41-42
   if (!(P.dx > 0.0)) raise(TG_ERR_CONFIG, "grid spacing must be > 0");
+  P.youngs_modulus = sp.youngs_modulus;
+  P.poisson_ratio = sp.poisson_ratio;
+  P.density = sp.density;
+  P.dt = sp.dt;
+  if (sp.fixed_bottom_layers < 0) raise(TG_ERR_CONFIG, "fixed_bottom_layers must be >= 0");
 
-  std::vector<V3> el;
-  el.reserve(n_el);
-  for (int i = 0; i < nx; ++i)
-    for (int j = 0; j < ny; ++j)
-      for (int k = 0; k < nz; ++k) el.push_back({origin[0] + i * h[0], origin[1] + j * h[1], origin[2] + k * h[2]});
+  // LatticeMeta::spacing (particle_set.hpp:23-26); make_elastomer_lattice
+  double h[3];
+  for (int a = 0; a < 3; ++a) h[a] = lat.dims[a] / (lat.counts[a] - 1);
+  std::vector<V3> el(static_cast<size_t>(n_el));
+  for (int64_t p = 0; p < n_el; ++p) {
+    if (lat.positions) {
+      el[p] = {lat.positions[3 * p], lat.positions[3 * p + 1], lat.positions[3 * p + 2]};
+    } else {
+      const int64_t i = p / (ny * nz), j = (p / nz) % ny, k = p % nz;
+      el[p] = {lat.origin[0] + i * h[0], lat.origin[1] + j * h[1], lat.origin[2] + k * h[2]};
+    }
+  }
   V3 lo, hi;
   bbox(el, lo, hi);
   check_margin(P, lo, hi, "elastomer");
   bbox(indenter, lo, hi);
   check_margin(P, lo, hi, "indenter");
 
-  const double el_volume = dims[0] * dims[1] * dims[2];
-  const double el_vol0 = el_volume / static_cast<double>(n_el);
-  const double el_mass = c.rho * el_vol0;
-  const double ext[3] = {hi.x - lo.x, hi.y - lo.y, hi.z - lo.z};
-  const double ind_bbox_vol = std::max(ext[0] * ext[1] * ext[2], 1e-30);
+  const double el_vol0 = lat.dims[0] * lat.dims[1] * lat.dims[2] / static_cast<double>(n_el);
+  const double el_mass = sp.density * el_vol0;
+  const double ind_bbox_vol = std::max((hi.x - lo.x) * (hi.y - lo.y) * (hi.z - lo.z), 1e-30);
   const double ind_vol0 = ind_bbox_vol / static_cast<double>(indenter.size());
-  const double ind_mass = c.rho * ind_vol0 * c.rigid_mass_scale;
+  const double ind_mass = sp.density * ind_vol0 * sp.indenter_mass_scale;
 
   const int64_t n = n_el + static_cast<int64_t>(indenter.size());
   sc.n_el = n_el;
   sc.x.resize(3 * n);
   sc.v.assign(3 * n, 0.0);
-  sc.mass.resize(n);
-  sc.vol0.resize(n);
-  sc.tag.resize(n);
+  sc.mass.assign(n, ind_mass);
+  sc.vol0.assign(n, ind_vol0);
+  sc.tag.assign(n, 2);  // Tag::Indenter
+  // lattice order (i, j, k), k fastest; the bottom layers k < n_fixed are
+  // ElastomerBottom (scene.cpp:54-60)
   for (int64_t p = 0; p < n_el; ++p) {
     sc.x[3 * p] = el[p].x;
     sc.x[3 * p + 1] = el[p].y;
     sc.x[3 * p + 2] = el[p].z;
     sc.mass[p] = el_mass;
     sc.vol0[p] = el_vol0;
-    sc.tag[p] = (p % nz) < c.fixed_bottom_layers ? 1 : 0;  // scene.cpp:58
+    sc.tag[p] = (p % nz) < sp.fixed_bottom_layers ? 1 : 0;
   }
   for (size_t q = 0; q < indenter.size(); ++q) {
     const int64_t p = n_el + static_cast<int64_t>(q);
     sc.x[3 * p] = indenter[q].x;
     sc.x[3 * p + 1] = indenter[q].y;
     sc.x[3 * p + 2] = indenter[q].z;
-    sc.mass[p] = ind_mass;
-    sc.vol0[p] = ind_vol0;
-    sc.tag[p] = 2;
+    for (int a = 0; a < 3; ++a) sc.v[3 * p + a] = v0[a];
   }
-  // SurfaceLattice (scene.cpp:71-84)
+  for (int a = 0; a < 3; ++a) sc.v0[a] = v0[a];
+  // SurfaceLattice (scene.cpp:71-84): the top layer k = nz - 1
   sc.surf.resize(nx * ny);
-  for (int i = 0; i < nx; ++i)
-    for (int j = 0; j < ny; ++j) sc.surf[i * ny + j] = static_cast<uint32_t>((i * ny + j) * nz + (nz - 1));
+  for (int64_t i = 0; i < nx; ++i)
+    for (int64_t j = 0; j < ny; ++j)
+      sc.surf[i * ny + j] = static_cast<uint32_t>((i * ny + j) * nz + (nz - 1));
   sc.S.nx = static_cast<int>(nx);
   sc.S.ny = static_cast<int>(ny);
-  sc.S.x0 = origin[0];
-  sc.S.y0 = origin[1];
+  sc.S.x0 = lat.origin[0];
+  sc.S.y0 = lat.origin[1];
   sc.S.sx = h[0];
   sc.S.sy = h[1];
-  sc.S.z0 = origin[2] + dims[2];
+  sc.S.z0 = lat.origin[2] + lat.dims[2];
   sc.S.particle = sc.surf.data();
   return sc;
 }
 
-int build_sim_from(int device, const Config& c, const std::vector<V3>& placed, tg_handle* out) {
-  Scene sc = build_scene(c, placed);
+// build_sim's SceneParams and elastomer_for(cfg) (scene_builder.cpp:13-31,
+// 63-78) around init_scene.
+Scene build_scene(const Config& c, const std::vector<V3>& indenter) {
+  tg_scene_params sp{};
+  const double edge = c.edge_mm * 1e-3;
+  tg_lattice lat{};
+  for (int a = 0; a < 3; ++a) {
+    sp.grid_resolution[a] = c.nodes[a];
+    sp.grid_origin[a] = 0.0;
+    lat.counts[a] = c.counts[a];
+    lat.dims[a] = c.size_mm[a] * 1e-3;
+    lat.origin[a] = 0.5 * edge - 0.5 * lat.dims[a];
+  }
+  sp.grid_edge = edge;
+  sp.youngs_modulus = c.E;
+  sp.poisson_ratio = c.nu;
+  sp.density = c.rho;
+  sp.dt = c.dt;
+  sp.fixed_bottom_layers = c.fixed_bottom_layers;
+  sp.gravity[0] = 0.0;
+  sp.gravity[1] = 0.0;
+  sp.gravity[2] = -c.gravity_mps2;
+  sp.indenter_mass_scale = c.rigid_mass_scale;
+  const double zero[3] = {0.0, 0.0, 0.0};  // build_sim passes no velocity
+  return init_scene_arrays(sp, lat, indenter, zero);
+}
+
+int create_from(int device, Scene& sc, tg_handle* out) {
   tg_particles tp{};
   tp.n = static_cast<int64_t>(sc.mass.size());
   tp.n_elastomer = sc.n_el;
@@ -694,7 +725,13 @@ int build_sim_from(int device, const Config& c, const std::vector<V3>& placed, t
   tp.mass = sc.mass.data();
   tp.volume0 = sc.vol0.data();
   tp.tag = sc.tag.data();
+  for (int a = 0; a < 3; ++a) tp.indenter_velocity[a] = sc.v0[a];
   return tg_create(device, &sc.P, &tp, &sc.S, out);
+}
+
+int build_sim_from(int device, const Config& c, const std::vector<V3>& placed, tg_handle* out) {
+  Scene sc = build_scene(c, placed);
+  return create_from(device, sc, out);
 }
 
 namespace {
@@ -807,6 +844,81 @@ int tg_build_sim(int device, const char* config_json, const char* object, double
     const Config c = parse_config(config_json);
     return build_sim_from(device, c, placed_indenter(c, object ? object : "", offset_x, offset_y),
                           out);
+  });
+}
+
+int tg_init_scene(int device, const tg_scene_params* params, const tg_lattice* elastomer,
+                  const double* indenter, int64_t n_indenter, const double indenter_velocity[3],
+                  tg_handle* out) {
+  return guarded([&] {
+    if (!params || !elastomer || !out || (n_indenter > 0 && !indenter))
+      raise(TG_ERR_INVALID_ARGUMENT, "tg_init_scene: null argument");
+    std::vector<V3> ind(static_cast<size_t>(std::max<int64_t>(n_indenter, 0)));
+    for (size_t q = 0; q < ind.size(); ++q) ind[q] = {indenter[3 * q], indenter[3 * q + 1], indenter[3 * q + 2]};
+    const double zero[3] = {0.0, 0.0, 0.0};
+    Scene sc = init_scene_arrays(*params, *elastomer, ind, indenter_velocity ? indenter_velocity : zero);
+    return create_from(device, sc, out);
+  });
+}
+
+int tg_build_sim_points(int device, const char* config_json, const double* indenter,
+                        int64_t n_indenter, tg_handle* out) {
+  return guarded([&] {
+    if (!out || (n_indenter > 0 && !indenter))
+      raise(TG_ERR_INVALID_ARGUMENT, "tg_build_sim_points: null argument");
+    const Config c = parse_config(config_json);
+    std::vector<V3> placed(static_cast<size_t>(std::max<int64_t>(n_indenter, 0)));
+    for (size_t q = 0; q < placed.size(); ++q)
+      placed[q] = {indenter[3 * q], indenter[3 * q + 1], indenter[3 * q + 2]};
+    return build_sim_from(device, c, placed, out);
+  });
+}
+
+// Many episodes of one object (config 4, the harness's positions): the
+// indenter cloud (rejection sampling + subsample, the expensive part) is
+// generated once and shared; each episode gets its own z-rotation and
+// lateral offset (place_for_press, scene_builder.cpp:48-61) and simulation.
+// Built on host threads; on failure every handle created so far is destroyed.
+int tg_build_episodes(int device, const char* config_json, const char* object, int n_episodes,
+                      const double* poses, tg_handle* out) {
+  return guarded([&] {
+    if (n_episodes < 0 || (n_episodes > 0 && (!poses || !out)))
+      raise(TG_ERR_INVALID_ARGUMENT, "tg_build_episodes: bad argument");
+    const Config base = parse_config(config_json);
+    const std::vector<V3> cloud = indenter_cloud_for(base, object ? object : "");
+    std::vector<int> rc(static_cast<size_t>(n_episodes), TG_OK);
+    std::vector<std::string> msg(static_cast<size_t>(n_episodes));
+    std::atomic<int> next{0};
+    auto worker = [&] {
+      for (int e; (e = next.fetch_add(1)) < n_episodes;) {
+        out[e] = nullptr;
+        try {
+          Config c = base;
+          c.z_rotation_rad = poses[3 * e + 2];
+          const std::vector<V3> placed = place_for_press(c, cloud, poses[3 * e], poses[3 * e + 1]);
+          rc[e] = build_sim_from(device, c, placed, &out[e]);
+          if (rc[e]) msg[e] = tg_last_error();
+        } catch (const HostError& err) {
+          rc[e] = err.code;
+          msg[e] = err.msg;
+        }
+      }
+    };
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nt = std::max(1, std::min<int>(n_episodes, static_cast<int>(std::min(8u, hw ? hw : 4u))));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    for (int e = 0; e < n_episodes; ++e)
+      if (rc[e]) {
+        for (int k = 0; k < n_episodes; ++k)
+          if (out[k]) {
+            tg_destroy(out[k]);
+            out[k] = nullptr;
+          }
+        raise(rc[e], msg[e]);
+      }
+    return TG_OK;
   });
 }
 

@@ -22,6 +22,20 @@ enum : int {
   kErrShapeMismatch = 8,
 };
 
+// Internal: a scatter would write outside the node arrays' allocation box;
+// the host grows the allocation and re-runs from that substep (engine.cu).
+constexpr int kErrRegrow = 250;
+constexpr unsigned long long kNoError = ~0ull;
+__host__ __device__ __forceinline__ unsigned long long err_key(int substep, int code) {
+  return (static_cast<unsigned long long>(substep) << 8) | static_cast<unsigned>(code & 0xff);
+}
+__host__ __device__ __forceinline__ int err_code_of(unsigned long long k) {
+  return k == kNoError ? 0 : static_cast<int>(k & 0xff);
+}
+__host__ __device__ __forceinline__ int err_substep_of(unsigned long long k) {
+  return static_cast<int>(k >> 8);
+}
+
 // Particle tags (geo/particle_set.hpp:12).
 enum : uint8_t { kElastomer = 0, kElastomerBottom = 1, kIndenter = 2 };
 

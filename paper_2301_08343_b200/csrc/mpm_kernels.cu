@@ -87,12 +87,13 @@ __device__ __forceinline__ unsigned long long trace_gtime() {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ void raise(Ctl* ctl, int code, int substep) {
-  if (atomicCAS(&ctl->err_code, 0, code) == 0) ctl->err_substep = substep;
+  atomicMin(&ctl->err, err_key(substep, code));
 }
 
 // True when an error latched for substep <= s (the work of substep s must not run).
 __device__ __forceinline__ bool stale(const Ctl* ctl, int s) {
-  return ctl->err_code != 0 && ctl->err_substep <= s;
+  return (*reinterpret_cast<volatile const unsigned long long*>(&ctl->err) >> 8) <=
+         static_cast<unsigned long long>(s);
 }
 
 // Block-uniform version (one read, broadcast through shared memory) for
@@ -184,7 +185,20 @@ __device__ __forceinline__ void st_keep1(double* p, double a) {
 }
 
 __device__ __forceinline__ size_t node_index(const Geometry& g, int i, int j, int k) {
-  return (static_cast<size_t>(i) * g.res[1] + j) * g.res[2] + k;
+  return (static_cast<size_t>(i - g.ga_lo[0]) * g.ga_dim[1] + (j - g.ga_lo[1])) * g.ga_dim[2] +
+         (k - g.ga_lo[2]);
+}
+
+// The node box [lo, hi) lies inside the node arrays' allocation box.
+__device__ __forceinline__ bool box_in_alloc(const Geometry& g, int l0, int l1, int l2, int h0,
+                                             int h1, int h2) {
+  return l0 >= g.ga_lo[0] && l1 >= g.ga_lo[1] && l2 >= g.ga_lo[2] &&
+         h0 <= g.ga_lo[0] + g.ga_dim[0] && h1 <= g.ga_lo[1] + g.ga_dim[1] &&
+         h2 <= g.ga_lo[2] + g.ga_dim[2];
+}
+// A particle's 27 stencil nodes [base, base + 3) are allocated.
+__device__ __forceinline__ bool stencil_in_alloc(const Geometry& g, const int* b) {
+  return box_in_alloc(g, b[0], b[1], b[2], b[0] + 3, b[1] + 3, b[2] + 3);
 }
 
 __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); }
@@ -560,15 +574,31 @@ __device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double
 // which an elastomer lattice coarser than the grid (0.2 mm vs 0.129 mm) never
 // does; the rare duplicates (detected through the owner table) and CTAs whose
 // footprint exceeds the tile fall back to direct REDs.
+// s_scatter: the substep whose P2G this is (a scatter that would leave the
+// node arrays' allocation latches kErrRegrow for it instead of writing).
 __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
-                                 const Geometry& g, NodeBuf grid, int cta, bool box_done) {
+                                 const Geometry& g, NodeBuf grid, int cta, bool box_done,
+                                 Ctl* ctl, int s_scatter) {
   const int tid = threadIdx.x;
   if (g.scatter_mode == 1 || g.scatter_mode == 3) {  // A/B switches without a tile
     if (tid == 0 && g.cta_box) g.cta_box[8 * cta + 6] = 0;  // next G2P: no staged box
-    if (g.scatter_mode == 1 && active) scatter_direct(g, grid, m, q);  // per-particle REDs
-    return;                                                            // (3: no scatter)
+    if (g.scatter_mode == 1 && active) {  // per-particle REDs (3: no scatter)
+      if (stencil_in_alloc(g, q.st.base)) scatter_direct(g, grid, m, q);
+      else raise(ctl, kErrRegrow, s_scatter);
+    }
+    return;
   }
   if (!box_done) tile_box(T, active, q.st.base);
+  // every node this CTA can touch, [min base, max base + 3), must be
+  // allocated (block-uniform: T is shared and complete after the barrier)
+  if (T.lo[0] != INT_MAX &&
+      !box_in_alloc(g, T.lo[0], T.lo[1], T.lo[2], T.hi[0] + 3, T.hi[1] + 3, T.hi[2] + 3)) {
+    if (tid == 0) {
+      raise(ctl, kErrRegrow, s_scatter);
+      if (g.cta_box) g.cta_box[8 * cta + 6] = 0;
+    }
+    return;
+  }
   if (tid == 0 && g.cta_box) {  // the next G2P of these particles stages this box
     int* b = g.cta_box + 8 * cta;
     for (int a = 0; a < 3; ++a) {
@@ -810,10 +840,7 @@ __device__ void finalize_warp(Ctl* ctl, const Geometry& g, int mode, FinFix& fx)
       ctl->step_count += 1;
       ctl->substep = s + 1;
     }
-    if (err && ctl->err_code == 0) {
-      ctl->err_code = kErrOutOfGrid;
-      ctl->err_substep = err == 1 ? s : ((mode & kFinAdvect) ? s + 1 : s);
-    }
+    if (err) raise(ctl, kErrOutOfGrid, err == 1 ? s : ((mode & kFinAdvect) ? s + 1 : s));
   }
   if (ax && shift) {
     ctl->ind_lo[cur][a] = order_key(il);
@@ -839,6 +866,11 @@ __device__ void finalize_warp(Ctl* ctl, const Geometry& g, int mode, FinFix& fx)
     }
     ctl->clr_lo[a] = prev_empty ? wlo : min(wlo, pl);
     ctl->clr_hi[a] = prev_empty ? whi : max(whi, ph);
+    // the reference's Grid::active window: after a step it is the window of
+    // the last substep's zero_grid (the one ending here), else the new one
+    const bool after_step = (mode & kFinAdvect) != 0;
+    ctl->ref_lo[a] = after_step ? ctl->win_lo[a] : wlo;
+    ctl->ref_hi[a] = after_step ? ctl->win_hi[a] : whi;
     ctl->win_lo[a] = ctl->prev_lo[a] = wlo;
     ctl->win_hi[a] = ctl->prev_hi[a] = whi;
   }
@@ -856,16 +888,23 @@ __device__ void finalize_warp(Ctl* ctl, const Geometry& g, int mode, FinFix& fx)
       fx.old_ok = old_ok;
       fx.need = new_any && !(old_ok && inside);
       fx.s = s;
+      if (fx.need) ctl->walk_fixups += 1;
     }
   }
 }
 
-// zero_grid's clear of Grid::mass / momentum over Ctl::clr (engine.cpp:72-83).
-__global__ void k_clear(NodeBuf grid, double* __restrict__ mi, Ctl* ctl, Geometry g) {
+// zero_grid's clear of Grid::mass / momentum / velocity over Ctl::clr
+// (engine.cpp:72-83).
+__global__ void k_clear(NodeBuf grid, double* __restrict__ mi, VelBuf vel, Ctl* ctl, Geometry g) {
   if (stale(ctl, ctl->substep)) return;
-  const int lx = ctl->clr_lo[0], ly = ctl->clr_lo[1], lz = ctl->clr_lo[2];
-  const int ny = ctl->clr_hi[1] - ly, nz = ctl->clr_hi[2] - lz;
-  const int64_t total = static_cast<int64_t>(ctl->clr_hi[0] - lx) * ny * nz;
+  // (the host grows the allocation over the window before the phase path
+  // runs; clamped so a stale box can never index outside it)
+  const int lx = max(ctl->clr_lo[0], g.ga_lo[0]), ly = max(ctl->clr_lo[1], g.ga_lo[1]),
+            lz = max(ctl->clr_lo[2], g.ga_lo[2]);
+  const int ny = max(min(ctl->clr_hi[1], g.ga_lo[1] + g.ga_dim[1]) - ly, 0);
+  const int nz = max(min(ctl->clr_hi[2], g.ga_lo[2] + g.ga_dim[2]) - lz, 0);
+  const int64_t total =
+      static_cast<int64_t>(max(min(ctl->clr_hi[0], g.ga_lo[0] + g.ga_dim[0]) - lx, 0)) * ny * nz;
   const double2 z = make_double2(0, 0);
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -877,6 +916,8 @@ __global__ void k_clear(NodeBuf grid, double* __restrict__ mi, Ctl* ctl, Geometr
     grid.lo[nd] = z;
     grid.hi[nd] = z;
     mi[nd] = 0.0;
+    vel.xy[nd] = z;
+    vel.z[nd] = 0.0;
   }
 }
 
@@ -911,7 +952,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_p2g_gel_tile(
     if (active && !stencil_in_grid(g, q.st)) active = false;  // zero_grid already raised
   }
   reduce_min_detf(ctl, s, active, J);
-  p2g_tile_scatter(T, active, q, m, g, grid, blockIdx.x, false);
+  p2g_tile_scatter(T, active, q, m, g, grid, blockIdx.x, false, ctl, s);
 }
 
 // Indenter scatter with a non-uniform velocity (only possible before the
@@ -927,6 +968,10 @@ __global__ void __launch_bounds__(256) k_p2g_ind_direct(const double* __restrict
   P2GPayload q;
   make_stencil(x[p], x[n + p], x[2 * n + p], g.origin, g.inv_dx, q.st);
   if (!stencil_in_grid(g, q.st)) return;
+  if (!stencil_in_alloc(g, q.st.base)) {
+    raise(ctl, kErrRegrow, ctl->substep);
+    return;
+  }
   q.mv[0] = m * v[p];
   q.mv[1] = m * v[n + p];
   q.mv[2] = m * v[2 * n + p];
@@ -1041,6 +1086,10 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
     Stencil st;
     make_stencil(px[j], py[j], pz[j], g.origin, g.inv_dx, st);
     if (!stencil_in_grid(g, st)) continue;  // finalize raises OutOfGrid
+    if (!stencil_in_alloc(g, st.base)) {    // the host grows the allocation
+      raise(ctl, kErrRegrow, kMove ? s + 1 : s);
+      continue;
+    }
     if (have && (st.base[0] != cb[0] || st.base[1] != cb[1] || st.base[2] != cb[2])) {
       // rare: the chunk crosses a base cell; flush the first part directly
 #pragma unroll
@@ -1096,7 +1145,7 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
     if (sum != 0.0) {
       const int64_t node = k0;  // node index of the base cell
       const int a = c / 9, b = (c / 3) % 3, cc = c % 3;
-      red_add(mi + node + (static_cast<int64_t>(a) * g.res[1] + b) * g.res[2] + cc, sum);
+      red_add(mi + node + (static_cast<int64_t>(a) * g.ga_dim[1] + b) * g.ga_dim[2] + cc, sum);
     }
   }
 }
@@ -1187,11 +1236,12 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
     const int64_t p = b0 + lane;
     const bool valid = p < a1;
     Stencil st;
-    bool beyond = false, contrib = false;
+    bool beyond = false, contrib = false, moved = false;
     if (valid) {
       double px = __ldcs(x + p), py = __ldcs(x + n + p), pz = __ldcs(x + 2 * n + p);
       const int done = moves[p - n_el];
-      if (done < target) {
+      moved = done < target;
+      if (moved) {
         for (int k = done; k < target; ++k) {
           px = add_rn(px, d[0]);
           py = add_rn(py, d[1]);
@@ -1205,7 +1255,13 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
       make_stencil(px, py, pz, g.origin, g.inv_dx, st);
       beyond = st.base[2] > ghi[2] - 1;  // this and every later particle of the column miss
       contrib = walk_contrib(g, st, glo, ghi);
+      if (contrib && !stencil_in_alloc(g, st.base)) {  // the host grows the allocation
+        raise(ctl, kErrRegrow, kMove ? s + 1 : s);
+        contrib = false;
+      }
     }
+    const unsigned mv = __ballot_sync(0xffffffffu, moved);
+    if (lane == 0 && mv) atomicAdd(&ctl->ind_walked, static_cast<unsigned long long>(__popc(mv)));
     const unsigned bey = __ballot_sync(0xffffffffu, beyond);
     const int first_beyond = bey ? __ffs(bey) - 1 : 32;
     if (lane > first_beyond) contrib = false;
@@ -1233,7 +1289,7 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
       double sum = 0.0;
       for (int t = t0; t < 32 && S.key[warp][t] == k0; ++t) sum += S.w[warp][comp][t];
       if (sum != 0.0)
-        red_add(mi + k0 + (static_cast<int64_t>(comp / 9) * g.res[1] + (comp / 3) % 3) * g.res[2] +
+        red_add(mi + k0 + (static_cast<int64_t>(comp / 9) * g.ga_dim[1] + (comp / 3) % 3) * g.ga_dim[2] +
                     comp % 3,
                 sum);
     }
@@ -1309,6 +1365,10 @@ __device__ void ind_walk_fixup(const FinFix& fx, const double* __restrict__ x, i
       make_stencil(px, py, pz, g.origin, g.inv_dx, st);
       if (!walk_contrib(g, st, fx.elo, fx.ehi)) continue;
       if (fx.old_ok && walk_contrib(g, st, fx.wlo, fx.whi)) continue;  // the walk had it
+      if (!stencil_in_alloc(g, st.base)) {
+        raise(const_cast<Ctl*>(ctl), kErrRegrow, fx.s + 1);
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 27; ++i) {
         const int ia = i / 9, ib = (i / 3) % 3, ic = i % 3;
@@ -1427,9 +1487,11 @@ __global__ void k_grid_update_window(NodeBuf mp, double* __restrict__ mi, VelBuf
                                      Ctl* ctl, Geometry g,
                                      double m_ind) {
   if (stale(ctl, ctl->substep)) return;
-  const int lx = ctl->win_lo[0], ly = ctl->win_lo[1], lz = ctl->win_lo[2];
-  const int ny = ctl->win_hi[1] - ly, nz = ctl->win_hi[2] - lz;
-  const int vol = (ctl->win_hi[0] - lx) * ny * nz;
+  const int lx = max(ctl->win_lo[0], g.ga_lo[0]), ly = max(ctl->win_lo[1], g.ga_lo[1]),
+            lz = max(ctl->win_lo[2], g.ga_lo[2]);
+  const int ny = max(min(ctl->win_hi[1], g.ga_lo[1] + g.ga_dim[1]) - ly, 0);
+  const int nz = max(min(ctl->win_hi[2], g.ga_lo[2] + g.ga_dim[2]) - lz, 0);
+  const int vol = max(min(ctl->win_hi[0], g.ga_lo[0] + g.ga_dim[0]) - lx, 0) * ny * nz;
   const double u0 = ctl->ind_v[0], u1 = ctl->ind_v[1], u2 = ctl->ind_v[2];
   for (BoxIter it(blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, ny, nz); it.e < vol;
        it.next(ny, nz))
@@ -1448,11 +1510,11 @@ __global__ void __launch_bounds__(256, 5) k_grid_update_boxes(NodeBuf mp, double
   if (g.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (stale(ctl, ctl->substep)) return;
   int lo[2][3], dm[2][3], vol[2];
-  for (int m = 0; m < 2; ++m) {
+  for (int m = 0; m < 2; ++m) {  // each box clamped to the allocation (no mass outside)
     vol[m] = 1;
     for (int a = 0; a < 3; ++a) {
-      lo[m][a] = ctl->box_lo[m][a];
-      dm[m][a] = max(ctl->box_hi[m][a] - lo[m][a], 0);
+      lo[m][a] = max(ctl->box_lo[m][a], g.ga_lo[a]);
+      dm[m][a] = max(min(ctl->box_hi[m][a], g.ga_lo[a] + g.ga_dim[a]) - lo[m][a], 0);
       vol[m] *= dm[m][a];
     }
   }
@@ -1481,11 +1543,16 @@ __global__ void __launch_bounds__(256, 5) k_grid_update_boxes(NodeBuf mp, double
 
 namespace {
 // engine.cpp:217-249 for one particle: v and C from the node velocities.
+// kGuard: nodes outside the allocation read as 0 (phase path, where positions
+// may have been uploaded after zero_grid); in the step path every stencil
+// lies in the box its own P2G scattered to, so no check is compiled in.
+template <bool kGuard>
 __device__ __forceinline__ void g2p_gather(const Geometry& g, VelBuf vel,
                                            double px0, double px1, double px2, double* vv,
                                            double* Cn) {
   Stencil st;
   make_stencil(px0, px1, px2, g.origin, g.inv_dx, st);
+  const bool inside = !kGuard || stencil_in_alloc(g, st.base);
   double v0 = 0, v1 = 0, vz = 0;
   double b00 = 0, b01 = 0, b02 = 0, b10 = 0, b11 = 0, b12 = 0, b20 = 0, b21 = 0, b22 = 0;
 #pragma unroll
@@ -1501,8 +1568,13 @@ __device__ __forceinline__ void g2p_gather(const Geometry& g, VelBuf vel,
       for (int c = 0; c < 3; ++c) {
         const double w = wab * st.w[2][c];
         const double dc = c - st.fx[2];
-        const double2 qa = __ldg(vel.xy + row + c);
-        const double2 qb = make_double2(__ldg(vel.z + row + c), 0.0);
+        // nodes outside the allocation hold no mass: velocity 0 (as the
+        // reference's cleared grid)
+        const bool in = inside || box_in_alloc(g, st.base[0] + a, st.base[1] + b, st.base[2] + c,
+                                               st.base[0] + a + 1, st.base[1] + b + 1,
+                                               st.base[2] + c + 1);
+        const double2 qa = in ? __ldg(vel.xy + row + c) : make_double2(0.0, 0.0);
+        const double2 qb = make_double2(in ? __ldg(vel.z + row + c) : 0.0, 0.0);
         const double wv0 = w * qa.x, wv1 = w * qa.y, wv2 = w * qb.x;
         v0 += wv0; v1 += wv1; vz += wv2;
         b00 += wv0 * da; b01 += wv0 * db; b02 += wv0 * dc;
@@ -1605,7 +1677,8 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
       T.lo[a] = b[a];
       T.dim[a] = b[3 + a];
     }
-    T.ok = b[6] && (g.res[2] & 1) == 0;  // vz row staging needs an even res2
+    // vz row staging needs even allocation rows (even start and length in z)
+    T.ok = b[6] && (g.ga_dim[2] & 1) == 0 && (g.ga_lo[2] & 1) == 0;
     T.pitch = tile_pitch(T.dim[2]);
   }
   pdl_wait();
@@ -1654,7 +1727,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
       vv[0] = vv[1] = vv[2] = 0.0;
       for (int i = 0; i < 9; ++i) Cn[i] = 0.0;
     } else if (staged) g2p_gather_smem(g, T, st_old, vv, Cn);
-    else g2p_gather(g, vel, px0, px1, px2, vv, Cn);
+    else g2p_gather<!kLookahead>(g, vel, px0, px1, px2, vv, Cn);
     TRACE_MARK(8);
     double G[9];
 #pragma unroll
@@ -1705,7 +1778,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     TRACE_MARK(4);
     // advect's motion reductions, min det F of s + 1 and the tile box together
     block_motion_box(T, ctl, s, active, v2, px0, px1, px2, go, J, q.st.base);
-    p2g_tile_scatter(T, go, q, m, g, grid, cta, true);
+    p2g_tile_scatter(T, go, q, m, g, grid, cta, true, ctl, s + 1);
   }
   TRACE_END();
 }
@@ -1793,6 +1866,18 @@ __global__ void k_gather_box(NodeBuf mp, const double* __restrict__ mi, VelBuf v
     const int64_t r = t / nz;
     const int j = lo.y + static_cast<int>(r % ny);
     const int i = lo.x + static_cast<int>(r / ny);
+    // Grid nodes outside the reference's active window are zero there
+    // (zero_grid cleared them when the window moved, engine.cpp:72-83)
+    const bool in_win = i >= ctl->ref_lo[0] && i < ctl->ref_hi[0] && j >= ctl->ref_lo[1] &&
+                        j < ctl->ref_hi[1] && k >= ctl->ref_lo[2] && k < ctl->ref_hi[2];
+    const bool alloc = i >= g.ga_lo[0] && i < g.ga_lo[0] + g.ga_dim[0] && j >= g.ga_lo[1] &&
+                       j < g.ga_lo[1] + g.ga_dim[1] && k >= g.ga_lo[2] &&
+                       k < g.ga_lo[2] + g.ga_dim[2];
+    if (!in_win || !alloc) {
+      mass[t] = 0.0;
+      for (int c = 0; c < 3; ++c) mom[3 * t + c] = velo[3 * t + c] = 0.0;
+      continue;
+    }
     const size_t nd = node_index(g, i, j, k);
     const double2 qa = mp.lo[nd], qb = mp.hi[nd];
     const double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
@@ -1943,7 +2028,8 @@ int launch_window(DeviceSim& s) {
 }
 
 int launch_clear(DeviceSim& s, int sms) {
-  k_clear<<<window_blocks(sms), kThreads, 0, s.stream>>>(s.grid_mp, s.grid_mi, s.ctl, s.geo);
+  k_clear<<<window_blocks(sms), kThreads, 0, s.stream>>>(s.grid_mp, s.grid_mi, s.grid_v, s.ctl,
+                                                        s.geo);
   s.kernel_launches += 1;
   s.grid_dirty = false;
   return 1;

@@ -304,6 +304,23 @@ def config3_full():
     np.savez_compressed(os.path.join(OUT, "config3_full.npz"), **out)
 
 
+def grid_post_step():
+    """The reference's Grid after mpm::step (SMALL scene, 20 substeps, then
+    7 more): active window, mass / momentum / velocity over the window plus
+    a 2-node margin (zero outside the window)."""
+    sim = R.RefSim.from_config(SMALL, "", threads=0)
+    out = {}
+    for tag, n in (("a", 20), ("b", 7)):
+        sim.step(SMALL_V, n)
+        gi = sim.grid_info()
+        lo, hi = gi["lo"] - 2, gi["hi"] + 2
+        m, mom, vel = sim.grid(lo, hi)
+        out.update({f"{tag}_win_lo": gi["lo"], f"{tag}_win_hi": gi["hi"], f"{tag}_lo": lo,
+                    f"{tag}_hi": hi, f"{tag}_mass": m, f"{tag}_mom": mom, f"{tag}_vel": vel,
+                    f"{tag}_x": sim.state()["x"]})
+    np.savez_compressed(os.path.join(OUT, "grid_post_step.npz"), **out)
+
+
 def acceptance3():
     """SPEC acceptance 3 scene: 60 particles on an 8^3 grid, one step of the
     reference's serial SVD oracle (tests/oracle/reference_mpm.cpp)."""
@@ -503,6 +520,8 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["kat", "small", "config1", "config3", "config5", "config2b", "acceptance3", "bridge", "harness", "parts", "background", "clouds"]
     if "config2b" in which:
         config2b()
+    if "grid_post_step" in which:
+        grid_post_step()
     if "config2a" in which:
         config2a()
     if "config4" in which:

@@ -349,6 +349,32 @@ def test_elastomer_moving_cells_per_substep_matches_oracle(tb, golden, oracle):
     assert np.abs(x - o.x).max() <= 1e-9 * moved
     np.testing.assert_allclose(s.state()["F"], o.F, rtol=0, atol=1e-11)
     assert s.step_count == 7
+    st = s.stats()
+    assert st["walk_fixups"] >= 1  # finalize completed the walks
+    assert st["regrows"] >= 1      # the node arrays followed the elastomer
+
+
+def test_windowed_node_arrays_match_dense(tb, monkeypatch):
+    """The node arrays cover the elastomer's box plus the walks' reach and
+    grow on demand; a dense res^3 allocation (TACCHI_DENSE_GRID=1) gives the
+    same trajectory (to summation order), and a default config-1 scene needs
+    a tenth of the dense 1.07 GB."""
+    from tests.scenes import CONFIG1
+
+    s = tb.sim.build_sim(CONFIG1)
+    st = s.stats()
+    assert st["grid_bytes"] < 160e6, st
+    monkeypatch.setenv("TACCHI_DENSE_GRID", "1")
+    d = tb.sim.build_sim(SMALL)
+    monkeypatch.delenv("TACCHI_DENSE_GRID")
+    w = tb.sim.build_sim(SMALL)
+    assert d.stats()["grid_nodes"] == 64 ** 3 > w.stats()["grid_nodes"]
+    for sim in (d, w):
+        tb.mpm.step(sim, SMALL_V, 100)
+        tb.mpm.step(sim, (0.02, -0.01, -0.05), 100)
+    x0 = tb.sim.build_sim(SMALL).positions()
+    disp = np.abs(d.positions() - x0).max()
+    assert np.abs(d.positions() - w.positions()).max() <= 1e-11 * disp
 
 
 def test_capture_with_background_image_matches_reference(tb, golden, tmp_path):
@@ -646,3 +672,181 @@ def test_polar_rotation_and_svd_fallback_match_reference(tb, golden):
                                rtol=0, atol=1e-13)
     assert np.all(np.linalg.det(Rs) > 0)
     np.testing.assert_allclose(Ss, S, rtol=0, atol=1e-8 * smax)
+
+
+def test_init_scene_from_reference_inputs(tb, golden):
+    """mpm::init_scene from its own inputs (SceneParams, the elastomer
+    lattice, the placed indenter points and v0; scene.cpp:28-87) computes the
+    reference's masses, rest volumes, tags and initial velocities bit for bit
+    (parts.npz was made by the reference's init_scene from the same inputs),
+    and the scene then steps as the reference's."""
+    from tests.scenes import PARTS, PARTS_STEPS, PARTS_V
+
+    g = golden("parts.npz")
+    P = PARTS
+    params = dict(grid_resolution=P["res"], grid_edge=P["grid_edge"], dt=P["dt"],
+                  gravity=P["gravity"])
+    lattice = dict(counts=P["lat_counts"], dims=P["lat_dims"], origin=P["lat_origin"])
+    s = tb.mpm.init_scene(params, lattice, g["ind"], P["ind_v0"])
+    st = s.state()
+    k = s.constants()
+    np.testing.assert_array_equal(st["x"], g["x0"])
+    np.testing.assert_array_equal(k["mass"], g["mass"])
+    np.testing.assert_array_equal(k["volume0"], g["vol0"])
+    np.testing.assert_array_equal(k["tag"], g["tag"])
+    ne = int(g["n_elastomer"])
+    assert s.elastomer_count == ne
+    assert not st["v"][:ne].any()
+    np.testing.assert_array_equal(st["v"][ne:], np.tile(P["ind_v0"], (s.n - ne, 1)))
+    s.set_state(v=g["v0"])  # the golden's non-uniform indenter velocity
+    tb.mpm.step(s, PARTS_V, PARTS_STEPS)
+    disp = np.abs(g["x"] - g["x0"]).max()
+    assert np.abs(s.positions() - g["x"]).max() <= 1e-8 * disp
+    # explicit lattice positions give the same scene
+    pos = g["x0"][:ne]
+    s2 = tb.mpm.init_scene(params, dict(lattice, positions=pos), g["ind"], P["ind_v0"])
+    np.testing.assert_array_equal(s2.state()["x"], g["x0"])
+    with pytest.raises(tb.EmptyScene):
+        tb.mpm.init_scene(params, lattice, np.zeros((0, 3)))
+    with pytest.raises(tb.GridTooSmall):
+        tb.mpm.init_scene(params, lattice, g["ind"] + np.array([0.0, 0.0, 0.1]))
+
+
+def test_build_sim_from_caller_points(tb, golden):
+    """sim::build_sim(cfg, indenter) with the caller's placed points equals
+    the config path that places the indenter itself."""
+    g = golden("small_scene.npz")
+    placed = tb.geo.placed_indenter(SMALL, "")
+    s = tb.sim.build_sim_points(SMALL, placed)
+    np.testing.assert_array_equal(s.state()["x"], g["x0"])
+    tb.mpm.step(s, SMALL_V, SMALL_STEPS)
+    disp = np.abs(g["x"] - g["x0"]).max()
+    assert np.abs(s.positions() - g["x"]).max() <= 1e-9 * disp
+
+
+def test_post_step_grid_matches_reference(tb, golden):
+    """After mpm::step the grid holds the last substep's P2G and grid_update
+    (engine.cpp:180-205) and zeros outside the active window: with keep_grid
+    the last substep runs the phase path, and tg_download_grid returns that
+    grid; after a fused step (the default) the grid is not retained and the
+    call says so."""
+    g = golden("grid_post_step.npz")
+    s = tb.sim.build_sim(SMALL)
+    s.set_keep_grid(True)
+    for tag, n in (("a", 20), ("b", 7)):
+        tb.mpm.step(s, SMALL_V, n)
+        lo, hi = s.grid_window()
+        np.testing.assert_array_equal(lo, g[f"{tag}_win_lo"])
+        np.testing.assert_array_equal(hi, g[f"{tag}_win_hi"])
+        m, mom, vel = s.grid(g[f"{tag}_lo"], g[f"{tag}_hi"])
+        gm = g[f"{tag}_mass"]
+        assert (m == 0).sum() == (gm == 0).sum()  # the same massless nodes
+        np.testing.assert_allclose(m, gm, rtol=0, atol=1e-12 * gm.max())
+        pmax = np.abs(g[f"{tag}_mom"]).max()
+        np.testing.assert_allclose(mom, g[f"{tag}_mom"], rtol=0, atol=1e-9 * pmax)
+        vmax = np.abs(g[f"{tag}_vel"]).max()
+        np.testing.assert_allclose(vel, g[f"{tag}_vel"], rtol=0, atol=1e-9 * vmax)
+        disp = np.abs(g[f"{tag}_x"] - s.state()["x"]).max()
+        assert disp <= 1e-15
+    s.set_keep_grid(False)
+    tb.mpm.step(s, SMALL_V, 3)
+    with pytest.raises(tb.InvalidArgument):
+        s.grid(g["a_lo"], g["a_hi"])
+
+
+def _check_checkpoint(tb, s, g, prefix, cfg, obj="", tol=1e-8, label=""):
+    """Positions (subset and top surface) within tol x the displacement, F,
+    diagnostics, height map <= 1e-7 m and image <= 2/255 vs a reference
+    checkpoint of make_golden._checkpoint."""
+    st = s.state()
+    sub = g[f"{prefix}subset"]
+    disp = np.abs(g[f"{prefix}x_subset"] - g[f"{prefix}x0_subset"]).max()
+    err = np.abs(st["x"][sub] - g[f"{prefix}x_subset"]).max()
+    surf = _default_surface()
+    serr = np.abs(st["x"][surf] - g[f"{prefix}x_surface"]).max()
+    print(f"{label} {prefix}: x err {err:.3e} m, surface {serr:.3e} m, displacement {disp:.3e} m")
+    assert disp > 0
+    assert err <= tol * disp, (err, disp)
+    assert serr <= tol * disp, (serr, disp)
+    assert err / np.abs(g[f"{prefix}x_subset"]).max() <= 1e-4  # north_star bar
+    np.testing.assert_allclose(st["F"].reshape(-1, 9)[sub], g[f"{prefix}F_subset"], rtol=0, atol=1e-9)
+    d = s.diag
+    assert d.step_count == int(g[f"{prefix}step_count"])
+    assert d.min_det_f == pytest.approx(float(g[f"{prefix}min_det_f"]), abs=1e-9)
+    depth, img = tb.sim.capture(s, cfg, obj)
+    assert np.abs(depth[::8, ::8] - g[f"{prefix}depth_sample"]).max() <= 1e-7
+    assert depth.max() == pytest.approx(float(g[f"{prefix}depth_max"]), abs=1e-9)
+    assert np.abs(img.astype(int) - g[f"{prefix}image"]).max() <= 2
+
+
+def test_config2a_bench_workload_matches_reference(tb, golden):
+    """Config 2a, the bench workload (1,214,221 particles: the sphere at 1e6
+    points), stepped exactly as bench.py steps it (tg_step_capture, 10
+    substeps + capture per frame) for 100 frames and on to 600 (past the
+    0.1 mm gap) vs the reference at both checkpoints."""
+    from tests.scenes import CONFIG2A, CONFIG2A_FRAMES, CONFIG2A_V
+
+    g = golden("config2a.npz")
+    s = tb.sim.build_sim(CONFIG2A)
+    assert s.n == int(g["n"]) and s.elastomer_count == int(g["n_elastomer"])
+    assert sha(s.positions()) == str(g["x0_hash"])
+    rp = tb.render_params(CONFIG2A, "")
+    done = 0
+    for f in CONFIG2A_FRAMES:
+        for _ in range(f - done):
+            tb.sim.step_capture(s, CONFIG2A_V, 10, params=rp, want_depth=False, want_image=False)
+        done = f
+        _check_checkpoint(tb, s, g, f"f{f}_", CONFIG2A, label="config2a")
+
+
+def test_config4_episodes_match_reference(tb, golden):
+    """Config 4: the first episodes of the 1024-episode batch (mt19937_64
+    draws: lateral offset over +-1 mm and z-rotation of the indenter),
+    stepped together with tg_step_capture_many for 200 frames, each vs the
+    reference's episode."""
+    from paper_2301_08343_b200 import episodes as E
+    from tests.scenes import CONFIG1, CONFIG1_V, CONFIG4_EPISODES, CONFIG4_FRAMES
+
+    g = golden("config4.npz")
+    eps = [E.make_episode(e) for e in range(CONFIG4_EPISODES)]
+    sims, cfgs = [], []
+    for e, ep in enumerate(eps):
+        np.testing.assert_array_equal(
+            g[f"e{e}_pose"], [ep.offset_x_m, ep.offset_y_m, ep.z_rotation_rad, ep.depth_m])
+        cfg = E.episode_config(CONFIG1, ep)
+        s = tb.sim.build_sim(cfg, "", ep.offset_x_m, ep.offset_y_m)
+        assert sha(s.positions()) == str(g[f"e{e}_x0_hash"])
+        sims.append(s)
+        cfgs.append(cfg)
+    # the batched builder (one shared cloud) gives the same episodes
+    poses = [[ep.offset_x_m, ep.offset_y_m, ep.z_rotation_rad] for ep in eps[:2]]
+    for e, b in enumerate(tb.sim.build_episodes(CONFIG1, "", poses)):
+        assert sha(b.positions()) == str(g[f"e{e}_x0_hash"])
+    rps = [tb.render_params(c, "") for c in cfgs]
+    vel = np.tile(CONFIG1_V, (len(sims), 1))
+    for _ in range(CONFIG4_FRAMES):
+        outs, status = tb.sim.step_capture_many(sims, vel, 10, rps, want_depth=False)
+        assert status == [0] * len(sims)
+    for e, (s, cfg) in enumerate(zip(sims, cfgs)):
+        _check_checkpoint(tb, s, g, f"e{e}_", cfg, label=f"config4 episode {e}")
+        assert np.abs(outs[e][1].astype(int) - g[f"e{e}_image"]).max() <= 2
+
+
+def test_config3_full_size_dots_press_and_slide(tb, golden):
+    """Config 3 at full size: the dot-grid indenter (3 x 3 studs, 1e5 points)
+    on the default gel and 256^3 grid, pressed until the commanded travel is
+    gap + 0.3 mm (20,000 substeps), then slid +x at 5 mm/s for 200 frames,
+    vs the reference after the press and after the slide."""
+    from tests.scenes import CONFIG1, CONFIG3_FULL_PRESS, CONFIG3_FULL_SHAPE, CONFIG3_FULL_SLIDE
+
+    g = golden("config3_full.npz")
+    shape = CONFIG3_FULL_SHAPE
+    s = tb.sim.build_sim(CONFIG1, shape)
+    assert sha(s.positions()) == str(g["x0_hash"])
+    tb.mpm.step(s, CONFIG3_FULL_PRESS[1], CONFIG3_FULL_PRESS[0])
+    _check_checkpoint(tb, s, g, "press_", CONFIG1, shape, label="config3 dots")
+    rp = tb.render_params(CONFIG1, shape)
+    for _ in range(CONFIG3_FULL_SLIDE[0] // 10):
+        tb.sim.step_capture(s, CONFIG3_FULL_SLIDE[1], 10, params=rp, want_depth=False,
+                            want_image=False)
+    _check_checkpoint(tb, s, g, "slide_", CONFIG1, shape, label="config3 dots")

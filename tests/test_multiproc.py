@@ -80,3 +80,24 @@ def test_waves_split_a_rank_share():
     eps = E.shard(1024, 3, 8)
     w = E.waves(eps, 50)
     assert [len(x) for x in w] == [50, 50, 28] and sum(w, []) == eps
+
+
+def test_bench_spawns_ranks_itself():
+    """`bench.py --gpus 2` outside torchrun relaunches itself as two ranks
+    (torch.distributed.run on 127.0.0.1); --dry-run runs the multi-rank
+    plumbing on CPU (gloo): config-4 episodes sharded e mod 2 and the
+    max-over-ranks device time."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--dry-run", "--workload", "config4", "--episodes", "1024"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["episodes_per_rank"] == [512, 512]
+    assert line["max_ms"] == 11.0  # rank 1's synthetic time wins

@@ -1,0 +1,63 @@
+"""A/B of environment switches on the config-2a frame: each variant runs in
+its own process (the switches are read at tg_create), interleaved `--rounds`
+times; prints frames/s and the per-kernel device times (tg_time_phases).
+
+    python tools/ab_env.py --variant base: --variant dense:TACCHI_DENSE_GRID=1
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys, time
+sys.path.insert(0, %r)
+import torch
+import paper_2301_08343_b200 as tb
+from tests.scenes import CONFIG2A, CONFIG2A_V
+cfg = CONFIG2A
+s = tb.sim.build_sim(cfg)
+rp = tb.render_params(cfg, "")
+for _ in range(5):
+    tb.sim.step_capture(s, CONFIG2A_V, 10, params=rp, want_depth=False, want_image=False)
+frames = %d
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+st = torch.cuda.ExternalStream(s.stream)
+e0.record(st)
+for _ in range(frames):
+    tb.sim.step_capture(s, CONFIG2A_V, 10, params=rp, want_depth=False, want_image=False)
+e1.record(st)
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1)
+ph = s.time_phases(CONFIG2A_V, reps=20)
+print(json.dumps({"fps": frames / ms * 1e3, "phases_us": {k: round(v * 1e3, 2) for k, v in ph.items()},
+                  "stats": s.stats()}))
+"""
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--variant", action="append", required=True, help="name:K=V,K=V")
+    ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--frames", type=int, default=100)
+    args = ap.parse_args()
+    variants = []
+    for v in args.variant:
+        name, _, kv = v.partition(":")
+        env = dict(p.split("=", 1) for p in kv.split(",") if p)
+        variants.append((name, env))
+    for r in range(args.rounds):
+        for name, env in variants:
+            e = dict(os.environ)
+            e.update(env)
+            out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, args.frames)], env=e,
+                                 capture_output=True, text=True)
+            line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-500:]
+            print(json.dumps({"round": r, "variant": name, "result": line}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -15,12 +15,13 @@ int main(int argc, char** argv) {
   const int steps = argc > 2 ? std::atoi(argv[2]) : 10;
   try {
     auto state = tacchi_b200::sim::build_sim(cfg, "");
+    const auto render = tacchi_b200::sim::RenderSetup::from_config(cfg, "");
     const tacchi_b200::Vec3 v = {0.0, 0.0, -0.01};
     double max_depth = 0.0;
     const auto t0 = std::chrono::steady_clock::now();
     for (int k = 0; k < steps; ++k) {
       tacchi_b200::mpm::step(state, v, 10);
-      const auto cap = tacchi_b200::sim::capture(state, cfg, "");
+      const auto cap = tacchi_b200::sim::capture(state, render);
       for (double d : cap.depth.values) max_depth = d > max_depth ? d : max_depth;
     }
     const double ms =
