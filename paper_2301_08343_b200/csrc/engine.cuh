@@ -127,7 +127,7 @@ struct DeviceSim {
   bool keep_grid = false;    // tg_set_keep_grid: the last substep of a step runs the phase
                              // path so the grid afterwards is the reference's (engine.cpp:288-297)
   int regrows = 0;            // node-array reallocations so far
-  int zpad = 16;              // allocation z-row length multiple (TACCHI_ZPAD)
+  int zpad = 2;               // allocation z-row length multiple (TACCHI_ZPAD)
   int resume_substeps = 0;    // after kResume: substeps of the call still to run
   bool grid_ref = true;      // the node arrays hold the reference's Grid state (not a
                              // fused look-ahead): tg_download_grid may read them
