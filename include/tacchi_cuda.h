@@ -218,6 +218,13 @@ int tg_grid_window(tg_handle h, int lo[3], int hi[3]);
  * substep's look-ahead scatter. */
 int tg_download_grid(tg_handle h, const int lo[3], const int hi[3], double* mass, double* momentum,
                      double* velocity);
+/* Deterministic mode (SceneConfig::deterministic, scene_config.hpp:78; SPEC
+ * "Concurrency Model", acceptance 10): with enabled != 0 the node sums that
+ * several CTAs / warps add to are accumulated as 64-bit fixed point, so
+ * reruns with identical inputs give bit-identical states. tg_build_sim /
+ * tg_build_sim_points / tg_build_episodes honour the config flag (default
+ * true); tg_create / tg_init_scene start in the fp64 fast mode. */
+int tg_set_deterministic(tg_handle h, int enabled);
 /* With enabled != 0 the last substep of every tg_step / tg_step_capture runs
  * the six phases (engine.cpp:288-297) instead of the fused plan, so the grid
  * afterwards is the reference's post-step grid (engine.cpp:180-205). Default

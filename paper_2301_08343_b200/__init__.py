@@ -118,7 +118,7 @@ EXPORTED = [
     "tg_stream", "tg_kernel_launches", "tg_set_graphs", "tg_last_error", "tg_version",
     "tg_generate_cloud", "tg_placed_indenter", "tg_time_phases", "tg_polar", "tg_init_scene",
     "tg_build_sim_points", "tg_download_constants", "tg_set_keep_grid", "tg_stats",
-    "tg_build_episodes",
+    "tg_build_episodes", "tg_set_deterministic",
 ]
 
 PHASE_TIMING_NAMES = ["p2g_elastomer_first", "p2g_indenter_first", "grid_update",
@@ -184,6 +184,7 @@ def lib():
         L.tg_download_constants.argtypes = [C.c_void_p, _dp, _dp, _u8p]
         L.tg_set_keep_grid.argtypes = [C.c_void_p, C.c_int]
         L.tg_stats.argtypes = [C.c_void_p, _i64p]
+        L.tg_set_deterministic.argtypes = [C.c_void_p, C.c_int]
         L.tg_build_episodes.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_int, _dp,
                                         C.POINTER(C.c_void_p)]
         L.tg_polar.argtypes = [C.c_int, _dp, C.c_int64, C.c_int, C.c_double, C.c_double, _dp, _dp]
@@ -288,6 +289,11 @@ class SimState:
         keys = ["kernel_launches", "regrows", "grid_bytes", "walk_fixups", "grid_nodes",
                 "graphs", "indenter_walked"]
         return dict(zip(keys, (int(v) for v in out)))
+
+    def set_deterministic(self, enabled: bool = True):
+        """Fixed-point node accumulation, bit-identical reruns
+        (tg_set_deterministic; build_sim follows SceneConfig.deterministic)."""
+        _check(lib().tg_set_deterministic(self._h, int(bool(enabled))))
 
     def set_keep_grid(self, enabled: bool = True):
         """Keep the reference's post-step grid (tg_set_keep_grid): the last

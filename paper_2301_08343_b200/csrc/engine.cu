@@ -313,6 +313,19 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   if (const char* e = std::getenv("TACCHI_PDL_EARLY")) g.pdl_early = std::atoi(e);
   if (const char* e = std::getenv("TACCHI_IND_FIRST")) g.ind_first = std::atoi(e);
   s->sms = sm_count(device);
+  // Deterministic-mode fixed-point scales (powers of two): A resolves 2^-50
+  // of one elastomer particle's mass (momentum: of its mass x 1 m/s), range
+  // 2^12 of them per node; M_I (sums of B-spline weights <= 1) resolves 2^-52.
+  {
+    const double m_ref = s->m_el > 0 ? s->m_el : (s->m_ind > 0 ? s->m_ind : 1.0);
+    int ex = 0;
+    std::frexp(m_ref, &ex);  // m_ref in [2^(ex-1), 2^ex)
+    g.fx_s = std::ldexp(1.0, 50 - ex);
+    g.fx_inv = std::ldexp(1.0, ex - 50);
+    g.fxi_s = std::ldexp(1.0, 52);
+    g.fxi_inv = std::ldexp(1.0, -52);
+    g.det = 0;
+  }
 
   // Indenter particles are re-ordered by base cell so that P2G scatters from
   // neighbouring lanes hit neighbouring nodes; perm maps back.
@@ -645,6 +658,8 @@ int step(DeviceSim& s, const double vind[3], int n_substeps) {
 }
 
 int check_device_public(int device) { return check_device(device); }
+void flush_indenter_public(DeviceSim& s) { flush_indenter(s); }
+void drop_graphs_public(DeviceSim& s) { drop_graphs(s); }
 
 // Per-kernel device times of the substep plan (CUDA events between the
 // launches, no graph), averaged over `reps` substeps: one mpm::step call of
@@ -1200,6 +1215,28 @@ int tg_stats(tg_handle h, int64_t out[7]) {
   out[4] = static_cast<int64_t>(s.n_nodes);
   out[5] = static_cast<int64_t>(s.graphs.size());
   out[6] = static_cast<int64_t>(s.h_ctl->ind_walked);
+  return TG_OK;
+}
+
+int tg_set_deterministic(tg_handle h, int enabled) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_set_deterministic: null handle");
+  DeviceSim& s = *H(h);
+  const int want = enabled != 0;
+  if (s.geo.det == want) return TG_OK;
+  cudaSetDevice(s.device);
+  // the accumulators change format: drop any pending scatter and the graphs
+  // (Geometry is captured by value)
+  tacchi_b200::flush_indenter_public(s);
+  if (cudaStreamSynchronize(s.stream) != cudaSuccess ||
+      cudaMemsetAsync(s.grid_slab, 0, s.grid_slab_bytes, s.stream) != cudaSuccess ||
+      cudaStreamSynchronize(s.stream) != cudaSuccess)
+    return fail(TG_ERR_CUDA, "tg_set_deterministic: device error");
+  tacchi_b200::drop_graphs_public(s);
+  s.geo.det = want;
+  s.grid_ready = false;
+  s.grid_dirty = false;
+  s.grid_ref = false;
+  s.window_valid = false;
   return TG_OK;
 }
 

@@ -67,6 +67,13 @@ struct Geometry {
                         // own griddepcontrol.wait (TACCHI_PDL_EARLY, default 1)
   int ind_first;        // the indenter blocks of the elastomer kernel come first
                         // (TACCHI_IND_FIRST, default 1)
+  // Deterministic mode (SceneConfig::deterministic, SPEC "Concurrency
+  // Model"): node sums that several CTAs / warps add to are accumulated as
+  // 64-bit fixed point (integer adds are exact, so the order does not
+  // matter). A (mass, momentum) in units of 1 / fx_s, M_I in 1 / fxi_s;
+  // both scales are powers of two.
+  int det;
+  double fx_s, fx_inv, fxi_s, fxi_inv;
 };
 
 // A dense node array in split layout: two 16-byte halves per node in two

@@ -731,7 +731,18 @@ int create_from(int device, Scene& sc, tg_handle* out) {
 
 int build_sim_from(int device, const Config& c, const std::vector<V3>& placed, tg_handle* out) {
   Scene sc = build_scene(c, placed);
-  return create_from(device, sc, out);
+  int rc = create_from(device, sc, out);
+  // SceneConfig::deterministic (scene_config.hpp:78, default true): the
+  // reference is bit-reproducible by construction; here it selects the
+  // fixed-point node accumulation (SPEC "Concurrency Model")
+  if (!rc && c.deterministic) {
+    rc = tg_set_deterministic(*out, 1);
+    if (rc) {
+      tg_destroy(*out);
+      *out = nullptr;
+    }
+  }
+  return rc;
 }
 
 namespace {

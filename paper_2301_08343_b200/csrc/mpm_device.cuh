@@ -25,6 +25,8 @@ enum : int {
 // Internal: a scatter would write outside the node arrays' allocation box;
 // the host grows the allocation and re-runs from that substep (engine.cu).
 constexpr int kErrRegrow = 250;
+// Internal: a deterministic-mode node sum left the fixed-point range.
+constexpr int kErrFixedRange = 249;
 constexpr unsigned long long kNoError = ~0ull;
 __host__ __device__ __forceinline__ unsigned long long err_key(int substep, int code) {
   return (static_cast<unsigned long long>(substep) << 8) | static_cast<unsigned>(code & 0xff);

@@ -203,6 +203,57 @@ __device__ __forceinline__ bool stencil_in_alloc(const Geometry& g, const int* b
 
 __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); }
 
+// Deterministic mode: v as 64-bit fixed point (v * scale rounded to nearest);
+// |v * scale| must stay below 2^62 (the sums of a node then cannot wrap).
+__device__ __forceinline__ long long to_fixed(double v, double scale, Ctl* ctl) {
+  const double t = v * scale;
+  if (!(fabs(t) < 4.611686018427388e18)) {
+    if (ctl) atomicMin(&ctl->err, err_key(ctl->substep, kErrFixedRange));
+    return 0;
+  }
+  return __double2ll_rn(t);
+}
+// llrint(v * scale) without F2I: two round-to-integer additions of
+// 1.5 * 2^52 (exact for |v * scale| < 2^62; `bad` is set outside that range),
+// returned as the int64's bit pattern in a double register.
+__device__ __forceinline__ double fixed_bits(double v, double scale, bool& bad) {
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  constexpr long long kMagicBits = 0x4338000000000000LL;
+  const double y = v * scale;  // exact (power-of-two scale)
+  bad |= !(fabs(y) < 4.611686018427388e18);
+  const double h = __dadd_rn(__fma_rn(y, 0x1p-32, kMagic), -kMagic);  // round(y / 2^32)
+  const double r = __fma_rn(-h, 0x1p32, y);                           // y - h 2^32, exact
+  const long long hi = __double_as_longlong(__dadd_rn(h, kMagic)) - kMagicBits;
+  const long long lo = __double_as_longlong(__dadd_rn(r, kMagic)) - kMagicBits;  // round(r)
+  return __longlong_as_double((hi << 32) + lo);
+}
+
+__device__ __forceinline__ double from_fixed(double bits, double inv) {
+  return static_cast<double>(__double_as_longlong(bits)) * inv;
+}
+// One scalar added to a node accumulator: RED.F64, or in deterministic mode
+// the exact integer RED.64 of its fixed-point value.
+__device__ __forceinline__ void acc_add(double* p, double v, bool det, double scale, Ctl* ctl) {
+  if (det)
+    atomicAdd(reinterpret_cast<unsigned long long*>(p),
+              static_cast<unsigned long long>(to_fixed(v, scale, ctl)));
+  else
+    atomicAdd(p, v);
+}
+// Accumulation mode of a code path: kDet < 0 reads Geometry::det at run
+// time; 0 / 1 fix it at compile time (the elastomer kernel is instantiated
+// per mode so the fast path carries no fixed-point code).
+template <int kDet>
+__device__ __forceinline__ bool det_on(const Geometry& g) {
+  return kDet < 0 ? g.det != 0 : kDet != 0;
+}
+
+// M_I (indenter weight sums).
+template <int kDet = -1>
+__device__ __forceinline__ void mi_add(const Geometry& g, double* p, double v, Ctl* ctl) {
+  acc_add(p, v, det_on<kDet>(g), g.fxi_s, ctl);
+}
+
 __device__ __forceinline__ bool stencil_in_grid(const Geometry& g, const Stencil& st) {
   return st.base[0] >= 0 && st.base[1] >= 0 && st.base[2] >= 0 && st.base[0] + 2 < g.res[0] &&
          st.base[1] + 2 < g.res[1] && st.base[2] + 2 < g.res[2];
@@ -310,6 +361,7 @@ __host__ __device__ __forceinline__ int tile_zpitch(int zcnt) { return ((zcnt + 
 // (UBLKRED.ADD.F64, element-wise atomic in L2) per z-row and half, issued by
 // the first 2*dim0*dim1 threads. Call after a __syncthreads that follows the
 // last tile write (and a fence_proxy_async by every writer).
+template <int kDet>
 __device__ __forceinline__ void tile_bulk_reduce(const P2GTile& T, const Geometry& g,
                                                  NodeBuf grid) {
   const int rows = T.dim[0] * T.dim[1];
@@ -320,10 +372,16 @@ __device__ __forceinline__ void tile_bulk_reduce(const P2GTile& T, const Geometr
     const int i = r / T.dim[1], j = r - i * T.dim[1];
     double2* dst = (half ? grid.hi : grid.lo) + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
     const double2* src = (half ? T.nhi : T.nlo) + r * T.pitch;
-    asm volatile(
-        "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
-        "r"(smem_addr(src)), "r"(static_cast<unsigned>(d2 * sizeof(double2)))
-        : "memory");
+    if (det_on<kDet>(g))  // fixed-point node sums: exact integer adds
+      asm volatile(
+          "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(dst),
+          "r"(smem_addr(src)), "r"(static_cast<unsigned>(d2 * sizeof(double2)))
+          : "memory");
+    else
+      asm volatile(
+          "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+          "r"(smem_addr(src)), "r"(static_cast<unsigned>(d2 * sizeof(double2)))
+          : "memory");
     issued = true;
   }
   if (issued) {
@@ -394,8 +452,11 @@ struct P2GPayload {
   double aff[9];
 };
 
+template <int kDet>
 __device__ __forceinline__ void scatter_direct(const Geometry& g, NodeBuf grid, double m,
-                                               const P2GPayload& q) {
+                                               const P2GPayload& q, Ctl* ctl) {
+  const bool det = det_on<kDet>(g);
+  const double fs = g.fx_s;
   const double dx = g.dx;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -415,10 +476,10 @@ __device__ __forceinline__ void scatter_direct(const Geometry& g, NodeBuf grid, 
         const double dxc = (c - q.st.fx[2]) * dx;
         double* lo = reinterpret_cast<double*>(grid.lo + row + c);
         double* hi = reinterpret_cast<double*>(grid.hi + row + c);
-        red_add(lo + 0, w * m);
-        red_add(lo + 1, w * (m0 + q.aff[2] * dxc));
-        red_add(hi + 0, w * (m1 + q.aff[5] * dxc));
-        red_add(hi + 1, w * (m2 + q.aff[8] * dxc));
+        acc_add(lo + 0, w * m, det, fs, ctl);
+        acc_add(lo + 1, w * (m0 + q.aff[2] * dxc), det, fs, ctl);
+        acc_add(hi + 0, w * (m1 + q.aff[5] * dxc), det, fs, ctl);
+        acc_add(hi + 1, w * (m2 + q.aff[8] * dxc), det, fs, ctl);
       }
     }
   }
@@ -576,6 +637,7 @@ __device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double
 // footprint exceeds the tile fall back to direct REDs.
 // s_scatter: the substep whose P2G this is (a scatter that would leave the
 // node arrays' allocation latches kErrRegrow for it instead of writing).
+template <int kDet>
 __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
                                  const Geometry& g, NodeBuf grid, int cta, bool box_done,
                                  Ctl* ctl, int s_scatter) {
@@ -583,7 +645,7 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
   if (g.scatter_mode == 1 || g.scatter_mode == 3) {  // A/B switches without a tile
     if (tid == 0 && g.cta_box) g.cta_box[8 * cta + 6] = 0;  // next G2P: no staged box
     if (g.scatter_mode == 1 && active) {  // per-particle REDs (3: no scatter)
-      if (stencil_in_alloc(g, q.st.base)) scatter_direct(g, grid, m, q);
+      if (stencil_in_alloc(g, q.st.base)) scatter_direct<kDet>(g, grid, m, q, ctl);
       else raise(ctl, kErrRegrow, s_scatter);
     }
     return;
@@ -628,7 +690,7 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
                  (q.st.base[2] - T.lo[2]);
       tiled = atomicCAS(&T.owner[base_idx], -1, tid) == -1;
     }
-    if (!tiled) scatter_direct(g, grid, m, q);
+    if (!tiled) scatter_direct<kDet>(g, grid, m, q, ctl);
   }
   if (!use_tile) return;  // block-uniform
   const double dx = g.dx;
@@ -661,9 +723,25 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
     }
   }
   TRACE_MARK(6);
+  if (det_on<kDet>(g)) {
+    // deterministic mode: the tile's node sums (a fixed phase order within
+    // the CTA) become 64-bit fixed point in place and reach the grid with
+    // integer bulk reductions, exact in any order across CTAs (a whole-block
+    // conversion pass; per-warp convert-and-issue measured slower, 84 vs
+    // 76 us on config 2a)
+    __syncthreads();
+    const double fs = g.fx_s;
+    bool bad = false;
+    for (int e = tid; e < vol; e += blockDim.x) {
+      const double2 a = T.nlo[e], b = T.nhi[e];
+      T.nlo[e] = make_double2(fixed_bits(a.x, fs, bad), fixed_bits(a.y, fs, bad));
+      T.nhi[e] = make_double2(fixed_bits(b.x, fs, bad), fixed_bits(b.y, fs, bad));
+    }
+    if (bad) raise(ctl, kErrFixedRange, s_scatter);
+  }
   fence_proxy_async();
   __syncthreads();
-  tile_bulk_reduce(T, g, grid);
+  tile_bulk_reduce<kDet>(T, g, grid);
   TRACE_MARK(7);
 }
 
@@ -952,7 +1030,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_p2g_gel_tile(
     if (active && !stencil_in_grid(g, q.st)) active = false;  // zero_grid already raised
   }
   reduce_min_detf(ctl, s, active, J);
-  p2g_tile_scatter(T, active, q, m, g, grid, blockIdx.x, false, ctl, s);
+  p2g_tile_scatter<-1>(T, active, q, m, g, grid, blockIdx.x, false, ctl, s);
 }
 
 // Indenter scatter with a non-uniform velocity (only possible before the
@@ -977,7 +1055,7 @@ __global__ void __launch_bounds__(256) k_p2g_ind_direct(const double* __restrict
   q.mv[2] = m * v[2 * n + p];
 #pragma unroll
   for (int i = 0; i < 9; ++i) q.aff[i] = 0.0;
-  scatter_direct(g, grid, m, q);
+  scatter_direct<-1>(g, grid, m, q, ctl);
 }
 
 // Rigid indenter: optional apply_boundary + advect (kMove) and the scatter of
@@ -1095,7 +1173,8 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
 #pragma unroll
       for (int i = 0; i < 27; ++i) {
         if (acc[i] != 0.0)
-          red_add(mi + node_index(g, cb[0] + i / 9, cb[1] + (i / 3) % 3, cb[2] + i % 3), acc[i]);
+          mi_add(g, mi + node_index(g, cb[0] + i / 9, cb[1] + (i / 3) % 3, cb[2] + i % 3), acc[i],
+                 ctl);
         acc[i] = 0.0;
       }
     }
@@ -1145,7 +1224,8 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
     if (sum != 0.0) {
       const int64_t node = k0;  // node index of the base cell
       const int a = c / 9, b = (c / 3) % 3, cc = c % 3;
-      red_add(mi + node + (static_cast<int64_t>(a) * g.ga_dim[1] + b) * g.ga_dim[2] + cc, sum);
+      mi_add(g, mi + node + (static_cast<int64_t>(a) * g.ga_dim[1] + b) * g.ga_dim[2] + cc, sum,
+             ctl);
     }
   }
 }
@@ -1196,7 +1276,7 @@ __device__ __forceinline__ bool walk_contrib(const Geometry& g, const Stencil& s
   return c;
 }
 
-template <bool kMove>
+template <bool kMove, int kDet = -1>
 __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __restrict__ x,
                                                int64_t n, int64_t n_el,
                                                const int64_t* __restrict__ col_start, int n_cols,
@@ -1289,9 +1369,9 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
       double sum = 0.0;
       for (int t = t0; t < 32 && S.key[warp][t] == k0; ++t) sum += S.w[warp][comp][t];
       if (sum != 0.0)
-        red_add(mi + k0 + (static_cast<int64_t>(comp / 9) * g.ga_dim[1] + (comp / 3) % 3) * g.ga_dim[2] +
+        mi_add<kDet>(g, mi + k0 + (static_cast<int64_t>(comp / 9) * g.ga_dim[1] + (comp / 3) % 3) * g.ga_dim[2] +
                     comp % 3,
-                sum);
+               sum, ctl);
     }
     __syncwarp();
     if (bey) break;  // the rest of the column is above the elastomer box
@@ -1372,8 +1452,8 @@ __device__ void ind_walk_fixup(const FinFix& fx, const double* __restrict__ x, i
 #pragma unroll
       for (int i = 0; i < 27; ++i) {
         const int ia = i / 9, ib = (i / 3) % 3, ic = i % 3;
-        red_add(mi + node_index(g, st.base[0] + ia, st.base[1] + ib, st.base[2] + ic),
-                st.w[0][ia] * st.w[1][ib] * st.w[2][ic]);
+        mi_add(g, mi + node_index(g, st.base[0] + ia, st.base[1] + ib, st.base[2] + ic),
+               st.w[0][ia] * st.w[1][ib] * st.w[2][ic], const_cast<Ctl*>(ctl));
       }
     }
   }
@@ -1419,12 +1499,12 @@ __device__ __forceinline__ double4 node_velocity(const Geometry& g, double4 q, d
                                                  int i, int j, int k) {
   double4 o = make_double4(0, 0, 0, 0);
   double mass = q.x, p0 = q.y, p1 = q.z, p2 = q.w;
-  if (wi != 0.0) {
-    const double M = wi * m_ind;
-    mass += M;
-    p0 += M * u0;
-    p1 += M * u1;
-    p2 += M * u2;
+  if (wi != 0.0) {  // explicit roundings: tg_download_grid forms the same sums
+    const double M = __dmul_rn(wi, m_ind);
+    mass = __dadd_rn(mass, M);
+    p0 = __dadd_rn(p0, __dmul_rn(M, u0));
+    p1 = __dadd_rn(p1, __dmul_rn(M, u1));
+    p2 = __dadd_rn(p2, __dmul_rn(M, u2));
   }
   if (mass > 0.0) {
     // p / mass, correctly rounded (Markstein: y = RN(1/mass), q = RN(p y),
@@ -1460,8 +1540,16 @@ __device__ __forceinline__ void update_node(NodeBuf mp, double* __restrict__ mi,
                                             int j, int k, bool with_mi) {
   const size_t nd = node_index(g, i, j, k);
   const double2 qa = mp.lo[nd], qb = mp.hi[nd];
-  const double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
-  const double wi = with_mi ? mi[nd] : 0.0;
+  // the accumulators' bits (fixed point in deterministic mode)
+  const bool filled = __double_as_longlong(qa.x) | __double_as_longlong(qa.y) |
+                      __double_as_longlong(qb.x) | __double_as_longlong(qb.y);
+  double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
+  double wi = with_mi ? mi[nd] : 0.0;
+  if (g.det) {
+    q = make_double4(from_fixed(qa.x, g.fx_inv), from_fixed(qa.y, g.fx_inv),
+                     from_fixed(qb.x, g.fx_inv), from_fixed(qb.y, g.fx_inv));
+    wi = from_fixed(wi, g.fxi_inv);
+  }
   double4 o = node_velocity(g, q, wi, m_ind, u0, u1, u2, i, j, k);
   const bool massive = o.w != 0.0;
   o.w = 0.0;
@@ -1473,7 +1561,7 @@ __device__ __forceinline__ void update_node(NodeBuf mp, double* __restrict__ mi,
     st_keep1(vel.z + nd, o.z);
   }
   if (kZero) {
-    if (q.x != 0.0 || q.y != 0.0 || q.z != 0.0 || q.w != 0.0) {  // next scatter target
+    if (filled) {  // next scatter target
       st_keep(mp.lo + nd, 0.0, 0.0);
       st_keep(mp.hi + nd, 0.0, 0.0);
     }
@@ -1636,7 +1724,7 @@ __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile
   Cn[6] = k * b20; Cn[7] = k * b21; Cn[8] = k * b22;
 }
 
-template <bool kBoundary, bool kAdvect, bool kLookahead>
+template <bool kBoundary, bool kAdvect, bool kLookahead, int kDet = -1>
 __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     double* __restrict__ x, double* __restrict__ v, double* __restrict__ Cm,
     double* __restrict__ Fm, const uint8_t* __restrict__ tag, int64_t n, int64_t n_el, GelMap M,
@@ -1688,7 +1776,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     // M_I; the elastomer box comes from the previous finalize, widened)
     const int s = ctl->substep;
     if (stale(ctl, s)) return;
-    ind_cols_block<true>(*reinterpret_cast<ColSmem*>(smem_raw), blockIdx.x - ia.ind_lo, x, n,
+    ind_cols_block<true, kDet>(*reinterpret_cast<ColSmem*>(smem_raw), blockIdx.x - ia.ind_lo, x, n,
                          n_el, ia.col_start, ia.n_cols, ia.moves, ctl, g, ia.mi, 2, s);
     TRACE_END();
     return;
@@ -1778,7 +1866,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     TRACE_MARK(4);
     // advect's motion reductions, min det F of s + 1 and the tile box together
     block_motion_box(T, ctl, s, active, v2, px0, px1, px2, go, J, q.st.base);
-    p2g_tile_scatter(T, go, q, m, g, grid, cta, true, ctl, s + 1);
+    p2g_tile_scatter<kDet>(T, go, q, m, g, grid, cta, true, ctl, s + 1);
   }
   TRACE_END();
 }
@@ -1880,14 +1968,22 @@ __global__ void k_gather_box(NodeBuf mp, const double* __restrict__ mi, VelBuf v
     }
     const size_t nd = node_index(g, i, j, k);
     const double2 qa = mp.lo[nd], qb = mp.hi[nd];
-    const double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
-    const double M = mi[nd] * m_ind;
+    double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
+    double wi = mi[nd];
+    if (g.det) {
+      q = make_double4(from_fixed(qa.x, g.fx_inv), from_fixed(qa.y, g.fx_inv),
+                       from_fixed(qb.x, g.fx_inv), from_fixed(qb.y, g.fx_inv));
+      wi = from_fixed(wi, g.fxi_inv);
+    }
+    const double M = __dmul_rn(wi, m_ind);
     const double2 ua = vel.xy[nd];
     const double4 u = make_double4(ua.x, ua.y, vel.z[nd], 0.0);
-    mass[t] = q.x + M;
-    mom[3 * t] = q.y + M * ctl->ind_v[0];
-    mom[3 * t + 1] = q.z + M * ctl->ind_v[1];
-    mom[3 * t + 2] = q.w + M * ctl->ind_v[2];
+    // the node sums exactly as grid_update forms them (node_velocity)
+    const bool ind = wi != 0.0;
+    mass[t] = ind ? __dadd_rn(q.x, M) : q.x;
+    mom[3 * t] = ind ? __dadd_rn(q.y, __dmul_rn(M, ctl->ind_v[0])) : q.y;
+    mom[3 * t + 1] = ind ? __dadd_rn(q.z, __dmul_rn(M, ctl->ind_v[1])) : q.z;
+    mom[3 * t + 2] = ind ? __dadd_rn(q.w, __dmul_rn(M, ctl->ind_v[2])) : q.w;
     velo[3 * t] = u.x;
     velo[3 * t + 1] = u.y;
     velo[3 * t + 2] = u.z;
@@ -1970,7 +2066,8 @@ int configure_device(int device) {
     if (r != cudaSuccess && e == cudaSuccess) e = r;
   };
   set(reinterpret_cast<const void*>(k_p2g_gel_tile), tile);
-  set(reinterpret_cast<const void*>(k_g2p2g_gel<true, true, true>), tile);
+  set(reinterpret_cast<const void*>(k_g2p2g_gel<true, true, true, 0>), tile);
+  set(reinterpret_cast<const void*>(k_g2p2g_gel<true, true, true, 1>), tile);
   set(reinterpret_cast<const void*>(k_ind_move_p2g<false, true>), static_cast<int>(kIndSmem));
   set(reinterpret_cast<const void*>(k_ind_move_p2g<true, true>), static_cast<int>(kIndSmem));
   set(reinterpret_cast<const void*>(k_ind_cols<true>), static_cast<int>(sizeof(ColSmem)));
@@ -2096,9 +2193,10 @@ int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter) {
     s.ind_v_uniform = true;
   }
   if (lookahead)
-    launch_pdl(k_g2p2g_gel<true, true, true>, dim3(gel_blocks(s) + extra), dim3(kGelThreads), kTileSmem,
-               s.stream, s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo,
-               s.grid_v, s.grid_mp, s.m_el, s.vol_el, ia);
+    launch_pdl(s.geo.det ? k_g2p2g_gel<true, true, true, 1> : k_g2p2g_gel<true, true, true, 0>,
+               dim3(gel_blocks(s) + extra), dim3(kGelThreads), kTileSmem, s.stream, s.x, s.v, s.C,
+               s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp, s.m_el,
+               s.vol_el, ia);
   else
     k_g2p2g_gel<true, true, false><<<gel_blocks(s), kGelThreads, 0, s.stream>>>(
         s.x, s.v, s.C, s.F, s.tag, s.n, s.n_el, gel_map(s), s.ctl, s.geo, s.grid_v, s.grid_mp,

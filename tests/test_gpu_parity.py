@@ -434,17 +434,18 @@ def test_config1_hundred_frames_match_reference(tb, golden):
 
 
 def test_reruns_agree_to_rounding(tb):
-    """Two runs of the config-1 press (1000 frames, gap crossed, 0.1 mm into
-    the gel) from the same inputs. The node sums are fp64 adds in hardware
-    order (tile bulk reductions from neighbouring CTAs, RED.F64), so reruns
-    are not bit-identical; this pins how far apart they are:
-    positions within 1e-11 of the displacement (measured ~3e-13), height maps
-    within 1e-15 m (measured ~3e-17 m), images within 1 LSB (measured equal)."""
+    """Fast mode (deterministic off): two runs of the config-1 press (1000
+    frames, gap crossed, 0.1 mm into the gel) from the same inputs. The node
+    sums are fp64 adds in hardware order (tile bulk reductions from
+    neighbouring CTAs, RED.F64), so reruns are not bit-identical (DESIGN §6);
+    this pins how far apart they are: positions within 1e-11 of the
+    displacement (measured ~3e-13), height maps within 1e-15 m (measured
+    ~3e-17 m), images within 1 LSB (measured equal)."""
     from tests.scenes import CONFIG1_DEEP_STEPS
 
     out = []
     for _ in range(2):
-        s = tb.sim.build_sim(CONFIG1)
+        s = tb.sim.build_sim({**CONFIG1, "deterministic": False})
         x0 = s.positions()
         for _ in range(CONFIG1_DEEP_STEPS // 10):
             tb.mpm.step(s, CONFIG1_V, 10)
@@ -850,3 +851,41 @@ def test_config3_full_size_dots_press_and_slide(tb, golden):
         tb.sim.step_capture(s, CONFIG3_FULL_SLIDE[1], 10, params=rp, want_depth=False,
                             want_image=False)
     _check_checkpoint(tb, s, g, "slide_", CONFIG1, shape, label="config3 dots")
+
+
+def test_deterministic_reruns_bit_identical(tb):
+    """SPEC acceptance 10 / "Concurrency Model": in deterministic mode
+    (SceneConfig.deterministic, the default) two runs of the config-1 press
+    (1000 frames: gap crossed, 0.1 mm into the gel) give byte-identical
+    particle states, height maps and images."""
+    from tests.scenes import CONFIG1_DEEP_STEPS
+
+    out = []
+    for _ in range(2):
+        s = tb.sim.build_sim(CONFIG1)  # deterministic: true by default
+        for _ in range(CONFIG1_DEEP_STEPS // 10):
+            tb.mpm.step(s, CONFIG1_V, 10)
+        depth, img = tb.sim.capture(s, CONFIG1)
+        st = s.state()
+        out.append((st["x"].tobytes(), st["v"].tobytes(), st["C"].tobytes(), st["F"].tobytes(),
+                    depth.tobytes(), img.tobytes()))
+        del s
+    assert out[0] == out[1]
+
+
+@pytest.mark.parametrize("det", [False, True])
+def test_small_scene_both_accumulation_modes_match_reference(tb, golden, det):
+    """The fp64 fast mode and the fixed-point deterministic mode both match
+    the reference (200 substeps of the SMALL press)."""
+    g = golden("small_scene.npz")
+    s = tb.sim.build_sim({**SMALL, "deterministic": det})
+    tb.mpm.step(s, SMALL_V, SMALL_STEPS // 2)
+    tb.mpm.step(s, SMALL_V, SMALL_STEPS // 2)
+    st = s.state()
+    disp = np.abs(g["x"] - g["x0"]).max()
+    assert np.abs(st["x"] - g["x"]).max() <= 1e-9 * disp
+    np.testing.assert_allclose(st["F"], g["F"], rtol=0, atol=1e-11)
+    np.testing.assert_allclose(st["v"], g["v"], rtol=0, atol=1e-8 * np.abs(g["v"]).max())
+    depth, img = tb.sim.capture(s, SMALL)
+    assert np.abs(depth - g["depth"]).max() <= 1e-7
+    assert np.abs(img.astype(int) - g["image"]).max() <= 2

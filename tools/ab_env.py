@@ -13,12 +13,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 CHILD = r"""
-import json, sys, time
+import json, os, sys, time
 sys.path.insert(0, %r)
 import torch
 import paper_2301_08343_b200 as tb
 from tests.scenes import CONFIG2A, CONFIG2A_V
-cfg = CONFIG2A
+cfg = {**CONFIG2A, **json.loads(os.environ.get("AB_CFG", "{}"))}
 s = tb.sim.build_sim(cfg)
 rp = tb.render_params(cfg, "")
 for _ in range(5):
