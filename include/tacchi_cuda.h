@@ -180,6 +180,12 @@ void tg_destroy(tg_handle h);
  * indenter_cloud_for + place_for_press (scene_builder.cpp:33-61); call the
  * latter with out == NULL to query *n. */
 int tg_generate_cloud(const char* shape, int64_t n, uint64_t seed, double* out);
+/* The same rejection sampling on `device` (setup_kernels.cu: the mt19937_64
+ * stream twisted in shared memory, candidates tested and compacted in stream
+ * order); bit-identical to tg_generate_cloud. tg_build_sim and
+ * tg_build_episodes sample generated indenters this way (TACCHI_HOST_SETUP=1
+ * selects the host restatement). */
+int tg_generate_cloud_device(int device, const char* shape, int64_t n, uint64_t seed, double* out);
 int tg_placed_indenter(const char* config_json, const char* object, double offset_x,
                        double offset_y, double* out, int64_t* n);
 

@@ -118,7 +118,7 @@ EXPORTED = [
     "tg_stream", "tg_kernel_launches", "tg_set_graphs", "tg_last_error", "tg_version",
     "tg_generate_cloud", "tg_placed_indenter", "tg_time_phases", "tg_polar", "tg_init_scene",
     "tg_build_sim_points", "tg_download_constants", "tg_set_keep_grid", "tg_stats",
-    "tg_build_episodes", "tg_set_deterministic",
+    "tg_build_episodes", "tg_set_deterministic", "tg_generate_cloud_device",
 ]
 
 PHASE_TIMING_NAMES = ["p2g_elastomer_first", "p2g_indenter_first", "grid_update",
@@ -185,6 +185,7 @@ def lib():
         L.tg_set_keep_grid.argtypes = [C.c_void_p, C.c_int]
         L.tg_stats.argtypes = [C.c_void_p, _i64p]
         L.tg_set_deterministic.argtypes = [C.c_void_p, C.c_int]
+        L.tg_generate_cloud_device.argtypes = [C.c_int, C.c_char_p, C.c_int64, C.c_uint64, _dp]
         L.tg_build_episodes.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_int, _dp,
                                         C.POINTER(C.c_void_p)]
         L.tg_polar.argtypes = [C.c_int, _dp, C.c_int64, C.c_int, C.c_double, C.c_double, _dp, _dp]
@@ -641,6 +642,13 @@ class geo:  # noqa: N801 — mirrors tacchi::geo (host setup)
     def generate_shape_cloud(name: str, n: int, seed: int) -> np.ndarray:
         out = np.empty((n, 3))
         _check(lib().tg_generate_cloud(name.encode(), n, seed, _p(out)))
+        return out
+
+    @staticmethod
+    def generate_shape_cloud_device(name: str, n: int, seed: int, device: int = 0) -> np.ndarray:
+        """generate_shape_cloud on the GPU (bit-identical to the host's)."""
+        out = np.empty((n, 3))
+        _check(lib().tg_generate_cloud_device(device, name.encode(), n, seed, _p(out)))
         return out
 
     @staticmethod

@@ -28,6 +28,7 @@
 #include "tacchi_cuda.h"
 
 #include "host_config.hpp"
+#include "setup_shapes.h"
 
 namespace tacchi_b200 {
 int fail(int code, const std::string& msg);
@@ -332,6 +333,54 @@ bool make_shape(const std::string& name, Shape& s) {
   return true;
 }
 
+// The device sampler's view of a shape (setup_shapes.h): its box and the
+// libm constants of its predicate, evaluated here exactly as the host
+// predicates above evaluate them.
+bool shape_table(const std::string& name, ShapeTable& t) {
+  static const char* kNames[] = {"sphere", "sphere2", "cone", "cylinder", "cylinder_shell",
+                                 "cylinder_side", "curved_surface", "flat_slab", "dot_in", "dots",
+                                 "hexagon", "triangle", "prism", "line", "parallel_lines",
+                                 "cross_lines", "moon", "pacman", "torus", "wave1", "random"};
+  Shape sh;
+  if (!make_shape(name, sh)) return false;
+  std::memset(&t, 0, sizeof(t));
+  t.id = -1;
+  for (int i = 0; i < 21; ++i)
+    if (name == kNames[i]) t.id = i;
+  if (t.id < 0) return false;
+  for (int a = 0; a < 3; ++a) {
+    t.lo[a] = sh.lo[a];
+    t.span[a] = sh.hi[a] - sh.lo[a];
+  }
+  if (t.id == kShHexagon) {  // polygon(x, y, 6, 3.5)
+    t.n_planes = 6;
+    t.apothem = 3.5 * std::cos(kPi / 6);
+    for (int k = 0; k < 6; ++k) {
+      const double a = (2.0 * kPi * k + kPi) / 6;
+      t.ca[k] = std::cos(a);
+      t.sa[k] = std::sin(a);
+    }
+  } else if (t.id == kShTriangle) {  // triangle(x, y, 6.5)
+    t.n_planes = 3;
+    const double r = 6.5 / std::sqrt(3.0);
+    t.apothem = r / 2.0;
+    for (int k = 0; k < 3; ++k) {
+      const double a = -kPi / 2.0 + 2.0 * kPi * k / 3.0;
+      t.ca[k] = std::cos(a);
+      t.sa[k] = std::sin(a);
+    }
+  } else if (t.id == kShRandom) {
+    static const Bumps field;
+    for (int i = 0; i < 28; ++i) {
+      t.bx[i] = field.cx[i];
+      t.by[i] = field.cy[i];
+      t.amp[i] = field.amp[i];
+      t.inv_s2[i] = field.inv_s2[i];
+    }
+  }
+  return true;
+}
+
 bool is_known_shape(const std::string& name) {
   Shape s;
   return make_shape(name, s);
@@ -564,6 +613,75 @@ std::vector<V3> place_for_press(const Config& c, const std::vector<V3>& cloud, d
 std::vector<V3> placed_indenter(const Config& c, const std::string& object, double off_x,
                                 double off_y) {
   return place_for_press(c, indenter_cloud_for(c, object), off_x, off_y);
+}
+
+// ---- episode setup on the device (f3; setup_kernels.cu) --------------------
+}  // namespace tacchi_b200::host
+namespace tacchi_b200 {
+int device_indenter_cloud(int device, const std::string& shape, uint64_t source_points,
+                          uint64_t target_points, uint64_t seed, double** d_cloud, int64_t* n_out);
+int device_place_for_press(const double* d_cloud, int64_t n, double z_rotation, double centre,
+                           double top_plus_gap, double off_x, double off_y,
+                           std::vector<host::V3>& out);
+void device_free(void* p);
+}  // namespace tacchi_b200
+namespace tacchi_b200::host {
+
+// The generated shape indenter_cloud_for would sample for (cfg, object), or
+// "" when the indenter comes from a point-cloud file (scene_builder.cpp:33-46).
+std::string generated_shape_of(const Config& c, const std::string& object) {
+  if (!c.cloud_path.empty() && (object.empty() || object == c.cloud_path)) return "";
+  const std::string shape = object.empty() ? c.generated_shape : object;
+  Shape probe;
+  return make_shape(shape, probe) ? shape : "";
+}
+
+// Device builds sample generated indenters on the GPU (TACCHI_HOST_SETUP=1
+// keeps the host restatement; both are bit-identical to the reference).
+bool device_setup_enabled() {
+  const char* e = std::getenv("TACCHI_HOST_SETUP");
+  return !(e && std::atoi(e) != 0);
+}
+
+// A generated indenter cloud in device memory (indenter_cloud_for), shared
+// by the placements of one object.
+struct DeviceCloud {
+  double* d = nullptr;
+  int64_t n = 0;
+  DeviceCloud() = default;
+  DeviceCloud(const DeviceCloud&) = delete;
+  DeviceCloud& operator=(const DeviceCloud&) = delete;
+  ~DeviceCloud() {
+    if (d) device_free(d);
+  }
+};
+
+void device_cloud_for(int device, const Config& c, const std::string& shape, DeviceCloud& dc) {
+  const int rc = device_indenter_cloud(device, shape, c.source_points, c.target_points, c.seed,
+                                       &dc.d, &dc.n);
+  if (rc) raise(rc, tg_last_error());
+}
+
+std::vector<V3> device_place(const DeviceCloud& dc, const Config& c, double off_x, double off_y) {
+  const double e = c.edge_mm * 1e-3;
+  const double centre = 0.5 * e;
+  const double top = 0.5 * e + 0.5 * (c.size_mm[2] * 1e-3);  // elastomer_top_z
+  std::vector<V3> out;
+  const int rc = device_place_for_press(dc.d, dc.n, c.z_rotation_rad, centre,
+                                        top + c.gap_mm * 1e-3, off_x, off_y, out);
+  if (rc) raise(rc, tg_last_error());
+  return out;
+}
+
+// placed_indenter for a simulation on `device`: generated shapes are sampled
+// and placed on the GPU, point-cloud files on the host.
+std::vector<V3> placed_indenter_on(int device, const Config& c, const std::string& object,
+                                   double off_x, double off_y) {
+  const std::string shape = generated_shape_of(c, object);
+  if (shape.empty() || !device_setup_enabled()) return placed_indenter(c, object, off_x, off_y);
+  DeviceCloud dc;
+  device_cloud_for(device, c, shape, dc);
+  return device_place(dc, c, off_x, off_y);
 }
 
 // init_scene's checks and particle assembly (scene.cpp:15-87) for
@@ -853,7 +971,8 @@ int tg_build_sim(int device, const char* config_json, const char* object, double
                  double offset_y, tg_handle* out) {
   return guarded([&] {
     const Config c = parse_config(config_json);
-    return build_sim_from(device, c, placed_indenter(c, object ? object : "", offset_x, offset_y),
+    return build_sim_from(device, c,
+                          placed_indenter_on(device, c, object ? object : "", offset_x, offset_y),
                           out);
   });
 }
@@ -896,7 +1015,14 @@ int tg_build_episodes(int device, const char* config_json, const char* object, i
     if (n_episodes < 0 || (n_episodes > 0 && (!poses || !out)))
       raise(TG_ERR_INVALID_ARGUMENT, "tg_build_episodes: bad argument");
     const Config base = parse_config(config_json);
-    const std::vector<V3> cloud = indenter_cloud_for(base, object ? object : "");
+    const std::string obj = object ? object : "";
+    // the cloud once per object: on the device for a generated shape
+    const std::string shape = generated_shape_of(base, obj);
+    const bool on_device = !shape.empty() && device_setup_enabled();
+    DeviceCloud dcloud;
+    std::vector<V3> cloud;
+    if (on_device) device_cloud_for(device, base, shape, dcloud);
+    else cloud = indenter_cloud_for(base, obj);
     std::vector<int> rc(static_cast<size_t>(n_episodes), TG_OK);
     std::vector<std::string> msg(static_cast<size_t>(n_episodes));
     std::atomic<int> next{0};
@@ -906,7 +1032,9 @@ int tg_build_episodes(int device, const char* config_json, const char* object, i
         try {
           Config c = base;
           c.z_rotation_rad = poses[3 * e + 2];
-          const std::vector<V3> placed = place_for_press(c, cloud, poses[3 * e], poses[3 * e + 1]);
+          const std::vector<V3> placed =
+              on_device ? device_place(dcloud, c, poses[3 * e], poses[3 * e + 1])
+                        : place_for_press(c, cloud, poses[3 * e], poses[3 * e + 1]);
           rc[e] = build_sim_from(device, c, placed, &out[e]);
           if (rc[e]) msg[e] = tg_last_error();
         } catch (const HostError& err) {

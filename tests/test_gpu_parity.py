@@ -889,3 +889,43 @@ def test_small_scene_both_accumulation_modes_match_reference(tb, golden, det):
     depth, img = tb.sim.capture(s, SMALL)
     assert np.abs(depth - g["depth"]).max() <= 1e-7
     assert np.abs(img.astype(int) - g["image"]).max() <= 2
+
+
+def test_device_shape_clouds_bit_identical(tb, golden):
+    """f3, episode setup on the GPU: the rejection sampler on the device
+    (mt19937_64 stream twisted in shared memory, candidates tested and
+    compacted in stream order) reproduces the host restatement -- and so the
+    reference (kat.npz cloud hashes) -- bit for bit for all 21 shapes, and at
+    the 1e6-point source size of the sphere, the dot grid, the wave and the
+    bump field (the shapes whose tests call libm)."""
+    from tests.scenes import SHAPES
+
+    k = golden("kat.npz")
+    for i, shape in enumerate(SHAPES):
+        d = tb.geo.generate_shape_cloud_device(shape, 2000, 7)
+        np.testing.assert_array_equal(d, tb.geo.generate_shape_cloud(shape, 2000, 7))
+        assert sha(d) == str(k["cloud_hash"][i]), shape
+    for shape in ("sphere", "dots", "wave1", "random", "pacman"):
+        d = tb.geo.generate_shape_cloud_device(shape, 1000000, 20230115)
+        h = tb.geo.generate_shape_cloud(shape, 1000000, 20230115)
+        assert np.array_equal(d, h), shape
+
+
+def test_device_and_host_setup_build_the_same_scene(tb, golden, monkeypatch):
+    """build_sim / build_episodes with the device setup (default) and the host
+    restatement (TACCHI_HOST_SETUP=1): identical particles for a rotated,
+    offset, subsampled indenter (config-4 pose)."""
+    from paper_2301_08343_b200 import episodes as E
+    from tests.scenes import CONFIG1
+
+    ep = E.make_episode(5)
+    cfg = E.episode_config(CONFIG1, ep)
+    dev = tb.sim.build_sim(cfg, "dots", ep.offset_x_m, ep.offset_y_m).positions()
+    dev_eps = tb.sim.build_episodes(CONFIG1, "dots", [[ep.offset_x_m, ep.offset_y_m,
+                                                       ep.z_rotation_rad]])[0].positions()
+    monkeypatch.setenv("TACCHI_HOST_SETUP", "1")
+    host = tb.sim.build_sim(cfg, "dots", ep.offset_x_m, ep.offset_y_m).positions()
+    np.testing.assert_array_equal(dev, host)
+    np.testing.assert_array_equal(dev_eps, host)
+    np.testing.assert_array_equal(host[-100000:], tb.geo.placed_indenter(cfg, "dots", ep.offset_x_m,
+                                                                          ep.offset_y_m))

@@ -15,7 +15,9 @@ from tests.scenes import CONFIG1, CONFIG2A, CONFIG2A_V, SUBSTEPS_PER_FRAME  # no
 
 name = sys.argv[1] if len(sys.argv) > 1 else "config2a"
 frames = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-cfg = CONFIG2A if name == "config2a" else CONFIG1
+# the bench's accumulation mode (fp64); "-det" selects the deterministic mode
+cfg = dict(CONFIG2A if name.startswith("config2a") else CONFIG1)
+cfg["deterministic"] = name.endswith("-det")
 s = tb.sim.build_sim(cfg)
 rp = tb.render_params(cfg, "")
 v = np.array(CONFIG2A_V)
