@@ -151,7 +151,7 @@ def _roofline(s, phase_ms, walked_per_substep, n_el, n_ind, window_nodes):
     achieved = per_kernel[dom] / (dom_ms * 1e-3) / 1e9
     per_substep = n_el * GEL_BYTES + n_ind * IND_BYTES
     substep_ms = (phase_ms["grid_update"] + phase_ms["g2p2g_elastomer"] + phase_ms["finalize"])
-    traffic = shared = None
+    traffic = shared = atomics = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f)
@@ -161,6 +161,17 @@ def _roofline(s, phase_ms, walked_per_substep, n_el, n_ind, window_nodes):
             if "shared_wavefronts_per_launch" in tr[kname]:
                 shared = {"wavefronts_per_launch": tr[kname]["shared_wavefronts_per_launch"],
                           "pct_of_peak_sustained": tr[kname]["shared_wavefronts_pct_of_peak"]}
+            red = tr[kname].get("l2_reduction")
+            if red:
+                atomics = {
+                    "l2_reduction_requests_per_launch": red["lts__t_requests_op_red.sum"],
+                    "l2_reduction_bytes_per_launch": 32 * red["lts__t_sectors_op_red.sum"],
+                    "l2_atomic_unit_active_pct_of_peak":
+                        red["lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed"],
+                    "bulk_reductions_per_launch": red["sm__sass_inst_executed_op_tma_red.sum"],
+                    "redg_instructions_per_launch": red["smsp__sass_inst_executed_op_global_red.sum"],
+                    "source": "profiles/traffic.json l2_reduction (ncu lts__t_*_op_red, "
+                              "lts__d_atomic_input_cycles_active; profiles/r2_atomics.md)"}
     except Exception:
         pass
     return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -173,7 +184,8 @@ def _roofline(s, phase_ms, walked_per_substep, n_el, n_ind, window_nodes):
                                          "written) + 48 B per indenter particle the launch "
                                          "advects (x read + written)",
             "indenter_particles_advected_per_launch": walked_per_substep,
-            "shared_memory": shared, "kernel_ms": dom_ms,
+            "traffic_over_algorithmic": (traffic / per_kernel[dom]) if traffic else None,
+            "shared_memory": shared, "atomics": atomics, "kernel_ms": dom_ms,
             "substep": {"ms": substep_ms, "algorithmic_bytes": per_substep,
                         "achieved_gbs": per_substep / (substep_ms * 1e-3) / 1e9,
                         "frac": per_substep / (substep_ms * 1e-3) / 1e9 / peak,
