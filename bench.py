@@ -278,12 +278,33 @@ def run_single(args):
     launches = s.kernel_launches - k0
 
     # --- timed region 2: end to end through the C-ABI with host buffers ---
+    # Pipelined control steps (tg_step_capture_submit / _wait): frame k's
+    # depth + RGB come back to pinned host memory while frame k+1 runs; the
+    # host reads every frame. Timed on the handle's stream from before the
+    # first submit to after the last frame's read-back, and on the wall clock.
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(device)
+    stream = torch.cuda.ExternalStream(s.stream, device=device)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    checksum = 0
     t0 = time.perf_counter()
-    e2e_ms, (depth, img) = _time_frames(tb, s, v, rp, args.steps, True)
+    e2.record(stream)
+    prev = tb.sim.step_capture_submit(s, v, SUBSTEPS_PER_FRAME, rp)
+    for _ in range(args.steps - 1):
+        cur = tb.sim.step_capture_submit(s, v, SUBSTEPS_PER_FRAME, rp)
+        depth, img = tb.sim.step_capture_wait(s, prev, rp)
+        checksum += int(img[rp.height // 2, rp.width // 2, 0]) + int(depth[0, 0] > 0)
+        prev = cur
+    depth, img = tb.sim.step_capture_wait(s, prev, rp)
+    checksum += int(img[rp.height // 2, rp.width // 2, 0])
+    e3.record(stream)
+    torch.cuda.synchronize(device)
+    e2e_ms = e2.elapsed_time(e3)
     e2e_wall = (time.perf_counter() - t0) * 1e3
+    # the synchronous call (one control step, one host sync: the Session's
+    # shape), for reference
+    sync_ms, _ = _time_frames(tb, s, v, rp, args.steps, True)
     clk = clocks.stop()
 
     # --- per-kernel timing for the roofline (after the timed regions) ---
@@ -298,6 +319,7 @@ def run_single(args):
     if world > 1:
         dev_ms = episodes.max_over_ranks(dev_ms, device=f"cuda:{device}")
         e2e_ms = episodes.max_over_ranks(e2e_ms, device=f"cuda:{device}")
+        sync_ms = episodes.max_over_ranks(sync_ms, device=f"cuda:{device}")
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -322,8 +344,13 @@ def run_single(args):
                 "frames_per_sec": args.steps * world / (e2e_ms * 1e-3),
                 "h2d_bytes_per_step": 3 * 8, "d2h_bytes_per_step": depth.nbytes + img.nbytes,
                 "wall_ms_per_step": e2e_wall / args.steps,
-                "api": "tb.sim.step_capture -> tg_step_capture (step + capture, one host sync; "
-                       "depth f64 + RGB8 D2H into the handle's pinned buffers each step)"},
+                "api": "tb.sim.step_capture_submit / _wait -> tg_step_capture_submit / "
+                       "tg_step_capture_wait (step + capture + depth f64 + RGB8 D2H into pinned "
+                       "host slots each step, two frames in flight, the host reads every frame)",
+                "synchronous": {"value": units / (sync_ms * 1e-3),
+                                "frames_per_sec": args.steps * world / (sync_ms * 1e-3),
+                                "api": "tb.sim.step_capture -> tg_step_capture (one control step, "
+                                       "one host sync per call)"}},
         "gpu_launches": int(launches),
         "roofline": _roofline(s, phase_ms, walked, n_el, n - n_el, window_nodes),
     }
@@ -362,8 +389,9 @@ def run_config4(args):
     n = sims[0].n if sims else 0
 
     def frame(want):
+        # outputs straight into each handle's pinned host buffers (zero_copy)
         outs, _ = tb.sim.step_capture_many(sims, vel, SUBSTEPS_PER_FRAME, rp, want_depth=want,
-                                           want_image=want)
+                                           want_image=want, zero_copy=want)
         return outs
 
     def timed(steps, want):
@@ -424,7 +452,8 @@ def run_config4(args):
         "e2e": {"value": units / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": 3 * 8 * len(sims), "d2h_bytes_per_step": d2h,
                 "api": "tb.sim.step_capture_many -> tg_step_capture_many (every episode's step + "
-                       "capture submitted before any wait; depth f64 + RGB8 to host each step)"},
+                       "capture submitted before any wait; depth f64 + RGB8 into each handle's "
+                       "pinned host buffers each step)"},
         "gpu_launches": int(launches),
     }
     if clk:

@@ -260,6 +260,19 @@ int tg_capture_buffers(tg_handle h, const tg_render* r, double** depth, uint8_t*
 int tg_step_capture(tg_handle h, const double indenter_velocity[3], int n_substeps,
                     const tg_render* r, double* depth_out, uint8_t* rgb_out);
 
+/* Pipelined control steps, for a caller that can take frame k's outputs
+ * while frame k+1 runs (a dataset writer, a batch consumer): submit enqueues
+ * mpm::step(v, n) + sim::capture(r) + the depth / RGB read-back into one of
+ * two pinned slots of the handle and returns at once (*ticket = the frame's
+ * number); wait (tickets in order) blocks until that frame is done and points
+ * *depth / *rgb at its slot, valid until the submit after next. At most two
+ * frames in flight; no other call on the handle while frames are in flight.
+ * A frame's error is reported by its wait; a frame submitted after a failing
+ * one reports it too (it ran as a no-op). n <= 200. */
+int tg_step_capture_submit(tg_handle h, const double indenter_velocity[3], int n_substeps,
+                           const tg_render* r, int64_t* ticket);
+int tg_step_capture_wait(tg_handle h, int64_t ticket, double** depth, uint8_t** rgb);
+
 /* render::extract_surface_depth(state, w, h, r) (depth_extract.cpp:10-49);
  * w <= 0 or h <= 0 selects the full-surface overload (:51-57) and returns
  * its size in *out_w / *out_h (call with out == NULL to query). */

@@ -119,6 +119,7 @@ EXPORTED = [
     "tg_generate_cloud", "tg_placed_indenter", "tg_time_phases", "tg_polar", "tg_init_scene",
     "tg_build_sim_points", "tg_download_constants", "tg_set_keep_grid", "tg_stats",
     "tg_build_episodes", "tg_set_deterministic", "tg_generate_cloud_device",
+    "tg_step_capture_submit", "tg_step_capture_wait",
 ]
 
 PHASE_TIMING_NAMES = ["p2g_elastomer_first", "p2g_indenter_first", "grid_update",
@@ -186,6 +187,10 @@ def lib():
         L.tg_stats.argtypes = [C.c_void_p, _i64p]
         L.tg_set_deterministic.argtypes = [C.c_void_p, C.c_int]
         L.tg_generate_cloud_device.argtypes = [C.c_int, C.c_char_p, C.c_int64, C.c_uint64, _dp]
+        L.tg_step_capture_submit.argtypes = [C.c_void_p, _dp, C.c_int, C.POINTER(TgRender),
+                                             _i64p]
+        L.tg_step_capture_wait.argtypes = [C.c_void_p, C.c_int64, C.POINTER(_dp),
+                                           C.POINTER(_u8p)]
         L.tg_build_episodes.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_int, _dp,
                                         C.POINTER(C.c_void_p)]
         L.tg_polar.argtypes = [C.c_int, _dp, C.c_int64, C.c_int, C.c_double, C.c_double, _dp, _dp]
@@ -522,6 +527,24 @@ class render:  # noqa: N801 — mirrors tacchi::render
         return out
 
 
+_VIEWS: dict = {}
+
+
+def _pinned_view(addr: int, shape, dtype) -> np.ndarray:
+    """numpy view of a pinned host buffer owned by the library (cached per
+    address: the slots are reused frame after frame)."""
+    key = (addr, shape, np.dtype(dtype).str)
+    v = _VIEWS.get(key)
+    if v is None:
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        buf = (C.c_char * n).from_address(addr)
+        v = np.frombuffer(buf, dtype=dtype).reshape(shape)
+        if len(_VIEWS) > 4096:
+            _VIEWS.clear()
+        _VIEWS[key] = v
+    return v
+
+
 class sim:  # noqa: N801 — mirrors tacchi::sim
     @staticmethod
     def build_sim(cfg=None, obj: str = "", offset_x: float = 0.0, offset_y: float = 0.0,
@@ -564,11 +587,11 @@ class sim:  # noqa: N801 — mirrors tacchi::sim
     def _pinned_views(state: SimState, rp: TgRender):
         """numpy views of the handle's pinned capture buffers (tg_capture_buffers);
         valid until the next capture on this state."""
-        dptr, rptr = C.POINTER(C.c_double)(), C.POINTER(C.c_uint8)()
-        _check(lib().tg_capture_buffers(state.handle, C.byref(rp), C.byref(dptr), C.byref(rptr)))
-        depth = np.ctypeslib.as_array(dptr, shape=(rp.height, rp.width))
-        img = np.ctypeslib.as_array(rptr, shape=(rp.height, rp.width, 3))
-        return depth, img
+        dptr, rptr = C.c_void_p(), C.c_void_p()
+        _check(lib().tg_capture_buffers(state.handle, C.byref(rp), C.cast(C.pointer(dptr), C.POINTER(_dp)),
+                                        C.cast(C.pointer(rptr), C.POINTER(_u8p))))
+        return (_pinned_view(dptr.value, (rp.height, rp.width), np.float64),
+                _pinned_view(rptr.value, (rp.height, rp.width, 3), np.uint8))
 
     @staticmethod
     def step_capture(state: SimState, indenter_velocity, n_substeps: int, cfg=None, obj: str = "",
@@ -592,11 +615,32 @@ class sim:  # noqa: N801 — mirrors tacchi::sim
 
 
     @staticmethod
+    def step_capture_submit(state: SimState, indenter_velocity, n_substeps: int,
+                            params: TgRender) -> int:
+        """Pipelined control step (tg_step_capture_submit): enqueue step +
+        capture + read-back, return the frame's ticket at once."""
+        t = C.c_int64()
+        _check(lib().tg_step_capture_submit(state.handle, _p(_vec(indenter_velocity)),
+                                            int(n_substeps), C.byref(params), C.byref(t)))
+        return t.value
+
+    @staticmethod
+    def step_capture_wait(state: SimState, ticket: int, params: TgRender):
+        """Outputs of a submitted frame (tickets in order): (depth, image) views
+        of its pinned slot, valid until the submit after next."""
+        dptr, rptr = C.c_void_p(), C.c_void_p()
+        _check(lib().tg_step_capture_wait(state.handle, int(ticket), C.cast(C.pointer(dptr), C.POINTER(_dp)),
+                                          C.cast(C.pointer(rptr), C.POINTER(_u8p))))
+        return (_pinned_view(dptr.value, (params.height, params.width), np.float64),
+                _pinned_view(rptr.value, (params.height, params.width, 3), np.uint8))
+
+    @staticmethod
     def step_capture_many(states, velocities, n_substeps: int, params, want_depth: bool = True,
-                          want_image: bool = True):
+                          want_image: bool = True, zero_copy: bool = False):
         """Batched control step (tg_step_capture_many): every state steps with
         its velocity row and is captured with `params` (one TgRender for all,
-        or one per state); all submitted before any wait. Returns
+        or one per state); all submitted before any wait; zero_copy returns
+        views of each handle's pinned buffers (overwritten by its next capture). Returns
         (outputs, status): outputs[i] = (depth, image) (None where not
         wanted), status[i] = the handle's error code (0 = OK). Raises the
         first failing handle's error after every handle was processed."""
@@ -609,8 +653,13 @@ class sim:  # noqa: N801 — mirrors tacchi::sim
         outs, dptr, iptr = [], (_dp * n)(), (_u8p * n)()
         for i in range(n):
             rp = ps[0] if len(ps) == 1 else ps[i]
-            d = np.empty((rp.height, rp.width)) if want_depth else None
-            im = np.empty((rp.height, rp.width, 3), np.uint8) if want_image else None
+            if zero_copy:  # views of the handle's pinned buffers (next capture overwrites)
+                d, im = sim._pinned_views(states[i], rp)
+                d = d if want_depth else None
+                im = im if want_image else None
+            else:
+                d = np.empty((rp.height, rp.width)) if want_depth else None
+                im = np.empty((rp.height, rp.width, 3), np.uint8) if want_image else None
             dptr[i] = _p(d)
             iptr[i] = _p(im, _u8p)
             outs.append((d, im))

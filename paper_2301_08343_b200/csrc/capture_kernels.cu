@@ -369,8 +369,33 @@ static void launch_surface_depth(DeviceSim& s) {
 // sim::capture. depth_host / rgb_host may be null (device-resident result).
 // Enqueues sim::capture on the handle's stream: the fused kernel and, when
 // requested, the D2H copies of depth / RGB into the handle's pinned buffers.
+int capture_enqueue_to(DeviceSim& s, const tg_render& r, double* depth_pinned, uint8_t* rgb_pinned,
+                       std::string& msg);
+
 int capture_enqueue(DeviceSim& s, const tg_render& r, bool want_depth, bool want_rgb,
                     std::string& msg) {
+  if (s.cap_pixels < static_cast<size_t>(r.width) * r.height || !s.h_depth_pinned) {
+    // allocate (ensure_capture_buffers) before taking the pinned pointers
+    const int rc = capture_enqueue_to(s, r, nullptr, nullptr, msg);
+    if (rc) return rc;
+    if (!want_depth && !want_rgb) return TG_OK;
+    // the capture ran; only the read-back is left
+    const size_t pixels = static_cast<size_t>(r.width) * r.height;
+    if (want_depth)
+      cudaMemcpyAsync(s.h_depth_pinned, s.cap_depth, pixels * sizeof(double),
+                      cudaMemcpyDeviceToHost, s.stream);
+    if (want_rgb)
+      cudaMemcpyAsync(s.h_rgb_pinned, s.cap_rgb, pixels * 3, cudaMemcpyDeviceToHost, s.stream);
+    return TG_OK;
+  }
+  return capture_enqueue_to(s, r, want_depth ? s.h_depth_pinned : nullptr,
+                            want_rgb ? s.h_rgb_pinned : nullptr, msg);
+}
+
+// sim::capture on the handle's stream; the depth / RGB read-backs (if the
+// destinations are given: pinned host buffers) are enqueued after it.
+int capture_enqueue_to(DeviceSim& s, const tg_render& r, double* depth_pinned, uint8_t* rgb_pinned,
+                       std::string& msg) {
   if (s.surf_nx < 2 || s.surf_ny < 2 || !s.surf_idx) {
     msg = "extract_surface_depth: state has no surface lattice";
     return kErrNoSurface;
@@ -409,11 +434,11 @@ int capture_enqueue(DeviceSim& s, const tg_render& r, bool want_depth, bool want
       s.surf_depth, s.surf_ny, mx, my, r.pixel_to_meter, cx, cy, ow, oh, r_out, make_shade(r),
       r.background ? s.cap_bg : nullptr, s.cap_depth, s.cap_rgb);
   s.kernel_launches += 1;
-  if (want_depth)
-    cudaMemcpyAsync(s.h_depth_pinned, s.cap_depth, pixels * sizeof(double),
-                    cudaMemcpyDeviceToHost, s.stream);
-  if (want_rgb)
-    cudaMemcpyAsync(s.h_rgb_pinned, s.cap_rgb, pixels * 3, cudaMemcpyDeviceToHost, s.stream);
+  if (depth_pinned)
+    cudaMemcpyAsync(depth_pinned, s.cap_depth, pixels * sizeof(double), cudaMemcpyDeviceToHost,
+                    s.stream);
+  if (rgb_pinned)
+    cudaMemcpyAsync(rgb_pinned, s.cap_rgb, pixels * 3, cudaMemcpyDeviceToHost, s.stream);
   s.cap_last_pixels = pixels;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -102,6 +102,16 @@ DeviceSim::~DeviceSim() {
   cudaFreeHost(h_vind);
   cudaFreeHost(h_depth_pinned);
   cudaFreeHost(h_rgb_pinned);
+  if (copy_stream) cudaStreamSynchronize(copy_stream);
+  for (FrameSlot& f : frames) {
+    cudaFreeHost(f.depth);
+    cudaFreeHost(f.rgb);
+    cudaFreeHost(f.ctl);
+    cudaFree(f.d_snap);
+    if (f.ev) cudaEventDestroy(f.ev);
+    if (f.captured) cudaEventDestroy(f.captured);
+  }
+  if (copy_stream) cudaStreamDestroy(copy_stream);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -309,6 +319,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   g.gu_bps = 10;
   g.pdl_early = 1;
   g.ind_first = 1;
+  g.early_zero = 1;
+  if (const char* e = std::getenv("TACCHI_EARLY_ZERO")) g.early_zero = std::atoi(e);
   if (const char* e = std::getenv("TACCHI_GU_BPS")) g.gu_bps = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("TACCHI_PDL_EARLY")) g.pdl_early = std::atoi(e);
   if (const char* e = std::getenv("TACCHI_IND_FIRST")) g.ind_first = std::atoi(e);
@@ -561,15 +573,18 @@ static int record_substeps(DeviceSim& s, int n_substeps) {
 }
 
 // Enqueues mpm::step's n_substeps (engine.cpp:288-297) on the handle's stream.
+constexpr int kChainMax = 200;
+
 int step_submit(DeviceSim& s, const double vind[3], int n_substeps) {
   CUDA_TRY(cudaSetDevice(s.device));
   s.pending_start = s.host_substep;
   if (n_substeps <= 0) return TG_OK;
   for (int a = 0; a < 3; ++a) s.h_vind[a] = vind[a];
   // the indenter chain continues only with the same velocity (bitwise) and
-  // while the per-particle 8-bit move counters cannot overflow
+  // for at most kChainMax substeps (the per-particle move counters are 8-bit;
+  // 200 = tg_step's chunk, so every 200 substeps of a long run pay one catch-up)
   if (s.chain_open && (std::memcmp(s.chain_vind, vind, sizeof(s.chain_vind)) != 0 ||
-                       s.chain_len + n_substeps > 255))
+                       s.chain_len + n_substeps > kChainMax))
     flush_indenter(s);
   // zero_grid of the first substep (a failing window latches OutOfGrid for
   // this substep and every later kernel exits early); it reads positions.
@@ -877,6 +892,140 @@ int download(DeviceSim& s, double* x, double* v, double* Cm, double* Fm) {
   }
   if (Cm && (rc = get9(s.C, Cm, false))) return rc;
   if (Fm && (rc = get9(s.F, Fm, true))) return rc;
+  return TG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined control steps: frame k's read-back overlaps frame k+1's substeps.
+// ---------------------------------------------------------------------------
+int capture_enqueue_to(DeviceSim& s, const tg_render& r, double* depth_pinned, uint8_t* rgb_pinned,
+                       std::string& msg);
+
+static int frame_buffers(DeviceSim& s, FrameSlot& f, size_t pixels) {
+  if (!s.copy_stream && cudaStreamCreateWithFlags(&s.copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(TG_ERR_CUDA, "pipelined capture: stream creation failed");
+  if ((!f.ev && cudaEventCreateWithFlags(&f.ev, cudaEventDisableTiming) != cudaSuccess) ||
+      (!f.captured && cudaEventCreateWithFlags(&f.captured, cudaEventDisableTiming) != cudaSuccess))
+    return fail(TG_ERR_CUDA, "pipelined capture: event creation failed");
+  if ((!f.ctl && cudaMallocHost(&f.ctl, sizeof(Ctl)) != cudaSuccess) ||
+      (!f.d_snap && cudaMalloc(&f.d_snap, sizeof(Ctl)) != cudaSuccess))
+    return fail(TG_ERR_CUDA, "pipelined capture: allocation failed");
+  if (pixels > f.pixels) {
+    cudaFreeHost(f.depth);
+    cudaFreeHost(f.rgb);
+    f.depth = nullptr;
+    f.rgb = nullptr;
+    if (cudaMallocHost(&f.depth, pixels * sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(&f.rgb, pixels * 3) != cudaSuccess)
+      return fail(TG_ERR_CUDA, "pipelined capture: pinned allocation failed");
+    f.pixels = pixels;
+  }
+  return TG_OK;
+}
+
+// mpm::step + sim::capture of one frame, synchronously, into the slot (the
+// keep_grid path, a frame that follows a grown allocation).
+static int frame_run_sync(DeviceSim& s, FrameSlot& f) {
+  // pending read-backs of other frames must drain the capture buffers first
+  if (s.copy_stream) CUDA_TRY(cudaStreamSynchronize(s.copy_stream));
+  int rc = step(s, f.v, f.n);
+  if (rc) return rc;
+  std::string msg;
+  rc = capture_enqueue_to(s, f.r, f.depth, f.rgb, msg);
+  if (rc) return fail(rc, msg);
+  CUDA_TRY(cudaStreamSynchronize(s.stream));
+  return TG_OK;
+}
+
+int frame_submit(DeviceSim& s, const double v[3], int n, const tg_render& r, int64_t* ticket) {
+  CUDA_TRY(cudaSetDevice(s.device));
+  if (n < 0 || n > 200) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture_submit: n outside [0, 200]");
+  FrameSlot& f = s.frames[s.frames_submitted % 2];
+  if (f.live)
+    return fail(TG_ERR_INVALID_ARGUMENT,
+                "tg_step_capture_submit: two frames in flight; wait for the oldest first");
+  int rc = frame_buffers(s, f, static_cast<size_t>(std::max(r.width, 0)) * std::max(r.height, 0));
+  if (rc) return rc;
+  for (int a = 0; a < 3; ++a) f.v[a] = v[a];
+  f.n = n;
+  f.r = r;
+  f.replay = false;
+  f.status = 0;
+  f.msg.clear();
+  if (s.keep_grid) {  // the last substep runs the (synchronous) phase path
+    rc = frame_run_sync(s, f);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(f.ctl, s.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s.stream));
+    CUDA_TRY(cudaEventRecord(f.ev, s.stream));
+  } else {
+    // handle stream: the substeps, then (once the previous frame's read-back
+    // has drained the capture buffers) the capture kernel and a device
+    // snapshot of the control block; copy stream: the read-backs, while the
+    // handle stream already runs the next frame's substeps
+    const int start = s.host_substep;
+    rc = step_submit(s, v, n);
+    if (rc) return rc;
+    const FrameSlot& prev = s.frames[(s.frames_submitted + 1) % 2];
+    if (prev.used) CUDA_TRY(cudaStreamWaitEvent(s.stream, prev.ev, 0));
+    std::string msg;
+    rc = capture_enqueue_to(s, r, nullptr, nullptr, msg);
+    if (rc) return fail(rc, msg);
+    CUDA_TRY(cudaMemcpyAsync(f.d_snap, s.ctl, sizeof(Ctl), cudaMemcpyDeviceToDevice, s.stream));
+    CUDA_TRY(cudaEventRecord(f.captured, s.stream));
+    CUDA_TRY(cudaStreamWaitEvent(s.copy_stream, f.captured, 0));
+    const size_t px = static_cast<size_t>(r.width) * r.height;
+    CUDA_TRY(cudaMemcpyAsync(f.depth, s.cap_depth, px * sizeof(double), cudaMemcpyDeviceToHost,
+                             s.copy_stream));
+    CUDA_TRY(cudaMemcpyAsync(f.rgb, s.cap_rgb, px * 3, cudaMemcpyDeviceToHost, s.copy_stream));
+    CUDA_TRY(cudaMemcpyAsync(f.ctl, f.d_snap, sizeof(Ctl), cudaMemcpyDeviceToHost, s.copy_stream));
+    CUDA_TRY(cudaEventRecord(f.ev, s.copy_stream));
+    f.end_substep = start + n;
+    s.host_substep = start + n;  // the host's view until the frame is waited for
+  }
+  f.used = true;
+  f.live = true;
+  *ticket = s.frames_submitted++;
+  return TG_OK;
+}
+
+int frame_wait(DeviceSim& s, int64_t ticket, double** depth, uint8_t** rgb) {
+  CUDA_TRY(cudaSetDevice(s.device));
+  if (ticket != s.frames_collected)
+    return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture_wait: frames are waited for in order");
+  FrameSlot& f = s.frames[ticket % 2];
+  if (!f.live) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture_wait: no such frame");
+  f.live = false;
+  s.frames_collected++;
+  CUDA_TRY(cudaEventSynchronize(f.ev));
+  int rc = TG_OK;
+  if (f.status) {
+    rc = fail(f.status, f.msg);  // an earlier frame failed; this one ran as a no-op
+  } else if (f.replay) {
+    rc = frame_run_sync(s, f);
+  } else if (f.ctl->err != kNoError) {
+    // the frame (or a later substep) latched an error: drain what follows it
+    // (no-ops under the latch) and clean up as tg_step does
+    CUDA_TRY(cudaStreamSynchronize(s.stream));
+    CUDA_TRY(cudaStreamSynchronize(s.copy_stream));
+    rc = sync_and_check(s, f.end_substep);
+    FrameSlot& next = s.frames[(ticket + 1) % 2];
+    if (rc == kResume) {  // node arrays grown: finish this frame, replay the next
+      rc = step(s, f.v, s.resume_substeps);
+      std::string msg;
+      if (!rc) rc = capture_enqueue_to(s, f.r, f.depth, f.rgb, msg);
+      if (!rc && cudaStreamSynchronize(s.stream) != cudaSuccess) rc = fail(TG_ERR_CUDA, "capture failed");
+      if (rc && !msg.empty()) rc = fail(rc, msg);
+      if (next.live) next.replay = true;
+    } else if (rc && next.live) {
+      next.status = rc;
+      next.msg = std::string("an earlier pipelined frame failed: ") + g_last_error;
+    }
+  } else {
+    s.host_substep = f.ctl->substep;
+  }
+  if (rc) return rc;
+  if (depth) *depth = f.depth;
+  if (rgb) *rgb = f.rgb;
   return TG_OK;
 }
 
@@ -1216,6 +1365,18 @@ int tg_stats(tg_handle h, int64_t out[7]) {
   out[5] = static_cast<int64_t>(s.graphs.size());
   out[6] = static_cast<int64_t>(s.h_ctl->ind_walked);
   return TG_OK;
+}
+
+int tg_step_capture_submit(tg_handle h, const double v[3], int n, const tg_render* r,
+                           int64_t* ticket) {
+  if (!h || !v || !r || !ticket)
+    return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture_submit: null argument");
+  return tacchi_b200::frame_submit(*H(h), v, n, *r, ticket);
+}
+
+int tg_step_capture_wait(tg_handle h, int64_t ticket, double** depth, uint8_t** rgb) {
+  if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture_wait: null handle");
+  return tacchi_b200::frame_wait(*H(h), ticket, depth, rgb);
 }
 
 int tg_set_deterministic(tg_handle h, int enabled) {

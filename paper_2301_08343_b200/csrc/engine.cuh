@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "mpm_device.cuh"
+#include "tacchi_cuda.h"
 
 namespace tacchi_b200 {
 
@@ -67,6 +68,8 @@ struct Geometry {
                         // own griddepcontrol.wait (TACCHI_PDL_EARLY, default 1)
   int ind_first;        // the indenter blocks of the elastomer kernel come first
                         // (TACCHI_IND_FIRST, default 1)
+  int early_zero;       // the elastomer kernel clears its P2G tile right after the
+                        // gather (TACCHI_EARLY_ZERO, default 1)
   // Deterministic mode (SceneConfig::deterministic, SPEC "Concurrency
   // Model"): node sums that several CTAs / warps add to are accumulated as
   // 64-bit fixed point (integer adds are exact, so the order does not
@@ -88,6 +91,28 @@ struct NodeBuf {
 struct VelBuf {
   double2* xy;
   double* z;
+};
+
+// One frame of the pipelined control step (tg_step_capture_submit / _wait):
+// its pinned outputs, a pinned snapshot of the control block taken after it,
+// the event that marks its end, and what was asked (to replay it).
+struct FrameSlot {
+  double* depth = nullptr;
+  uint8_t* rgb = nullptr;
+  size_t pixels = 0;
+  Ctl* ctl = nullptr;             // pinned snapshot of the control block after the frame
+  Ctl* d_snap = nullptr;          // device copy of it, taken on the handle's stream
+  cudaEvent_t captured = nullptr; // the frame's capture kernel (and snapshot) are done
+  cudaEvent_t ev = nullptr;       // its read-back is done (copy stream)
+  bool used = false;              // `ev` has been recorded at least once
+  bool live = false;    // submitted, not yet waited for
+  bool replay = false;  // an earlier frame grew the node arrays: run this one again
+  int status = 0;       // error to report at its wait (an earlier frame failed)
+  std::string msg;
+  double v[3] = {0, 0, 0};
+  int n = 0;
+  int end_substep = 0;
+  tg_render r{};
 };
 
 // Internal return code of step_finish / phase: the node arrays were grown
@@ -166,10 +191,14 @@ struct DeviceSim {
   // Indenter chain: consecutive step calls with one commanded velocity; the
   // advects of indenter particles the column walks skip stay pending (per-
   // particle counters since Ctl::chain_start) until the chain is flushed by
-  // k_ind_catchup (velocity change, state access, 255 substeps).
+  // k_ind_catchup (velocity change, state access, 200 substeps).
   bool chain_open = false;
   int chain_len = 0;
   double chain_vind[3] = {0, 0, 0};
+
+  FrameSlot frames[2];          // pipelined control steps in flight (at most two)
+  cudaStream_t copy_stream = nullptr;  // their read-backs, beside the next frame's substeps
+  int64_t frames_submitted = 0, frames_collected = 0;
 
   ~DeviceSim();
 };

@@ -929,3 +929,38 @@ def test_device_and_host_setup_build_the_same_scene(tb, golden, monkeypatch):
     np.testing.assert_array_equal(dev_eps, host)
     np.testing.assert_array_equal(host[-100000:], tb.geo.placed_indenter(cfg, "dots", ep.offset_x_m,
                                                                           ep.offset_y_m))
+
+
+def test_pipelined_step_capture_matches_synchronous(tb):
+    """tg_step_capture_submit / _wait (two frames in flight, the read-back of
+    frame k overlapping frame k+1) gives the frames of tg_step_capture;
+    order and capacity rules; an error surfaces at its frame's wait and at
+    the wait of the frame submitted after it."""
+    rp = tb.render_params(SMALL, "")
+    a, b = tb.sim.build_sim(SMALL), tb.sim.build_sim(SMALL)
+    ref = [tb.sim.step_capture(b, SMALL_V, 10, params=rp) for _ in range(6)]
+    t = [tb.sim.step_capture_submit(a, SMALL_V, 10, rp)]
+    got = []
+    for k in range(1, 6):
+        t.append(tb.sim.step_capture_submit(a, SMALL_V, 10, rp))
+        if k == 1:
+            with pytest.raises(tb.InvalidArgument):  # a third frame in flight
+                tb.sim.step_capture_submit(a, SMALL_V, 10, rp)
+        d, im = tb.sim.step_capture_wait(a, t[k - 1], rp)
+        got.append((d.copy(), im.copy()))
+    d, im = tb.sim.step_capture_wait(a, t[-1], rp)
+    got.append((d.copy(), im.copy()))
+    for (d, im), (dr, imr) in zip(got, ref):
+        np.testing.assert_allclose(d, dr, rtol=0, atol=1e-12)
+        assert np.abs(im.astype(int) - imr).max() <= 1
+    assert a.step_count == b.step_count == 60
+    # an error in frame k: reported at its wait and at the next frame's
+    x = a.positions()
+    x[-1, 2] = (64 - 3) * (12e-3 / 64) + 0.49 * (12e-3 / 64)
+    a.set_state(x=x)
+    t1 = tb.sim.step_capture_submit(a, (0.0, 0.0, 1.0), 200, rp)
+    t2 = tb.sim.step_capture_submit(a, (0.0, 0.0, 1.0), 10, rp)
+    with pytest.raises(tb.OutOfGrid):
+        tb.sim.step_capture_wait(a, t1, rp)
+    with pytest.raises(tb.OutOfGrid):
+        tb.sim.step_capture_wait(a, t2, rp)
