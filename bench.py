@@ -195,6 +195,31 @@ def _roofline(s, phase_ms, walked_per_substep, n_el, n_ind, window_nodes):
             "phase_ms": phase_ms}
 
 
+def _time_pipelined(tb, s, v, rp, steps, read_back):
+    """Device time of `steps` pipelined frames (tg_step_capture_submit /
+    _wait, two in flight): from before the first submit to after the last
+    frame's shading (and read-back) on the handle's streams; the host reads
+    every frame it gets back. Returns (ms, checksum, last outputs)."""
+    import torch
+
+    stream = torch.cuda.ExternalStream(s.stream, device=s.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    checksum = 0
+    e0.record(stream)
+    prev = tb.sim.step_capture_submit(s, v, SUBSTEPS_PER_FRAME, rp, read_back)
+    out = (None, None)
+    for _ in range(steps - 1):
+        cur = tb.sim.step_capture_submit(s, v, SUBSTEPS_PER_FRAME, rp, read_back)
+        out = tb.sim.step_capture_wait(s, prev, rp)
+        if read_back:
+            checksum += int(out[1][rp.height // 2, rp.width // 2, 0]) + int(out[0][0, 0] > 0)
+        prev = cur
+    out = tb.sim.step_capture_wait(s, prev, rp)  # waits for the frame's last stream
+    e1.record(stream)
+    torch.cuda.synchronize(s.device)
+    return e0.elapsed_time(e1), checksum, out
+
+
 def _time_frames(tb, s, v, rp, steps, want):
     """Device time (CUDA events on the handle's stream) of `steps` frames."""
     import torch
@@ -265,17 +290,21 @@ def run_single(args):
     v = np.array(v)
 
     clocks = Clocks(device)  # sampled from before warm-up until after the timed regions
+    # warm-up through both call forms (graphs, pinned slots, the copy stream)
     for _ in range(args.warmup):
         tb.sim.step_capture(s, v, SUBSTEPS_PER_FRAME, params=rp, want_depth=False, want_image=False)
+    _time_pipelined(tb, s, v, rp, args.warmup, True)
     torch.cuda.synchronize(device)
 
-    # --- timed region 1: device-resident (value) ---
+    # --- timed region 1: device-resident (value): pipelined frames, step +
+    # capture with the outputs left on the device ---
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(device)
     k0 = s.kernel_launches
-    dev_ms, _ = _time_frames(tb, s, v, rp, args.steps, False)
+    dev_ms, _, _ = _time_pipelined(tb, s, v, rp, args.steps, False)
     launches = s.kernel_launches - k0
+    dev_sync_ms, _ = _time_frames(tb, s, v, rp, args.steps, False)  # one sync per call
 
     # --- timed region 2: end to end through the C-ABI with host buffers ---
     # Pipelined control steps (tg_step_capture_submit / _wait): frame k's
@@ -285,22 +314,8 @@ def run_single(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(device)
-    stream = torch.cuda.ExternalStream(s.stream, device=device)
-    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    checksum = 0
     t0 = time.perf_counter()
-    e2.record(stream)
-    prev = tb.sim.step_capture_submit(s, v, SUBSTEPS_PER_FRAME, rp)
-    for _ in range(args.steps - 1):
-        cur = tb.sim.step_capture_submit(s, v, SUBSTEPS_PER_FRAME, rp)
-        depth, img = tb.sim.step_capture_wait(s, prev, rp)
-        checksum += int(img[rp.height // 2, rp.width // 2, 0]) + int(depth[0, 0] > 0)
-        prev = cur
-    depth, img = tb.sim.step_capture_wait(s, prev, rp)
-    checksum += int(img[rp.height // 2, rp.width // 2, 0])
-    e3.record(stream)
-    torch.cuda.synchronize(device)
-    e2e_ms = e2.elapsed_time(e3)
+    e2e_ms, _, (depth, img) = _time_pipelined(tb, s, v, rp, args.steps, True)
     e2e_wall = (time.perf_counter() - t0) * 1e3
     # the synchronous call (one control step, one host sync: the Session's
     # shape), for reference
@@ -320,6 +335,7 @@ def run_single(args):
         dev_ms = episodes.max_over_ranks(dev_ms, device=f"cuda:{device}")
         e2e_ms = episodes.max_over_ranks(e2e_ms, device=f"cuda:{device}")
         sync_ms = episodes.max_over_ranks(sync_ms, device=f"cuda:{device}")
+        dev_sync_ms = episodes.max_over_ranks(dev_sync_ms, device=f"cuda:{device}")
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -340,6 +356,11 @@ def run_single(args):
                          "box ~60 MB through the 126 MB L2 (in-pipeline DRAM traffic ~240 MB per "
                          "substep, DESIGN.md 4.4): inputs are not L2-resident between steps"},
         "frames_per_sec": args.steps * world / (dev_ms * 1e-3),
+        "value_api": "pipelined tg_step_capture_submit / _wait with read_back = 0 (step + capture "
+                     "per frame, outputs stay in HBM)",
+        "value_synchronous": {"value": units / (dev_sync_ms * 1e-3),
+                              "frames_per_sec": args.steps * world / (dev_sync_ms * 1e-3),
+                              "api": "tg_step_capture with no outputs, one host sync per frame"},
         "e2e": {"value": units / (e2e_ms * 1e-3), "unit": UNIT,
                 "frames_per_sec": args.steps * world / (e2e_ms * 1e-3),
                 "h2d_bytes_per_step": 3 * 8, "d2h_bytes_per_step": depth.nbytes + img.nbytes,

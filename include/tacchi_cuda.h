@@ -268,9 +268,12 @@ int tg_step_capture(tg_handle h, const double indenter_velocity[3], int n_subste
  * *depth / *rgb at its slot, valid until the submit after next. At most two
  * frames in flight; no other call on the handle while frames are in flight.
  * A frame's error is reported by its wait; a frame submitted after a failing
- * one reports it too (it ran as a no-op). n <= 200. */
+ * one reports it too (it ran as a no-op). n <= 200. read_back = 0 keeps the
+ * frame's depth / RGB on the device (wait then returns NULL pointers). Only
+ * the surface gather runs on the handle's stream; the shading and the
+ * read-back run on a second stream beside the next frame's substeps. */
 int tg_step_capture_submit(tg_handle h, const double indenter_velocity[3], int n_substeps,
-                           const tg_render* r, int64_t* ticket);
+                           const tg_render* r, int read_back, int64_t* ticket);
 int tg_step_capture_wait(tg_handle h, int64_t ticket, double** depth, uint8_t** rgb);
 
 /* render::extract_surface_depth(state, w, h, r) (depth_extract.cpp:10-49);

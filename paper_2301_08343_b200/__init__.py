@@ -188,7 +188,7 @@ def lib():
         L.tg_set_deterministic.argtypes = [C.c_void_p, C.c_int]
         L.tg_generate_cloud_device.argtypes = [C.c_int, C.c_char_p, C.c_int64, C.c_uint64, _dp]
         L.tg_step_capture_submit.argtypes = [C.c_void_p, _dp, C.c_int, C.POINTER(TgRender),
-                                             _i64p]
+                                             C.c_int, _i64p]
         L.tg_step_capture_wait.argtypes = [C.c_void_p, C.c_int64, C.POINTER(_dp),
                                            C.POINTER(_u8p)]
         L.tg_build_episodes.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_int, _dp,
@@ -616,12 +616,13 @@ class sim:  # noqa: N801 — mirrors tacchi::sim
 
     @staticmethod
     def step_capture_submit(state: SimState, indenter_velocity, n_substeps: int,
-                            params: TgRender) -> int:
+                            params: TgRender, read_back: bool = True) -> int:
         """Pipelined control step (tg_step_capture_submit): enqueue step +
-        capture + read-back, return the frame's ticket at once."""
+        capture (+ read-back), return the frame's ticket at once."""
         t = C.c_int64()
         _check(lib().tg_step_capture_submit(state.handle, _p(_vec(indenter_velocity)),
-                                            int(n_substeps), C.byref(params), C.byref(t)))
+                                            int(n_substeps), C.byref(params), int(bool(read_back)),
+                                            C.byref(t)))
         return t.value
 
     @staticmethod
@@ -631,6 +632,8 @@ class sim:  # noqa: N801 — mirrors tacchi::sim
         dptr, rptr = C.c_void_p(), C.c_void_p()
         _check(lib().tg_step_capture_wait(state.handle, int(ticket), C.cast(C.pointer(dptr), C.POINTER(_dp)),
                                           C.cast(C.pointer(rptr), C.POINTER(_u8p))))
+        if not dptr.value:  # submitted with read_back=False
+            return None, None
         return (_pinned_view(dptr.value, (params.height, params.width), np.float64),
                 _pinned_view(rptr.value, (params.height, params.width, 3), np.uint8))
 

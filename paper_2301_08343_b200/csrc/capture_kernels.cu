@@ -370,7 +370,8 @@ static void launch_surface_depth(DeviceSim& s) {
 // Enqueues sim::capture on the handle's stream: the fused kernel and, when
 // requested, the D2H copies of depth / RGB into the handle's pinned buffers.
 int capture_enqueue_to(DeviceSim& s, const tg_render& r, double* depth_pinned, uint8_t* rgb_pinned,
-                       std::string& msg);
+                       std::string& msg, cudaStream_t shade = nullptr,
+                       cudaEvent_t surface_done = nullptr);
 
 int capture_enqueue(DeviceSim& s, const tg_render& r, bool want_depth, bool want_rgb,
                     std::string& msg) {
@@ -394,8 +395,12 @@ int capture_enqueue(DeviceSim& s, const tg_render& r, bool want_depth, bool want
 
 // sim::capture on the handle's stream; the depth / RGB read-backs (if the
 // destinations are given: pinned host buffers) are enqueued after it.
+// With `shade` (and `surface_done`): only the surface gather runs on the
+// handle's stream (it is all that reads the particles); the shading kernel
+// and the read-backs run on `shade` after `surface_done`, beside whatever the
+// handle's stream does next (the pipelined frames' next substeps).
 int capture_enqueue_to(DeviceSim& s, const tg_render& r, double* depth_pinned, uint8_t* rgb_pinned,
-                       std::string& msg) {
+                       std::string& msg, cudaStream_t shade, cudaEvent_t surface_done) {
   if (s.surf_nx < 2 || s.surf_ny < 2 || !s.surf_idx) {
     msg = "extract_surface_depth: state has no surface lattice";
     return kErrNoSurface;
@@ -424,21 +429,25 @@ int capture_enqueue_to(DeviceSim& s, const tg_render& r, double* depth_pinned, u
   if (r.background)
     cudaMemcpyAsync(s.cap_bg, r.background, pixels * 3, cudaMemcpyHostToDevice, s.stream);
   launch_surface_depth(s);
+  cudaStream_t st = s.stream;
+  if (shade && surface_done) {
+    cudaEventRecord(surface_done, s.stream);
+    cudaStreamWaitEvent(shade, surface_done, 0);
+    st = shade;
+  }
   const LinMap mx = make_linmap(s.surf_nx, s.surf_geom[0], s.surf_geom[2], fw);
   const LinMap my = make_linmap(s.surf_ny, s.surf_geom[1], s.surf_geom[3], fh);
   const CropMap cx = make_cropmap(fw, ow, r.crop_scale, r.crop_offset[0]);
   const CropMap cy = make_cropmap(fh, oh, r.crop_scale, r.crop_offset[1]);
   const double r_out = r.pixel_to_meter * r.crop_scale;  // depth_map.cpp:68
   const dim3 grid((ow + kTileW - 1) / kTileW, (oh + kTileH - 1) / kTileH);
-  k_capture<<<grid, dim3(kTileW, kTileH), 0, s.stream>>>(
+  k_capture<<<grid, dim3(kTileW, kTileH), 0, st>>>(
       s.surf_depth, s.surf_ny, mx, my, r.pixel_to_meter, cx, cy, ow, oh, r_out, make_shade(r),
       r.background ? s.cap_bg : nullptr, s.cap_depth, s.cap_rgb);
   s.kernel_launches += 1;
   if (depth_pinned)
-    cudaMemcpyAsync(depth_pinned, s.cap_depth, pixels * sizeof(double), cudaMemcpyDeviceToHost,
-                    s.stream);
-  if (rgb_pinned)
-    cudaMemcpyAsync(rgb_pinned, s.cap_rgb, pixels * 3, cudaMemcpyDeviceToHost, s.stream);
+    cudaMemcpyAsync(depth_pinned, s.cap_depth, pixels * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (rgb_pinned) cudaMemcpyAsync(rgb_pinned, s.cap_rgb, pixels * 3, cudaMemcpyDeviceToHost, st);
   s.cap_last_pixels = pixels;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

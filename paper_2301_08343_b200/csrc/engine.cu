@@ -27,6 +27,7 @@ int launch_grid_update(DeviceSim& s, int sms, bool zero);
 int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter = false);
 int launch_ind_move(DeviceSim& s, bool lookahead);
 int launch_finalize_step(DeviceSim& s, bool walk_fix = false);
+int launch_snapshot_ctl(DeviceSim& s, Ctl* out);
 int launch_chain_begin(DeviceSim& s);
 int launch_ind_cols(DeviceSim& s, bool move);
 int launch_ind_catchup(DeviceSim& s);
@@ -319,8 +320,6 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   g.gu_bps = 10;
   g.pdl_early = 1;
   g.ind_first = 1;
-  g.early_zero = 1;
-  if (const char* e = std::getenv("TACCHI_EARLY_ZERO")) g.early_zero = std::atoi(e);
   if (const char* e = std::getenv("TACCHI_GU_BPS")) g.gu_bps = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("TACCHI_PDL_EARLY")) g.pdl_early = std::atoi(e);
   if (const char* e = std::getenv("TACCHI_IND_FIRST")) g.ind_first = std::atoi(e);
@@ -899,7 +898,8 @@ int download(DeviceSim& s, double* x, double* v, double* Cm, double* Fm) {
 // Pipelined control steps: frame k's read-back overlaps frame k+1's substeps.
 // ---------------------------------------------------------------------------
 int capture_enqueue_to(DeviceSim& s, const tg_render& r, double* depth_pinned, uint8_t* rgb_pinned,
-                       std::string& msg);
+                       std::string& msg, cudaStream_t shade = nullptr,
+                       cudaEvent_t surface_done = nullptr);
 
 static int frame_buffers(DeviceSim& s, FrameSlot& f, size_t pixels) {
   if (!s.copy_stream && cudaStreamCreateWithFlags(&s.copy_stream, cudaStreamNonBlocking) != cudaSuccess)
@@ -937,7 +937,8 @@ static int frame_run_sync(DeviceSim& s, FrameSlot& f) {
   return TG_OK;
 }
 
-int frame_submit(DeviceSim& s, const double v[3], int n, const tg_render& r, int64_t* ticket) {
+int frame_submit(DeviceSim& s, const double v[3], int n, const tg_render& r, bool read_back,
+                 int64_t* ticket) {
   CUDA_TRY(cudaSetDevice(s.device));
   if (n < 0 || n > 200) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture_submit: n outside [0, 200]");
   FrameSlot& f = s.frames[s.frames_submitted % 2];
@@ -958,25 +959,20 @@ int frame_submit(DeviceSim& s, const double v[3], int n, const tg_render& r, int
     CUDA_TRY(cudaMemcpyAsync(f.ctl, s.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s.stream));
     CUDA_TRY(cudaEventRecord(f.ev, s.stream));
   } else {
-    // handle stream: the substeps, then (once the previous frame's read-back
-    // has drained the capture buffers) the capture kernel and a device
-    // snapshot of the control block; copy stream: the read-backs, while the
-    // handle stream already runs the next frame's substeps
+    // handle stream: the substeps, a device snapshot of the control block
+    // and (once the previous frame's shading has released the capture
+    // buffers) the surface gather; copy stream: the shading kernel and the
+    // read-backs, while the handle stream already runs the next frame
     const int start = s.host_substep;
     rc = step_submit(s, v, n);
     if (rc) return rc;
+    launch_snapshot_ctl(s, f.d_snap);
     const FrameSlot& prev = s.frames[(s.frames_submitted + 1) % 2];
     if (prev.used) CUDA_TRY(cudaStreamWaitEvent(s.stream, prev.ev, 0));
     std::string msg;
-    rc = capture_enqueue_to(s, r, nullptr, nullptr, msg);
+    rc = capture_enqueue_to(s, r, read_back ? f.depth : nullptr, read_back ? f.rgb : nullptr, msg,
+                            s.copy_stream, f.captured);
     if (rc) return fail(rc, msg);
-    CUDA_TRY(cudaMemcpyAsync(f.d_snap, s.ctl, sizeof(Ctl), cudaMemcpyDeviceToDevice, s.stream));
-    CUDA_TRY(cudaEventRecord(f.captured, s.stream));
-    CUDA_TRY(cudaStreamWaitEvent(s.copy_stream, f.captured, 0));
-    const size_t px = static_cast<size_t>(r.width) * r.height;
-    CUDA_TRY(cudaMemcpyAsync(f.depth, s.cap_depth, px * sizeof(double), cudaMemcpyDeviceToHost,
-                             s.copy_stream));
-    CUDA_TRY(cudaMemcpyAsync(f.rgb, s.cap_rgb, px * 3, cudaMemcpyDeviceToHost, s.copy_stream));
     CUDA_TRY(cudaMemcpyAsync(f.ctl, f.d_snap, sizeof(Ctl), cudaMemcpyDeviceToHost, s.copy_stream));
     CUDA_TRY(cudaEventRecord(f.ev, s.copy_stream));
     f.end_substep = start + n;
@@ -984,6 +980,7 @@ int frame_submit(DeviceSim& s, const double v[3], int n, const tg_render& r, int
   }
   f.used = true;
   f.live = true;
+  f.read_back = read_back;
   *ticket = s.frames_submitted++;
   return TG_OK;
 }
@@ -1024,8 +1021,8 @@ int frame_wait(DeviceSim& s, int64_t ticket, double** depth, uint8_t** rgb) {
     s.host_substep = f.ctl->substep;
   }
   if (rc) return rc;
-  if (depth) *depth = f.depth;
-  if (rgb) *rgb = f.rgb;
+  if (depth) *depth = f.read_back ? f.depth : nullptr;
+  if (rgb) *rgb = f.read_back ? f.rgb : nullptr;
   return TG_OK;
 }
 
@@ -1368,10 +1365,10 @@ int tg_stats(tg_handle h, int64_t out[7]) {
 }
 
 int tg_step_capture_submit(tg_handle h, const double v[3], int n, const tg_render* r,
-                           int64_t* ticket) {
+                           int read_back, int64_t* ticket) {
   if (!h || !v || !r || !ticket)
     return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture_submit: null argument");
-  return tacchi_b200::frame_submit(*H(h), v, n, *r, ticket);
+  return tacchi_b200::frame_submit(*H(h), v, n, *r, read_back != 0, ticket);
 }
 
 int tg_step_capture_wait(tg_handle h, int64_t ticket, double** depth, uint8_t** rgb) {

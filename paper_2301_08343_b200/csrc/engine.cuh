@@ -46,6 +46,7 @@ struct Ctl {
   long long walk_fixups;                  // substeps whose walks finalize completed
   unsigned long long ind_walked;          // indenter particles advected by the column walks
 };
+static_assert(sizeof(Ctl) % 8 == 0, "the control block is copied in 8-byte words");
 
 struct Geometry {
   int res[3];
@@ -68,8 +69,6 @@ struct Geometry {
                         // own griddepcontrol.wait (TACCHI_PDL_EARLY, default 1)
   int ind_first;        // the indenter blocks of the elastomer kernel come first
                         // (TACCHI_IND_FIRST, default 1)
-  int early_zero;       // the elastomer kernel clears its P2G tile right after the
-                        // gather (TACCHI_EARLY_ZERO, default 1)
   // Deterministic mode (SceneConfig::deterministic, SPEC "Concurrency
   // Model"): node sums that several CTAs / warps add to are accumulated as
   // 64-bit fixed point (integer adds are exact, so the order does not
@@ -106,6 +105,7 @@ struct FrameSlot {
   cudaEvent_t ev = nullptr;       // its read-back is done (copy stream)
   bool used = false;              // `ev` has been recorded at least once
   bool live = false;    // submitted, not yet waited for
+  bool read_back = true;  // depth / RGB come back to the pinned slot
   bool replay = false;  // an earlier frame grew the node arrays: run this one again
   int status = 0;       // error to report at its wait (an earlier frame failed)
   std::string msg;

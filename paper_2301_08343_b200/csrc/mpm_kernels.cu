@@ -638,11 +638,9 @@ __device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double
 // s_scatter: the substep whose P2G this is (a scatter that would leave the
 // node arrays' allocation latches kErrRegrow for it instead of writing).
 template <int kDet>
-// pre_zeroed: the caller already cleared the whole tile (node halves and
-// owner table), overlapping the stores with its own work.
 __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
                                  const Geometry& g, NodeBuf grid, int cta, bool box_done,
-                                 Ctl* ctl, int s_scatter, bool pre_zeroed = false) {
+                                 Ctl* ctl, int s_scatter) {
   const int tid = threadIdx.x;
   if (g.scatter_mode == 1 || g.scatter_mode == 3) {  // A/B switches without a tile
     if (tid == 0 && g.cta_box) g.cta_box[8 * cta + 6] = 0;  // next G2P: no staged box
@@ -674,7 +672,7 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
   const int d1 = T.dim[1], d2 = T.pitch;  // row pitch
   const int vol = T.dim[0] * d1 * d2;
   const bool use_tile = T.ok != 0;
-  if (use_tile && !pre_zeroed) {
+  if (use_tile) {
     const double2 z2 = make_double2(0.0, 0.0);
     for (int e = tid; e < vol; e += blockDim.x) {
       T.nlo[e] = z2;
@@ -1771,12 +1769,6 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     T.ok = b[6] && (g.ga_dim[2] & 1) == 0 && (g.ga_lo[2] & 1) == 0;
     T.pitch = tile_pitch(T.dim[2]);
   }
-  // the owner table is not used by the G2P half: clear it while the
-  // velocity staging is in flight (tile_bulk_stage_issue's barrier orders it
-  // before any P2G use)
-  const bool early_zero = kLookahead && g.early_zero != 0 && gel_block;
-  if (early_zero)
-    for (int e = threadIdx.x; e < kTileCap; e += blockDim.x) T.owner[e] = -1;
   pdl_wait();
   TRACE_MARK(1);
   if (!gel_block) {
@@ -1860,17 +1852,6 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
   if (kLookahead) {
     static_assert(!kLookahead || kAdvect, "the look-ahead scatter follows an advect");
     // particle_to_grid of substep s + 1 with the state just written.
-    if (early_zero) {
-      // every gather from the staged tile is done: clear the node halves of
-      // the whole tile now, so the stores drain while the payload (det F,
-      // polar, stress) is computed
-      __syncthreads();
-      const double2 z2 = make_double2(0.0, 0.0);
-      for (int e = threadIdx.x; e < kTileCap; e += blockDim.x) {
-        T.nlo[e] = z2;
-        T.nhi[e] = z2;
-      }
-    }
     P2GPayload q;
     double J = 1.0;
     bool go = active;
@@ -1885,9 +1866,23 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     TRACE_MARK(4);
     // advect's motion reductions, min det F of s + 1 and the tile box together
     block_motion_box(T, ctl, s, active, v2, px0, px1, px2, go, J, q.st.base);
-    p2g_tile_scatter<kDet>(T, go, q, m, g, grid, cta, true, ctl, s + 1, early_zero);
+    p2g_tile_scatter<kDet>(T, go, q, m, g, grid, cta, true, ctl, s + 1);
   }
   TRACE_END();
+}
+
+// A copy of the control block (the pipelined frames' snapshot, taken in
+// stream order right after the frame's capture).
+__global__ void k_snapshot_ctl(const Ctl* __restrict__ ctl, Ctl* __restrict__ out) {
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ctl);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(out);
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(Ctl) / 8); i += blockDim.x) dst[i] = src[i];
+}
+
+int launch_snapshot_ctl(DeviceSim& s, Ctl* out) {
+  k_snapshot_ctl<<<1, 64, 0, s.stream>>>(s.ctl, out);
+  s.kernel_launches += 1;
+  return 1;
 }
 
 // Phase-API pieces (engine.cpp:254-286).
