@@ -1426,7 +1426,7 @@ __global__ void k_ind_catchup(double* __restrict__ x, int64_t n, int64_t n_el,
 // (pending advects applied on the fly, as the walks do).
 __device__ void ind_walk_fixup(const FinFix& fx, const double* __restrict__ x, int64_t n,
                                int64_t n_el, const int64_t* __restrict__ col_start, int n_cols,
-                               const uint8_t* __restrict__ moves, const Ctl* ctl,
+                               const uint8_t* __restrict__ moves, Ctl* ctl,
                                const Geometry& g, double* __restrict__ mi) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int target = fx.s - ctl->chain_start + 1;
@@ -1446,14 +1446,14 @@ __device__ void ind_walk_fixup(const FinFix& fx, const double* __restrict__ x, i
       if (!walk_contrib(g, st, fx.elo, fx.ehi)) continue;
       if (fx.old_ok && walk_contrib(g, st, fx.wlo, fx.whi)) continue;  // the walk had it
       if (!stencil_in_alloc(g, st.base)) {
-        raise(const_cast<Ctl*>(ctl), kErrRegrow, fx.s + 1);
+        raise(ctl, kErrRegrow, fx.s + 1);
         continue;
       }
 #pragma unroll
       for (int i = 0; i < 27; ++i) {
         const int ia = i / 9, ib = (i / 3) % 3, ic = i % 3;
         mi_add(g, mi + node_index(g, st.base[0] + ia, st.base[1] + ib, st.base[2] + ic),
-               st.w[0][ia] * st.w[1][ib] * st.w[2][ic], const_cast<Ctl*>(ctl));
+               st.w[0][ia] * st.w[1][ib] * st.w[2][ic], ctl);
       }
     }
   }
