@@ -170,9 +170,17 @@ class WriterPool {
   std::exception_ptr error_;
 };
 
+// One object's indenter cloud, shared by its positions: sampled on the
+// device for a generated shape (f3), else generated / loaded on the host.
+struct ObjectCloud {
+  std::shared_ptr<host::DeviceCloud> dev;
+  std::vector<V3> host;
+  size_t size() const { return dev ? host::device_cloud_size(*dev) : host.size(); }
+};
+
 struct PositionJob {
   std::string object;
-  std::shared_ptr<const std::vector<V3>> cloud;
+  std::shared_ptr<ObjectCloud> cloud;
   int position_index;
   double offset_x_m, offset_y_m;
 };
@@ -300,13 +308,13 @@ DatasetResult run_press_dataset(const std::string& cfg_json, const fs::path& out
   std::vector<ManifestRow>& kept = resume.kept;
   const auto& done = resume.complete;
 
-  // Jobs: every object at every press-grid position; one cloud per object,
-  // generated on host threads in parallel (rejection sampling of 1e6 points
-  // per object, harness.cpp:194-195 shares it across positions).
+  // Jobs: every object at every press-grid position; one cloud per object
+  // (harness.cpp:194-195 shares it across positions): generated shapes are
+  // sampled on the device, point-cloud files are read on host threads.
   const double step_m = cfg.step_mm * 1e-3;
   std::vector<PositionJob> jobs;
   size_t skipped = 0;
-  std::map<std::string, std::shared_ptr<std::vector<V3>>> clouds;
+  std::map<std::string, std::shared_ptr<ObjectCloud>> clouds;
   for (const std::string& object : cfg.objects)
     for (int py = 0; py < cfg.positions_y; ++py)
       for (int px = 0; px < cfg.positions_x; ++px) {
@@ -316,7 +324,7 @@ DatasetResult run_press_dataset(const std::string& cfg_json, const fs::path& out
           continue;
         }
         auto& cloud = clouds[object];
-        if (!cloud) cloud = std::make_shared<std::vector<V3>>();
+        if (!cloud) cloud = std::make_shared<ObjectCloud>();
         jobs.push_back({object, cloud, index, (px - 0.5 * (cfg.positions_x - 1)) * step_m,
                         (py - 0.5 * (cfg.positions_y - 1)) * step_m});
       }
@@ -325,13 +333,15 @@ DatasetResult run_press_dataset(const std::string& cfg_json, const fs::path& out
     std::vector<std::exception_ptr> errs(clouds.size());
     size_t k = 0;
     for (auto& [object, cloud] : clouds) {
-      gen.emplace_back([&cfg, object = object, cloud = cloud, &errs, k] {
-        try {
-          *cloud = host::indenter_cloud_for(cfg, object);
-        } catch (...) {
-          errs[k] = std::current_exception();
-        }
-      });
+      cloud->dev = host::device_cloud_for_object(device, cfg, object);
+      if (!cloud->dev)
+        gen.emplace_back([&cfg, object = object, cloud = cloud, &errs, k] {
+          try {
+            cloud->host = host::indenter_cloud_for(cfg, object);
+          } catch (...) {
+            errs[k] = std::current_exception();
+          }
+        });
       ++k;
     }
     for (auto& t : gen) t.join();
@@ -370,7 +380,9 @@ DatasetResult run_press_dataset(const std::string& cfg_json, const fs::path& out
       for (size_t i = 0; i < nb; ++i) {
         const PositionJob& job = jobs[b0 + i];
         const std::vector<V3> placed =
-            host::place_for_press(cfg, *job.cloud, job.offset_x_m, job.offset_y_m);
+            job.cloud->dev
+                ? host::place_for_press_on(*job.cloud->dev, cfg, job.offset_x_m, job.offset_y_m)
+                : host::place_for_press(cfg, job.cloud->host, job.offset_x_m, job.offset_y_m);
         check(host::build_sim_from(device, cfg, placed, &sims[i].h));
         hs[i] = sims[i].h;
       }

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -88,6 +89,18 @@ std::string to_json_string(const Config& c);
 std::vector<V3> indenter_cloud_for(const Config& c, const std::string& object);
 std::vector<V3> place_for_press(const Config& c, const std::vector<V3>& cloud, double off_x,
                                 double off_y);
+
+// Episode setup on the device (setup_kernels.cu, §8 row f3): a generated
+// indenter cloud (indenter_cloud_for) in device memory, shared by the
+// placements of one object; null when the object is a point-cloud file or
+// TACCHI_HOST_SETUP=1 selects the host restatement.
+struct DeviceCloud;
+std::shared_ptr<DeviceCloud> device_cloud_for_object(int device, const Config& c,
+                                                     const std::string& object);
+// place_for_press (scene_builder.cpp:48-61) of a device cloud -> host points.
+std::vector<V3> place_for_press_on(const DeviceCloud& dc, const Config& c, double off_x,
+                                   double off_y);
+size_t device_cloud_size(const DeviceCloud& dc);
 
 // sim::build_sim (scene_builder.cpp:63-78) from an already placed indenter.
 int build_sim_from(int device, const Config& c, const std::vector<V3>& placed, tg_handle* out);

@@ -673,6 +673,22 @@ std::vector<V3> device_place(const DeviceCloud& dc, const Config& c, double off_
   return out;
 }
 
+std::shared_ptr<DeviceCloud> device_cloud_for_object(int device, const Config& c,
+                                                     const std::string& object) {
+  const std::string shape = generated_shape_of(c, object);
+  if (shape.empty() || !device_setup_enabled()) return nullptr;
+  auto dc = std::make_shared<DeviceCloud>();
+  device_cloud_for(device, c, shape, *dc);
+  return dc;
+}
+
+std::vector<V3> place_for_press_on(const DeviceCloud& dc, const Config& c, double off_x,
+                                   double off_y) {
+  return device_place(dc, c, off_x, off_y);
+}
+
+size_t device_cloud_size(const DeviceCloud& dc) { return static_cast<size_t>(dc.n); }
+
 // placed_indenter for a simulation on `device`: generated shapes are sampled
 // and placed on the GPU, point-cloud files on the host.
 std::vector<V3> placed_indenter_on(int device, const Config& c, const std::string& object,

@@ -101,3 +101,22 @@ def test_bench_spawns_ranks_itself():
     line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["episodes_per_rank"] == [512, 512]
     assert line["max_ms"] == 11.0  # rank 1's synthetic time wins
+
+
+def test_config4_cpu_baseline_harness_pattern():
+    """bench.py's config-4 CPU baseline runs the reference's harness pattern
+    (harness.cpp:206-237: a worker per host core, each simulation on one
+    thread) over config-4 episodes; here on 2 episodes x 1 frame."""
+    import os
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from oracle import refpy
+
+    if not refpy.available():
+        pytest.skip("oracle/_ref not built")
+    import bench
+
+    value, threads, k = bench._harness_pattern(1, 2)
+    assert value > 0 and threads >= 1 and k == 2
