@@ -1040,6 +1040,15 @@ struct tg_sim : DeviceSim {};
 
 static DeviceSim* H(tg_handle h) { return static_cast<DeviceSim*>(reinterpret_cast<void*>(h)); }
 
+// Pipelined frames own the handle until they are waited for.
+static int in_flight(tg_handle h, const char* who) {
+  const DeviceSim& s = *H(h);
+  if (s.frames_submitted != s.frames_collected)
+    return fail(TG_ERR_INVALID_ARGUMENT,
+                std::string(who) + ": pipelined frames are in flight; tg_step_capture_wait first");
+  return TG_OK;
+}
+
 extern "C" {
 
 const char* tg_last_error(void) { return g_last_error.c_str(); }
@@ -1058,6 +1067,7 @@ void tg_destroy(tg_handle h) { delete H(h); }
 
 int tg_step(tg_handle h, const double v[3], int n) {
   if (!h || !v) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step: null argument");
+  if (const int rc = in_flight(h, "tg_step")) return rc;
   if (H(h)->keep_grid) return tacchi_b200::step(*H(h), v, n);
   // The per-call indenter move counters are 8-bit: long calls run in chunks
   // (identical results; one extra host sync per 200 substeps).
@@ -1072,6 +1082,7 @@ int tg_step(tg_handle h, const double v[3], int n) {
 
 int tg_phase(tg_handle h, int phase, const double v[3]) {
   if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_phase: null handle");
+  if (const int rc = in_flight(h, "tg_phase")) return rc;
   const double zero[3] = {0, 0, 0};
   return tacchi_b200::phase(*H(h), phase, v ? v : zero);
 }
@@ -1081,11 +1092,13 @@ int64_t tg_num_elastomer(tg_handle h) { return h ? H(h)->n_el : 0; }
 
 int tg_download(tg_handle h, double* x, double* v, double* C, double* F) {
   if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_download: null handle");
+  if (const int rc = in_flight(h, "tg_download")) return rc;
   return tacchi_b200::download(*H(h), x, v, C, F);
 }
 
 int tg_upload(tg_handle h, const double* x, const double* v, const double* C, const double* F) {
   if (!h) return fail(TG_ERR_INVALID_ARGUMENT, "tg_upload: null handle");
+  if (const int rc = in_flight(h, "tg_upload")) return rc;
   return tacchi_b200::upload(*H(h), x, v, C, F, false);
 }
 
@@ -1150,6 +1163,7 @@ int tg_download_grid(tg_handle h, const int lo[3], const int hi[3], double* mass
 
 int tg_capture(tg_handle h, const tg_render* r, double* depth_out, uint8_t* rgb_out) {
   if (!h || !r) return fail(TG_ERR_INVALID_ARGUMENT, "tg_capture: null argument");
+  if (const int rc = in_flight(h, "tg_capture")) return rc;
   DeviceSim& s = *H(h);
   cudaSetDevice(s.device);
   std::string msg;
@@ -1171,6 +1185,7 @@ int tg_capture_buffers(tg_handle h, const tg_render* r, double** depth, uint8_t*
 int tg_step_capture(tg_handle h, const double v[3], int n, const tg_render* r, double* depth_out,
                     uint8_t* rgb_out) {
   if (!h || !v || !r) return fail(TG_ERR_INVALID_ARGUMENT, "tg_step_capture: null argument");
+  if (const int rc = in_flight(h, "tg_step_capture")) return rc;
   DeviceSim& s = *H(h);
   if (s.keep_grid) {  // the step ends on the phase path; capture afterwards
     const int rc = tacchi_b200::step(s, v, n);
@@ -1259,8 +1274,10 @@ static int many(tg_handle* hs, int n_handles, const double* velocities, int n_su
     return fail(TG_ERR_INVALID_ARGUMENT, std::string(who) + ": null argument");
   if (n_substeps < 0 || n_substeps > 200)
     return fail(TG_ERR_INVALID_ARGUMENT, std::string(who) + ": n_substeps outside [0, 200]");
-  for (int i = 0; i < n_handles; ++i)
+  for (int i = 0; i < n_handles; ++i) {
     if (!hs[i]) return fail(TG_ERR_INVALID_ARGUMENT, std::string(who) + ": null handle");
+    if (const int rc = in_flight(hs[i], who)) return rc;
+  }
   std::vector<int> rc(n_handles, TG_OK), crc(n_handles, TG_OK);
   std::vector<std::string> msg(n_handles);
   std::vector<char> submitted(n_handles, 0), stepped(n_handles, 0);

@@ -953,7 +953,12 @@ def test_pipelined_step_capture_matches_synchronous(tb):
     for (d, im), (dr, imr) in zip(got, ref):
         np.testing.assert_allclose(d, dr, rtol=0, atol=1e-12)
         assert np.abs(im.astype(int) - imr).max() <= 1
-    assert a.step_count == b.step_count == 60
+    t_open = tb.sim.step_capture_submit(a, SMALL_V, 10, rp, read_back=False)
+    with pytest.raises(tb.InvalidArgument):  # the handle is busy while frames are in flight
+        tb.mpm.step(a, SMALL_V, 1)
+    assert tb.sim.step_capture_wait(a, t_open, rp) == (None, None)
+    tb.mpm.step(b, SMALL_V, 10)
+    assert a.step_count == b.step_count == 70
     # an error in frame k: reported at its wait and at the next frame's
     x = a.positions()
     x[-1, 2] = (64 - 3) * (12e-3 / 64) + 0.49 * (12e-3 / 64)
