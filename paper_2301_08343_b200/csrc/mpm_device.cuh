@@ -156,6 +156,19 @@ static __device__ __noinline__ void polar_rotation_svd(const double* F, double* 
   matmul3(U, Vt, R);
 }
 
+// The SVD fallback through private copies: the caller's F and R arrays never
+// have their address taken, so they stay in registers on the hot path (a
+// noinline callee taking them directly forced both into local memory for
+// every particle).
+__device__ __forceinline__ void polar_svd_fallback(const double* F, double* R) {
+  double f[9], r[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) f[i] = F[i];
+  polar_rotation_svd(f, r);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = r[i];
+}
+
 // material.cpp:27-81 — scaled Newton iteration R <- (g R + R^-T / g) / 2 with
 // the cofactor inverse; <= 40 iterations, stop when the max step < 1e-13;
 // SVD fallback for a vanishing determinant or no convergence. Caller has
@@ -175,7 +188,7 @@ __device__ __forceinline__ void polar_rotation(const double* F, double* R) {
     const double c21 = r02 * r10 - r00 * r12;
     const double c22 = r00 * r11 - r01 * r10;
     const double d = r00 * c00 + r01 * c01 + r02 * c02;
-    if (!(fabs(d) > 1e-300)) { polar_rotation_svd(F, R); return; }
+    if (!(fabs(d) > 1e-300)) { polar_svd_fallback(F, R); return; }
     const double g = fabs(d - 1.0) > 1e-2 ? 1.0 / cbrt(fabs(d)) : 1.0;
     const double hg = 0.5 * g;
     const double hd = 0.5 / (g * d);
@@ -201,7 +214,7 @@ __device__ __forceinline__ void polar_rotation(const double* F, double* R) {
       return;
     }
   }
-  polar_rotation_svd(F, R);
+  polar_svd_fallback(F, R);
 }
 
 // corotated_stress (material.cpp:83-89) given R = polar_rotation(F) and
