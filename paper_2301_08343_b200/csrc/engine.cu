@@ -316,6 +316,7 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   if (const char* f = std::getenv("TACCHI_FULL_INDENTER")) s->full_indenter = std::atoi(f) != 0;
   // launch-shape A/B switches (tools/README.md); defaults are the measured best
   s->zpad = 2;
+  if (const char* e = std::getenv("TACCHI_AB_NO_WALKS")) s->ab_no_walks = std::atoi(e) != 0;
   if (const char* e = std::getenv("TACCHI_ZPAD")) s->zpad = std::max(2, std::atoi(e) & ~1);
   g.gu_bps = 10;
   g.pdl_early = 1;

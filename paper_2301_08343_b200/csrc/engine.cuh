@@ -160,6 +160,7 @@ struct DeviceSim {
                              // path so the grid afterwards is the reference's (engine.cpp:288-297)
   int regrows = 0;            // node-array reallocations so far
   int zpad = 2;               // allocation z-row length multiple (TACCHI_ZPAD)
+  bool ab_no_walks = false;   // TACCHI_AB_NO_WALKS: timing A/B only (wrong physics)
   int resume_substeps = 0;    // after kResume: substeps of the call still to run
   bool grid_ref = true;      // the node arrays hold the reference's Grid state (not a
                              // fused look-ahead): tg_download_grid may read them

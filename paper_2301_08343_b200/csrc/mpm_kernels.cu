@@ -2199,7 +2199,8 @@ int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter) {
   IndArgs ia{};
   unsigned extra = 0;
   if (with_indenter) {  // the indenter's look-ahead column walks ride along
-    extra = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
+    // (TACCHI_AB_NO_WALKS: A/B timing only, the indenter then scatters nothing)
+    extra = s.ab_no_walks ? 0u : static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
     const int gel = static_cast<int>(gel_blocks(s));
     const bool ind_first = s.geo.ind_first != 0;
     ia = IndArgs{s.col_start, s.ind_moves, s.grid_mi, s.n_cols, gel,
