@@ -29,7 +29,7 @@ def test_mirror_demo_setup_grid_and_capture():
     assert abs(r["grid_mass"] - r["total_mass"]) <= 1e-10 * r["total_mass"]
     lo, hi = r["window"][:3], r["window"][3:]
     assert all(h > l for l, h in zip(lo, hi))
-    assert r["image"] == [640, 480] and r["max_depth_m"] > 0.0
+    assert r["image"] == [160, 120] and r["max_depth_m"] > 0.0
 
 
 def test_press_demo_session_loop():

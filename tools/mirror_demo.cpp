@@ -23,6 +23,7 @@ int main() {
         "{\"elastomer\": {\"size_mm\": [6, 6, 1.2], \"particle_counts\": [31, 31, 7]},"
         " \"grid\": {\"nodes_per_axis\": [64, 64, 64], \"edge_mm\": 12.0},"
         " \"time\": {\"dt_s\": 2e-6},"
+        " \"render\": {\"image_width\": 160, \"image_height\": 120},"
         " \"indenter\": {\"generated_shape\": \"sphere2\", \"source_points\": 20000,"
         " \"target_points\": 3000, \"gap_mm\": 0.02}}";
     int64_t n = 0;
