@@ -969,3 +969,33 @@ def test_pipelined_step_capture_matches_synchronous(tb):
         tb.sim.step_capture_wait(a, t1, rp)
     with pytest.raises(tb.OutOfGrid):
         tb.sim.step_capture_wait(a, t2, rp)
+
+
+def test_pipelined_frames_across_a_regrow(tb):
+    """A pipelined frame whose scatter outgrows the node arrays (the scene
+    translating 3.2 cells per substep) is finished after the regrow and the
+    frame submitted behind it is replayed: the frames equal the synchronous
+    ones."""
+    rp = tb.render_params(SMALL, "")
+    sims = [tb.sim.build_sim(SMALL), tb.sim.build_sim(SMALL)]
+    vfast = (300.0, -120.0, 0.0)
+    for s in sims:
+        tb.mpm.step(s, SMALL_V, 4)
+        v = s.state()["v"]
+        v[:] += np.array(vfast)
+        v[s.elastomer_count:] = vfast
+        s.set_state(v=v)
+    a, b = sims
+    before = a.stats()["regrows"]
+    t1 = tb.sim.step_capture_submit(a, vfast, 2, rp)
+    t2 = tb.sim.step_capture_submit(a, vfast, 1, rp)
+    d1, i1 = (x.copy() for x in tb.sim.step_capture_wait(a, t1, rp))
+    d2, i2 = (x.copy() for x in tb.sim.step_capture_wait(a, t2, rp))
+    r1 = tb.sim.step_capture(b, vfast, 2, params=rp)
+    r2 = tb.sim.step_capture(b, vfast, 1, params=rp)
+    assert a.stats()["regrows"] > before
+    np.testing.assert_allclose(d1, r1[0], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(d2, r2[0], rtol=0, atol=1e-12)
+    assert np.abs(i2.astype(int) - r2[1]).max() <= 1
+    assert a.step_count == b.step_count == 7
+    assert np.abs(a.positions() - b.positions()).max() <= 1e-12
