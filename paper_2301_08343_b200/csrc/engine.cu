@@ -1018,9 +1018,9 @@ int frame_wait(DeviceSim& s, int64_t ticket, double** depth, uint8_t** rgb) {
       next.status = rc;
       next.msg = std::string("an earlier pipelined frame failed: ") + g_last_error;
     }
-  } else {
-    s.host_substep = f.ctl->substep;
   }
+  // (on success the host's substep count was already advanced at submit: a
+  // later frame may be in flight, so it is not reset from this snapshot)
   if (rc) return rc;
   if (depth) *depth = f.read_back ? f.depth : nullptr;
   if (rgb) *rgb = f.read_back ? f.rgb : nullptr;

@@ -1312,14 +1312,32 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
   double d[3] = {0, 0, 0};
   for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
   const int64_t a0 = col_start[c], a1 = col_start[c + 1];
+  // the chunk's loads are issued one chunk ahead (most columns take two or
+  // three chunks; each was a dependent DRAM round trip)
+  double nx = 0, ny = 0, nz = 0;
+  int ndone = 0;
+  if (a0 + lane < a1) {
+    const int64_t p = a0 + lane;
+    nx = __ldcs(x + p);
+    ny = __ldcs(x + n + p);
+    nz = __ldcs(x + 2 * n + p);
+    ndone = moves[p - n_el];
+  }
   for (int64_t b0 = a0; b0 < a1; b0 += 32) {
     const int64_t p = b0 + lane;
     const bool valid = p < a1;
+    double px = nx, py = ny, pz = nz;
+    const int done = ndone;
+    if (b0 + 32 + lane < a1) {
+      const int64_t q = b0 + 32 + lane;
+      nx = __ldcs(x + q);
+      ny = __ldcs(x + n + q);
+      nz = __ldcs(x + 2 * n + q);
+      ndone = moves[q - n_el];
+    }
     Stencil st;
     bool beyond = false, contrib = false, moved = false;
     if (valid) {
-      double px = __ldcs(x + p), py = __ldcs(x + n + p), pz = __ldcs(x + 2 * n + p);
-      const int done = moves[p - n_el];
       moved = done < target;
       if (moved) {
         for (int k = done; k < target; ++k) {
