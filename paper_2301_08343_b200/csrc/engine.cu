@@ -28,6 +28,7 @@ int launch_g2p2g_gel(DeviceSim& s, bool lookahead, bool with_indenter = false);
 int launch_ind_move(DeviceSim& s, bool lookahead);
 int launch_finalize_step(DeviceSim& s, bool walk_fix = false);
 int launch_snapshot_ctl(DeviceSim& s, Ctl* out);
+int launch_ind_walks_on(DeviceSim& s, cudaStream_t st);
 int launch_chain_begin(DeviceSim& s);
 int launch_ind_cols(DeviceSim& s, bool move);
 int launch_ind_catchup(DeviceSim& s);
@@ -103,6 +104,10 @@ DeviceSim::~DeviceSim() {
   cudaFreeHost(h_vind);
   cudaFreeHost(h_depth_pinned);
   cudaFreeHost(h_rgb_pinned);
+  if (walk_stream) cudaStreamSynchronize(walk_stream);
+  if (walk_stream) cudaStreamDestroy(walk_stream);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   if (copy_stream) cudaStreamSynchronize(copy_stream);
   for (FrameSlot& f : frames) {
     cudaFreeHost(f.depth);
@@ -169,10 +174,11 @@ static bool alloc_grid(DeviceSim& s, const int lo[3], const int dim[3]) {
   const size_t bz = ((n + 2) * sizeof(double) + 255) & ~size_t(255);
   const size_t b1 = n * sizeof(double);
   void* slab = nullptr;
-  if (cudaMalloc(&slab, 3 * b2 + bz + b1) != cudaSuccess) return false;
+  if (cudaMalloc(&slab, 3 * b2 + bz + 2 * b1) != cudaSuccess) return false;  // M_I x 2
   cudaFree(s.grid_slab);
   s.grid_slab = slab;
-  s.grid_slab_bytes = 3 * b2 + bz + b1;
+  s.grid_slab_bytes = 3 * b2 + bz + 2 * b1;
+  s.geo.mi_stride = n;
   s.n_nodes = n;
   for (int a = 0; a < 3; ++a) {
     s.geo.ga_lo[a] = lo[a];
@@ -372,6 +378,12 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
     col_starts = {n_el, n};
   }
   cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (const char* e = std::getenv("TACCHI_WALKS")) s->fork_walks = std::string(e) != "fused";
+  if (s->fork_walks &&
+      (cudaStreamCreateWithFlags(&s->walk_stream, cudaStreamNonBlocking) != cudaSuccess ||
+       cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess))
+    s->fork_walks = false;
   // Node arrays over the elastomer's node box plus the walks' reach (the
   // step path touches nothing else); the whole window when there is no
   // elastomer. They grow on demand (ensure_alloc).
@@ -546,6 +558,21 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
 // chain without a standalone scatter.
 // One substep of the step path.
 static int record_substep(DeviceSim& s, int sms, bool cols) {
+  if (cols && s.n_el > 0 && s.fork_walks && s.walk_stream) {
+    // the walks of substep s need only the previous finalize (box, chain),
+    // the indenter's own state and M_I buffer (s + 1) & 1: fork them beside
+    // grid_update and the elastomer kernel, join before this finalize (which
+    // completes them if the elastomer left their box)
+    cudaEventRecord(s.ev_fork, s.stream);
+    cudaStreamWaitEvent(s.walk_stream, s.ev_fork, 0);
+    int k = launch_ind_walks_on(s, s.walk_stream);
+    cudaEventRecord(s.ev_join, s.walk_stream);
+    k += launch_grid_update(s, sms, true);
+    k += launch_g2p2g_gel(s, true, false);
+    cudaStreamWaitEvent(s.stream, s.ev_join, 0);
+    k += launch_finalize_step(s, true);
+    return k;
+  }
   int k = launch_grid_update(s, sms, true);
   if (cols && s.n_el > 0) {
     // the indenter's column walks run as extra blocks of the elastomer kernel

@@ -40,6 +40,10 @@ struct Ctl {
   int box_lo[2][3], box_hi[2][3];         // per-material node boxes (elastomer, indenter)
   double vind[3];                         // commanded indenter velocity
   double ind_v[3];                        // uniform indenter velocity (P2G input)
+  double ind_vp[2][3];                    // the indenter velocity of the M_I scatter of
+                                          // substep s, slot s & 1 (grid_update's input)
+  int mi_last;                            // substep of the last phase-path P2G (its M_I buffer)
+  int pad1;
   int chain_start;                        // first substep of the open indenter chain
   double diag_min_det_f, diag_max_speed;  // StepDiagnostics
   long long step_count;                   // SimState::step_count
@@ -76,6 +80,10 @@ struct Geometry {
   // both scales are powers of two.
   int det;
   double fx_s, fx_inv, fxi_s, fxi_inv;
+  // M_I is double-buffered by substep parity (the walks of substep s scatter
+  // into buffer (s + 1) & 1 while grid_update consumes buffer s & 1): the
+  // second buffer starts mi_stride doubles after the first.
+  size_t mi_stride;
 };
 
 // A dense node array in split layout: two 16-byte halves per node in two
@@ -161,6 +169,12 @@ struct DeviceSim {
   int regrows = 0;            // node-array reallocations so far
   int zpad = 2;               // allocation z-row length multiple (TACCHI_ZPAD)
   bool ab_no_walks = false;   // TACCHI_AB_NO_WALKS: timing A/B only (wrong physics)
+  // The indenter's look-ahead walks: extra blocks of the elastomer kernel, or
+  // (fork_walks) a kernel of their own on a forked stream, beside grid_update
+  // and the elastomer kernel (TACCHI_WALKS=fork|fused)
+  bool fork_walks = true;
+  cudaStream_t walk_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int resume_substeps = 0;    // after kResume: substeps of the call still to run
   bool grid_ref = true;      // the node arrays hold the reference's Grid state (not a
                              // fused look-ahead): tg_download_grid may read them

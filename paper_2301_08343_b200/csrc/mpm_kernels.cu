@@ -189,6 +189,11 @@ __device__ __forceinline__ size_t node_index(const Geometry& g, int i, int j, in
          (k - g.ga_lo[2]);
 }
 
+// The M_I buffer of substep s (double-buffered by parity, Geometry::mi_stride).
+__device__ __forceinline__ double* mi_at(const Geometry& g, double* mi, int s) {
+  return mi + static_cast<size_t>(s & 1) * g.mi_stride;
+}
+
 // The node box [lo, hi) lies inside the node arrays' allocation box.
 __device__ __forceinline__ bool box_in_alloc(const Geometry& g, int l0, int l1, int l2, int h0,
                                              int h1, int h2) {
@@ -975,6 +980,8 @@ __device__ void finalize_warp(Ctl* ctl, const Geometry& g, int mode, FinFix& fx)
 // (engine.cpp:72-83).
 __global__ void k_clear(NodeBuf grid, double* __restrict__ mi, VelBuf vel, Ctl* ctl, Geometry g) {
   if (stale(ctl, ctl->substep)) return;
+  // both M_I buffers: the phase path's grid_update leaves its M_I in place,
+  // and the next substep's look-ahead scatter goes into the other one
   // (the host grows the allocation over the window before the phase path
   // runs; clamped so a stale box can never index outside it)
   const int lx = max(ctl->clr_lo[0], g.ga_lo[0]), ly = max(ctl->clr_lo[1], g.ga_lo[1]),
@@ -994,6 +1001,7 @@ __global__ void k_clear(NodeBuf grid, double* __restrict__ mi, VelBuf vel, Ctl* 
     grid.lo[nd] = z;
     grid.hi[nd] = z;
     mi[nd] = 0.0;
+    mi[g.mi_stride + nd] = 0.0;
     vel.xy[nd] = z;
     vel.z[nd] = 0.0;
   }
@@ -1095,12 +1103,15 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
   if (stale(ctl, s)) return;  // stable: nothing raises for substep s while this runs
   const int tid = threadIdx.x;
   const int64_t gt = static_cast<int64_t>(blockIdx.x) * kIndThreads + tid;
-  if (kMove && gt == 0) {
+  const int s_scatter = kMove ? s + 1 : s;
+  mi = mi_at(g, mi, s_scatter);
+  if (gt == 0) {
     // apply_boundary: every indenter velocity becomes the command
-    // (engine.cpp:260-261); the next grid_update uses it as M_I's velocity.
-    ctl->ind_v[0] = ctl->vind[0];
-    ctl->ind_v[1] = ctl->vind[1];
-    ctl->ind_v[2] = ctl->vind[2];
+    // (engine.cpp:260-261); M_I's velocity for grid_update of s_scatter
+    for (int a = 0; a < 3; ++a) {
+      if (kMove) ctl->ind_v[a] = ctl->vind[a];
+      if (kScatter) ctl->ind_vp[s_scatter & 1][a] = kMove ? ctl->vind[a] : ctl->ind_v[a];
+    }
   }
   // Coalesced move: the warp's 32 * kIndK consecutive particles, lane l
   // touching elements l + 32 i; then a register transpose (shuffles) gives
@@ -1165,7 +1176,7 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
     make_stencil(px[j], py[j], pz[j], g.origin, g.inv_dx, st);
     if (!stencil_in_grid(g, st)) continue;  // finalize raises OutOfGrid
     if (!stencil_in_alloc(g, st.base)) {    // the host grows the allocation
-      raise(ctl, kErrRegrow, kMove ? s + 1 : s);
+      raise(ctl, kErrRegrow, s_scatter);
       continue;
     }
     if (have && (st.base[0] != cb[0] || st.base[1] != cb[1] || st.base[2] != cb[2])) {
@@ -1284,10 +1295,13 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
                                                const Geometry& g, double* __restrict__ mi,
                                                int box_mode, int s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (kMove && blk == 0 && threadIdx.x == 0) {
-    ctl->ind_v[0] = ctl->vind[0];  // apply_boundary (engine.cpp:260-261)
-    ctl->ind_v[1] = ctl->vind[1];
-    ctl->ind_v[2] = ctl->vind[2];
+  const int s_scatter = kMove ? s + 1 : s;
+  mi = mi_at(g, mi, s_scatter);
+  if (blk == 0 && threadIdx.x == 0) {
+    for (int a = 0; a < 3; ++a) {
+      if (kMove) ctl->ind_v[a] = ctl->vind[a];  // apply_boundary (engine.cpp:260-261)
+      ctl->ind_vp[s_scatter & 1][a] = kMove ? ctl->vind[a] : ctl->ind_v[a];
+    }
   }
   const int c = blk * kColWarps + warp;
   if (c >= n_cols) return;  // warp-uniform; only __syncwarp below
@@ -1448,6 +1462,7 @@ __device__ void ind_walk_fixup(const FinFix& fx, const double* __restrict__ x, i
                                const Geometry& g, double* __restrict__ mi) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int target = fx.s - ctl->chain_start + 1;
+  mi = mi_at(g, mi, fx.s + 1);
   double d[3];
   for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
   for (int c = warp; c < n_cols; c += nw) {
@@ -1593,6 +1608,7 @@ __global__ void k_grid_update_window(NodeBuf mp, double* __restrict__ mi, VelBuf
                                      Ctl* ctl, Geometry g,
                                      double m_ind) {
   if (stale(ctl, ctl->substep)) return;
+  mi = mi_at(g, mi, ctl->substep);
   const int lx = max(ctl->win_lo[0], g.ga_lo[0]), ly = max(ctl->win_lo[1], g.ga_lo[1]),
             lz = max(ctl->win_lo[2], g.ga_lo[2]);
   const int ny = max(min(ctl->win_hi[1], g.ga_lo[1] + g.ga_dim[1]) - ly, 0);
@@ -1614,7 +1630,9 @@ __global__ void __launch_bounds__(256, 5) k_grid_update_boxes(NodeBuf mp, double
   // The elastomer kernel that follows reads its particle state (written two
   // kernels back, complete now) before its own wait: let it launch early.
   if (g.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (stale(ctl, ctl->substep)) return;
+  const int s = ctl->substep;
+  if (stale(ctl, s)) return;
+  mi = mi_at(g, mi, s);
   int lo[2][3], dm[2][3], vol[2];
   for (int m = 0; m < 2; ++m) {  // each box clamped to the allocation (no mass outside)
     vol[m] = 1;
@@ -1624,7 +1642,9 @@ __global__ void __launch_bounds__(256, 5) k_grid_update_boxes(NodeBuf mp, double
       vol[m] *= dm[m][a];
     }
   }
-  const double u0 = ctl->ind_v[0], u1 = ctl->ind_v[1], u2 = ctl->ind_v[2];
+  // the indenter velocity its M_I scatter was made with (the walks of the
+  // previous substep may already be writing the other slot)
+  const double u0 = ctl->ind_vp[s & 1][0], u1 = ctl->ind_vp[s & 1][1], u2 = ctl->ind_vp[s & 1][2];
   const int first = blockIdx.x * blockDim.x + threadIdx.x, step = gridDim.x * blockDim.x;
   auto in_box = [&](int m, int i, int j, int k) {
     return vol[m] > 0 && i >= lo[m][0] && i < lo[m][0] + dm[m][0] && j >= lo[m][1] &&
@@ -1968,6 +1988,7 @@ __global__ void k_ind_boundary(Ctl* ctl) {
 __global__ void k_p2g_done(Ctl* ctl) {
   const int s = ctl->substep;
   if (stale(ctl, s)) return;
+  ctl->mi_last = s;  // the M_I buffer tg_download_grid reads
   ctl->diag_min_det_f = order_val(ctl->min_detf[s & 1]);
   ctl->min_detf[s & 1] = order_key(1.0);
 }
@@ -2001,7 +2022,7 @@ __global__ void k_gather_box(NodeBuf mp, const double* __restrict__ mi, VelBuf v
     const size_t nd = node_index(g, i, j, k);
     const double2 qa = mp.lo[nd], qb = mp.hi[nd];
     double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
-    double wi = mi[nd];
+    double wi = mi[static_cast<size_t>(ctl->mi_last & 1) * g.mi_stride + nd];
     if (g.det) {
       q = make_double4(from_fixed(qa.x, g.fx_inv), from_fixed(qa.y, g.fx_inv),
                        from_fixed(qb.x, g.fx_inv), from_fixed(qb.y, g.fx_inv));
@@ -2271,6 +2292,19 @@ int launch_ind_cols(DeviceSim& s, bool move) {
   else
     k_ind_cols<false><<<blocks, kColWarps * 32, kColSmem, s.stream>>>(
         s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 0);
+  s.ind_v_uniform = true;
+  s.kernel_launches += 1;
+  return 1;
+}
+
+// The look-ahead walks as a kernel of their own on `st` (the forked walk
+// stream of the substep plan): the previous finalize's elastomer box widened
+// by one node, completed by this substep's finalize if the elastomer leaves it.
+int launch_ind_walks_on(DeviceSim& s, cudaStream_t st) {
+  if (s.n_ind <= 0 || s.n_cols <= 0) return 0;
+  const unsigned blocks = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
+  k_ind_cols<true><<<blocks, kColWarps * 32, kColSmem, st>>>(
+      s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 2);
   s.ind_v_uniform = true;
   s.kernel_launches += 1;
   return 1;

@@ -873,6 +873,41 @@ def test_deterministic_reruns_bit_identical(tb):
     assert out[0] == out[1]
 
 
+_WALK_CHILD = r"""
+import hashlib, json, sys
+sys.path.insert(0, %r)
+import paper_2301_08343_b200 as tb
+from tests.scenes import CONFIG2A, CONFIG2A_V
+s = tb.sim.build_sim({**CONFIG2A, "deterministic": True})
+for _ in range(30):
+    tb.mpm.step(s, CONFIG2A_V, 10)
+st = s.state()
+print(json.dumps({k: hashlib.sha1(st[k].tobytes()).hexdigest() for k in ("x", "v", "C", "F")}))
+"""
+
+
+def test_walk_plans_byte_identical():
+    """The indenter's look-ahead walks as extra blocks of the elastomer kernel
+    (TACCHI_WALKS=fused) or as their own kernel on a forked stream
+    (TACCHI_WALKS=fork, the default; double-buffered M_I) scatter the same
+    contributions: in deterministic mode 300 substeps of config 2a give
+    byte-identical particle states (one process per plan: the switch is read
+    at tg_create)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for plan in ("fused", "fork"):
+        p = subprocess.run([sys.executable, "-c", _WALK_CHILD % root], capture_output=True,
+                           text=True, env={**os.environ, "TACCHI_WALKS": plan}, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[plan] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert out["fused"] == out["fork"]
+
+
 @pytest.mark.parametrize("det", [False, True])
 def test_small_scene_both_accumulation_modes_match_reference(tb, golden, det):
     """The fp64 fast mode and the fixed-point deterministic mode both match
