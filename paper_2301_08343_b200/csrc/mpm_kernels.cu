@@ -341,6 +341,7 @@ struct P2GTile {
   double2 nhi[kTileCap];  // {py, pz} / vz rows (as doubles, pitch zp, offset zoff)
   int owner[kTileCap];
   int lo[3], hi[3], dim[3];
+  int blo[3], bhi[3];  // block_motion_box's node box reduction
   int ok;
   int pitch;     // node row pitch (>= dim[2], = 1 mod 8: rows shift the 16-byte bank slot)
   int zp, zoff;  // staged vz: node (row r, column c) at ((double*)nhi)[r * zp + zoff + c]
@@ -552,16 +553,20 @@ __device__ void tile_box(P2GTile& T, bool active, const int* base) {
   __syncthreads();
 }
 
-// The look-ahead kernel's block reductions in one pass (2 barriers instead of
-// the 2 + 4 of reduce_motion + tile_box): advect's max |v|^2 and bbox of x
+// The look-ahead kernel's block reductions: advect's max |v|^2 and bbox of x
 // (engine.cpp:273-282) into the substep-s slots of the control block, the
 // min det F of substep s + 1 (engine.cpp:119,135), and the CTA's P2G node box
-// into T (as tile_box). All threads of the block must call it; the first
-// barrier also retires every earlier reader of T (the G2P gathers).
+// into T (as tile_box). Warps reduce with shuffles; the node box goes into
+// T.blo / T.bhi with shared int atomics (set to the empty box at the
+// kernel's entry); after the first barrier warp w reduces quantity w over the
+// eight warps and issues its one RED into the control block (one per CTA and
+// quantity: per-warp REDs on these eight words measured 83 vs 66 us), and
+// thread 0 derives the tile box. All threads of the block must call it; the
+// first barrier also retires every earlier reader of T (the G2P gathers).
 __device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double v2, double x0,
                                  double x1, double x2, bool go, double J, const int* base) {
-  __shared__ double redd[8][kGelThreads / 32];
-  __shared__ int redi[6][kGelThreads / 32];
+  static_assert(kGelThreads / 32 == 8, "one warp per reduced quantity");
+  __shared__ double redd[8][8];
   double r[8];
   r[0] = moved ? v2 : 0.0;
   r[1] = moved ? x0 : INFINITY;
@@ -584,52 +589,51 @@ __device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double
     bi[3 + a] = __reduce_max_sync(0xffffffffu, go ? base[a] : INT_MIN);
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kWarps = kGelThreads / 32;
   if (lane == 0) {
 #pragma unroll
     for (int a = 0; a < 8; ++a) redd[a][warp] = r[a];
+    if (bi[0] != INT_MAX) {
 #pragma unroll
-    for (int a = 0; a < 6; ++a) redi[a][warp] = bi[a];
+      for (int a = 0; a < 3; ++a) {
+        atomicMin(&T.blo[a], bi[a]);
+        atomicMax(&T.bhi[a], bi[3 + a]);
+      }
+    }
   }
   __syncthreads();
-  if (warp == 0) {
+  {
+    // quantity `warp`: 0 max v^2, 1-3 min x, 4-6 max x, 7 min det F
+    const int q = warp;
+    const double ident = q == 0 ? 0.0 : (q < 4 ? INFINITY : (q < 7 ? -INFINITY : 1.0));
+    double v = lane < 8 ? redd[q][lane] : ident;
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      const double ident = (a == 0) ? 0.0 : (a < 4 ? INFINITY : (a < 7 ? -INFINITY : 1.0));
-      r[a] = lane < kWarps ? redd[a][lane] : ident;
+    for (int o = 4; o > 0; o >>= 1) {
+      const double w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = (q == 0 || (q >= 4 && q < 7)) ? fmax(v, w) : fmin(v, w);
     }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      bi[a] = __reduce_min_sync(0xffffffffu, lane < kWarps ? redi[a][lane] : INT_MAX);
-      bi[3 + a] = __reduce_max_sync(0xffffffffu, lane < kWarps ? redi[3 + a][lane] : INT_MIN);
-    }
-    r[0] = warp_max(r[0]);
-#pragma unroll
-    for (int a = 1; a < 4; ++a) r[a] = warp_min(r[a]);
-#pragma unroll
-    for (int a = 4; a < 7; ++a) r[a] = warp_max(r[a]);
-    r[7] = warp_min(r[7]);
     if (lane == 0) {
-      if (r[1] <= r[4]) {
-        atomicMax(&ctl->max_v2[s & 1], static_cast<unsigned long long>(__double_as_longlong(r[0])));
-        atomicMin(&ctl->bb_lo[s & 1][0], order_key(r[1]));
-        atomicMin(&ctl->bb_lo[s & 1][1], order_key(r[2]));
-        atomicMin(&ctl->bb_lo[s & 1][2], order_key(r[3]));
-        atomicMax(&ctl->bb_hi[s & 1][0], order_key(r[4]));
-        atomicMax(&ctl->bb_hi[s & 1][1], order_key(r[5]));
-        atomicMax(&ctl->bb_hi[s & 1][2], order_key(r[6]));
+      if (q == 0) {
+        if (v > 0.0)
+          atomicMax(&ctl->max_v2[s & 1], static_cast<unsigned long long>(__double_as_longlong(v)));
+      } else if (q < 4) {
+        if (v < INFINITY) atomicMin(&ctl->bb_lo[s & 1][q - 1], order_key(v));
+      } else if (q < 7) {
+        if (v > -INFINITY) atomicMax(&ctl->bb_hi[s & 1][q - 4], order_key(v));
+      } else if (v < 1.0) {
+        atomicMin(&ctl->min_detf[(s + 1) & 1], order_key(v));
       }
-      if (r[7] < 1.0) atomicMin(&ctl->min_detf[(s + 1) & 1], order_key(r[7]));
-      const bool any = bi[0] != INT_MAX;
-      for (int a = 0; a < 3; ++a) {
-        T.lo[a] = bi[a];
-        T.hi[a] = bi[3 + a];
-        T.dim[a] = any ? bi[3 + a] - bi[a] + 3 : 0;
-      }
-      T.pitch = tile_pitch(T.dim[2]);
-      const int rows = T.dim[0] * T.dim[1];
-      T.ok = any && rows * T.pitch <= kTileCap && rows * tile_zpitch(T.dim[2] + 2) <= 2 * kTileCap;
     }
+  }
+  if (threadIdx.x == 0) {
+    const bool any = T.blo[0] != INT_MAX;
+    for (int a = 0; a < 3; ++a) {
+      T.lo[a] = T.blo[a];
+      T.hi[a] = T.bhi[a];
+      T.dim[a] = any ? T.bhi[a] - T.blo[a] + 3 : 0;
+    }
+    T.pitch = tile_pitch(T.dim[2]);
+    const int rows = T.dim[0] * T.dim[1];
+    T.ok = any && rows * T.pitch <= kTileCap && rows * tile_zpitch(T.dim[2] + 2) <= 2 * kTileCap;
   }
   __syncthreads();
 }
@@ -1806,6 +1810,10 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     // vz row staging needs even allocation rows (even start and length in z)
     T.ok = b[6] && (g.ga_dim[2] & 1) == 0 && (g.ga_lo[2] & 1) == 0;
     T.pitch = tile_pitch(T.dim[2]);
+    for (int a = 0; a < 3; ++a) {  // the empty box for block_motion_box
+      T.blo[a] = INT_MAX;
+      T.bhi[a] = INT_MIN;
+    }
   }
   pdl_wait();
   TRACE_MARK(1);
