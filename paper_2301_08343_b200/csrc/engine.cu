@@ -38,6 +38,7 @@ int launch_phase_advect(DeviceSim& s);
 int launch_gather_box(DeviceSim& s, const int lo[3], const int hi[3], double* mass, double* mom,
                       double* vel);
 void configure_gel_tiling(DeviceSim& s, int nx, int ny, int nz);
+void configure_gel_lanes(DeviceSim& s, const double* x_in);
 unsigned gel_block_count(const DeviceSim& s);
 constexpr int kResetAll = 7;
 // capture_kernels.cu
@@ -104,6 +105,7 @@ DeviceSim::~DeviceSim() {
   cudaFreeHost(h_vind);
   cudaFreeHost(h_depth_pinned);
   cudaFreeHost(h_rgb_pinned);
+  if (gel_lanes) cudaFree(gel_lanes);
   if (walk_stream) cudaStreamSynchronize(walk_stream);
   if (walk_stream) cudaStreamDestroy(walk_stream);
   if (ev_fork) cudaEventDestroy(ev_fork);
@@ -475,6 +477,7 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
     // of an nx x ny x nz elastomer lattice.
     const int64_t cols = static_cast<int64_t>(surf->nx) * surf->ny;
     if (n_el % cols == 0) configure_gel_tiling(*s, surf->nx, surf->ny, static_cast<int>(n_el / cols));
+    configure_gel_lanes(*s, in->x);
   }
   // Per-CTA tile boxes carried from each P2G to the next G2P (mpm_kernels.cu).
   const size_t ctas = std::max<size_t>(gel_block_count(*s), 1);
