@@ -38,7 +38,7 @@ int launch_phase_advect(DeviceSim& s);
 int launch_gather_box(DeviceSim& s, const int lo[3], const int hi[3], double* mass, double* mom,
                       double* vel);
 void configure_gel_tiling(DeviceSim& s, int nx, int ny, int nz);
-void configure_gel_lanes(DeviceSim& s, const double* x_in);
+void permute_gel_lanes(DeviceSim& s, const double* x_in);
 unsigned gel_block_count(const DeviceSim& s);
 constexpr int kResetAll = 7;
 // capture_kernels.cu
@@ -105,7 +105,6 @@ DeviceSim::~DeviceSim() {
   cudaFreeHost(h_vind);
   cudaFreeHost(h_depth_pinned);
   cudaFreeHost(h_rgb_pinned);
-  if (gel_lanes) cudaFree(gel_lanes);
   if (walk_stream) cudaStreamSynchronize(walk_stream);
   if (walk_stream) cudaStreamDestroy(walk_stream);
   if (ev_fork) cudaEventDestroy(ev_fork);
@@ -379,6 +378,17 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   } else if (n_ind == 1) {
     col_starts = {n_el, n};
   }
+  // Lattice metadata (particle_set.hpp:16-17): the surface is the top layer
+  // of an nx x ny x nz elastomer lattice; the CTA tiling follows it, and the
+  // elastomer's storage order within each warp's slots is dealt for the
+  // shared-memory banks (permute_gel_lanes, folded into perm).
+  if (surf && surf->particle && surf->nx >= 2 && surf->ny >= 2) {
+    const int64_t cols = static_cast<int64_t>(surf->nx) * surf->ny;
+    if (n_el % cols == 0) {
+      configure_gel_tiling(*s, surf->nx, surf->ny, static_cast<int>(n_el / cols));
+      permute_gel_lanes(*s, in->x);
+    }
+  }
   cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
   if (const char* e = std::getenv("TACCHI_WALKS")) s->fork_walks = std::string(e) != "fused";
   if (s->fork_walks &&
@@ -439,7 +449,7 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
 
   // Tags of the elastomer (Elastomer / ElastomerBottom).
   std::vector<uint8_t> tags(std::max<int64_t>(n_el, 1));
-  for (int64_t p = 0; p < n_el; ++p) tags[p] = in->tag[p];
+  for (int64_t p = 0; p < n_el; ++p) tags[p] = in->tag[s->perm[p]];
   copy_sync(*s, s->tag, tags.data(), n_el, cudaMemcpyHostToDevice);
 
   rc = upload(*s, in->x, in->v, in->C, in->F, true);
@@ -473,11 +483,6 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
       return fail(TG_ERR_CUDA, "tg_create: device allocation failed");
     }
     copy_sync(*s, s->surf_idx, idx.data(), cnt * sizeof(uint32_t), cudaMemcpyHostToDevice);
-    // Lattice metadata (particle_set.hpp:16-17): the surface is the top layer
-    // of an nx x ny x nz elastomer lattice.
-    const int64_t cols = static_cast<int64_t>(surf->nx) * surf->ny;
-    if (n_el % cols == 0) configure_gel_tiling(*s, surf->nx, surf->ny, static_cast<int>(n_el / cols));
-    configure_gel_lanes(*s, in->x);
   }
   // Per-CTA tile boxes carried from each P2G to the next G2P (mpm_kernels.cu).
   const size_t ctas = std::max<size_t>(gel_block_count(*s), 1);
@@ -903,8 +908,8 @@ int download(DeviceSim& s, double* x, double* v, double* Cm, double* Fm) {
       buf.resize(9 * s.n_el);
       const cudaError_t e = copy_sync(s, buf.data(), src, buf.size() * sizeof(double), cudaMemcpyDeviceToHost);
       if (e != cudaSuccess) return fail(TG_ERR_CUDA, cudaGetErrorString(e));
-      for (int64_t q = 0; q < s.n_el; ++q)
-        for (int c = 0; c < 9; ++c) dst[9 * q + c] = buf[static_cast<size_t>(c) * s.n_el + q];
+      for (int64_t q = 0; q < s.n_el; ++q)  // perm: the lane order within warps
+        for (int c = 0; c < 9; ++c) dst[9 * s.perm[q] + c] = buf[static_cast<size_t>(c) * s.n_el + q];
     }
     // Indenter particles keep C = 0 and F = I (engine.cpp:218; scene.cpp:67-68).
     for (int64_t q = s.n_el; q < s.n; ++q)

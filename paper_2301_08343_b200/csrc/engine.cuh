@@ -158,9 +158,6 @@ struct DeviceSim {
   int lat[3] = {0, 0, 0};
   int tile[3] = {0, 0, 0};   // lattice block per CTA (ti, tj, tk)
   int tiles[3] = {0, 0, 0};  // blocks per axis
-  // Per elastomer CTA and thread: the lattice slot the thread handles
-  // (a permutation within each warp, configure_gel_lanes); null: identity.
-  uint8_t* gel_lanes = nullptr;
   bool grid_dirty = false;   // A / M_I may hold a phase-mode P2G (needs k_clear)
   void* grid_slab = nullptr;  // one allocation holding grid_mp, grid_v, grid_mi
   size_t grid_slab_bytes = 0;

@@ -285,7 +285,6 @@ struct GelMap {
   int lat[3];
   int tile[3];
   int tiles[3];
-  const uint8_t* lanes;  // [cta][thread] -> lattice slot of the CTA block (null: identity)
 };
 
 // The rigid indenter's look-ahead column walks, run by extra blocks of the
@@ -304,10 +303,9 @@ struct IndArgs {
 
 namespace {
 
-constexpr int kGelThreadsMap = 256;  // == kGelThreads (static_assert below)
 __device__ __forceinline__ int64_t gel_particle(const GelMap& M, int64_t n_el, int cta) {
   if (M.lat[0] > 0) {
-    const int t = M.lanes ? M.lanes[cta * kGelThreadsMap + threadIdx.x] : threadIdx.x;
+    const int t = threadIdx.x;
     const int per_col = M.tile[2];
     const int kk = t % per_col;
     const int jj = (t / per_col) % M.tile[1];
@@ -2098,7 +2096,6 @@ GelMap gel_map(const DeviceSim& s) {
     M.tile[a] = s.tile[a];
     M.tiles[a] = s.tiles[a];
   }
-  M.lanes = s.gel_lanes;
   return M;
 }
 
@@ -2170,50 +2167,42 @@ void configure_gel_tiling(DeviceSim& s, int nx, int ny, int nz) {
   s.tiles[2] = 1;
 }
 
-// Lane map of the lattice-block CTAs: within each warp, the threads take the
-// warp's 32 lattice slots in an order that spreads the 16-byte bank slots of
-// the particles' P2G / G2P tile nodes over the quarter-warps. A 128-bit
-// shared access is served a quarter-warp (8 lanes) at a time; in lattice
-// order a quarter-warp holds 8 consecutive particles of a column whose z
-// bases, 1.55 cells apart, span more than the 8 slots, so its tile accesses
-// took ~2x the ideal wavefronts (ncu). Slots are sorted by the residue mod 8
-// of their tile node offset at the initial positions (the tile box and pitch
-// as the kernel derives them) and dealt round robin to the quarter-warps.
-// Any permutation is correct (each slot is still handled by one thread of
-// the same warp, so the warp touches the same memory sectors); this one only
-// changes the bank pattern, and the node sums do not depend on it (the tile
-// phases fix the order per node).
-void configure_gel_lanes(DeviceSim& s, const double* x_in) {
-  if (s.gel_lanes) {
-    cudaFree(s.gel_lanes);
-    s.gel_lanes = nullptr;
-  }
+// Lane order of the lattice-block CTAs: within each warp, the particles of
+// the warp's 32 lattice slots are stored in an order dealt by the residue
+// mod 8 of their tile node offsets, so a quarter-warp's 128-bit tile
+// accesses spread over the shared-memory banks. A 128-bit shared access is
+// served a quarter-warp (8 lanes) at a time; in lattice order a quarter-warp
+// holds 8 consecutive particles of a column whose z bases, 1.55 cells
+// apart, span more than the 8 bank slots, so its tile accesses took ~2x the
+// ideal wavefronts (ncu). Slots are sorted by the residue at the initial
+// positions (tile box and pitch as the kernel derives them) and dealt round
+// robin to the quarter-warps; the result permutes the elastomer part of
+// DeviceSim::perm within each warp's slots, so the warp's particles, and the
+// memory sectors it touches, stay the same. Any order is correct: the node
+// sums of the tile do not depend on it (the phases fix the order per node).
+void permute_gel_lanes(DeviceSim& s, const double* x_in) {
   if (s.lat[0] <= 0 || !x_in) return;
   if (const char* e = std::getenv("TACCHI_GEL_LANES"))
     if (!std::atoi(e)) return;
-  static_assert(kGelThreadsMap == kGelThreads, "lane map size");
-  std::vector<int64_t> inv(static_cast<size_t>(s.n_el), -1);
-  for (int64_t q = 0; q < s.n; ++q)
-    if (q < s.n_el) inv[q] = s.perm[q];  // device slot q holds input particle perm[q]
   const int ctas = s.tiles[0] * s.tiles[1];
-  std::vector<uint8_t> lanes(static_cast<size_t>(ctas) * kGelThreads);
   const Geometry& g = s.geo;
   auto base_of_x = [&](double x, int a) {
     return static_cast<int>(std::floor((x - g.origin[a]) * g.inv_dx - 0.5));
   };
+  const std::vector<int64_t> perm0(s.perm.begin(), s.perm.begin() + s.n_el);
   for (int cta = 0; cta < ctas; ++cta) {
     int b[kGelThreads][3];
-    bool act[kGelThreads];
+    int64_t slot[kGelThreads];  // lattice (storage) index of thread t's slot, -1: none
     int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
     for (int t = 0; t < kGelThreads; ++t) {
       const int per_col = s.tile[2];
       const int kk = t % per_col, jj = (t / per_col) % s.tile[1], ii = t / (per_col * s.tile[1]);
       const int bj = cta % s.tiles[1], bi = cta / s.tiles[1];
       const int i = bi * s.tile[0] + ii, j = bj * s.tile[1] + jj;
-      act[t] = ii < s.tile[0] && i < s.lat[0] && j < s.lat[1] && kk < s.lat[2];
-      if (!act[t]) continue;
-      const int64_t q = (static_cast<int64_t>(i) * s.lat[1] + j) * s.lat[2] + kk;
-      const int64_t r = inv[q];
+      const bool act = ii < s.tile[0] && i < s.lat[0] && j < s.lat[1] && kk < s.lat[2];
+      slot[t] = act ? (static_cast<int64_t>(i) * s.lat[1] + j) * s.lat[2] + kk : -1;
+      if (!act) continue;
+      const int64_t r = perm0[slot[t]];
       for (int a = 0; a < 3; ++a) {
         b[t][a] = base_of_x(x_in[3 * r + a], a);
         lo[a] = std::min(lo[a], b[t][a]);
@@ -2222,32 +2211,27 @@ void configure_gel_lanes(DeviceSim& s, const double* x_in) {
     }
     const int d1 = hi[1] - lo[1] + 3, pitch = tile_pitch(hi[2] - lo[2] + 3);
     for (int w = 0; w < kGelThreads / 32; ++w) {
-      std::vector<int> used, idle;
-      for (int l = 0; l < 32; ++l) (act[32 * w + l] ? used : idle).push_back(32 * w + l);
+      std::vector<int> used;
+      for (int l = 0; l < 32; ++l)
+        if (slot[32 * w + l] >= 0) used.push_back(32 * w + l);
+      if (used.size() < 2) continue;
       auto res = [&](int t) {
         const long e = (static_cast<long>(b[t][0] - lo[0]) * d1 + (b[t][1] - lo[1])) * pitch +
                        (b[t][2] - lo[2]);
         return static_cast<int>(e & 7);
       };
-      std::stable_sort(used.begin(), used.end(), [&](int x, int y) { return res(x) < res(y); });
-      // deal: the k-th slot in residue order goes to quarter k % 4
-      std::vector<int> quarter[4];
-      for (size_t k = 0; k < used.size(); ++k) quarter[k % 4].push_back(used[k]);
-      int l = 0;
-      for (int q4 = 0; q4 < 4; ++q4) {
-        for (int t : quarter[q4]) lanes[static_cast<size_t>(cta) * kGelThreads + 32 * w + l++] = static_cast<uint8_t>(t);
-        for (size_t k = quarter[q4].size(); k < 8; ++k) {
-          lanes[static_cast<size_t>(cta) * kGelThreads + 32 * w + l++] = static_cast<uint8_t>(idle.back());
-          idle.pop_back();
-        }
-      }
+      std::vector<int> order = used;
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return res(x) < res(y); });
+      // the k-th particle in residue order goes to quarter k % 4; the warp's
+      // occupied slots (in lane order) are refilled quarter by quarter
+      std::vector<int> dealt;
+      for (int q4 = 0; q4 < 4; ++q4)
+        for (size_t k = q4; k < order.size(); k += 4) dealt.push_back(order[k]);
+      // lanes of the warp with a slot, in order: lane u gets the particle of
+      // slot dealt[u'] (u' its rank among the occupied lanes)
+      for (size_t u = 0; u < used.size(); ++u) s.perm[slot[used[u]]] = perm0[slot[dealt[u]]];
     }
   }
-  if (cudaMalloc(&s.gel_lanes, lanes.size()) != cudaSuccess) {
-    s.gel_lanes = nullptr;
-    return;
-  }
-  cudaMemcpy(s.gel_lanes, lanes.data(), lanes.size(), cudaMemcpyHostToDevice);
 }
 
 int launch_reset(DeviceSim& s, int mask) {
