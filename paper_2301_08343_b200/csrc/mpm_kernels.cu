@@ -2182,8 +2182,9 @@ void configure_gel_tiling(DeviceSim& s, int nx, int ny, int nz) {
 // sums of the tile do not depend on it (the phases fix the order per node).
 void permute_gel_lanes(DeviceSim& s, const double* x_in) {
   if (s.lat[0] <= 0 || !x_in) return;
-  if (const char* e = std::getenv("TACCHI_GEL_LANES"))
-    if (!std::atoi(e)) return;
+  int mode = 2;  // 0: lattice order, 1: dealt within each warp, 2: across the CTA
+  if (const char* e = std::getenv("TACCHI_GEL_LANES")) mode = std::atoi(e);
+  if (mode <= 0) return;
   const int ctas = s.tiles[0] * s.tiles[1];
   const Geometry& g = s.geo;
   auto base_of_x = [&](double x, int a) {
@@ -2210,6 +2211,32 @@ void permute_gel_lanes(DeviceSim& s, const double* x_in) {
       }
     }
     const int d1 = hi[1] - lo[1] + 3, pitch = tile_pitch(hi[2] - lo[2] + 3);
+    auto residue = [&](int t) {
+      const long e = (static_cast<long>(b[t][0] - lo[0]) * d1 + (b[t][1] - lo[1])) * pitch +
+                     (b[t][2] - lo[2]);
+      return static_cast<int>(e & 7);
+    };
+    if (mode == 2) {
+      // across the CTA: the slots stay where they are (each warp reads the
+      // same memory), the particles are dealt to the 32 quarter-warps in
+      // residue order, one per quarter in turn, skipping full quarters
+      std::vector<int> order;
+      std::vector<int> quarter_slots[kGelThreads / 8];
+      for (int t = 0; t < kGelThreads; ++t)
+        if (slot[t] >= 0) {
+          order.push_back(t);
+          quarter_slots[t / 8].push_back(t);
+        }
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return residue(x) < residue(y); });
+      std::vector<size_t> fill(kGelThreads / 8, 0);
+      int q = 0;
+      for (int t : order) {
+        while (fill[q] >= quarter_slots[q].size()) q = (q + 1) % (kGelThreads / 8);
+        s.perm[slot[quarter_slots[q][fill[q]++]]] = perm0[slot[t]];
+        q = (q + 1) % (kGelThreads / 8);
+      }
+      continue;
+    }
     for (int w = 0; w < kGelThreads / 32; ++w) {
       std::vector<int> used;
       for (int l = 0; l < 32; ++l)
