@@ -347,7 +347,8 @@ struct P2GTile {
   int lo[3], hi[3], dim[3];
   int blo[3], bhi[3];  // block_motion_box's node box reduction
   int ok;
-  int pitch;     // node row pitch (>= dim[2], = 1 mod 8: rows shift the 16-byte bank slot)
+  int pitch;     // node row pitch (>= dim[2], tile_pitch)
+  int rd;        // rows per x-slab (dim[1] + kRowPad)
   int zp, zoff;  // staged vz: node (row r, column c) at ((double*)nhi)[r * zp + zoff + c]
   unsigned long long bar;  // mbarrier of the staging copies
 };
@@ -361,11 +362,28 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Row pitches of the tile: nodes of the same z in neighbouring rows land in
-// different 16-byte bank slots (pitch = 1 mod 8 nodes); the staged vz rows
-// (8-byte elements, 16-byte aligned starts) use an even pitch = 2 mod 16.
-__host__ __device__ __forceinline__ int tile_pitch(int d2) { return ((d2 + 6) & ~7) + 1; }
-__host__ __device__ __forceinline__ int tile_zpitch(int zcnt) { return ((zcnt + 13) & ~15) + 2; }
+// Row pitches of the tile: 16-byte node slots, pitch = 5 mod 8 nodes, and
+// x-slabs of dim[1] + kRowPad rows; with the elastomer's storage order dealt
+// by the residue of the node offsets (permute_gel_lanes) these spread a
+// quarter-warp's 128-bit accesses over the bank slots best (a bank model of
+// config 2a's CTAs: 1.12x the ideal wavefronts vs 1.30x with pitch = 1 mod 8
+// and unpadded slabs). The staged vz rows (8-byte elements, 16-byte aligned
+// starts) use an even pitch = 6 mod 16.
+#ifndef TACCHI_PITCH_RES
+#define TACCHI_PITCH_RES 5
+#endif
+#ifndef TACCHI_ZPITCH_RES
+#define TACCHI_ZPITCH_RES 6
+#endif
+#ifndef TACCHI_ROW_PAD
+#define TACCHI_ROW_PAD 2
+#endif
+__host__ __device__ __forceinline__ int tile_pitch(int d2) { return d2 + ((TACCHI_PITCH_RES - d2) & 7); }
+__host__ __device__ __forceinline__ int tile_zpitch(int zcnt) {
+  return zcnt + ((TACCHI_ZPITCH_RES - zcnt) & 15);
+}
+// Rows of one x-slab of the tile (the j extent padded by kRowPad rows).
+constexpr int kRowPad = TACCHI_ROW_PAD;
 
 // Adds the CTA's node box into the global grid: one bulk-async reduction
 // (UBLKRED.ADD.F64, element-wise atomic in L2) per z-row and half, issued by
@@ -381,7 +399,7 @@ __device__ __forceinline__ void tile_bulk_reduce(const P2GTile& T, const Geometr
     const int r = t >> 1, half = t & 1;
     const int i = r / T.dim[1], j = r - i * T.dim[1];
     double2* dst = (half ? grid.hi : grid.lo) + node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
-    const double2* src = (half ? T.nhi : T.nlo) + r * T.pitch;
+    const double2* src = (half ? T.nhi : T.nlo) + (i * T.rd + j) * T.pitch;
     if (det_on<kDet>(g))  // fixed-point node sums: exact integer adds
       asm volatile(
           "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(dst),
@@ -430,10 +448,11 @@ __device__ __forceinline__ void tile_bulk_stage_issue(P2GTile& T, const Geometry
   for (int t = threadIdx.x; t < 2 * rows; t += blockDim.x) {
     const int r = t >> 1, half = t & 1;
     const int i = r / T.dim[1], j = r - i * T.dim[1];
+    const int sr = i * T.rd + j;  // the row in the tile
     const size_t nd = node_index(g, T.lo[0] + i, T.lo[1] + j, T.lo[2]);
     const void* sp = half ? static_cast<const void*>(src.z + (nd - zoff))
                           : static_cast<const void*>(src.xy + nd);
-    void* dp = half ? static_cast<void*>(zs + r * zp) : static_cast<void*>(T.nlo + r * T.pitch);
+    void* dp = half ? static_cast<void*>(zs + sr * zp) : static_cast<void*>(T.nlo + sr * T.pitch);
     const unsigned bytes = half ? zcnt * sizeof(double) : d2 * sizeof(double2);
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
@@ -551,7 +570,8 @@ __device__ void tile_box(P2GTile& T, bool active, const int* base) {
     const bool any = T.lo[0] != INT_MAX;
     for (int a = 0; a < 3; ++a) T.dim[a] = any ? T.hi[a] - T.lo[a] + 3 : 0;
     T.pitch = tile_pitch(T.dim[2]);
-    const int rows = T.dim[0] * T.dim[1];
+    T.rd = T.dim[1] + kRowPad;
+    const int rows = T.dim[0] * T.rd;
     T.ok = any && rows * T.pitch <= kTileCap && rows * tile_zpitch(T.dim[2] + 2) <= 2 * kTileCap;
   }
   __syncthreads();
@@ -636,7 +656,8 @@ __device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double
       T.dim[a] = any ? T.bhi[a] - T.blo[a] + 3 : 0;
     }
     T.pitch = tile_pitch(T.dim[2]);
-    const int rows = T.dim[0] * T.dim[1];
+    T.rd = T.dim[1] + kRowPad;
+    const int rows = T.dim[0] * T.rd;
     T.ok = any && rows * T.pitch <= kTileCap && rows * tile_zpitch(T.dim[2] + 2) <= 2 * kTileCap;
   }
   __syncthreads();
@@ -682,7 +703,7 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
     }
     b[6] = T.ok;
   }
-  const int d1 = T.dim[1], d2 = T.pitch;  // row pitch
+  const int d1 = T.rd, d2 = T.pitch;  // x-slab rows, row pitch
   const int vol = T.dim[0] * d1 * d2;
   const bool use_tile = T.ok != 0;
   if (use_tile) {
@@ -1731,7 +1752,7 @@ __device__ __forceinline__ void g2p_gather(const Geometry& g, VelBuf vel,
 // T.nlo[.].x/y, T.nhi[.].x), same arithmetic as g2p_gather.
 __device__ __forceinline__ void g2p_gather_smem(const Geometry& g, const P2GTile& T,
                                                 const Stencil& st, double* vv, double* Cn) {
-  const int d1 = T.dim[1], d2 = T.pitch, zp = T.zp;
+  const int d1 = T.rd, d2 = T.pitch, zp = T.zp;
   const int r0 = (st.base[0] - T.lo[0]) * d1 + (st.base[1] - T.lo[1]);
   const int c0 = st.base[2] - T.lo[2];
   const double* zs = reinterpret_cast<const double*>(T.nhi);
@@ -1814,6 +1835,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     // vz row staging needs even allocation rows (even start and length in z)
     T.ok = b[6] && (g.ga_dim[2] & 1) == 0 && (g.ga_lo[2] & 1) == 0;
     T.pitch = tile_pitch(T.dim[2]);
+    T.rd = T.dim[1] + kRowPad;
     for (int a = 0; a < 3; ++a) {  // the empty box for block_motion_box
       T.blo[a] = INT_MAX;
       T.bhi[a] = INT_MIN;
@@ -2210,7 +2232,7 @@ void permute_gel_lanes(DeviceSim& s, const double* x_in) {
         hi[a] = std::max(hi[a], b[t][a]);
       }
     }
-    const int d1 = hi[1] - lo[1] + 3, pitch = tile_pitch(hi[2] - lo[2] + 3);
+    const int d1 = hi[1] - lo[1] + 3 + kRowPad, pitch = tile_pitch(hi[2] - lo[2] + 3);
     auto residue = [&](int t) {
       const long e = (static_cast<long>(b[t][0] - lo[0]) * d1 + (b[t][1] - lo[1])) * pitch +
                      (b[t][2] - lo[2]);
