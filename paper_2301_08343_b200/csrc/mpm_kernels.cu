@@ -346,6 +346,7 @@ struct P2GTile {
   int owner[kTileCap];
   int lo[3], hi[3], dim[3];
   int blo[3], bhi[3];  // block_motion_box's node box reduction
+  int cur_s, cur_stale;  // the substep and its stale flag (thread 0, after the wait)
   int ok;
   int pitch;     // node row pitch (>= dim[2], tile_pitch)
   int rd;        // rows per x-slab (dim[1] + kRowPad)
@@ -419,31 +420,37 @@ __device__ __forceinline__ void tile_bulk_reduce(const P2GTile& T, const Geometr
   }
 }
 
-// Issues the staging of grid rows [lo, lo + dim) of `src` (both halves) into
-// T as bulk-async copies completing on T.bar (tile_bulk_wait). All threads of
-// the block must call it; T.dim / T.lo / T.ok are set.
-__device__ __forceinline__ void tile_bulk_stage_issue(P2GTile& T, const Geometry& g, VelBuf src) {
+// Staging of grid rows [lo, lo + dim) of `src` (both halves) into T as
+// bulk-async copies completing on T.bar (tile_bulk_wait), in two parts:
+// tile_bulk_stage_init (thread 0: pitches, mbarrier, expected bytes) and,
+// after a barrier, tile_bulk_stage_copies (every thread, one copy per row and
+// half). T.dim / T.lo / T.ok are set.
+// vz rows are 8-byte elements: each row is copied from the even node at or
+// below its start (16-byte aligned; res2 is even, so every row of the box
+// has the same parity zoff) over an even count, into rows of pitch zp.
+__device__ __forceinline__ void tile_bulk_stage_init(P2GTile& T) {
+  const int rows = T.dim[0] * T.dim[1];
+  const int d2 = T.dim[2];
+  const unsigned bar = smem_addr(&T.bar);
+  const int zoff = T.lo[2] & 1;
+  const int zcnt = (zoff + d2 + 1) & ~1;
+  T.zp = tile_zpitch(zcnt);
+  T.zoff = zoff;
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(static_cast<unsigned>(rows * (d2 * sizeof(double2) + zcnt * sizeof(double))))
+               : "memory");
+}
+
+__device__ __forceinline__ void tile_bulk_stage_copies(P2GTile& T, const Geometry& g, VelBuf src) {
   const int rows = T.dim[0] * T.dim[1];
   const int d2 = T.dim[2];
   const unsigned bar = smem_addr(&T.bar);
   unsigned long long pol;  // V is dead once the CTAs around it have staged it
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  // vz rows are 8-byte elements: each row is copied from the even node at or
-  // below its start (16-byte aligned; res2 is even, so every row of the box
-  // has the same parity zoff) over an even count, into rows of pitch zp.
-  const int zoff = T.lo[2] & 1;
+  const int zoff = T.zoff, zp = T.zp;
   const int zcnt = (zoff + d2 + 1) & ~1;
-  const int zp = tile_zpitch(zcnt);
-  if (threadIdx.x == 0) {
-    T.zp = zp;
-    T.zoff = zoff;
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                 "r"(static_cast<unsigned>(rows * (d2 * sizeof(double2) + zcnt * sizeof(double))))
-                 : "memory");
-  }
-  __syncthreads();
   double* zs = reinterpret_cast<double*>(T.nhi);
   for (int t = threadIdx.x; t < 2 * rows; t += blockDim.x) {
     const int r = t >> 1, half = t & 1;
@@ -461,6 +468,7 @@ __device__ __forceinline__ void tile_bulk_stage_issue(P2GTile& T, const Geometry
         : "memory");
   }
 }
+
 __device__ __forceinline__ void tile_bulk_wait(P2GTile& T) {
   const unsigned bar = smem_addr(&T.bar);
   asm volatile(
@@ -1836,12 +1844,19 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     T.ok = b[6] && (g.ga_dim[2] & 1) == 0 && (g.ga_lo[2] & 1) == 0;
     T.pitch = tile_pitch(T.dim[2]);
     T.rd = T.dim[1] + kRowPad;
+    if (T.ok && g.scatter_mode != 5) tile_bulk_stage_init(T);
     for (int a = 0; a < 3; ++a) {  // the empty box for block_motion_box
       T.blo[a] = INT_MAX;
       T.bhi[a] = INT_MIN;
     }
   }
   pdl_wait();
+  if (kLookahead && gel_block && threadIdx.x == 0) {
+    // the substep and its stale flag, shared at the barrier below
+    const int sc = ctl->substep;
+    T.cur_s = sc;
+    T.cur_stale = stale(ctl, sc) ? 1 : 0;
+  }
   TRACE_MARK(1);
   if (!gel_block) {
     // indenter blocks: the s+1 column walks (they touch only indenter x and
@@ -1856,20 +1871,21 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
   double F[9], vv[3], Cn[9];  // defined for active particles only
   bool staged = false;
   Stencil st_old;
+  int s;
   if (kLookahead) {
     // Stage the grid velocities of the CTA's G2P footprint (coalesced rows
-    // along z) in the shared tile before the gathers; the copies are in
-    // flight while the control block is read.
-    __syncthreads();  // T.lo / dim / ok from thread 0
+    // along z) in the shared tile before the gathers. One barrier publishes
+    // thread 0's tile box, mbarrier and control-block read.
+    __syncthreads();
+    s = T.cur_s;
+    if (T.cur_stale) return;  // block-uniform; no copy issued yet
     staged = T.ok != 0;
-    if (staged && g.scatter_mode != 5) tile_bulk_stage_issue(T, g, vel);
+    if (staged && g.scatter_mode != 5) tile_bulk_stage_copies(T, g, vel);
+  } else {
+    s = ctl->substep;
+    if (stale_block(ctl, s)) return;
   }
   const bool staging = kLookahead && staged && g.scatter_mode != 5;
-  const int s = ctl->substep;
-  if (stale_block(ctl, s)) {
-    if (staging) tile_bulk_wait(T);  // no bulk copy may land in a retired CTA's smem
-    return;
-  }
   // the stencil needs x: its loads complete while the staging copies fly
   if (active) make_stencil(px0, px1, px2, g.origin, g.inv_dx, st_old);
   // F (prefetched into L2 at entry) is loaded while the staging copies
