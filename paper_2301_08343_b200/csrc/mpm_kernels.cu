@@ -1304,6 +1304,7 @@ struct ColSmem {
   double w[kColWarps][27][33];
   long long key[kColWarps][32];
   int run_start[kColWarps][33];
+  int run_end[kColWarps][33];
 };
 
 // One block's column walks (blk = block index among the indenter blocks).
@@ -1342,6 +1343,27 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
   }
   const int c = blk * kColWarps + warp;
   if (c >= n_cols) return;  // warp-uniform; only __syncwarp below
+  // Every input of the walk is loaded up front (one round trip for the
+  // column bounds, the box, the chain start and the velocity instead of a
+  // chain of dependent reads), then the column's first chunk.
+  const int64_t a0 = col_start[c], a1 = col_start[c + 1];
+  int blo0[3], bhi0[3];
+  for (int a = 0; a < 3; ++a) {
+    blo0[a] = ctl->box_lo[0][a];
+    bhi0[a] = ctl->box_hi[0][a];
+  }
+  const int chain_start = ctl->chain_start;
+  double vind[3];
+  for (int a = 0; a < 3; ++a) vind[a] = ctl->vind[a];
+  double nx = 0, ny = 0, nz = 0;
+  int ndone = 0;
+  if (a0 + lane < a1) {
+    const int64_t p = a0 + lane;
+    nx = __ldcs(x + p);
+    ny = __ldcs(x + n + p);
+    nz = __ldcs(x + 2 * n + p);
+    ndone = moves[p - n_el];
+  }
   // Elastomer node box of the substep being scattered.
   int glo[3], ghi[3];
   for (int a = 0; a < 3; ++a) {
@@ -1352,28 +1374,19 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
       ghi[a] = static_cast<int>(floor(sub_rn(mul_rn(sub_rn(h, g.origin[a]), g.inv_dx), 0.5))) + 3;
     } else {
       const int widen = box_mode == 2 ? 1 : 0;
-      glo[a] = ctl->box_lo[0][a];
-      ghi[a] = ctl->box_hi[0][a];
+      glo[a] = blo0[a];
+      ghi[a] = bhi0[a];
       if (ghi[a] <= glo[a]) return;
       glo[a] -= widen;
       ghi[a] += widen;
     }
   }
-  const int target = s - ctl->chain_start + (kMove ? 1 : 0);  // chain advects after this kernel
+  const int target = s - chain_start + (kMove ? 1 : 0);  // chain advects after this kernel
   double d[3] = {0, 0, 0};
-  for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, ctl->vind[a]);
-  const int64_t a0 = col_start[c], a1 = col_start[c + 1];
-  // the chunk's loads are issued one chunk ahead (most columns take two or
-  // three chunks; each was a dependent DRAM round trip)
-  double nx = 0, ny = 0, nz = 0;
-  int ndone = 0;
-  if (a0 + lane < a1) {
-    const int64_t p = a0 + lane;
-    nx = __ldcs(x + p);
-    ny = __ldcs(x + n + p);
-    nz = __ldcs(x + 2 * n + p);
-    ndone = moves[p - n_el];
-  }
+  for (int a = 0; a < 3; ++a) d[a] = mul_rn(g.dt, vind[a]);
+  // the next chunk's loads are issued one chunk ahead (most columns take two
+  // or three chunks; each was a dependent DRAM round trip)
+  unsigned walked = 0;
   for (int64_t b0 = a0; b0 < a1; b0 += 32) {
     const int64_t p = b0 + lane;
     const bool valid = p < a1;
@@ -1409,8 +1422,7 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
         contrib = false;
       }
     }
-    const unsigned mv = __ballot_sync(0xffffffffu, moved);
-    if (lane == 0 && mv) atomicAdd(&ctl->ind_walked, static_cast<unsigned long long>(__popc(mv)));
+    walked += __popc(__ballot_sync(0xffffffffu, moved));
     const unsigned bey = __ballot_sync(0xffffffffu, beyond);
     const int first_beyond = bey ? __ffs(bey) - 1 : 32;
     if (lane > first_beyond) contrib = false;
@@ -1426,17 +1438,22 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
       }
     S.key[warp][lane] = key;
     __syncwarp();
+    // runs of equal keys (contributing lanes only): heads and tails ranked
+    // by ballot, so the sums below walk [start, end) without key compares
     const bool head = contrib && (lane == 0 || S.key[warp][lane - 1] != key);
+    const bool tail = contrib && (lane == 31 || S.key[warp][lane + 1] != key);
     const unsigned hb = __ballot_sync(0xffffffffu, head);
+    const unsigned tb = __ballot_sync(0xffffffffu, tail);
     if (head) S.run_start[warp][__popc(hb & ((1u << lane) - 1))] = lane;
+    if (tail) S.run_end[warp][__popc(tb & ((1u << lane) - 1))] = lane + 1;
     __syncwarp();
     const int nruns = __popc(hb);
     for (int task = lane; task < nruns * 27; task += 32) {
       const int r = task / 27, comp = task % 27;
-      const int t0 = S.run_start[warp][r];
+      const int t0 = S.run_start[warp][r], t1 = S.run_end[warp][r];
       const long long k0 = S.key[warp][t0];
       double sum = 0.0;
-      for (int t = t0; t < 32 && S.key[warp][t] == k0; ++t) sum += S.w[warp][comp][t];
+      for (int t = t0; t < t1; ++t) sum += S.w[warp][comp][t];
       if (sum != 0.0)
         mi_add<kDet>(g, mi + k0 + (static_cast<int64_t>(comp / 9) * g.ga_dim[1] + (comp / 3) % 3) * g.ga_dim[2] +
                     comp % 3,
@@ -1445,6 +1462,9 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
     __syncwarp();
     if (bey) break;  // the rest of the column is above the elastomer box
   }
+  // tg_stats' walked count: one RED per column (per chunk, they queued on
+  // one control-block word)
+  if (lane == 0 && walked) atomicAdd(&ctl->ind_walked, static_cast<unsigned long long>(walked));
 }
 
 template <bool kMove>
