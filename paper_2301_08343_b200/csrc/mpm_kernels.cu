@@ -1335,7 +1335,7 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s_scatter = kMove ? s + 1 : s;
   mi = mi_at(g, mi, s_scatter);
-  if (blk == 0 && threadIdx.x == 0) {
+  if (blk == 0 && threadIdx.x == 0 && !stale(ctl, s)) {
     for (int a = 0; a < 3; ++a) {
       if (kMove) ctl->ind_v[a] = ctl->vind[a];  // apply_boundary (engine.cpp:260-261)
       ctl->ind_vp[s_scatter & 1][a] = kMove ? ctl->vind[a] : ctl->ind_v[a];
@@ -1364,6 +1364,8 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
     nz = __ldcs(x + 2 * n + p);
     ndone = moves[p - n_el];
   }
+  // (k_ind_cols checks staleness here, after issuing its loads)
+  if (stale(ctl, s)) return;
   // Elastomer node box of the substep being scattered.
   int glo[3], ghi[3];
   for (int a = 0; a < 3; ++a) {
@@ -1426,6 +1428,10 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
     const unsigned bey = __ballot_sync(0xffffffffu, beyond);
     const int first_beyond = bey ? __ffs(bey) - 1 : 32;
     if (lane > first_beyond) contrib = false;
+    if (!__any_sync(0xffffffffu, contrib)) {  // nothing to scatter in this chunk
+      if (bey) break;
+      continue;
+    }
     const long long key = contrib ? static_cast<long long>(node_index(g, st.base[0], st.base[1], st.base[2]))
                                   : -1 - static_cast<long long>(lane);
 #pragma unroll
@@ -1475,10 +1481,9 @@ __global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ColSmem& S = *reinterpret_cast<ColSmem*>(smem_raw);
   pdl_wait();
-  const int s = ctl->substep;
-  if (stale(ctl, s)) return;
+  // staleness is checked inside, once the walk's loads are in flight
   ind_cols_block<kMove>(S, blockIdx.x, x, n, n_el, col_start, n_cols, moves, ctl, g, mi, box_mode,
-                        s);
+                        ctl->substep);
 }
 
 // Applies the pending advects of the indenter particles the column walks did
