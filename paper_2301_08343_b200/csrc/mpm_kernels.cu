@@ -2292,12 +2292,50 @@ void permute_gel_lanes(DeviceSim& s, const double* x_in) {
         }
       std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return residue(x) < residue(y); });
       std::vector<size_t> fill(kGelThreads / 8, 0);
+      std::vector<int> src(kGelThreads, -1);  // thread -> the thread slot whose particle it takes
       int q = 0;
       for (int t : order) {
         while (fill[q] >= quarter_slots[q].size()) q = (q + 1) % (kGelThreads / 8);
-        s.perm[slot[quarter_slots[q][fill[q]++]]] = perm0[slot[t]];
+        src[quarter_slots[q][fill[q]++]] = t;
         q = (q + 1) % (kGelThreads / 8);
       }
+      // Keep the lattice order where it already spreads the banks (a gel
+      // spacing below one cell, config 2b: 8 consecutive z particles span
+      // fewer than 8 nodes): the bank cost of an order is the sum over
+      // quarter-warps of the largest number of distinct tile nodes sharing a
+      // 16-byte slot (the same for every tile phase: the phases shift all
+      // lanes' nodes by one offset).
+      auto cost = [&](auto&& who) {
+        long c = 0;
+        for (int q4 = 0; q4 < kGelThreads / 8; ++q4) {
+          long node[8];
+          int cnt = 0;
+          for (int l = 0; l < 8; ++l) {
+            const int t = who(8 * q4 + l);
+            if (t < 0) continue;
+            node[cnt++] = (static_cast<long>(b[t][0] - lo[0]) * d1 + (b[t][1] - lo[1])) * pitch +
+                          (b[t][2] - lo[2]);
+          }
+          int worst = 0;
+          for (int r = 0; r < 8; ++r) {
+            int m = 0;
+            for (int i = 0; i < cnt; ++i) {
+              if ((node[i] & 7) != r) continue;
+              bool dup = false;
+              for (int k = 0; k < i; ++k) dup = dup || node[k] == node[i];
+              m += dup ? 0 : 1;
+            }
+            worst = std::max(worst, m);
+          }
+          c += worst;
+        }
+        return c;
+      };
+      const long c_lat = cost([&](int t) { return slot[t] >= 0 ? t : -1; });
+      const long c_deal = cost([&](int t) { return src[t]; });
+      if (10 * c_deal < 9 * c_lat)
+        for (int t = 0; t < kGelThreads; ++t)
+          if (src[t] >= 0) s.perm[slot[t]] = perm0[slot[src[t]]];
       continue;
     }
     for (int w = 0; w < kGelThreads / 32; ++w) {

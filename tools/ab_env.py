@@ -3,6 +3,9 @@ its own process (the switches are read at tg_create), interleaved `--rounds`
 times; prints frames/s and the per-kernel device times (tg_time_phases).
 
     python tools/ab_env.py --variant base: --variant dense:TACCHI_DENSE_GRID=1
+
+AB_CFG: SceneConfig overrides as JSON, or @file holding them (for JSON with
+commas, which the variant syntax splits on).
 """
 import argparse
 import json
@@ -18,7 +21,8 @@ sys.path.insert(0, %r)
 import torch
 import paper_2301_08343_b200 as tb
 from tests.scenes import CONFIG2A, CONFIG2A_V
-cfg = {**CONFIG2A, **json.loads(os.environ.get("AB_CFG", "{}"))}
+_ab = os.environ.get("AB_CFG", "{}")
+cfg = {**CONFIG2A, **json.loads(open(_ab[1:]).read() if _ab.startswith("@") else _ab)}
 s = tb.sim.build_sim(cfg)
 rp = tb.render_params(cfg, "")
 for _ in range(5):
