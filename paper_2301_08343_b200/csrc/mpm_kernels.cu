@@ -1857,7 +1857,17 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     for (int i = 0; i < 9; ++i) asm volatile("prefetch.global.L2 [%0];" ::"l"(Fm + i * n_el + p));
     if (kBoundary) bottom = __ldg(tag + p) == kElastomerBottom;
   }
+  int ctl_s = 0;
+  bool ctl_stale = false;
   if (kLookahead && gel_block && threadIdx.x == 0) {
+    // The control block as the previous finalize left it, read beside the
+    // tile box (one round trip instead of two): finalize(s - 1) is complete
+    // once grid_update passed its own wait (the only way this grid can have
+    // been launched), grid_update raises nothing, and the walks beside it
+    // raise only for s + 1, so neither the substep nor its stale flag can
+    // change before this grid's wait.
+    ctl_s = ctl->substep;
+    ctl_stale = stale(ctl, ctl_s);
     // The G2P footprint is the tile box of the P2G that scattered these
     // particles at these positions (the previous kernel of this CTA).
     const int* b = g.cta_box + 8 * cta;
@@ -1878,9 +1888,8 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
   pdl_wait();
   if (kLookahead && gel_block && threadIdx.x == 0) {
     // the substep and its stale flag, shared at the barrier below
-    const int sc = ctl->substep;
-    T.cur_s = sc;
-    T.cur_stale = stale(ctl, sc) ? 1 : 0;
+    T.cur_s = ctl_s;
+    T.cur_stale = ctl_stale ? 1 : 0;
   }
   TRACE_MARK(1);
   if (!gel_block) {
