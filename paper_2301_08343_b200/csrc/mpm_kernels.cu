@@ -896,19 +896,41 @@ __device__ void finalize_warp(Ctl* ctl, const Geometry& g, int mode, FinFix& fx)
   const int lane = threadIdx.x;
   const bool ax = lane < 3;
   const int a = ax ? lane : 0;
+  // Every input is loaded in one round trip (both parity slots of the
+  // slotted reductions; the substep picks one afterwards): finalize sits on
+  // the substep's critical path, between the elastomer kernel and the next
+  // grid_update.
   const int s = ctl->substep;
-  if (stale(ctl, s)) return;
+  const unsigned long long errk = *reinterpret_cast<volatile const unsigned long long*>(&ctl->err);
+  unsigned long long kbl[2], kbh[2], kil[2], kih[2], ki0l[2], ki0h[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    kbl[q] = ctl->bb_lo[q][a];
+    kbh[q] = ctl->bb_hi[q][a];
+    kil[q] = ctl->ind_lo[q][a];
+    kih[q] = ctl->ind_hi[q][a];
+    ki0l[q] = ctl->ind_lo[q][0];
+    ki0h[q] = ctl->ind_hi[q][0];
+  }
+  const double va = ctl->vind[a];
+  const double u0 = ctl->vind[0], u1 = ctl->vind[1], u2 = ctl->vind[2];
+  const int pl = ctl->prev_lo[a], ph = ctl->prev_hi[a];
+  const int olo = ctl->box_lo[0][a], ohi = ctl->box_hi[0][a];
+  const unsigned long long kdf[2] = {ctl->min_detf[0], ctl->min_detf[1]};
+  const unsigned long long kv2[2] = {ctl->max_v2[0], ctl->max_v2[1]};
+  const long long steps = ctl->step_count;
+  const int wl_old = ctl->win_lo[a], wh_old = ctl->win_hi[a];
+  const long long fixups = ctl->walk_fixups;
+  if ((errk >> 8) <= static_cast<unsigned long long>(s)) return;  // stale(ctl, s)
   // after an advect the reductions of substep s are in slot s & 1; a window
   // of the current positions (before P2G(s)) reads slot (s + 1) & 1
   const int cur = (mode & kFinAdvect) ? (s & 1) : ((s + 1) & 1);
   // the indenter box is advanced from the previous slot when shifting
   const int isl = (mode & kFinIndShift) ? (cur ^ 1) : cur;
   // per-axis inputs
-  const bool ind_any = order_val(ctl->ind_lo[isl][0]) <= order_val(ctl->ind_hi[isl][0]);
-  double bl = order_val(ctl->bb_lo[cur][a]), bh = order_val(ctl->bb_hi[cur][a]);
-  double il = order_val(ctl->ind_lo[isl][a]), ih = order_val(ctl->ind_hi[isl][a]);
-  const double va = ctl->vind[a];
-  const int pl = ctl->prev_lo[a], ph = ctl->prev_hi[a];
+  const bool ind_any = order_val(ki0l[isl]) <= order_val(ki0h[isl]);
+  double bl = order_val(kbl[cur]), bh = order_val(kbh[cur]);
+  double il = order_val(kil[isl]), ih = order_val(kih[isl]);
   const bool shift = (mode & kFinIndShift) && ind_any;
   if (shift) {
     // The indenter moved rigidly with vind: fl(x + fl(dt v)) is monotone in
@@ -919,9 +941,8 @@ __device__ void finalize_warp(Ctl* ctl, const Geometry& g, int mode, FinFix& fx)
   }
   const double lo = fmin(bl, il), hi = fmax(bh, ih);
   int err = 0;  // warp-uniform
-  // the elastomer box the look-ahead walks of this substep used (before it
-  // is replaced below)
-  const int olo = ctl->box_lo[0][a], ohi = ctl->box_hi[0][a];
+  // (olo, ohi: the elastomer box the look-ahead walks of this substep used,
+  // read above before it is replaced below)
   if (mode & kFinAdvect) {
     // engine.cpp:279-285 (grid.cpp:29-36 per axis: xn = (x - o) / dx)
     bool ok = true;
@@ -947,17 +968,14 @@ __device__ void finalize_warp(Ctl* ctl, const Geometry& g, int mode, FinFix& fx)
   const bool prev_empty = __any_sync(0xffffffffu, ax && ph - pl <= 0);
   if (lane == 0) {
     if (mode & kFinDiag) {  // particle_to_grid's min_det_f (engine.cpp:119,177)
-      ctl->diag_min_det_f = order_val(ctl->min_detf[s & 1]);
+      ctl->diag_min_det_f = order_val(kdf[s & 1]);
       ctl->min_detf[s & 1] = order_key(1.0);
     }
     if (mode & kFinAdvect) {
-      double v2 = __longlong_as_double(static_cast<long long>(ctl->max_v2[cur]));
-      if (shift) {
-        const double u0 = ctl->vind[0], u1 = ctl->vind[1], u2 = ctl->vind[2];
-        v2 = fmax(v2, u0 * u0 + u1 * u1 + u2 * u2);
-      }
+      double v2 = __longlong_as_double(static_cast<long long>(kv2[cur]));
+      if (shift) v2 = fmax(v2, u0 * u0 + u1 * u1 + u2 * u2);
       ctl->diag_max_speed = sqrt(v2);
-      ctl->step_count += 1;
+      ctl->step_count = steps + 1;
       ctl->substep = s + 1;
     }
     if (err) raise(ctl, kErrOutOfGrid, err == 1 ? s : ((mode & kFinAdvect) ? s + 1 : s));
@@ -989,8 +1007,8 @@ __device__ void finalize_warp(Ctl* ctl, const Geometry& g, int mode, FinFix& fx)
     // the reference's Grid::active window: after a step it is the window of
     // the last substep's zero_grid (the one ending here), else the new one
     const bool after_step = (mode & kFinAdvect) != 0;
-    ctl->ref_lo[a] = after_step ? ctl->win_lo[a] : wlo;
-    ctl->ref_hi[a] = after_step ? ctl->win_hi[a] : whi;
+    ctl->ref_lo[a] = after_step ? wl_old : wlo;
+    ctl->ref_hi[a] = after_step ? wh_old : whi;
     ctl->win_lo[a] = ctl->prev_lo[a] = wlo;
     ctl->win_hi[a] = ctl->prev_hi[a] = whi;
   }
@@ -1008,7 +1026,7 @@ __device__ void finalize_warp(Ctl* ctl, const Geometry& g, int mode, FinFix& fx)
       fx.old_ok = old_ok;
       fx.need = new_any && !(old_ok && inside);
       fx.s = s;
-      if (fx.need) ctl->walk_fixups += 1;
+      if (fx.need) ctl->walk_fixups = fixups + 1;
     }
   }
 }
