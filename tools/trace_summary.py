@@ -28,10 +28,13 @@ def main(path, tag):
            "OUT=$PWD/paper_2301_08343_b200/_lib_trace EXTRA_NVFLAGS=-DTACCHI_TRACE` and run as",
            "`TACCHI_LIB=paper_2301_08343_b200/_lib_trace/libtacchi_cuda.so python tools/trace_gel.py`",
            f"(`{path}`). The marks add ~1 µs to the kernel; use for shares, not totals.", "",
-           f"- {d['ctas_gel']} elastomer CTAs (252 particles each) + {d['ctas_ind']} indenter-walk blocks "
-           f"(launched first, {d['ind_block_us_mean']} µs each, done by {d['ind_start_end_us'][1]} µs)",
+           (f"- {d['ctas_gel']} elastomer CTAs (252 particles each) + {d['ctas_ind']} indenter-walk blocks "
+            f"(launched first, {d['ind_block_us_mean']} µs each, done by {d['ind_start_end_us'][1]} µs)"
+            if d.get("ctas_ind") else
+            f"- {d['ctas_gel']} elastomer CTAs (252 particles each); the indenter walks run as a kernel "
+            "of their own on the forked walk stream"),
            f"- kernel span {d['kernel_span_us']} µs; CTA wall time {d['cta_wall_us_mean']} µs mean; 2 CTAs per SM "
-           "(128 registers × 256 threads each fill the register file; 112 KB of shared memory each), "
+           "(128 registers × 256 threads each fill the register file; ~103 KB of shared memory each), "
            "884 / 296 slots = 3 waves",
            f"- elastomer CTA starts (µs, percentiles 0/25/50/75/90/100): {d['gel_start_us_pct']}; "
            f"ends: {d['gel_end_us_pct']}", "",
@@ -39,7 +42,7 @@ def main(path, tag):
     for k in m:
         out.append(f"| {k}: {DESC.get(k, k)} | {m[k]} | {p[k]} |")
     out += ["", f"Sum {d['cta_us_mean']} µs per CTA. The 27 phases are the largest single stage "
-            "(shared-memory wavefront bound, DESIGN §4.2); the rest is latency exposed with only two "
+            "(barrier- and shared-memory-bound, DESIGN §4.2); the rest is latency exposed with only two "
             "CTAs (16 warps) per SM. The ramp-down after the last CTA starts costs ~7 µs of full-GPU "
             "time per launch.", "",
             "Resident elastomer CTAs per µs: " + " ".join(str(c) for c in conc[:80])]
