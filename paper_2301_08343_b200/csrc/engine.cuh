@@ -68,7 +68,7 @@ struct Geometry {
   double stress_scale;  // -dt * 4 * inv_dx^2 (engine.cpp:114)
   int scatter_mode;     // 0: shared-memory tile (default), 1: direct RED (A/B switch)
   int* cta_box;         // per elastomer CTA: {lo[3], dim[3], ok} of its last P2G tile
-  int gu_bps;           // grid_update blocks per SM (TACCHI_GU_BPS, default 10)
+  int gu_bps;           // grid_update blocks per SM (TACCHI_GU_BPS, default 5)
   int pdl_early;        // grid_update triggers its dependent launch right after its
                         // own griddepcontrol.wait (TACCHI_PDL_EARLY, default 1)
   int ind_first;        // the indenter blocks of the elastomer kernel come first
