@@ -886,6 +886,28 @@ print(json.dumps({k: hashlib.sha1(st[k].tobytes()).hexdigest() for k in ("x", "v
 """
 
 
+def test_storage_orders_byte_identical():
+    """The elastomer's storage order within each CTA's slots (dealt for the
+    shared-memory banks, TACCHI_GEL_LANES=2 the default; 1 within warps; 0
+    lattice order) only changes which thread handles which particle: in
+    deterministic mode (fixed-point node sums) 300 substeps of config 2a
+    give byte-identical particle states in every order (downloaded through
+    the permutation)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("0", "1", "2"):
+        p = subprocess.run([sys.executable, "-c", _WALK_CHILD % root], capture_output=True,
+                           text=True, env={**os.environ, "TACCHI_GEL_LANES": mode}, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[mode] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert out["0"] == out["1"] == out["2"]
+
+
 def test_walk_plans_byte_identical():
     """The indenter's look-ahead walks as extra blocks of the elastomer kernel
     (TACCHI_WALKS=fused) or as their own kernel on a forked stream
