@@ -1316,14 +1316,23 @@ __global__ void __launch_bounds__(kIndThreads) k_ind_move_p2g(double* __restrict
 // ---------------------------------------------------------------------------
 __global__ void k_chain_begin(Ctl* ctl) { ctl->chain_start = ctl->substep; }
 
-constexpr int kColWarps = 8;
+constexpr int kColWarps = 8;  // the walk blocks inside the elastomer kernel (TACCHI_WALKS=fused)
+#ifndef TACCHI_WALK_WARPS
+#define TACCHI_WALK_WARPS 4
+#endif
+// Warps (columns) per block of the walk kernel of its own: small blocks
+// retire as soon as their columns are done instead of holding shared memory
+// and registers for their longest column.
+constexpr int kWalkWarps = TACCHI_WALK_WARPS;
 
-struct ColSmem {
-  double w[kColWarps][27][33];
-  long long key[kColWarps][32];
-  int run_start[kColWarps][33];
-  int run_end[kColWarps][33];
+template <int W>
+struct ColSmemT {
+  double w[W][27][33];
+  long long key[W][32];
+  int run_start[W][33];
+  int run_end[W][33];
 };
+using ColSmem = ColSmemT<kColWarps>;
 
 // One block's column walks (blk = block index among the indenter blocks).
 // box_mode: 0 = Ctl::box[0] (the elastomer box of the substep being
@@ -1343,8 +1352,8 @@ __device__ __forceinline__ bool walk_contrib(const Geometry& g, const Stencil& s
   return c;
 }
 
-template <bool kMove, int kDet = -1>
-__device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __restrict__ x,
+template <bool kMove, int kDet = -1, int W = kColWarps>
+__device__ __forceinline__ void ind_cols_block(ColSmemT<W>& S, int blk, double* __restrict__ x,
                                                int64_t n, int64_t n_el,
                                                const int64_t* __restrict__ col_start, int n_cols,
                                                uint8_t* __restrict__ moves, Ctl* ctl,
@@ -1359,7 +1368,7 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
       ctl->ind_vp[s_scatter & 1][a] = kMove ? ctl->vind[a] : ctl->ind_v[a];
     }
   }
-  const int c = blk * kColWarps + warp;
+  const int c = blk * W + warp;
   if (c >= n_cols) return;  // warp-uniform; only __syncwarp below
   // Every input of the walk is loaded up front (one round trip for the
   // column bounds, the box, the chain start and the velocity instead of a
@@ -1492,16 +1501,16 @@ __device__ __forceinline__ void ind_cols_block(ColSmem& S, int blk, double* __re
 }
 
 template <bool kMove>
-__global__ void __launch_bounds__(kColWarps * 32) k_ind_cols(
+__global__ void __launch_bounds__(kWalkWarps * 32) k_ind_cols(
     double* __restrict__ x, int64_t n, int64_t n_el, const int64_t* __restrict__ col_start,
     int n_cols, uint8_t* __restrict__ moves, Ctl* ctl, Geometry g, double* __restrict__ mi,
     int box_mode) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ColSmem& S = *reinterpret_cast<ColSmem*>(smem_raw);
+  ColSmemT<kWalkWarps>& S = *reinterpret_cast<ColSmemT<kWalkWarps>*>(smem_raw);
   pdl_wait();
   // staleness is checked inside, once the walk's loads are in flight
-  ind_cols_block<kMove>(S, blockIdx.x, x, n, n_el, col_start, n_cols, moves, ctl, g, mi, box_mode,
-                        ctl->substep);
+  ind_cols_block<kMove, -1, kWalkWarps>(S, blockIdx.x, x, n, n_el, col_start, n_cols, moves, ctl,
+                                        g, mi, box_mode, ctl->substep);
 }
 
 // Applies the pending advects of the indenter particles the column walks did
@@ -2225,8 +2234,8 @@ int configure_device(int device) {
   set(reinterpret_cast<const void*>(k_g2p2g_gel<true, true, true, 1>), tile);
   set(reinterpret_cast<const void*>(k_ind_move_p2g<false, true>), static_cast<int>(kIndSmem));
   set(reinterpret_cast<const void*>(k_ind_move_p2g<true, true>), static_cast<int>(kIndSmem));
-  set(reinterpret_cast<const void*>(k_ind_cols<true>), static_cast<int>(sizeof(ColSmem)));
-  set(reinterpret_cast<const void*>(k_ind_cols<false>), static_cast<int>(sizeof(ColSmem)));
+  set(reinterpret_cast<const void*>(k_ind_cols<true>), static_cast<int>(sizeof(ColSmemT<kWalkWarps>)));
+  set(reinterpret_cast<const void*>(k_ind_cols<false>), static_cast<int>(sizeof(ColSmemT<kWalkWarps>)));
   if (cur >= 0 && cur != device) cudaSetDevice(cur);
   if (e != cudaSuccess) return 2;
   g_cfg_done[device] = true;
@@ -2506,7 +2515,7 @@ int launch_ind_move(DeviceSim& s, bool lookahead) {
   return 1;
 }
 
-constexpr size_t kColSmem = sizeof(ColSmem);
+constexpr size_t kColSmem = sizeof(ColSmemT<kWalkWarps>);  // the walk kernel of its own
 
 int launch_chain_begin(DeviceSim& s) {
   k_chain_begin<<<1, 1, 0, s.stream>>>(s.ctl);
@@ -2518,13 +2527,13 @@ int launch_chain_begin(DeviceSim& s) {
 // positions as they are) or fused with this substep's advect (look-ahead).
 int launch_ind_cols(DeviceSim& s, bool move) {
   if (s.n_ind <= 0 || s.n_cols <= 0) return 0;
-  const unsigned blocks = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
+  const unsigned blocks = static_cast<unsigned>((s.n_cols + kWalkWarps - 1) / kWalkWarps);
   if (move)
-    launch_pdl(k_ind_cols<true>, dim3(blocks), dim3(kColWarps * 32), kColSmem, s.stream, s.x,
+    launch_pdl(k_ind_cols<true>, dim3(blocks), dim3(kWalkWarps * 32), kColSmem, s.stream, s.x,
                s.n, s.n_el, static_cast<const int64_t*>(s.col_start), s.n_cols, s.ind_moves,
                s.ctl, s.geo, s.grid_mi, 1);
   else
-    k_ind_cols<false><<<blocks, kColWarps * 32, kColSmem, s.stream>>>(
+    k_ind_cols<false><<<blocks, kWalkWarps * 32, kColSmem, s.stream>>>(
         s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 0);
   s.ind_v_uniform = true;
   s.kernel_launches += 1;
@@ -2536,8 +2545,8 @@ int launch_ind_cols(DeviceSim& s, bool move) {
 // by one node, completed by this substep's finalize if the elastomer leaves it.
 int launch_ind_walks_on(DeviceSim& s, cudaStream_t st) {
   if (s.n_ind <= 0 || s.n_cols <= 0) return 0;
-  const unsigned blocks = static_cast<unsigned>((s.n_cols + kColWarps - 1) / kColWarps);
-  k_ind_cols<true><<<blocks, kColWarps * 32, kColSmem, st>>>(
+  const unsigned blocks = static_cast<unsigned>((s.n_cols + kWalkWarps - 1) / kWalkWarps);
+  k_ind_cols<true><<<blocks, kWalkWarps * 32, kColSmem, st>>>(
       s.x, s.n, s.n_el, s.col_start, s.n_cols, s.ind_moves, s.ctl, s.geo, s.grid_mi, 2);
   s.ind_v_uniform = true;
   s.kernel_launches += 1;
