@@ -2379,13 +2379,8 @@ void permute_gel_lanes(DeviceSim& s, const double* x_in) {
       for (int l = 0; l < 32; ++l)
         if (slot[32 * w + l] >= 0) used.push_back(32 * w + l);
       if (used.size() < 2) continue;
-      auto res = [&](int t) {
-        const long e = (static_cast<long>(b[t][0] - lo[0]) * d1 + (b[t][1] - lo[1])) * pitch +
-                       (b[t][2] - lo[2]);
-        return static_cast<int>(e & 7);
-      };
       std::vector<int> order = used;
-      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return res(x) < res(y); });
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return residue(x) < residue(y); });
       // the k-th particle in residue order goes to quarter k % 4; the warp's
       // occupied slots (in lane order) are refilled quarter by quarter
       std::vector<int> dealt;
