@@ -353,8 +353,10 @@ def run_single(args):
                                    "mode is the `secondary` config2a-deterministic line",
                    "parallelism": f"independent episodes x{world} (one per GPU), no collective",
                    "l2": "no flush; per substep the particle state streams ~62 MB and the node "
-                         "box ~60 MB through the 126 MB L2 (in-pipeline DRAM traffic ~240 MB per "
-                         "substep, DESIGN.md 4.4): inputs are not L2-resident between steps"},
+                         "box ~60 MB through the 126 MB L2 (warm-cache DRAM traffic ~200 MB per "
+                         "substep: elastomer kernel 136 MB, grid_update 58 MB, ncu "
+                         "--cache-control none, DESIGN.md 4): inputs are not L2-resident between "
+                         "steps"},
         "frames_per_sec": args.steps * world / (dev_ms * 1e-3),
         "value_api": "pipelined tg_step_capture_submit / _wait with read_back = 0 (step + capture "
                      "per frame, outputs stay in HBM)",
