@@ -151,7 +151,7 @@ def _roofline(s, phase_ms, walked_per_substep, n_el, n_ind, window_nodes):
     achieved = per_kernel[dom] / (dom_ms * 1e-3) / 1e9
     per_substep = n_el * GEL_BYTES + n_ind * IND_BYTES
     substep_ms = (phase_ms["grid_update"] + phase_ms["g2p2g_elastomer"] + phase_ms["finalize"])
-    traffic = shared = atomics = None
+    traffic = shared = atomics = fp64 = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f)
@@ -161,6 +161,14 @@ def _roofline(s, phase_ms, walked_per_substep, n_el, n_ind, window_nodes):
             if "shared_wavefronts_per_launch" in tr[kname]:
                 shared = {"wavefronts_per_launch": tr[kname]["shared_wavefronts_per_launch"],
                           "pct_of_peak_sustained": tr[kname]["shared_wavefronts_pct_of_peak"]}
+            f = tr[kname].get("fp64")
+            if f and "peak_tflops" in f:
+                # the kernel's fp64 work (ncu op counts per launch, a property
+                # of the code and the config) over its live time
+                ach = f["flop_per_launch"] / (dom_ms * 1e-3) / 1e12
+                fp64 = {"achieved": ach, "peak": f["peak_tflops"], "unit": "TFLOP/s",
+                        "frac": ach / f["peak_tflops"], "flop_per_launch": f["flop_per_launch"],
+                        "source": f["source"], "peak_source": f["peak_source"]}
             red = tr[kname].get("l2_reduction")
             if red:
                 atomics = {
@@ -185,7 +193,7 @@ def _roofline(s, phase_ms, walked_per_substep, n_el, n_ind, window_nodes):
                                          "advects (x read + written)",
             "indenter_particles_advected_per_launch": walked_per_substep,
             "traffic_over_algorithmic": (traffic / per_kernel[dom]) if traffic else None,
-            "shared_memory": shared, "atomics": atomics, "kernel_ms": dom_ms,
+            "shared_memory": shared, "atomics": atomics, "fp64_compute": fp64, "kernel_ms": dom_ms,
             "substep": {"ms": substep_ms, "algorithmic_bytes": per_substep,
                         "achieved_gbs": per_substep / (substep_ms * 1e-3) / 1e9,
                         "frac": per_substep / (substep_ms * 1e-3) / 1e9 / peak,
