@@ -1874,14 +1874,12 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     // kernel, which is complete once the kernel before this one passed its
     // own griddepcontrol.wait (the only way this grid can have been
     // launched), so they are read before this grid's wait, overlapping the
-    // tail of grid_update. F is only prefetched into L2 here (loaded into
-    // registers this early it is spilled, and the spill store waits for the
-    // load); it is loaded once the stencil is computed.
+    // tail of grid_update. F is loaded once the stencil is computed (loaded
+    // into registers this early it is spilled; an L2 prefetch of it here
+    // measured 0.6 % slower than none, round 2).
     px0 = __ldcs(x + p);
     px1 = __ldcs(x + n + p);
     px2 = __ldcs(x + 2 * n + p);
-#pragma unroll
-    for (int i = 0; i < 9; ++i) asm volatile("prefetch.global.L2 [%0];" ::"l"(Fm + i * n_el + p));
     if (kBoundary) bottom = __ldg(tag + p) == kElastomerBottom;
   }
   int ctl_s = 0;
@@ -1949,9 +1947,9 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
   const bool staging = kLookahead && staged && g.scatter_mode != 5;
   // the stencil needs x: its loads complete while the staging copies fly
   if (active) make_stencil(px0, px1, px2, g.origin, g.inv_dx, st_old);
-  // F (prefetched into L2 at entry) is loaded while the staging copies
-  // complete: loaded at entry it was spilled (the spill store waited for the
-  // load), loaded after the gather its L2 latency was exposed (DESIGN 4.5)
+  // F is loaded while the staging copies complete: loaded at entry it was
+  // spilled (the spill store waited for the load), loaded after the gather
+  // its latency was exposed (DESIGN 4.5)
   double F0[9];
   if (active) {
 #pragma unroll
