@@ -132,13 +132,17 @@ __global__ void k_metrics_finish(const Partial* __restrict__ partials, int ctas,
   const double n = static_cast<double>(w) * h * 3;
   const double mse = static_cast<double>(se) / n;
   out[3 * pair + 0] = ssim / windows;
-  out[3 * pair + 1] = mse == 0.0 ? CUDART_INF : 10.0 * log10(255.0 * 255.0 / mse);
+  // the mse (exact: an integer sum over n); tg_image_metrics turns it into
+  // PSNR on the host with the host's log10, the reference's own call
+  // (image_metrics.cpp:99) — the device log10 differs in the last ulp
+  out[3 * pair + 1] = mse;
   out[3 * pair + 2] = static_cast<double>(ae) / n / 255.0 * 100.0;
 }
 
 }  // namespace
 
-// Batched metrics on device buffers (stream-ordered).
+// Batched metrics on device buffers (stream-ordered): per pair {ssim, mse,
+// mae %}; the caller forms PSNR from the mse on the host (psnr_from_mse).
 int image_metrics_device(const uint8_t* d_a, const uint8_t* d_b, int w, int h, int count,
                          double* d_out, cudaStream_t stream) {
   int sms = 148;
@@ -191,5 +195,11 @@ extern "C" int tg_image_metrics(int device, const uint8_t* a, const uint8_t* b, 
   cudaStreamDestroy(s);
   if (rc == TG_OK && e != cudaSuccess)
     rc = fail(TG_ERR_CUDA, std::string("tg_image_metrics: ") + cudaGetErrorString(e));
+  if (rc == TG_OK)  // PSNR from the exact mse with the reference's expression
+    for (int p = 0; p < count; ++p) {
+      const double mse = out[3 * p + 1];
+      out[3 * p + 1] = mse == 0.0 ? std::numeric_limits<double>::infinity()
+                                  : 10.0 * std::log10(255.0 * 255.0 / mse);
+    }
   return rc;
 }

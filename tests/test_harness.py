@@ -252,6 +252,25 @@ def test_image_metrics_match_reference(golden):
 
 
 @pytest.mark.gpu
+def test_image_metrics_exact_on_random_pairs():
+    """PSNR and MAE bit-equal to the reference's metrics::compare on random
+    noise pairs (the device sums squared / absolute differences in integers;
+    PSNR's log10 is taken on the host, the reference's own call — the device
+    log10 differed in the last ulp on some pairs), SSIM to 1e-12."""
+    from oracle import refpy  # the reference, as the checker
+
+    tb = _tb()
+    rng = np.random.default_rng(11)
+    a = rng.integers(0, 256, (16, 48, 64, 3), dtype=np.uint8)
+    b = np.clip(a.astype(np.int32) + rng.integers(-20, 21, a.shape), 0, 255).astype(np.uint8)
+    m = tb.metrics.compare_batch(a, b)
+    for i in range(len(a)):
+        r = refpy.image_metrics(a[i], b[i])
+        assert abs(m[i, 0] - r[0]) <= 1e-12
+        assert (m[i, 1], m[i, 2]) == (r[1], r[2])
+
+
+@pytest.mark.gpu
 def test_compare_datasets(tmp_path):
     """compare_datasets over two harness outputs: identical -> SSIM 1, PSNR
     inf, MAE 0; a perturbed copy -> per-pair metrics equal metrics.compare."""
