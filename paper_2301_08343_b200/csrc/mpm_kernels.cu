@@ -13,12 +13,16 @@
 //                        det F, Newton polar, corotated stress, APIC) through
 //                        a shared-memory node tile: 27 barrier-separated
 //                        conflict-free accumulation phases, then one TMA bulk
-//                        reduction per tile row. Extra blocks of the same
-//                        launch (the lowest block indices) run the rigid
-//                        indenter's apply_boundary +
-//                        advect + s+1 scatter (ind_cols_block: warp per
-//                        z-sorted column, run-length accumulation of B-spline
-//                        weight sums, one RED.F64 per touched node into M_I;
+//                        reduction per tile row (the particles' storage order
+//                        within each CTA's slots is dealt for the banks,
+//                        permute_gel_lanes).
+//   k_ind_cols           (on the handle's walk stream, forked after the
+//                        previous finalize and joined before this one; with
+//                        TACCHI_WALKS=fused, extra blocks of k_g2p2g_gel) the
+//                        rigid indenter's apply_boundary + advect + s+1
+//                        scatter (ind_cols_block: warp per z-sorted column,
+//                        run-length accumulation of B-spline weight sums, one
+//                        RED.F64 per touched node into M_I buffer (s+1) & 1;
 //                        the indenter's momentum is M_I * v, v uniform).
 //   k_finalize           advect's in_range check / step_count / max_speed and
 //                        the next zero_grid window (engine.cpp:53-68, 279-285).
