@@ -569,8 +569,9 @@ static int sync_and_check(DeviceSim& s, int end_substep) {
 
 // The substep plan of one mpm::step call (see mpm_kernels.cu): a standalone
 // scatter for the first substep, then per substep grid_update (re-zeroing the
-// accumulators) and the fused G2P(+boundary+advect)+look-ahead-P2G kernels;
-// the last substep does no look-ahead.
+// accumulators), the fused G2P(+boundary+advect)+look-ahead-P2G kernel and
+// finalize, with the indenter's look-ahead walks on the walk stream beside
+// the first two (forked after the previous finalize, joined before this one).
 // When the previous call already scattered this call's first substep
 // (grid_ready), the standalone scatter is skipped; every substep, the last one
 // included, scatters the next substep's particles, so consecutive step() calls
