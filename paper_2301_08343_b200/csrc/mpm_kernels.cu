@@ -390,6 +390,29 @@ __host__ __device__ __forceinline__ int tile_zpitch(int zcnt) {
 // Rows of one x-slab of the tile (the j extent padded by kRowPad rows).
 constexpr int kRowPad = TACCHI_ROW_PAD;
 
+// The CTA's P2G node box as every thread holds it (block_motion_box computes
+// it from T.blo / T.bhi in each thread, so the tile zeroing needs no barrier
+// to publish it; thread 0 also stores it in T for the flush).
+struct TileBox {
+  int lo[3], hi[3], dim[3];
+  int pitch, rd, ok;
+};
+
+__device__ __forceinline__ TileBox tile_box_of(const int* blo, const int* bhi) {
+  TileBox b;
+  const bool any = blo[0] != INT_MAX;
+  for (int a = 0; a < 3; ++a) {
+    b.lo[a] = blo[a];
+    b.hi[a] = bhi[a];
+    b.dim[a] = any ? bhi[a] - blo[a] + 3 : 0;
+  }
+  b.pitch = tile_pitch(b.dim[2]);
+  b.rd = b.dim[1] + kRowPad;
+  const int rows = b.dim[0] * b.rd;
+  b.ok = any && rows * b.pitch <= kTileCap && rows * tile_zpitch(b.dim[2] + 2) <= 2 * kTileCap;
+  return b;
+}
+
 // Adds the CTA's node box into the global grid: one bulk-async reduction
 // (UBLKRED.ADD.F64, element-wise atomic in L2) per z-row and half, issued by
 // the first 2*dim0*dim1 threads. Call after a __syncthreads that follows the
@@ -600,7 +623,8 @@ __device__ void tile_box(P2GTile& T, bool active, const int* base) {
 // thread 0 derives the tile box. All threads of the block must call it; the
 // first barrier also retires every earlier reader of T (the G2P gathers).
 __device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double v2, double x0,
-                                 double x1, double x2, bool go, double J, const int* base) {
+                                 double x1, double x2, bool go, double J, const int* base,
+                                 TileBox& box) {
   static_assert(kGelThreads / 32 == 8, "one warp per reduced quantity");
   __shared__ double redd[8][8];
   double r[8];
@@ -660,19 +684,19 @@ __device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double
       }
     }
   }
+  // every thread derives the box (T.blo / T.bhi are final after the barrier);
+  // thread 0 stores it for the flush, which follows later barriers
+  box = tile_box_of(T.blo, T.bhi);
   if (threadIdx.x == 0) {
-    const bool any = T.blo[0] != INT_MAX;
     for (int a = 0; a < 3; ++a) {
-      T.lo[a] = T.blo[a];
-      T.hi[a] = T.bhi[a];
-      T.dim[a] = any ? T.bhi[a] - T.blo[a] + 3 : 0;
+      T.lo[a] = box.lo[a];
+      T.hi[a] = box.hi[a];
+      T.dim[a] = box.dim[a];
     }
-    T.pitch = tile_pitch(T.dim[2]);
-    T.rd = T.dim[1] + kRowPad;
-    const int rows = T.dim[0] * T.rd;
-    T.ok = any && rows * T.pitch <= kTileCap && rows * tile_zpitch(T.dim[2] + 2) <= 2 * kTileCap;
+    T.pitch = box.pitch;
+    T.rd = box.rd;
+    T.ok = box.ok;
   }
-  __syncthreads();
 }
 
 // CTA-cooperative scatter. All threads of the block must call it.
@@ -685,7 +709,7 @@ __device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double
 // node arrays' allocation latches kErrRegrow for it instead of writing).
 template <int kDet>
 __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
-                                 const Geometry& g, NodeBuf grid, int cta, bool box_done,
+                                 const Geometry& g, NodeBuf grid, int cta, const TileBox* given,
                                  Ctl* ctl, int s_scatter) {
   const int tid = threadIdx.x;
   if (g.scatter_mode == 1 || g.scatter_mode == 3) {  // A/B switches without a tile
@@ -696,11 +720,24 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
     }
     return;
   }
-  if (!box_done) tile_box(T, active, q.st.base);
+  TileBox B;
+  if (given) {
+    B = *given;
+  } else {
+    tile_box(T, active, q.st.base);
+    for (int a = 0; a < 3; ++a) {
+      B.lo[a] = T.lo[a];
+      B.hi[a] = T.hi[a];
+      B.dim[a] = T.dim[a];
+    }
+    B.pitch = T.pitch;
+    B.rd = T.dim[1] + kRowPad;
+    B.ok = T.ok;
+  }
   // every node this CTA can touch, [min base, max base + 3), must be
-  // allocated (block-uniform: T is shared and complete after the barrier)
-  if (T.lo[0] != INT_MAX &&
-      !box_in_alloc(g, T.lo[0], T.lo[1], T.lo[2], T.hi[0] + 3, T.hi[1] + 3, T.hi[2] + 3)) {
+  // allocated (block-uniform: every thread holds the same box)
+  if (B.lo[0] != INT_MAX &&
+      !box_in_alloc(g, B.lo[0], B.lo[1], B.lo[2], B.hi[0] + 3, B.hi[1] + 3, B.hi[2] + 3)) {
     if (tid == 0) {
       raise(ctl, kErrRegrow, s_scatter);
       if (g.cta_box) g.cta_box[8 * cta + 6] = 0;
@@ -710,14 +747,14 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
   if (tid == 0 && g.cta_box) {  // the next G2P of these particles stages this box
     int* b = g.cta_box + 8 * cta;
     for (int a = 0; a < 3; ++a) {
-      b[a] = T.lo[a];
-      b[3 + a] = T.dim[a];
+      b[a] = B.lo[a];
+      b[3 + a] = B.dim[a];
     }
-    b[6] = T.ok;
+    b[6] = B.ok;
   }
-  const int d1 = T.rd, d2 = T.pitch;  // x-slab rows, row pitch
-  const int vol = T.dim[0] * d1 * d2;
-  const bool use_tile = T.ok != 0;
+  const int d1 = B.rd, d2 = B.pitch;  // x-slab rows, row pitch
+  const int vol = B.dim[0] * d1 * d2;
+  const bool use_tile = B.ok != 0;
   if (use_tile) {
     const double2 z2 = make_double2(0.0, 0.0);
     for (int e = tid; e < vol; e += blockDim.x) {
@@ -732,8 +769,8 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
   TRACE_MARK(5);
   if (active) {
     if (use_tile) {
-      base_idx = ((q.st.base[0] - T.lo[0]) * d1 + (q.st.base[1] - T.lo[1])) * d2 +
-                 (q.st.base[2] - T.lo[2]);
+      base_idx = ((q.st.base[0] - B.lo[0]) * d1 + (q.st.base[1] - B.lo[1])) * d2 +
+                 (q.st.base[2] - B.lo[2]);
       tiled = atomicCAS(&T.owner[base_idx], -1, tid) == -1;
     }
     if (!tiled) scatter_direct<kDet>(g, grid, m, q, ctl);
@@ -1097,7 +1134,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_p2g_gel_tile(
     if (active && !stencil_in_grid(g, q.st)) active = false;  // zero_grid already raised
   }
   reduce_min_detf(ctl, s, active, J);
-  p2g_tile_scatter<-1>(T, active, q, m, g, grid, blockIdx.x, false, ctl, s);
+  p2g_tile_scatter<-1>(T, active, q, m, g, grid, blockIdx.x, nullptr, ctl, s);
 }
 
 // Indenter scatter with a non-uniform velocity (only possible before the
@@ -2016,8 +2053,9 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     }
     TRACE_MARK(4);
     // advect's motion reductions, min det F of s + 1 and the tile box together
-    block_motion_box(T, ctl, s, active, v2, px0, px1, px2, go, J, q.st.base);
-    p2g_tile_scatter<kDet>(T, go, q, m, g, grid, cta, true, ctl, s + 1);
+    TileBox box;
+    block_motion_box(T, ctl, s, active, v2, px0, px1, px2, go, J, q.st.base, box);
+    p2g_tile_scatter<kDet>(T, go, q, m, g, grid, cta, &box, ctl, s + 1);
   }
   TRACE_END();
 }
