@@ -789,7 +789,9 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
       const double m2 = q.mv[2] + q.aff[6] * dxa + q.aff[7] * dxb;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        __syncthreads();
+        // phase (0,0,0) follows the zeroing barrier directly (the owner CAS
+        // touches only the owner table)
+        if (a | b | c) __syncthreads();
         if (tiled && g.scatter_mode != 2) {
           const double dxc = (c - q.st.fx[2]) * dx;
           const double w = wab * q.st.w[2][c];
