@@ -177,6 +177,9 @@ __device__ __forceinline__ void polar_rotation(const double* F, double* R) {
   double r00 = F[0], r01 = F[1], r02 = F[2];
   double r10 = F[3], r11 = F[4], r12 = F[5];
   double r20 = F[6], r21 = F[7], r22 = F[8];
+  // the SVD fallback is called once, after the loop (a call inside the loop
+  // made every Newton value live across it)
+  bool converged = false;
   for (int it = 0; it < 40; ++it) {
     const double c00 = r11 * r22 - r12 * r21;
     const double c01 = r12 * r20 - r10 * r22;
@@ -188,7 +191,7 @@ __device__ __forceinline__ void polar_rotation(const double* F, double* R) {
     const double c21 = r02 * r10 - r00 * r12;
     const double c22 = r00 * r11 - r01 * r10;
     const double d = r00 * c00 + r01 * c01 + r02 * c02;
-    if (!(fabs(d) > 1e-300)) { polar_svd_fallback(F, R); return; }
+    if (!(fabs(d) > 1e-300)) break;  // vanishing determinant: SVD below
     const double g = fabs(d - 1.0) > 1e-2 ? 1.0 / cbrt(fabs(d)) : 1.0;
     const double hg = 0.5 * g;
     const double hd = 0.5 / (g * d);
@@ -208,11 +211,15 @@ __device__ __forceinline__ void polar_rotation(const double* F, double* R) {
     r10 = n10; r11 = n11; r12 = n12;
     r20 = n20; r21 = n21; r22 = n22;
     if (step < 1e-13) {
-      R[0] = r00; R[1] = r01; R[2] = r02;
-      R[3] = r10; R[4] = r11; R[5] = r12;
-      R[6] = r20; R[7] = r21; R[8] = r22;
-      return;
+      converged = true;
+      break;
     }
+  }
+  if (converged) {
+    R[0] = r00; R[1] = r01; R[2] = r02;
+    R[3] = r10; R[4] = r11; R[5] = r12;
+    R[6] = r20; R[7] = r21; R[8] = r22;
+    return;
   }
   polar_svd_fallback(F, R);
 }
