@@ -327,6 +327,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   if (const char* e = std::getenv("TACCHI_ZPAD")) s->zpad = std::max(2, std::atoi(e) & ~1);
   g.gu_bps = 5;  // one wave of resident blocks (1367 vs 1360 frames/s with 10)
   g.pdl_early = 1;
+  g.gel_trigger = 1;
+  if (const char* e = std::getenv("TACCHI_GEL_TRIGGER")) g.gel_trigger = std::atoi(e);
   g.ind_first = 1;
   if (const char* e = std::getenv("TACCHI_GU_BPS")) g.gu_bps = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("TACCHI_PDL_EARLY")) g.pdl_early = std::atoi(e);

@@ -71,6 +71,8 @@ struct Geometry {
   int gu_bps;           // grid_update blocks per SM (TACCHI_GU_BPS, default 5)
   int pdl_early;        // grid_update triggers its dependent launch right after its
                         // own griddepcontrol.wait (TACCHI_PDL_EARLY, default 1)
+  int gel_trigger;      // the elastomer kernel triggers its dependent launch at
+                        // its start (TACCHI_GEL_TRIGGER, default 1)
   int ind_first;        // the indenter blocks of the elastomer kernel come first
                         // (TACCHI_IND_FIRST, default 1)
   // Deterministic mode (SceneConfig::deterministic, SPEC "Concurrency

@@ -1954,6 +1954,10 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     }
   }
   pdl_wait();
+  // Let finalize (which waits for this whole grid) be launched once every CTA
+  // of it has started: it is then resident when the last CTA retires
+  // instead of being launched after it (TACCHI_GEL_TRIGGER=0: off)
+  if (kLookahead && g.gel_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (kLookahead && gel_block && threadIdx.x == 0) {
     // the substep and its stale flag, shared at the barrier below
     T.cur_s = ctl_s;
