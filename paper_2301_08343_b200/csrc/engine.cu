@@ -329,6 +329,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   g.pdl_early = 1;
   g.gel_trigger = 1;
   if (const char* e = std::getenv("TACCHI_GEL_TRIGGER")) g.gel_trigger = std::atoi(e);
+  g.fin_trigger = 1;
+  if (const char* e = std::getenv("TACCHI_FIN_TRIGGER")) g.fin_trigger = std::atoi(e);
   g.ind_first = 1;
   if (const char* e = std::getenv("TACCHI_GU_BPS")) g.gu_bps = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("TACCHI_PDL_EARLY")) g.pdl_early = std::atoi(e);

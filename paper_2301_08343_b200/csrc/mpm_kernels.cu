@@ -1638,11 +1638,14 @@ struct FixArgs {
 // (finalize_warp, warp 0); with kFinWalkFix the other warps of the block
 // stand by for the walk fix-up.
 __global__ void __launch_bounds__(256) k_finalize(Ctl* ctl, Geometry g, int mode, FixArgs fa) {
-  pdl_wait();
   // every kernel that follows finalize in a step plan (grid_update,
   // k_ind_catchup) reads nothing before its own wait: let it launch while
-  // this block runs
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // this block runs -- by default before finalize's own wait, so the next
+  // grid_update's blocks fill the SMs the elastomer kernel's tail frees and
+  // are resident when finalize completes
+  if (g.fin_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  pdl_wait();
+  if (!g.fin_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ FinFix fx;
   if (threadIdx.x == 0) fx.need = 0;
   if (blockDim.x > 32) __syncthreads();
