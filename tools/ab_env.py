@@ -5,7 +5,10 @@ times; prints frames/s and the per-kernel device times (tg_time_phases).
     python tools/ab_env.py --variant base: --variant dense:TACCHI_DENSE_GRID=1
 
 AB_CFG: SceneConfig overrides as JSON, or @file holding them (for JSON with
-commas, which the variant syntax splits on).
+commas, which the variant syntax splits on). AB_PREALLOC_KB: device memory
+allocated before the handle (moves its allocations' addresses).
+Without AB_CFG the scene runs in SceneConfig's default deterministic mode;
+the bench's headline is fast mode: AB_CFG='{"deterministic": false}'.
 """
 import argparse
 import json
@@ -23,6 +26,8 @@ import paper_2301_08343_b200 as tb
 from tests.scenes import CONFIG2A, CONFIG2A_V
 _ab = os.environ.get("AB_CFG", "{}")
 cfg = {**CONFIG2A, **json.loads(open(_ab[1:]).read() if _ab.startswith("@") else _ab)}
+_pre = int(os.environ.get("AB_PREALLOC_KB", "0"))  # shifts the handle's allocations
+_buf = torch.cuda.caching_allocator_alloc(_pre << 10) if _pre else None
 s = tb.sim.build_sim(cfg)
 rp = tb.render_params(cfg, "")
 for _ in range(5):
