@@ -73,6 +73,8 @@ struct Geometry {
                         // own griddepcontrol.wait (TACCHI_PDL_EARLY, default 1)
   int gel_trigger;      // the elastomer kernel triggers its dependent launch at
                         // its start (TACCHI_GEL_TRIGGER, default 1)
+  int det_skip0;        // deterministic conversion pass skips all-zero tile nodes
+                        // (TACCHI_DET_SKIP0, default 1)
   int fin_trigger;      // finalize triggers its dependent launch before its own
                         // griddepcontrol.wait (TACCHI_FIN_TRIGGER, default 1)
   int ind_first;        // the indenter blocks of the elastomer kernel come first

@@ -228,7 +228,9 @@ __device__ __forceinline__ long long to_fixed(double v, double scale, Ctl* ctl) 
 }
 // llrint(v * scale) without F2I: two round-to-integer additions of
 // 1.5 * 2^52 (exact for |v * scale| < 2^62; `bad` is set outside that range),
-// returned as the int64's bit pattern in a double register.
+// returned as the int64's bit pattern in a double register. (A one-addition
+// path for |v * scale| < 2^51 behind a per-value branch measured slower:
+// 60.6 vs 59.5 us on the deterministic config-2a elastomer kernel.)
 __device__ __forceinline__ double fixed_bits(double v, double scale, bool& bad) {
   constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
   constexpr long long kMagicBits = 0x4338000000000000LL;
@@ -710,7 +712,7 @@ __device__ void block_motion_box(P2GTile& T, Ctl* ctl, int s, bool moved, double
 template <int kDet>
 __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, double m,
                                  const Geometry& g, NodeBuf grid, int cta, const TileBox* given,
-                                 Ctl* ctl, int s_scatter) {
+                                 Ctl* ctl, int s_scatter, bool owners_reset) {
   const int tid = threadIdx.x;
   if (g.scatter_mode == 1 || g.scatter_mode == 3) {  // A/B switches without a tile
     if (tid == 0 && g.cta_box) g.cta_box[8 * cta + 6] = 0;  // next G2P: no staged box
@@ -755,26 +757,44 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
   const int d1 = B.rd, d2 = B.pitch;  // x-slab rows, row pitch
   const int vol = B.dim[0] * d1 * d2;
   const bool use_tile = B.ok != 0;
+  // Deterministic mode: a duplicate's contributions reach the grid as
+  // separately rounded fixed-point REDs, the owner's inside the tile sum, so
+  // the owner of a shared base cell must not depend on timing: the highest
+  // thread takes it (atomicMax). With the owner table reset at kernel entry
+  // (owners_reset) the claims go in before the zeroing barrier and are read
+  // after it; otherwise they need a barrier of their own.
+  const bool det = det_on<kDet>(g);
+  const bool pre = det && owners_reset;
+  int base_idx = 0;
+  if (active && use_tile) {
+    base_idx = ((q.st.base[0] - B.lo[0]) * d1 + (q.st.base[1] - B.lo[1])) * d2 +
+               (q.st.base[2] - B.lo[2]);
+    if (pre) atomicMax(&T.owner[base_idx], tid);
+  }
   if (use_tile) {
     const double2 z2 = make_double2(0.0, 0.0);
     for (int e = tid; e < vol; e += blockDim.x) {
       T.nlo[e] = z2;
       T.nhi[e] = z2;
-      T.owner[e] = -1;
+      if (!pre) T.owner[e] = -1;
     }
   }
   __syncthreads();
-  int base_idx = 0;
   bool tiled = false;
   TRACE_MARK(5);
-  if (active) {
-    if (use_tile) {
-      base_idx = ((q.st.base[0] - B.lo[0]) * d1 + (q.st.base[1] - B.lo[1])) * d2 +
-                 (q.st.base[2] - B.lo[2]);
+  if (active && use_tile) {
+    if (pre)
+      tiled = T.owner[base_idx] == tid;
+    else if (det)
+      atomicMax(&T.owner[base_idx], tid);
+    else  // fast mode: first come
       tiled = atomicCAS(&T.owner[base_idx], -1, tid) == -1;
-    }
-    if (!tiled) scatter_direct<kDet>(g, grid, m, q, ctl);
   }
+  if (det && !pre && use_tile) {  // block-uniform
+    __syncthreads();
+    if (active) tiled = T.owner[base_idx] == tid;
+  }
+  if (active && !tiled) scatter_direct<kDet>(g, grid, m, q, ctl);
   if (!use_tile) return;  // block-uniform
   const double dx = g.dx;
 #pragma unroll
@@ -819,6 +839,10 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
     bool bad = false;
     for (int e = tid; e < vol; e += blockDim.x) {
       const double2 a = T.nlo[e], b = T.nhi[e];
+      // untouched nodes (slab / pitch padding, empty corners) are +0: bits 0
+      if (g.det_skip0 && (__double_as_longlong(a.x) | __double_as_longlong(a.y) |
+                          __double_as_longlong(b.x) | __double_as_longlong(b.y)) == 0)
+        continue;
       T.nlo[e] = make_double2(fixed_bits(a.x, fs, bad), fixed_bits(a.y, fs, bad));
       T.nhi[e] = make_double2(fixed_bits(b.x, fs, bad), fixed_bits(b.y, fs, bad));
     }
@@ -1136,7 +1160,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_p2g_gel_tile(
     if (active && !stencil_in_grid(g, q.st)) active = false;  // zero_grid already raised
   }
   reduce_min_detf(ctl, s, active, J);
-  p2g_tile_scatter<-1>(T, active, q, m, g, grid, blockIdx.x, nullptr, ctl, s);
+  p2g_tile_scatter<-1>(T, active, q, m, g, grid, blockIdx.x, nullptr, ctl, s, false);
 }
 
 // Indenter scatter with a non-uniform velocity (only possible before the
@@ -1956,6 +1980,11 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
       T.bhi[a] = INT_MIN;
     }
   }
+  if (kLookahead && kDet == 1 && gel_block) {
+    // the deterministic scatter's owner table (p2g_tile_scatter owners_reset),
+    // shared memory only: before the wait, published by the start barrier
+    for (int e = threadIdx.x; e < kTileCap; e += blockDim.x) T.owner[e] = -1;
+  }
   pdl_wait();
   // Let finalize (which waits for this whole grid) be launched once every CTA
   // of it has started: it is then resident when the last CTA retires
@@ -2064,7 +2093,7 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
     // advect's motion reductions, min det F of s + 1 and the tile box together
     TileBox box;
     block_motion_box(T, ctl, s, active, v2, px0, px1, px2, go, J, q.st.base, box);
-    p2g_tile_scatter<kDet>(T, go, q, m, g, grid, cta, &box, ctl, s + 1);
+    p2g_tile_scatter<kDet>(T, go, q, m, g, grid, cta, &box, ctl, s + 1, kDet == 1);
   }
   TRACE_END();
 }

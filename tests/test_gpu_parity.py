@@ -873,6 +873,29 @@ def test_deterministic_reruns_bit_identical(tb):
     assert out[0] == out[1]
 
 
+def test_deterministic_reruns_bit_identical_with_duplicates(tb):
+    """Deterministic mode where gel particles share base cells (config 2b:
+    0.91-cell spacing, about a quarter of the particles are duplicates): the
+    duplicates' contributions reach the grid as their own fixed-point REDs,
+    the owner's inside the tile sum, so the owner must not be chosen by
+    timing (the highest thread of the CTA takes the cell). Two runs of the
+    press + slide slice give byte-identical states, height maps and images."""
+    from tests.scenes import CONFIG2B, CONFIG2B_PRESS, CONFIG2B_SLIDE
+
+    out = []
+    for _ in range(2):
+        s = tb.sim.build_sim({**CONFIG2B, "deterministic": True})
+        for n, v in (CONFIG2B_PRESS, CONFIG2B_SLIDE):
+            for _ in range(n):
+                tb.mpm.step(s, v, 10)
+        depth, img = tb.sim.capture(s, CONFIG2B)
+        st = s.state()
+        out.append((st["x"].tobytes(), st["v"].tobytes(), st["C"].tobytes(), st["F"].tobytes(),
+                    depth.tobytes(), img.tobytes()))
+        del s
+    assert out[0] == out[1]
+
+
 _WALK_CHILD = r"""
 import hashlib, json, sys
 sys.path.insert(0, %r)
@@ -892,7 +915,10 @@ def test_storage_orders_byte_identical():
     lattice order) only changes which thread handles which particle: in
     deterministic mode (fixed-point node sums) 300 substeps of config 2a
     give byte-identical particle states in every order (downloaded through
-    the permutation)."""
+    the permutation). Config 2a's gel has no duplicate base cells; where
+    there are duplicates the cell's owner is the CTA's highest thread, a
+    function of the storage order, and the rounding of the fixed-point sums
+    follows it."""
     import json
     import os
     import subprocess

@@ -23,7 +23,8 @@ import numpy as np  # noqa: E402
 import paper_2301_08343_b200 as tb  # noqa: E402
 from tests.scenes import CONFIG2A, CONFIG2A_V, SUBSTEPS_PER_FRAME  # noqa: E402
 
-s = tb.sim.build_sim({**CONFIG2A, "deterministic": False})  # the bench mode
+# the bench mode (fast) unless TRACE_DET=1 (SceneConfig's default deterministic mode)
+s = tb.sim.build_sim({**CONFIG2A, "deterministic": os.environ.get("TRACE_DET") == "1"})
 for _ in range(5):
     tb.mpm.step(s, CONFIG2A_V, SUBSTEPS_PER_FRAME)
 s.sync()
