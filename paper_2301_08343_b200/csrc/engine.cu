@@ -331,6 +331,8 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   if (const char* e = std::getenv("TACCHI_GEL_TRIGGER")) g.gel_trigger = std::atoi(e);
   g.fin_trigger = 1;
   g.det_skip0 = 1;
+  g.det_fast4 = 1;
+  if (const char* e = std::getenv("TACCHI_DET_FAST4")) g.det_fast4 = std::atoi(e);
   if (const char* e = std::getenv("TACCHI_DET_SKIP0")) g.det_skip0 = std::atoi(e);
   if (const char* e = std::getenv("TACCHI_FIN_TRIGGER")) g.fin_trigger = std::atoi(e);
   g.ind_first = 1;

@@ -75,6 +75,8 @@ struct Geometry {
                         // its start (TACCHI_GEL_TRIGGER, default 1)
   int det_skip0;        // deterministic conversion pass skips all-zero tile nodes
                         // (TACCHI_DET_SKIP0, default 1)
+  int det_fast4;        // deterministic conversion: one magic addition per sum where
+                        // a node's four fit 2^51 (TACCHI_DET_FAST4, default 1)
   int fin_trigger;      // finalize triggers its dependent launch before its own
                         // griddepcontrol.wait (TACCHI_FIN_TRIGGER, default 1)
   int ind_first;        // the indenter blocks of the elastomer kernel come first

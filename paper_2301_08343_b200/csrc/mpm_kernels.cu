@@ -243,6 +243,32 @@ __device__ __forceinline__ double fixed_bits(double v, double scale, bool& bad) 
   return __longlong_as_double((hi << 32) + lo);
 }
 
+// fixed_bits of a node's four sums: where every |v * scale| < 2^51 (node
+// sums of a few particle masses, ~2^48, and every momentum; tested on the
+// exponent bits, no fp64 compare) one round-to-integer addition each gives
+// llrint (round half to even, as the two-addition path), else fixed_bits.
+__device__ __forceinline__ void fixed_bits4(double2& lo, double2& hi, double scale, bool& bad) {
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  constexpr long long kMagicBits = 0x4338000000000000LL;
+  constexpr unsigned kExp51 = (1023u + 51u) << 20;  // |y| < 2^51 <=> biased exponent < 1074
+  const double y[4] = {lo.x * scale, lo.y * scale, hi.x * scale, hi.y * scale};
+  bool small = true;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    small &= (static_cast<unsigned>(__double2hiint(y[i])) & 0x7ff00000u) < kExp51;
+  double r[4];
+  if (small) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      r[i] = __longlong_as_double(__double_as_longlong(__dadd_rn(y[i], kMagic)) - kMagicBits);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[i] = fixed_bits(y[i], 1.0, bad);
+  }
+  lo = make_double2(r[0], r[1]);
+  hi = make_double2(r[2], r[3]);
+}
+
 __device__ __forceinline__ double from_fixed(double bits, double inv) {
   return static_cast<double>(__double_as_longlong(bits)) * inv;
 }
@@ -843,8 +869,15 @@ __device__ void p2g_tile_scatter(P2GTile& T, bool active, const P2GPayload& q, d
       if (g.det_skip0 && (__double_as_longlong(a.x) | __double_as_longlong(a.y) |
                           __double_as_longlong(b.x) | __double_as_longlong(b.y)) == 0)
         continue;
-      T.nlo[e] = make_double2(fixed_bits(a.x, fs, bad), fixed_bits(a.y, fs, bad));
-      T.nhi[e] = make_double2(fixed_bits(b.x, fs, bad), fixed_bits(b.y, fs, bad));
+      double2 lo2 = a, hi2 = b;
+      if (g.det_fast4) {
+        fixed_bits4(lo2, hi2, fs, bad);
+      } else {
+        lo2 = make_double2(fixed_bits(a.x, fs, bad), fixed_bits(a.y, fs, bad));
+        hi2 = make_double2(fixed_bits(b.x, fs, bad), fixed_bits(b.y, fs, bad));
+      }
+      T.nlo[e] = lo2;
+      T.nhi[e] = hi2;
     }
     if (bad) raise(ctl, kErrFixedRange, s_scatter);
   }
