@@ -83,49 +83,89 @@ def _peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clocks and clock-event (throttle) reasons sampled every ~5 ms by a
+    thread from before the warm-up until after the timed regions
+    (B200_PROFILING.md's clocks line). NVML (nvidia_ml_py, the library
+    nvidia-smi reads) when it loads, else one-shot `nvidia-smi --query-gpu`
+    calls; every sample is also written to gpurun_out/clocks_rank<i>.csv.
+    (A streaming `nvidia-smi -lms` child block-buffers its output into a
+    file and lost its samples when terminated.)"""
+
+    # nvmlClocksEventReason* bits
+    _BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+             0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
+        import threading
+
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [t.strip() for t in vis.split(",") if t.strip()]
+        self.phys = int(ids[index]) if index < len(ids) and ids[index].isdigit() else index
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.source = None
+        self.nvml = None
         try:
-            self.f = open(self.path, "w")
-            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.phys)
+            self.nvml = pynvml
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.source = "nvml"
         except Exception:
-            self.p = None
+            self.source = "nvidia-smi"
+        self.stop_ev = threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _sample(self):
+        if self.nvml is not None:
+            p = self.nvml
+            sm = float(p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM))
+            try:
+                bits = int(p.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except AttributeError:
+                bits = int(p.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+            return sm, self.max_mhz, bits
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", f"--id={self.phys}", f"--query-gpu={q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=10).stdout.strip().splitlines()[0]
+        parts = [t.strip() for t in out.split(",")]
+        bits = 0
+        for bit, val in zip((0x8, 0x40, 0x20, 0x4), parts[2:6]):
+            if val.lower() == "active":
+                bits |= bit
+        return float(parts[0]), float(parts[1]), bits
+
+    def _run(self):
+        with open(self.path, "w") as f:
+            f.write("t_s,sm_mhz,sm_max_mhz,reasons_bits\n")
+            t0 = time.perf_counter()
+            while not self.stop_ev.is_set():
+                try:
+                    smp = self._sample()
+                    self.samples.append(smp)
+                    f.write(f"{time.perf_counter() - t0:.3f},{smp[0]:.0f},{smp[1]:.0f},{smp[2]:#x}\n")
+                except Exception:
+                    pass
+                self.stop_ev.wait(0.005)
 
     def stop(self):
-        if self.p is None:
+        self.stop_ev.set()
+        self.t.join(timeout=15)
+        if not self.samples:
             return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.close()
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [t.strip() for t in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = max(mx, float(parts[2]))
-            except ValueError:
-                continue
-            for nm, val in zip(names, parts[5:9]):
-                if val.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        # under load: samples without the GpuIdle reason (bit 0x1)
+        sm = [x[0] for x in self.samples if not x[2] & 0x1] or [x[0] for x in self.samples]
+        reasons = sorted({nm for _, _, b in self.samples for bit, nm in self._BITS.items() if b & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(x[1] for x in self.samples),
+                "reasons": reasons, "samples": len(sm), "samples_total": len(self.samples),
+                "source": self.source}
 
 
 # SURVEY §8(d) official yardstick: per substep every particle's persistent
