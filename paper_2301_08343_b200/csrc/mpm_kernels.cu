@@ -359,6 +359,9 @@ __device__ __forceinline__ int64_t gel_particle(const GelMap& M, int64_t n_el, i
 #ifndef TACCHI_TILE_CAP
 #define TACCHI_TILE_CAP 2816
 #endif
+#ifndef TACCHI_F_EARLY
+#define TACCHI_F_EARLY 7  // F components loaded before the staging wait (DESIGN 4.5)
+#endif
 #ifndef TACCHI_GEL_THREADS
 #define TACCHI_GEL_THREADS 256
 #endif
@@ -2065,10 +2068,14 @@ __global__ void __launch_bounds__(kGelThreads, kGelMinBlocks) k_g2p2g_gel(
   double F0[9];
   if (active) {
 #pragma unroll
-    for (int i = 0; i < 9; ++i) F0[i] = __ldcs(Fm + i * n_el + p);
+    for (int i = 0; i < TACCHI_F_EARLY; ++i) F0[i] = __ldcs(Fm + i * n_el + p);
   }
   if (staging) tile_bulk_wait(T);
   TRACE_MARK(2);
+  if (active) {
+#pragma unroll
+    for (int i = TACCHI_F_EARLY; i < 9; ++i) F0[i] = __ldcs(Fm + i * n_el + p);
+  }
   if (active) {
     if (g.scatter_mode == 5) {  // A/B timing: no velocity staging / gather
       vv[0] = vv[1] = vv[2] = 0.0;
