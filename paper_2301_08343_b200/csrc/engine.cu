@@ -400,7 +400,10 @@ int create(int device, const tg_params* P, const tg_particles* in, const tg_surf
   // Stream priorities: the handle's stream (grid_update, elastomer kernel:
   // the substep's critical path) above the walk stream, whose kernel has the
   // whole substep to finish before the join (1362 vs 1358.5 frames/s;
-  // TACCHI_WALK_PRIO=0 gives both the default priority).
+  // TACCHI_WALK_PRIO=0 gives both the default priority). Graph replays run
+  // every node at the launch stream's priority: instantiating with
+  // cudaGraphInstantiateFlagUseNodePriority measured slower either way
+  // (DESIGN 4.5).
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   const bool prio = !std::getenv("TACCHI_WALK_PRIO") || std::atoi(std::getenv("TACCHI_WALK_PRIO"));
